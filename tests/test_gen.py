@@ -1,0 +1,207 @@
+"""Pins of the input generator (ietigen): spline spaces, de Rham assembly,
+weights, Kruskal tree, primal selection, multiplier pairing.
+
+Every check is against something other than the generator itself: SPEC/paper
+numbers (tests/golden/counts.json), closed forms, exact identities of the de Rham
+complex, brute force (pure-Python Kruskal, finite differences).
+"""
+import json
+import os
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import scipy.sparse as sp
+from scipy.sparse.csgraph import connected_components
+
+from ietigen import configs as cf
+from ietigen.problem import Problem, local_curl, local_grad, cube_spaces, kruskal_unionfind
+from ietigen.splines import Space1D, knot_vector, bspline_values, dspline_values
+from ietigen.bundle import make_bundle
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "counts.json")))
+
+
+def cfg_custom(name, npatch, p, e, tiling, **kw):
+    return cf.Config(name, npatch, p, e, tiling, **kw)
+
+
+# ---------------------------------------------------------------- splines ---
+@pytest.mark.parametrize("p,e,key", [(1, 1, "p1_e1"), (2, 4, "p2_e4"), (3, 8, "p3_e8")])
+def test_single_patch_dims(p, e, key):
+    """1-form dimension of one patch."""
+    sp1 = Space1D(0.0, 1.0, 1, e, p)
+    m = sp1.m
+    assert m == e + p
+    assert 3 * (m - 1) * m * m == GOLD["space_dims"][key]
+
+
+@pytest.mark.parametrize("p", [1, 2, 3])
+def test_partition_of_unity_and_derivative(p):
+    """B-splines sum to 1; B_i' = D_{i-1} - D_i checked by central
+    differences; each D_j integrates to 1."""
+    s = Space1D(0.0, 1.0, 3, 4, p)
+    x = np.random.default_rng(0).uniform(0.01, 0.99, 40)
+    B = s.B(x)
+    assert np.allclose(B.sum(axis=1), 1.0, atol=1e-14)
+    h = 1e-6
+    dB = (s.B(x + h) - s.B(x - h)) / (2 * h)
+    D = s.D(x)
+    Dpad = np.concatenate([np.zeros((len(x), 1)), D, np.zeros((len(x), 1))], axis=1)
+    pred = Dpad[:, :-1] - Dpad[:, 1:]
+    # away from knots (random points) the derivative is smooth
+    assert np.allclose(dB, pred, atol=1e-6)
+    xq, wq = s.quad(p + 1)
+    assert np.allclose((s.D(xq) * wq[:, None]).sum(axis=0), 1.0, atol=1e-13)
+
+
+# --------------------------------------------------------------- assembly ---
+def test_curl_grad_zero_exact_and_K_kernel():
+    """C . G_grad = 0 in integers and K G_grad = 0 to 1e-12 ||K|| (BJ "discrete
+    curl o grad = 0")."""
+    cfg = cf.get("C2r")
+    P = Problem(cfg)
+    sd = P.subs[3]
+    C = local_curl(sd.ml)
+    G = local_grad(sd.ml)
+    assert abs(C @ G).max() == 0
+    spaces = cube_spaces(cfg, sd)
+    from ietigen.problem import cube_mass2
+    M2 = cube_mass2(cfg, sd, spaces, P.nu)
+    K = C.T @ M2 @ C
+    assert abs(K @ G).max() <= 1e-12 * abs(K).max()
+    assert abs(K - K.T).max() <= 1e-14 * abs(K).max()
+    w = np.linalg.eigvalsh(K.toarray())
+    assert w.min() > -1e-12 * w.max()
+
+
+def test_loads_discretely_divergence_free():
+    """G_grad^T j = (C G)^T t = 0: weak-curl loads annihilate gradients."""
+    cfg = cf.get("C5r")
+    P = Problem(cfg)
+    sd = P.subs[5]
+    K, j, Cm, M2, t = P.assemble(sd, with_face=True)
+    G = local_grad(sd.ml)
+    jf = local_curl(sd.ml).T @ t
+    assert abs(G.T @ jf).max() <= 1e-13 * abs(jf).max()
+
+
+def test_manufactured_source_identity():
+    """J = curl curl A* = 2 pi^2 A* (SURVEY O3): curl of the generator's T by
+    central differences at random points."""
+    terms = cf.source_terms(cf.C1)[0]
+
+    def T(x):
+        out = np.zeros(3)
+        for c in range(3):
+            for coef, fx, fy, fz in terms[c]:
+                out[c] += coef * cf.f1d(fx)(x[0]) * cf.f1d(fy)(x[1]) * cf.f1d(fz)(x[2])
+        return out
+
+    rng = np.random.default_rng(1)
+    h = 1e-5
+    for _ in range(10):
+        x = rng.uniform(0, 1, 3)
+        J = np.zeros((3, 3))
+        for b in range(3):
+            dx = np.zeros(3)
+            dx[b] = h
+            J[:, b] = (T(x + dx) - T(x - dx)) / (2 * h)
+        curlT = np.array([J[2, 1] - J[1, 2], J[0, 2] - J[2, 0], J[1, 0] - J[0, 1]])
+        s = np.sin(np.pi * x)
+        Astar = np.array([s[1] * s[2], s[2] * s[0], s[0] * s[1]])
+        assert np.allclose(curlT, 2 * np.pi ** 2 * Astar, atol=1e-6)
+
+
+# ------------------------------------------------------------ gauge, counts ---
+def test_bar_and_cube27_trees():
+    """SPEC.md:127-128, :310-312 graph and tree counts."""
+    bar = Problem(cfg_custom("bar", (2, 1, 1), 1, 1, (2, 1, 1)))
+    g = GOLD["bar2_p1_e1"]
+    assert bar.grid.nv == g["vertices"] and bar.grid.ne == g["edges"]
+    assert bar.tree.sum() == g["tree"]
+    w1 = bar.weight == 1
+    assert w1.sum() == g["weight1"] and (bar.tree & w1).sum() == g["weight1_in_tree"]
+    c27 = Problem(cfg_custom("c27", (3, 3, 3), 1, 1, (3, 1, 1)))
+    g = GOLD["cube27_p1_e1"]
+    assert c27.grid.nv == g["vertices"] and c27.grid.ne == g["edges"] and c27.tree.sum() == g["tree"]
+
+
+def _closed_form_ngp(T):
+    nx, ny, nz = T
+    lines = (ny - 1) * (nz - 1) + (nx - 1) * (nz - 1) + (nx - 1) * (ny - 1)
+    junctions = (nx - 1) * (ny - 1) * (nz - 1)
+    return lines + 2 * junctions
+
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3", "C5"])
+def test_global_counts(name):
+    """E_int - V_int = (m-2)^2 (2m-1); n_gp closed form F4 (App. B3);
+    weight-1/2 counts (App. A); Sum n_r - m_r + n_gp = E_int - V_int."""
+    cfg = cf.get(name)
+    P = Problem(cfg)
+    c = P.counts()
+    m = P.grid.m[0]
+    assert c["E_int"] - c["V_int"] == (m - 2) ** 2 * (2 * m - 1)
+    assert c["n_gp"] == _closed_form_ngp(cfg.tiling)
+    w1, w2, ngp = GOLD["weight12_counts"][name]
+    assert (c["w_counts"][0], c["w_counts"][1], c["n_gp"]) == (w1, w2, ngp)
+    assert c["sum_nr"] - c["m_r"] + c["n_gp"] == c["E_int"] - c["V_int"]
+    if name == "C2":
+        assert c["m_r"] == GOLD["C2_m_r_hand_count"]["m_r"]
+
+
+@pytest.mark.parametrize("name", ["C1", "C2r", "C3r", "C5r"])
+def test_tree_properties(name):
+    """Spanning tree (V-1 edges, connected), pure-Python Kruskal equals the
+    unique-key MST, Dirichlet restriction is a spanning tree of the boundary
+    graph, classes exhaustive/disjoint, n_gp independent of e
+    (PAPER.md:180)."""
+    cfg = cf.get(name)
+    P = Problem(cfg, kruskal="python")
+    Q = Problem(cfg, kruskal="scipy")
+    assert np.array_equal(P.tree, Q.tree)
+    g = P.grid
+    assert P.tree.sum() == g.nv - 1
+    A = sp.csr_matrix((np.ones(P.tree.sum()), (P.eu[P.tree], P.ev[P.tree])), shape=(g.nv, g.nv))
+    assert connected_components(A, directed=False)[0] == 1
+    dv = g.dirichlet_vertices()
+    de = P.dir_edge
+    nb = dv.sum()
+    Ab = sp.csr_matrix((np.ones(de.sum()), (P.eu[de], P.ev[de])), shape=(g.nv, g.nv))
+    ncomp_b = connected_components(Ab[dv][:, dv], directed=False)[0]
+    assert (P.tree & de).sum() == nb - ncomp_b
+    assert set(np.unique(P.weight)) <= {1, 2, 3, 4, 5}
+    full = Problem(cf.get(name[:2])) if name != "C1" else P
+    assert P.n_primal == full.n_primal
+
+
+def test_c1_per_subdomain_counts():
+    b, P = make_bundle("C1", with_problem=True)
+    g = GOLD["C1_per_subdomain"]
+    for s in b["subs"]:
+        nr = s["n"] - len(s["tree"]) - len(s["prim"])
+        assert s["n"] == g["n_k"] and len(s["tree"]) == g["tree"] and nr == g["n_r"]
+        assert len(s["B_dof"]) == g["r_I"] and nr - len(s["B_dof"]) == g["r_V"]
+
+
+@pytest.mark.parametrize("name", ["C2r", "C5r"])
+def test_B_structure(name):
+    """Each multiplier row has one +1 (lower subdomain) and one -1 (F3);
+    each remaining interface DOF in exactly one row; tree consistent across
+    interfaces; primal DOFs shared by >= 3 subdomains."""
+    b, P = make_bundle(name, with_problem=True)
+    rows = {}
+    for k, s in enumerate(b["subs"]):
+        assert len(np.unique(s["B_dof"])) == len(s["B_dof"])
+        for lam, sg in zip(s["B_lambda"], s["B_sign"]):
+            rows.setdefault(int(lam), []).append((k, int(sg)))
+    assert len(rows) == b["n_lambda"]
+    for lam, ent in rows.items():
+        assert len(ent) == 2
+        (k1, s1), (k2, s2) = sorted(ent)
+        assert s1 == 1 and s2 == -1
+    for sd in P.subs:
+        tr = P.tree[sd.gid]
+        assert np.array_equal(np.flatnonzero(tr), sd.tree)
+    assert np.all(P.membership[P.primal_edges] >= 3)

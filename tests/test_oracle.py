@@ -1,0 +1,172 @@
+"""Pins of the CPU oracle (oracle/dp.py): it must reproduce plain definitions it
+does not share code with — the monolithic gauged Galerkin solve,
+the direct solve of the saddle system Eq. (5) — plus
+operator properties (symmetry, definiteness), the degenerate cases, the energy
+identity, the scaling invariance of PCG and the flux error's order h^p
+(PAPER.md:258).
+"""
+from dataclasses import replace
+
+import numpy as np
+import pytest
+import scipy.linalg as la
+
+from ietigen import configs as cf
+from ietigen.bundle import make_bundle
+from ietigen.problem import Problem
+from oracle import dp, brute
+
+
+def rel(a, b):
+    return np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300)
+
+
+@pytest.fixture(scope="module")
+def bundles():
+    return {n: make_bundle(n) for n in ["C1", "C2r", "C3r"]}
+
+
+@pytest.mark.parametrize("name", ["C1", "C2r", "C3r"])
+def test_dd_equals_monolithic_and_saddle(bundles, name):
+    b = bundles[name]
+    res = dp.solve(b, tol=1e-12, check_spd=(name == "C1"))
+    U = np.concatenate(res["u"])
+    um, _, _, _ = brute.monolithic_solve(b)
+    us, lam_s, p_s = brute.saddle_solve(b)
+    assert rel(U, np.concatenate(um)) <= 1e-9
+    assert rel(U, np.concatenate(us)) <= 1e-9
+    # lambda is a force like j; C1's lambda vanishes by mirror symmetry, so the
+    # denominator is floored at ||j|| (reading R9)
+    jn = np.linalg.norm(np.concatenate([s["f"].ravel() for s in b["subs"]]))
+    assert np.linalg.norm(res["lam"] - lam_s) <= 1e-8 * max(np.linalg.norm(lam_s), jn)
+    assert np.all(res["converged"]) and np.all(res["rel_residual"] <= 1e-11)
+
+
+def test_operator_symmetric_positive_definite(bundles):
+    """F_DP (= -S of PAPER.md:128) SPD, M_D^-1 symmetric PSD, S_PiPi SPD."""
+    for name in ["C1", "C2r"]:
+        D = dp.DualPrimal(bundles[name])
+        n = D.nl
+        if n > 800:
+            idx = np.random.default_rng(0).choice(n, 60, replace=False)
+            E = np.zeros((n, 60))
+            E[idx, np.arange(60)] = 1
+            X = np.random.default_rng(1).standard_normal((n, 8))
+            FX = D.apply_F(X)
+            assert np.allclose(X.T @ FX, (X.T @ FX).T, rtol=1e-10, atol=1e-10 * abs(X.T @ FX).max())
+            MX = D.apply_M(X)
+            assert np.allclose(X.T @ MX, (X.T @ MX).T, rtol=1e-10, atol=1e-10 * abs(X.T @ MX).max())
+            assert np.all(np.einsum("ij,ij->j", X, FX) > 0)
+            continue
+        F = D.apply_F(np.eye(n))
+        M = D.apply_M(np.eye(n))
+        assert np.allclose(F, F.T, atol=1e-12 * abs(F).max())
+        assert np.linalg.eigvalsh(F).min() > 0
+        assert np.linalg.eigvalsh((M + M.T) / 2).min() > -1e-12 * abs(M).max()
+        if D.ng:
+            assert np.linalg.eigvalsh(D.S).min() > 0
+
+
+def test_dirichlet_schur_is_inverse_of_inverse_block(bundles):
+    """S_{r_I r_I} of Eq. (10) equals ([K_rr^-1]_{II})^-1 (Schur-complement identity),
+    computed two independent ways."""
+    D = dp.DualPrimal(bundles["C2r"])
+    L = D.loc[5]
+    Kd = L.Krr.toarray()
+    Kinv = np.linalg.inv(Kd)
+    S2 = np.linalg.inv(Kinv[np.ix_(L.rI, L.rI)])
+    assert rel(L.SII, S2) <= 1e-9
+
+
+def test_zero_rhs_zero_iterations(bundles):
+    D = dp.DualPrimal(bundles["C2r"])
+    lam, info = D.pcg(d=np.zeros((D.nl, 1)))
+    assert info["iters"][0] == 0 and np.all(lam == 0)
+
+
+def test_continuity_energy_and_jump(bundles):
+    """B u = 0 at convergence and sum_k u_k^T K_k u_k = j^T u."""
+    b = bundles["C3r"]
+    res = dp.solve(b)
+    D = res["dp"]
+    jump = np.zeros((D.nl, 1))
+    energy = 0.0
+    work = 0.0
+    for L, u in zip(D.loc, res["u"]):
+        jump += L.Br @ u[L.r]
+        energy += float(u[:, 0] @ (L.K @ u[:, 0]))
+        work += float(L.f[:, 0] @ u[:, 0])
+    unorm = np.linalg.norm(np.concatenate(res["u"]))
+    assert np.linalg.norm(jump) <= 1e-8 * unorm
+    assert abs(energy - work) <= 1e-9 * abs(work)
+
+
+def test_single_subdomain_degenerate():
+    """N_sub = 1: m_r = 0, n_gp = 0, DD = monolithic."""
+    cfg = replace(cf.C1, name="one", tiling=(1, 1, 1))
+    b = make_bundle(cfg)
+    assert b["n_lambda"] == 0 and b["n_primal"] == 0
+    res = dp.solve(b)
+    um, _, _, _ = brute.monolithic_solve(b)
+    assert rel(np.concatenate(res["u"]), np.concatenate(um)) <= 1e-12
+    assert res["iters"][0] == 0
+
+
+def test_ungauged_block_is_singular():
+    """Without the tree elimination K_rr keeps the gradient kernel."""
+    b = make_bundle("C1")
+    b["subs"][1]["tree"] = np.zeros(0, np.int32)
+    with pytest.raises(dp.LocalSingular) as ei:
+        dp.DualPrimal(b, check_spd=True)
+    assert ei.value.k == 1
+
+
+def test_multiplicity_scaling_equals_identity_scaling(bundles):
+    """delta = 1/2 gives the same iterates as D_s = I: PCG is
+    invariant under M -> c M (SURVEY App. B numerical confirmation)."""
+    b = bundles["C2r"]
+    D = dp.DualPrimal(b, scaling="multiplicity")
+    lam1, i1 = D.pcg(tol=1e-10)
+    for L in D.loc:
+        L.BD = L.BD * 2.0
+    lam2, i2 = D.pcg(tol=1e-10)
+    assert i1["iters"][0] == i2["iters"][0]
+    assert rel(lam1, lam2) <= 1e-12
+
+
+def test_stiffness_weights_partition_of_unity():
+    b = make_bundle("C3r")
+    D = dp.DualPrimal(b)
+    acc = {}
+    for L in D.loc:
+        for lam, dlt in zip(L.B_lambda, L.delta):
+            acc[int(lam)] = acc.get(int(lam), 0.0) + dlt
+    assert np.allclose(list(acc.values()), 1.0, atol=1e-15)
+
+
+def _eps_B(cfg, us=None):
+    """Flux error via ||B_h - T||^2 = b'M2b - 2 b't + ||T||^2,
+    ||curl A*||^2 = 3 pi^2 / 2 over the unit cube (closed form)."""
+    b, P = make_bundle(cfg, with_problem=True)
+    if us is None:
+        us, _, _, _ = brute.monolithic_solve(b)
+    tot = 0.0
+    for sd, u in zip(P.subs, us):
+        K, j, C, M2, t = P.assemble(sd, with_face=True)
+        bf = C @ u[:, 0]
+        tot += bf @ (M2 @ bf) - 2 * bf @ t[:, 0]
+    return np.sqrt(tot + 1.5 * np.pi ** 2)
+
+
+def test_flux_error_order_p():
+    """EOC of eps_B = p +- 0.3; DD eps_B equals the
+    monolithic eps_B."""
+    e1 = [_eps_B(replace(cf.C1, name=f"C1e{e}", e=e)) for e in (2, 4, 8)]
+    eoc1 = np.log2(np.array(e1[:-1]) / np.array(e1[1:]))
+    assert np.all(np.abs(eoc1 - 1) <= 0.3), eoc1
+    e2 = [_eps_B(replace(cf.C2, name=f"C2e{e}", e=e)) for e in (2, 4)]
+    eoc2 = np.log2(e2[0] / e2[1])
+    assert abs(eoc2 - 2) <= 0.3, eoc2
+    c = replace(cf.C1, name="C1e4", e=4)
+    res = dp.solve(make_bundle(c), tol=1e-12)
+    assert abs(_eps_B(c, res["u"]) - e1[1]) <= 1e-9 * e1[1]
