@@ -1,0 +1,864 @@
+// Host-side set-up of the IETI-DP solve phase: validation of the C-ABI inputs,
+// DOF classification (tree / primal / r_V / r_I),
+// nested-dissection ordering of r_V with r_I last,
+// symbolic supernodal factorisation and the batched level schedule.
+//
+// This is integer work only (the documented host exception, like a
+// sparse direct solver's reordering); every floating-point operation of the
+// method runs in the CUDA kernels. Values are never touched here except for
+// being copied to the device.
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <climits>
+#include <cstring>
+#include <numeric>
+#include <thread>
+
+#include "handle.h"
+
+namespace ieti {
+
+namespace {
+
+struct LocalResult {
+  SubPlan sp;
+  std::vector<SnHost> sn;  // local ids, parent local
+  ietidp_status st = IETIDP_OK;
+  std::string err;
+};
+
+// ---------------------------------------------------------------------------
+// Nested dissection on the graph of K_VV (level-structure vertex separators)
+// ---------------------------------------------------------------------------
+struct NestedDissection {
+  const std::vector<int>& xadj;
+  const std::vector<int>& adj;
+  int leaf;
+  std::vector<int> reg, stamp, lev;
+  int next_reg = 1, cur_stamp = 0;
+  struct Node {
+    std::vector<int> vars;
+    std::vector<int> children;
+  };
+  std::vector<Node> nodes;
+
+  NestedDissection(const std::vector<int>& xa, const std::vector<int>& ad, int nv, int leaf_)
+      : xadj(xa), adj(ad), leaf(leaf_), reg(nv, 0), stamp(nv, 0), lev(nv, 0) {}
+
+  // BFS inside region rid; returns visit order and level starts.
+  void bfs(int src, int rid, std::vector<int>& order, std::vector<int>& lstart) {
+    ++cur_stamp;
+    order.clear();
+    lstart.clear();
+    order.push_back(src);
+    stamp[src] = cur_stamp;
+    lev[src] = 0;
+    lstart.push_back(0);
+    size_t head = 0;
+    int curlev = 0;
+    while (head < order.size()) {
+      int v = order[head];
+      if (lev[v] != curlev) {
+        curlev = lev[v];
+        lstart.push_back((int)head);
+      }
+      ++head;
+      for (int e = xadj[v]; e < xadj[v + 1]; ++e) {
+        int u = adj[e];
+        if (reg[u] != rid || stamp[u] == cur_stamp) continue;
+        stamp[u] = cur_stamp;
+        lev[u] = lev[v] + 1;
+        order.push_back(u);
+      }
+    }
+    lstart.push_back((int)order.size());
+  }
+
+  int degree_in(int v, int rid) const {
+    int d = 0;
+    for (int e = xadj[v]; e < xadj[v + 1]; ++e) d += (reg[adj[e]] == rid);
+    return d;
+  }
+
+  // Split the vertices of region `rid` (listed in C) into connected components,
+  // each getting a fresh region id.
+  std::vector<std::pair<std::vector<int>, int>> components(const std::vector<int>& C, int rid) {
+    std::vector<std::pair<std::vector<int>, int>> out;
+    for (int v : C) {
+      if (reg[v] != rid) continue;
+      int nr = next_reg++;
+      std::vector<int> comp{v};
+      reg[v] = nr;
+      for (size_t h = 0; h < comp.size(); ++h) {
+        int w = comp[h];
+        for (int e = xadj[w]; e < xadj[w + 1]; ++e) {
+          int u = adj[e];
+          if (reg[u] == rid) {
+            reg[u] = nr;
+            comp.push_back(u);
+          }
+        }
+      }
+      out.emplace_back(std::move(comp), nr);
+    }
+    return out;
+  }
+
+  int make_node(std::vector<int> vars, std::vector<int> children) {
+    std::sort(vars.begin(), vars.end());
+    nodes.push_back({std::move(vars), std::move(children)});
+    return (int)nodes.size() - 1;
+  }
+
+  int build(const std::vector<int>& C, int rid) {
+    if ((int)C.size() <= leaf) return make_node(C, {});
+    std::vector<int> order, lstart;
+    // pseudo-peripheral start vertex (George-Liu style)
+    int v = C[0];
+    int ecc = -1;
+    for (int it = 0; it < 5; ++it) {
+      bfs(v, rid, order, lstart);
+      int nlev = (int)lstart.size() - 1;
+      if (nlev - 1 <= ecc) break;
+      ecc = nlev - 1;
+      int best = order[lstart[nlev - 1]], bd = INT_MAX;
+      for (int i = lstart[nlev - 1]; i < lstart[nlev]; ++i) {
+        int d = degree_in(order[i], rid);
+        if (d < bd) bd = d, best = order[i];
+      }
+      v = best;
+    }
+    bfs(v, rid, order, lstart);
+    int nlev = (int)lstart.size() - 1;
+    if (nlev < 3) return make_node(C, {});
+    const int n = (int)C.size();
+    // smallest level among the balanced ones (both sides >= 30% of the rest)
+    int pick = -1, psz = INT_MAX, half = -1, hdist = INT_MAX;
+    for (int l = 1; l < nlev - 1; ++l) {
+      int below = lstart[l], sz = lstart[l + 1] - lstart[l], above = n - lstart[l + 1];
+      int rest = n - sz;
+      if (std::min(below, above) >= 0.30 * rest && sz < psz) psz = sz, pick = l;
+      int dist = std::abs(below - above);
+      if (dist < hdist) hdist = dist, half = l;
+    }
+    if (pick < 0) pick = half;
+    std::vector<int> sep(order.begin() + lstart[pick], order.begin() + lstart[pick + 1]);
+    for (int s : sep) reg[s] = 0;
+    std::vector<int> rest;
+    rest.reserve(n - sep.size());
+    for (int u : C)
+      if (reg[u] == rid) rest.push_back(u);
+    auto comps = components(rest, rid);
+    std::vector<int> ch;
+    for (auto& c : comps) ch.push_back(build(c.first, c.second));
+    return make_node(std::move(sep), std::move(ch));
+  }
+};
+
+LocalResult analyze_sub(const SubIn& in, int k, int nrhs, int ordering, int leaf) {
+  LocalResult R;
+  SubPlan& sp = R.sp;
+  const int n = in.n;
+  auto fail = [&](ietidp_status st, const std::string& m) {
+    R.st = st;
+    R.err = "subdomain " + std::to_string(k) + ": " + m;
+    return R;
+  };
+  // ---- classification (tree / primal / remaining; r_I = supp B) ----
+  std::vector<int8_t> cls(n, 0);
+  for (int t : in.tree) {
+    if (cls[t]) return fail(IETIDP_E_ARG, "tree DOF listed twice");
+    cls[t] = 1;
+  }
+  for (int t : in.prim) {
+    if (cls[t]) return fail(IETIDP_E_ARG, "primal DOF overlaps the tree or repeats");
+    cls[t] = 2;
+  }
+  std::vector<char> isB(n, 0);
+  for (int d : in.B_dof) {
+    if (cls[d]) return fail(IETIDP_E_B_STRUCTURE, "B touches a tree or primal DOF");
+    if (isB[d]) return fail(IETIDP_E_B_STRUCTURE, "a DOF carries two multipliers");
+    isB[d] = 1;
+  }
+  std::vector<int> rV, rI, vidx(n, -1);
+  for (int i = 0; i < n; ++i) {
+    if (cls[i]) continue;
+    if (isB[i]) rI.push_back(i);
+    else {
+      vidx[i] = (int)rV.size();
+      rV.push_back(i);
+    }
+  }
+  sp.nV = (int)rV.size();
+  sp.nI = (int)rI.size();
+  sp.nr = sp.nV + sp.nI;
+  sp.nP = (int)in.prim.size();
+  sp.ploc.assign(n, -1);
+  for (int q = 0; q < sp.nP; ++q) sp.ploc[in.prim[q]] = q;
+
+  // ---- graph of K_VV ----
+  std::vector<int> xadj(sp.nV + 1, 0), adj;
+  for (int a = 0; a < sp.nV; ++a) {
+    int i = rV[a];
+    for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) {
+      int j = in.col[e];
+      if (j != i && vidx[j] >= 0) adj.push_back(vidx[j]);
+    }
+    xadj[a + 1] = (int)adj.size();
+  }
+
+  // ---- ordering: supernode tree in postorder ----
+  std::vector<std::vector<int>> sn_vars;       // in postorder (local vertex ids of rV)
+  if (sp.nV > 0) {
+    if (ordering == IETIDP_ORDER_DENSE) {
+      std::vector<int> all(sp.nV);
+      std::iota(all.begin(), all.end(), 0);
+      sn_vars.push_back(all);
+    } else {
+      NestedDissection nd(xadj, adj, sp.nV, std::max(leaf, 8));
+      std::vector<int> all(sp.nV);
+      std::iota(all.begin(), all.end(), 0);
+      for (int a = 0; a < sp.nV; ++a) nd.reg[a] = -1;
+      auto comps = nd.components(all, -1);
+      std::vector<int> roots;
+      for (auto& c : comps) roots.push_back(nd.build(c.first, c.second));
+      // iterative postorder
+      std::vector<std::pair<int, size_t>> st;
+      for (int r : roots) {
+        st.push_back({r, 0});
+        while (!st.empty()) {
+          auto& top = st.back();
+          auto& node = nd.nodes[top.first];
+          if (top.second < node.children.size()) {
+            int c = node.children[top.second++];
+            st.push_back({c, 0});
+          } else {
+            sn_vars.push_back(node.vars);
+            st.pop_back();
+          }
+        }
+      }
+    }
+  }
+  // positions
+  sp.perm.resize(sp.nr);
+  sp.pos.assign(n, -1);
+  std::vector<int> owner(sp.nr, -1);
+  int p = 0;
+  for (size_t s = 0; s < sn_vars.size(); ++s) {
+    SnHost h;
+    h.sub = k;
+    h.c0 = p;
+    h.npiv = (int)sn_vars[s].size();
+    h.parent = -1;
+    h.level = 0;
+    for (int v : sn_vars[s]) {
+      int dof = rV[v];
+      sp.perm[p] = dof;
+      sp.pos[dof] = p;
+      owner[p] = (int)s;
+      ++p;
+    }
+    R.sn.push_back(std::move(h));
+  }
+  if (sp.nI > 0) {
+    SnHost h;
+    h.sub = k;
+    h.c0 = p;
+    h.npiv = sp.nI;
+    h.parent = -1;
+    h.level = 0;
+    for (int dof : rI) {
+      sp.perm[p] = dof;
+      sp.pos[dof] = p;
+      owner[p] = (int)R.sn.size();
+      ++p;
+    }
+    sp.root = (int)R.sn.size();
+    R.sn.push_back(std::move(h));
+  }
+  // ---- symbolic factorisation: row structure of every supernode ----
+  std::vector<int> mark(sp.nr, -1);
+  for (size_t s = 0; s < R.sn.size(); ++s) {
+    SnHost& h = R.sn[s];
+    int last = h.c0 + h.npiv - 1;
+    std::vector<int> rows;
+    for (int q = h.c0; q <= last; ++q) {
+      int dof = sp.perm[q];
+      for (int64_t e = in.rowptr[dof]; e < in.rowptr[dof + 1]; ++e) {
+        int pj = sp.pos[in.col[e]];
+        if (pj > last && mark[pj] != (int)s) {
+          mark[pj] = (int)s;
+          rows.push_back(pj);
+        }
+      }
+    }
+    for (int c : h.children)
+      for (int x : R.sn[c].rows)
+        if (x > last && mark[x] != (int)s) {
+          mark[x] = (int)s;
+          rows.push_back(x);
+        }
+    std::sort(rows.begin(), rows.end());
+    h.rows = std::move(rows);
+    h.f = h.npiv + (int)h.rows.size();
+    if (!h.rows.empty()) {
+      h.parent = owner[h.rows[0]];
+      R.sn[h.parent].children.push_back((int)s);
+    }
+    int lv = 0;
+    for (int c : h.children) lv = std::max(lv, R.sn[c].level + 1);
+    h.level = lv;
+  }
+  (void)nrhs;
+  return R;
+}
+
+int find_in_front(const SnHost& s, int x) {
+  if (x >= s.c0 && x < s.c0 + s.npiv) return x - s.c0;
+  auto it = std::lower_bound(s.rows.begin(), s.rows.end(), x);
+  if (it == s.rows.end() || *it != x) return -1;
+  return s.npiv + (int)(it - s.rows.begin());
+}
+
+}  // namespace
+
+static void fill_report(ietidp_s* h) {
+  const Plan& P = h->plan;
+  const int ns = h->n_sub;
+  const int nsn = (int)P.sn.size();
+  h->rep.n_supernodes = nsn;
+  h->rep.n_levels = P.max_level + 1;
+  h->rep.max_front = P.max_front;
+  h->rep.max_nI = P.max_nI;
+  long long snr = 0, snI = 0, sI2 = 0, sIP = 0;
+  for (int k = 0; k < ns; ++k) {
+    snr += P.subs[k].nr;
+    snI += P.subs[k].nI;
+    sI2 += (long long)P.subs[k].nI * P.subs[k].nI;
+    sIP += (long long)P.subs[k].nI * P.subs[k].nP;
+  }
+  h->rep.sum_nr = snr;
+  h->rep.sum_nI = snI;
+  h->rep.nnz_L = P.nnz_L;
+  h->rep.factor_flops = P.flops;
+  // algorithmic bytes (DESIGN.md §"Rooflines"): the F-apply reads the lower
+  // triangle of every L_II twice (forward, backward) and G twice; the
+  // preconditioner reads it twice (L^T, L).
+  h->rep.f_apply_bytes = 2 * 8 * ((sI2 + snI) / 2) + 2 * 8 * sIP;
+  h->rep.pcg_bytes_per_iter = 4 * 8 * ((sI2 + snI) / 2) + 2 * 8 * sIP;
+}
+
+// Build the complete plan and upload every structure and the raw values.
+void analyze_all(ietidp_s* h) {
+  auto t0 = std::chrono::steady_clock::now();
+  const int ns = h->n_sub, nrhs = h->nrhs;
+  for (int k = 0; k < ns; ++k)
+    if (!h->in[k].set) throw Error(IETIDP_E_STATE, "subdomain " + std::to_string(k) + " not set");
+
+  // ---- global B validation (R6) ----
+  std::vector<int> cnt(h->n_lambda, 0), ssum(h->n_lambda, 0), firstsub(h->n_lambda, -1);
+  for (int k = 0; k < ns; ++k) {
+    const SubIn& in = h->in[k];
+    for (size_t e = 0; e < in.B_lambda.size(); ++e) {
+      int l = in.B_lambda[e];
+      if (cnt[l] == 1 && firstsub[l] == k)
+        throw Error(IETIDP_E_B_STRUCTURE, "multiplier " + std::to_string(l) + " twice in subdomain " + std::to_string(k));
+      cnt[l]++;
+      ssum[l] += in.B_sign[e];
+      firstsub[l] = k;
+    }
+  }
+  for (int l = 0; l < h->n_lambda; ++l)
+    if (cnt[l] != 2 || ssum[l] != 0)
+      throw Error(IETIDP_E_B_STRUCTURE, "multiplier row " + std::to_string(l) + " is not {+1,-1} in two subdomains");
+
+  // ---- per-subdomain analysis, in parallel ----
+  std::vector<LocalResult> loc(ns);
+  {
+    int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    std::atomic<int> next{0};
+    for (int t = 0; t < nth; ++t)
+      th.emplace_back([&]() {
+        for (int k; (k = next++) < ns;)
+          loc[k] = analyze_sub(h->in[k], k, nrhs, h->opt.ordering, h->opt.leaf_size);
+      });
+    for (auto& x : th) x.join();
+  }
+  for (int k = 0; k < ns; ++k)
+    if (loc[k].st != IETIDP_OK) throw Error(loc[k].st, loc[k].err);
+
+  Plan& P = h->plan;
+  P = Plan();
+  P.subs.resize(ns);
+  h->h_sub.assign(ns, SubDev{});
+  // ---- global supernode numbering ----
+  std::vector<int> sn_base(ns + 1, 0);
+  for (int k = 0; k < ns; ++k) sn_base[k + 1] = sn_base[k] + (int)loc[k].sn.size();
+  P.sn.reserve(sn_base[ns]);
+  for (int k = 0; k < ns; ++k) {
+    P.subs[k] = std::move(loc[k].sp);
+    for (auto& s : loc[k].sn) {
+      SnHost g = std::move(s);
+      if (g.parent >= 0) g.parent += sn_base[k];
+      for (int& c : g.children) c += sn_base[k];
+      P.sn.push_back(std::move(g));
+    }
+    P.subs[k].sn_begin = {sn_base[k], sn_base[k + 1]};
+    if (P.subs[k].root >= 0) P.subs[k].root += sn_base[k];
+  }
+  const int nsn = (int)P.sn.size();
+  for (auto& s : P.sn) P.max_level = std::max(P.max_level, s.level);
+  // level groups, each sorted by npiv descending (the active fronts of a panel are a prefix)
+  std::vector<std::vector<int>> bylev(P.max_level + 1);
+  for (int i = 0; i < nsn; ++i) bylev[P.sn[i].level].push_back(i);
+  for (auto& v : bylev)
+    std::stable_sort(v.begin(), v.end(), [&](int a, int b) { return P.sn[a].npiv > P.sn[b].npiv; });
+
+  // ---- memory layout ----
+  std::vector<SnDev> sd(nsn);
+  std::vector<int> rows_all, rel_all, children_all, work;
+  long long pool = 0, dinv = 0, vec = 0;
+  P.levels.resize(P.max_level + 1);
+  for (int L = 0; L <= P.max_level; ++L) {
+    LevelPlan& lp = P.levels[L];
+    lp.front_begin = pool;
+    lp.sn_off = (int)P.level_sn.size();
+    lp.sn_n = (int)bylev[L].size();
+    for (int i : bylev[L]) {
+      SnHost& s = P.sn[i];
+      SnDev& d = sd[i];
+      d.f = s.f;
+      d.ld = (s.f + 3) & ~3;
+      d.npiv = s.npiv;
+      d.c0 = s.c0;
+      d.sub = s.sub;
+      d.parent = s.parent;
+      d.front_off = pool;
+      pool += (long long)d.ld * d.f;
+      d.dinv_off = dinv;
+      dinv += (long long)((s.npiv + TB - 1) / TB) * TILE_ELEMS;
+      d.vec_off = vec;
+      vec += s.f;
+      P.level_sn.push_back(i);
+      P.max_front = std::max(P.max_front, s.f);
+      for (int j = 0; j < s.npiv; ++j) {
+        long long c = s.f - j;
+        P.nnz_L += c;
+        P.flops += c * c;
+      }
+    }
+    lp.front_end = pool;
+  }
+  P.pool_doubles = pool;
+  P.dinv_doubles = dinv;
+  P.vec_doubles = vec;
+  for (int i = 0; i < nsn; ++i) {
+    SnHost& s = P.sn[i];
+    SnDev& d = sd[i];
+    d.rows_off = (int)rows_all.size();
+    rows_all.insert(rows_all.end(), s.rows.begin(), s.rows.end());
+    d.rel_off = (int)rel_all.size();
+    if (s.parent >= 0) {
+      const SnHost& par = P.sn[s.parent];
+      for (int x : s.rows) {
+        int r = find_in_front(par, x);
+        if (r < 0) throw Error(IETIDP_E_ARG, "internal: symbolic structure not nested");
+        rel_all.push_back(r);
+      }
+    }
+    d.child_off = (int)children_all.size();
+    d.nchild = (int)s.children.size();
+    children_all.insert(children_all.end(), s.children.begin(), s.children.end());
+  }
+
+  // ---- work lists of the factorisation ----
+  for (int L = 0; L <= P.max_level; ++L) {
+    LevelPlan& lp = P.levels[L];
+    // extend-add, one launch per child slot
+    int maxc = 0;
+    for (int i : bylev[L]) maxc = std::max(maxc, (int)P.sn[i].children.size());
+    for (int q = 0; q < maxc; ++q) {
+      int off = (int)work.size() / 3, n = 0;
+      for (int i : bylev[L])
+        if ((int)P.sn[i].children.size() > q) {
+          int c = P.sn[i].children[q];
+          int nu = P.sn[c].f - P.sn[c].npiv;
+          for (int j0 = 0; j0 < nu; j0 += 32) {
+            work.insert(work.end(), {c, j0, std::min(nu, j0 + 32)});
+            ++n;
+          }
+        }
+      if (n) lp.ea.push_back({off, n});
+    }
+    int maxp = 0;
+    for (int i : bylev[L]) maxp = std::max(maxp, (P.sn[i].npiv + TB - 1) / TB);
+    for (int kp = 0; kp < maxp; ++kp) {
+      LevelPlan::Panel pn{};
+      pn.potrf_off = (int)work.size() / 3;
+      for (int i : bylev[L])
+        if (P.sn[i].npiv > kp * TB) {
+          work.insert(work.end(), {i, kp, 0});
+          pn.potrf_n++;
+        }
+      pn.trsm_off = (int)work.size() / 3;
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (s.npiv <= kp * TB) continue;
+        int b = std::min(TB, s.npiv - kp * TB);
+        int start = kp * TB + b, nrow = s.f - start;
+        for (int t = 0; t * TB < nrow; ++t) {
+          work.insert(work.end(), {i, kp, t});
+          pn.trsm_n++;
+        }
+      }
+      pn.upd_off = (int)work.size() / 3;
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (s.npiv <= kp * TB) continue;
+        int b = std::min(TB, s.npiv - kp * TB);
+        int start = kp * TB + b, nrow = s.f - start;
+        int nt = (nrow + TB - 1) / TB;
+        // trailing update of the lower triangle: later pivot columns and the
+        // update (Schur) block alike
+        for (int ti = 0; ti < nt; ++ti)
+          for (int tj = 0; tj <= ti; ++tj) {
+            work.insert(work.end(), {i, kp, ti * 65536 + tj});
+            pn.upd_n++;
+          }
+      }
+      lp.panels.push_back(pn);
+    }
+  }
+
+  // ---- per-subdomain offsets ----
+  long long kv = 0, fv = 0, xo = 0, rio = 0, kppo = 0, go = 0, slo = 0, to = 0, dto = 0;
+  int po = 0, permo = 0;
+  P.nPmax = 0;
+  for (int k = 0; k < ns; ++k) P.nPmax = std::max(P.nPmax, P.subs[k].nP);
+  P.ncx = P.nPmax + nrhs;
+  h->kval_off.resize(ns);
+  h->fval_off.resize(ns);
+  h->u_off.resize(ns);
+  long long uo = 0;
+  for (int k = 0; k < ns; ++k) {
+    SubPlan& sp = P.subs[k];
+    SubDev& d = h->h_sub[k];
+    const SubIn& in = h->in[k];
+    d.nk = in.n;
+    d.nr = sp.nr;
+    d.nI = sp.nI;
+    d.nV = sp.nV;
+    d.nP = sp.nP;
+    d.root = sp.root;
+    d.x_off = xo;
+    xo += sp.nr;
+    d.rI_off = rio;
+    rio += sp.nI;
+    d.kval_off = kv;
+    h->kval_off[k] = kv;
+    kv += (long long)in.val.size();
+    d.f_off = fv;
+    h->fval_off[k] = fv;
+    fv += (long long)in.n * nrhs;
+    d.kpp_off = kppo;
+    kppo += (long long)sp.nP * sp.nP;
+    d.jp_off = (long long)po * nrhs;
+    d.floc_off = (long long)po * nrhs;
+    d.gk_off = (long long)po * nrhs;
+    d.prim_off = po;
+    po += sp.nP;
+    d.g_off = go;
+    go += (long long)sp.nI * sp.nP;
+    d.sloc_off = slo;
+    slo += (long long)sp.nP * sp.nP;
+    d.nt = (sp.nI + TB - 1) / TB;
+    d.tile_off = to;
+    to += (long long)d.nt * (d.nt + 1) / 2 * TILE_ELEMS;
+    d.dtile_off = dto;
+    dto += (long long)d.nt * TILE_ELEMS;
+    d.perm_off = permo;
+    permo += sp.nr;
+    h->u_off[k] = uo;
+    uo += (long long)in.n * nrhs;
+    P.max_nI = std::max(P.max_nI, sp.nI);
+  }
+  h->n_slots = (int)rio;
+  h->sum_nP = po;
+
+  // ---- scatter lists (built per subdomain in parallel, merged per level) ----
+  struct Scat {
+    std::vector<std::vector<long long>> fd;  // per level
+    std::vector<std::vector<int>> fs;
+    std::vector<long long> xd, kd, fxd, fpd;
+    std::vector<int> xs, ks, fxs, fps;
+    std::vector<int> kdiag;
+    std::string err;
+  };
+  std::vector<Scat> sc(ns);
+  {
+    int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+    std::vector<std::thread> th;
+    std::atomic<int> next{0};
+    for (int t = 0; t < nth; ++t)
+      th.emplace_back([&]() {
+        for (int k; (k = next++) < ns;) {
+          Scat& S = sc[k];
+          const SubIn& in = h->in[k];
+          const SubPlan& sp = P.subs[k];
+          const SubDev& d = h->h_sub[k];
+          S.fd.resize(P.max_level + 1);
+          S.fs.resize(P.max_level + 1);
+          // owner supernode of each position
+          std::vector<int> own(sp.nr);
+          for (int s = sp.sn_begin[0]; s < sp.sn_begin[1]; ++s)
+            for (int q = 0; q < P.sn[s].npiv; ++q) own[P.sn[s].c0 + q] = s;
+          S.kdiag.assign(sp.nI, -1);
+          // K_rr lower triangle, column by column in position order
+          for (int pj = 0; pj < sp.nr; ++pj) {
+            int j = sp.perm[pj];
+            int s = own[pj];
+            const SnHost& hs = P.sn[s];
+            const SnDev& ds = sd[s];
+            int lcol = pj - hs.c0;
+            for (int64_t e = in.rowptr[j]; e < in.rowptr[j + 1]; ++e) {
+              int i = in.col[e];
+              int pi = sp.pos[i];
+              if (pi < pj) continue;  // tree/primal (-1) or upper triangle
+              int lrow = find_in_front(hs, pi);
+              if (lrow < 0) {
+                S.err = "internal: entry outside the symbolic structure";
+                break;
+              }
+              S.fd[hs.level].push_back(ds.front_off + (long long)lcol * ds.ld + lrow);
+              S.fs[hs.level].push_back((int)(d.kval_off + e));
+              if (pi == pj && pj >= sp.nV) S.kdiag[pj - sp.nV] = (int)(d.kval_off + e);
+            }
+          }
+          for (int a = 0; a < sp.nI; ++a)
+            if (S.kdiag[a] < 0) S.err = "subdomain " + std::to_string(k) + ": missing diagonal entry";
+          // K_rP -> X0, K_PP -> kpp, f -> X0 / jp
+          for (int i = 0; i < in.n; ++i) {
+            int pi = sp.pos[i], qi = sp.ploc[i];
+            if (pi < 0 && qi < 0) continue;
+            for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) {
+              int qj = sp.ploc[in.col[e]];
+              if (qj < 0) continue;
+              if (pi >= 0) {
+                S.xd.push_back((d.x_off + pi) * P.ncx + qj);
+                S.xs.push_back((int)(d.kval_off + e));
+              } else {
+                S.kd.push_back(d.kpp_off + (long long)qi * sp.nP + qj);
+                S.ks.push_back((int)(d.kval_off + e));
+              }
+            }
+            for (int c = 0; c < nrhs; ++c) {
+              if (pi >= 0) {
+                S.fxd.push_back((d.x_off + pi) * P.ncx + P.nPmax + c);
+                S.fxs.push_back((int)(d.f_off + i + (long long)c * in.n));
+              } else {
+                S.fpd.push_back(d.jp_off + (long long)qi * nrhs + c);
+                S.fps.push_back((int)(d.f_off + i + (long long)c * in.n));
+              }
+            }
+          }
+        }
+      });
+    for (auto& x : th) x.join();
+  }
+  for (int k = 0; k < ns; ++k)
+    if (!sc[k].err.empty()) throw Error(IETIDP_E_ARG, sc[k].err);
+
+  std::vector<long long> fdst, xdst, kdst, fxdst, fpdst;
+  std::vector<int> fsrc, xsrc, ksrc, fxsrc, fpsrc, kdiag;
+  for (int L = 0; L <= P.max_level; ++L) {
+    P.levels[L].scat_begin = (long long)fdst.size();
+    for (int k = 0; k < ns; ++k) {
+      fdst.insert(fdst.end(), sc[k].fd[L].begin(), sc[k].fd[L].end());
+      fsrc.insert(fsrc.end(), sc[k].fs[L].begin(), sc[k].fs[L].end());
+      std::vector<long long>().swap(sc[k].fd[L]);
+      std::vector<int>().swap(sc[k].fs[L]);
+    }
+    P.levels[L].scat_end = (long long)fdst.size();
+  }
+  for (int k = 0; k < ns; ++k) {
+    xdst.insert(xdst.end(), sc[k].xd.begin(), sc[k].xd.end());
+    xsrc.insert(xsrc.end(), sc[k].xs.begin(), sc[k].xs.end());
+    kdst.insert(kdst.end(), sc[k].kd.begin(), sc[k].kd.end());
+    ksrc.insert(ksrc.end(), sc[k].ks.begin(), sc[k].ks.end());
+    fxdst.insert(fxdst.end(), sc[k].fxd.begin(), sc[k].fxd.end());
+    fxsrc.insert(fxsrc.end(), sc[k].fxs.begin(), sc[k].fxs.end());
+    fpdst.insert(fpdst.end(), sc[k].fpd.begin(), sc[k].fpd.end());
+    fpsrc.insert(fpsrc.end(), sc[k].fps.begin(), sc[k].fps.end());
+    kdiag.insert(kdiag.end(), sc[k].kdiag.begin(), sc[k].kdiag.end());
+  }
+
+  // ---- multipliers, slots, primal bookkeeping ----
+  std::vector<int> slot_lam(h->n_slots), slot_sub(h->n_slots);
+  std::vector<float> slot_sign(h->n_slots);
+  std::vector<LamDev> lam(h->n_lambda);
+  std::vector<int> lamfill(h->n_lambda, 0);
+  std::vector<int> prim_dof(po), prim_gid(po);
+  std::vector<int> perm_all(permo);
+  std::vector<char> gid_seen(h->n_primal, 0);
+  for (int k = 0; k < ns; ++k) {
+    const SubIn& in = h->in[k];
+    const SubPlan& sp = P.subs[k];
+    const SubDev& d = h->h_sub[k];
+    for (size_t e = 0; e < in.B_dof.size(); ++e) {
+      int slot = (int)d.rI_off + sp.pos[in.B_dof[e]] - sp.nV;
+      int l = in.B_lambda[e];
+      slot_lam[slot] = l;
+      slot_sub[slot] = k;
+      slot_sign[slot] = (float)in.B_sign[e];
+      lam[l].slot[lamfill[l]] = slot;
+      lam[l].sign[lamfill[l]] = (float)in.B_sign[e];
+      lamfill[l]++;
+    }
+    for (int q = 0; q < sp.nP; ++q) {
+      prim_dof[d.prim_off + q] = in.prim[q];
+      prim_gid[d.prim_off + q] = in.prim_gid[q];
+      gid_seen[in.prim_gid[q]] = 1;
+    }
+    std::copy(sp.perm.begin(), sp.perm.end(), perm_all.begin() + d.perm_off);
+  }
+  for (int g = 0; g < h->n_primal; ++g)
+    if (!gid_seen[g]) throw Error(IETIDP_E_ARG, "global primal " + std::to_string(g) + " has no local DOF");
+  // S_PP entry (g1, g2) <- sloc entries; global primal g <- primal rows
+  const int ng = h->n_primal;
+  std::vector<std::vector<int>> sl((size_t)ng * ng);
+  std::vector<std::vector<int>> pc(ng);
+  for (int k = 0; k < ns; ++k) {
+    const SubDev& d = h->h_sub[k];
+    for (int a = 0; a < d.nP; ++a) {
+      int ga = prim_gid[d.prim_off + a];
+      pc[ga].push_back(d.prim_off + a);
+      for (int b = 0; b < d.nP; ++b) {
+        int gb = prim_gid[d.prim_off + b];
+        sl[(size_t)ga * ng + gb].push_back((int)(d.sloc_off + (long long)a * d.nP + b));
+      }
+    }
+  }
+  std::vector<int> scoef_ptr((size_t)ng * ng + 1, 0), scoef_src, pcon_ptr(ng + 1, 0), pcon_src;
+  for (size_t e = 0; e < sl.size(); ++e) {
+    scoef_src.insert(scoef_src.end(), sl[e].begin(), sl[e].end());
+    scoef_ptr[e + 1] = (int)scoef_src.size();
+  }
+  for (int g = 0; g < ng; ++g) {
+    pcon_src.insert(pcon_src.end(), pc[g].begin(), pc[g].end());
+    pcon_ptr[g + 1] = (int)pcon_src.size();
+  }
+  for (int k = 0; k < ns; ++k) {
+    h->h_sub[k].root = P.subs[k].root;
+  }
+  auto t1 = std::chrono::steady_clock::now();
+  fill_report(h);
+  if (h->opt.device < 0) {  // host-only analysis mode: no device work
+    h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    return;
+  }
+
+  // ---- upload ----
+  cudaStream_t s = h->stream;
+  h->d_sn.upload(sd, s);
+  h->d_sub.upload(h->h_sub, s);
+  h->d_rows.upload(rows_all, s);
+  h->d_rel.upload(rel_all, s);
+  h->d_children.upload(children_all, s);
+  h->d_work.upload(work, s);
+  h->d_level_sn.upload(P.level_sn, s);
+  h->d_perm.upload(perm_all, s);
+  h->d_uoff.upload(h->u_off, s);
+  h->d_prim_dof.upload(prim_dof, s);
+  h->d_prim_gid.upload(prim_gid, s);
+  h->sc_front_dst.upload(fdst, s);
+  h->sc_front_src.upload(fsrc, s);
+  h->sc_x0_dst.upload(xdst, s);
+  h->sc_x0_src.upload(xsrc, s);
+  h->sc_kpp_dst.upload(kdst, s);
+  h->sc_kpp_src.upload(ksrc, s);
+  h->sc_fx_dst.upload(fxdst, s);
+  h->sc_fx_src.upload(fxsrc, s);
+  h->sc_fp_dst.upload(fpdst, s);
+  h->sc_fp_src.upload(fpsrc, s);
+  h->kdiag_src.upload(kdiag, s);
+  h->slot_lam.upload(slot_lam, s);
+  h->slot_sub.upload(slot_sub, s);
+  h->slot_sign.upload(slot_sign, s);
+  {
+    std::vector<long long> goff(h->n_slots);
+    std::vector<int> np(h->n_slots), poff(h->n_slots);
+    for (int k = 0; k < ns; ++k) {
+      const SubDev& d = h->h_sub[k];
+      for (int a = 0; a < d.nI; ++a) {
+        goff[d.rI_off + a] = d.g_off + (long long)a * d.nP;
+        np[d.rI_off + a] = d.nP;
+        poff[d.rI_off + a] = d.prim_off;
+      }
+    }
+    h->slot_goff.upload(goff, s);
+    h->slot_np.upload(np, s);
+    h->slot_poff.upload(poff, s);
+  }
+  h->lam.upload(lam, s);
+  h->scoef_ptr.upload(scoef_ptr, s);
+  h->scoef_src.upload(scoef_src, s);
+  h->pcon_ptr.upload(pcon_ptr, s);
+  h->pcon_src.upload(pcon_src, s);
+  // raw values
+  std::vector<double> kvals(kv), fvals(fv);
+  for (int k = 0; k < ns; ++k) {
+    std::copy(h->in[k].val.begin(), h->in[k].val.end(), kvals.begin() + h->kval_off[k]);
+    std::copy(h->in[k].f.begin(), h->in[k].f.end(), fvals.begin() + h->fval_off[k]);
+  }
+  h->kval.upload(kvals, s);
+  h->fval.upload(fvals, s);
+  // numeric buffers
+  const int nc = nrhs;
+  h->pool.alloc(P.pool_doubles);
+  h->dinv.alloc(P.dinv_doubles);
+  h->vecw.alloc((size_t)P.vec_doubles * std::max(P.ncx, 1));
+  h->X0.alloc((size_t)xo * P.ncx);
+  h->X.alloc((size_t)xo * P.ncx);
+  h->Xr.alloc((size_t)xo * nc);
+  h->kpp.alloc(kppo);
+  h->jp.alloc((size_t)po * nc);
+  h->G.alloc(go);
+  h->sloc.alloc(slo);
+  h->floc.alloc((size_t)po * nc);
+  h->S.alloc((size_t)ng * ng);
+  h->Sinv.alloc((size_t)ng * ng);
+  h->ftil.alloc((size_t)ng * nc);
+  h->zc0.alloc((size_t)ng * nc);
+  h->err_flag.alloc(4);
+  h->tiles.alloc(to);
+  h->dtiles.alloc(dto);
+  h->delta.alloc(h->n_slots);
+  h->kdiag.alloc(h->n_slots);
+  const size_t m = (size_t)h->n_lambda * nc;
+  h->d_vec.alloc(m);
+  h->lam_vec.alloc(m);
+  h->r_vec.alloc(m);
+  h->p_vec.alloc(m);
+  h->q_vec.alloc(m);
+  h->z_vec.alloc(m);
+  h->e_vec.alloc(m);
+  h->xI.alloc((size_t)h->n_slots * nc);
+  h->zI.alloc((size_t)h->n_slots * nc);
+  h->gk.alloc((size_t)po * nc);
+  h->zc.alloc((size_t)ng * nc);
+  h->partial.alloc(4 * 1024 * (size_t)nc);
+  h->state.alloc(16 * IETIDP_MAX_RHS + 64);
+  h->tmp_in.alloc(m);
+  h->tmp_out.alloc(m);
+  h->U.alloc(uo);
+  IETI_CUDA(cudaStreamSynchronize(s));
+  auto t2 = std::chrono::steady_clock::now();
+
+  h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t2 - t0).count();
+  (void)t1;
+}
+
+}  // namespace ieti

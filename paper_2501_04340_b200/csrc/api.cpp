@@ -1,0 +1,389 @@
+// C-ABI entry points of libietidp.so (include/ietidp.h). Argument checking,
+// call-order state machine, error translation; the work is in analyze.cpp and
+// the CUDA translation units.
+#include <chrono>
+#include <climits>
+#include <cstring>
+#include <new>
+
+#include "handle.h"
+
+namespace ieti {
+void analyze_all(ietidp_s* h);
+void finish_solve(ietidp_s* h, ietidp_report* rep);
+void destroy_graph(ietidp_s* h);
+}  // namespace ieti
+
+using ieti::Error;
+
+namespace {
+
+template <class F>
+ietidp_status guard(ietidp_t h, F&& f) {
+  if (!h) return IETIDP_E_ARG;
+  try {
+    f();
+    h->err.clear();
+    return IETIDP_OK;
+  } catch (const Error& e) {
+    h->err = e.what();
+    return e.st;
+  } catch (const std::bad_alloc&) {
+    h->err = "host allocation failed";
+    return IETIDP_E_NOMEM;
+  } catch (const std::exception& e) {
+    h->err = e.what();
+    return IETIDP_E_CUDA;
+  }
+}
+
+void require(bool c, ietidp_status st, const char* msg) {
+  if (!c) throw Error(st, msg);
+}
+
+struct EvPair {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EvPair() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~EvPair() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  float ms() {
+    float t = 0.f;
+    cudaEventElapsedTime(&t, a, b);
+    return t;
+  }
+};
+
+void set_device(ietidp_t h) {
+  if (h->opt.device < 0) throw Error(IETIDP_E_STATE, "handle created in host-only analysis mode (device < 0)");
+  IETI_CUDA(cudaSetDevice(h->opt.device));
+}
+
+}  // namespace
+
+extern "C" {
+
+void ietidp_options_default(ietidp_options* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->tol = 1e-10;
+  o->max_iter = 500;
+  o->scaling = IETIDP_SCALE_MULTIPLICITY;
+  o->fixed_iters = 0;
+  o->ordering = IETIDP_ORDER_NESTED_DISSECTION;
+  o->leaf_size = 96;
+  o->device = 0;
+  o->stream = nullptr;
+}
+
+const char* ietidp_status_string(ietidp_status s) {
+  switch (s) {
+    case IETIDP_OK: return "IETIDP_OK";
+    case IETIDP_E_ARG: return "IETIDP_E_ARG";
+    case IETIDP_E_STATE: return "IETIDP_E_STATE";
+    case IETIDP_E_B_STRUCTURE: return "IETIDP_E_B_STRUCTURE";
+    case IETIDP_E_NOT_SPD: return "IETIDP_E_NOT_SPD";
+    case IETIDP_E_NO_CONVERGENCE: return "IETIDP_E_NO_CONVERGENCE";
+    case IETIDP_E_CUDA: return "IETIDP_E_CUDA";
+    case IETIDP_E_NOMEM: return "IETIDP_E_NOMEM";
+  }
+  return "unknown";
+}
+
+ietidp_status ietidp_create(const ietidp_options* opt, int n_sub, int n_lambda, int n_primal, int nrhs, ietidp_t* out) {
+  if (!out) return IETIDP_E_ARG;
+  *out = nullptr;
+  if (n_sub < 1 || n_lambda < 0 || n_primal < 0 || nrhs < 1 || nrhs > IETIDP_MAX_RHS) return IETIDP_E_ARG;
+  ietidp_s* h = new (std::nothrow) ietidp_s();
+  if (!h) return IETIDP_E_NOMEM;
+  if (opt) h->opt = *opt;
+  else ietidp_options_default(&h->opt);
+  if (h->opt.leaf_size <= 0) h->opt.leaf_size = 96;
+  h->n_sub = n_sub;
+  h->n_lambda = n_lambda;
+  h->n_primal = n_primal;
+  h->nrhs = nrhs;
+  h->in.resize(n_sub);
+  h->rep.failed_subdomain = -1;
+  *out = h;
+  return guard(h, [&]() {
+    require(h->opt.tol >= 0.0 && h->opt.max_iter >= 0 && h->opt.fixed_iters >= 0, IETIDP_E_ARG, "bad options");
+    require(h->opt.scaling == IETIDP_SCALE_MULTIPLICITY || h->opt.scaling == IETIDP_SCALE_STIFFNESS, IETIDP_E_ARG,
+            "bad scaling");
+    if (h->opt.device < 0) return;  // host-only analysis mode (tests without a GPU)
+    set_device(h);
+    if (h->opt.stream) {
+      h->stream = (cudaStream_t)h->opt.stream;
+    } else {
+      IETI_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
+      h->own_stream = true;
+    }
+  });
+}
+
+ietidp_status ietidp_set_subdomain(ietidp_t h, int k, int n_k, const int64_t* K_rowptr, const int32_t* K_col,
+                                   const double* K_val, const double* f, int nB, const int32_t* B_lambda,
+                                   const int32_t* B_dof, const int8_t* B_sign, int n_tree, const int32_t* tree_dofs,
+                                   int n_prim, const int32_t* prim_dofs, const int32_t* prim_global) {
+  return guard(h, [&]() {
+    require(!h->analyzed, IETIDP_E_STATE, "set_subdomain after analysis");
+    require(k >= 0 && k < h->n_sub, IETIDP_E_ARG, "subdomain index out of range");
+    require(!h->in[k].set, IETIDP_E_STATE, "subdomain set twice");
+    require(n_k >= 0 && nB >= 0 && n_tree >= 0 && n_prim >= 0, IETIDP_E_ARG, "negative size");
+    require(K_rowptr && (n_k == 0 || (K_col && K_val && f)), IETIDP_E_ARG, "null pointer");
+    require(nB == 0 || (B_lambda && B_dof && B_sign), IETIDP_E_ARG, "null B pointer");
+    require(n_tree == 0 || tree_dofs, IETIDP_E_ARG, "null tree pointer");
+    require(n_prim == 0 || (prim_dofs && prim_global), IETIDP_E_ARG, "null primal pointer");
+    ieti::SubIn& in = h->in[k];
+    in.n = n_k;
+    require(K_rowptr[0] == 0, IETIDP_E_ARG, "rowptr[0] != 0");
+    const int64_t nnz = K_rowptr[n_k];
+    require(nnz >= 0 && nnz < (int64_t)INT_MAX, IETIDP_E_ARG, "bad nnz");
+    in.rowptr.assign(K_rowptr, K_rowptr + n_k + 1);
+    in.col.assign(K_col, K_col + nnz);
+    in.val.assign(K_val, K_val + nnz);
+    in.f.assign(f, f + (size_t)n_k * h->nrhs);
+    for (int i = 0; i < n_k; ++i) {
+      require(in.rowptr[i + 1] >= in.rowptr[i], IETIDP_E_ARG, "rowptr not monotone");
+      for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) {
+        require(in.col[e] >= 0 && in.col[e] < n_k, IETIDP_E_ARG, "column index out of range");
+        require(e == in.rowptr[i] || in.col[e] > in.col[e - 1], IETIDP_E_ARG, "CSR columns not sorted/unique");
+      }
+    }
+    // pattern symmetry
+    for (int i = 0; i < n_k; ++i)
+      for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) {
+        const int j = in.col[e];
+        const int32_t* b = in.col.data() + in.rowptr[j];
+        const int32_t* en = in.col.data() + in.rowptr[j + 1];
+        const int32_t* it = std::lower_bound(b, en, i);
+        require(it != en && *it == i, IETIDP_E_ARG, "CSR pattern not symmetric");
+      }
+    in.B_lambda.assign(B_lambda, B_lambda + nB);
+    in.B_dof.assign(B_dof, B_dof + nB);
+    in.B_sign.assign(B_sign, B_sign + nB);
+    for (int e = 0; e < nB; ++e) {
+      require(in.B_lambda[e] >= 0 && in.B_lambda[e] < h->n_lambda, IETIDP_E_ARG, "B multiplier out of range");
+      require(in.B_dof[e] >= 0 && in.B_dof[e] < n_k, IETIDP_E_ARG, "B DOF out of range");
+      if (in.B_sign[e] != 1 && in.B_sign[e] != -1) throw Error(IETIDP_E_B_STRUCTURE, "B sign not +1/-1");
+    }
+    in.tree.assign(tree_dofs, tree_dofs + n_tree);
+    for (int t : in.tree) require(t >= 0 && t < n_k, IETIDP_E_ARG, "tree DOF out of range");
+    in.prim.assign(prim_dofs, prim_dofs + n_prim);
+    in.prim_gid.assign(prim_global, prim_global + n_prim);
+    for (int q = 0; q < n_prim; ++q) {
+      require(in.prim[q] >= 0 && in.prim[q] < n_k, IETIDP_E_ARG, "primal DOF out of range");
+      require(in.prim_gid[q] >= 0 && in.prim_gid[q] < h->n_primal, IETIDP_E_ARG, "primal id out of range");
+    }
+    in.set = true;
+  });
+}
+
+ietidp_status ietidp_analyze(ietidp_t h) {
+  return guard(h, [&]() {
+    require(!h->analyzed, IETIDP_E_STATE, "already analyzed");
+    if (h->opt.device >= 0) set_device(h);
+    ieti::analyze_all(h);
+    h->analyzed = true;
+  });
+}
+
+ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const double* f) {
+  return guard(h, [&]() {
+    require(h->analyzed, IETIDP_E_STATE, "set_values before analysis");
+    require(k >= 0 && k < h->n_sub, IETIDP_E_ARG, "subdomain index out of range");
+    const ieti::SubIn& in = h->in[k];
+    if (K_val)
+      IETI_CUDA(cudaMemcpyAsync(h->kval.p + h->kval_off[k], K_val, in.val.size() * sizeof(double),
+                                cudaMemcpyHostToDevice, h->stream));
+    if (f)
+      IETI_CUDA(cudaMemcpyAsync(h->fval.p + h->fval_off[k], f, (size_t)in.n * h->nrhs * sizeof(double),
+                                cudaMemcpyHostToDevice, h->stream));
+    h->factored = false;
+    h->solved = false;
+  });
+}
+
+ietidp_status ietidp_factor(ietidp_t h) {
+  if (h && !h->analyzed) {
+    ietidp_status st = ietidp_analyze(h);
+    if (st != IETIDP_OK) return st;
+  }
+  return guard(h, [&]() {
+    set_device(h);
+    h->factored = false;
+    h->solved = false;
+    h->factor_failed = true;
+    EvPair e1, e2;
+    IETI_CUDA(cudaEventRecord(e1.a, h->stream));
+    ieti::run_factor(h);
+    IETI_CUDA(cudaEventRecord(e1.b, h->stream));
+    IETI_CUDA(cudaEventRecord(e2.a, h->stream));
+    ieti::run_coarse(h);
+    IETI_CUDA(cudaEventRecord(e2.b, h->stream));
+    int flags[2];
+    IETI_CUDA(cudaMemcpyAsync(flags, h->err_flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
+    IETI_CUDA(cudaStreamSynchronize(h->stream));
+    h->rep.ms_factor = e1.ms();
+    h->rep.ms_coarse = e2.ms();
+    if (flags[0] != INT_MAX) {
+      h->failed_sub = flags[0];
+      h->rep.failed_subdomain = flags[0];
+      throw Error(IETIDP_E_NOT_SPD, "K_rr of subdomain " + std::to_string(flags[0]) + " is not SPD");
+    }
+    if (flags[1] == 0) {
+      h->failed_sub = -1;
+      h->rep.failed_subdomain = -1;
+      throw Error(IETIDP_E_NOT_SPD, "coarse matrix S_PP is not SPD");
+    }
+    h->rep.failed_subdomain = -1;
+    h->factor_failed = false;
+    h->factored = true;
+  });
+}
+
+ietidp_status ietidp_solve(ietidp_t h, double* lambda, ietidp_report* report) {
+  bool noconv = false;
+  ietidp_status st = guard(h, [&]() {
+    require(h->factored, IETIDP_E_STATE, "solve before a successful factor");
+    set_device(h);
+    EvPair e1, e2;
+    IETI_CUDA(cudaEventRecord(e1.a, h->stream));
+    ieti::run_solve(h);
+    IETI_CUDA(cudaEventRecord(e1.b, h->stream));
+    IETI_CUDA(cudaEventRecord(e2.a, h->stream));
+    ieti::run_recover(h);
+    IETI_CUDA(cudaEventRecord(e2.b, h->stream));
+    ieti::finish_solve(h, &h->rep);
+    h->rep.ms_pcg = e1.ms();
+    h->rep.ms_recover = e2.ms();
+    if (lambda && h->n_lambda) {
+      ieti::transpose_out(h, h->n_lambda, h->nrhs, h->lam_vec.p, h->tmp_out.p);
+      IETI_CUDA(cudaMemcpyAsync(lambda, h->tmp_out.p, (size_t)h->n_lambda * h->nrhs * sizeof(double),
+                                cudaMemcpyDeviceToHost, h->stream));
+      IETI_CUDA(cudaStreamSynchronize(h->stream));
+    }
+    h->solved = true;
+    if (!h->opt.fixed_iters)
+      for (int c = 0; c < h->nrhs; ++c)
+        if (!h->rep.converged[c]) noconv = true;
+  });
+  if (h) {
+    h->rep.n_sub = h->n_sub;
+    h->rep.n_lambda = h->n_lambda;
+    h->rep.n_primal = h->n_primal;
+    h->rep.nrhs = h->nrhs;
+    if (report) *report = h->rep;
+  }
+  if (st == IETIDP_OK && noconv) {
+    h->err = "PCG reached max_iter without convergence";
+    return IETIDP_E_NO_CONVERGENCE;
+  }
+  return st;
+}
+
+ietidp_status ietidp_get_u(ietidp_t h, int k, double* u) {
+  return guard(h, [&]() {
+    require(h->solved, IETIDP_E_STATE, "no solution yet");
+    require(k >= 0 && k < h->n_sub && u, IETIDP_E_ARG, "bad argument");
+    IETI_CUDA(cudaMemcpyAsync(u, h->U.p + h->u_off[k], (size_t)h->in[k].n * h->nrhs * sizeof(double),
+                              cudaMemcpyDeviceToHost, h->stream));
+    IETI_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+ietidp_status ietidp_get_u_device(ietidp_t h, int k, double* d_u) {
+  return guard(h, [&]() {
+    require(h->solved, IETIDP_E_STATE, "no solution yet");
+    require(k >= 0 && k < h->n_sub && d_u, IETIDP_E_ARG, "bad argument");
+    IETI_CUDA(cudaMemcpyAsync(d_u, h->U.p + h->u_off[k], (size_t)h->in[k].n * h->nrhs * sizeof(double),
+                              cudaMemcpyDeviceToDevice, h->stream));
+  });
+}
+
+ietidp_status ietidp_get_lambda_device(ietidp_t h, double* d_lambda) {
+  return guard(h, [&]() {
+    require(h->solved, IETIDP_E_STATE, "no solution yet");
+    require(d_lambda || h->n_lambda == 0, IETIDP_E_ARG, "null pointer");
+    if (h->n_lambda) ieti::transpose_out(h, h->n_lambda, h->nrhs, h->lam_vec.p, d_lambda);
+  });
+}
+
+static ietidp_status apply_op(ietidp_t h, int ncols, const double* d_x, double* d_y, bool F) {
+  return guard(h, [&]() {
+    require(h->factored, IETIDP_E_STATE, "operator before a successful factor");
+    require(ncols >= 1 && ncols <= h->nrhs, IETIDP_E_ARG, "ncols out of range");
+    require(h->n_lambda == 0 || (d_x && d_y), IETIDP_E_ARG, "null pointer");
+    if (h->n_lambda == 0) return;
+    set_device(h);
+    const double* xin = d_x;
+    double* yout = d_y;
+    if (ncols > 1) {
+      ieti::transpose_in(h, h->n_lambda, ncols, d_x, h->tmp_in.p);
+      xin = h->tmp_in.p;
+      yout = h->tmp_out.p;
+    }
+    if (F) ieti::run_apply_F(h, ncols, xin, yout);
+    else ieti::run_apply_M(h, ncols, xin, yout);
+    if (ncols > 1) ieti::transpose_out(h, h->n_lambda, ncols, h->tmp_out.p, d_y);
+  });
+}
+
+ietidp_status ietidp_apply_F(ietidp_t h, int ncols, const double* d_x, double* d_y) {
+  return apply_op(h, ncols, d_x, d_y, true);
+}
+ietidp_status ietidp_apply_precond(ietidp_t h, int ncols, const double* d_x, double* d_y) {
+  return apply_op(h, ncols, d_x, d_y, false);
+}
+
+ietidp_status ietidp_get_coarse(ietidp_t h, double* S) {
+  return guard(h, [&]() {
+    require(h->factored, IETIDP_E_STATE, "coarse matrix before factor");
+    require(S || h->n_primal == 0, IETIDP_E_ARG, "null pointer");
+    if (!h->n_primal) return;
+    IETI_CUDA(cudaMemcpyAsync(S, h->S.p, (size_t)h->n_primal * h->n_primal * sizeof(double), cudaMemcpyDeviceToHost,
+                              h->stream));
+    IETI_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+ietidp_status ietidp_get_rhs(ietidp_t h, double* d) {
+  return guard(h, [&]() {
+    require(h->factored, IETIDP_E_STATE, "rhs before factor");
+    require(d || h->n_lambda == 0, IETIDP_E_ARG, "null pointer");
+    if (!h->n_lambda) return;
+    ieti::transpose_out(h, h->n_lambda, h->nrhs, h->d_vec.p, h->tmp_out.p);
+    IETI_CUDA(cudaMemcpyAsync(d, h->tmp_out.p, (size_t)h->n_lambda * h->nrhs * sizeof(double),
+                              cudaMemcpyDeviceToHost, h->stream));
+    IETI_CUDA(cudaStreamSynchronize(h->stream));
+  });
+}
+
+ietidp_status ietidp_get_report(ietidp_t h, ietidp_report* r) {
+  if (!h || !r) return IETIDP_E_ARG;
+  h->rep.n_sub = h->n_sub;
+  h->rep.n_lambda = h->n_lambda;
+  h->rep.n_primal = h->n_primal;
+  h->rep.nrhs = h->nrhs;
+  *r = h->rep;
+  return IETIDP_OK;
+}
+
+long long ietidp_kernel_launches(ietidp_t h) { return h ? h->launches : 0; }
+
+const char* ietidp_last_error(ietidp_t h) { return h ? h->err.c_str() : "null handle"; }
+
+void ietidp_destroy(ietidp_t h) {
+  if (!h) return;
+  if (h->opt.device >= 0) cudaSetDevice(h->opt.device);
+  if (h->stream) cudaStreamSynchronize(h->stream);
+  ieti::destroy_graph(h);
+  if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
+  delete h;
+}
+
+}  // extern "C"

@@ -1,0 +1,134 @@
+// The opaque handle behind ietidp_t and the device-buffer helper.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "impl.h"
+
+namespace ieti {
+
+struct Error : std::runtime_error {
+  ietidp_status st;
+  Error(ietidp_status s, const std::string& m) : std::runtime_error(m), st(s) {}
+};
+
+#define IETI_CUDA(call)                                                              \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess)                                                           \
+      throw ::ieti::Error(e_ == cudaErrorMemoryAllocation ? IETIDP_E_NOMEM : IETIDP_E_CUDA, \
+                          std::string(#call) + ": " + cudaGetErrorString(e_));       \
+  } while (0)
+
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  ~DevBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    if (count) IETI_CUDA(cudaMalloc(&p, count * sizeof(T)));
+  }
+  void zero(cudaStream_t s) {
+    if (n) IETI_CUDA(cudaMemsetAsync(p, 0, n * sizeof(T), s));
+  }
+  void upload(const std::vector<T>& v, cudaStream_t s) {
+    alloc(v.size());
+    if (n) IETI_CUDA(cudaMemcpyAsync(p, v.data(), n * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+};
+
+}  // namespace ieti
+
+struct ietidp_s {
+  ietidp_options opt{};
+  int n_sub = 0, n_lambda = 0, n_primal = 0, nrhs = 1;
+  std::vector<ieti::SubIn> in;
+  std::string err;
+  bool analyzed = false, factored = false, solved = false, factor_failed = false;
+  int failed_sub = -1;
+  ieti::Plan plan;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  long long launches = 0;
+  ietidp_report rep{};
+
+  // ---- raw values (uploaded once, refreshed by ietidp_set_values) ----
+  ieti::DevBuf<double> kval, fval;
+  std::vector<long long> kval_off, fval_off;
+  // ---- scatter lists: dst offset <- src index ----
+  ieti::DevBuf<long long> sc_front_dst;   // K_rr lower -> fronts pool (sorted by level)
+  ieti::DevBuf<int> sc_front_src;
+  ieti::DevBuf<long long> sc_x0_dst;      // K_rP -> X0 (row-major nr x ncx)
+  ieti::DevBuf<int> sc_x0_src;
+  ieti::DevBuf<long long> sc_kpp_dst;     // K_PP -> kpp
+  ieti::DevBuf<int> sc_kpp_src;
+  ieti::DevBuf<long long> sc_fx_dst;      // f -> X0 (j_r columns)
+  ieti::DevBuf<int> sc_fx_src;
+  ieti::DevBuf<long long> sc_fp_dst;      // f -> jp
+  ieti::DevBuf<int> sc_fp_src;
+  ieti::DevBuf<int> kdiag_src;            // K value index of the diagonal at each r_I slot
+  // ---- symbolic structures ----
+  ieti::DevBuf<ieti::SnDev> d_sn;
+  ieti::DevBuf<ieti::SubDev> d_sub;
+  std::vector<ieti::SubDev> h_sub;
+  ieti::DevBuf<int> d_rows, d_rel, d_children, d_work, d_level_sn;
+  ieti::DevBuf<int> d_perm;               // r position -> local DOF (per subdomain)
+  ieti::DevBuf<int> d_prim_dof, d_prim_gid;
+  // ---- numeric ----
+  ieti::DevBuf<double> pool, dinv, vecw;  // fronts, inverted diagonal blocks, sweep workspace
+  ieti::DevBuf<double> X0, X, Xr;         // sweep RHS/solutions (coarse set-up, recovery)
+  ieti::DevBuf<double> kpp, jp, G, sloc, floc;
+  ieti::DevBuf<double> S, Sinv, ftil, zc0;  // coarse: S_PP, S_PP^-1, ftilde, S^-1 ftilde
+  ieti::DevBuf<int> scoef_ptr, scoef_src; // S_PP entry <- sloc entries
+  ieti::DevBuf<int> pcon_ptr, pcon_src;   // global primal <- primal rows
+  ieti::DevBuf<int> err_flag;             // min failing subdomain (INT_MAX: none)
+  // ---- loop ----
+  ieti::DevBuf<double> tiles, dtiles;     // packed L_II tiles and Dinv_II tiles
+  ieti::DevBuf<ieti::LamDev> lam;
+  ieti::DevBuf<int> slot_lam, slot_sub;   // per r_I slot: multiplier, subdomain
+  ieti::DevBuf<float> slot_sign;
+  ieti::DevBuf<long long> slot_goff;      // per r_I slot: its row of G_k in the G pool
+  ieti::DevBuf<int> slot_np, slot_poff;   // per r_I slot: n_P of its subdomain, primal-row offset
+  ieti::DevBuf<double> delta, kdiag;      // scaling weights per slot, K diagonal per slot
+  ieti::DevBuf<double> d_vec, lam_vec, r_vec, p_vec, q_vec, z_vec, xI, zI, gk, zc, e_vec;
+  ieti::DevBuf<double> partial;           // per-block dot partials
+  ieti::DevBuf<double> state;             // PCG scalars (see pcg.cu)
+  ieti::DevBuf<double> tmp_in, tmp_out;   // col-major <-> interleaved staging
+  ieti::DevBuf<double> U;                 // subdomain solutions u^(k), n_k x nrhs col-major
+  std::vector<long long> u_off;
+  ieti::DevBuf<long long> d_uoff;
+  int n_slots = 0, sum_nP = 0;
+  // CUDA graph of one PCG iteration (while-conditional), built lazily
+  void* graph_exec = nullptr;
+  void* graph = nullptr;
+  int graph_ncols = 0;
+  unsigned long long cond_handle = 0;
+  ieti::DevBuf<ieti::Work> dummy_;
+};
+
+// Device-side entry points implemented in the .cu files (host launchers).
+namespace ieti {
+void upload_plan(ietidp_s* h);                 // analyze.cpp -> device buffers
+void run_factor(ietidp_s* h);                  // factor.cu
+void run_coarse(ietidp_s* h);                  // coarse.cu
+void run_solve(ietidp_s* h);                   // pcg.cu
+void run_apply_F(ietidp_s* h, int ncols, const double* x, double* y);
+void run_apply_M(ietidp_s* h, int ncols, const double* x, double* y);
+void run_recover(ietidp_s* h);                 // coarse.cu
+void transpose_in(ietidp_s* h, int rows, int ncols, const double* colmajor, double* inter);
+void transpose_out(ietidp_s* h, int rows, int ncols, const double* inter, double* colmajor);
+}  // namespace ieti

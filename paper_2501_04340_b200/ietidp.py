@@ -1,0 +1,240 @@
+"""Thin ctypes binding of libietidp.so (include/ietidp.h): argument marshalling
+only — every numeric step runs in the library's CUDA kernels. There is no CPU
+fallback: if the library is missing or no CUDA device is present the calls
+fail loudly.
+"""
+import ctypes as C
+import os
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libietidp.so")
+
+MAX_RHS = 64
+STATUS = {0: "IETIDP_OK", 1: "IETIDP_E_ARG", 2: "IETIDP_E_STATE", 3: "IETIDP_E_B_STRUCTURE",
+          4: "IETIDP_E_NOT_SPD", 5: "IETIDP_E_NO_CONVERGENCE", 6: "IETIDP_E_CUDA", 7: "IETIDP_E_NOMEM"}
+OK, E_ARG, E_STATE, E_B_STRUCTURE, E_NOT_SPD, E_NO_CONVERGENCE, E_CUDA, E_NOMEM = range(8)
+SCALING = {"multiplicity": 0, "stiffness": 1}
+ORDERING = {"nd": 0, "dense": 1}
+
+# every entry point include/ietidp.h declares
+SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "ietidp_analyze",
+           "ietidp_set_values", "ietidp_factor", "ietidp_solve", "ietidp_get_u", "ietidp_get_u_device",
+           "ietidp_get_lambda_device", "ietidp_apply_F", "ietidp_apply_precond", "ietidp_get_coarse",
+           "ietidp_get_rhs", "ietidp_get_report", "ietidp_kernel_launches", "ietidp_last_error",
+           "ietidp_status_string", "ietidp_destroy"]
+
+
+class Options(C.Structure):
+    _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("scaling", C.c_int), ("fixed_iters", C.c_int),
+                ("ordering", C.c_int), ("leaf_size", C.c_int), ("device", C.c_int), ("stream", C.c_void_p)]
+
+
+class Report(C.Structure):
+    _fields_ = [("n_sub", C.c_int), ("n_lambda", C.c_int), ("n_primal", C.c_int), ("nrhs", C.c_int),
+                ("failed_subdomain", C.c_int), ("n_supernodes", C.c_int), ("n_levels", C.c_int),
+                ("max_front", C.c_int), ("max_nI", C.c_int),
+                ("sum_nr", C.c_longlong), ("sum_nI", C.c_longlong), ("nnz_L", C.c_longlong),
+                ("factor_flops", C.c_longlong), ("pcg_bytes_per_iter", C.c_longlong),
+                ("f_apply_bytes", C.c_longlong),
+                ("iters", C.c_int * MAX_RHS), ("converged", C.c_int * MAX_RHS),
+                ("rel_residual", C.c_double * MAX_RHS),
+                ("ms_analyze", C.c_double), ("ms_factor", C.c_double), ("ms_coarse", C.c_double),
+                ("ms_pcg", C.c_double), ("ms_recover", C.c_double)]
+
+    def to_dict(self):
+        n = self.nrhs
+        d = {k: getattr(self, k) for k, _ in self._fields_ if k not in ("iters", "converged", "rel_residual")}
+        d["iters"] = list(self.iters[:n])
+        d["converged"] = list(self.converged[:n])
+        d["rel_residual"] = list(self.rel_residual[:n])
+        return d
+
+
+_lib = None
+
+
+def load():
+    """Load libietidp.so (raises if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} not built: run `python -m paper_2501_04340_b200.build`")
+    lib = C.CDLL(LIB_PATH)
+    P, I, D, LL = C.c_void_p, C.c_int, C.c_double, C.c_longlong
+    sig = {
+        "ietidp_options_default": (None, [C.POINTER(Options)]),
+        "ietidp_create": (I, [C.POINTER(Options), I, I, I, I, C.POINTER(P)]),
+        "ietidp_set_subdomain": (I, [P, I, I, P, P, P, P, I, P, P, P, I, P, I, P, P]),
+        "ietidp_analyze": (I, [P]),
+        "ietidp_set_values": (I, [P, I, P, P]),
+        "ietidp_factor": (I, [P]),
+        "ietidp_solve": (I, [P, P, C.POINTER(Report)]),
+        "ietidp_get_u": (I, [P, I, P]),
+        "ietidp_get_u_device": (I, [P, I, P]),
+        "ietidp_get_lambda_device": (I, [P, P]),
+        "ietidp_apply_F": (I, [P, I, P, P]),
+        "ietidp_apply_precond": (I, [P, I, P, P]),
+        "ietidp_get_coarse": (I, [P, P]),
+        "ietidp_get_rhs": (I, [P, P]),
+        "ietidp_get_report": (I, [P, C.POINTER(Report)]),
+        "ietidp_kernel_launches": (LL, [P]),
+        "ietidp_last_error": (C.c_char_p, [P]),
+        "ietidp_status_string": (C.c_char_p, [I]),
+        "ietidp_destroy": (None, [P]),
+    }
+    for name, (res, args) in sig.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+class IetiError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"{STATUS.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _ptr(a):
+    return a.ctypes.data_as(C.c_void_p) if a is not None and a.size else None
+
+
+class Solver:
+    """One IETI-DP handle (include/ietidp.h). Host numpy arrays in, host arrays out;
+    the *_device methods take torch CUDA tensors (plumbing only)."""
+
+    def __init__(self, n_sub, n_lambda, n_primal, nrhs=1, tol=1e-10, max_iter=500, scaling="multiplicity",
+                 fixed_iters=0, ordering="nd", leaf_size=96, device=0, stream=None):
+        lib = load()
+        self.lib = lib
+        o = Options()
+        lib.ietidp_options_default(C.byref(o))
+        o.tol, o.max_iter, o.scaling, o.fixed_iters = tol, max_iter, SCALING[scaling], fixed_iters
+        o.ordering, o.leaf_size, o.device = ORDERING[ordering], leaf_size, device
+        o.stream = stream
+        h = C.c_void_p()
+        st = lib.ietidp_create(C.byref(o), n_sub, n_lambda, n_primal, nrhs, C.byref(h))
+        self.h = h
+        self.n_sub, self.n_lambda, self.n_primal, self.nrhs = n_sub, n_lambda, n_primal, nrhs
+        self._n = [0] * n_sub
+        self._keep = []
+        self._check(st)
+
+    def _check(self, st, allow=()):
+        if st != OK and st not in allow:
+            msg = self.lib.ietidp_last_error(self.h).decode() if self.h else ""
+            raise IetiError(st, msg)
+        return st
+
+    def set_subdomain(self, k, K_indptr, K_indices, K_data, f, B_lambda, B_dof, B_sign, tree, prim, prim_gid):
+        a = dict(ip=np.ascontiguousarray(K_indptr, np.int64), ix=np.ascontiguousarray(K_indices, np.int32),
+                 v=np.ascontiguousarray(K_data, np.float64), f=np.ascontiguousarray(f, np.float64),
+                 bl=np.ascontiguousarray(B_lambda, np.int32), bd=np.ascontiguousarray(B_dof, np.int32),
+                 bs=np.ascontiguousarray(B_sign, np.int8), tr=np.ascontiguousarray(tree, np.int32),
+                 pr=np.ascontiguousarray(prim, np.int32), pg=np.ascontiguousarray(prim_gid, np.int32))
+        n = len(a["ip"]) - 1
+        self._n[k] = n
+        st = self.lib.ietidp_set_subdomain(self.h, k, n, _ptr(a["ip"]), _ptr(a["ix"]), _ptr(a["v"]), _ptr(a["f"]),
+                                           len(a["bl"]), _ptr(a["bl"]), _ptr(a["bd"]), _ptr(a["bs"]),
+                                           len(a["tr"]), _ptr(a["tr"]), len(a["pr"]), _ptr(a["pr"]), _ptr(a["pg"]))
+        self._check(st)
+
+    def analyze(self):
+        self._check(self.lib.ietidp_analyze(self.h))
+
+    def set_values(self, k, K_data=None, f=None):
+        v = None if K_data is None else np.ascontiguousarray(K_data, np.float64)
+        ff = None if f is None else np.ascontiguousarray(f, np.float64)
+        self._check(self.lib.ietidp_set_values(self.h, k, _ptr(v), _ptr(ff)))
+
+    def factor(self):
+        self._check(self.lib.ietidp_factor(self.h))
+
+    def solve(self, want_lambda=True, allow_noconv=False):
+        lam = np.zeros((self.nrhs, self.n_lambda)) if want_lambda else None
+        rep = Report()
+        st = self.lib.ietidp_solve(self.h, _ptr(lam), C.byref(rep))
+        self._check(st, allow=(E_NO_CONVERGENCE,) if allow_noconv else ())
+        return (lam.T.copy() if want_lambda else None), rep.to_dict()
+
+    def get_u(self, k):
+        u = np.zeros((self.nrhs, self._n[k]))
+        self._check(self.lib.ietidp_get_u(self.h, k, _ptr(u)))
+        return u.T.copy()
+
+    def get_coarse(self):
+        S = np.zeros((self.n_primal, self.n_primal))
+        self._check(self.lib.ietidp_get_coarse(self.h, _ptr(S)))
+        return S
+
+    def get_rhs(self):
+        d = np.zeros((self.nrhs, self.n_lambda))
+        self._check(self.lib.ietidp_get_rhs(self.h, _ptr(d)))
+        return d.T.copy()
+
+    def report(self):
+        rep = Report()
+        self._check(self.lib.ietidp_get_report(self.h, C.byref(rep)))
+        return rep.to_dict()
+
+    def kernel_launches(self):
+        return int(self.lib.ietidp_kernel_launches(self.h))
+
+    # --- device operator access (torch CUDA tensors, n_lambda x ncols column-major) ---
+    def apply_F_device(self, x, y, ncols):
+        self._check(self.lib.ietidp_apply_F(self.h, ncols, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr())))
+
+    def apply_precond_device(self, x, y, ncols):
+        self._check(self.lib.ietidp_apply_precond(self.h, ncols, C.c_void_p(x.data_ptr()),
+                                                  C.c_void_p(y.data_ptr())))
+
+    def get_u_device(self, k, out):
+        self._check(self.lib.ietidp_get_u_device(self.h, k, C.c_void_p(out.data_ptr())))
+
+    def get_lambda_device(self, out):
+        self._check(self.lib.ietidp_get_lambda_device(self.h, C.c_void_p(out.data_ptr())))
+
+    def apply_F(self, X):
+        """Host convenience: y = F_DP X for X (n_lambda x ncols), via the device entry point."""
+        return self._host_op(X, self.apply_F_device)
+
+    def apply_precond(self, X):
+        return self._host_op(X, self.apply_precond_device)
+
+    def _host_op(self, X, fn):
+        import torch
+        X = np.asarray(X, np.float64)
+        if X.ndim == 1:
+            X = X[:, None]
+        ncols = X.shape[1]
+        xt = torch.from_numpy(np.ascontiguousarray(X.T)).cuda()
+        yt = torch.empty_like(xt)
+        fn(xt, yt, ncols)
+        torch.cuda.synchronize()
+        return yt.cpu().numpy().T.copy()
+
+    def close(self):
+        if self.h:
+            self.lib.ietidp_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def from_bundle(b, **opts):
+    """A Solver with every subdomain of a generator bundle (ietigen.bundle) set."""
+    opts.setdefault("scaling", b["scaling"])
+    opts.setdefault("tol", b["tol"])
+    s = Solver(b["n_sub"], b["n_lambda"], b["n_primal"], b["nrhs"], **opts)
+    for k, sd in enumerate(b["subs"]):
+        s.set_subdomain(k, sd["K_indptr"], sd["K_indices"], sd["K_data"], sd["f"], sd["B_lambda"], sd["B_dof"],
+                        sd["B_sign"], sd["tree"], sd["prim"], sd["prim_gid"])
+    return s
