@@ -1,0 +1,350 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 IETI-DP solve phase (BASELINE.json metric).
+
+A step = one pass of the whole hot path on one synthetic
+workload resident in HBM: batched multifrontal Cholesky of every K_rr^(k),
+coarse set-up (K_rr^-1 K_rP, S_PP, G) and d_DP, the PCG loop on F_DP lambda = d_DP,
+and the recovery of every u^(k). Host analysis (ordering/symbolic) and the
+one-time upload happen before the timed region.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2] [--impl reference]
+
+value = solves per second over all ranks (N independent replicas, weak
+scaling: the single-GPU design has no data-path exchange).
+"""
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "IETI-DP solve time, F-applies/s; % of FP64-TC peak (factor) and HBM (PCG)"
+L2_FLUSH_BYTES = 512 << 20  # > 126 MB L2
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="C2")
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--fapply-iters", type=int, default=200)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    return ap.parse_args()
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f)
+    except OSError:
+        return {"hbm_gbs": 6650.0, "_fallback": True}
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev = dev
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            time.sleep(0.25)
+            self.p.terminate()
+            out, _ = self.p.communicate(timeout=10)
+            self.rows = [r.split(", ") for r in out.strip().splitlines() if r.strip()]
+        else:
+            self.rows = []
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in self.rows:
+            try:
+                sm.append(float(r[1]))
+                mx = float(r[2])
+                for n, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(n)
+            except (ValueError, IndexError):
+                pass
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def dist_init(args):
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl" if args.impl == "ours" else "gloo")
+    return rank, world, local
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def max_over_ranks(x, world, device=None):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+# ---------------------------------------------------------------------------
+# CPU oracle (the reported baseline; the one place bench.py runs oracle/)
+# ---------------------------------------------------------------------------
+def oracle_sample(bundle, n_iter, subs):
+    """Time the oracle on a bounded sample: full local set-up (factorisation of
+    K_rr, explicit S_{r_I r_I}, coarse columns) of the subdomains `subs` plus
+    n_iter local F-apply and preconditioner contributions each; extrapolated to
+    all subdomains. Returns (seconds per full solve, threads)."""
+    from oracle import dp
+    import threadpoolctl
+    nl = int(bundle["n_lambda"])
+    rng = np.random.default_rng(0)
+    t0 = time.perf_counter()
+    for k in subs:
+        L = dp.Local(k, bundle["subs"][k], nl, False)
+        L.schur_II(False)
+        if len(L.prim):
+            L.Kinv(L.Krp.toarray())
+        L.Kinv(L.jr)
+        x = rng.standard_normal((nl, int(bundle["nrhs"])))
+        for _ in range(n_iter):
+            L.Br @ L.Kinv(L.Br.T @ x)
+    dt = time.perf_counter() - t0
+    threads = max((i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()), default=1)
+    return dt * len(bundle["subs"]) / len(subs), threads
+
+
+def run_reference(args, rank, world):
+    if rank != 0:
+        return
+    from ietigen.bundle import make_bundle
+    b = make_bundle(args.config)
+    n_iter = 30
+    times = []
+    threads = 1
+    nsub = b["n_sub"]
+    for s in range(args.warmup + args.steps):
+        k = s % nsub
+        t, threads = oracle_sample(b, n_iter, [k])
+        if s >= args.warmup:
+            times.append(t)
+    sec = statistics.mean(times)
+    val = 1.0 / sec
+    line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "solves/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": args.config, "n_sub": nsub, "n_lambda": int(b["n_lambda"]),
+                       "n_primal": int(b["n_primal"]), "nrhs": int(b["nrhs"])},
+            "cpu_baseline": {"value": val, "unit": "solves/s", "cores": threads, "kind": "oracle",
+                             "sample": f"per step: oracle local set-up of 1 of {nsub} subdomains + {n_iter} "
+                                       f"local F-apply contributions, extrapolated x{nsub}"},
+            "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------------------
+# GPU arm
+# ---------------------------------------------------------------------------
+def measure_dgemm_tflops(torch, dev):
+    n = 8192
+    a = torch.randn(n, n, dtype=torch.float64, device=dev)
+    b = torch.randn(n, n, dtype=torch.float64, device=dev)
+    best = 1e30
+    for _ in range(4):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        torch.matmul(a, b)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
+    del a, b
+    return 2 * n ** 3 / (best * 1e-3) / 1e12
+
+
+def run_ours(args, rank, world, local):
+    import torch
+    from ietigen.bundle import make_bundle
+    from paper_2501_04340_b200 import ietidp
+
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    b = make_bundle(args.config)
+    stream = torch.cuda.Stream(device=dev)
+    S = ietidp.from_bundle(b, device=local, stream=stream.cuda_stream)
+    S.analyze()
+    flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
+    ev = lambda: torch.cuda.Event(enable_timing=True)
+
+    def step():
+        S.factor()
+        return S.solve(want_lambda=False)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            step()
+        torch.cuda.synchronize()
+        barrier(world)
+        launches0 = S.kernel_launches()
+        times, reps = [], []
+        with Clocks(local) as clk:
+            t_wall = time.perf_counter()
+            for _ in range(args.steps):
+                flush.fill_(1.0)  # L2 flush between timed steps (not timed)
+                torch.cuda.synchronize()
+                e0, e1 = ev(), ev()
+                e0.record(stream)
+                _, rep = step()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                times.append(e0.elapsed_time(e1))
+                reps.append(rep)
+            t_wall = time.perf_counter() - t_wall
+        torch.cuda.synchronize()
+        barrier(world)
+        launches = (S.kernel_launches() - launches0) // max(args.steps, 1)
+        ms_step = max_over_ranks(statistics.mean(times), world, dev)
+        rep = reps[-1]
+
+        # ---- F-applies/s (operator loop alone, ncols = nrhs) ----
+        nc = b["nrhs"]
+        x = torch.randn(nc, b["n_lambda"], dtype=torch.float64, device=dev)
+        y = torch.empty_like(x)
+        for _ in range(5):
+            S.apply_F_device(x, y, nc)
+        torch.cuda.synchronize()
+        e0, e1 = ev(), ev()
+        e0.record(stream)
+        for _ in range(args.fapply_iters):
+            S.apply_F_device(x, y, nc)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        fa_ms = e0.elapsed_time(e1) / args.fapply_iters
+        f_apply_per_s = nc / (fa_ms * 1e-3)
+
+        # ---- end-to-end through the C-ABI with host buffers ----
+        e2e = None
+        if not args.no_e2e:
+            kv = [torch.from_numpy(sd["K_data"]).pin_memory() for sd in b["subs"]]
+            fv = [torch.from_numpy(np.ascontiguousarray(sd["f"])).pin_memory() for sd in b["subs"]]
+            uo = [torch.empty((nc, sd["n"]), dtype=torch.float64).pin_memory() for sd in b["subs"]]
+            lam_host = torch.empty((nc, b["n_lambda"]), dtype=torch.float64).pin_memory()
+            import ctypes as C
+            h2d = sum(t.numel() * 8 for t in kv) + sum(t.numel() * 8 for t in fv)
+            d2h = lam_host.numel() * 8 + sum(t.numel() * 8 for t in uo)
+            ets = []
+            rep_e = ietidp.Report()
+            for it in range(2 + args.steps):
+                flush.fill_(1.0)
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                for k in range(b["n_sub"]):
+                    S._check(S.lib.ietidp_set_values(S.h, k, C.c_void_p(kv[k].data_ptr()),
+                                                     C.c_void_p(fv[k].data_ptr())))
+                S.factor()
+                S._check(S.lib.ietidp_solve(S.h, C.c_void_p(lam_host.data_ptr()), C.byref(rep_e)))
+                for k in range(b["n_sub"]):
+                    S._check(S.lib.ietidp_get_u(S.h, k, C.c_void_p(uo[k].data_ptr())))
+                dt = time.perf_counter() - t0
+                if it >= 2:
+                    ets.append(dt)
+            e2e_s = max_over_ranks(statistics.mean(ets), world, dev)
+            e2e = {"value": world / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
+                   "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3}
+
+        fp64_peak = measure_dgemm_tflops(torch, dev) if rank == 0 else None
+
+    if rank != 0:
+        return
+    pk = peaks()
+    hbm = pk.get("hbm_gbs", 6650.0)
+    it_max = max(rep["iters"])
+    pcg_bytes = rep["pcg_bytes_per_iter"] * 1.0
+    pcg_ms_iter = rep["ms_pcg"] / max(it_max, 1)
+    pcg_gbs = pcg_bytes / (pcg_ms_iter * 1e-3) / 1e9 if it_max else 0.0
+    fac_tflops = rep["factor_flops"] / (rep["ms_factor"] * 1e-3) / 1e12
+    fa_gbs = rep["f_apply_bytes"] * nc / (fa_ms * 1e-3) / 1e9
+    phases = {"factor": rep["ms_factor"], "coarse_rhs": rep["ms_coarse"], "pcg": rep["ms_pcg"],
+              "recover": rep["ms_recover"]}
+    dominant = max(phases, key=phases.get)
+    roof_pcg = {"kernel": "pcg loop (k_local solve+precond, k_bgather x2, k_coarse, cg updates) per iteration",
+                "bound": "hbm", "achieved": pcg_gbs, "peak": hbm, "unit": "GB/s", "frac": pcg_gbs / hbm,
+                "traffic": None, "algorithmic_bytes_per_iter": int(pcg_bytes)}
+    roof_fac = {"kernel": "batched multifrontal Cholesky (k_potrf, k_panel_gemm DMMA, k_extend_add, k_scatter)",
+                "bound": "tensor", "achieved": fac_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                "frac": fac_tflops / fp64_peak if fp64_peak else None, "traffic": None,
+                "useful_flops": rep["factor_flops"], "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"}
+    roofline = roof_fac if dominant == "factor" else roof_pcg
+    cpu = None
+    if not args.no_cpu_baseline and world == 1:
+        sec, threads = oracle_sample(b, it_max, [0, 1])
+        cpu = {"value": 1.0 / sec, "unit": "solves/s", "cores": threads, "kind": "oracle",
+               "sample": f"oracle local set-up of subdomains 0-1 of {b['n_sub']} + {it_max} local F-apply "
+                         f"contributions each, extrapolated x{b['n_sub'] / 2:g}"}
+    line = {
+        "metric": METRIC, "value": world / (ms_step * 1e-3), "unit": "solves/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": args.config, "n_sub": b["n_sub"], "n_lambda": b["n_lambda"],
+                   "n_primal": b["n_primal"], "nrhs": nc, "l2": "flushed between timed steps (512 MB write)",
+                   "replicas": world},
+        "phases_ms": phases, "iters": rep["iters"], "rel_residual": max(rep["rel_residual"]),
+        "f_applies_per_s": f_apply_per_s, "f_apply_us": fa_ms * 1e3, "f_apply_gbs": fa_gbs,
+        "f_apply_note": "operator loop alone; L_II working set %.0f MB (L2 126 MB)" % (rep["f_apply_bytes"] / 2 / 1e6),
+        "roofline": roofline, "rooflines": {"factor": roof_fac, "pcg": roof_pcg},
+        "fp64_dgemm_tflops": fp64_peak, "clocks": clk.summary(), "gpu_launches": int(launches),
+        "e2e": e2e, "cpu_baseline": cpu,
+        "symbolic": {"n_supernodes": rep["n_supernodes"], "n_levels": rep["n_levels"], "max_front": rep["max_front"],
+                     "nnz_L": rep["nnz_L"], "factor_flops": rep["factor_flops"]},
+        "wall_s": t_wall,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_init(args)
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

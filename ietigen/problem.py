@@ -397,6 +397,11 @@ class Problem:
         j = C.T @ t
         m = sd.local_mask
         K = K[m][:, m].tocsr()
+        # C^T M2 C in floating point is symmetric only up to rounding, and SpGEMM
+        # drops an entry that cancels to exactly 0.0 on one side only: store the
+        # exactly symmetric part on the union pattern (the C-ABI requires a
+        # symmetric CSR pattern, include/ietidp.h).
+        K = ((K + K.T) * 0.5).tocsr()
         K.sort_indices()
         j = np.ascontiguousarray(j[m])
         if with_face:
