@@ -156,7 +156,7 @@ struct NestedDissection {
   }
 };
 
-LocalResult analyze_sub(const SubIn& in, int k, int nrhs, int ordering, int leaf) {
+LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf) {
   LocalResult R;
   SubPlan& sp = R.sp;
   const int n = in.n;
@@ -194,8 +194,7 @@ LocalResult analyze_sub(const SubIn& in, int k, int nrhs, int ordering, int leaf
   sp.nI = (int)rI.size();
   sp.nr = sp.nV + sp.nI;
   sp.nP = (int)in.prim.size();
-  sp.ploc.assign(n, -1);
-  for (int q = 0; q < sp.nP; ++q) sp.ploc[in.prim[q]] = q;
+  const int ne = sp.nr + sp.nP;
 
   // ---- graph of K_VV ----
   std::vector<int> xadj(sp.nV + 1, 0), adj;
@@ -208,22 +207,19 @@ LocalResult analyze_sub(const SubIn& in, int k, int nrhs, int ordering, int leaf
     xadj[a + 1] = (int)adj.size();
   }
 
-  // ---- ordering: supernode tree in postorder ----
-  std::vector<std::vector<int>> sn_vars;       // in postorder (local vertex ids of rV)
+  // ---- ordering of r_V: supernode tree in postorder ----
+  std::vector<std::vector<int>> sn_vars;
   if (sp.nV > 0) {
+    std::vector<int> all(sp.nV);
+    std::iota(all.begin(), all.end(), 0);
     if (ordering == IETIDP_ORDER_DENSE) {
-      std::vector<int> all(sp.nV);
-      std::iota(all.begin(), all.end(), 0);
       sn_vars.push_back(all);
     } else {
       NestedDissection nd(xadj, adj, sp.nV, std::max(leaf, 8));
-      std::vector<int> all(sp.nV);
-      std::iota(all.begin(), all.end(), 0);
       for (int a = 0; a < sp.nV; ++a) nd.reg[a] = -1;
       auto comps = nd.components(all, -1);
       std::vector<int> roots;
       for (auto& c : comps) roots.push_back(nd.build(c.first, c.second));
-      // iterative postorder
       std::vector<std::pair<int, size_t>> st;
       for (int r : roots) {
         st.push_back({r, 0});
@@ -241,45 +237,39 @@ LocalResult analyze_sub(const SubIn& in, int k, int nrhs, int ordering, int leaf
       }
     }
   }
-  // positions
-  sp.perm.resize(sp.nr);
+  // ---- positions: r_V (ND), r_I, P ----
+  sp.perm.resize(ne);
   sp.pos.assign(n, -1);
-  std::vector<int> owner(sp.nr, -1);
+  std::vector<int> owner(ne, -1);
   int p = 0;
-  for (size_t s = 0; s < sn_vars.size(); ++s) {
+  auto add_sn = [&](const std::vector<int>& dofs, int coarse) {
     SnHost h;
     h.sub = k;
     h.c0 = p;
-    h.npiv = (int)sn_vars[s].size();
+    h.npiv = (int)dofs.size();
     h.parent = -1;
     h.level = 0;
-    for (int v : sn_vars[s]) {
-      int dof = rV[v];
-      sp.perm[p] = dof;
-      sp.pos[dof] = p;
-      owner[p] = (int)s;
-      ++p;
-    }
-    R.sn.push_back(std::move(h));
-  }
-  if (sp.nI > 0) {
-    SnHost h;
-    h.sub = k;
-    h.c0 = p;
-    h.npiv = sp.nI;
-    h.parent = -1;
-    h.level = 0;
-    for (int dof : rI) {
+    h.coarse = coarse;
+    for (int dof : dofs) {
       sp.perm[p] = dof;
       sp.pos[dof] = p;
       owner[p] = (int)R.sn.size();
       ++p;
     }
-    sp.root = (int)R.sn.size();
     R.sn.push_back(std::move(h));
+    return (int)R.sn.size() - 1;
+  };
+  for (auto& vars : sn_vars) {
+    std::vector<int> dofs;
+    dofs.reserve(vars.size());
+    for (int v : vars) dofs.push_back(rV[v]);
+    add_sn(dofs, 0);
   }
+  if (sp.nI > 0) sp.root = add_sn(rI, 0);
+  if (sp.nP > 0) sp.pnode = add_sn(std::vector<int>(in.prim.begin(), in.prim.end()), 1);
+
   // ---- symbolic factorisation: row structure of every supernode ----
-  std::vector<int> mark(sp.nr, -1);
+  std::vector<int> mark(ne, -1);
   for (size_t s = 0; s < R.sn.size(); ++s) {
     SnHost& h = R.sn[s];
     int last = h.c0 + h.npiv - 1;
@@ -311,7 +301,6 @@ LocalResult analyze_sub(const SubIn& in, int k, int nrhs, int ordering, int leaf
     for (int c : h.children) lv = std::max(lv, R.sn[c].level + 1);
     h.level = lv;
   }
-  (void)nrhs;
   return R;
 }
 
@@ -322,32 +311,43 @@ int find_in_front(const SnHost& s, int x) {
   return s.npiv + (int)(it - s.rows.begin());
 }
 
+template <class F>
+void parallel_for(int n, F&& fn) {
+  int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
+  std::vector<std::thread> th;
+  std::atomic<int> next{0};
+  for (int t = 0; t < nth; ++t)
+    th.emplace_back([&]() {
+      for (int k; (k = next++) < n;) fn(k);
+    });
+  for (auto& x : th) x.join();
+}
+
 }  // namespace
 
 static void fill_report(ietidp_s* h) {
   const Plan& P = h->plan;
-  const int ns = h->n_sub;
-  const int nsn = (int)P.sn.size();
-  h->rep.n_supernodes = nsn;
+  h->rep.n_supernodes = (int)P.sn.size();
   h->rep.n_levels = P.max_level + 1;
   h->rep.max_front = P.max_front;
   h->rep.max_nI = P.max_nI;
-  long long snr = 0, snI = 0, sI2 = 0, sIP = 0;
-  for (int k = 0; k < ns; ++k) {
-    snr += P.subs[k].nr;
-    snI += P.subs[k].nI;
-    sI2 += (long long)P.subs[k].nI * P.subs[k].nI;
-    sIP += (long long)P.subs[k].nI * P.subs[k].nP;
+  long long snr = 0, snI = 0, tri = 0, sIP = 0;
+  for (int k = 0; k < h->n_sub; ++k) {
+    const SubPlan& sp = P.subs[k];
+    snr += sp.nr;
+    snI += sp.nI;
+    tri += (long long)sp.nI * (sp.nI + 1) / 2;
+    sIP += (long long)sp.nI * sp.nP;
   }
   h->rep.sum_nr = snr;
   h->rep.sum_nI = snI;
   h->rep.nnz_L = P.nnz_L;
   h->rep.factor_flops = P.flops;
-  // algorithmic bytes (DESIGN.md §"Rooflines"): the F-apply reads the lower
-  // triangle of every L_II twice (forward, backward) and G twice; the
-  // preconditioner reads it twice (L^T, L).
-  h->rep.f_apply_bytes = 2 * 8 * ((sI2 + snI) / 2) + 2 * 8 * sIP;
-  h->rep.pcg_bytes_per_iter = 4 * 8 * ((sI2 + snI) / 2) + 2 * 8 * sIP;
+  // algorithmic bytes: one F-apply reads the lower
+  // triangle of every L_II^-1 twice (forward, backward) and L_PI twice; the
+  // preconditioner reads the lower triangle of every L_II twice (L^T, L).
+  h->rep.f_apply_bytes = 2 * 8 * tri + 2 * 8 * sIP;
+  h->rep.pcg_bytes_per_iter = 4 * 8 * tri + 2 * 8 * sIP;
 }
 
 // Build the complete plan and upload every structure and the raw values.
@@ -363,8 +363,9 @@ void analyze_all(ietidp_s* h) {
     const SubIn& in = h->in[k];
     for (size_t e = 0; e < in.B_lambda.size(); ++e) {
       int l = in.B_lambda[e];
-      if (cnt[l] == 1 && firstsub[l] == k)
-        throw Error(IETIDP_E_B_STRUCTURE, "multiplier " + std::to_string(l) + " twice in subdomain " + std::to_string(k));
+      if (cnt[l] >= 1 && firstsub[l] == k)
+        throw Error(IETIDP_E_B_STRUCTURE,
+                    "multiplier " + std::to_string(l) + " twice in subdomain " + std::to_string(k));
       cnt[l]++;
       ssum[l] += in.B_sign[e];
       firstsub[l] = k;
@@ -372,21 +373,12 @@ void analyze_all(ietidp_s* h) {
   }
   for (int l = 0; l < h->n_lambda; ++l)
     if (cnt[l] != 2 || ssum[l] != 0)
-      throw Error(IETIDP_E_B_STRUCTURE, "multiplier row " + std::to_string(l) + " is not {+1,-1} in two subdomains");
+      throw Error(IETIDP_E_B_STRUCTURE,
+                  "multiplier row " + std::to_string(l) + " is not {+1,-1} in two subdomains");
 
   // ---- per-subdomain analysis, in parallel ----
   std::vector<LocalResult> loc(ns);
-  {
-    int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> th;
-    std::atomic<int> next{0};
-    for (int t = 0; t < nth; ++t)
-      th.emplace_back([&]() {
-        for (int k; (k = next++) < ns;)
-          loc[k] = analyze_sub(h->in[k], k, nrhs, h->opt.ordering, h->opt.leaf_size);
-      });
-    for (auto& x : th) x.join();
-  }
+  parallel_for(ns, [&](int k) { loc[k] = analyze_sub(h->in[k], k, h->opt.ordering, h->opt.leaf_size); });
   for (int k = 0; k < ns; ++k)
     if (loc[k].st != IETIDP_OK) throw Error(loc[k].st, loc[k].err);
 
@@ -408,19 +400,20 @@ void analyze_all(ietidp_s* h) {
     }
     P.subs[k].sn_begin = {sn_base[k], sn_base[k + 1]};
     if (P.subs[k].root >= 0) P.subs[k].root += sn_base[k];
+    if (P.subs[k].pnode >= 0) P.subs[k].pnode += sn_base[k];
   }
   const int nsn = (int)P.sn.size();
   for (auto& s : P.sn) P.max_level = std::max(P.max_level, s.level);
-  // level groups, each sorted by npiv descending (the active fronts of a panel are a prefix)
   std::vector<std::vector<int>> bylev(P.max_level + 1);
   for (int i = 0; i < nsn; ++i) bylev[P.sn[i].level].push_back(i);
   for (auto& v : bylev)
     std::stable_sort(v.begin(), v.end(), [&](int a, int b) { return P.sn[a].npiv > P.sn[b].npiv; });
 
-  // ---- memory layout ----
+  // ---- memory layout of the supernodes ----
   std::vector<SnDev> sd(nsn);
   std::vector<int> rows_all, rel_all, children_all, work;
-  long long pool = 0, dinv = 0, vec = 0;
+  std::vector<GemmWork> gwork;
+  long long pool = 0, dinv = 0, inv = 0, vec = 0;
   P.levels.resize(P.max_level + 1);
   for (int L = 0; L <= P.max_level; ++L) {
     LevelPlan& lp = P.levels[L];
@@ -436,25 +429,33 @@ void analyze_all(ietidp_s* h) {
       d.c0 = s.c0;
       d.sub = s.sub;
       d.parent = s.parent;
+      d.coarse = s.coarse;
       d.front_off = pool;
       pool += (long long)d.ld * d.f;
-      d.dinv_off = dinv;
-      dinv += (long long)((s.npiv + TB - 1) / TB) * TILE_ELEMS;
       d.vec_off = vec;
       vec += s.f;
+      d.ldi = (s.npiv + 3) & ~3;
+      if (!s.coarse) {
+        d.dinv_off = dinv;
+        dinv += (long long)((s.npiv + TB - 1) / TB) * TILE_ELEMS;
+        d.inv_off = inv;
+        inv += (long long)d.ldi * s.npiv;
+        for (int j = 0; j < s.npiv; ++j) {
+          long long c = s.f - j;
+          P.nnz_L += c;
+          P.flops += c * c;
+        }
+        P.inv_flops += (long long)s.npiv * s.npiv * s.npiv / 3;
+      }
       P.level_sn.push_back(i);
       P.max_front = std::max(P.max_front, s.f);
-      for (int j = 0; j < s.npiv; ++j) {
-        long long c = s.f - j;
-        P.nnz_L += c;
-        P.flops += c * c;
-      }
     }
     lp.front_end = pool;
   }
   P.pool_doubles = pool;
   P.dinv_doubles = dinv;
-  P.vec_doubles = vec;
+  P.inv_doubles = inv;
+  P.vec_rows = vec;
   for (int i = 0; i < nsn; ++i) {
     SnHost& s = P.sn[i];
     SnDev& d = sd[i];
@@ -474,10 +475,11 @@ void analyze_all(ietidp_s* h) {
     children_all.insert(children_all.end(), s.children.begin(), s.children.end());
   }
 
-  // ---- work lists of the factorisation ----
+  auto push = [&](int a, int b, int c) { work.insert(work.end(), {a, b, c}); };
+  auto tiles_of = [](int n) { return (n + TB - 1) / TB; };
+  // ---- work lists: factorisation and sweeps, per level ----
   for (int L = 0; L <= P.max_level; ++L) {
     LevelPlan& lp = P.levels[L];
-    // extend-add, one launch per child slot
     int maxc = 0;
     for (int i : bylev[L]) maxc = std::max(maxc, (int)P.sn[i].children.size());
     for (int q = 0; q < maxc; ++q) {
@@ -486,75 +488,153 @@ void analyze_all(ietidp_s* h) {
         if ((int)P.sn[i].children.size() > q) {
           int c = P.sn[i].children[q];
           int nu = P.sn[c].f - P.sn[c].npiv;
-          for (int j0 = 0; j0 < nu; j0 += 32) {
-            work.insert(work.end(), {c, j0, std::min(nu, j0 + 32)});
-            ++n;
-          }
+          for (int j0 = 0; j0 < nu; j0 += 32, ++n) push(c, j0, std::min(nu, j0 + 32));
         }
       if (n) lp.ea.push_back({off, n});
     }
     int maxp = 0;
-    for (int i : bylev[L]) maxp = std::max(maxp, (P.sn[i].npiv + TB - 1) / TB);
+    for (int i : bylev[L])
+      if (!P.sn[i].coarse) maxp = std::max(maxp, tiles_of(P.sn[i].npiv));
     for (int kp = 0; kp < maxp; ++kp) {
       LevelPlan::Panel pn{};
       pn.potrf_off = (int)work.size() / 3;
       for (int i : bylev[L])
-        if (P.sn[i].npiv > kp * TB) {
-          work.insert(work.end(), {i, kp, 0});
+        if (!P.sn[i].coarse && P.sn[i].npiv > kp * TB) {
+          push(i, kp, 0);
           pn.potrf_n++;
         }
       pn.trsm_off = (int)work.size() / 3;
       for (int i : bylev[L]) {
         const SnHost& s = P.sn[i];
-        if (s.npiv <= kp * TB) continue;
+        if (s.coarse || s.npiv <= kp * TB) continue;
         int b = std::min(TB, s.npiv - kp * TB);
-        int start = kp * TB + b, nrow = s.f - start;
-        for (int t = 0; t * TB < nrow; ++t) {
-          work.insert(work.end(), {i, kp, t});
-          pn.trsm_n++;
-        }
+        int nrow = s.f - (kp * TB + b);
+        for (int t = 0; t * TB < nrow; ++t, ++pn.trsm_n) push(i, kp, t);
       }
       pn.upd_off = (int)work.size() / 3;
       for (int i : bylev[L]) {
         const SnHost& s = P.sn[i];
-        if (s.npiv <= kp * TB) continue;
+        if (s.coarse || s.npiv <= kp * TB) continue;
         int b = std::min(TB, s.npiv - kp * TB);
-        int start = kp * TB + b, nrow = s.f - start;
-        int nt = (nrow + TB - 1) / TB;
-        // trailing update of the lower triangle: later pivot columns and the
-        // update (Schur) block alike
+        int nt = tiles_of(s.f - (kp * TB + b));
         for (int ti = 0; ti < nt; ++ti)
-          for (int tj = 0; tj <= ti; ++tj) {
-            work.insert(work.end(), {i, kp, ti * 65536 + tj});
-            pn.upd_n++;
-          }
+          for (int tj = 0; tj <= ti; ++tj, ++pn.upd_n) push(i, kp, ti * 65536 + tj);
       }
       lp.panels.push_back(pn);
     }
+    // sweeps
+    lp.fs_off = (int)work.size() / 3;
+    for (int i : bylev[L])
+      if (!P.sn[i].coarse)
+        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.fs_n) push(i, t, 0);
+    lp.fu_off = (int)work.size() / 3;
+    for (int i : bylev[L])
+      if (!P.sn[i].coarse)
+        for (int t = 0; t < tiles_of(P.sn[i].f - P.sn[i].npiv); ++t, ++lp.fu_n) push(i, t, 0);
+    lp.bt_off = (int)work.size() / 3;
+    for (int i : bylev[L])
+      if (!P.sn[i].coarse && P.sn[i].f > P.sn[i].npiv)
+        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bt_n) push(i, t, 0);
+    lp.bx_off = (int)work.size() / 3;
+    for (int i : bylev[L])
+      if (!P.sn[i].coarse)
+        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bx_n) push(i, t, 0);
+  }
+  // ---- partitioned inverse L11^-1 by recursive doubling over TB-blocks ----
+  P.inv_copy_off = (int)work.size() / 3;
+  for (int i = 0; i < nsn; ++i)
+    if (!P.sn[i].coarse)
+      for (int kp = 0; kp < tiles_of(P.sn[i].npiv); ++kp, ++P.inv_copy_n) push(i, kp, 0);
+  int maxnb = 0;
+  for (auto& s : P.sn)
+    if (!s.coarse) maxnb = std::max(maxnb, tiles_of(s.npiv));
+  long long tmpoff_dummy = 0;
+  (void)tmpoff_dummy;
+  for (int half = 1; half < maxnb; half *= 2) {
+    // step 1: T(second, first) = L11(second, first-half) * Linv(first, first)
+    int off1 = (int)gwork.size();
+    for (int i = 0; i < nsn; ++i) {
+      const SnHost& s = P.sn[i];
+      if (s.coarse) continue;
+      const SnDev& d = sd[i];
+      const int nb = tiles_of(s.npiv);
+      for (int fs = 0; fs < nb; fs += 2 * half) {
+        int ss = fs + half, se = std::min(fs + 2 * half, nb);
+        if (ss >= nb) continue;
+        for (int ti = ss; ti < se; ++ti)
+          for (int tj = fs; tj < ss; ++tj) {
+            GemmWork g{};
+            int k0 = tj * TB, k1 = std::min(ss * TB, s.npiv);
+            g.c_off = d.inv_off + (long long)tj * TB * d.ldi + ti * TB;  // T stored in tpool, same layout
+            g.a_off = d.front_off + (long long)k0 * d.ld + ti * TB;
+            g.b_off = d.inv_off + (long long)tj * TB * d.ldi + k0;
+            g.lda = d.ld;
+            g.ldb = d.ldi;
+            g.ldc = d.ldi;
+            g.m = std::min(TB, s.npiv - ti * TB);
+            g.n = std::min(TB, s.npiv - tj * TB);
+            g.kdim = k1 - k0;
+            g.mode = 0;
+            gwork.push_back(g);
+          }
+      }
+    }
+    P.inv_rounds.push_back({off1, (int)gwork.size() - off1});
+    // step 2: Linv(second, first) = -Linv(second, second) * T(second, first)
+    int off2 = (int)gwork.size();
+    for (int i = 0; i < nsn; ++i) {
+      const SnHost& s = P.sn[i];
+      if (s.coarse) continue;
+      const SnDev& d = sd[i];
+      const int nb = tiles_of(s.npiv);
+      for (int fs = 0; fs < nb; fs += 2 * half) {
+        int ss = fs + half, se = std::min(fs + 2 * half, nb);
+        if (ss >= nb) continue;
+        for (int ti = ss; ti < se; ++ti)
+          for (int tj = fs; tj < ss; ++tj) {
+            GemmWork g{};
+            int k0 = ss * TB, k1 = std::min((ti + 1) * TB, s.npiv);
+            g.c_off = d.inv_off + (long long)tj * TB * d.ldi + ti * TB;
+            g.a_off = d.inv_off + (long long)k0 * d.ldi + ti * TB;
+            g.b_off = d.inv_off + (long long)tj * TB * d.ldi + k0;  // T in tpool
+            g.lda = d.ldi;
+            g.ldb = d.ldi;
+            g.ldc = d.ldi;
+            g.m = std::min(TB, s.npiv - ti * TB);
+            g.n = std::min(TB, s.npiv - tj * TB);
+            g.kdim = k1 - k0;
+            g.mode = 1;  // negate
+            gwork.push_back(g);
+          }
+      }
+    }
+    P.inv_rounds.push_back({off2, (int)gwork.size() - off2});
   }
 
   // ---- per-subdomain offsets ----
-  long long kv = 0, fv = 0, xo = 0, rio = 0, kppo = 0, go = 0, slo = 0, to = 0, dto = 0;
-  int po = 0, permo = 0;
+  long long kv = 0, fv = 0, xo = 0, rio = 0, lpio = 0, to = 0, uo = 0;
+  int po = 0, permo = 0, cta = 0;
   P.nPmax = 0;
-  for (int k = 0; k < ns; ++k) P.nPmax = std::max(P.nPmax, P.subs[k].nP);
-  P.ncx = P.nPmax + nrhs;
   h->kval_off.resize(ns);
   h->fval_off.resize(ns);
   h->u_off.resize(ns);
-  long long uo = 0;
+  std::vector<LoopWork> loopwork;
+  std::vector<int> sub_cta0(ns), sub_ncta(ns);
   for (int k = 0; k < ns; ++k) {
     SubPlan& sp = P.subs[k];
     SubDev& d = h->h_sub[k];
     const SubIn& in = h->in[k];
+    P.nPmax = std::max(P.nPmax, sp.nP);
     d.nk = in.n;
     d.nr = sp.nr;
     d.nI = sp.nI;
     d.nV = sp.nV;
     d.nP = sp.nP;
+    d.ne = sp.nr + sp.nP;
     d.root = sp.root;
+    d.pnode = sp.pnode;
     d.x_off = xo;
-    xo += sp.nr;
+    xo += d.ne;
     d.rI_off = rio;
     rio += sp.nI;
     d.kval_off = kv;
@@ -563,116 +643,88 @@ void analyze_all(ietidp_s* h) {
     d.f_off = fv;
     h->fval_off[k] = fv;
     fv += (long long)in.n * nrhs;
-    d.kpp_off = kppo;
-    kppo += (long long)sp.nP * sp.nP;
-    d.jp_off = (long long)po * nrhs;
-    d.floc_off = (long long)po * nrhs;
-    d.gk_off = (long long)po * nrhs;
+    d.lpi_off = lpio;
+    lpio += (long long)sp.nP * sp.nI;
+    d.nt = tiles_of(sp.nI);
+    d.tile_off = to;
+    d.itile_off = to;  // same offsets in the two tile arrays
+    to += (long long)d.nt * (d.nt + 1) / 2 * TILE_ELEMS;
     d.prim_off = po;
     po += sp.nP;
-    d.g_off = go;
-    go += (long long)sp.nI * sp.nP;
-    d.sloc_off = slo;
-    slo += (long long)sp.nP * sp.nP;
-    d.nt = (sp.nI + TB - 1) / TB;
-    d.tile_off = to;
-    to += (long long)d.nt * (d.nt + 1) / 2 * TILE_ELEMS;
-    d.dtile_off = dto;
-    dto += (long long)d.nt * TILE_ELEMS;
     d.perm_off = permo;
-    permo += sp.nr;
+    permo += d.ne;
     h->u_off[k] = uo;
     uo += (long long)in.n * nrhs;
     P.max_nI = std::max(P.max_nI, sp.nI);
+    // loop CTAs: block pairs (i, nt-1-i)
+    d.cta0 = cta;
+    sub_cta0[k] = cta;
+    for (int i = 0; i < (d.nt + 1) / 2; ++i) {
+      int j = d.nt - 1 - i;
+      loopwork.push_back({k, i == j ? 1 : 2, i, j});
+      ++cta;
+    }
+    sub_ncta[k] = cta - d.cta0;
   }
+  if (P.max_nI > 32 * TB) throw Error(IETIDP_E_ARG, "interface block larger than 2048 DOFs is not supported");
+  if (P.nPmax > 16) throw Error(IETIDP_E_ARG, "more than 16 primal DOFs in one subdomain is not supported");
   h->n_slots = (int)rio;
   h->sum_nP = po;
+  h->n_loopwork = (int)loopwork.size();
 
-  // ---- scatter lists (built per subdomain in parallel, merged per level) ----
+  // ---- scatter lists (per subdomain in parallel, merged per level) ----
   struct Scat {
-    std::vector<std::vector<long long>> fd;  // per level
+    std::vector<std::vector<long long>> fd;
     std::vector<std::vector<int>> fs;
-    std::vector<long long> xd, kd, fxd, fpd;
-    std::vector<int> xs, ks, fxs, fps;
+    std::vector<long long> fxd;
+    std::vector<int> fxs;
     std::vector<int> kdiag;
     std::string err;
   };
   std::vector<Scat> sc(ns);
-  {
-    int nth = std::max(1u, std::min(16u, std::thread::hardware_concurrency()));
-    std::vector<std::thread> th;
-    std::atomic<int> next{0};
-    for (int t = 0; t < nth; ++t)
-      th.emplace_back([&]() {
-        for (int k; (k = next++) < ns;) {
-          Scat& S = sc[k];
-          const SubIn& in = h->in[k];
-          const SubPlan& sp = P.subs[k];
-          const SubDev& d = h->h_sub[k];
-          S.fd.resize(P.max_level + 1);
-          S.fs.resize(P.max_level + 1);
-          // owner supernode of each position
-          std::vector<int> own(sp.nr);
-          for (int s = sp.sn_begin[0]; s < sp.sn_begin[1]; ++s)
-            for (int q = 0; q < P.sn[s].npiv; ++q) own[P.sn[s].c0 + q] = s;
-          S.kdiag.assign(sp.nI, -1);
-          // K_rr lower triangle, column by column in position order
-          for (int pj = 0; pj < sp.nr; ++pj) {
-            int j = sp.perm[pj];
-            int s = own[pj];
-            const SnHost& hs = P.sn[s];
-            const SnDev& ds = sd[s];
-            int lcol = pj - hs.c0;
-            for (int64_t e = in.rowptr[j]; e < in.rowptr[j + 1]; ++e) {
-              int i = in.col[e];
-              int pi = sp.pos[i];
-              if (pi < pj) continue;  // tree/primal (-1) or upper triangle
-              int lrow = find_in_front(hs, pi);
-              if (lrow < 0) {
-                S.err = "internal: entry outside the symbolic structure";
-                break;
-              }
-              S.fd[hs.level].push_back(ds.front_off + (long long)lcol * ds.ld + lrow);
-              S.fs[hs.level].push_back((int)(d.kval_off + e));
-              if (pi == pj && pj >= sp.nV) S.kdiag[pj - sp.nV] = (int)(d.kval_off + e);
-            }
-          }
-          for (int a = 0; a < sp.nI; ++a)
-            if (S.kdiag[a] < 0) S.err = "subdomain " + std::to_string(k) + ": missing diagonal entry";
-          // K_rP -> X0, K_PP -> kpp, f -> X0 / jp
-          for (int i = 0; i < in.n; ++i) {
-            int pi = sp.pos[i], qi = sp.ploc[i];
-            if (pi < 0 && qi < 0) continue;
-            for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) {
-              int qj = sp.ploc[in.col[e]];
-              if (qj < 0) continue;
-              if (pi >= 0) {
-                S.xd.push_back((d.x_off + pi) * P.ncx + qj);
-                S.xs.push_back((int)(d.kval_off + e));
-              } else {
-                S.kd.push_back(d.kpp_off + (long long)qi * sp.nP + qj);
-                S.ks.push_back((int)(d.kval_off + e));
-              }
-            }
-            for (int c = 0; c < nrhs; ++c) {
-              if (pi >= 0) {
-                S.fxd.push_back((d.x_off + pi) * P.ncx + P.nPmax + c);
-                S.fxs.push_back((int)(d.f_off + i + (long long)c * in.n));
-              } else {
-                S.fpd.push_back(d.jp_off + (long long)qi * nrhs + c);
-                S.fps.push_back((int)(d.f_off + i + (long long)c * in.n));
-              }
-            }
-          }
+  parallel_for(ns, [&](int k) {
+    Scat& S = sc[k];
+    const SubIn& in = h->in[k];
+    const SubPlan& sp = P.subs[k];
+    const SubDev& d = h->h_sub[k];
+    const int ne = d.ne;
+    S.fd.resize(P.max_level + 1);
+    S.fs.resize(P.max_level + 1);
+    std::vector<int> own(ne);
+    for (int s = sp.sn_begin[0]; s < sp.sn_begin[1]; ++s)
+      for (int q = 0; q < P.sn[s].npiv; ++q) own[P.sn[s].c0 + q] = s;
+    S.kdiag.assign(sp.nI, -1);
+    // K lower triangle in position order, column by column (pi >= pj)
+    for (int pj = 0; pj < ne; ++pj) {
+      int j = sp.perm[pj];
+      int s = own[pj];
+      const SnHost& hs = P.sn[s];
+      const SnDev& ds = sd[s];
+      int lcol = pj - hs.c0;
+      for (int64_t e = in.rowptr[j]; e < in.rowptr[j + 1]; ++e) {
+        int pi = sp.pos[in.col[e]];
+        if (pi < pj) continue;  // tree DOF (-1) or upper triangle
+        int lrow = find_in_front(hs, pi);
+        if (lrow < 0) {
+          S.err = "internal: entry outside the symbolic structure";
+          return;
         }
-      });
-    for (auto& x : th) x.join();
-  }
+        S.fd[hs.level].push_back(ds.front_off + (long long)lcol * ds.ld + lrow);
+        S.fs[hs.level].push_back((int)(d.kval_off + e));
+        if (pi == pj && pj >= sp.nV && pj < sp.nr) S.kdiag[pj - sp.nV] = (int)(d.kval_off + e);
+      }
+      for (int c = 0; c < nrhs; ++c) {
+        S.fxd.push_back((d.x_off + pj) * nrhs + c);
+        S.fxs.push_back((int)(d.f_off + j + (long long)c * in.n));
+      }
+    }
+    for (int a = 0; a < sp.nI; ++a)
+      if (S.kdiag[a] < 0) S.err = "subdomain " + std::to_string(k) + ": missing diagonal entry";
+  });
   for (int k = 0; k < ns; ++k)
     if (!sc[k].err.empty()) throw Error(IETIDP_E_ARG, sc[k].err);
-
-  std::vector<long long> fdst, xdst, kdst, fxdst, fpdst;
-  std::vector<int> fsrc, xsrc, ksrc, fxsrc, fpsrc, kdiag;
+  std::vector<long long> fdst, fxdst;
+  std::vector<int> fsrc, fxsrc, kdiag;
   for (int L = 0; L <= P.max_level; ++L) {
     P.levels[L].scat_begin = (long long)fdst.size();
     for (int k = 0; k < ns; ++k) {
@@ -684,23 +736,17 @@ void analyze_all(ietidp_s* h) {
     P.levels[L].scat_end = (long long)fdst.size();
   }
   for (int k = 0; k < ns; ++k) {
-    xdst.insert(xdst.end(), sc[k].xd.begin(), sc[k].xd.end());
-    xsrc.insert(xsrc.end(), sc[k].xs.begin(), sc[k].xs.end());
-    kdst.insert(kdst.end(), sc[k].kd.begin(), sc[k].kd.end());
-    ksrc.insert(ksrc.end(), sc[k].ks.begin(), sc[k].ks.end());
     fxdst.insert(fxdst.end(), sc[k].fxd.begin(), sc[k].fxd.end());
     fxsrc.insert(fxsrc.end(), sc[k].fxs.begin(), sc[k].fxs.end());
-    fpdst.insert(fpdst.end(), sc[k].fpd.begin(), sc[k].fpd.end());
-    fpsrc.insert(fpsrc.end(), sc[k].fps.begin(), sc[k].fps.end());
     kdiag.insert(kdiag.end(), sc[k].kdiag.begin(), sc[k].kdiag.end());
   }
 
   // ---- multipliers, slots, primal bookkeeping ----
-  std::vector<int> slot_lam(h->n_slots), slot_sub(h->n_slots);
+  std::vector<int> slot_lam(h->n_slots);
   std::vector<float> slot_sign(h->n_slots);
   std::vector<LamDev> lam(h->n_lambda);
   std::vector<int> lamfill(h->n_lambda, 0);
-  std::vector<int> prim_dof(po), prim_gid(po);
+  std::vector<int> prim_gid(po);
   std::vector<int> perm_all(permo);
   std::vector<char> gid_seen(h->n_primal, 0);
   for (int k = 0; k < ns; ++k) {
@@ -711,14 +757,12 @@ void analyze_all(ietidp_s* h) {
       int slot = (int)d.rI_off + sp.pos[in.B_dof[e]] - sp.nV;
       int l = in.B_lambda[e];
       slot_lam[slot] = l;
-      slot_sub[slot] = k;
       slot_sign[slot] = (float)in.B_sign[e];
       lam[l].slot[lamfill[l]] = slot;
       lam[l].sign[lamfill[l]] = (float)in.B_sign[e];
       lamfill[l]++;
     }
     for (int q = 0; q < sp.nP; ++q) {
-      prim_dof[d.prim_off + q] = in.prim[q];
       prim_gid[d.prim_off + q] = in.prim_gid[q];
       gid_seen[in.prim_gid[q]] = 1;
     }
@@ -726,32 +770,36 @@ void analyze_all(ietidp_s* h) {
   }
   for (int g = 0; g < h->n_primal; ++g)
     if (!gid_seen[g]) throw Error(IETIDP_E_ARG, "global primal " + std::to_string(g) + " has no local DOF");
-  // S_PP entry (g1, g2) <- sloc entries; global primal g <- primal rows
+  // S_PP entry (g1, g2) <- lower entries of the P fronts; global primal g <- (k, q)
   const int ng = h->n_primal;
-  std::vector<std::vector<int>> sl((size_t)ng * ng);
-  std::vector<std::vector<int>> pc(ng);
+  std::vector<std::vector<long long>> sl((size_t)ng * ng);
+  std::vector<std::vector<std::pair<int, int>>> pc(ng);
   for (int k = 0; k < ns; ++k) {
     const SubDev& d = h->h_sub[k];
+    if (d.pnode < 0) continue;
+    const SnDev& pn = sd[d.pnode];
     for (int a = 0; a < d.nP; ++a) {
       int ga = prim_gid[d.prim_off + a];
-      pc[ga].push_back(d.prim_off + a);
+      pc[ga].push_back({k, a});
       for (int b = 0; b < d.nP; ++b) {
         int gb = prim_gid[d.prim_off + b];
-        sl[(size_t)ga * ng + gb].push_back((int)(d.sloc_off + (long long)a * d.nP + b));
+        int r = std::max(a, b), c = std::min(a, b);
+        sl[(size_t)ga * ng + gb].push_back(pn.front_off + (long long)c * pn.ld + r);
       }
     }
   }
-  std::vector<int> scoef_ptr((size_t)ng * ng + 1, 0), scoef_src, pcon_ptr(ng + 1, 0), pcon_src;
+  std::vector<int> scoef_ptr((size_t)ng * ng + 1, 0), pcon_ptr(ng + 1, 0), pcon_sub, pcon_q;
+  std::vector<long long> scoef_src;
   for (size_t e = 0; e < sl.size(); ++e) {
     scoef_src.insert(scoef_src.end(), sl[e].begin(), sl[e].end());
     scoef_ptr[e + 1] = (int)scoef_src.size();
   }
   for (int g = 0; g < ng; ++g) {
-    pcon_src.insert(pcon_src.end(), pc[g].begin(), pc[g].end());
-    pcon_ptr[g + 1] = (int)pcon_src.size();
-  }
-  for (int k = 0; k < ns; ++k) {
-    h->h_sub[k].root = P.subs[k].root;
+    for (auto& x : pc[g]) {
+      pcon_sub.push_back(x.first);
+      pcon_q.push_back(x.second);
+    }
+    pcon_ptr[g + 1] = (int)pcon_sub.size();
   }
   auto t1 = std::chrono::steady_clock::now();
   fill_report(h);
@@ -768,46 +816,27 @@ void analyze_all(ietidp_s* h) {
   h->d_rel.upload(rel_all, s);
   h->d_children.upload(children_all, s);
   h->d_work.upload(work, s);
+  h->d_gwork.upload(gwork, s);
   h->d_level_sn.upload(P.level_sn, s);
   h->d_perm.upload(perm_all, s);
   h->d_uoff.upload(h->u_off, s);
-  h->d_prim_dof.upload(prim_dof, s);
   h->d_prim_gid.upload(prim_gid, s);
   h->sc_front_dst.upload(fdst, s);
   h->sc_front_src.upload(fsrc, s);
-  h->sc_x0_dst.upload(xdst, s);
-  h->sc_x0_src.upload(xsrc, s);
-  h->sc_kpp_dst.upload(kdst, s);
-  h->sc_kpp_src.upload(ksrc, s);
   h->sc_fx_dst.upload(fxdst, s);
   h->sc_fx_src.upload(fxsrc, s);
-  h->sc_fp_dst.upload(fpdst, s);
-  h->sc_fp_src.upload(fpsrc, s);
   h->kdiag_src.upload(kdiag, s);
   h->slot_lam.upload(slot_lam, s);
-  h->slot_sub.upload(slot_sub, s);
   h->slot_sign.upload(slot_sign, s);
-  {
-    std::vector<long long> goff(h->n_slots);
-    std::vector<int> np(h->n_slots), poff(h->n_slots);
-    for (int k = 0; k < ns; ++k) {
-      const SubDev& d = h->h_sub[k];
-      for (int a = 0; a < d.nI; ++a) {
-        goff[d.rI_off + a] = d.g_off + (long long)a * d.nP;
-        np[d.rI_off + a] = d.nP;
-        poff[d.rI_off + a] = d.prim_off;
-      }
-    }
-    h->slot_goff.upload(goff, s);
-    h->slot_np.upload(np, s);
-    h->slot_poff.upload(poff, s);
-  }
   h->lam.upload(lam, s);
   h->scoef_ptr.upload(scoef_ptr, s);
   h->scoef_src.upload(scoef_src, s);
   h->pcon_ptr.upload(pcon_ptr, s);
-  h->pcon_src.upload(pcon_src, s);
-  // raw values
+  h->pcon_sub.upload(pcon_sub, s);
+  h->pcon_q.upload(pcon_q, s);
+  h->d_loopwork.upload(loopwork, s);
+  h->sub_cta0.upload(sub_cta0, s);
+  h->sub_ncta.upload(sub_ncta, s);
   std::vector<double> kvals(kv), fvals(fv);
   for (int k = 0; k < ns; ++k) {
     std::copy(h->in[k].val.begin(), h->in[k].val.end(), kvals.begin() + h->kval_off[k]);
@@ -815,26 +844,22 @@ void analyze_all(ietidp_s* h) {
   }
   h->kval.upload(kvals, s);
   h->fval.upload(fvals, s);
-  // numeric buffers
   const int nc = nrhs;
   h->pool.alloc(P.pool_doubles);
   h->dinv.alloc(P.dinv_doubles);
-  h->vecw.alloc((size_t)P.vec_doubles * std::max(P.ncx, 1));
-  h->X0.alloc((size_t)xo * P.ncx);
-  h->X.alloc((size_t)xo * P.ncx);
+  h->ipool.alloc(P.inv_doubles);
+  h->tpool.alloc(P.inv_doubles);
+  h->vecw.alloc((size_t)P.vec_rows * 16);  // sweeps use up to 16 interleaved columns
+  h->Xf.alloc((size_t)xo * nc);
   h->Xr.alloc((size_t)xo * nc);
-  h->kpp.alloc(kppo);
-  h->jp.alloc((size_t)po * nc);
-  h->G.alloc(go);
-  h->sloc.alloc(slo);
-  h->floc.alloc((size_t)po * nc);
   h->S.alloc((size_t)ng * ng);
   h->Sinv.alloc((size_t)ng * ng);
   h->ftil.alloc((size_t)ng * nc);
   h->zc0.alloc((size_t)ng * nc);
   h->err_flag.alloc(4);
   h->tiles.alloc(to);
-  h->dtiles.alloc(dto);
+  h->itiles.alloc(to);
+  h->lpi.alloc(lpio);
   h->delta.alloc(h->n_slots);
   h->kdiag.alloc(h->n_slots);
   const size_t m = (size_t)h->n_lambda * nc;
@@ -844,11 +869,12 @@ void analyze_all(ietidp_s* h) {
   h->p_vec.alloc(m);
   h->q_vec.alloc(m);
   h->z_vec.alloc(m);
-  h->e_vec.alloc(m);
+  h->yI.alloc((size_t)h->n_slots * nc);
   h->xI.alloc((size_t)h->n_slots * nc);
+  h->sI.alloc((size_t)h->n_slots * nc);
   h->zI.alloc((size_t)h->n_slots * nc);
-  h->gk.alloc((size_t)po * nc);
-  h->zc.alloc((size_t)ng * nc);
+  h->gpart.alloc((size_t)std::max(cta, 1) * std::max(P.nPmax, 1) * nc);
+  h->zc.alloc((size_t)std::max(ng, 1) * nc);
   h->partial.alloc(4 * 1024 * (size_t)nc);
   h->state.alloc(16 * IETIDP_MAX_RHS + 64);
   h->tmp_in.alloc(m);
@@ -856,9 +882,7 @@ void analyze_all(ietidp_s* h) {
   h->U.alloc(uo);
   IETI_CUDA(cudaStreamSynchronize(s));
   auto t2 = std::chrono::steady_clock::now();
-
   h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t2 - t0).count();
-  (void)t1;
 }
 
 }  // namespace ieti

@@ -211,6 +211,78 @@ __global__ void __launch_bounds__(128) k_panel_gemm(const Work* __restrict__ wor
       }
 }
 
+// General batched tile GEMM (DMMA): C = (+/-) A * B (+ C) on one <= TB x TB tile
+// per CTA, K looped in TB chunks; column-major operands in three base arrays
+// (GemmWork). Used for the partitioned inverse L11^-1 (recursive doubling).
+template <int NEG_BIT_UNUSED>
+__global__ void __launch_bounds__(128) k_tgemm(const GemmWork* __restrict__ work, const double* __restrict__ Ab,
+                                               const double* __restrict__ Bb, double* __restrict__ Cb) {
+  extern __shared__ double sm[];
+  double* As = sm;            // [k][r], stride KS
+  double* Bs = sm + TB * KS;  // [k][c], stride KS
+  const GemmWork w = work[blockIdx.x];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int g = lane >> 2, t = lane & 3;
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  for (int kk = 0; kk < w.kdim; kk += TB) {
+    const int kb = min(TB, w.kdim - kk);
+    __syncthreads();
+    for (int e = tid; e < TB * TB; e += 128) {
+      const int k = e / TB, r = e % TB;  // A column k contiguous in r
+      As[k * KS + r] = (k < kb && r < w.m) ? Ab[w.a_off + (long long)(kk + k) * w.lda + r] : 0.0;
+    }
+    for (int e = tid; e < TB * TB; e += 128) {
+      const int c = e / TB, k = e % TB;  // B column c contiguous in k
+      Bs[k * KS + c] = (k < kb && c < w.n) ? Bb[w.b_off + (long long)c * w.ldb + kk + k] : 0.0;
+    }
+    __syncthreads();
+    const int kend = (kb + 3) & ~3;
+    for (int k0 = 0; k0 < kend; k0 += 4) {
+      double a[4], bb[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[(k0 + t) * KS + wm + i * 8 + g];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bb[j] = Bs[(k0 + t) * KS + wn + j * 8 + g];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+    }
+  }
+  const double sgn = (w.mode & 1) ? -1.0 : 1.0;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + q;
+        if (r < w.m && c < w.n) {
+          double* C = Cb + w.c_off + (long long)c * w.ldc + r;
+          *C = (w.mode & 2) ? *C + sgn * acc[i][j][q] : sgn * acc[i][j][q];
+        }
+      }
+}
+
+// Diagonal TB-blocks of L11^-1 are the Dinv blocks of the panels.
+__global__ void k_inv_copy(const Work* __restrict__ work, const SnDev* __restrict__ sn, const double* __restrict__ dinv,
+                           double* __restrict__ ipool) {
+  const Work w = work[blockIdx.x];
+  const SnDev s = sn[w.sn];
+  const int p0 = w.a * TB, b = min(TB, s.npiv - p0);
+  const double* D = dinv + s.dinv_off + (long long)w.a * TILE_ELEMS;
+  double* I = ipool + s.inv_off + (long long)p0 * s.ldi + p0;
+  for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
+    const int c = e / TB, r = e % TB;
+    if (r < b && c < b) I[(long long)c * s.ldi + r] = D[e];
+  }
+}
+
 static void set_smem(const void* f, int bytes) {
   IETI_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
@@ -225,6 +297,7 @@ void run_factor(ietidp_s* h) {
     set_smem((const void*)k_potrf, sm_potrf);
     set_smem((const void*)k_panel_gemm<0>, sm_gemm);
     set_smem((const void*)k_panel_gemm<1>, sm_gemm);
+    set_smem((const void*)k_tgemm<0>, sm_gemm);
     attr = true;
   }
   static const int init_flags[2] = {INT_MAX, 1};  // failing subdomain (min), coarse OK
@@ -260,6 +333,19 @@ void run_factor(ietidp_s* h) {
         IETI_LAUNCHED(h);
       }
     }
+  }
+  // partitioned inverse L11^-1 of every factored supernode (all at once)
+  if (P.inv_copy_n) {
+    k_inv_copy<<<P.inv_copy_n, 256, 0, st>>>(W + P.inv_copy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
+    IETI_LAUNCHED(h);
+  }
+  for (size_t r = 0; r < P.inv_rounds.size(); ++r) {
+    const auto& rg = P.inv_rounds[r];
+    if (!rg.second) continue;
+    const bool step1 = (r % 2) == 0;
+    k_tgemm<0><<<rg.second, 128, sm_gemm, st>>>(h->d_gwork.p + rg.first, step1 ? h->pool.p : h->ipool.p,
+                                                step1 ? h->ipool.p : h->tpool.p, step1 ? h->tpool.p : h->ipool.p);
+    IETI_LAUNCHED(h);
   }
   IETI_CHECK_LAUNCH();
 }

@@ -70,59 +70,54 @@ struct ietidp_s {
   ieti::DevBuf<double> kval, fval;
   std::vector<long long> kval_off, fval_off;
   // ---- scatter lists: dst offset <- src index ----
-  ieti::DevBuf<long long> sc_front_dst;   // K_rr lower -> fronts pool (sorted by level)
+  ieti::DevBuf<long long> sc_front_dst;   // K lower (r and P positions) -> fronts pool, by level
   ieti::DevBuf<int> sc_front_src;
-  ieti::DevBuf<long long> sc_x0_dst;      // K_rP -> X0 (row-major nr x ncx)
-  ieti::DevBuf<int> sc_x0_src;
-  ieti::DevBuf<long long> sc_kpp_dst;     // K_PP -> kpp
-  ieti::DevBuf<int> sc_kpp_src;
-  ieti::DevBuf<long long> sc_fx_dst;      // f -> X0 (j_r columns)
+  ieti::DevBuf<long long> sc_fx_dst;      // f -> X (every non-tree DOF)
   ieti::DevBuf<int> sc_fx_src;
-  ieti::DevBuf<long long> sc_fp_dst;      // f -> jp
-  ieti::DevBuf<int> sc_fp_src;
   ieti::DevBuf<int> kdiag_src;            // K value index of the diagonal at each r_I slot
   // ---- symbolic structures ----
   ieti::DevBuf<ieti::SnDev> d_sn;
   ieti::DevBuf<ieti::SubDev> d_sub;
   std::vector<ieti::SubDev> h_sub;
   ieti::DevBuf<int> d_rows, d_rel, d_children, d_work, d_level_sn;
-  ieti::DevBuf<int> d_perm;               // r position -> local DOF (per subdomain)
-  ieti::DevBuf<int> d_prim_dof, d_prim_gid;
+  ieti::DevBuf<ieti::GemmWork> d_gwork;
+  ieti::DevBuf<int> d_perm;               // position -> local DOF (per subdomain, ne entries)
+  ieti::DevBuf<int> d_prim_gid;           // per primal row (prim_off + q): global primal id
+  ieti::DevBuf<long long> d_uoff;
+  std::vector<long long> u_off;
   // ---- numeric ----
-  ieti::DevBuf<double> pool, dinv, vecw;  // fronts, inverted diagonal blocks, sweep workspace
-  ieti::DevBuf<double> X0, X, Xr;         // sweep RHS/solutions (coarse set-up, recovery)
-  ieti::DevBuf<double> kpp, jp, G, sloc, floc;
+  ieti::DevBuf<double> pool, dinv, ipool, tpool, vecw;  // fronts, Dinv blocks, L11^-1, temp, sweep workspace
+  ieti::DevBuf<double> Xf, Xr;            // forward-swept loads (kept) / recovery sweep (ne rows x nrhs)
   ieti::DevBuf<double> S, Sinv, ftil, zc0;  // coarse: S_PP, S_PP^-1, ftilde, S^-1 ftilde
-  ieti::DevBuf<int> scoef_ptr, scoef_src; // S_PP entry <- sloc entries
-  ieti::DevBuf<int> pcon_ptr, pcon_src;   // global primal <- primal rows
-  ieti::DevBuf<int> err_flag;             // min failing subdomain (INT_MAX: none)
+  ieti::DevBuf<long long> scoef_src;      // S_PP entry <- P-front pool offsets
+  ieti::DevBuf<int> scoef_ptr;
+  ieti::DevBuf<int> pcon_ptr, pcon_sub, pcon_q;  // global primal <- (subdomain, local primal)
+  ieti::DevBuf<int> err_flag;             // [0] min failing subdomain (INT_MAX: none), [1] coarse ok
   // ---- loop ----
-  ieti::DevBuf<double> tiles, dtiles;     // packed L_II tiles and Dinv_II tiles
+  ieti::DevBuf<double> tiles, itiles, lpi;  // packed L_II, L_II^-1 tiles; L_PI
+  ieti::DevBuf<ieti::LoopWork> d_loopwork;
+  int n_loopwork = 0;
+  ieti::DevBuf<int> sub_cta0, sub_ncta;   // loop CTAs of each subdomain
   ieti::DevBuf<ieti::LamDev> lam;
-  ieti::DevBuf<int> slot_lam, slot_sub;   // per r_I slot: multiplier, subdomain
+  ieti::DevBuf<int> slot_lam;             // per r_I slot: multiplier
   ieti::DevBuf<float> slot_sign;
-  ieti::DevBuf<long long> slot_goff;      // per r_I slot: its row of G_k in the G pool
-  ieti::DevBuf<int> slot_np, slot_poff;   // per r_I slot: n_P of its subdomain, primal-row offset
   ieti::DevBuf<double> delta, kdiag;      // scaling weights per slot, K diagonal per slot
-  ieti::DevBuf<double> d_vec, lam_vec, r_vec, p_vec, q_vec, z_vec, xI, zI, gk, zc, e_vec;
+  ieti::DevBuf<double> d_vec, lam_vec, r_vec, p_vec, q_vec, z_vec;
+  ieti::DevBuf<double> yI, xI, sI, zI;    // per-slot vectors (sum n_I x ncols)
+  ieti::DevBuf<double> gpart, zc;         // coarse partials per loop CTA; coarse solution
   ieti::DevBuf<double> partial;           // per-block dot partials
   ieti::DevBuf<double> state;             // PCG scalars (see pcg.cu)
   ieti::DevBuf<double> tmp_in, tmp_out;   // col-major <-> interleaved staging
   ieti::DevBuf<double> U;                 // subdomain solutions u^(k), n_k x nrhs col-major
-  std::vector<long long> u_off;
-  ieti::DevBuf<long long> d_uoff;
   int n_slots = 0, sum_nP = 0;
-  // CUDA graph of one PCG iteration (while-conditional), built lazily
+  // CUDA graph of the PCG loop (while-conditional), built lazily
   void* graph_exec = nullptr;
   void* graph = nullptr;
-  int graph_ncols = 0;
   unsigned long long cond_handle = 0;
-  ieti::DevBuf<ieti::Work> dummy_;
 };
 
 // Device-side entry points implemented in the .cu files (host launchers).
 namespace ieti {
-void upload_plan(ietidp_s* h);                 // analyze.cpp -> device buffers
 void run_factor(ietidp_s* h);                  // factor.cu
 void run_coarse(ietidp_s* h);                  // coarse.cu
 void run_solve(ietidp_s* h);                   // pcg.cu

@@ -7,66 +7,73 @@
 
 #include "../../include/ietidp.h"
 
-#ifdef __CUDACC__
-#define IETI_HD __host__ __device__
-#else
-#define IETI_HD
-#endif
-
 namespace ieti {
 
-constexpr int TB = 64;            // panel width of the supernodal Cholesky = loop tile size
+constexpr int TB = 64;  // panel width of the supernodal Cholesky = tile size everywhere
 constexpr int TILE_ELEMS = TB * TB;
 
 // ---------------------------------------------------------------------------
 // Device descriptors (plain structs, copied to the device as arrays)
 // ---------------------------------------------------------------------------
 
-// One supernode (front) of one subdomain's K_rr.
-// The front is an f x f column-major block (leading dimension ld) in the fronts
-// pool; its first npiv columns hold [L11; L21] after the partial factorisation,
-// its trailing (f-npiv)^2 block the update (Schur) matrix passed to the parent.
+// One supernode (front) of one subdomain.
+// Local positions of a subdomain: [0, nV) r_V in nested-dissection order,
+// [nV, nr) r_I, [nr, ne) the primal DOFs (P).  The front is an f x f
+// column-major block (leading dimension ld) in the fronts pool; after the
+// partial factorisation its first npiv columns hold [L11; L21] and the trailing
+// block the update matrix for the parent. The P supernode ("coarse", one per
+// subdomain with primal DOFs) is assembled but never factored: its front ends up
+// holding S_loc = K_PP - K_Pr K_rr^-1 K_rP (SPD sign).
 struct SnDev {
-  long long front_off;  // into the fronts pool (doubles)
-  long long dinv_off;   // into the Dinv pool: ceil(npiv/TB) tiles of TB x TB (col-major)
-  long long vec_off;    // into the sweep vector workspace: f x ncols_max (row-major)
+  long long front_off;  // fronts pool (doubles)
+  long long dinv_off;   // inverted diagonal TB-blocks: ceil(npiv/TB) tiles (col-major)
+  long long inv_off;    // partitioned inverse L11^-1 (npiv x npiv col-major, ld = ldi)
+  long long vec_off;    // sweep vector workspace (rows; x ncols at run time)
   int f, ld, npiv, c0;  // front size, leading dim, #pivots, first pivot position
+  int ldi, coarse;      // leading dim of L11^-1; 1 = P supernode (not factored)
   int sub, parent;      // subdomain, parent supernode (-1: root)
-  int rows_off;         // rows[rows_off .. +f-npiv): positions (in the subdomain's r order)
-  int rel_off;          // rel[rel_off .. +f-npiv): local row index of each update row in the parent front
-  int child_off, nchild;// children[child_off .. +nchild)
+  int rows_off;         // rows[rows_off .. +f-npiv): positions of the update rows
+  int rel_off;          // rel[rel_off .. +f-npiv): row index of each update row in the parent front
+  int child_off, nchild;
 };
 
 // Per-subdomain descriptor.
 struct SubDev {
-  int nk, nr, nI, nV, nP;     // local DOFs, remaining, interface-remaining, interior, primal
-  int root;                   // supernode holding r_I (-1 if nI == 0)
-  long long x_off;            // sweep matrix X: nr x ncx (row-major, ncx = nPmax + nrhs)
-  long long rI_off;           // offset in the concatenated r_I slot arrays
-  long long kval_off, f_off;  // raw CSR values / raw loads (nk x nrhs col-major)
-  long long kpp_off;          // dense K_PP^(k): nP x nP
-  long long jp_off;           // j_P^(k): nP x nrhs (row-major)
-  long long g_off;            // G_k = X_k[r_I, P]: nI x nP (row-major)
-  long long sloc_off;         // local coarse block nP x nP
-  long long floc_off;         // local coarse rhs  nP x nrhs
-  long long gk_off;           // per-iteration G_k^T b: nP x ncols
-  long long tile_off;         // packed L_II tiles (row-block order, TB x TB row-major)
-  long long dtile_off;        // packed Dinv_II tiles (TB x TB row-major), one per block row
-  int prim_off;               // into prim_gid / prim_dof arrays
-  int perm_off;               // perm[perm_off .. +nr): r position -> local DOF
-  int nt;                     // ceil(nI / TB)
+  int nk, nr, nI, nV, nP, ne;  // local DOFs, remaining, r_I, r_V, primal, nr + nP
+  int root, pnode;             // r_I supernode, P supernode (-1 if absent)
+  long long x_off;             // first row of the subdomain in the sweep matrices (ne rows)
+  long long rI_off;            // offset in the concatenated r_I slot arrays
+  long long kval_off, f_off;   // raw CSR values / raw loads (nk x nrhs col-major)
+  long long lpi_off;           // L_PI packed row-major nP x nI (zeros where not coupled)
+  long long tile_off;          // packed L_II tiles (row-block order, TB x TB row-major)
+  long long itile_off;         // packed L_II^-1 tiles (same layout)
+  int prim_off, perm_off, nt, cta0;  // primal rows, perm, #tile blocks, first loop CTA
+};
+
+// One multiplier's two B entries (every row is {+1, -1} in two subdomains).
+struct LamDev {
+  int slot[2];    // positions in the concatenated r_I storage
+  float sign[2];  // +1 / -1
+};
+
+// Work item for the factorisation kernels (k_potrf / k_panel_gemm / extend-add).
+struct Work {
+  int sn, a, b;
+};
+
+// Work item of the general batched tile GEMM:
+// C(m x n tile) = (+/-) A(m x K) B(K x n) (+ C), column-major operands,
+// A[r][k] = A_base[a_off + k*lda + r], B[k][c] = B_base[b_off + c*ldb + k].
+struct GemmWork {
+  long long c_off, a_off, b_off;
+  int lda, ldb, ldc, m, n, kdim;
+  int mode;  // bit0: negate, bit1: accumulate into C
   int pad_;
 };
 
-// One multiplier's two B entries (F3: every row is {+1, -1} in two subdomains).
-struct LamDev {
-  int slot[2];     // positions in the concatenated r_I storage
-  float sign[2];   // +1 / -1
-};
-
-// Work item for the tiled factorisation kernels.
-struct Work {
-  int sn, a, b;
+// A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).
+struct LoopWork {
+  int sub, nblk, blk0, blk1;
 };
 
 // ---------------------------------------------------------------------------
@@ -86,40 +93,45 @@ struct SubIn {
 };
 
 struct SnHost {
-  int sub, c0, npiv, f, parent, level;
+  int sub, c0, npiv, f, parent, level, coarse;
   std::vector<int> rows;
   std::vector<int> children;
 };
 
 struct SubPlan {
   int nr = 0, nI = 0, nV = 0, nP = 0;
-  std::vector<int> perm;     // r position -> local DOF
-  std::vector<int> pos;      // local DOF -> r position (-1 tree, -1 primal)
-  std::vector<int> ploc;     // local DOF -> primal local index (-1 otherwise)
-  std::vector<int> sn_begin; // supernode ids of this subdomain [first, last)
-  int root = -1;
+  std::vector<int> perm;      // position -> local DOF (ne = nr + nP entries)
+  std::vector<int> pos;       // local DOF -> position (-1 for tree DOFs)
+  std::vector<int> sn_begin;  // supernode ids of this subdomain [first, last)
+  int root = -1, pnode = -1;
 };
 
-// A launch of the factorisation for one level (host plan, device work lists).
+// Launch ranges of one elimination level.
 struct LevelPlan {
-  long long front_begin = 0, front_end = 0;   // pool range zeroed before assembly
-  long long scat_begin = 0, scat_end = 0;     // entries of the K scatter list
-  std::vector<std::pair<int, int>> ea;        // extend-add launches: (work offset, count), one per child slot
+  long long front_begin = 0, front_end = 0;  // pool range zeroed before assembly
+  long long scat_begin = 0, scat_end = 0;    // entries of the K scatter list
+  std::vector<std::pair<int, int>> ea;       // extend-add launches (work offset, count), one per child slot
   struct Panel {
     int potrf_off, potrf_n, trsm_off, trsm_n, upd_off, upd_n;
   };
   std::vector<Panel> panels;
-  int sn_off = 0, sn_n = 0;                   // supernodes of this level (in level_sn list)
+  int sn_off = 0, sn_n = 0;                  // supernodes of this level (level_sn list)
+  int fs_off = 0, fs_n = 0;                  // forward sweep: solve items (sn, row tile)
+  int fu_off = 0, fu_n = 0;                  // forward sweep: update items (sn, update-row tile)
+  int bt_off = 0, bt_n = 0;                  // backward sweep: t items (sn, pivot col tile), nupd > 0
+  int bx_off = 0, bx_n = 0;                  // backward sweep: x items (sn, pivot col tile)
 };
 
 struct Plan {
   std::vector<SubPlan> subs;
-  std::vector<SnHost> sn;        // all supernodes, global ids
-  std::vector<int> level_sn;     // supernode ids grouped by level
+  std::vector<SnHost> sn;     // all supernodes, global ids
+  std::vector<int> level_sn;  // supernode ids grouped by level
   std::vector<LevelPlan> levels;
-  long long pool_doubles = 0, dinv_doubles = 0, vec_doubles = 0;
-  int max_level = 0, max_front = 0, max_nI = 0, nPmax = 0, ncx = 0;
-  long long nnz_L = 0, flops = 0;
+  std::vector<std::pair<int, int>> inv_rounds;  // GemmWork ranges: (offset, count), 2 per round
+  int inv_copy_off = 0, inv_copy_n = 0;         // Work items (sn, panel) copying Dinv into L11^-1
+  long long pool_doubles = 0, dinv_doubles = 0, inv_doubles = 0, vec_rows = 0;
+  int max_level = 0, max_front = 0, max_nI = 0, nPmax = 0;
+  long long nnz_L = 0, flops = 0, inv_flops = 0;
 };
 
 }  // namespace ieti

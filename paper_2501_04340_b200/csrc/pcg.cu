@@ -1,18 +1,26 @@
 // The PCG loop on F_DP lambda = d_DP.
 //
-// Per iteration (all on device, one CUDA-graph while-loop, no host sync):
-//   k_local<SOLVE>  per subdomain: b = B_I^T p (gather), g_k = G_k^T b,
-//                   x = L_II^-T L_II^-1 b (tile-streamed, inverted diagonal tiles)
-//   k_coarse        g = sum_k C_k g_k, z = S_PP^-1 g            (one CTA)
-//   k_bgather       q = sum_k B_I (x_k + G_k C_k^T z), partial p.q
-//   k_cg_alpha      alpha, lambda += alpha p, r -= alpha q, partial r.r
-//   k_local<PREC>   b = B_D^T r, z_loc = L_II (L_II^T b)        (F2)
-//   k_bgather       z = sum_k B_D z_loc, partial r.z
-//   k_cg_beta       beta, p = z + beta p
-//   k_ctl           iteration counts, stop test, graph condition
-// Vectors are interleaved: v[j * ncols + c]. Dot products are fixed-order
-// two-stage reductions (per-block partials, reduced redundantly by consumers),
-// so results are bit-reproducible run to run.
+// With the P (primal) DOFs ordered after r_I, the local
+// and coarse parts of F_DP only need the trailing blocks L_II and L_PI:
+//   G_k^T b = L_PI L_II^-1 b,   G_k z = L_II^-T L_PI^T z        (F2')
+// so   F_DP p = sum_k B_I L_II^-T ( L_II^-1 b_k + L_PI^T C_k z ),
+//      z = S_PP^-1 sum_k C_k^T L_PI L_II^-1 b_k,   b_k = B_I^(k)T p.
+// Per iteration (one CUDA-graph while-loop, no host sync):
+//   k_tmv<FWD>   y_k = L_II^-1 b_k (tiles of the stored inverse), g partials
+//   k_coarse     z = S_PP^-1 g                                  (one CTA)
+//   k_tmv<BWD>   x_k = L_II^-T (y_k + L_PI^T z_k)
+//   k_bgather    q = sum_k B x_k, partial p.q
+//   k_cg_alpha   alpha; lambda += alpha p; r -= alpha q; partial r.r
+//   k_tmv<PRE1>  s_k = L_II^T B_D^(k)T r
+//   k_tmv<PRE2>  z_k = L_II s_k
+//   k_bgather    z = sum_k B_D z_k, partial r.z
+//   k_cg_beta    beta; p = z + beta p
+//   k_ctl        iteration counts, stop test, graph condition
+// Each k_tmv CTA owns one subdomain's block pair (i, nt-1-i) of output rows
+// (FWD, PRE2: block rows of a lower triangle) or columns (BWD, PRE1), streams
+// its tiles through a cp.async ring and writes finished blocks: no reductions
+// across CTAs. Vectors are interleaved v[j * ncols + c]; dot products are
+// fixed-order two-stage reductions (bit-reproducible run to run).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -35,138 +43,118 @@ struct PcgState {
 constexpr int NBLK = 296;  // blocks of the vector kernels = 2 x 148 SMs
 constexpr int VT = 256;    // threads of the vector kernels
 
-// ---------------------------------------------------------------------------
-// Per-subdomain tile-streamed kernel
-// ---------------------------------------------------------------------------
-enum StepKind { ACC_N = 0, ACC_T = 1, DIAG_N = 2, DIAG_T = 3, LAST_N = 4, LAST_T = 5 };
+enum TmvMode { FWD = 0, BWD = 1, PRE1 = 2, PRE2 = 3 };
 
-struct Step {
-  int src;   // >= 0: tile index into tiles; < 0: -1-index into dtiles
-  short kind, blk;  // blk: input vector block (ACC), or the finalised block
-};
-
-constexpr int MAX_STEPS = 2 * (32 * 33 / 2 + 32);
-
-__device__ __forceinline__ void load_tile_async(double* dst, const double* src, int tid, int nthreads) {
-  for (int q = tid; q < TB * TB / 2; q += nthreads) {
+__device__ __forceinline__ void load_tile_async(double* dst, const double* src, int tid) {
+#pragma unroll 4
+  for (int q = tid; q < TB * TB / 2; q += 256) {
     const int r = q >> 5, c = q & 31;
     cp_async16(dst + r * TB + ((c ^ (r & 7)) << 1), src + r * TB + 2 * c);
   }
 }
 
-// MODE 0: x = L^-T L^-1 b (F-apply local part), also g_k = G_k^T b.
-// MODE 1: z = L L^T b (Dirichlet preconditioner local part).
-// NCP = 1: DFMA path (warp owns 8 rows, lanes split columns);
-// NCP = 8/16: DMMA path (warp owns 8 output rows, NCP/8 column blocks).
-template <int MODE, int NCP, int STAGES>
-__global__ void __launch_bounds__(256, 1)
-    k_local(const SubDev* __restrict__ sub, const double* __restrict__ tiles, const double* __restrict__ dtiles,
-            const double* __restrict__ G, const int* __restrict__ slot_lam, const float* __restrict__ slot_sign,
-            const double* __restrict__ weight, const double* __restrict__ vin, double* __restrict__ vout,
-            double* __restrict__ gk, int ncols, int c_off, const PcgState* __restrict__ st,
-            const double* __restrict__ rr_part, int check) {
-  extern __shared__ __align__(16) double smem[];
-  constexpr int VS = (NCP == 1) ? 1 : NCP + 4;
-  __shared__ Step steps[MAX_STEPS];
-  __shared__ int nsteps_s;
-  __shared__ double red[8][TB];
-  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int ncl = min(NCP, ncols - c_off);  // columns handled by this launch
+struct TmvArgs {
+  const LoopWork* work;
+  const SubDev* sub;
+  const double* tiles;     // L_II tiles (PRE1/PRE2) or L_II^-1 tiles (FWD/BWD)
+  const double* lpi;       // L_PI (nP x nI row-major)
+  const int* slot_lam;
+  const float* slot_sign;
+  const int* prim_gid;
+  const double* weight;    // PRE1: scaling weights per slot (nullable)
+  const double* vin;       // FWD/PRE1: lambda-space vector; BWD: y (slots); PRE2: s (slots)
+  const double* z;         // BWD: coarse solution (n_primal x ncols) or null
+  double zsign;
+  double* vout;            // slot vector
+  double* gpart;           // FWD: coarse partials [cta][nPmax][ncols] (nullable)
+  int nPmax, ncols, c_off;
+  const PcgState* st;
+  const double* rr_part;   // PRE1 inside the loop: convergence test
+  int check;
+};
 
-  if (st) {
-    if (st->done) return;
-    if (MODE == 1 && check && !st->fixed) {
-      // convergence of the columns after this iteration's r update (any active?)
-      __shared__ int any_s;
+template <int MODE, int NCP, int STAGES>
+__global__ void __launch_bounds__(256, 1) k_tmv(const TmvArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  constexpr bool TRANS = (MODE == BWD || MODE == PRE1);
+  constexpr int VS = (NCP == 1) ? 1 : NCP + 4;
+  constexpr int NB = (NCP == 1) ? 1 : NCP / 8;
+  __shared__ double red[8][TB];
+  __shared__ int any_s;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ncl = min(NCP, A.ncols - A.c_off);
+
+  if (A.st) {
+    if (A.st->done) return;
+    if (MODE == PRE1 && A.check && !A.st->fixed) {
       if (tid == 0) any_s = 0;
       __syncthreads();
-      if (tid < st->ncols && st->active[tid]) {
+      if (tid < A.st->ncols && A.st->active[tid]) {
         double s = 0.0;
-        for (int b = 0; b < NBLK; ++b) s += rr_part[b * st->ncols + tid];
-        if (!(sqrt(s) <= st->tol * st->r0[tid])) atomicOr(&any_s, 1);
+        for (int b = 0; b < NBLK; ++b) s += A.rr_part[b * A.st->ncols + tid];
+        if (!(sqrt(s) <= A.st->tol * A.st->r0[tid])) atomicOr(&any_s, 1);
       }
       __syncthreads();
       if (!any_s) return;
     }
   }
-  const SubDev d = sub[blockIdx.x];
-  if (d.nI == 0) return;
+  const LoopWork lw = A.work[blockIdx.x];
+  const SubDev d = A.sub[lw.sub];
   const int nt = d.nt;
+  const int ob[2] = {lw.blk0, lw.blk1};
+  const int nob = lw.nblk;
+  // input rows needed: N-op (FWD, PRE2) blocks [0, max ob], T-op (BWD, PRE1) blocks [min ob, nt)
+  const int bmin = min(ob[0], ob[nob - 1]), bmax = max(ob[0], ob[nob - 1]);
+  const int lo = TRANS ? bmin * TB : 0;
+  const int hi = TRANS ? nt * TB : (bmax + 1) * TB;
   double* ring = smem;
-  double* vec = smem + STAGES * TILE_ELEMS;
-  double* scratch = vec + nt * TB * VS;
+  double* vec = smem + STAGES * TILE_ELEMS;  // rows [lo, hi)
+  double* outb = vec + (hi - lo) * VS;       // one finished output block (FWD partials)
 
-  // ---- step list ----
-  if (tid == 0) {
-    int n = 0;
-    auto T = [](int i, int j) { return i * (i + 1) / 2 + j; };
-    const int tb = (int)(d.tile_off / TILE_ELEMS), db = (int)(d.dtile_off / TILE_ELEMS);
-    if (MODE == 0) {
-      for (int i = 0; i < nt; ++i) {
-        for (int j = 0; j < i; ++j) steps[n++] = {tb + T(i, j), ACC_N, (short)j};
-        steps[n++] = {-1 - (db + i), DIAG_N, (short)i};
-      }
-      for (int i = nt - 1; i >= 0; --i) {
-        for (int j = nt - 1; j > i; --j) steps[n++] = {tb + T(j, i), ACC_T, (short)j};
-        steps[n++] = {-1 - (db + i), DIAG_T, (short)i};
-      }
-    } else {
-      for (int j = 0; j < nt; ++j) {
-        for (int i = nt - 1; i > j; --i) steps[n++] = {tb + T(i, j), ACC_T, (short)i};
-        steps[n++] = {tb + T(j, j), LAST_T, (short)j};
-      }
-      for (int i = nt - 1; i >= 0; --i) {
-        for (int j = 0; j < i; ++j) steps[n++] = {tb + T(i, j), ACC_N, (short)j};
-        steps[n++] = {tb + T(i, i), LAST_N, (short)i};
-      }
-    }
-    nsteps_s = n;
-  }
-  // ---- gather b (with sign and weight) ----
-  const int nrow = nt * TB;
-  for (int e = tid; e < nrow * VS; e += 256) {
-    const int a = e / VS, c = e - a * VS;
+  // ---- input vector ----
+  for (int e = tid; e < (hi - lo) * VS; e += 256) {
+    const int a = lo + e / VS, c = e % VS;
     double v = 0.0;
     if (a < d.nI && c < ncl) {
-      const int slot = (int)d.rI_off + a;
-      const double w = weight ? weight[slot] : 1.0;
-      v = (double)slot_sign[slot] * w * vin[(long long)slot_lam[slot] * ncols + c_off + c];
+      const long long slot = d.rI_off + a;
+      if (MODE == FWD || MODE == PRE1) {
+        const double w = (MODE == PRE1 && A.weight) ? A.weight[slot] : 1.0;
+        v = (double)A.slot_sign[slot] * w * A.vin[(long long)A.slot_lam[slot] * A.ncols + A.c_off + c];
+      } else {
+        v = A.vin[slot * A.ncols + A.c_off + c];
+        if (MODE == BWD && A.z) {
+          const double* lp = A.lpi + d.lpi_off + a;
+          double s = 0.0;
+          for (int q = 0; q < d.nP; ++q)
+            s += lp[(long long)q * d.nI] * A.z[(long long)A.prim_gid[d.prim_off + q] * A.ncols + A.c_off + c];
+          v += A.zsign * s;
+        }
+      }
     }
     vec[e] = v;
   }
-  __syncthreads();
-  const int nsteps = nsteps_s;
-  // ---- prologue prefetch (overlaps with g_k below) ----
+  // ---- tile schedule: per output block o, N: (o, 0..o), T: (o..nt-1, o) ----
+  auto ntiles_of = [&](int o) { return TRANS ? nt - o : o + 1; };
+  const int n0 = ntiles_of(ob[0]);
+  const int nsteps = n0 + (nob == 2 ? ntiles_of(ob[1]) : 0);
+  auto tile_ptr = [&](int s) {
+    const int which = s < n0 ? 0 : 1;
+    const int o = ob[which], k = which ? s - n0 : s;
+    const int i = TRANS ? o + k : o, j = TRANS ? o : k;
+    return A.tiles + d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
+  };
 #pragma unroll
   for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nsteps) {
-      const Step sp = steps[s];
-      const double* src = sp.src >= 0 ? tiles + (long long)sp.src * TILE_ELEMS : dtiles + (long long)(-1 - sp.src) * TILE_ELEMS;
-      load_tile_async(ring + s * TILE_ELEMS, src, tid, 256);
-    }
+    if (s < nsteps) load_tile_async(ring + s * TILE_ELEMS, tile_ptr(s), tid);
     cp_async_commit();
   }
-  // ---- coarse: g_k = G_k^T b (MODE 0) ----
-  if (MODE == 0 && gk && d.nP > 0) {
-    const double* Gk = G + d.g_off;
-    for (int pc = warp; pc < d.nP * ncl; pc += 8) {
-      const int pi = pc / ncl, c = pc - pi * ncl;
-      double acc = 0.0;
-      for (int a = lane; a < d.nI; a += 32) acc += Gk[(long long)a * d.nP + pi] * vec[a * VS + c];
-      acc = warp_sum(acc);
-      if (lane == 0) gk[(long long)(d.prim_off + pi) * ncols + c_off + c] = acc;
-    }
-  }
-
-  // accumulators
-  double accN[8];   // DFMA: per-lane partial row sums (rows 8w+rr)
-  double accT[2];   // DFMA: per-warp partial column sums (cols lane, lane+32)
-  double acc[NCP == 1 ? 1 : NCP / 8][2];  // DMMA: rows 8w+g, cols nb*8+2t+q
+  double gacc = 0.0;  // FWD coarse partial of (q, c) = (tid / NCP, tid % NCP)
+  double accN[8], accT[2], acc[NB][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i) accN[i] = 0.0;
   accT[0] = accT[1] = 0.0;
 #pragma unroll
-  for (int i = 0; i < (NCP == 1 ? 1 : NCP / 8); ++i) acc[i][0] = acc[i][1] = 0.0;
+  for (int i = 0; i < NB; ++i) acc[i][0] = acc[i][1] = 0.0;
   const int g = lane >> 2, t4 = lane & 3;
 
   for (int s = 0; s < nsteps; ++s) {
@@ -174,41 +162,24 @@ __global__ void __launch_bounds__(256, 1)
     __syncthreads();
     {
       const int sn = s + STAGES - 1;
-      if (sn < nsteps) {
-        const Step sp = steps[sn];
-        const double* src = sp.src >= 0 ? tiles + (long long)sp.src * TILE_ELEMS : dtiles + (long long)(-1 - sp.src) * TILE_ELEMS;
-        load_tile_async(ring + (sn % STAGES) * TILE_ELEMS, src, tid, 256);
-      }
+      if (sn < nsteps) load_tile_async(ring + (sn % STAGES) * TILE_ELEMS, tile_ptr(sn), tid);
       cp_async_commit();
     }
     const double* Tt = ring + (s % STAGES) * TILE_ELEMS;
-    const Step sp = steps[s];
-    double* vb = vec + sp.blk * TB * VS;
+    const int which = s < n0 ? 0 : 1;
+    const int o = ob[which], k = which ? s - n0 : s;
+    const int inblk = TRANS ? o + k : k;  // input vector block
+    const double* vb = vec + (inblk * TB - lo) * VS;
+    const bool last = (k == ntiles_of(o) - 1);
     if constexpr (NCP == 1) {
-      // ------------------------- DFMA path -------------------------
-      if (sp.kind == ACC_N || sp.kind == LAST_N) {
+      if (!TRANS) {
         const double x0 = vb[lane], x1 = vb[lane + 32];
 #pragma unroll
         for (int rr = 0; rr < 8; ++rr) {
           const int r = warp * 8 + rr;
           accN[rr] += Tt[swz(r, lane)] * x0 + Tt[swz(r, lane + 32)] * x1;
         }
-        if (sp.kind == LAST_N) {
-          double full[8];
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) full[rr] = warp_sum(accN[rr]);
-          __syncthreads();
-          if (lane < 8) {
-            double v = full[0];
-#pragma unroll
-            for (int rr = 1; rr < 8; ++rr)
-              if (lane == rr) v = full[rr];
-            vb[warp * 8 + lane] = v;
-          }
-#pragma unroll
-          for (int rr = 0; rr < 8; ++rr) accN[rr] = 0.0;
-        }
-      } else if (sp.kind == ACC_T || sp.kind == LAST_T) {
+      } else {
 #pragma unroll
         for (int rr = 0; rr < 8; ++rr) {
           const int r = warp * 8 + rr;
@@ -216,7 +187,24 @@ __global__ void __launch_bounds__(256, 1)
           accT[0] += Tt[swz(r, lane)] * xr;
           accT[1] += Tt[swz(r, lane + 32)] * xr;
         }
-        if (sp.kind == LAST_T) {
+      }
+      if (last) {
+        // finished output block o -> outb (64 values)
+        if (!TRANS) {
+          double full[8];
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) full[rr] = warp_sum(accN[rr]);
+          if (lane < 8) {
+            double v = full[0];
+#pragma unroll
+            for (int rr = 1; rr < 8; ++rr)
+              if (lane == rr) v = full[rr];
+            outb[warp * 8 + lane] = v;
+          }
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) accN[rr] = 0.0;
+          __syncthreads();
+        } else {
           red[warp][lane] = accT[0];
           red[warp][lane + 32] = accT[1];
           __syncthreads();
@@ -224,122 +212,49 @@ __global__ void __launch_bounds__(256, 1)
             double v = 0.0;
 #pragma unroll
             for (int w = 0; w < 8; ++w) v += red[w][tid];
-            vb[tid] = v;
+            outb[tid] = v;
           }
           accT[0] = accT[1] = 0.0;
+          __syncthreads();
         }
-      } else if (sp.kind == DIAG_N) {
-        // t = b_i - sum_j L_ij y_j ; y_i = Dinv_i t
-        double full[8];
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) full[rr] = warp_sum(accN[rr]);
-        if (lane < 8) {
-          double v = full[0];
-#pragma unroll
-          for (int rr = 1; rr < 8; ++rr)
-            if (lane == rr) v = full[rr];
-          scratch[warp * 8 + lane] = vb[warp * 8 + lane] - v;
-        }
-        __syncthreads();
-        const double t0 = scratch[lane], t1 = scratch[lane + 32];
-        double y[8];
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-          const int r = warp * 8 + rr;
-          y[rr] = warp_sum(Tt[swz(r, lane)] * t0 + Tt[swz(r, lane + 32)] * t1);
-        }
-        if (lane < 8) {
-          double v = y[0];
-#pragma unroll
-          for (int rr = 1; rr < 8; ++rr)
-            if (lane == rr) v = y[rr];
-          vb[warp * 8 + lane] = v;
-        }
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) accN[rr] = 0.0;
-      } else {  // DIAG_T: t = y_i - sum_{j>i} L_ji^T x_j ; x_i = Dinv_i^T t
-        red[warp][lane] = accT[0];
-        red[warp][lane + 32] = accT[1];
-        __syncthreads();
-        if (tid < TB) {
-          double v = 0.0;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) v += red[w][tid];
-          scratch[tid] = vb[tid] - v;
-        }
-        __syncthreads();
-        double p0 = 0.0, p1 = 0.0;
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) {
-          const int r = warp * 8 + rr;
-          const double tr = scratch[r];
-          p0 += Tt[swz(r, lane)] * tr;
-          p1 += Tt[swz(r, lane + 32)] * tr;
-        }
-        red[warp][lane] = p0;
-        red[warp][lane + 32] = p1;
-        __syncthreads();
-        if (tid < TB) {
-          double v = 0.0;
-#pragma unroll
-          for (int w = 0; w < 8; ++w) v += red[w][tid];
-          vb[tid] = v;
-        }
-        accT[0] = accT[1] = 0.0;
       }
     } else {
-      // ------------------------- DMMA path -------------------------
-      constexpr int NB = NCP / 8;
-      const bool trans = (sp.kind == ACC_T || sp.kind == LAST_T);
-      if (sp.kind == ACC_N || sp.kind == ACC_T || sp.kind == LAST_N || sp.kind == LAST_T) {
 #pragma unroll 4
-        for (int k0 = 0; k0 < TB; k0 += 4) {
-          const double a = trans ? Tt[swz(k0 + t4, warp * 8 + g)] : Tt[swz(warp * 8 + g, k0 + t4)];
+      for (int k0 = 0; k0 < TB; k0 += 4) {
+        const double a = TRANS ? Tt[swz(k0 + t4, warp * 8 + g)] : Tt[swz(warp * 8 + g, k0 + t4)];
 #pragma unroll
-          for (int nb = 0; nb < NB; ++nb) dmma8x8x4(acc[nb][0], acc[nb][1], a, vb[(k0 + t4) * VS + nb * 8 + g]);
-        }
-        if (sp.kind == LAST_N || sp.kind == LAST_T) {
-          __syncthreads();
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb) {
-            vb[(warp * 8 + g) * VS + nb * 8 + 2 * t4] = acc[nb][0];
-            vb[(warp * 8 + g) * VS + nb * 8 + 2 * t4 + 1] = acc[nb][1];
-            acc[nb][0] = acc[nb][1] = 0.0;
-          }
-        }
-      } else {
-        // DIAG: t = v_i - acc -> scratch ; v_i = D t (N) or D^T t (T)
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int idx = (warp * 8 + g) * VS + nb * 8 + 2 * t4 + q;
-            scratch[idx] = vb[idx] - acc[nb][q];
-            acc[nb][q] = 0.0;
-          }
-        __syncthreads();
-        const bool tr = (sp.kind == DIAG_T);
-#pragma unroll 4
-        for (int k0 = 0; k0 < TB; k0 += 4) {
-          const double a = tr ? Tt[swz(k0 + t4, warp * 8 + g)] : Tt[swz(warp * 8 + g, k0 + t4)];
-#pragma unroll
-          for (int nb = 0; nb < NB; ++nb)
-            dmma8x8x4(acc[nb][0], acc[nb][1], a, scratch[(k0 + t4) * VS + nb * 8 + g]);
-        }
+        for (int nb = 0; nb < NB; ++nb) dmma8x8x4(acc[nb][0], acc[nb][1], a, vb[(k0 + t4) * VS + nb * 8 + g]);
+      }
+      if (last) {
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) {
-          vb[(warp * 8 + g) * VS + nb * 8 + 2 * t4] = acc[nb][0];
-          vb[(warp * 8 + g) * VS + nb * 8 + 2 * t4 + 1] = acc[nb][1];
+          outb[(warp * 8 + g) * VS + nb * 8 + 2 * t4] = acc[nb][0];
+          outb[(warp * 8 + g) * VS + nb * 8 + 2 * t4 + 1] = acc[nb][1];
           acc[nb][0] = acc[nb][1] = 0.0;
         }
+        __syncthreads();
       }
+    }
+    if (last) {
+      // write the finished block; FWD also accumulates the coarse partial L_PI y
+      for (int e = tid; e < TB * ncl; e += 256) {
+        const int r = e / ncl, c = e % ncl;
+        const int a = o * TB + r;
+        if (a < d.nI) A.vout[(d.rI_off + a) * A.ncols + A.c_off + c] = outb[r * VS + c];
+      }
+      if (MODE == FWD && A.gpart && tid < d.nP * NCP) {
+        const int q = tid / NCP, c = tid % NCP;
+        const double* lp = A.lpi + d.lpi_off + (long long)q * d.nI + o * TB;
+        const int na = min(TB, d.nI - o * TB);
+        for (int r = 0; r < na; ++r) gacc += lp[r] * outb[r * VS + c];
+      }
+      __syncthreads();
     }
   }
   cp_async_wait<0>();
-  __syncthreads();
-  for (int e = tid; e < d.nI * ncl; e += 256) {
-    const int a = e / ncl, c = e - a * ncl;
-    vout[(d.rI_off + a) * ncols + c_off + c] = vec[a * VS + c];
+  if (MODE == FWD && A.gpart && tid < d.nP * NCP) {
+    const int q = tid / NCP, c = tid % NCP;
+    if (c < ncl) A.gpart[((long long)blockIdx.x * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
   }
 }
 
@@ -352,8 +267,6 @@ __device__ __forceinline__ int pow2ge(int x) {
   return p;
 }
 
-// Block reduction of per-thread column partials (thread column c = tid % P2);
-// writes partial[blockIdx.x * ncols + c].
 __device__ void block_col_reduce(double v, int ncols, int P2, double* partial) {
   __shared__ double red[VT];
   const int tid = threadIdx.x;
@@ -366,14 +279,11 @@ __device__ void block_col_reduce(double v, int ncols, int P2, double* partial) {
   if (tid < ncols) partial[blockIdx.x * ncols + tid] = red[tid];
 }
 
-// out[j][c] = sum_{2 slots} sign * w * (x[slot][c] + coef * G_k[row] . z[C_k^T][c])
-template <bool COARSE>
+// out[j][c] = sum_{2 slots} sign * w * x[slot][c]   (+ partial dot with dotv)
 __global__ void __launch_bounds__(VT)
     k_bgather(int m, int ncols, const LamDev* __restrict__ lam, const double* __restrict__ x,
-              const double* __restrict__ weight, const long long* __restrict__ slot_goff,
-              const int* __restrict__ slot_np, const int* __restrict__ slot_poff, const double* __restrict__ G,
-              const int* __restrict__ prim_gid, const double* __restrict__ z, double coef, double* __restrict__ out,
-              const double* __restrict__ dotv, double* __restrict__ partial, const PcgState* __restrict__ st) {
+              const double* __restrict__ weight, double* __restrict__ out, const double* __restrict__ dotv,
+              double* __restrict__ partial, const PcgState* __restrict__ st) {
   if (st && st->done) return;
   const int P2 = pow2ge(ncols);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
@@ -385,16 +295,7 @@ __global__ void __launch_bounds__(VT)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int a = L.slot[q];
-        double xv = x[(long long)a * ncols + c];
-        if (COARSE) {
-          const int np = slot_np[a];
-          const double* Gr = G + slot_goff[a];
-          const int* gid = prim_gid + slot_poff[a];
-          double s = 0.0;
-          for (int p = 0; p < np; ++p) s += Gr[p] * z[gid[p] * ncols + c];
-          xv += coef * s;
-        }
-        val += (double)L.sign[q] * (weight ? weight[a] : 1.0) * xv;
+        val += (double)L.sign[q] * (weight ? weight[a] : 1.0) * x[(long long)a * ncols + c];
       }
       out[(long long)j * ncols + c] = val;
       if (dotv) dot += val * dotv[(long long)j * ncols + c];
@@ -403,17 +304,22 @@ __global__ void __launch_bounds__(VT)
   if (partial) block_col_reduce(dot, ncols, P2, partial);
 }
 
-// z = S^-1 (add + sum_k C_k g_k)  (one CTA)
+// z = S^-1 (add + sum_k C_k sum_{cta of k} gpart)   (one CTA)
 __global__ void __launch_bounds__(1024)
-    k_coarse(int ng, int ncols, const int* __restrict__ pcon_ptr, const int* __restrict__ pcon_src,
-             const double* __restrict__ gk, const double* __restrict__ add, const double* __restrict__ Sinv,
+    k_coarse(int ng, int ncols, int nPmax, const int* __restrict__ pcon_ptr, const int* __restrict__ pcon_sub,
+             const int* __restrict__ pcon_q, const int* __restrict__ sub_cta0, const int* __restrict__ sub_ncta,
+             const double* __restrict__ gpart, const double* __restrict__ add, const double* __restrict__ Sinv,
              double* __restrict__ z, const PcgState* __restrict__ st) {
   if (st && st->done) return;
   extern __shared__ double gs[];  // ng x ncols
   for (int e = threadIdx.x; e < ng * ncols; e += blockDim.x) {
     const int gi = e / ncols, c = e - gi * ncols;
     double s = add ? add[e] : 0.0;
-    for (int q = pcon_ptr[gi]; q < pcon_ptr[gi + 1]; ++q) s += gk[(long long)pcon_src[q] * ncols + c];
+    for (int q = pcon_ptr[gi]; q < pcon_ptr[gi + 1]; ++q) {
+      const int k = pcon_sub[q], lq = pcon_q[q];
+      for (int cta = sub_cta0[k]; cta < sub_cta0[k] + sub_ncta[k]; ++cta)
+        s += gpart[((long long)cta * nPmax + lq) * ncols + c];
+    }
     gs[e] = s;
   }
   __syncthreads();
@@ -428,7 +334,6 @@ __global__ void __launch_bounds__(1024)
 }
 
 __device__ void reduce_cols(const double* part, int nblk, int ncols, double* out_smem) {
-  // thread c < ncols sums column c in fixed order
   if (threadIdx.x < ncols) {
     double s = 0.0;
     for (int b = 0; b < nblk; ++b) s += part[b * ncols + threadIdx.x];
@@ -533,7 +438,6 @@ __global__ void k_ctl(PcgState* __restrict__ st, const double* __restrict__ rr_p
   }
 }
 
-// ---- initialisation ----
 __global__ void __launch_bounds__(VT) k_init(int m, int ncols, const double* __restrict__ d, double* __restrict__ lam,
                                              double* __restrict__ r, double* __restrict__ rr_part) {
   const int P2 = pow2ge(ncols);
@@ -612,75 +516,101 @@ __global__ void k_transpose(int rows, int ncols, const double* __restrict__ in, 
 // ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
-struct LocalCfg {
+struct TmvCfg {
   int ncp, stages, smem;
 };
 
-static LocalCfg local_cfg(const ietidp_s* h, int ncols) {
+static TmvCfg tmv_cfg(const ietidp_s* h, int ncols) {
   const int nt = (h->plan.max_nI + TB - 1) / TB;
-  LocalCfg c{};
-  if (ncols == 1) {
-    c.ncp = 1;
-    c.stages = 3;
-    c.smem = (c.stages * TILE_ELEMS + nt * TB * 1 + TB * 1) * 8;
-    return c;
-  }
-  const int ncps[2] = {16, 8};
-  for (int ncp : ncps) {
+  if (ncols == 1) return {1, 3, (3 * TILE_ELEMS + nt * TB + TB) * 8};
+  for (int ncp : {16, 8}) {
     if (ncp == 16 && ncols <= 8) continue;
     const int vs = ncp + 4;
     for (int stages = 3; stages >= 2; --stages) {
       int bytes = (stages * TILE_ELEMS + nt * TB * vs + TB * vs) * 8;
-      if (bytes <= 200 * 1024) return {ncp, stages, bytes};
+      if (bytes <= 210 * 1024) return {ncp, stages, bytes};
     }
   }
-  throw Error(IETIDP_E_ARG, "interface block too large for the shared-memory loop kernel");
+  throw Error(IETIDP_E_ARG, "interface block too large for the shared-memory loop kernels");
 }
 
 template <int MODE, int NCP, int STAGES>
-static void launch_local_t(ietidp_s* h, const LocalCfg& cfg, const double* weight, const double* vin, double* vout,
-                           double* gk, int ncols, int c_off, const PcgState* st, const double* rr_part, int check) {
-  auto kern = k_local<MODE, NCP, STAGES>;
+static void launch_tmv_t(ietidp_s* h, const TmvCfg& cfg, TmvArgs a) {
+  auto kern = k_tmv<MODE, NCP, STAGES>;
   IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
-  const double* tl = h->tiles.p;
-  kern<<<h->n_sub, 256, cfg.smem, h->stream>>>(h->d_sub.p, tl, h->dtiles.p, h->G.p, h->slot_lam.p, h->slot_sign.p,
-                                               weight, vin, vout, gk, ncols, c_off, st, rr_part, check);
+  kern<<<h->n_loopwork, 256, cfg.smem, h->stream>>>(a);
   IETI_LAUNCHED(h);
 }
 
 template <int MODE>
-static void launch_local(ietidp_s* h, const double* weight, const double* vin, double* vout, double* gk, int ncols,
-                         const PcgState* st, const double* rr_part, int check) {
-  const LocalCfg cfg = local_cfg(h, ncols);
-  for (int c0 = 0; c0 < ncols; c0 += cfg.ncp) {
-    if (cfg.ncp == 1) launch_local_t<MODE, 1, 3>(h, cfg, weight, vin, vout, gk, ncols, c0, st, rr_part, check);
-    else if (cfg.ncp == 16 && cfg.stages == 3) launch_local_t<MODE, 16, 3>(h, cfg, weight, vin, vout, gk, ncols, c0, st, rr_part, check);
-    else if (cfg.ncp == 16) launch_local_t<MODE, 16, 2>(h, cfg, weight, vin, vout, gk, ncols, c0, st, rr_part, check);
-    else if (cfg.stages == 3) launch_local_t<MODE, 8, 3>(h, cfg, weight, vin, vout, gk, ncols, c0, st, rr_part, check);
-    else launch_local_t<MODE, 8, 2>(h, cfg, weight, vin, vout, gk, ncols, c0, st, rr_part, check);
+static void launch_tmv(ietidp_s* h, TmvArgs a) {
+  if (h->n_loopwork == 0) return;
+  const TmvCfg cfg = tmv_cfg(h, a.ncols);
+  a.work = h->d_loopwork.p;
+  a.sub = h->d_sub.p;
+  a.tiles = (MODE == FWD || MODE == BWD) ? h->itiles.p : h->tiles.p;
+  a.lpi = h->lpi.p;
+  a.slot_lam = h->slot_lam.p;
+  a.slot_sign = h->slot_sign.p;
+  a.prim_gid = h->d_prim_gid.p;
+  a.nPmax = std::max(h->plan.nPmax, 1);
+  for (int c0 = 0; c0 < a.ncols; c0 += cfg.ncp) {
+    a.c_off = c0;
+    if (cfg.ncp == 1) launch_tmv_t<MODE, 1, 3>(h, cfg, a);
+    else if (cfg.ncp == 16 && cfg.stages == 3) launch_tmv_t<MODE, 16, 3>(h, cfg, a);
+    else if (cfg.ncp == 16) launch_tmv_t<MODE, 16, 2>(h, cfg, a);
+    else if (cfg.stages == 3) launch_tmv_t<MODE, 8, 3>(h, cfg, a);
+    else launch_tmv_t<MODE, 8, 2>(h, cfg, a);
   }
 }
 
-// out = sum_k B (x + coef G z) with optional weight; optional dot partials with dotv.
-static void bgather(ietidp_s* h, int ncols, const double* x, const double* weight, const double* z, double coef,
-                    double* out, const double* dotv, double* partial, const PcgState* st) {
+static int tmv_launches(const ietidp_s* h, int ncols) {
+  const TmvCfg cfg = tmv_cfg(h, ncols);
+  return (ncols + cfg.ncp - 1) / cfg.ncp;
+}
+
+// y_k = L_II^-1 B_I^T v (per slot) and the coarse partials L_PI y_k
+void loop_fwd(ietidp_s* h, int ncols, const double* v, double* y, bool partials, const void* stv) {
+  const PcgState* st = static_cast<const PcgState*>(stv);
+  TmvArgs a{};
+  a.vin = v;
+  a.vout = y;
+  a.gpart = (partials && h->n_primal) ? h->gpart.p : nullptr;
+  a.ncols = ncols;
+  a.st = st;
+  launch_tmv<FWD>(h, a);
+}
+// x_k = L_II^-T (y_k + zsign L_PI^T z_k)
+void loop_bwd(ietidp_s* h, int ncols, const double* y, const double* z, double zsign, double* x, const void* stv) {
+  const PcgState* st = static_cast<const PcgState*>(stv);
+  TmvArgs a{};
+  a.vin = y;
+  a.z = h->n_primal ? z : nullptr;
+  a.zsign = zsign;
+  a.vout = x;
+  a.ncols = ncols;
+  a.st = st;
+  launch_tmv<BWD>(h, a);
+}
+
+void bgather(ietidp_s* h, int ncols, const double* x, const double* weight, double* out, const double* dotv,
+             double* partial, const void* stv) {
+  const PcgState* st = static_cast<const PcgState*>(stv);
   if (h->n_lambda == 0) return;
-  const int grid = NBLK;
-  if (z && h->n_primal > 0)
-    k_bgather<true><<<grid, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, x, weight, h->slot_goff.p, h->slot_np.p, h->slot_poff.p,
-                                                h->G.p, h->d_prim_gid.p, z, coef, out, dotv, partial, st);
-  else
-    k_bgather<false><<<grid, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, x, weight, nullptr, nullptr, nullptr,
-                                                 nullptr, nullptr, nullptr, 0.0, out, dotv, partial, st);
+  k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, x, weight, out, dotv, partial, st);
   IETI_LAUNCHED(h);
 }
 
-static void coarse_apply(ietidp_s* h, int ncols, const double* gk, const double* add, double* z, const PcgState* st) {
+// z = S^-1 (add + sum of the coarse partials)
+void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const void* stv) {
+  const PcgState* st = static_cast<const PcgState*>(stv);
   if (h->n_primal == 0) return;
   const int smem = h->n_primal * ncols * 8;
   if (smem > 48 * 1024)
     IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
-  k_coarse<<<1, 1024, smem, h->stream>>>(h->n_primal, ncols, h->pcon_ptr.p, h->pcon_src.p, gk, add, h->Sinv.p, z, st);
+  k_coarse<<<1, 1024, smem, h->stream>>>(h->n_primal, ncols, std::max(h->plan.nPmax, 1), h->pcon_ptr.p,
+                                         h->pcon_sub.p, h->pcon_q.p, h->sub_cta0.p, h->sub_ncta.p, h->gpart.p, add,
+                                         h->Sinv.p, z, st);
   IETI_LAUNCHED(h);
 }
 
@@ -688,16 +618,32 @@ static void coarse_apply(ietidp_s* h, int ncols, const double* gk, const double*
 static void apply_F_inter(ietidp_s* h, int ncols, const double* x, double* y, const PcgState* st, const double* dotv,
                           double* partial) {
   if (h->n_lambda == 0) return;
-  launch_local<0>(h, nullptr, x, h->xI.p, h->n_primal ? h->gk.p : nullptr, ncols, st, nullptr, 0);
-  coarse_apply(h, ncols, h->gk.p, nullptr, h->zc.p, st);
-  bgather(h, ncols, h->xI.p, nullptr, h->n_primal ? h->zc.p : nullptr, 1.0, y, dotv, partial, st);
+  loop_fwd(h, ncols, x, h->yI.p, true, st);
+  coarse_apply(h, ncols, nullptr, h->zc.p, st);
+  loop_bwd(h, ncols, h->yI.p, h->zc.p, 1.0, h->xI.p, st);
+  bgather(h, ncols, h->xI.p, nullptr, y, dotv, partial, st);
 }
 
+// y = M_D^-1 x
 static void apply_M_inter(ietidp_s* h, int ncols, const double* x, double* y, const PcgState* st, const double* rr_part,
                           int check, const double* dotv, double* partial) {
   if (h->n_lambda == 0) return;
-  launch_local<1>(h, h->delta.p, x, h->zI.p, nullptr, ncols, st, rr_part, check);
-  bgather(h, ncols, h->zI.p, h->delta.p, nullptr, 0.0, y, dotv, partial, st);
+  TmvArgs a{};
+  a.vin = x;
+  a.weight = h->delta.p;
+  a.vout = h->sI.p;
+  a.ncols = ncols;
+  a.st = st;
+  a.rr_part = rr_part;
+  a.check = check;
+  launch_tmv<PRE1>(h, a);
+  TmvArgs b{};
+  b.vin = h->sI.p;
+  b.vout = h->zI.p;
+  b.ncols = ncols;
+  b.st = st;
+  launch_tmv<PRE2>(h, b);
+  bgather(h, ncols, h->zI.p, h->delta.p, y, dotv, partial, st);
 }
 
 void run_apply_F(ietidp_s* h, int ncols, const double* x, double* y) {
@@ -709,18 +655,8 @@ void run_apply_M(ietidp_s* h, int ncols, const double* x, double* y) {
   IETI_CHECK_LAUNCH();
 }
 
-// exported for coarse.cu (d = e - G S^-1 ftilde)
-void bgather_public(ietidp_s* h, int ncols, const double* x, const double* z, double coef, double* out) {
-  bgather(h, ncols, x, nullptr, z, coef, out, nullptr, nullptr, nullptr);
-}
-void coarse_apply_public(ietidp_s* h, int ncols, const double* gk, const double* add, double* z) {
-  coarse_apply(h, ncols, gk, add, z, nullptr);
-}
-
 static int body_launches(ietidp_s* h, int ncols) {
-  const LocalCfg cfg = local_cfg(h, ncols);
-  const int chunks = (ncols + cfg.ncp - 1) / cfg.ncp;
-  return 2 * chunks + (h->n_primal ? 1 : 0) + 2 + 3;
+  return 4 * tmv_launches(h, ncols) + (h->n_primal ? 1 : 0) + 2 + 3;
 }
 
 static void iteration_body(ietidp_s* h, PcgState* st, int use_graph) {
@@ -738,8 +674,10 @@ static void iteration_body(ietidp_s* h, PcgState* st, int use_graph) {
   IETI_LAUNCHED(h);
 }
 
-static bool build_graph(ietidp_s* h, PcgState* st) {
-  if (h->graph_exec && h->graph_ncols == h->nrhs) return true;
+static void build_graph(ietidp_s* h, PcgState* st) {
+  if (h->graph_exec) return;
+  // set the kernels' shared-memory attributes outside the capture
+  (void)tmv_cfg(h, h->nrhs);
   cudaGraph_t graph;
   IETI_CUDA(cudaGraphCreate(&graph, 0));
   cudaGraphConditionalHandle handle;
@@ -763,8 +701,6 @@ static bool build_graph(ietidp_s* h, PcgState* st) {
   IETI_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   h->graph = graph;
   h->graph_exec = exec;
-  h->graph_ncols = h->nrhs;
-  return true;
 }
 
 void destroy_graph(ietidp_s* h) {
@@ -798,7 +734,6 @@ void run_solve(ietidp_s* h) {
   IETI_CHECK_LAUNCH();
 }
 
-// After run_solve: read the state; count graph-launched kernels; true residual.
 void finish_solve(ietidp_s* h, ietidp_report* rep) {
   const int nc = h->nrhs, m = h->n_lambda;
   PcgState hs;
@@ -809,7 +744,6 @@ void finish_solve(ietidp_s* h, ietidp_report* rep) {
     rep->iters[c] = hs.iters[c];
     rep->converged[c] = h->opt.fixed_iters ? 1 : !hs.active[c];
   }
-  // true residual ||d - F lambda|| / ||d||
   if (m > 0) {
     double* part = h->partial.p + 3 * NBLK * nc;
     apply_F_inter(h, nc, h->lam_vec.p, h->tmp_out.p, nullptr, nullptr, nullptr);

@@ -1,0 +1,145 @@
+"""The C-ABI library without a GPU: it builds, loads, exports every entry point
+include/ietidp.h declares, and its host-side analysis (validation, DOF
+classification, nested dissection, symbolic factorisation) behaves as the header
+documents. Handles created with device = -1 run the analysis only."""
+import os
+import re
+
+import numpy as np
+import pytest
+
+from ietigen.bundle import make_bundle
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2501_04340_b200 import ietidp
+    return ietidp
+
+
+def test_exports_every_declared_symbol(lib):
+    hdr = open(os.path.join(ROOT, "include", "ietidp.h")).read()
+    declared = set(re.findall(r"\b(ietidp_[A-Za-z_]+)\s*\(", hdr))
+    assert declared == set(lib.SYMBOLS)
+    so = lib.load()
+    for name in declared:
+        assert hasattr(so, name), name
+
+
+def host_solver(lib, b, **kw):
+    return lib.from_bundle(b, device=-1, **kw)
+
+
+@pytest.mark.parametrize("name", ["C1", "C2r", "C3r"])
+def test_host_analysis_counts(lib, name):
+    b, P = make_bundle(name, with_problem=True)
+    s = host_solver(lib, b)
+    s.analyze()
+    r = s.report()
+    c = P.counts()
+    assert r["sum_nr"] == c["sum_nr"]
+    nI = [len(sd["B_dof"]) for sd in b["subs"]]
+    assert r["sum_nI"] == sum(nI) == 2 * b["n_lambda"]  # every multiplier has two entries (F3)
+    assert r["max_nI"] == max(nI)
+    # the supernodal structure stores at least the lower triangle's diagonal
+    assert r["nnz_L"] >= r["sum_nr"]
+
+
+def test_nested_dissection_beats_dense_ordering(lib):
+    b = make_bundle("C2r")
+    s1 = host_solver(lib, b)
+    s1.analyze()
+    s2 = host_solver(lib, b, ordering="dense")
+    s2.analyze()
+    r1, r2 = s1.report(), s2.report()
+    assert r1["factor_flops"] < r2["factor_flops"]
+    # dense ordering: one r_V supernode + r_I root + P node per subdomain
+    assert r2["n_supernodes"] == sum(1 + (len(sd["B_dof"]) > 0) + (len(sd["prim"]) > 0) for sd in b["subs"])
+
+
+def test_c1_dense_flops_closed_form(lib):
+    """C1 with the dense ordering: each subdomain's K_rr (n_r = 48) is one dense
+    front of 48 pivots... split as r_V (33) then r_I (15) plus the P node (none on
+    C1): sum_j c_j^2 over columns = sum_{c=1}^{48} c^2 per subdomain."""
+    b = make_bundle("C1")
+    s = host_solver(lib, b, ordering="dense")
+    s.analyze()
+    r = s.report()
+    per = sum(c * c for c in range(1, 49))
+    assert r["factor_flops"] == 2 * per
+    assert r["nnz_L"] == 2 * 48 * 49 // 2
+
+
+def test_b_row_with_three_entries(lib):
+    b = make_bundle("C1")
+    sd = b["subs"][0]
+    # duplicate multiplier 0 onto another remaining DOF of subdomain 1
+    sd1 = b["subs"][1]
+    free = np.setdiff1d(np.arange(sd1["n"]), np.concatenate([sd1["tree"], sd1["prim"], sd1["B_dof"]]))
+    sd1["B_lambda"] = np.append(sd1["B_lambda"], sd["B_lambda"][0]).astype(np.int32)
+    sd1["B_dof"] = np.append(sd1["B_dof"], free[0]).astype(np.int32)
+    sd1["B_sign"] = np.append(sd1["B_sign"], -1).astype(np.int8)
+    s = host_solver(lib, b)
+    with pytest.raises(lib.IetiError) as e:
+        s.analyze()
+    assert e.value.status == lib.E_B_STRUCTURE
+
+
+def test_b_touching_tree_dof(lib):
+    b = make_bundle("C1")
+    sd = b["subs"][0]
+    sd["B_dof"] = sd["B_dof"].copy()
+    sd["B_dof"][0] = sd["tree"][0]
+    s = host_solver(lib, b)
+    with pytest.raises(lib.IetiError) as e:
+        s.analyze()
+    assert e.value.status == lib.E_B_STRUCTURE
+
+
+def test_nonsymmetric_pattern_rejected(lib):
+    b = make_bundle("C1")
+    sd = b["subs"][0]
+    ip, ix = sd["K_indptr"].copy(), sd["K_indices"].copy()
+    # drop the last entry of row 0 (its transpose stays)
+    row0 = ix[ip[0]:ip[1]]
+    keep = np.ones(len(ix), bool)
+    keep[ip[1] - 1] = False
+    assert row0[-1] != 0
+    sd["K_indices"] = ix[keep]
+    sd["K_data"] = sd["K_data"][keep]
+    sd["K_indptr"] = np.concatenate([[0], ip[1:] - 1])
+    with pytest.raises(lib.IetiError) as e:
+        host_solver(lib, b)
+    assert e.value.status == lib.E_ARG
+
+
+def test_state_machine(lib):
+    b = make_bundle("C1")
+    s = host_solver(lib, b)
+    with pytest.raises(lib.IetiError) as e:
+        s.solve()
+    assert e.value.status == lib.E_STATE
+    sd = b["subs"][0]
+    with pytest.raises(lib.IetiError) as e:
+        s.set_subdomain(0, sd["K_indptr"], sd["K_indices"], sd["K_data"], sd["f"], sd["B_lambda"], sd["B_dof"],
+                        sd["B_sign"], sd["tree"], sd["prim"], sd["prim_gid"])
+    assert e.value.status == lib.E_STATE
+    s.analyze()
+    with pytest.raises(lib.IetiError) as e:
+        s.factor()  # host-only handle: no device work
+    assert e.value.status == lib.E_STATE
+
+
+def test_missing_subdomain(lib):
+    b = make_bundle("C1")
+    s = lib.Solver(b["n_sub"], b["n_lambda"], b["n_primal"], b["nrhs"], device=-1)
+    sd = b["subs"][0]
+    s.set_subdomain(0, sd["K_indptr"], sd["K_indices"], sd["K_data"], sd["f"], sd["B_lambda"], sd["B_dof"],
+                    sd["B_sign"], sd["tree"], sd["prim"], sd["prim_gid"])
+    with pytest.raises(lib.IetiError) as e:
+        s.analyze()
+    assert e.value.status == lib.E_STATE
