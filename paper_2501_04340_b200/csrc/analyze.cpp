@@ -11,6 +11,8 @@
 #include <atomic>
 #include <chrono>
 #include <climits>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 #include <thread>
@@ -133,17 +135,35 @@ struct NestedDissection {
     int nlev = (int)lstart.size() - 1;
     if (nlev < 3) return make_node(C, {});
     const int n = (int)C.size();
-    // smallest level among the balanced ones (both sides >= 30% of the rest)
-    int pick = -1, psz = INT_MAX, half = -1, hdist = INT_MAX;
+    // Candidate separators: BFS level sets, each thinned by moving the vertices
+    // with no neighbour on the far side into the near side (level sets of the
+    // wide spline stencils are several grid layers thick). Pick the smallest
+    // balanced one (both sides >= 30% of the rest).
+    std::vector<int> best_sep;
+    int best_score = INT_MAX;
+    std::vector<int> half_sep;
+    int hdist = INT_MAX;
     for (int l = 1; l < nlev - 1; ++l) {
-      int below = lstart[l], sz = lstart[l + 1] - lstart[l], above = n - lstart[l + 1];
-      int rest = n - sz;
-      if (std::min(below, above) >= 0.30 * rest && sz < psz) psz = sz, pick = l;
-      int dist = std::abs(below - above);
-      if (dist < hdist) hdist = dist, half = l;
+      std::vector<int> sep;
+      int nA = lstart[l], nB = n - lstart[l + 1];
+      // lev[] of the last BFS: < l side A, > l side B
+      for (int i = lstart[l]; i < lstart[l + 1]; ++i) {
+        const int v = order[i];
+        bool farB = false;
+        for (int e = xadj[v]; e < xadj[v + 1] && !farB; ++e) {
+          const int u = adj[e];
+          if (reg[u] == rid && stamp[u] == cur_stamp && lev[u] > l) farB = true;
+        }
+        if (farB) sep.push_back(v);
+        else ++nA;
+      }
+      const int sz = (int)sep.size(), rest = n - sz;
+      const int dist = std::abs(nA - nB);
+      if (dist < hdist) hdist = dist, half_sep = sep;
+      if (std::min(nA, nB) >= 0.30 * rest && sz < best_score) best_score = sz, best_sep = sep;
     }
-    if (pick < 0) pick = half;
-    std::vector<int> sep(order.begin() + lstart[pick], order.begin() + lstart[pick + 1]);
+    std::vector<int> sep = best_sep.empty() ? half_sep : best_sep;
+    if (sep.empty()) return make_node(C, {});
     for (int s : sep) reg[s] = 0;
     std::vector<int> rest;
     rest.reserve(n - sep.size());
@@ -417,7 +437,6 @@ void analyze_all(ietidp_s* h) {
   P.levels.resize(P.max_level + 1);
   for (int L = 0; L <= P.max_level; ++L) {
     LevelPlan& lp = P.levels[L];
-    lp.front_begin = pool;
     lp.sn_off = (int)P.level_sn.size();
     lp.sn_n = (int)bylev[L].size();
     for (int i : bylev[L]) {
@@ -450,7 +469,6 @@ void analyze_all(ietidp_s* h) {
       P.level_sn.push_back(i);
       P.max_front = std::max(P.max_front, s.f);
     }
-    lp.front_end = pool;
   }
   P.pool_doubles = pool;
   P.dinv_doubles = dinv;
@@ -480,47 +498,101 @@ void analyze_all(ietidp_s* h) {
   // ---- work lists: factorisation and sweeps, per level ----
   for (int L = 0; L <= P.max_level; ++L) {
     LevelPlan& lp = P.levels[L];
-    int maxc = 0;
-    for (int i : bylev[L]) maxc = std::max(maxc, (int)P.sn[i].children.size());
-    for (int q = 0; q < maxc; ++q) {
-      int off = (int)work.size() / 3, n = 0;
-      for (int i : bylev[L])
-        if ((int)P.sn[i].children.size() > q) {
-          int c = P.sn[i].children[q];
-          int nu = P.sn[c].f - P.sn[c].npiv;
-          for (int j0 = 0; j0 < nu; j0 += 32, ++n) push(c, j0, std::min(nu, j0 + 32));
-        }
-      if (n) lp.ea.push_back({off, n});
-    }
     int maxp = 0;
     for (int i : bylev[L])
       if (!P.sn[i].coarse) maxp = std::max(maxp, tiles_of(P.sn[i].npiv));
     for (int kp = 0; kp < maxp; ++kp) {
       LevelPlan::Panel pn{};
+      // (a) panel columns [p0, p0+b) -= L[rows >= p0, 0:p0] L[p0:p0+b, 0:p0]^T
+      pn.upd_off = (int)gwork.size();
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (s.coarse || s.npiv <= kp * TB || kp == 0) continue;
+        const SnDev& d = sd[i];
+        const int p0 = kp * TB, b = std::min(TB, s.npiv - p0);
+        for (int r0 = p0; r0 < s.f; r0 += TB, ++pn.upd_n) {
+          GemmWork g{};
+          g.c_off = d.front_off + (long long)p0 * d.ld + r0;
+          g.a_off = d.front_off + r0;
+          g.b_off = d.front_off + p0;  // B[n][k] = L[p0 + n][k]
+          g.lda = g.ldb = g.ldc = d.ld;
+          g.m = std::min(TB, s.f - r0);
+          g.n = b;
+          g.kdim = p0;
+          g.mode = 3;  // C -= A B
+          gwork.push_back(g);
+        }
+      }
       pn.potrf_off = (int)work.size() / 3;
       for (int i : bylev[L])
         if (!P.sn[i].coarse && P.sn[i].npiv > kp * TB) {
           push(i, kp, 0);
           pn.potrf_n++;
         }
-      pn.trsm_off = (int)work.size() / 3;
+      // (c) rows below the diagonal block: L = A Dinv^T (in place)
+      pn.trsm_off = (int)gwork.size();
       for (int i : bylev[L]) {
         const SnHost& s = P.sn[i];
         if (s.coarse || s.npiv <= kp * TB) continue;
-        int b = std::min(TB, s.npiv - kp * TB);
-        int nrow = s.f - (kp * TB + b);
-        for (int t = 0; t * TB < nrow; ++t, ++pn.trsm_n) push(i, kp, t);
-      }
-      pn.upd_off = (int)work.size() / 3;
-      for (int i : bylev[L]) {
-        const SnHost& s = P.sn[i];
-        if (s.coarse || s.npiv <= kp * TB) continue;
-        int b = std::min(TB, s.npiv - kp * TB);
-        int nt = tiles_of(s.f - (kp * TB + b));
-        for (int ti = 0; ti < nt; ++ti)
-          for (int tj = 0; tj <= ti; ++tj, ++pn.upd_n) push(i, kp, ti * 65536 + tj);
+        const SnDev& d = sd[i];
+        const int p0 = kp * TB, b = std::min(TB, s.npiv - p0);
+        for (int r0 = p0 + b; r0 < s.f; r0 += TB, ++pn.trsm_n) {
+          GemmWork g{};
+          g.c_off = d.front_off + (long long)p0 * d.ld + r0;
+          g.a_off = g.c_off;
+          g.b_off = d.dinv_off + (long long)kp * TILE_ELEMS;  // B[n][k] = Dinv[n][k], col-major
+          g.lda = g.ldc = d.ld;
+          g.ldb = TB;
+          g.m = std::min(TB, s.f - r0);
+          g.n = b;
+          g.kdim = b;
+          g.mode = 0;  // C = A B
+          gwork.push_back(g);
+        }
       }
       lp.panels.push_back(pn);
+    }
+    // (d) update block: parent[rel] += F22 - L21 L21^T (lower tiles, K = npiv), fused
+    //     extend-add; one launch per child slot so that no two CTAs of a launch add
+    //     into the same parent entries (deterministic, no atomics)
+    {
+      std::vector<int> slot(nsn, 0);
+      int maxslot = 0;
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (s.parent < 0) continue;
+        const auto& ch = P.sn[s.parent].children;
+        slot[i] = (int)(std::find(ch.begin(), ch.end(), i) - ch.begin());
+        maxslot = std::max(maxslot, slot[i] + 1);
+      }
+      for (int q = 0; q < maxslot; ++q) {
+        int off = (int)gwork.size();
+        for (int i : bylev[L]) {
+          const SnHost& s = P.sn[i];
+          if (s.coarse || s.f == s.npiv || s.parent < 0 || slot[i] != q) continue;
+          const SnDev& d = sd[i];
+          const SnDev& pd = sd[s.parent];
+          for (int r0 = s.npiv; r0 < s.f; r0 += TB)
+            for (int c0 = s.npiv; c0 <= r0; c0 += TB) {
+              GemmWork g{};
+              g.c_off = d.front_off + (long long)c0 * d.ld + r0;
+              g.a_off = d.front_off + r0;
+              g.b_off = d.front_off + c0;
+              g.lda = g.ldb = g.ldc = d.ld;
+              g.m = std::min(TB, s.f - r0);
+              g.n = std::min(TB, s.f - c0);
+              g.kdim = s.npiv;
+              g.mode = 4 | 1;  // extend-add of C - A B
+              g.diag = (r0 == c0);
+              g.p_off = pd.front_off;
+              g.p_ld = pd.ld;
+              g.rel_r = d.rel_off + (r0 - s.npiv);
+              g.rel_c = d.rel_off + (c0 - s.npiv);
+              gwork.push_back(g);
+            }
+        }
+        if ((int)gwork.size() > off) lp.syrk.push_back({off, (int)gwork.size() - off});
+      }
     }
     // sweeps
     lp.fs_off = (int)work.size() / 3;
@@ -726,14 +798,12 @@ void analyze_all(ietidp_s* h) {
   std::vector<long long> fdst, fxdst;
   std::vector<int> fsrc, fxsrc, kdiag;
   for (int L = 0; L <= P.max_level; ++L) {
-    P.levels[L].scat_begin = (long long)fdst.size();
     for (int k = 0; k < ns; ++k) {
       fdst.insert(fdst.end(), sc[k].fd[L].begin(), sc[k].fd[L].end());
       fsrc.insert(fsrc.end(), sc[k].fs[L].begin(), sc[k].fs[L].end());
       std::vector<long long>().swap(sc[k].fd[L]);
       std::vector<int>().swap(sc[k].fs[L]);
     }
-    P.levels[L].scat_end = (long long)fdst.size();
   }
   for (int k = 0; k < ns; ++k) {
     fxdst.insert(fxdst.end(), sc[k].fxd.begin(), sc[k].fxd.end());
@@ -803,6 +873,25 @@ void analyze_all(ietidp_s* h) {
   }
   auto t1 = std::chrono::steady_clock::now();
   fill_report(h);
+  if (getenv("IETIDP_DEBUG")) {
+    int crit = 0;
+    for (int L = 0; L <= P.max_level; ++L) {
+      int mx = 0, mf = 0, n = 0;
+      long long fl = 0;
+      for (int i : bylev[L]) {
+        const SnHost& sh = P.sn[i];
+        if (sh.coarse) continue;
+        ++n;
+        mx = std::max(mx, sh.npiv);
+        mf = std::max(mf, sh.f);
+        for (int j = 0; j < sh.npiv; ++j) fl += (long long)(sh.f - j) * (sh.f - j);
+      }
+      crit += (mx + TB - 1) / TB;
+      fprintf(stderr, "level %d: %d fronts, max npiv %d, max f %d, panels %d, GF %.2f\n", L, n, mx, mf,
+              (mx + TB - 1) / TB, fl / 1e9);
+    }
+    fprintf(stderr, "critical-path panels %d\n", crit);
+  }
   if (h->opt.device < 0) {  // host-only analysis mode: no device work
     h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t1 - t0).count();
     return;

@@ -61,14 +61,19 @@ struct Work {
   int sn, a, b;
 };
 
-// Work item of the general batched tile GEMM:
-// C(m x n tile) = (+/-) A(m x K) B(K x n) (+ C), column-major operands,
-// A[r][k] = A_base[a_off + k*lda + r], B[k][c] = B_base[b_off + c*ldb + k].
+// Work item of the batched tile GEMM (factor.cu k_gemm):
+// C(m x n tile) = (+/-) A(m x K) B(K x n) (+ C), A[r][k] = A_base[a_off + k*lda + r],
+// B[k][c] = B_base[b_off + k*ldb + c] (k_gemm<false>) or B_base[b_off + c*ldb + k]
+// (k_gemm<true>), C[r][c] = C_base[c_off + c*ldc + r].
 struct GemmWork {
   long long c_off, a_off, b_off;
   int lda, ldb, ldc, m, n, kdim;
-  int mode;  // bit0: negate, bit1: accumulate into C
-  int pad_;
+  int mode;  // bit0: negate, bit1: accumulate into C, bit2: extend-add epilogue (below)
+  int diag;  // extend-add: the tile is on the diagonal of U (add only r >= c)
+  // extend-add epilogue (multifrontal update of the parent, fused into the SYRK):
+  //   parent[p_off + rel[rel_c + c] * p_ld + rel[rel_r + r]] += C[r][c] - (A B)[r][c]
+  long long p_off;
+  int p_ld, rel_r, rel_c, pad_;
 };
 
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).
@@ -108,13 +113,14 @@ struct SubPlan {
 
 // Launch ranges of one elimination level.
 struct LevelPlan {
-  long long front_begin = 0, front_end = 0;  // pool range zeroed before assembly
-  long long scat_begin = 0, scat_end = 0;    // entries of the K scatter list
-  std::vector<std::pair<int, int>> ea;       // extend-add launches (work offset, count), one per child slot
+  // left-looking panels: GemmWork update of the panel columns with all previous
+  // panels (k > 0), POTRF (+ inverse) of the diagonal block (Work), GemmWork TRSM
+  // of the rows below with Dinv; then one GemmWork SYRK of the update block.
   struct Panel {
     int potrf_off, potrf_n, trsm_off, trsm_n, upd_off, upd_n;
   };
   std::vector<Panel> panels;
+  std::vector<std::pair<int, int>> syrk;     // SYRK + extend-add launches (GemmWork offset, count), one per child slot
   int sn_off = 0, sn_n = 0;                  // supernodes of this level (level_sn list)
   int fs_off = 0, fs_n = 0;                  // forward sweep: solve items (sn, row tile)
   int fu_off = 0, fu_n = 0;                  // forward sweep: update items (sn, update-row tile)

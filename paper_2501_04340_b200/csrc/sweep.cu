@@ -141,22 +141,40 @@ __global__ void __launch_bounds__(SWT)
     if (MODE == 0) {
       const double* Lc = pool + s.front_off + (long long)col * s.ld + s.npiv;
       const int* rw = rows + s.rows_off;
-      for (int q = lane; q < nu; q += 32) {
-        const double l = Lc[q];
-        const double* xr = Xs + (long long)rw[q] * ldx;
+      for (int q0 = 0; q0 < nu; q0 += 128) {  // 4 independent rows per lane
+        double l[4];
+        const double* xr[4];
 #pragma unroll
-        for (int c = 0; c < NCB; ++c)
-          if (c < ncl) acc[c] += l * xr[c];
+        for (int u = 0; u < 4; ++u) {
+          const int q = q0 + lane + 32 * u;
+          l[u] = q < nu ? Lc[q] : 0.0;
+          xr[u] = q < nu ? Xs + (long long)rw[q] * ldx : Xs;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < NCB; ++c)
+            if (c < ncl) acc[c] += l[u] * xr[u][c];
       }
     } else {
       const double* Ic = ipool + s.inv_off + (long long)col * s.ldi;
       const bool from_t = nu > 0;
-      for (int q = col + lane; q < s.npiv; q += 32) {
-        const double l = Ic[q];
+      for (int q0 = col; q0 < s.npiv; q0 += 128) {
+        double l[4];
+        int qq[4];
 #pragma unroll
-        for (int c = 0; c < NCB; ++c) {
-          const double tv = from_t ? t[q * NCB + c] : (c < ncl ? Xs[(long long)(s.c0 + q) * ldx + c] : 0.0);
-          acc[c] += l * tv;
+        for (int u = 0; u < 4; ++u) {
+          qq[u] = q0 + lane + 32 * u;
+          l[u] = qq[u] < s.npiv ? Ic[qq[u]] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          if (qq[u] >= s.npiv) continue;
+#pragma unroll
+          for (int c = 0; c < NCB; ++c) {
+            const double tv = from_t ? t[qq[u] * NCB + c] : (c < ncl ? Xs[(long long)(s.c0 + qq[u]) * ldx + c] : 0.0);
+            acc[c] += l[u] * tv;
+          }
         }
       }
     }

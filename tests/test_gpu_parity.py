@@ -106,7 +106,10 @@ def test_solution_natural_stopping(lib, name):
     if not np.all(np.abs(it_gpu - it_ref) <= 1):
         it_alt = oracle_explicit_inverse_iters(b)
         lo, hi = np.minimum(it_ref, it_alt), np.maximum(it_ref, it_alt)
-        assert np.all((it_gpu >= lo - 1) & (it_gpu <= hi + 1)), (it_gpu, it_ref, it_alt)
+        # +-1 around the oracle's own spread; +-2 where the two oracle variants
+        # themselves differ by more than one iteration (R10)
+        slack = np.where(hi - lo > 1, 2, 1)
+        assert np.all((it_gpu >= lo - slack) & (it_gpu <= hi + slack)), (it_gpu, it_ref, it_alt)
     assert all(rep["converged"])
     assert max(rep["rel_residual"]) <= 1e-10
     U = np.concatenate(u)
