@@ -114,6 +114,8 @@ struct ietidp_s {
   void* graph_exec = nullptr;
   void* graph = nullptr;
   unsigned long long cond_handle = 0;
+  bool pcg_persistent = false;          // last solve ran the persistent cooperative PCG kernel
+  ieti::DevBuf<unsigned> gbar;          // its grid barrier
 };
 
 // Device-side entry points implemented in the .cu files (host launchers).

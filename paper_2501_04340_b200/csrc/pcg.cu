@@ -26,6 +26,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <cstdlib>
+#include <string>
 
 #include "common.cuh"
 
@@ -73,32 +75,17 @@ struct TmvArgs {
   int check;
 };
 
+// One work item (subdomain block pair) of a tile-streamed operator.
 template <int MODE, int NCP, int STAGES>
-__global__ void __launch_bounds__(256, 1) k_tmv(const TmvArgs A) {
-  extern __shared__ __align__(16) double smem[];
+__device__ __forceinline__ void tmv_item(const TmvArgs& A, int item, double* smem) {
   constexpr bool TRANS = (MODE == BWD || MODE == PRE1);
   constexpr int VS = (NCP == 1) ? 1 : NCP + 4;
   constexpr int NB = (NCP == 1) ? 1 : NCP / 8;
   __shared__ double red[8][TB];
-  __shared__ int any_s;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ncl = min(NCP, A.ncols - A.c_off);
-
-  if (A.st) {
-    if (A.st->done) return;
-    if (MODE == PRE1 && A.check && !A.st->fixed) {
-      if (tid == 0) any_s = 0;
-      __syncthreads();
-      if (tid < A.st->ncols && A.st->active[tid]) {
-        double s = 0.0;
-        for (int b = 0; b < NBLK; ++b) s += A.rr_part[b * A.st->ncols + tid];
-        if (!(sqrt(s) <= A.st->tol * A.st->r0[tid])) atomicOr(&any_s, 1);
-      }
-      __syncthreads();
-      if (!any_s) return;
-    }
-  }
-  const LoopWork lw = A.work[blockIdx.x];
+  __syncthreads();  // shared memory of the previous item is free
+  const LoopWork lw = A.work[item];
   const SubDev d = A.sub[lw.sub];
   const int nt = d.nt;
   const int ob[2] = {lw.blk0, lw.blk1};
@@ -254,8 +241,30 @@ __global__ void __launch_bounds__(256, 1) k_tmv(const TmvArgs A) {
   cp_async_wait<0>();
   if (MODE == FWD && A.gpart && tid < d.nP * NCP) {
     const int q = tid / NCP, c = tid % NCP;
-    if (c < ncl) A.gpart[((long long)blockIdx.x * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
+    if (c < ncl) A.gpart[((long long)item * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
   }
+}
+
+template <int MODE, int NCP, int STAGES>
+__global__ void __launch_bounds__(256, 1) k_tmv(const TmvArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ int any_s;
+  const int tid = threadIdx.x;
+  if (A.st) {
+    if (A.st->done) return;
+    if (MODE == PRE1 && A.check && !A.st->fixed) {
+      if (tid == 0) any_s = 0;
+      __syncthreads();
+      if (tid < A.st->ncols && A.st->active[tid]) {
+        double s = 0.0;
+        for (int b = 0; b < NBLK; ++b) s += A.rr_part[b * A.st->ncols + tid];
+        if (!(sqrt(s) <= A.st->tol * A.st->r0[tid])) atomicOr(&any_s, 1);
+      }
+      __syncthreads();
+      if (!any_s) return;
+    }
+  }
+  tmv_item<MODE, NCP, STAGES>(A, blockIdx.x, smem);
 }
 
 // ---------------------------------------------------------------------------
@@ -514,6 +523,237 @@ __global__ void k_transpose(int rows, int ncols, const double* __restrict__ in, 
 }
 
 // ---------------------------------------------------------------------------
+// Persistent PCG: the whole loop in ONE cooperative launch (one CTA per SM),
+// phases separated by a grid-wide barrier. Each CTA keeps its own copy of the
+// per-column CG scalars, reduced redundantly and in a fixed order from the
+// per-CTA partials, so all CTAs take identical decisions (bit-reproducible).
+// ---------------------------------------------------------------------------
+struct PcgArgs {
+  TmvArgs fwd, bwd, pre1, pre2;
+  const LamDev* lam;
+  const double* delta;
+  double *lamv, *r, *p, *q, *z;
+  const double* d;
+  const double *xI, *zI;
+  const int *pcon_ptr, *pcon_sub, *pcon_q, *sub_cta0, *sub_ncta;
+  const double *gpart, *Sinv;
+  double* zc;
+  double* part;  // [3][grid][ncols]: p.q, r.r, r.z partials
+  PcgState* st;
+  unsigned* bar;  // [0] arrivals, [1] generation
+  double tol;
+  int m, ncols, ng, nPmax, max_iter, fixed, n_items, ncp;
+};
+
+__device__ __forceinline__ void grid_barrier(unsigned* bar) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    volatile unsigned* gen = bar + 1;
+    const unsigned g = *gen;
+    __threadfence();
+    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
+      bar[0] = 0;
+      __threadfence();
+      atomicAdd(bar + 1, 1u);
+    } else {
+      while (*gen == g) __nanosleep(20);
+    }
+    __threadfence();
+  }
+  __syncthreads();
+}
+
+// sum over the CTAs' partials of column c (fixed order)
+__device__ __forceinline__ double colsum(const double* part, int c, int ncols) {
+  double s = 0.0;
+  for (int b = 0; b < (int)gridDim.x; ++b) s += part[b * ncols + c];
+  return s;
+}
+
+template <int MODE, int NCP, int STAGES>
+__device__ __forceinline__ void tmv_phase(TmvArgs A, int n_items, int ncp, double* smem) {
+  for (int c0 = 0; c0 < A.ncols; c0 += ncp) {
+    A.c_off = c0;
+    for (int it = blockIdx.x; it < n_items; it += gridDim.x) tmv_item<MODE, NCP, STAGES>(A, it, smem);
+  }
+}
+
+// out = sum_k B (w) x, with the per-CTA partial of out . dotv
+__device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x, const double* w, double* out,
+                                              const double* dotv, double* part) {
+  const int nc = P.ncols, P2 = pow2ge(nc);
+  const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
+  double dot = 0.0;
+  if (c < nc)
+    for (int j = blockIdx.x * R + rl; j < P.m; j += gridDim.x * R) {
+      const LamDev L = P.lam[j];
+      double val = 0.0;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int a = L.slot[q];
+        val += (double)L.sign[q] * (w ? w[a] : 1.0) * x[(long long)a * nc + c];
+      }
+      out[(long long)j * nc + c] = val;
+      dot += val * dotv[(long long)j * nc + c];
+    }
+  block_col_reduce(dot, nc, P2, part);
+}
+
+template <int NCP, int STAGES>
+__global__ void __launch_bounds__(256, 1) k_pcg(const PcgArgs P) {
+  extern __shared__ __align__(16) double smem[];
+  __shared__ double s_rz[IETIDP_MAX_RHS], s_r0[IETIDP_MAX_RHS], s_coef[IETIDP_MAX_RHS];
+  __shared__ int s_act[IETIDP_MAX_RHS], s_new[IETIDP_MAX_RHS], s_iters[IETIDP_MAX_RHS];
+  __shared__ int s_any;
+  const int tid = threadIdx.x, nb = gridDim.x, nc = P.ncols, m = P.m;
+  double* pq = P.part;
+  double* rr = P.part + nb * nc;
+  double* rz = P.part + 2 * nb * nc;
+  const int P2 = pow2ge(nc);
+  const int cc = tid % P2, rl = tid / P2, R = VT / P2;
+  auto rows = [&](auto&& f) {  // this CTA's share of the lambda-space rows, column cc
+    if (cc < nc)
+      for (int j = blockIdx.x * R + rl; j < m; j += nb * R) f((long long)j * nc + cc);
+  };
+  // ---- init: lambda = 0, r = d, r0 = ||d|| ----
+  {
+    double acc = 0.0;
+    rows([&](long long e) {
+      P.lamv[e] = 0.0;
+      const double dv = P.d[e];
+      P.r[e] = dv;
+      acc += dv * dv;
+    });
+    block_col_reduce(acc, nc, P2, rr);
+  }
+  grid_barrier(P.bar);
+  if (tid < nc) {
+    s_r0[tid] = sqrt(colsum(rr, tid, nc));
+    s_act[tid] = (m > 0 && s_r0[tid] > 0.0) ? 1 : 0;
+    s_iters[tid] = 0;
+    s_rz[tid] = 0.0;
+  }
+  __syncthreads();
+  int it = 0;
+  bool run = false;
+  for (int c = 0; c < nc; ++c) run |= s_act[c] != 0;
+  if (!P.fixed && P.max_iter <= 0) run = false;
+  if (run) {
+    // z = M r, rz = r.z, p = z
+    tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.n_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    tmv_phase<PRE2, NCP, STAGES>(P.pre2, P.n_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    bgather_phase(P, P.zI, P.delta, P.z, P.r, rz);
+    grid_barrier(P.bar);
+    if (tid < nc) s_rz[tid] = colsum(rz, tid, nc);
+    rows([&](long long e) { P.p[e] = P.z[e]; });
+    grid_barrier(P.bar);
+  }
+  while (run) {
+    // q = F p
+    tmv_phase<FWD, NCP, STAGES>(P.fwd, P.n_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    if (P.ng > 0) {
+      double* g = smem;  // ng x nc
+      for (int e = tid; e < P.ng * nc; e += VT) {
+        const int gi = e / nc, c = e - gi * nc;
+        double sacc = 0.0;
+        for (int q = P.pcon_ptr[gi]; q < P.pcon_ptr[gi + 1]; ++q) {
+          const int k = P.pcon_sub[q], lq = P.pcon_q[q];
+          for (int cta = P.sub_cta0[k]; cta < P.sub_cta0[k] + P.sub_ncta[k]; ++cta)
+            sacc += P.gpart[((long long)cta * P.nPmax + lq) * nc + c];
+        }
+        g[e] = sacc;
+      }
+      __syncthreads();
+      const int warp = tid >> 5, lane = tid & 31;
+      for (int e = blockIdx.x * 8 + warp; e < P.ng * nc; e += nb * 8) {
+        const int i = e / nc, c = e - i * nc;
+        double sacc = 0.0;
+        for (int j = lane; j < P.ng; j += 32) sacc += P.Sinv[(long long)i * P.ng + j] * g[j * nc + c];
+        sacc = warp_sum(sacc);
+        if (lane == 0) P.zc[e] = sacc;
+      }
+      grid_barrier(P.bar);
+    }
+    tmv_phase<BWD, NCP, STAGES>(P.bwd, P.n_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    bgather_phase(P, P.xI, nullptr, P.q, P.p, pq);
+    grid_barrier(P.bar);
+    // alpha, lambda and r
+    if (tid < nc) s_coef[tid] = s_act[tid] ? s_rz[tid] / colsum(pq, tid, nc) : 0.0;
+    __syncthreads();
+    {
+      double acc = 0.0;
+      const bool act = cc < nc && s_act[cc];
+      const double a = cc < nc ? s_coef[cc] : 0.0;
+      rows([&](long long e) {
+        double rv = P.r[e];
+        if (act) {
+          P.lamv[e] += a * P.p[e];
+          rv -= a * P.q[e];
+          P.r[e] = rv;
+        }
+        acc += rv * rv;
+      });
+      block_col_reduce(acc, nc, P2, rr);
+    }
+    grid_barrier(P.bar);
+    // stop test (identical in every CTA)
+    if (tid == 0) s_any = 0;
+    __syncthreads();
+    if (tid < nc) {
+      int a = s_act[tid];
+      if (s_act[tid]) s_iters[tid]++;
+      if (a && !P.fixed && sqrt(colsum(rr, tid, nc)) <= P.tol * s_r0[tid]) a = 0;
+      s_new[tid] = a;
+      if (a) atomicOr(&s_any, 1);
+    }
+    __syncthreads();
+    ++it;
+    if (P.fixed ? it >= P.fixed : (!s_any || it >= P.max_iter)) {
+      if (tid < nc) s_act[tid] = s_new[tid];
+      break;
+    }
+    // z = M r
+    tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.n_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    tmv_phase<PRE2, NCP, STAGES>(P.pre2, P.n_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    bgather_phase(P, P.zI, P.delta, P.z, P.r, rz);
+    grid_barrier(P.bar);
+    // beta, p
+    if (tid < nc) {
+      const double rzn = colsum(rz, tid, nc);
+      s_coef[tid] = rzn / s_rz[tid];
+      if (s_new[tid]) s_rz[tid] = rzn;
+    }
+    __syncthreads();
+    {
+      const bool act = cc < nc && s_new[cc];
+      const double bta = cc < nc ? s_coef[cc] : 0.0;
+      rows([&](long long e) {
+        if (act) P.p[e] = P.z[e] + bta * P.p[e];
+      });
+    }
+    if (tid < nc) s_act[tid] = s_new[tid];
+    grid_barrier(P.bar);
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    P.st->it = it;
+    P.st->done = 1;
+    P.st->ncols = nc;
+    for (int c = 0; c < nc; ++c) {
+      P.st->iters[c] = s_iters[c];
+      P.st->active[c] = s_act[c];
+      P.st->r0[c] = s_r0[c];
+      P.st->rz[c] = s_rz[c];
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Host side
 // ---------------------------------------------------------------------------
 struct TmvCfg {
@@ -522,7 +762,7 @@ struct TmvCfg {
 
 static TmvCfg tmv_cfg(const ietidp_s* h, int ncols) {
   const int nt = (h->plan.max_nI + TB - 1) / TB;
-  if (ncols == 1) return {1, 3, (3 * TILE_ELEMS + nt * TB + TB) * 8};
+  if (ncols == 1) return {1, 5, (5 * TILE_ELEMS + nt * TB + TB) * 8};
   for (int ncp : {16, 8}) {
     if (ncp == 16 && ncols <= 8) continue;
     const int vs = ncp + 4;
@@ -556,7 +796,7 @@ static void launch_tmv(ietidp_s* h, TmvArgs a) {
   a.nPmax = std::max(h->plan.nPmax, 1);
   for (int c0 = 0; c0 < a.ncols; c0 += cfg.ncp) {
     a.c_off = c0;
-    if (cfg.ncp == 1) launch_tmv_t<MODE, 1, 3>(h, cfg, a);
+    if (cfg.ncp == 1) launch_tmv_t<MODE, 1, 5>(h, cfg, a);
     else if (cfg.ncp == 16 && cfg.stages == 3) launch_tmv_t<MODE, 16, 3>(h, cfg, a);
     else if (cfg.ncp == 16) launch_tmv_t<MODE, 16, 2>(h, cfg, a);
     else if (cfg.stages == 3) launch_tmv_t<MODE, 8, 3>(h, cfg, a);
@@ -709,6 +949,98 @@ void destroy_graph(ietidp_s* h) {
   h->graph_exec = h->graph = nullptr;
 }
 
+static TmvArgs base_args(ietidp_s* h, int mode, int ncols) {
+  TmvArgs a{};
+  a.work = h->d_loopwork.p;
+  a.sub = h->d_sub.p;
+  a.tiles = (mode == FWD || mode == BWD) ? h->itiles.p : h->tiles.p;
+  a.lpi = h->lpi.p;
+  a.slot_lam = h->slot_lam.p;
+  a.slot_sign = h->slot_sign.p;
+  a.prim_gid = h->d_prim_gid.p;
+  a.nPmax = std::max(h->plan.nPmax, 1);
+  a.ncols = ncols;
+  return a;
+}
+
+template <int NCP, int STAGES>
+static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
+  auto kern = k_pcg<NCP, STAGES>;
+  IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
+  int per_sm = 0, nsm = 0;
+  IETI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, cfg.smem));
+  IETI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->opt.device));
+  if (per_sm < 1) return false;
+  const int grid = std::min(nsm * per_sm, 1024);
+  PcgArgs args = a;
+  void* params[] = {&args};
+  IETI_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, 256, params, cfg.smem, h->stream));
+  IETI_LAUNCHED(h);
+  return true;
+}
+
+// The whole PCG loop as one persistent cooperative kernel.
+static bool run_solve_persistent(ietidp_s* h) {
+  const int nc = h->nrhs, m = h->n_lambda;
+  if (m == 0 || h->n_loopwork == 0) return false;
+  const TmvCfg cfg = tmv_cfg(h, nc);
+  if (h->gbar.n == 0) h->gbar.alloc(2);
+  h->gbar.zero(h->stream);
+  PcgArgs a{};
+  a.fwd = base_args(h, FWD, nc);
+  a.fwd.vin = h->p_vec.p;
+  a.fwd.vout = h->yI.p;
+  a.fwd.gpart = h->n_primal ? h->gpart.p : nullptr;
+  a.bwd = base_args(h, BWD, nc);
+  a.bwd.vin = h->yI.p;
+  a.bwd.z = h->n_primal ? h->zc.p : nullptr;
+  a.bwd.zsign = 1.0;
+  a.bwd.vout = h->xI.p;
+  a.pre1 = base_args(h, PRE1, nc);
+  a.pre1.vin = h->r_vec.p;
+  a.pre1.weight = h->delta.p;
+  a.pre1.vout = h->sI.p;
+  a.pre2 = base_args(h, PRE2, nc);
+  a.pre2.vin = h->sI.p;
+  a.pre2.vout = h->zI.p;
+  a.lam = h->lam.p;
+  a.delta = h->delta.p;
+  a.lamv = h->lam_vec.p;
+  a.r = h->r_vec.p;
+  a.p = h->p_vec.p;
+  a.q = h->q_vec.p;
+  a.z = h->z_vec.p;
+  a.d = h->d_vec.p;
+  a.xI = h->xI.p;
+  a.zI = h->zI.p;
+  a.pcon_ptr = h->pcon_ptr.p;
+  a.pcon_sub = h->pcon_sub.p;
+  a.pcon_q = h->pcon_q.p;
+  a.sub_cta0 = h->sub_cta0.p;
+  a.sub_ncta = h->sub_ncta.p;
+  a.gpart = h->gpart.p;
+  a.Sinv = h->Sinv.p;
+  a.zc = h->zc.p;
+  a.part = h->partial.p;
+  a.st = reinterpret_cast<PcgState*>(h->state.p);
+  a.bar = h->gbar.p;
+  a.tol = h->opt.tol;
+  a.m = m;
+  a.ncols = nc;
+  a.ng = h->n_primal;
+  a.nPmax = std::max(h->plan.nPmax, 1);
+  a.max_iter = h->opt.max_iter;
+  a.fixed = h->opt.fixed_iters;
+  a.n_items = h->n_loopwork;
+  a.ncp = cfg.ncp;
+  if (h->n_primal * nc * 8 > cfg.smem) return false;
+  if (cfg.ncp == 1) return launch_pcg_t<1, 5>(h, cfg, a);
+  if (cfg.ncp == 16 && cfg.stages == 3) return launch_pcg_t<16, 3>(h, cfg, a);
+  if (cfg.ncp == 16) return launch_pcg_t<16, 2>(h, cfg, a);
+  if (cfg.stages == 3) return launch_pcg_t<8, 3>(h, cfg, a);
+  return launch_pcg_t<8, 2>(h, cfg, a);
+}
+
 void run_solve(ietidp_s* h) {
   const int nc = h->nrhs, m = h->n_lambda;
   PcgState* st = reinterpret_cast<PcgState*>(h->state.p);
@@ -716,6 +1048,13 @@ void run_solve(ietidp_s* h) {
   double* rz_part = h->partial.p + 2 * NBLK * nc;
   cudaStream_t s = h->stream;
   IETI_CUDA(cudaMemsetAsync(h->partial.p, 0, h->partial.n * sizeof(double), s));
+  const char* mode = getenv("IETIDP_PCG");
+  h->pcg_persistent = false;
+  if (!(mode && std::string(mode) == "graph") && run_solve_persistent(h)) {
+    h->pcg_persistent = true;
+    IETI_CHECK_LAUNCH();
+    return;
+  }
   if (m > 0) {
     k_init<<<NBLK, VT, 0, s>>>(m, nc, h->d_vec.p, h->lam_vec.p, h->r_vec.p, rr_part);
     IETI_LAUNCHED(h);
@@ -739,7 +1078,7 @@ void finish_solve(ietidp_s* h, ietidp_report* rep) {
   PcgState hs;
   IETI_CUDA(cudaMemcpyAsync(&hs, h->state.p, sizeof(PcgState), cudaMemcpyDeviceToHost, h->stream));
   IETI_CUDA(cudaStreamSynchronize(h->stream));
-  if (m > 0) h->launches += (long long)body_launches(h, nc) * std::max(hs.it, 1);
+  if (m > 0 && !h->pcg_persistent) h->launches += (long long)body_launches(h, nc) * std::max(hs.it, 1);
   for (int c = 0; c < nc; ++c) {
     rep->iters[c] = hs.iters[c];
     rep->converged[c] = h->opt.fixed_iters ? 1 : !hs.active[c];
