@@ -71,6 +71,14 @@ typedef enum {
 } ietidp_scaling;
 
 typedef enum {
+  IETIDP_LOOP_EXPLICIT = 0,   /* default: the loop applies W_k = S_II^-1 and S_II, each stored once
+                                 as a symmetric lower-tile matrix and streamed in one pass per
+                                 operator; G_k = L_II^-T L_PI^T explicit       */
+  IETIDP_LOOP_TRIANGULAR = 1  /* forward/backward substitutions with L_II^-1 and L_II per iteration
+                                 (two passes per operator)                      */
+} ietidp_loop;
+
+typedef enum {
   IETIDP_ORDER_NESTED_DISSECTION = 0, /* default: nested dissection of r_V, r_I last     */
   IETIDP_ORDER_DENSE = 1              /* r_V as one dense supernode (test/oracle aid)    */
 } ietidp_ordering;
@@ -83,6 +91,7 @@ typedef struct {
   int fixed_iters;  /* > 0: run exactly this many iterations, no stop test (parity mode)  */
   int ordering;     /* ietidp_ordering; default nested dissection                         */
   int leaf_size;    /* nested-dissection leaf size (supernode of the leaves); default 96  */
+  int loop;         /* ietidp_loop: operators of the PCG loop; default IETIDP_LOOP_EXPLICIT */
   int device;       /* CUDA device ordinal; default 0                                     */
   void* stream;     /* cudaStream_t all work is issued on; NULL = library-owned stream    */
 } ietidp_options;
@@ -168,7 +177,8 @@ ietidp_status ietidp_get_lambda_device(ietidp_t h, double* d_lambda);
  * n_lambda x ncols column-major, 1 <= ncols <= nrhs, issued on the handle's stream
  * (asynchronous; synchronise the stream before reading d_y).
  *   y = F_DP x = sum_k B_I L_II^-T L_II^-1 B_I^T x + G S_PP^-1 G^T x   (F2)
- *   y = M_D^-1 x = sum_k B_D L_II L_II^T B_D^T x */
+ *   y = M_D^-1 x = sum_k B_D L_II L_II^T B_D^T x
+ * applied with the handle's loop operators (ietidp_options.loop). */
 ietidp_status ietidp_apply_F(ietidp_t h, int ncols, const double* d_x, double* d_y);
 ietidp_status ietidp_apply_precond(ietidp_t h, int ncols, const double* d_x, double* d_y);
 

@@ -366,8 +366,15 @@ static void fill_report(ietidp_s* h) {
   // algorithmic bytes: one F-apply reads the lower
   // triangle of every L_II^-1 twice (forward, backward) and L_PI twice; the
   // preconditioner reads the lower triangle of every L_II twice (L^T, L).
-  h->rep.f_apply_bytes = 2 * 8 * tri + 2 * 8 * sIP;
-  h->rep.pcg_bytes_per_iter = 4 * 8 * tri + 2 * 8 * sIP;
+  if (h->opt.loop == IETIDP_LOOP_EXPLICIT) {
+    // explicit: one pass over the lower triangle of W_k = S_II^-1 and G_k
+    // twice per F-apply, one pass over S_II per preconditioner application
+    h->rep.f_apply_bytes = 8 * tri + 2 * 8 * sIP;
+    h->rep.pcg_bytes_per_iter = 2 * 8 * tri + 2 * 8 * sIP;
+  } else {
+    h->rep.f_apply_bytes = 2 * 8 * tri + 2 * 8 * sIP;
+    h->rep.pcg_bytes_per_iter = 4 * 8 * tri + 2 * 8 * sIP;
+  }
 }
 
 // Build the complete plan and upload every structure and the raw values.
@@ -684,7 +691,7 @@ void analyze_all(ietidp_s* h) {
   }
 
   // ---- per-subdomain offsets ----
-  long long kv = 0, fv = 0, xo = 0, rio = 0, lpio = 0, to = 0, uo = 0;
+  long long kv = 0, fv = 0, xo = 0, rio = 0, lpio = 0, to = 0, uo = 0, spo = 0;
   int po = 0, permo = 0, cta = 0;
   P.nPmax = 0;
   h->kval_off.resize(ns);
@@ -716,8 +723,11 @@ void analyze_all(ietidp_s* h) {
     h->fval_off[k] = fv;
     fv += (long long)in.n * nrhs;
     d.lpi_off = lpio;
+    d.g_off = lpio;  // G_k has the same size as L_PI (nI x nP)
     lpio += (long long)sp.nP * sp.nI;
     d.nt = tiles_of(sp.nI);
+    d.spart_off = spo;
+    spo += (long long)d.nt * (d.nt - 1) / 2;
     d.tile_off = to;
     d.itile_off = to;  // same offsets in the two tile arrays
     to += (long long)d.nt * (d.nt + 1) / 2 * TILE_ELEMS;
@@ -733,7 +743,7 @@ void analyze_all(ietidp_s* h) {
     sub_cta0[k] = cta;
     for (int i = 0; i < (d.nt + 1) / 2; ++i) {
       int j = d.nt - 1 - i;
-      loopwork.push_back({k, i == j ? 1 : 2, i, j});
+      loopwork.push_back({k, i == j ? 1 : 2, i, j, i == j ? i + 1 : d.nt + 1});
       ++cta;
     }
     sub_ncta[k] = cta - d.cta0;
@@ -743,6 +753,32 @@ void analyze_all(ietidp_s* h) {
   h->n_slots = (int)rio;
   h->sum_nP = po;
   h->n_loopwork = (int)loopwork.size();
+  // explicit loop operators: W = L_II^-T L_II^-1 (lower tiles, into tpool at the root's
+  // L11^-1 layout) and the roots by level (S_II is copied before the root is factored)
+  P.roots_by_level.assign(P.max_level + 1, {});
+  P.w_off = (int)gwork.size();
+  for (int k = 0; k < ns; ++k) {
+    const SubDev& d = h->h_sub[k];
+    if (d.root < 0) continue;
+    P.roots_by_level[P.sn[d.root].level].push_back(k);
+    if (h->opt.loop != IETIDP_LOOP_EXPLICIT) continue;
+    const SnDev& r = sd[d.root];
+    for (int i = 0; i < d.nt; ++i)
+      for (int j = 0; j <= i; ++j) {
+        GemmWork g{};
+        const int k0 = i * TB;
+        g.c_off = r.inv_off + (long long)(j * TB) * r.ldi + i * TB;
+        g.a_off = r.inv_off + (long long)(i * TB) * r.ldi + k0;  // A[r][k] = Linv[k][iTB + r] (k contiguous)
+        g.b_off = r.inv_off + (long long)(j * TB) * r.ldi + k0;  // B[k][c] = Linv[k][jTB + c] (k contiguous)
+        g.lda = g.ldb = g.ldc = r.ldi;
+        g.m = std::min(TB, d.nI - i * TB);
+        g.n = std::min(TB, d.nI - j * TB);
+        g.kdim = d.nI - k0;
+        g.mode = 0;
+        gwork.push_back(g);
+      }
+  }
+  P.w_n = (int)gwork.size() - P.w_off;
 
   // ---- scatter lists (per subdomain in parallel, merged per level) ----
   struct Scat {
@@ -924,6 +960,35 @@ void analyze_all(ietidp_s* h) {
   h->pcon_sub.upload(pcon_sub, s);
   h->pcon_q.upload(pcon_q, s);
   h->d_loopwork.upload(loopwork, s);
+  h->h_loopwork = loopwork;
+  h->lpt_grid = 0;
+  {
+    std::vector<int> rl;
+    h->rootlist_range.assign(P.max_level + 1, {0, 0});
+    for (int L = 0; L <= P.max_level; ++L) {
+      h->rootlist_range[L] = {(int)rl.size(), (int)P.roots_by_level[L].size()};
+      rl.insert(rl.end(), P.roots_by_level[L].begin(), P.roots_by_level[L].end());
+    }
+    h->d_rootlist.upload(rl, s);
+    std::vector<long long> goff(h->n_slots);
+    std::vector<int> np(h->n_slots), poff(h->n_slots);
+    for (int k = 0; k < ns; ++k) {
+      const SubDev& d = h->h_sub[k];
+      for (int a = 0; a < d.nI; ++a) {
+        goff[d.rI_off + a] = d.g_off + (long long)a * d.nP;
+        np[d.rI_off + a] = d.nP;
+        poff[d.rI_off + a] = d.prim_off;
+      }
+    }
+    h->slot_goff.upload(goff, s);
+    std::vector<int2> blk;
+    for (int k = 0; k < ns; ++k)
+      for (int j = 0; j < h->h_sub[k].nt; ++j) blk.push_back(make_int2(k, j));
+    h->n_blk = (int)blk.size();
+    h->d_blk.upload(blk, s);
+    h->slot_np.upload(np, s);
+    h->slot_poff.upload(poff, s);
+  }
   h->sub_cta0.upload(sub_cta0, s);
   h->sub_ncta.upload(sub_ncta, s);
   std::vector<double> kvals(kv), fvals(fv);
@@ -949,6 +1014,12 @@ void analyze_all(ietidp_s* h) {
   h->tiles.alloc(to);
   h->itiles.alloc(to);
   h->lpi.alloc(lpio);
+  h->G.alloc(lpio);
+  if (h->opt.loop == IETIDP_LOOP_EXPLICIT) {
+    h->wtiles.alloc(to);
+    h->stiles.alloc(to);
+  }
+  h->spart.alloc((size_t)std::max(spo, 1LL) * TB * nc);
   h->delta.alloc(h->n_slots);
   h->kdiag.alloc(h->n_slots);
   const size_t m = (size_t)h->n_lambda * nc;

@@ -76,6 +76,7 @@ void ietidp_options_default(ietidp_options* o) {
   o->fixed_iters = 0;
   o->ordering = IETIDP_ORDER_NESTED_DISSECTION;
   o->leaf_size = 96;
+  o->loop = IETIDP_LOOP_EXPLICIT;
   o->device = 0;
   o->stream = nullptr;
 }
@@ -114,6 +115,8 @@ ietidp_status ietidp_create(const ietidp_options* opt, int n_sub, int n_lambda, 
     require(h->opt.tol >= 0.0 && h->opt.max_iter >= 0 && h->opt.fixed_iters >= 0, IETIDP_E_ARG, "bad options");
     require(h->opt.scaling == IETIDP_SCALE_MULTIPLICITY || h->opt.scaling == IETIDP_SCALE_STIFFNESS, IETIDP_E_ARG,
             "bad scaling");
+    require(h->opt.loop == IETIDP_LOOP_EXPLICIT || h->opt.loop == IETIDP_LOOP_TRIANGULAR, IETIDP_E_ARG,
+            "bad loop operators");
     if (h->opt.device < 0) return;  // host-only analysis mode (tests without a GPU)
     set_device(h);
     if (h->opt.stream) {

@@ -182,6 +182,28 @@ __global__ void __launch_bounds__(256)
   }
 }
 
+// G_k = L_II^-T L_PI^T (n_I x n_P, row-major): G[a][q] = sum_{m >= a} Linv[m][a] L_PI[q][m].
+// One CTA per (subdomain, 64-row chunk of G), warp per (a, q).
+__global__ void __launch_bounds__(256)
+    k_form_G(const SubDev* __restrict__ sub, const SnDev* __restrict__ sn, const double* __restrict__ ipool,
+             const double* __restrict__ lpi, double* __restrict__ G, int maxnt) {
+  const SubDev d = sub[blockIdx.x / maxnt];
+  const int chunk = blockIdx.x % maxnt;
+  if (d.nI == 0 || d.nP == 0 || chunk >= d.nt) return;
+  const SnDev s = sn[d.root];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int a0 = chunk * TB, na = min(TB, d.nI - a0);
+  for (int e = warp; e < na * d.nP; e += 8) {
+    const int a = a0 + e / d.nP, q = e % d.nP;
+    const double* Ic = ipool + s.inv_off + (long long)a * s.ldi;  // column a of L_II^-1
+    const double* lp = lpi + d.lpi_off + (long long)q * d.nI;
+    double acc = 0.0;
+    for (int m = a + lane; m < d.nI; m += 32) acc += Ic[m] * lp[m];
+    acc = warp_sum(acc);
+    if (lane == 0) G[d.g_off + (long long)a * d.nP + q] = acc;
+  }
+}
+
 // y_I (slot vector) <- the r_I rows of X
 __global__ void k_gather_I(const SubDev* __restrict__ sub, int nrhs, const double* __restrict__ X,
                            double* __restrict__ y) {
@@ -234,6 +256,10 @@ void run_coarse(ietidp_s* h) {
     k_pack<<<h->n_sub * maxnt, 256, 0, s>>>(h->d_sub.p, h->d_sn.p, h->d_rows.p, h->pool.p, h->ipool.p, h->tiles.p,
                                             h->itiles.p, h->lpi.p, maxnt);
     IETI_LAUNCHED(h);
+    if (ng > 0) {
+      k_form_G<<<h->n_sub * maxnt, 256, 0, s>>>(h->d_sub.p, h->d_sn.p, h->ipool.p, h->lpi.p, h->G.p, maxnt);
+      IETI_LAUNCHED(h);
+    }
   }
   // loads -> X (position order), forward sweep: X = L^-1 j, P rows = ftilde^(k)
   h->Xf.zero(s);

@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(POTRF_T) k_potrf(const Work* __restrict__ work
 //   A[r][k] = Ab[a_off + k*lda + r]   (column-major, r contiguous)
 //   BKC = false: B[k][n] = Bb[b_off + k*ldb + n]  (n contiguous: L^T of a front panel, Dinv^T)
 //   BKC = true:  B[k][n] = Bb[b_off + n*ldb + k]  (k contiguous: column-major B)
+//   ATR = true:  A[r][k] = Ab[a_off + r*lda + k]  (A given transposed, k contiguous)
 // ---------------------------------------------------------------------------
 constexpr int KC = 32, GST = 2, KS = 72;  // 2 stages: 74 KB smem, 3 CTAs/SM
 constexpr int GEMM_SMEM = GST * 2 * KC * KS * (int)sizeof(double);
@@ -211,7 +212,7 @@ __device__ __forceinline__ void load_rc(double* dst, const double* src, long lon
   }
 }
 
-template <bool BKC>
+template <bool BKC, bool ATR = false>
 __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work, const double* __restrict__ Ab,
                                               const double* __restrict__ Bb, double* __restrict__ Cb,
                                               const int* __restrict__ d_rel) {
@@ -227,7 +228,17 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
   auto Bs = [&](int st) { return sm + st * 2 * KC * KS + KC * KS; };
   auto load = [&](int st, int ch) {
     const int k0 = ch * KC, kb = min(KC, w.kdim - k0);
-    load_rc(As(st), Ab + w.a_off + (long long)k0 * w.lda, w.lda, kb, w.m, a16, tid);
+    if (!ATR) {
+      load_rc(As(st), Ab + w.a_off + (long long)k0 * w.lda, w.lda, kb, w.m, a16, tid);
+    } else {  // A[r][k] = Ab[a_off + r*lda + k] (k contiguous)
+      double* d = As(st);
+      for (int q = tid; q < KC * 64; q += 128) {
+        const int r = q >> 5, k = q & 31;
+        const int nv = (k < kb && r < w.m) ? 1 : 0;
+        const double* gp = Ab + (nv ? w.a_off + (long long)r * w.lda + k0 + k : 0);
+        cp_async_z8(d + k * KS + r, gp, nv * 8);
+      }
+    }
     if (!BKC) {
       load_rc(Bs(st), Bb + w.b_off + (long long)k0 * w.ldb, w.ldb, kb, w.n, b16, tid);
     } else {
@@ -319,6 +330,31 @@ __global__ void k_inv_copy(const Work* __restrict__ work, const SnDev* __restric
   }
 }
 
+// Pack the symmetric n_I x n_I matrix held in the lower triangle of a column-major
+// block (the r_I root front, or its L11^-1-shaped buffer) into row-major lower
+// TB-tiles with full (mirrored) diagonal tiles. One CTA per (entry, block row).
+__global__ void __launch_bounds__(256)
+    k_pack_sym(const int* __restrict__ list, int maxnt, const SubDev* __restrict__ sub, const SnDev* __restrict__ sn,
+               const double* __restrict__ base, int from_front, double* __restrict__ dst) {
+  const int e = blockIdx.x / maxnt, i = blockIdx.x % maxnt;
+  const int k = list ? list[e] : e;
+  const SubDev d = sub[k];
+  if (d.nI == 0 || i >= d.nt) return;
+  const SnDev s = sn[d.root];
+  const double* M = base + (from_front ? s.front_off : s.inv_off);
+  const long long ld = from_front ? s.ld : s.ldi;
+  for (int j = 0; j <= i; ++j) {
+    double* T = dst + d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
+    for (int q = threadIdx.x; q < TILE_ELEMS; q += blockDim.x) {
+      const int c = q / TB, r = q % TB;
+      const int R = i * TB + r, C = j * TB + c;
+      double v = 0.0;
+      if (R < d.nI && C < d.nI) v = (R >= C) ? M[(long long)C * ld + R] : M[(long long)R * ld + C];
+      T[r * TB + c] = v;
+    }
+  }
+}
+
 static void set_smem(const void* f, int bytes) {
   IETI_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
@@ -332,6 +368,7 @@ void run_factor(ietidp_s* h) {
     set_smem((const void*)k_potrf, sm_potrf);
     set_smem((const void*)k_gemm<false>, GEMM_SMEM);
     set_smem((const void*)k_gemm<true>, GEMM_SMEM);
+    set_smem((const void*)k_gemm<true, true>, GEMM_SMEM);
     attr = true;
   }
   static const int init_flags[2] = {INT_MAX, 1};  // failing subdomain (min), coarse OK
@@ -347,8 +384,18 @@ void run_factor(ietidp_s* h) {
     IETI_LAUNCHED(h);
   }
   const int* rel = h->d_rel.p;
+  int maxnt = 0;
+  for (auto& d : h->h_sub) maxnt = std::max(maxnt, d.nt);
+  const bool expl = h->opt.loop == IETIDP_LOOP_EXPLICIT;
   for (int L = 0; L <= P.max_level; ++L) {
     const LevelPlan& lp = P.levels[L];
+    // explicit loop: S_II is the assembled r_I root front before its factorisation
+    if (expl && h->rootlist_range[L].second > 0) {
+      k_pack_sym<<<h->rootlist_range[L].second * maxnt, 256, 0, st>>>(h->d_rootlist.p + h->rootlist_range[L].first,
+                                                                       maxnt, h->d_sub.p, h->d_sn.p, pool, 1,
+                                                                       h->stiles.p);
+      IETI_LAUNCHED(h);
+    }
     for (auto& pn : lp.panels) {
       if (pn.upd_n) {
         k_gemm<false><<<pn.upd_n, 128, GEMM_SMEM, st>>>(GW + pn.upd_off, pool, pool, pool, rel);
@@ -380,6 +427,13 @@ void run_factor(ietidp_s* h) {
     k_gemm<true><<<rg.second, 128, GEMM_SMEM, st>>>(GW + rg.first, step1 ? pool : h->ipool.p,
                                                     step1 ? h->ipool.p : h->tpool.p, step1 ? h->tpool.p : h->ipool.p,
                                                     rel);
+    IETI_LAUNCHED(h);
+  }
+  // explicit loop: W_k = L_II^-T L_II^-1 (lower tiles; tpool is free again)
+  if (expl && P.w_n) {
+    k_gemm<true, true><<<P.w_n, 128, GEMM_SMEM, st>>>(GW + P.w_off, h->ipool.p, h->ipool.p, h->tpool.p, rel);
+    IETI_LAUNCHED(h);
+    k_pack_sym<<<h->n_sub * maxnt, 256, 0, st>>>(nullptr, maxnt, h->d_sub.p, h->d_sn.p, h->tpool.p, 0, h->wtiles.p);
     IETI_LAUNCHED(h);
   }
   IETI_CHECK_LAUNCH();

@@ -95,8 +95,19 @@ struct ietidp_s {
   ieti::DevBuf<int> err_flag;             // [0] min failing subdomain (INT_MAX: none), [1] coarse ok
   // ---- loop ----
   ieti::DevBuf<double> tiles, itiles, lpi;  // packed L_II, L_II^-1 tiles; L_PI
+  ieti::DevBuf<double> wtiles, stiles, G;   // explicit loop: W = S_II^-1 and S_II tiles, G_k
+  ieti::DevBuf<double> spart;               // symmetric-pass partial blocks
+  ieti::DevBuf<int2> d_blk;                 // (subdomain, block) items of the partial reduction
+  int n_blk = 0;
+  ieti::DevBuf<int> d_rootlist;             // subdomains by level of their r_I root (for the S_II copy)
+  std::vector<std::pair<int, int>> rootlist_range;  // per level: (offset, count) into d_rootlist
+  ieti::DevBuf<long long> slot_goff;        // per r_I slot: its row of G_k
+  ieti::DevBuf<int> slot_np, slot_poff;     // per r_I slot: n_P of its subdomain, primal-row offset
   ieti::DevBuf<ieti::LoopWork> d_loopwork;
+  std::vector<ieti::LoopWork> h_loopwork;
   int n_loopwork = 0;
+  ieti::DevBuf<int> cta_ptr, cta_items;     // persistent PCG: work items per CTA
+  int lpt_grid = 0;
   ieti::DevBuf<int> sub_cta0, sub_ncta;   // loop CTAs of each subdomain
   ieti::DevBuf<ieti::LamDev> lam;
   ieti::DevBuf<int> slot_lam;             // per r_I slot: multiplier
@@ -104,6 +115,7 @@ struct ietidp_s {
   ieti::DevBuf<double> delta, kdiag;      // scaling weights per slot, K diagonal per slot
   ieti::DevBuf<double> d_vec, lam_vec, r_vec, p_vec, q_vec, z_vec;
   ieti::DevBuf<double> yI, xI, sI, zI;    // per-slot vectors (sum n_I x ncols)
+  ieti::DevBuf<double> pslot, rslot;      // persistent PCG: B^T p and B_D^T r in slot order
   ieti::DevBuf<double> gpart, zc;         // coarse partials per loop CTA; coarse solution
   ieti::DevBuf<double> partial;           // per-block dot partials
   ieti::DevBuf<double> state;             // PCG scalars (see pcg.cu)

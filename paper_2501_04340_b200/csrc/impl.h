@@ -46,7 +46,9 @@ struct SubDev {
   long long kval_off, f_off;   // raw CSR values / raw loads (nk x nrhs col-major)
   long long lpi_off;           // L_PI packed row-major nP x nI (zeros where not coupled)
   long long tile_off;          // packed L_II tiles (row-block order, TB x TB row-major)
-  long long itile_off;         // packed L_II^-1 tiles (same layout)
+  long long itile_off;         // packed L_II^-1 tiles (same layout; also W = S_II^-1 and S_II tiles)
+  long long g_off;             // G_k = L_II^-T L_PI^T: nI x nP row-major (explicit loop)
+  long long spart_off;         // symmetric-pass partial blocks: nt(nt-1)/2 blocks of TB x ncols
   int prim_off, perm_off, nt, cta0;  // primal rows, perm, #tile blocks, first loop CTA
 };
 
@@ -79,6 +81,7 @@ struct GemmWork {
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).
 struct LoopWork {
   int sub, nblk, blk0, blk1;
+  int cost;  // tiles streamed by the item (for the persistent kernel's balancing)
 };
 
 // ---------------------------------------------------------------------------
@@ -134,6 +137,8 @@ struct Plan {
   std::vector<int> level_sn;  // supernode ids grouped by level
   std::vector<LevelPlan> levels;
   std::vector<std::pair<int, int>> inv_rounds;  // GemmWork ranges: (offset, count), 2 per round
+  int w_off = 0, w_n = 0;                       // GemmWork: W = L_II^-T L_II^-1 lower tiles (explicit loop)
+  std::vector<std::vector<int>> roots_by_level; // subdomains whose r_I root front is at level L
   int inv_copy_off = 0, inv_copy_n = 0;         // Work items (sn, panel) copying Dinv into L11^-1
   long long pool_doubles = 0, dinv_doubles = 0, inv_doubles = 0, vec_rows = 0;
   int max_level = 0, max_front = 0, max_nI = 0, nPmax = 0;

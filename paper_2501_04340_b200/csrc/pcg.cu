@@ -68,12 +68,113 @@ struct TmvArgs {
   const double* z;         // BWD: coarse solution (n_primal x ncols) or null
   double zsign;
   double* vout;            // slot vector
-  double* gpart;           // FWD: coarse partials [cta][nPmax][ncols] (nullable)
+  double* gpart;           // FWD/SYM: coarse partials [cta][nPmax][ncols] (nullable)
+  const double* gmat;      // SYM: G_k (n_I x n_P row-major) for the coarse partials
+  double* spart;           // SYM: partial blocks of the transposed tile products
+  int slot_in;             // FWD/PRE1/SYM: vin is already in slot order (B^T, weights applied)
   int nPmax, ncols, c_off;
   const PcgState* st;
   const double* rr_part;   // PRE1 inside the loop: convergence test
   int check;
 };
+
+// Asynchronous gather of rows [lo, hi) of a slot-ordered vector (row-major,
+// A.ncols columns) into vec (stride VS, columns [0, ncl) of the chunk c_off):
+// cp.async of every element (8 bytes, 16 where aligned), zero padding written
+// directly. The caller commits it with the first tile prefetches.
+template <int VS>
+__device__ __forceinline__ void gather_async(double* vec, int lo, int hi, const SubDev& d, const TmvArgs& A, int ncl) {
+  const int tid = threadIdx.x;
+  const int nrow = hi - lo;
+  const bool pair16 = (ncl % 2 == 0) && (A.ncols % 2 == 0) && (A.c_off % 2 == 0) && (VS % 2 == 0);
+  if (pair16) {
+    const int hp = VS / 2;  // 16-byte pairs per row
+    for (int e = tid; e < nrow * hp; e += 256) {
+      const int a = lo + e / hp, cp = (e % hp) * 2;
+      double* dst = vec + (a - lo) * VS + cp;
+      if (a < d.nI && cp < ncl)
+        cp_async16(dst, A.vin + (d.rI_off + a) * (long long)A.ncols + A.c_off + cp);
+      else {
+        dst[0] = 0.0;
+        dst[1] = 0.0;
+      }
+    }
+  } else {
+    for (int e = tid; e < nrow * VS; e += 256) {
+      const int a = lo + e / VS, c = e % VS;
+      double* dst = vec + (a - lo) * VS + c;
+      if (a < d.nI && c < ncl) {
+        const unsigned sa = (unsigned)__cvta_generic_to_shared(dst);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa),
+                     "l"(A.vin + (d.rI_off + a) * (long long)A.ncols + A.c_off + c));
+      } else {
+        *dst = 0.0;
+      }
+    }
+  }
+}
+
+// Gather the input rows [lo, hi) of one subdomain into shared memory
+// (vec[(a - lo) * VS + c]): from the lambda-space vector through B^T (sign, optional
+// weight) when LAMBDA, else from a slot vector (plus, for BWD, zsign * L_PI^T z_k
+// with z_k staged in zs). VS == 1: thread per row; VS > 1: warp per row, lanes over
+// columns, slot metadata loaded once per row, four rows in flight per warp.
+template <int VS, bool LAMBDA, bool BWDZ>
+__device__ __forceinline__ void gather_rows(double* vec, int lo, int hi, const SubDev& d, const TmvArgs& A, int ncl,
+                                            const double* zs, int NCPz) {
+  const int tid = threadIdx.x;
+  if (VS == 1) {
+    for (int a = lo + tid; a < hi; a += 256) {
+      double v = 0.0;
+      if (a < d.nI && ncl > 0) {
+        const long long slot = d.rI_off + a;
+        if (LAMBDA) {
+          const double w = A.weight ? A.weight[slot] : 1.0;
+          v = (double)A.slot_sign[slot] * w * A.vin[(long long)A.slot_lam[slot] * A.ncols + A.c_off];
+        } else {
+          v = A.vin[slot * A.ncols + A.c_off];
+          if (BWDZ) {
+            const double* lp = A.lpi + d.lpi_off + a;
+            double s2 = 0.0;
+#pragma unroll 4
+            for (int q = 0; q < d.nP; ++q) s2 += lp[(long long)q * d.nI] * zs[q * NCPz];
+            v += A.zsign * s2;
+          }
+        }
+      }
+      vec[a - lo] = v;
+    }
+    return;
+  }
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int a0 = lo + warp * 4; a0 < hi; a0 += 32) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int a = a0 + u;
+      v[u] = 0.0;
+      if (a < hi && a < d.nI && lane < ncl) {
+        const long long slot = d.rI_off + a;
+        if (LAMBDA) {
+          const double w = A.weight ? A.weight[slot] : 1.0;
+          v[u] = (double)A.slot_sign[slot] * w * A.vin[(long long)A.slot_lam[slot] * A.ncols + A.c_off + lane];
+        } else {
+          v[u] = A.vin[slot * A.ncols + A.c_off + lane];
+          if (BWDZ) {
+            const double* lp = A.lpi + d.lpi_off + a;
+            double s2 = 0.0;
+#pragma unroll 4
+            for (int q = 0; q < d.nP; ++q) s2 += lp[(long long)q * d.nI] * zs[q * NCPz + lane];
+            v[u] += A.zsign * s2;
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (a0 + u < hi && lane < VS) vec[(a0 + u - lo) * VS + lane] = v[u];
+  }
+}
 
 // One work item (subdomain block pair) of a tile-streamed operator.
 template <int MODE, int NCP, int STAGES>
@@ -99,27 +200,17 @@ __device__ __forceinline__ void tmv_item(const TmvArgs& A, int item, double* sme
   double* outb = vec + (hi - lo) * VS;       // one finished output block (FWD partials)
 
   // ---- input vector ----
-  for (int e = tid; e < (hi - lo) * VS; e += 256) {
-    const int a = lo + e / VS, c = e % VS;
-    double v = 0.0;
-    if (a < d.nI && c < ncl) {
-      const long long slot = d.rI_off + a;
-      if (MODE == FWD || MODE == PRE1) {
-        const double w = (MODE == PRE1 && A.weight) ? A.weight[slot] : 1.0;
-        v = (double)A.slot_sign[slot] * w * A.vin[(long long)A.slot_lam[slot] * A.ncols + A.c_off + c];
-      } else {
-        v = A.vin[slot * A.ncols + A.c_off + c];
-        if (MODE == BWD && A.z) {
-          const double* lp = A.lpi + d.lpi_off + a;
-          double s = 0.0;
-          for (int q = 0; q < d.nP; ++q)
-            s += lp[(long long)q * d.nI] * A.z[(long long)A.prim_gid[d.prim_off + q] * A.ncols + A.c_off + c];
-          v += A.zsign * s;
-        }
-      }
+  double* zs = outb + TB * VS;  // BWD: z_k (nP x NCP)
+  if (MODE == BWD && A.z) {
+    for (int e = tid; e < d.nP * NCP; e += 256) {
+      const int q = e / NCP, c = e % NCP;
+      zs[e] = c < ncl ? A.z[(long long)A.prim_gid[d.prim_off + q] * A.ncols + A.c_off + c] : 0.0;
     }
-    vec[e] = v;
+    __syncthreads();
   }
+  if ((MODE == FWD || MODE == PRE1) && !A.slot_in) gather_rows<VS, true, false>(vec, lo, hi, d, A, ncl, zs, NCP);
+  else if (MODE == BWD && A.z) gather_rows<VS, false, true>(vec, lo, hi, d, A, ncl, zs, NCP);
+  else gather_async<VS>(vec, lo, hi, d, A, ncl);  // committed with the first tile
   // ---- tile schedule: per output block o, N: (o, 0..o), T: (o..nt-1, o) ----
   auto ntiles_of = [&](int o) { return TRANS ? nt - o : o + 1; };
   const int n0 = ntiles_of(ob[0]);
@@ -229,11 +320,18 @@ __device__ __forceinline__ void tmv_item(const TmvArgs& A, int item, double* sme
         const int a = o * TB + r;
         if (a < d.nI) A.vout[(d.rI_off + a) * A.ncols + A.c_off + c] = outb[r * VS + c];
       }
-      if (MODE == FWD && A.gpart && tid < d.nP * NCP) {
-        const int q = tid / NCP, c = tid % NCP;
-        const double* lp = A.lpi + d.lpi_off + (long long)q * d.nI + o * TB;
+      if (MODE == FWD && A.gpart && d.nP > 0) {
+        double* gs = outb + TB * VS;  // nP x TB (L_PI columns of this block)
         const int na = min(TB, d.nI - o * TB);
-        for (int r = 0; r < na; ++r) gacc += lp[r] * outb[r * VS + c];
+        for (int e = tid; e < d.nP * TB; e += 256) {
+          const int q = e / TB, r = e % TB;
+          gs[e] = r < na ? A.lpi[d.lpi_off + (long long)q * d.nI + o * TB + r] : 0.0;
+        }
+        __syncthreads();
+        if (tid < d.nP * NCP) {
+          const int q = tid / NCP, c = tid % NCP;
+          for (int r = 0; r < na; ++r) gacc += gs[q * TB + r] * outb[r * VS + c];
+        }
       }
       __syncthreads();
     }
@@ -243,6 +341,195 @@ __device__ __forceinline__ void tmv_item(const TmvArgs& A, int item, double* sme
     const int q = tid / NCP, c = tid % NCP;
     if (c < ncl) A.gpart[((long long)item * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
   }
+}
+
+// One work item of a symmetric matrix held as lower TB-tiles (diagonal tiles full):
+// y = S x in ONE pass. For each own block row o, tile (o, j) contributes S_oj x_j to
+// y_o (kept in registers) and, for j < o, S_oj^T x_o to y_j (written as partial
+// block (o, j), summed later in a fixed order by sym_reduce). The input x is
+// gathered from the lambda-space vector (sign, optional weight); the F-apply also
+// accumulates the coarse partial G_k^T x of its own rows.
+template <int NCP, int STAGES>
+__device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* smem) {
+  constexpr int VS = (NCP == 1) ? 1 : NCP + 4;
+  constexpr int NB = (NCP == 1) ? 1 : NCP / 8;
+  __shared__ double red[8][TB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ncl = min(NCP, A.ncols - A.c_off);
+  __syncthreads();
+  const LoopWork lw = A.work[item];
+  const SubDev d = A.sub[lw.sub];
+  const int ob[2] = {lw.blk0, lw.blk1};
+  const int nob = lw.nblk;
+  const int bmax = max(ob[0], ob[nob - 1]);
+  const int hi = (bmax + 1) * TB;
+  double* ring = smem;
+  double* vec = smem + STAGES * TILE_ELEMS;  // rows [0, hi)
+  double* outb = vec + hi * VS;
+  if (A.slot_in) gather_async<VS>(vec, 0, hi, d, A, ncl);  // committed with the first tile
+  else gather_rows<VS, true, false>(vec, 0, hi, d, A, ncl, nullptr, NCP);
+  const int n0 = ob[0] + 1;
+  const int nsteps = n0 + (nob == 2 ? ob[1] + 1 : 0);
+  auto tile_ptr = [&](int s) {
+    const int which = s < n0 ? 0 : 1;
+    const int o = ob[which], j = which ? s - n0 : s;
+    return A.tiles + d.tile_off + (long long)(o * (o + 1) / 2 + j) * TILE_ELEMS;
+  };
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; ++s) {
+    if (s < nsteps) load_tile_async(ring + s * TILE_ELEMS, tile_ptr(s), tid);
+    cp_async_commit();
+  }
+  cp_async_wait<STAGES - 2>();  // group 0: the gathered input and tile 0
+  __syncthreads();              // vec complete
+  // coarse partial: G_k^T x over the own block rows (G rows staged in smem)
+  double gacc = 0.0;
+  if (A.gpart && d.nP > 0) {
+    double* gs = outb + TB * VS;  // TB x nP
+    for (int w2 = 0; w2 < nob; ++w2) {
+      const int o = ob[w2];
+      const int na = min(TB, d.nI - o * TB);
+      const double* Gb = A.gmat + d.g_off + (long long)o * TB * d.nP;
+      for (int e = tid; e < na * d.nP; e += 256) gs[e] = Gb[e];
+      __syncthreads();
+      if (tid < d.nP * NCP) {
+        const int q = tid / NCP, c = tid % NCP;
+        for (int r = 0; r < na; ++r) gacc += gs[r * d.nP + q] * vec[(o * TB + r) * VS + c];
+      }
+      __syncthreads();
+    }
+  }
+  double accN[8], acc[NB][2];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) accN[i] = 0.0;
+#pragma unroll
+  for (int i = 0; i < NB; ++i) acc[i][0] = acc[i][1] = 0.0;
+  const int g = lane >> 2, t4 = lane & 3;
+  for (int s = 0; s < nsteps; ++s) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();
+    {
+      const int sn = s + STAGES - 1;
+      if (sn < nsteps) load_tile_async(ring + (sn % STAGES) * TILE_ELEMS, tile_ptr(sn), tid);
+      cp_async_commit();
+    }
+    const double* Tt = ring + (s % STAGES) * TILE_ELEMS;
+    const int which = s < n0 ? 0 : 1;
+    const int o = ob[which], j = which ? s - n0 : s;
+    const bool last = (j == o);
+    const double* xj = vec + j * TB * VS;
+    const double* xo = vec + o * TB * VS;
+    double* pblk = A.spart + ((d.spart_off + (long long)o * (o - 1) / 2 + j) * TB) * A.ncols + A.c_off;
+    if constexpr (NCP == 1) {
+      {  // N: y_o += S_oj x_j
+        const double x0 = xj[lane], x1 = xj[lane + 32];
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int r = warp * 8 + rr;
+          accN[rr] += Tt[swz(r, lane)] * x0 + Tt[swz(r, lane + 32)] * x1;
+        }
+      }
+      if (!last) {  // T: partial (o, j) = S_oj^T x_o
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) {
+          const int r = warp * 8 + rr;
+          const double xr = xo[r];
+          p0 += Tt[swz(r, lane)] * xr;
+          p1 += Tt[swz(r, lane + 32)] * xr;
+        }
+        red[warp][lane] = p0;
+        red[warp][lane + 32] = p1;
+        __syncthreads();
+        if (tid < TB) {
+          double v = 0.0;
+#pragma unroll
+          for (int w2 = 0; w2 < 8; ++w2) v += red[w2][tid];
+          pblk[(long long)tid * A.ncols] = v;
+        }
+      } else {
+        double full[8];
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) full[rr] = warp_sum(accN[rr]);
+        if (lane < 8) {
+          double v = full[0];
+#pragma unroll
+          for (int rr = 1; rr < 8; ++rr)
+            if (lane == rr) v = full[rr];
+          const int a = o * TB + warp * 8 + lane;
+          if (a < d.nI) A.vout[(d.rI_off + a) * A.ncols + A.c_off] = v;
+        }
+#pragma unroll
+        for (int rr = 0; rr < 8; ++rr) accN[rr] = 0.0;
+      }
+    } else {
+#pragma unroll 4
+      for (int k0 = 0; k0 < TB; k0 += 4) {
+        const double a = Tt[swz(warp * 8 + g, k0 + t4)];
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) dmma8x8x4(acc[nb][0], acc[nb][1], a, xj[(k0 + t4) * VS + nb * 8 + g]);
+      }
+      if (!last) {
+        double pt[NB][2];
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb) pt[nb][0] = pt[nb][1] = 0.0;
+#pragma unroll 4
+        for (int k0 = 0; k0 < TB; k0 += 4) {
+          const double a = Tt[swz(k0 + t4, warp * 8 + g)];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma8x8x4(pt[nb][0], pt[nb][1], a, xo[(k0 + t4) * VS + nb * 8 + g]);
+        }
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int c = nb * 8 + 2 * t4 + q;
+            if (c < ncl) pblk[(long long)(warp * 8 + g) * A.ncols + c] = pt[nb][q];
+          }
+      } else {
+#pragma unroll
+        for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            const int c = nb * 8 + 2 * t4 + q;
+            const int a = o * TB + warp * 8 + g;
+            if (c < ncl && a < d.nI) A.vout[(d.rI_off + a) * A.ncols + A.c_off + c] = acc[nb][q];
+            acc[nb][q] = 0.0;
+          }
+      }
+    }
+  }
+  cp_async_wait<0>();
+  if (A.gpart && tid < d.nP * NCP) {
+    const int q = tid / NCP, c = tid % NCP;
+    if (c < ncl) A.gpart[((long long)item * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
+  }
+  (void)outb;
+}
+
+// y_j += sum_{i > j} partial (i, j), for one (subdomain, block) work item.
+__device__ __forceinline__ void sym_reduce_item(const TmvArgs& A, int k, int j) {
+  const SubDev d = A.sub[k];
+  const int nc = A.ncols;
+  for (int e = threadIdx.x; e < TB * nc; e += 256) {
+    const int r = e / nc, c = e - r * nc;
+    const int a = j * TB + r;
+    if (a >= d.nI) continue;
+    double v = 0.0;
+    for (int i = j + 1; i < d.nt; ++i) v += A.spart[((d.spart_off + (long long)i * (i - 1) / 2 + j) * TB + r) * nc + c];
+    A.vout[(d.rI_off + a) * nc + c] += v;
+  }
+}
+
+template <int NCP, int STAGES>
+__global__ void __launch_bounds__(256, 1) k_sym(const TmvArgs A) {
+  extern __shared__ __align__(16) double smem[];
+  sym_item<NCP, STAGES>(A, blockIdx.x, smem);
+}
+
+__global__ void __launch_bounds__(256) k_sym_reduce(const TmvArgs A, const int2* __restrict__ blk) {
+  const int2 kb = blk[blockIdx.x];
+  sym_reduce_item(A, kb.x, kb.y);
 }
 
 template <int MODE, int NCP, int STAGES>
@@ -288,11 +575,27 @@ __device__ void block_col_reduce(double v, int ncols, int P2, double* partial) {
   if (tid < ncols) partial[blockIdx.x * ncols + tid] = red[tid];
 }
 
-// out[j][c] = sum_{2 slots} sign * w * x[slot][c]   (+ partial dot with dotv)
+// out[j][c] = sum_{2 slots} sign * w * (x[slot][c] + G_k[slot row] . z[C_k^T][c])
+// (+ partial dot with dotv). The coarse term is the explicit loop's G_k z.
+struct CoarseTerm {
+  const long long* goff;
+  const int *np, *poff, *prim_gid;
+  const double *G, *z;
+};
+
+__device__ __forceinline__ double coarse_term(const CoarseTerm& ct, int a, int ncols, int c) {
+  const int np = ct.np[a];
+  const double* Gr = ct.G + ct.goff[a];
+  const int* gid = ct.prim_gid + ct.poff[a];
+  double s = 0.0;
+  for (int q = 0; q < np; ++q) s += Gr[q] * ct.z[(long long)gid[q] * ncols + c];
+  return s;
+}
+
 __global__ void __launch_bounds__(VT)
     k_bgather(int m, int ncols, const LamDev* __restrict__ lam, const double* __restrict__ x,
               const double* __restrict__ weight, double* __restrict__ out, const double* __restrict__ dotv,
-              double* __restrict__ partial, const PcgState* __restrict__ st) {
+              double* __restrict__ partial, const PcgState* __restrict__ st, CoarseTerm ct) {
   if (st && st->done) return;
   const int P2 = pow2ge(ncols);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
@@ -304,7 +607,9 @@ __global__ void __launch_bounds__(VT)
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int a = L.slot[q];
-        val += (double)L.sign[q] * (weight ? weight[a] : 1.0) * x[(long long)a * ncols + c];
+        double xv = x[(long long)a * ncols + c];
+        if (ct.z) xv += coarse_term(ct, a, ncols, c);
+        val += (double)L.sign[q] * (weight ? weight[a] : 1.0) * xv;
       }
       out[(long long)j * ncols + c] = val;
       if (dotv) dot += val * dotv[(long long)j * ncols + c];
@@ -529,12 +834,16 @@ __global__ void k_transpose(int rows, int ncols, const double* __restrict__ in, 
 // per-CTA partials, so all CTAs take identical decisions (bit-reproducible).
 // ---------------------------------------------------------------------------
 struct PcgArgs {
-  TmvArgs fwd, bwd, pre1, pre2;
+  TmvArgs fwd, bwd, pre1, pre2;  // triangular loop
+  TmvArgs wsym, ssym;            // explicit loop: W = S_II^-1, S_II
+  CoarseTerm ct;                 // explicit loop: G_k z in the gather
+  const int2* blk;               // (subdomain, block) items of the partial reduction
   const LamDev* lam;
   const double* delta;
   double *lamv, *r, *p, *q, *z;
   const double* d;
-  const double *xI, *zI;
+  double *xI, *zI;
+  double *pslot, *rslot;  // B^T p and B_D^T r in slot order (operator inputs)
   const int *pcon_ptr, *pcon_sub, *pcon_q, *sub_cta0, *sub_ncta;
   const double *gpart, *Sinv;
   double* zc;
@@ -542,7 +851,8 @@ struct PcgArgs {
   PcgState* st;
   unsigned* bar;  // [0] arrivals, [1] generation
   double tol;
-  int m, ncols, ng, nPmax, max_iter, fixed, n_items, ncp;
+  int m, ncols, ng, nPmax, max_iter, fixed, n_items, ncp, n_blk;
+  const int *cta_ptr, *cta_items;  // this CTA's work items (tile-balanced, longest first)
 };
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
@@ -571,16 +881,59 @@ __device__ __forceinline__ double colsum(const double* part, int c, int ncols) {
 }
 
 template <int MODE, int NCP, int STAGES>
-__device__ __forceinline__ void tmv_phase(TmvArgs A, int n_items, int ncp, double* smem) {
+__device__ __forceinline__ void tmv_phase(TmvArgs A, const int* cta_ptr, const int* cta_items, int ncp, double* smem) {
   for (int c0 = 0; c0 < A.ncols; c0 += ncp) {
     A.c_off = c0;
-    for (int it = blockIdx.x; it < n_items; it += gridDim.x) tmv_item<MODE, NCP, STAGES>(A, it, smem);
+    for (int e = cta_ptr[blockIdx.x]; e < cta_ptr[blockIdx.x + 1]; ++e)
+      tmv_item<MODE, NCP, STAGES>(A, cta_items[e], smem);
   }
 }
 
-// out = sum_k B (w) x, with the per-CTA partial of out . dotv
+template <int NCP, int STAGES>
+__device__ __forceinline__ void sym_phase(TmvArgs A, const int* cta_ptr, const int* cta_items, int ncp, double* smem) {
+  for (int c0 = 0; c0 < A.ncols; c0 += ncp) {
+    A.c_off = c0;
+    for (int e = cta_ptr[blockIdx.x]; e < cta_ptr[blockIdx.x + 1]; ++e) sym_item<NCP, STAGES>(A, cta_items[e], smem);
+  }
+}
+
+__device__ __forceinline__ void reduce_phase(const TmvArgs& A, const int2* blk, int n_blk) {
+  for (int it = blockIdx.x; it < n_blk; it += gridDim.x) {
+    const int2 kb = blk[it];
+    sym_reduce_item(A, kb.x, kb.y);
+  }
+}
+
+// z = S_PP^-1 sum of the coarse partials: every CTA assembles g, each computes a
+// slice of the rows of z.
+__device__ __forceinline__ void coarse_phase(const PcgArgs& P, double* smem) {
+  const int nc = P.ncols, tid = threadIdx.x, nb = gridDim.x;
+  double* g = smem;  // ng x nc
+  __syncthreads();
+  for (int e = tid; e < P.ng * nc; e += VT) {
+    const int gi = e / nc, c = e - gi * nc;
+    double sacc = 0.0;
+    for (int q = P.pcon_ptr[gi]; q < P.pcon_ptr[gi + 1]; ++q) {
+      const int k = P.pcon_sub[q], lq = P.pcon_q[q];
+      for (int cta = P.sub_cta0[k]; cta < P.sub_cta0[k] + P.sub_ncta[k]; ++cta)
+        sacc += P.gpart[((long long)cta * P.nPmax + lq) * nc + c];
+    }
+    g[e] = sacc;
+  }
+  __syncthreads();
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int e = blockIdx.x * 8 + warp; e < P.ng * nc; e += nb * 8) {
+    const int i = e / nc, c = e - i * nc;
+    double sacc = 0.0;
+    for (int j = lane; j < P.ng; j += 32) sacc += P.Sinv[(long long)i * P.ng + j] * g[j * nc + c];
+    sacc = warp_sum(sacc);
+    if (lane == 0) P.zc[e] = sacc;
+  }
+}
+
+// out = sum_k B (w) (x + G z), with the per-CTA partial of out . dotv
 __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x, const double* w, double* out,
-                                              const double* dotv, double* part) {
+                                              const double* dotv, double* part, bool coarse) {
   const int nc = P.ncols, P2 = pow2ge(nc);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
   double dot = 0.0;
@@ -591,7 +944,9 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int a = L.slot[q];
-        val += (double)L.sign[q] * (w ? w[a] : 1.0) * x[(long long)a * nc + c];
+        double xv = x[(long long)a * nc + c];
+        if (coarse) xv += coarse_term(P.ct, a, nc, c);
+        val += (double)L.sign[q] * (w ? w[a] : 1.0) * xv;
       }
       out[(long long)j * nc + c] = val;
       dot += val * dotv[(long long)j * nc + c];
@@ -599,8 +954,56 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
   block_col_reduce(dot, nc, P2, part);
 }
 
-template <int NCP, int STAGES>
-__global__ void __launch_bounds__(256, 1) k_pcg(const PcgArgs P) {
+// write B^T v (optionally weighted) of lambda-row j, column c into the slot vector
+__device__ __forceinline__ void to_slots(const PcgArgs& P, long long j, int c, double v, const double* w, double* out) {
+  const LamDev L = P.lam[j];
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {
+    const int a = L.slot[q];
+    out[(long long)a * P.ncols + c] = (double)L.sign[q] * (w ? w[a] : 1.0) * v;
+  }
+}
+
+template <int NCP, int STAGES, bool EXPL>
+__device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, double* pq) {
+  if (EXPL) {
+    sym_phase<NCP, STAGES>(P.wsym, P.cta_ptr, P.cta_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    reduce_phase(P.wsym, P.blk, P.n_blk);
+    if (P.ng > 0) coarse_phase(P, smem);
+    grid_barrier(P.bar);
+    bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0);
+  } else {
+    tmv_phase<FWD, NCP, STAGES>(P.fwd, P.cta_ptr, P.cta_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    if (P.ng > 0) {
+      coarse_phase(P, smem);
+      grid_barrier(P.bar);
+    }
+    tmv_phase<BWD, NCP, STAGES>(P.bwd, P.cta_ptr, P.cta_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, false);
+  }
+}
+
+template <int NCP, int STAGES, bool EXPL>
+__device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, double* rz) {
+  if (EXPL) {
+    sym_phase<NCP, STAGES>(P.ssym, P.cta_ptr, P.cta_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    reduce_phase(P.ssym, P.blk, P.n_blk);
+    grid_barrier(P.bar);
+  } else {
+    tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.cta_ptr, P.cta_items, P.ncp, smem);
+    grid_barrier(P.bar);
+    tmv_phase<PRE2, NCP, STAGES>(P.pre2, P.cta_ptr, P.cta_items, P.ncp, smem);
+    grid_barrier(P.bar);
+  }
+  bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false);
+}
+
+template <int NCP, int STAGES, bool EXPL>
+__global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double s_rz[IETIDP_MAX_RHS], s_r0[IETIDP_MAX_RHS], s_coef[IETIDP_MAX_RHS];
   __shared__ int s_act[IETIDP_MAX_RHS], s_new[IETIDP_MAX_RHS], s_iters[IETIDP_MAX_RHS];
@@ -613,15 +1016,16 @@ __global__ void __launch_bounds__(256, 1) k_pcg(const PcgArgs P) {
   const int cc = tid % P2, rl = tid / P2, R = VT / P2;
   auto rows = [&](auto&& f) {  // this CTA's share of the lambda-space rows, column cc
     if (cc < nc)
-      for (int j = blockIdx.x * R + rl; j < m; j += nb * R) f((long long)j * nc + cc);
+      for (int j = blockIdx.x * R + rl; j < m; j += nb * R) f((long long)j * nc + cc, j);
   };
   // ---- init: lambda = 0, r = d, r0 = ||d|| ----
   {
     double acc = 0.0;
-    rows([&](long long e) {
+    rows([&](long long e, int j) {
       P.lamv[e] = 0.0;
       const double dv = P.d[e];
       P.r[e] = dv;
+      to_slots(P, j, cc, dv, P.delta, P.rslot);
       acc += dv * dv;
     });
     block_col_reduce(acc, nc, P2, rr);
@@ -640,46 +1044,18 @@ __global__ void __launch_bounds__(256, 1) k_pcg(const PcgArgs P) {
   if (!P.fixed && P.max_iter <= 0) run = false;
   if (run) {
     // z = M r, rz = r.z, p = z
-    tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.n_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    tmv_phase<PRE2, NCP, STAGES>(P.pre2, P.n_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    bgather_phase(P, P.zI, P.delta, P.z, P.r, rz);
+    apply_M_phases<NCP, STAGES, EXPL>(P, smem, rz);
     grid_barrier(P.bar);
     if (tid < nc) s_rz[tid] = colsum(rz, tid, nc);
-    rows([&](long long e) { P.p[e] = P.z[e]; });
+    rows([&](long long e, int j) {
+      const double zv = P.z[e];
+      P.p[e] = zv;
+      to_slots(P, j, cc, zv, nullptr, P.pslot);
+    });
     grid_barrier(P.bar);
   }
   while (run) {
-    // q = F p
-    tmv_phase<FWD, NCP, STAGES>(P.fwd, P.n_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    if (P.ng > 0) {
-      double* g = smem;  // ng x nc
-      for (int e = tid; e < P.ng * nc; e += VT) {
-        const int gi = e / nc, c = e - gi * nc;
-        double sacc = 0.0;
-        for (int q = P.pcon_ptr[gi]; q < P.pcon_ptr[gi + 1]; ++q) {
-          const int k = P.pcon_sub[q], lq = P.pcon_q[q];
-          for (int cta = P.sub_cta0[k]; cta < P.sub_cta0[k] + P.sub_ncta[k]; ++cta)
-            sacc += P.gpart[((long long)cta * P.nPmax + lq) * nc + c];
-        }
-        g[e] = sacc;
-      }
-      __syncthreads();
-      const int warp = tid >> 5, lane = tid & 31;
-      for (int e = blockIdx.x * 8 + warp; e < P.ng * nc; e += nb * 8) {
-        const int i = e / nc, c = e - i * nc;
-        double sacc = 0.0;
-        for (int j = lane; j < P.ng; j += 32) sacc += P.Sinv[(long long)i * P.ng + j] * g[j * nc + c];
-        sacc = warp_sum(sacc);
-        if (lane == 0) P.zc[e] = sacc;
-      }
-      grid_barrier(P.bar);
-    }
-    tmv_phase<BWD, NCP, STAGES>(P.bwd, P.n_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    bgather_phase(P, P.xI, nullptr, P.q, P.p, pq);
+    apply_F_phases<NCP, STAGES, EXPL>(P, smem, pq);  // q = F p
     grid_barrier(P.bar);
     // alpha, lambda and r
     if (tid < nc) s_coef[tid] = s_act[tid] ? s_rz[tid] / colsum(pq, tid, nc) : 0.0;
@@ -688,13 +1064,14 @@ __global__ void __launch_bounds__(256, 1) k_pcg(const PcgArgs P) {
       double acc = 0.0;
       const bool act = cc < nc && s_act[cc];
       const double a = cc < nc ? s_coef[cc] : 0.0;
-      rows([&](long long e) {
+      rows([&](long long e, int j) {
         double rv = P.r[e];
         if (act) {
           P.lamv[e] += a * P.p[e];
           rv -= a * P.q[e];
           P.r[e] = rv;
         }
+        to_slots(P, j, cc, rv, P.delta, P.rslot);
         acc += rv * rv;
       });
       block_col_reduce(acc, nc, P2, rr);
@@ -716,12 +1093,7 @@ __global__ void __launch_bounds__(256, 1) k_pcg(const PcgArgs P) {
       if (tid < nc) s_act[tid] = s_new[tid];
       break;
     }
-    // z = M r
-    tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.n_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    tmv_phase<PRE2, NCP, STAGES>(P.pre2, P.n_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    bgather_phase(P, P.zI, P.delta, P.z, P.r, rz);
+    apply_M_phases<NCP, STAGES, EXPL>(P, smem, rz);  // z = M r
     grid_barrier(P.bar);
     // beta, p
     if (tid < nc) {
@@ -733,8 +1105,13 @@ __global__ void __launch_bounds__(256, 1) k_pcg(const PcgArgs P) {
     {
       const bool act = cc < nc && s_new[cc];
       const double bta = cc < nc ? s_coef[cc] : 0.0;
-      rows([&](long long e) {
-        if (act) P.p[e] = P.z[e] + bta * P.p[e];
+      rows([&](long long e, int j) {
+        double pv = P.p[e];
+        if (act) {
+          pv = P.z[e] + bta * pv;
+          P.p[e] = pv;
+        }
+        to_slots(P, j, cc, pv, nullptr, P.pslot);
       });
     }
     if (tid < nc) s_act[tid] = s_new[tid];
@@ -762,16 +1139,49 @@ struct TmvCfg {
 
 static TmvCfg tmv_cfg(const ietidp_s* h, int ncols) {
   const int nt = (h->plan.max_nI + TB - 1) / TB;
-  if (ncols == 1) return {1, 5, (5 * TILE_ELEMS + nt * TB + TB) * 8};
+  if (ncols == 1) {
+    // many work items: 3 stages (two CTAs per SM hide each other's barriers);
+    // few (C2: 128 items): 5 stages, one deep-pipelined CTA per SM
+    int st = h->n_loopwork >= 2 * 148 ? 3 : 5;
+    if (getenv("IETIDP_STAGES1")) st = atoi(getenv("IETIDP_STAGES1")) == 5 ? 5 : 3;
+    return {1, st, (st * TILE_ELEMS + nt * TB + TB + TB * 16) * 8};
+  }
   for (int ncp : {16, 8}) {
     if (ncp == 16 && ncols <= 8) continue;
     const int vs = ncp + 4;
     for (int stages = 3; stages >= 2; --stages) {
-      int bytes = (stages * TILE_ELEMS + nt * TB * vs + TB * vs) * 8;
+      int bytes = (stages * TILE_ELEMS + nt * TB * vs + TB * vs + TB * 16) * 8;
       if (bytes <= 210 * 1024) return {ncp, stages, bytes};
     }
   }
   throw Error(IETIDP_E_ARG, "interface block too large for the shared-memory loop kernels");
+}
+
+static TmvArgs sym_args(ietidp_s* h, const double* tiles, int ncols) {
+  TmvArgs a{};
+  a.work = h->d_loopwork.p;
+  a.sub = h->d_sub.p;
+  a.tiles = tiles;
+  a.slot_lam = h->slot_lam.p;
+  a.slot_sign = h->slot_sign.p;
+  a.prim_gid = h->d_prim_gid.p;
+  a.gmat = h->G.p;
+  a.spart = h->spart.p;
+  a.nPmax = std::max(h->plan.nPmax, 1);
+  a.ncols = ncols;
+  return a;
+}
+
+static CoarseTerm coarse_term_args(ietidp_s* h) {
+  CoarseTerm ct{};
+  if (h->n_primal == 0) return ct;
+  ct.goff = h->slot_goff.p;
+  ct.np = h->slot_np.p;
+  ct.poff = h->slot_poff.p;
+  ct.prim_gid = h->d_prim_gid.p;
+  ct.G = h->G.p;
+  ct.z = h->zc.p;
+  return ct;
 }
 
 template <int MODE, int NCP, int STAGES>
@@ -796,7 +1206,8 @@ static void launch_tmv(ietidp_s* h, TmvArgs a) {
   a.nPmax = std::max(h->plan.nPmax, 1);
   for (int c0 = 0; c0 < a.ncols; c0 += cfg.ncp) {
     a.c_off = c0;
-    if (cfg.ncp == 1) launch_tmv_t<MODE, 1, 5>(h, cfg, a);
+    if (cfg.ncp == 1 && cfg.stages == 5) launch_tmv_t<MODE, 1, 5>(h, cfg, a);
+    else if (cfg.ncp == 1) launch_tmv_t<MODE, 1, 3>(h, cfg, a);
     else if (cfg.ncp == 16 && cfg.stages == 3) launch_tmv_t<MODE, 16, 3>(h, cfg, a);
     else if (cfg.ncp == 16) launch_tmv_t<MODE, 16, 2>(h, cfg, a);
     else if (cfg.stages == 3) launch_tmv_t<MODE, 8, 3>(h, cfg, a);
@@ -837,7 +1248,8 @@ void bgather(ietidp_s* h, int ncols, const double* x, const double* weight, doub
              double* partial, const void* stv) {
   const PcgState* st = static_cast<const PcgState*>(stv);
   if (h->n_lambda == 0) return;
-  k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, x, weight, out, dotv, partial, st);
+  k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, x, weight, out, dotv, partial, st,
+                                        CoarseTerm{});
   IETI_LAUNCHED(h);
 }
 
@@ -854,10 +1266,50 @@ void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const vo
   IETI_LAUNCHED(h);
 }
 
+template <int NCP, int STAGES>
+static void launch_sym_t(ietidp_s* h, const TmvCfg& cfg, TmvArgs a) {
+  auto kern = k_sym<NCP, STAGES>;
+  IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
+  kern<<<h->n_loopwork, 256, cfg.smem, h->stream>>>(a);
+  IETI_LAUNCHED(h);
+}
+
+// y = S x for the symmetric tile matrix `tiles` (explicit loop), into the slot vector a.vout
+static void sym_apply(ietidp_s* h, TmvArgs a) {
+  if (h->n_loopwork == 0) return;
+  const TmvCfg cfg = tmv_cfg(h, a.ncols);
+  for (int c0 = 0; c0 < a.ncols; c0 += cfg.ncp) {
+    a.c_off = c0;
+    if (cfg.ncp == 1 && cfg.stages == 5) launch_sym_t<1, 5>(h, cfg, a);
+    else if (cfg.ncp == 1) launch_sym_t<1, 3>(h, cfg, a);
+    else if (cfg.ncp == 16 && cfg.stages == 3) launch_sym_t<16, 3>(h, cfg, a);
+    else if (cfg.ncp == 16) launch_sym_t<16, 2>(h, cfg, a);
+    else if (cfg.stages == 3) launch_sym_t<8, 3>(h, cfg, a);
+    else launch_sym_t<8, 2>(h, cfg, a);
+  }
+  a.c_off = 0;
+  if (h->n_blk) {
+    k_sym_reduce<<<h->n_blk, 256, 0, h->stream>>>(a, h->d_blk.p);
+    IETI_LAUNCHED(h);
+  }
+}
+
 // y = F_DP x (interleaved, ncols columns)
 static void apply_F_inter(ietidp_s* h, int ncols, const double* x, double* y, const PcgState* st, const double* dotv,
                           double* partial) {
   if (h->n_lambda == 0) return;
+  if (h->opt.loop == IETIDP_LOOP_EXPLICIT) {
+    TmvArgs a = sym_args(h, h->wtiles.p, ncols);
+    a.vin = x;
+    a.vout = h->xI.p;
+    a.gpart = h->n_primal ? h->gpart.p : nullptr;
+    sym_apply(h, a);
+    coarse_apply(h, ncols, nullptr, h->zc.p, st);
+    CoarseTerm ct = coarse_term_args(h);
+    k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, h->xI.p, nullptr, y, dotv, partial, st, ct);
+    IETI_LAUNCHED(h);
+    return;
+  }
   loop_fwd(h, ncols, x, h->yI.p, true, st);
   coarse_apply(h, ncols, nullptr, h->zc.p, st);
   loop_bwd(h, ncols, h->yI.p, h->zc.p, 1.0, h->xI.p, st);
@@ -868,6 +1320,15 @@ static void apply_F_inter(ietidp_s* h, int ncols, const double* x, double* y, co
 static void apply_M_inter(ietidp_s* h, int ncols, const double* x, double* y, const PcgState* st, const double* rr_part,
                           int check, const double* dotv, double* partial) {
   if (h->n_lambda == 0) return;
+  if (h->opt.loop == IETIDP_LOOP_EXPLICIT) {
+    TmvArgs a = sym_args(h, h->stiles.p, ncols);
+    a.vin = x;
+    a.weight = h->delta.p;
+    a.vout = h->zI.p;
+    sym_apply(h, a);
+    bgather(h, ncols, h->zI.p, h->delta.p, y, dotv, partial, st);
+    return;
+  }
   TmvArgs a{};
   a.vin = x;
   a.weight = h->delta.p;
@@ -963,16 +1424,42 @@ static TmvArgs base_args(ietidp_s* h, int mode, int ncols) {
   return a;
 }
 
-template <int NCP, int STAGES>
+template <int NCP, int STAGES, bool EXPL>
 static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
-  auto kern = k_pcg<NCP, STAGES>;
+  auto kern = k_pcg<NCP, STAGES, EXPL>;
   IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
   int per_sm = 0, nsm = 0;
   IETI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, cfg.smem));
   IETI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->opt.device));
   if (per_sm < 1) return false;
   const int grid = std::min(nsm * per_sm, 1024);
+  if (h->lpt_grid != grid) {  // items over the persistent CTAs: longest processing time first
+    std::vector<std::pair<int, int>> cost(h->n_loopwork);
+    for (int i = 0; i < h->n_loopwork; ++i) cost[i] = {h->h_loopwork[i].cost, i};
+    std::sort(cost.begin(), cost.end(), [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second < y.second); });
+    std::vector<std::vector<int>> lists(grid);
+    std::vector<std::pair<long long, int>> heap;
+    for (int b = 0; b < grid; ++b) heap.push_back({0, b});
+    auto cmp = [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second > y.second); };
+    std::make_heap(heap.begin(), heap.end(), cmp);
+    for (auto& c : cost) {
+      std::pop_heap(heap.begin(), heap.end(), cmp);
+      heap.back().first += c.first;
+      lists[heap.back().second].push_back(c.second);
+      std::push_heap(heap.begin(), heap.end(), cmp);
+    }
+    std::vector<int> ptr(grid + 1, 0), items;
+    for (int b = 0; b < grid; ++b) {
+      items.insert(items.end(), lists[b].begin(), lists[b].end());
+      ptr[b + 1] = (int)items.size();
+    }
+    h->cta_ptr.upload(ptr, h->stream);
+    h->cta_items.upload(items, h->stream);
+    h->lpt_grid = grid;
+  }
   PcgArgs args = a;
+  args.cta_ptr = h->cta_ptr.p;
+  args.cta_items = h->cta_items.p;
   void* params[] = {&args};
   IETI_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, 256, params, cfg.smem, h->stream));
   IETI_LAUNCHED(h);
@@ -987,8 +1474,15 @@ static bool run_solve_persistent(ietidp_s* h) {
   if (h->gbar.n == 0) h->gbar.alloc(2);
   h->gbar.zero(h->stream);
   PcgArgs a{};
+  if (h->pslot.n == 0) {
+    h->pslot.alloc((size_t)std::max(h->n_slots, 1) * nc);
+    h->rslot.alloc((size_t)std::max(h->n_slots, 1) * nc);
+  }
+  a.pslot = h->pslot.p;  // B^T p in slot order, written by the CG vector phases
+  a.rslot = h->rslot.p;  // B_D^T r in slot order
   a.fwd = base_args(h, FWD, nc);
-  a.fwd.vin = h->p_vec.p;
+  a.fwd.vin = a.pslot;
+  a.fwd.slot_in = 1;
   a.fwd.vout = h->yI.p;
   a.fwd.gpart = h->n_primal ? h->gpart.p : nullptr;
   a.bwd = base_args(h, BWD, nc);
@@ -997,12 +1491,24 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.bwd.zsign = 1.0;
   a.bwd.vout = h->xI.p;
   a.pre1 = base_args(h, PRE1, nc);
-  a.pre1.vin = h->r_vec.p;
-  a.pre1.weight = h->delta.p;
+  a.pre1.vin = a.rslot;
+  a.pre1.slot_in = 1;
   a.pre1.vout = h->sI.p;
   a.pre2 = base_args(h, PRE2, nc);
   a.pre2.vin = h->sI.p;
   a.pre2.vout = h->zI.p;
+  a.wsym = sym_args(h, h->wtiles.p, nc);
+  a.wsym.vin = a.pslot;
+  a.wsym.slot_in = 1;
+  a.wsym.vout = h->xI.p;
+  a.wsym.gpart = h->n_primal ? h->gpart.p : nullptr;
+  a.ssym = sym_args(h, h->stiles.p, nc);
+  a.ssym.vin = a.rslot;
+  a.ssym.slot_in = 1;
+  a.ssym.vout = h->zI.p;
+  a.ct = coarse_term_args(h);
+  a.blk = h->d_blk.p;
+  a.n_blk = h->n_blk;
   a.lam = h->lam.p;
   a.delta = h->delta.p;
   a.lamv = h->lam_vec.p;
@@ -1034,11 +1540,20 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.n_items = h->n_loopwork;
   a.ncp = cfg.ncp;
   if (h->n_primal * nc * 8 > cfg.smem) return false;
-  if (cfg.ncp == 1) return launch_pcg_t<1, 5>(h, cfg, a);
-  if (cfg.ncp == 16 && cfg.stages == 3) return launch_pcg_t<16, 3>(h, cfg, a);
-  if (cfg.ncp == 16) return launch_pcg_t<16, 2>(h, cfg, a);
-  if (cfg.stages == 3) return launch_pcg_t<8, 3>(h, cfg, a);
-  return launch_pcg_t<8, 2>(h, cfg, a);
+  if (h->opt.loop == IETIDP_LOOP_EXPLICIT) {
+    if (cfg.ncp == 1 && cfg.stages == 5) return launch_pcg_t<1, 5, true>(h, cfg, a);
+    if (cfg.ncp == 1) return launch_pcg_t<1, 3, true>(h, cfg, a);
+    if (cfg.ncp == 16 && cfg.stages == 3) return launch_pcg_t<16, 3, true>(h, cfg, a);
+    if (cfg.ncp == 16) return launch_pcg_t<16, 2, true>(h, cfg, a);
+    if (cfg.stages == 3) return launch_pcg_t<8, 3, true>(h, cfg, a);
+    return launch_pcg_t<8, 2, true>(h, cfg, a);
+  }
+  if (cfg.ncp == 1 && cfg.stages == 5) return launch_pcg_t<1, 5, false>(h, cfg, a);
+  if (cfg.ncp == 1) return launch_pcg_t<1, 3, false>(h, cfg, a);
+  if (cfg.ncp == 16 && cfg.stages == 3) return launch_pcg_t<16, 3, false>(h, cfg, a);
+  if (cfg.ncp == 16) return launch_pcg_t<16, 2, false>(h, cfg, a);
+  if (cfg.stages == 3) return launch_pcg_t<8, 3, false>(h, cfg, a);
+  return launch_pcg_t<8, 2, false>(h, cfg, a);
 }
 
 void run_solve(ietidp_s* h) {

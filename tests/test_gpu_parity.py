@@ -50,11 +50,14 @@ def gpu_solve(lib, b, **kw):
     return s, lam, u, rep
 
 
+@pytest.mark.parametrize("loop", ["explicit", "triangular"])
 @pytest.mark.parametrize("name", CASES)
-def test_operators_match_oracle(lib, name):
+def test_operators_match_oracle(lib, name, loop):
+    """Both loop variants: explicit W_k = S_II^-1, S_II and triangular
+    L_II^-1 / L_II substitutions."""
     b, ref = case(name)
     D = ref["dp"]
-    s = lib.from_bundle(b)
+    s = lib.from_bundle(b, loop=loop)
     s.factor()
     if b["n_primal"]:
         S = s.get_coarse()
@@ -129,6 +132,15 @@ def test_solution_iteration_matched(lib, name):
     # lambda vanishes by symmetry on C1; floor the denominator at ||j|| (R9)
     assert np.linalg.norm(lam - lam_ref) <= 1e-8 * max(np.linalg.norm(lam_ref), jn)
     assert rel(np.concatenate(u), np.concatenate(ref_f["u"])) <= 1e-8
+
+
+@pytest.mark.parametrize("name", ["C2r", "C3r"])
+def test_triangular_loop_solution(lib, name):
+    b, ref = case(name)
+    s, lam, u, rep = gpu_solve(lib, b, loop="triangular")
+    assert np.all(np.abs(np.asarray(rep["iters"]) - np.asarray(ref["iters"])) <= 1)
+    assert max(rep["rel_residual"]) <= 1e-10
+    assert rel(np.concatenate(u), np.concatenate(ref["u"])) <= 1e-8
 
 
 def test_dense_ordering_equals_nested_dissection(lib):
