@@ -52,9 +52,14 @@ CONFIGS = {c.name: c for c in (C1, C2, C3, C4, C5)}
 
 
 def get(name: str) -> Config:
-    """'C2' -> full config; 'C2r' -> reduced e=2 variant; 'C1e4' -> C1 with e=4."""
+    """'C2' -> full config; 'C2r' -> reduced e=2 variant; 'C1e4' -> C1 with e=4;
+    'C4m<p>e<e>' -> the cylinder with the manufactured A* = sin(2 pi (r - 1/2)) e_z."""
     if name in CONFIGS:
         return CONFIGS[name]
+    if name.startswith("C4m"):
+        p, e = name[3:].split("e")
+        return replace(C4, name=name, p=int(p), e=int(e), material="one", rhs="c4_manufactured",
+                       scaling="multiplicity")
     if name.endswith("r") and name[:-1] in CONFIGS:
         return CONFIGS[name[:-1]].reduced()
     if "e" in name[1:]:

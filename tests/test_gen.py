@@ -205,3 +205,56 @@ def test_B_structure(name):
         tr = P.tree[sd.gid]
         assert np.array_equal(np.flatnonzero(tr), sd.tree)
     assert np.all(P.membership[P.primal_edges] >= 3)
+
+
+# -------------------------------------------------------------- cylinder ---
+def test_cylinder_geometry_exact():
+    """C4: the rational quadratic arcs lie on the unit circle, the
+    angular speed integrates to 2 pi, |det J| integrates to the tube volume."""
+    from ietigen import cylinder as cy
+    C, dC = cy.arc(np.linspace(0.0, 1.0, 33))
+    assert np.abs(np.linalg.norm(C, axis=-1) - 1.0).max() <= 1e-15
+    # arc endpoints: angle 0 and 2 pi/16
+    assert np.allclose(C[0], [1.0, 0.0]) and np.allclose(C[-1], [np.cos(np.pi / 8), np.sin(np.pi / 8)])
+    x, w = np.polynomial.legendre.leggauss(24)
+    s, ws = 0.5 * (x + 1), 0.5 * w
+    th = sum((ws * cy.theta_s((a + s) / 16)).sum() / 16 for a in range(16))
+    assert abs(th - 2 * np.pi) <= 1e-13
+    vol = th * (ws * 0.5 * cy.radius(s)).sum() * 1.0
+    assert abs(vol - 0.75 * np.pi) <= 1e-13
+
+
+def test_cylinder_counts():
+    """C4 integer pins: E_int = 184,448, V_int = 59,520,
+    n_gp = 64 (16 z-lines + 16 r-lines + closed theta ring with 16 junctions),
+    m_r = 14,208, sum n_r = 139,072, weight-1/2 edges (2,048, 896); the reduced
+    variant keeps n_gp with 14,848 gauged DOFs."""
+    P = Problem(cf.get("C4"))
+    c = P.counts()
+    assert (c["E_int"], c["V_int"]) == (184448, 59520)
+    assert (c["n_gp"], c["m_r"], c["sum_nr"]) == (64, 14208, 139072)
+    assert (c["w_counts"][0], c["w_counts"][1]) == (2048, 896)
+    assert c["sum_nr"] - c["m_r"] + c["n_gp"] == c["E_int"] - c["V_int"]
+    r = Problem(cf.get("C4r")).counts()
+    assert r["n_gp"] == 64 and r["E_int"] - r["V_int"] == 14848
+
+
+def test_cylinder_curl_grad_and_loads():
+    """Discrete curl o grad = 0 on the curved, periodic patches; K symmetric PSD;
+    loads discretely divergence-free (G^T j = 0)."""
+    from ietigen import cylinder as cy
+    cfg = cf.get("C4r")
+    P = Problem(cfg)
+    for sd in P.subs[:3]:
+        C = local_curl(sd.ml)
+        Gd = local_grad(sd.ml)
+        assert abs(C @ Gd).max() == 0
+        spaces = cy.cylinder_spaces(cfg, sd)
+        M2 = cy.cylinder_mass2(cfg, sd, spaces, P.nu)
+        t = cy.cylinder_face_loads(cfg, sd, spaces)
+        Kf = (C.T @ M2 @ C).tocsr()
+        assert abs(Kf @ Gd).max() <= 1e-12 * abs(Kf).max()
+        assert abs(Gd.T @ (C.T @ t)).max() <= 1e-12 * abs(t).max()
+        K, j = P.assemble(sd)
+        ev = np.linalg.eigvalsh(K.toarray())
+        assert ev.min() >= -1e-10 * ev.max()

@@ -16,7 +16,7 @@ from oracle import dp
 
 pytestmark = pytest.mark.gpu
 
-CASES = ["C1", "C2r", "C3r", "C5r"]
+CASES = ["C1", "C2r", "C3r", "C4r", "C5r"]
 
 
 def rel(a, b):
