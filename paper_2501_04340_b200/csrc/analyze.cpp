@@ -512,23 +512,57 @@ void analyze_all(ietidp_s* h) {
       LevelPlan::Panel pn{};
       // (a) panel columns [p0, p0+b) -= L[rows >= p0, 0:p0] L[p0:p0+b, 0:p0]^T
       pn.upd_off = (int)gwork.size();
-      for (int i : bylev[L]) {
-        const SnHost& s = P.sn[i];
-        if (s.coarse || s.npiv <= kp * TB || kp == 0) continue;
-        const SnDev& d = sd[i];
-        const int p0 = kp * TB, b = std::min(TB, s.npiv - p0);
-        for (int r0 = p0; r0 < s.f; r0 += TB, ++pn.upd_n) {
-          GemmWork g{};
-          g.c_off = d.front_off + (long long)p0 * d.ld + r0;
-          g.a_off = d.front_off + r0;
-          g.b_off = d.front_off + p0;  // B[n][k] = L[p0 + n][k]
-          g.lda = g.ldb = g.ldc = d.ld;
-          g.m = std::min(TB, s.f - r0);
-          g.n = b;
-          g.kdim = p0;
-          g.mode = 3;  // C -= A B
-          gwork.push_back(g);
+      {
+        // tiles of this panel update; long K on few tiles is split over CTAs (split-K)
+        int ntile = 0;
+        long long kmax = 0;
+        for (int i : bylev[L]) {
+          const SnHost& s = P.sn[i];
+          if (s.coarse || s.npiv <= kp * TB || kp == 0) continue;
+          ntile += tiles_of(s.f - kp * TB);
+          kmax = std::max<long long>(kmax, (long long)kp * TB);
         }
+        int nks = 1;
+        if (ntile > 0) {
+          const int want = SPLITK_TARGET_CTAS / ntile;  // parts that still fit in one wave
+          nks = std::max(1, std::min({SPLITK_MAX, want, (int)(kmax / SPLITK_MIN_K)}));
+        }
+        int tile = 0;
+        long long ws = 0;
+        for (int i : bylev[L]) {
+          const SnHost& s = P.sn[i];
+          if (s.coarse || s.npiv <= kp * TB || kp == 0) continue;
+          const SnDev& d = sd[i];
+          const int p0 = kp * TB, b = std::min(TB, s.npiv - p0);
+          // K range [0, p0) in nks chunks of a multiple of 32 columns
+          const int chunk = ((p0 + nks - 1) / nks + 31) / 32 * 32;
+          const int parts = (p0 + chunk - 1) / chunk;
+          for (int r0 = p0; r0 < s.f; r0 += TB, ++tile) {
+            for (int q = 0; q < parts; ++q, ++pn.upd_n) {
+              const int k0 = q * chunk;
+              GemmWork g{};
+              g.c_off = d.front_off + (long long)p0 * d.ld + r0;
+              g.a_off = d.front_off + (long long)k0 * d.ld + r0;
+              g.b_off = d.front_off + (long long)k0 * d.ld + p0;  // B[k][n] = L[p0 + n][k]
+              g.lda = g.ldb = g.ldc = d.ld;
+              g.m = std::min(TB, s.f - r0);
+              g.n = b;
+              g.kdim = std::min(chunk, p0 - k0);
+              g.mode = 3;  // C -= A B
+              if (parts > 1) {
+                g.mode |= 8;
+                g.ks = q;
+                g.nks = parts;
+                g.cnt = tile;
+                g.ws_off = ws;
+              }
+              gwork.push_back(g);
+            }
+            if (parts > 1) ws += (long long)parts * TILE_ELEMS;
+          }
+        }
+        P.splitk_doubles = std::max(P.splitk_doubles, ws);
+        P.splitk_tiles = std::max(P.splitk_tiles, tile);
       }
       pn.potrf_off = (int)work.size() / 3;
       for (int i : bylev[L])
@@ -619,75 +653,76 @@ void analyze_all(ietidp_s* h) {
       if (!P.sn[i].coarse)
         for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bx_n) push(i, t, 0);
   }
-  // ---- partitioned inverse L11^-1 by recursive doubling over TB-blocks ----
-  P.inv_copy_off = (int)work.size() / 3;
-  for (int i = 0; i < nsn; ++i)
-    if (!P.sn[i].coarse)
-      for (int kp = 0; kp < tiles_of(P.sn[i].npiv); ++kp, ++P.inv_copy_n) push(i, kp, 0);
-  int maxnb = 0;
-  for (auto& s : P.sn)
-    if (!s.coarse) maxnb = std::max(maxnb, tiles_of(s.npiv));
-  long long tmpoff_dummy = 0;
-  (void)tmpoff_dummy;
-  for (int half = 1; half < maxnb; half *= 2) {
-    // step 1: T(second, first) = L11(second, first-half) * Linv(first, first)
-    int off1 = (int)gwork.size();
-    for (int i = 0; i < nsn; ++i) {
-      const SnHost& s = P.sn[i];
-      if (s.coarse) continue;
-      const SnDev& d = sd[i];
-      const int nb = tiles_of(s.npiv);
-      for (int fs = 0; fs < nb; fs += 2 * half) {
-        int ss = fs + half, se = std::min(fs + 2 * half, nb);
-        if (ss >= nb) continue;
-        for (int ti = ss; ti < se; ++ti)
-          for (int tj = fs; tj < ss; ++tj) {
-            GemmWork g{};
-            int k0 = tj * TB, k1 = std::min(ss * TB, s.npiv);
-            g.c_off = d.inv_off + (long long)tj * TB * d.ldi + ti * TB;  // T stored in tpool, same layout
-            g.a_off = d.front_off + (long long)k0 * d.ld + ti * TB;
-            g.b_off = d.inv_off + (long long)tj * TB * d.ldi + k0;
-            g.lda = d.ld;
-            g.ldb = d.ldi;
-            g.ldc = d.ldi;
-            g.m = std::min(TB, s.npiv - ti * TB);
-            g.n = std::min(TB, s.npiv - tj * TB);
-            g.kdim = k1 - k0;
-            g.mode = 0;
-            gwork.push_back(g);
-          }
+  // ---- partitioned inverse L11^-1 by recursive doubling over TB-blocks, per level ----
+  for (int L = 0; L <= P.max_level; ++L) {
+    LevelPlan& lp = P.levels[L];
+    lp.inv_copy_off = (int)work.size() / 3;
+    int maxnb = 0;
+    for (int i : bylev[L])
+      if (!P.sn[i].coarse) {
+        for (int kp = 0; kp < tiles_of(P.sn[i].npiv); ++kp, ++lp.inv_copy_n) push(i, kp, 0);
+        maxnb = std::max(maxnb, tiles_of(P.sn[i].npiv));
       }
-    }
-    P.inv_rounds.push_back({off1, (int)gwork.size() - off1});
-    // step 2: Linv(second, first) = -Linv(second, second) * T(second, first)
-    int off2 = (int)gwork.size();
-    for (int i = 0; i < nsn; ++i) {
-      const SnHost& s = P.sn[i];
-      if (s.coarse) continue;
-      const SnDev& d = sd[i];
-      const int nb = tiles_of(s.npiv);
-      for (int fs = 0; fs < nb; fs += 2 * half) {
-        int ss = fs + half, se = std::min(fs + 2 * half, nb);
-        if (ss >= nb) continue;
-        for (int ti = ss; ti < se; ++ti)
-          for (int tj = fs; tj < ss; ++tj) {
-            GemmWork g{};
-            int k0 = ss * TB, k1 = std::min((ti + 1) * TB, s.npiv);
-            g.c_off = d.inv_off + (long long)tj * TB * d.ldi + ti * TB;
-            g.a_off = d.inv_off + (long long)k0 * d.ldi + ti * TB;
-            g.b_off = d.inv_off + (long long)tj * TB * d.ldi + k0;  // T in tpool
-            g.lda = d.ldi;
-            g.ldb = d.ldi;
-            g.ldc = d.ldi;
-            g.m = std::min(TB, s.npiv - ti * TB);
-            g.n = std::min(TB, s.npiv - tj * TB);
-            g.kdim = k1 - k0;
-            g.mode = 1;  // negate
-            gwork.push_back(g);
-          }
+    for (int half = 1; half < maxnb; half *= 2) {
+      // step 1: T(second, first) = L11(second, first-half) * Linv(first, first)
+      int off1 = (int)gwork.size();
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (s.coarse) continue;
+        const SnDev& d = sd[i];
+        const int nb = tiles_of(s.npiv);
+        for (int fs = 0; fs < nb; fs += 2 * half) {
+          int ss = fs + half, se = std::min(fs + 2 * half, nb);
+          if (ss >= nb) continue;
+          for (int ti = ss; ti < se; ++ti)
+            for (int tj = fs; tj < ss; ++tj) {
+              GemmWork g{};
+              int k0 = tj * TB, k1 = std::min(ss * TB, s.npiv);
+              g.c_off = d.inv_off + (long long)tj * TB * d.ldi + ti * TB;  // T stored in tpool, same layout
+              g.a_off = d.front_off + (long long)k0 * d.ld + ti * TB;
+              g.b_off = d.inv_off + (long long)tj * TB * d.ldi + k0;
+              g.lda = d.ld;
+              g.ldb = d.ldi;
+              g.ldc = d.ldi;
+              g.m = std::min(TB, s.npiv - ti * TB);
+              g.n = std::min(TB, s.npiv - tj * TB);
+              g.kdim = k1 - k0;
+              g.mode = 0;
+              gwork.push_back(g);
+            }
+        }
       }
+      lp.inv_rounds.push_back({off1, (int)gwork.size() - off1});
+      // step 2: Linv(second, first) = -Linv(second, second) * T(second, first)
+      int off2 = (int)gwork.size();
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (s.coarse) continue;
+        const SnDev& d = sd[i];
+        const int nb = tiles_of(s.npiv);
+        for (int fs = 0; fs < nb; fs += 2 * half) {
+          int ss = fs + half, se = std::min(fs + 2 * half, nb);
+          if (ss >= nb) continue;
+          for (int ti = ss; ti < se; ++ti)
+            for (int tj = fs; tj < ss; ++tj) {
+              GemmWork g{};
+              int k0 = ss * TB, k1 = std::min((ti + 1) * TB, s.npiv);
+              g.c_off = d.inv_off + (long long)tj * TB * d.ldi + ti * TB;
+              g.a_off = d.inv_off + (long long)k0 * d.ldi + ti * TB;
+              g.b_off = d.inv_off + (long long)tj * TB * d.ldi + k0;  // T in tpool
+              g.lda = d.ldi;
+              g.ldb = d.ldi;
+              g.ldc = d.ldi;
+              g.m = std::min(TB, s.npiv - ti * TB);
+              g.n = std::min(TB, s.npiv - tj * TB);
+              g.kdim = k1 - k0;
+              g.mode = 1;  // negate
+              gwork.push_back(g);
+            }
+        }
+      }
+      lp.inv_rounds.push_back({off2, (int)gwork.size() - off2});
     }
-    P.inv_rounds.push_back({off2, (int)gwork.size() - off2});
   }
 
   // ---- per-subdomain offsets ----
@@ -927,6 +962,28 @@ void analyze_all(ietidp_s* h) {
               (mx + TB - 1) / TB, fl / 1e9);
     }
     fprintf(stderr, "critical-path panels %d\n", crit);
+    auto gflops = [&](int off, int n) {
+      long long f = 0;
+      for (int q = off; q < off + n; ++q) f += 2LL * gwork[q].m * gwork[q].n * gwork[q].kdim;
+      return f / 1e9;
+    };
+    for (int L = 0; L <= P.max_level; ++L) {
+      double up = 0, tr = 0;
+      for (auto& pn : P.levels[L].panels) {
+        up += gflops(pn.upd_off, pn.upd_n);
+        tr += gflops(pn.trsm_off, pn.trsm_n);
+      }
+      fprintf(stderr, "level %d: upd %.2f GF, trsm %.2f GF, syrk:", L, up, tr);
+      for (auto& sy : P.levels[L].syrk) {
+        int kmin = 1 << 30, kmax = 0;
+        for (int q = sy.first; q < sy.first + sy.second; ++q) {
+          kmin = std::min(kmin, gwork[q].kdim);
+          kmax = std::max(kmax, gwork[q].kdim);
+        }
+        fprintf(stderr, " [%d tiles, K %d-%d, %.2f GF]", sy.second, kmin, kmax, gflops(sy.first, sy.second));
+      }
+      fprintf(stderr, "\n");
+    }
   }
   if (h->opt.device < 0) {  // host-only analysis mode: no device work
     h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -1003,6 +1060,9 @@ void analyze_all(ietidp_s* h) {
   h->dinv.alloc(P.dinv_doubles);
   h->ipool.alloc(P.inv_doubles);
   h->tpool.alloc(P.inv_doubles);
+  h->skws.alloc(std::max<long long>(1, P.splitk_doubles));
+  h->skcnt.alloc(std::max(1, P.splitk_tiles));
+  IETI_CUDA(cudaMemset(h->skcnt.p, 0, h->skcnt.n * sizeof(int)));
   h->vecw.alloc((size_t)P.vec_rows * 16);  // sweeps use up to 16 interleaved columns
   h->Xf.alloc((size_t)xo * nc);
   h->Xr.alloc((size_t)xo * nc);

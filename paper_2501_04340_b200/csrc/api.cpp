@@ -125,6 +125,10 @@ ietidp_status ietidp_create(const ietidp_options* opt, int n_sub, int n_lambda, 
       IETI_CUDA(cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking));
       h->own_stream = true;
     }
+    if (const char* tp = getenv("IETIDP_TRACE")) {
+      h->trace.on = true;
+      h->trace.path = tp;
+    }
   });
 }
 
@@ -223,6 +227,7 @@ ietidp_status ietidp_factor(ietidp_t h) {
     h->factor_failed = true;
     EvPair e1, e2;
     IETI_CUDA(cudaEventRecord(e1.a, h->stream));
+    h->trace.start(h->stream);
     ieti::run_factor(h);
     IETI_CUDA(cudaEventRecord(e1.b, h->stream));
     IETI_CUDA(cudaEventRecord(e2.a, h->stream));
@@ -231,6 +236,7 @@ ietidp_status ietidp_factor(ietidp_t h) {
     int flags[2];
     IETI_CUDA(cudaMemcpyAsync(flags, h->err_flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     IETI_CUDA(cudaStreamSynchronize(h->stream));
+    h->trace.dump("factor");
     h->rep.ms_factor = e1.ms();
     h->rep.ms_coarse = e2.ms();
     if (flags[0] != INT_MAX) {
@@ -256,12 +262,14 @@ ietidp_status ietidp_solve(ietidp_t h, double* lambda, ietidp_report* report) {
     set_device(h);
     EvPair e1, e2;
     IETI_CUDA(cudaEventRecord(e1.a, h->stream));
+    h->trace.start(h->stream);
     ieti::run_solve(h);
     IETI_CUDA(cudaEventRecord(e1.b, h->stream));
     IETI_CUDA(cudaEventRecord(e2.a, h->stream));
     ieti::run_recover(h);
     IETI_CUDA(cudaEventRecord(e2.b, h->stream));
     ieti::finish_solve(h, &h->rep);
+    h->trace.dump("solve");
     h->rep.ms_pcg = e1.ms();
     h->rep.ms_recover = e2.ms();
     if (lambda && h->n_lambda) {
@@ -385,6 +393,8 @@ void ietidp_destroy(ietidp_t h) {
   if (h->opt.device >= 0) cudaSetDevice(h->opt.device);
   if (h->stream) cudaStreamSynchronize(h->stream);
   ieti::destroy_graph(h);
+  for (auto e : h->fev) cudaEventDestroy(e);
+  if (h->side) cudaStreamDestroy(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }

@@ -47,9 +47,17 @@ inline int grid_for(long long n, int block, int cap = 148 * 16) {
   return (int)g;
 }
 
-#define IETI_LAUNCHED(h) \
-  do {                   \
-    (h)->launches++;     \
+// Every kernel launch is counted; with IETIDP_TRACE=<file> set, an event is also
+// recorded after it (per-launch device durations, written by the API at the end of
+// factor / solve; a diagnostics aid, off by default).
+#define IETI_LAUNCHED(h)                                                   \
+  do {                                                                     \
+    (h)->launches++;                                                       \
+    if ((h)->trace.on) (h)->trace.mark((h)->stream, __FILE__, __LINE__);   \
+  } while (0)
+#define IETI_LAUNCHED_SIDE(h) \
+  do {                        \
+    (h)->launches++;          \
   } while (0)
 
 #define IETI_CHECK_LAUNCH() IETI_CUDA(cudaGetLastError())

@@ -27,147 +27,163 @@ __global__ void k_scatter(long long n, const long long* __restrict__ dst, const 
     out[dst[i]] = vals[src[i]];
 }
 
-// 1/sqrt(a) in FP64 without the slow-path sqrt and divide: a float MUFU seed
-// (~2^-23) refined by two Newton steps r <- r (3 - a r^2) / 2 (~2^-46, ~2^-92:
-// within rounding of the correctly rounded value). The pivot chain of POTRF runs
-// through this once per column, so its latency sets the kernel's.
-__device__ __forceinline__ double rsqrt_fast(double a) {
+// POTRF of the diagonal block of panel w.a of front w.sn, and its inverse Dinv = L^-1.
+// 128 threads; thread (r, h) holds the columns c = 2i + h (i < 32) of row r in registers
+// (h is warp-uniform). Elimination step j (64 unrolled steps, one barrier each):
+//   s_r = a_r[j] / a_jj,  a_r[c] -= s_r a_c[j]  for c > j,
+// with column j read from a double-buffered shared copy. The next pivot column j+1 is
+// updated first and published; its owner lanes compute the pivot's reciprocal square
+// root (float seed + one third-order correction) while the rest of the row is updated.
+// Entries above the diagonal are updated too (never read) so that the step is free of
+// per-element predicates; the published column is zero above the diagonal.
+// Inverse: 32-blocks X11 = L11^-1, X22 = L22^-1 by forward substitution (lane = column),
+// then X21 = -X22 (L21 X11).
+constexpr int POTRF_T = 128;
+__device__ __forceinline__ double rsqrt_h(double a) {
   if (!(a > 1e-30 && a < 1e30)) return 1.0 / sqrt(a);
-  double r = (double)rsqrtf((float)a);
-  r = r * (1.5 - 0.5 * a * r * r);
-  r = r * (1.5 - 0.5 * a * r * r);
-  return r;
+  const double r0 = (double)rsqrtf((float)a);
+  const double e = fma(-a * r0, r0, 1.0);  // |e| ~ 2^-22
+  return fma(r0 * e, fma(0.375, e, 0.5), r0);  // r0 (1 + e/2 + 3e^2/8): error O(e^3)
 }
-
-// POTRF of the diagonal block of panel w.a of front w.sn, and its inverse.
-// Cholesky: one barrier per elimination step. Step j reads the pivot column from a
-// double-buffered copy `cb` (static smem, so the trailing update's loads and stores
-// to A stay in flight) and the pivot's reciprocal square root `pr`, which the thread
-// that updates the next diagonal entry computes ahead (hidden behind the update).
-// Inverse: the four 16 x 16 diagonal blocks are inverted by four warps, the
-// off-diagonal blocks follow in three block-row steps (X_ib,jb = -X_ib,ib sum L X).
-constexpr int POTRF_T = 256;
-constexpr int SB = 16;  // sub-block of the inverse
+template <int H>
+__device__ __forceinline__ void potrf_steps(double (&a)[32], int r, double (*cb)[TB], double* pr, double* dg,
+                                            bool& ok) {
+#pragma unroll
+  for (int j = 0; j < TB; ++j) {
+    const double rj = pr[j & 1];
+    const double* col = cb[j & 1];
+    double* nxt = cb[(j + 1) & 1];
+    const double cr = col[r];
+    const double s = cr * rj * rj;  // a_r[j] / a_jj
+    if ((j & 1) == H) {
+      if (r >= j) a[j >> 1] = cr * rj;  // L[r][j]
+    }
+    if (j + 1 < TB) {
+      if (((j + 1) & 1) == H) {
+        const int i1 = (j + 1) >> 1;
+        a[i1] = fma(-s, col[j + 1], a[i1]);
+        const double v = a[i1];
+        nxt[r] = (r > j) ? v : 0.0;
+        const double rn = rsqrt_h(v);
+        if (r == j + 1) {
+          pr[(j + 1) & 1] = rn;
+          dg[j + 1] = rn;
+          ok = ok && (v > 0.0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int c = 2 * i + H;
+        if (c >= j + 2) a[i] = fma(-s, col[c], a[i]);
+      }
+      if (r >= 32) {
+#pragma unroll
+        for (int i = 16; i < 32; ++i) {
+          const int c = 2 * i + H;
+          if (c >= j + 2) a[i] = fma(-s, col[c], a[i]);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
 __global__ void __launch_bounds__(POTRF_T) k_potrf(const Work* __restrict__ work, const SnDev* __restrict__ sn,
                                                    double* __restrict__ pool, double* __restrict__ dinv,
                                                    int* __restrict__ err) {
-  extern __shared__ double sm[];
-  double(*A)[TB + 1] = reinterpret_cast<double(*)[TB + 1]>(sm);  // working copy, then X = L^-1
-  __shared__ double L[TB][TB + 1];
-  __shared__ double T[SB][3 * SB + 1];  // scratch (L X) of one block row: 16 x 48
-  __shared__ double dg[TB];
   __shared__ double cb[2][TB];
   __shared__ double pr[2];
-  __shared__ int bad;
+  __shared__ double dg[TB];  // 1 / L[j][j]
+  __shared__ double Ls[TB][TB + 1];
+  __shared__ double Ts[32][33];
   const Work w = work[blockIdx.x];
   const SnDev s = sn[w.sn];
   const int p0 = w.a * TB;
   const int b = min(TB, s.npiv - p0);
   double* F = pool + s.front_off + (long long)p0 * s.ld + p0;
-  const int tid = threadIdx.x;
-  if (tid == 0) bad = 0;
-  __syncthreads();
-  for (int e = tid; e < TB * TB; e += POTRF_T) {
-    const int c = e / TB, r = e % TB;  // column-major walk: coalesced along r
+  const int t = threadIdx.x, r = t & 63, h = t >> 6;
+  double a[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = 2 * i + h;
     double v;
-    if (r < b && c < b) v = (r >= c) ? F[(long long)c * s.ld + r] : 0.0;
-    else v = (r == c) ? 1.0 : 0.0;
-    A[r][c] = v;
-    if (c == 0) cb[0][r] = v;
-    if (e == 0) {
-      const bool ok = v > 0.0;
-      if (!ok) bad = 1;
-      pr[0] = ok ? rsqrt_fast(v) : 1.0;
+    if (r < b && c < b) v = (c <= r) ? F[(long long)c * s.ld + r] : 0.0;
+    else v = (r == c) ? 1.0 : 0.0;  // identity padding of a partial block
+    a[i] = v;
+  }
+  bool ok = true;
+  if (h == 0) {
+    cb[0][r] = a[0];
+    if (r == 0) {
+      pr[0] = rsqrt_h(a[0]);
+      dg[0] = pr[0];
+      ok = a[0] > 0.0;
     }
   }
   __syncthreads();
-  const int r = tid & 63, cg = tid >> 6;  // 64 rows x 4 column groups
-  for (int j = 0; j < TB; ++j) {
-    const double* col = cb[j & 1];
-    double* nxt = cb[(j + 1) & 1];
-    const double rj = pr[j & 1];
-    const double ajj = col[j];
-    if (r >= j && cg == 0) L[r][j] = (r == j) ? ajj * rj : col[r] * rj;
-    if (r > j) {
-      const double lr = col[r] * rj * rj;
-      int c = j + 1 + cg;
-      if (cg == 0) {  // column j+1: the next pivot column
-        const double v = A[r][c] - lr * col[c];
-        A[r][c] = v;
-        nxt[r] = v;
-        if (r == j + 1) {  // the next pivot: its rsqrt ahead of the barrier
-          const bool ok = v > 0.0;
-          if (!ok) bad = 1;
-          pr[(j + 1) & 1] = ok ? rsqrt_fast(v) : 1.0;
-        }
-        c += 4;
-      }
-      for (; c + 12 <= r; c += 16) {
-        const double a0 = A[r][c], a1 = A[r][c + 4], a2 = A[r][c + 8], a3 = A[r][c + 12];
-        const double b0 = col[c], b1 = col[c + 4], b2 = col[c + 8], b3 = col[c + 12];
-        A[r][c] = a0 - lr * b0;
-        A[r][c + 4] = a1 - lr * b1;
-        A[r][c + 8] = a2 - lr * b2;
-        A[r][c + 12] = a3 - lr * b3;
-      }
-      for (; c <= r; c += 4) A[r][c] -= lr * col[c];
-    }
-    __syncthreads();
+  if (h == 0) potrf_steps<0>(a, r, cb, pr, dg, ok);
+  else potrf_steps<1>(a, r, cb, pr, dg, ok);
+  if (!ok) atomicMin(err, s.sub);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = 2 * i + h;
+    if (r < b && c < b && c <= r) F[(long long)c * s.ld + r] = a[i];
+    Ls[r][c] = (c <= r) ? a[i] : 0.0;
   }
-  if (tid == 0 && bad) atomicMin(err, s.sub);
-  for (int e = tid; e < TB * TB; e += POTRF_T) {
-    const int c = e / TB, rr = e % TB;
-    if (rr < b && c < b && rr >= c) F[(long long)c * s.ld + rr] = L[rr][c];
-  }
-  // ---- X = L^-1 ----
-  double(*X)[TB + 1] = A;
-  for (int e = tid; e < TB * TB; e += POTRF_T) X[e / TB][e % TB] = 0.0;
-  if (tid < TB) dg[tid] = 1.0 / L[tid][tid];
   __syncthreads();
-  {
-    // diagonal 16-blocks: warp wb < 4 inverts block wb; lane c < 16 solves column c
-    const int warp = tid >> 5, lane = tid & 31;
-    if (warp < 4 && lane < SB) {
-      const int o = warp * SB, c = lane;
-      double xc[SB];  // column c of the block inverse, in registers
+  if (t < 64) {
+    const int o = (t >> 5) * 32, c = t & 31;
+    double x[32];
 #pragma unroll
-      for (int m = 0; m < SB; ++m) xc[m] = (m == c) ? dg[o + c] : 0.0;
-      X[o + c][o + c] = dg[o + c];
+    for (int m = 0; m < 32; ++m) {
+      double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
 #pragma unroll
-      for (int rr = 1; rr < SB; ++rr) {
-        if (rr <= c) continue;
-        double sum = 0.0;
-#pragma unroll
-        for (int m = 0; m < rr; ++m) sum += L[o + rr][o + m] * xc[m];  // xc[m] = 0 for m < c
-        xc[rr] = -sum * dg[o + rr];
-        X[o + rr][o + c] = xc[rr];
+      for (int kk = 0; kk < m; kk += 4) {
+        s0 = fma(Ls[o + m][o + kk], x[kk], s0);
+        if (kk + 1 < m) s1 = fma(Ls[o + m][o + kk + 1], x[kk + 1], s1);
+        if (kk + 2 < m) s2 = fma(Ls[o + m][o + kk + 2], x[kk + 2], s2);
+        if (kk + 3 < m) s3 = fma(Ls[o + m][o + kk + 3], x[kk + 3], s3);
       }
+      // x[m] = (delta_mc - sum_{k<m} L[m][k] x[k]) / L[m][m]  (0 for m < c)
+      x[m] = ((m == c ? 1.0 : 0.0) - ((s0 + s1) + (s2 + s3))) * dg[o + m];
+    }
+    __syncwarp();
+    // X11 over L11; X22 into the unused upper block Ls[m][32 + c]
+#pragma unroll
+    for (int m = 0; m < 32; ++m) {
+      if (o == 0) Ls[m][c] = x[m];
+      else Ls[m][32 + c] = x[m];
     }
   }
   __syncthreads();
-  for (int ib = 1; ib < TB / SB; ++ib) {
-    // T[r][c] = sum_m L[ib*16 + r][m] X[m][c] over the block rows jb..ib-1 of X
-    const int nc = ib * SB;
-    for (int e = tid; e < SB * nc; e += POTRF_T) {
-      const int rr = e / nc, c = e % nc;
-      double sum = 0.0;
-      for (int m = (c / SB) * SB; m < nc; ++m) sum += L[ib * SB + rr][m] * X[m][c];
-      T[rr][c] = sum;
-    }
-    __syncthreads();
-    // X[ib*16 + r][c] = -sum_k X_diag[r][k] T[k][c]
-    for (int e = tid; e < SB * nc; e += POTRF_T) {
-      const int rr = e / nc, c = e % nc;
-      double sum = 0.0;
-      for (int k = 0; k <= rr; ++k) sum += X[ib * SB + rr][ib * SB + k] * T[k][c];
-      X[ib * SB + rr][c] = -sum;
-    }
-    __syncthreads();
+  const int rr = t >> 2, c0 = (t & 3) * 8;
+  double tv[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tv[q] = 0.0;
+#pragma unroll 4
+  for (int kk = 0; kk < 32; ++kk) {  // T = L21 X11
+    const double l = Ls[32 + rr][kk];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tv[q] = fma(l, (kk >= c0 + q) ? Ls[kk][c0 + q] : 0.0, tv[q]);
   }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) Ts[rr][c0 + q] = tv[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 8; ++q) tv[q] = 0.0;
+  for (int kk = 0; kk <= rr; ++kk) {  // X21 = -X22 T into the L21 block
+    const double xk = Ls[rr][32 + kk];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) tv[q] = fma(xk, Ts[kk][c0 + q], tv[q]);
+  }
+#pragma unroll
+  for (int q = 0; q < 8; ++q) Ls[32 + rr][c0 + q] = -tv[q];
+  __syncthreads();
   double* D = dinv + s.dinv_off + (long long)w.a * TILE_ELEMS;  // column-major TB x TB
-  for (int e = tid; e < TB * TB; e += POTRF_T) {
-    const int c = e / TB, rr = e % TB;
-    D[e] = (rr < b && c < b && rr >= c) ? X[rr][c] : 0.0;
+  for (int e = t; e < TILE_ELEMS; e += POTRF_T) {
+    const int c = e >> 6, m = e & 63;
+    double v = 0.0;
+    if (m >= c && m < b && c < b) v = (c >= 32) ? Ls[m - 32][c] : Ls[m][c];
+    D[e] = v;
   }
 }
 
@@ -180,7 +196,7 @@ __global__ void __launch_bounds__(POTRF_T) k_potrf(const Work* __restrict__ work
 //   BKC = true:  B[k][n] = Bb[b_off + n*ldb + k]  (k contiguous: column-major B)
 //   ATR = true:  A[r][k] = Ab[a_off + r*lda + k]  (A given transposed, k contiguous)
 // ---------------------------------------------------------------------------
-constexpr int KC = 32, GST = 2, KS = 72;  // 2 stages: 74 KB smem, 3 CTAs/SM
+constexpr int KC = 32, GST = 2, KS = 68;  // 2 stages: 70 KB smem, 3 CTAs/SM; KS = 4 mod 16: conflict-free fragment loads
 constexpr int GEMM_SMEM = GST * 2 * KC * KS * (int)sizeof(double);
 
 __device__ __forceinline__ void cp_async_z16(void* smem, const void* gmem, int src_bytes) {
@@ -215,7 +231,8 @@ __device__ __forceinline__ void load_rc(double* dst, const double* src, long lon
 template <bool BKC, bool ATR = false>
 __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work, const double* __restrict__ Ab,
                                               const double* __restrict__ Bb, double* __restrict__ Cb,
-                                              const int* __restrict__ d_rel) {
+                                              const int* __restrict__ d_rel, double* __restrict__ skws = nullptr,
+                                              int* __restrict__ skcnt = nullptr) {
   extern __shared__ __align__(16) double sm[];
   const GemmWork w = work[blockIdx.x];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -283,37 +300,125 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
   }
   cp_async_wait<0>();
   __syncthreads();  // C may alias A (in-place TRSM): all reads done before any write
-  const double sgn = (w.mode & 1) ? -1.0 : 1.0;
-  if (w.mode & 4) {
-    // fused multifrontal extend-add: parent[rel_c, rel_r] += C - A B (lower part)
-    const int* rr = d_rel + w.rel_r;
-    const int* rc = d_rel + w.rel_c;
-#pragma unroll
-    for (int i = 0; i < 4; ++i)
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-#pragma unroll
-        for (int q = 0; q < 2; ++q) {
-          const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + q;
-          if (r < w.m && c < w.n && (!w.diag || r >= c)) {
-            const double v = Cb[w.c_off + (long long)c * w.ldc + r] + sgn * acc[i][j][q];
-            Cb[w.p_off + (long long)rc[c] * w.p_ld + rr[r]] += v;
-          }
-        }
-    return;
-  }
+  // The accumulator tile goes through shared memory (column-major, stride ETS) so that
+  // the epilogue walks whole columns: warp w takes the columns c = w (mod 4), lane l the
+  // rows 2l, 2l+1 -- every global access of a warp is one contiguous 512-byte column.
+  constexpr int ETS = 66;  // 2 ETS = 4 (mod 32): conflict-free fragment stores
+  double* Ts = sm;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < 4; ++j) {
+      const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t;
+      Ts[c * ETS + r] = acc[i][j][0];
+      Ts[(c + 1) * ETS + r] = acc[i][j][1];
+    }
+  __syncthreads();
+  const double sgn = (w.mode & 1) ? -1.0 : 1.0;
+  const int r0 = 2 * lane;
+  if (w.mode & 8) {
+    // split-K part: store the partial product; the last part to arrive reduces all
+    // parts in index order (deterministic) into C
+    double* Pp = skws + w.ws_off + (long long)w.ks * TILE_ELEMS;
+    for (int c = warp; c < TB; c += 4)
+      *reinterpret_cast<double2*>(Pp + c * TB + r0) = *reinterpret_cast<const double2*>(Ts + c * ETS + r0);
+    __threadfence();
+    __syncthreads();
+    __shared__ int last;
+    if (tid == 0) last = (atomicAdd(skcnt + w.cnt, 1) == w.nks - 1);
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    // each thread reduces 4 x 2 consecutive entries with all SPLITK_MAX loads in flight
+    const double* P0 = skws + w.ws_off;
+    for (int e0 = 2 * tid; e0 < TILE_ELEMS; e0 += 4 * 256) {
+      double2 v[4][SPLITK_MAX];
 #pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        const int r = wm + i * 8 + g, c = wn + j * 8 + 2 * t + q;
-        if (r < w.m && c < w.n) {
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int q = 0; q < SPLITK_MAX; ++q)
+          if (q < w.nks)
+            v[u][q] = __ldcg(reinterpret_cast<const double2*>(P0 + (long long)q * TILE_ELEMS + e0 + u * 256));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        double s0 = v[u][0].x, s1 = v[u][0].y;
+#pragma unroll
+        for (int q = 1; q < SPLITK_MAX; ++q)
+          if (q < w.nks) {
+            s0 += v[u][q].x;
+            s1 += v[u][q].y;
+          }
+        const int e = e0 + u * 256;
+        const int r = e & (TB - 1), c = e >> 6;  // r even: r, r + 1 in the same column
+        if (c < w.n) {
           double* C = Cb + w.c_off + (long long)c * w.ldc + r;
-          *C = (w.mode & 2) ? *C + sgn * acc[i][j][q] : sgn * acc[i][j][q];
+          if (r < w.m) C[0] = (w.mode & 2) ? C[0] + sgn * s0 : sgn * s0;
+          if (r + 1 < w.m) C[1] = (w.mode & 2) ? C[1] + sgn * s1 : sgn * s1;
         }
       }
+    }
+    if (tid == 0) skcnt[w.cnt] = 0;  // ready for the next launch
+    return;
+  }
+  const bool ok0 = r0 < w.m, ok1 = r0 + 1 < w.m;
+  if (w.mode & 4) {
+    // fused multifrontal extend-add: parent[rel_c[c], rel_r[r]] += C - A B (lower part)
+    const int* rr = d_rel + w.rel_r;
+    const int* rc = d_rel + w.rel_c;
+    const int pr0 = ok0 ? __ldg(rr + r0) : 0, pr1 = ok1 ? __ldg(rr + r0 + 1) : 0;
+    const double* Cc = Cb + w.c_off + r0;
+    double* Pb = Cb + w.p_off;
+    constexpr int U = 4;  // columns in flight per warp
+    for (int c0 = warp; c0 < w.n; c0 += 4 * U) {
+      double cv[U][2], pv[U][2];
+      long long po[U];
+      bool v0[U], v1[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 4 * u;
+        const bool cok = c < w.n;
+        v0[u] = cok && ok0 && (!w.diag || r0 >= c);
+        v1[u] = cok && ok1 && (!w.diag || r0 + 1 >= c);
+        po[u] = cok ? (long long)__ldg(rc + c) * w.p_ld : 0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 4 * u;
+        cv[u][0] = v0[u] ? Cc[(long long)c * w.ldc] : 0.0;
+        cv[u][1] = v1[u] ? Cc[(long long)c * w.ldc + 1] : 0.0;
+        pv[u][0] = v0[u] ? Pb[po[u] + pr0] : 0.0;
+        pv[u][1] = v1[u] ? Pb[po[u] + pr1] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int c = c0 + 4 * u;
+        if (v0[u]) Pb[po[u] + pr0] = pv[u][0] + (cv[u][0] + sgn * Ts[c * ETS + r0]);
+        if (v1[u]) Pb[po[u] + pr1] = pv[u][1] + (cv[u][1] + sgn * Ts[c * ETS + r0 + 1]);
+      }
+    }
+    return;
+  }
+  const bool accum = (w.mode & 2) != 0;
+  double* Cc = Cb + w.c_off + r0;
+  constexpr int U = 4;
+  for (int c0 = warp; c0 < w.n; c0 += 4 * U) {
+    double cv[U][2];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + 4 * u;
+      const bool cok = c < w.n && accum;
+      cv[u][0] = (cok && ok0) ? Cc[(long long)c * w.ldc] : 0.0;
+      cv[u][1] = (cok && ok1) ? Cc[(long long)c * w.ldc + 1] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int c = c0 + 4 * u;
+      if (c < w.n) {
+        if (ok0) Cc[(long long)c * w.ldc] = cv[u][0] + sgn * Ts[c * ETS + r0];
+        if (ok1) Cc[(long long)c * w.ldc + 1] = cv[u][1] + sgn * Ts[c * ETS + r0 + 1];
+      }
+    }
+  }
 }
 
 // Diagonal TB-blocks of L11^-1 are the Dinv blocks of the panels.
@@ -363,9 +468,7 @@ void run_factor(ietidp_s* h) {
   cudaStream_t st = h->stream;
   const Plan& P = h->plan;
   static bool attr = false;
-  const int sm_potrf = TB * (TB + 1) * sizeof(double);  // A (then X = L^-1); L static
   if (!attr) {
-    set_smem((const void*)k_potrf, sm_potrf);
     set_smem((const void*)k_gemm<false>, GEMM_SMEM);
     set_smem((const void*)k_gemm<true>, GEMM_SMEM);
     set_smem((const void*)k_gemm<true, true>, GEMM_SMEM);
@@ -387,7 +490,20 @@ void run_factor(ietidp_s* h) {
   int maxnt = 0;
   for (auto& d : h->h_sub) maxnt = std::max(maxnt, d.nt);
   const bool expl = h->opt.loop == IETIDP_LOOP_EXPLICIT;
-  for (int L = 0; L <= P.max_level; ++L) {
+  // Two streams: the panels and SYRKs of level after level on the main stream; the
+  // partitioned inverse of a level's supernodes (and finally W_k) on the side stream,
+  // started as soon as that level's panels are factored, so that it overlaps the
+  // latency-bound SYRK / panel launches of the levels above.
+  const int nlev = P.max_level + 1;
+  if (!h->side) {
+    IETI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
+    h->fev.resize(nlev + 2);
+    for (auto& e : h->fev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  cudaStream_t s2 = h->side;
+  IETI_CUDA(cudaEventRecord(h->fev[nlev + 1], st));  // side work starts after the scatter
+  IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[nlev + 1], 0));
+  for (int L = 0; L < nlev; ++L) {
     const LevelPlan& lp = P.levels[L];
     // explicit loop: S_II is the assembled r_I root front before its factorisation
     if (expl && h->rootlist_range[L].second > 0) {
@@ -398,11 +514,12 @@ void run_factor(ietidp_s* h) {
     }
     for (auto& pn : lp.panels) {
       if (pn.upd_n) {
-        k_gemm<false><<<pn.upd_n, 128, GEMM_SMEM, st>>>(GW + pn.upd_off, pool, pool, pool, rel);
+        k_gemm<false><<<pn.upd_n, 128, GEMM_SMEM, st>>>(GW + pn.upd_off, pool, pool, pool, rel, h->skws.p,
+                                                         h->skcnt.p);
         IETI_LAUNCHED(h);
       }
       if (pn.potrf_n) {
-        k_potrf<<<pn.potrf_n, POTRF_T, sm_potrf, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
+        k_potrf<<<pn.potrf_n, POTRF_T, 0, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
         IETI_LAUNCHED(h);
       }
       if (pn.trsm_n) {
@@ -410,32 +527,36 @@ void run_factor(ietidp_s* h) {
         IETI_LAUNCHED(h);
       }
     }
+    IETI_CUDA(cudaEventRecord(h->fev[L], st));
     for (auto& sy : lp.syrk) {
       k_gemm<false><<<sy.second, 128, GEMM_SMEM, st>>>(GW + sy.first, pool, pool, pool, rel);
       IETI_LAUNCHED(h);
     }
-  }
-  // partitioned inverse L11^-1 of every factored supernode (all at once)
-  if (P.inv_copy_n) {
-    k_inv_copy<<<P.inv_copy_n, 256, 0, st>>>(W + P.inv_copy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
-    IETI_LAUNCHED(h);
-  }
-  for (size_t r = 0; r < P.inv_rounds.size(); ++r) {
-    const auto& rg = P.inv_rounds[r];
-    if (!rg.second) continue;
-    const bool step1 = (r % 2) == 0;
-    k_gemm<true><<<rg.second, 128, GEMM_SMEM, st>>>(GW + rg.first, step1 ? pool : h->ipool.p,
-                                                    step1 ? h->ipool.p : h->tpool.p, step1 ? h->tpool.p : h->ipool.p,
-                                                    rel);
-    IETI_LAUNCHED(h);
+    // side stream: partitioned inverse L11^-1 of this level's supernodes
+    IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[L], 0));
+    if (lp.inv_copy_n) {
+      k_inv_copy<<<lp.inv_copy_n, 256, 0, s2>>>(W + lp.inv_copy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
+      IETI_LAUNCHED_SIDE(h);
+    }
+    for (size_t r = 0; r < lp.inv_rounds.size(); ++r) {
+      const auto& rg = lp.inv_rounds[r];
+      if (!rg.second) continue;
+      const bool step1 = (r % 2) == 0;
+      k_gemm<true><<<rg.second, 128, GEMM_SMEM, s2>>>(GW + rg.first, step1 ? pool : h->ipool.p,
+                                                      step1 ? h->ipool.p : h->tpool.p,
+                                                      step1 ? h->tpool.p : h->ipool.p, rel);
+      IETI_LAUNCHED_SIDE(h);
+    }
   }
   // explicit loop: W_k = L_II^-T L_II^-1 (lower tiles; tpool is free again)
   if (expl && P.w_n) {
-    k_gemm<true, true><<<P.w_n, 128, GEMM_SMEM, st>>>(GW + P.w_off, h->ipool.p, h->ipool.p, h->tpool.p, rel);
-    IETI_LAUNCHED(h);
-    k_pack_sym<<<h->n_sub * maxnt, 256, 0, st>>>(nullptr, maxnt, h->d_sub.p, h->d_sn.p, h->tpool.p, 0, h->wtiles.p);
-    IETI_LAUNCHED(h);
+    k_gemm<true, true><<<P.w_n, 128, GEMM_SMEM, s2>>>(GW + P.w_off, h->ipool.p, h->ipool.p, h->tpool.p, rel);
+    IETI_LAUNCHED_SIDE(h);
+    k_pack_sym<<<h->n_sub * maxnt, 256, 0, s2>>>(nullptr, maxnt, h->d_sub.p, h->d_sn.p, h->tpool.p, 0, h->wtiles.p);
+    IETI_LAUNCHED_SIDE(h);
   }
+  IETI_CUDA(cudaEventRecord(h->fev[nlev], s2));
+  IETI_CUDA(cudaStreamWaitEvent(st, h->fev[nlev], 0));
   IETI_CHECK_LAUNCH();
 }
 

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -53,6 +54,47 @@ struct DevBuf {
 
 }  // namespace ieti
 
+// Launch tracer (IETIDP_TRACE=<file>): events recorded after each launch.
+struct LaunchTrace {
+  bool on = false;
+  std::string path;
+  std::vector<cudaEvent_t> ev;
+  std::vector<std::pair<const char*, int>> tag;
+  size_t used = 0;
+  void start(cudaStream_t s) {
+    if (!on) return;
+    used = 0;
+    mark(s, "start", 0);
+  }
+  void mark(cudaStream_t s, const char* file, int line) {
+    if (used == ev.size()) {
+      cudaEvent_t e;
+      if (cudaEventCreate(&e) != cudaSuccess) return;
+      ev.push_back(e);
+      tag.push_back({file, line});
+    }
+    tag[used] = {file, line};
+    cudaEventRecord(ev[used++], s);
+  }
+  void dump(const char* phase) {
+    if (!on || used < 2) return;
+    cudaEventSynchronize(ev[used - 1]);
+    FILE* f = fopen(path.c_str(), "a");
+    if (!f) return;
+    for (size_t i = 1; i < used; ++i) {
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, ev[i - 1], ev[i]);
+      const char* b = strrchr(tag[i].first, '/');
+      fprintf(f, "%s %s:%d %.2f\n", phase, b ? b + 1 : tag[i].first, tag[i].second, ms * 1e3);
+    }
+    fclose(f);
+    used = 0;
+  }
+  ~LaunchTrace() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+
 struct ietidp_s {
   ietidp_options opt{};
   int n_sub = 0, n_lambda = 0, n_primal = 0, nrhs = 1;
@@ -63,7 +105,11 @@ struct ietidp_s {
   ieti::Plan plan;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  // side stream of the factorisation (partitioned inverse, W_k) and its events
+  cudaStream_t side = nullptr;
+  std::vector<cudaEvent_t> fev;  // [0..levels): level's panels done; [levels]: side done
   long long launches = 0;
+  LaunchTrace trace;
   ietidp_report rep{};
 
   // ---- raw values (uploaded once, refreshed by ietidp_set_values) ----
@@ -87,6 +133,8 @@ struct ietidp_s {
   std::vector<long long> u_off;
   // ---- numeric ----
   ieti::DevBuf<double> pool, dinv, ipool, tpool, vecw;  // fronts, Dinv blocks, L11^-1, temp, sweep workspace
+  ieti::DevBuf<double> skws;                             // split-K partial products
+  ieti::DevBuf<int> skcnt;                               // split-K arrival counters (zero between uses)
   ieti::DevBuf<double> Xf, Xr;            // forward-swept loads (kept) / recovery sweep (ne rows x nrhs)
   ieti::DevBuf<double> S, Sinv, ftil, zc0;  // coarse: S_PP, S_PP^-1, ftilde, S^-1 ftilde
   ieti::DevBuf<long long> scoef_src;      // S_PP entry <- P-front pool offsets

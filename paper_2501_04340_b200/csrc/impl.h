@@ -11,6 +11,9 @@ namespace ieti {
 
 constexpr int TB = 64;  // panel width of the supernodal Cholesky = tile size everywhere
 constexpr int TILE_ELEMS = TB * TB;
+// split-K of the panel updates (long K on few tiles): aim for this many CTAs per launch
+// (3 resident GEMM CTAs per SM x 148 SMs), at most SPLITK_MAX parts of >= SPLITK_MIN_K
+constexpr int SPLITK_TARGET_CTAS = 444, SPLITK_MAX = 8, SPLITK_MIN_K = 128;
 
 // ---------------------------------------------------------------------------
 // Device descriptors (plain structs, copied to the device as arrays)
@@ -70,12 +73,18 @@ struct Work {
 struct GemmWork {
   long long c_off, a_off, b_off;
   int lda, ldb, ldc, m, n, kdim;
-  int mode;  // bit0: negate, bit1: accumulate into C, bit2: extend-add epilogue (below)
+  int mode;  // bit0: negate, bit1: accumulate into C, bit2: extend-add epilogue (below),
+             // bit3: split-K part (below)
   int diag;  // extend-add: the tile is on the diagonal of U (add only r >= c)
   // extend-add epilogue (multifrontal update of the parent, fused into the SYRK):
   //   parent[p_off + rel[rel_c + c] * p_ld + rel[rel_r + r]] += C[r][c] - (A B)[r][c]
   long long p_off;
-  int p_ld, rel_r, rel_c, pad_;
+  int p_ld, rel_r, rel_c;
+  // split-K (deterministic): part ks of nks writes its partial product to
+  //   ws[ws_off + ks * TILE_ELEMS] (column-major TB x TB); the last part to arrive
+  //   (counter cnt) adds sum_{s=0..nks-1} partial_s, in that order, into C.
+  int ks, nks, cnt;
+  long long ws_off;
 };
 
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).
@@ -129,6 +138,10 @@ struct LevelPlan {
   int fu_off = 0, fu_n = 0;                  // forward sweep: update items (sn, update-row tile)
   int bt_off = 0, bt_n = 0;                  // backward sweep: t items (sn, pivot col tile), nupd > 0
   int bx_off = 0, bx_n = 0;                  // backward sweep: x items (sn, pivot col tile)
+  // partitioned inverse L11^-1 of this level's supernodes (runs on the side stream
+  // as soon as the level's panels are factored, overlapping the SYRK and later levels)
+  int inv_copy_off = 0, inv_copy_n = 0;          // Work items (sn, panel) copying Dinv into L11^-1
+  std::vector<std::pair<int, int>> inv_rounds;   // GemmWork ranges, 2 per doubling round
 };
 
 struct Plan {
@@ -136,11 +149,11 @@ struct Plan {
   std::vector<SnHost> sn;     // all supernodes, global ids
   std::vector<int> level_sn;  // supernode ids grouped by level
   std::vector<LevelPlan> levels;
-  std::vector<std::pair<int, int>> inv_rounds;  // GemmWork ranges: (offset, count), 2 per round
   int w_off = 0, w_n = 0;                       // GemmWork: W = L_II^-T L_II^-1 lower tiles (explicit loop)
   std::vector<std::vector<int>> roots_by_level; // subdomains whose r_I root front is at level L
-  int inv_copy_off = 0, inv_copy_n = 0;         // Work items (sn, panel) copying Dinv into L11^-1
   long long pool_doubles = 0, dinv_doubles = 0, inv_doubles = 0, vec_rows = 0;
+  long long splitk_doubles = 0;  // split-K partials workspace (max over launches)
+  int splitk_tiles = 0;          // split-K counters (max tiles per launch)
   int max_level = 0, max_front = 0, max_nI = 0, nPmax = 0;
   long long nnz_L = 0, flops = 0, inv_flops = 0;
 };
