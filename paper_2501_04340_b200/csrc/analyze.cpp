@@ -635,6 +635,10 @@ void analyze_all(ietidp_s* h) {
         if ((int)gwork.size() > off) lp.syrk.push_back({off, (int)gwork.size() - off});
       }
     }
+    // assembly: zero the lower trapezoid of every front of this level (coarse node too)
+    lp.zr_off = (int)work.size() / 3;
+    for (int i : bylev[L])
+      for (int t = 0; t < tiles_of(P.sn[i].f); ++t, ++lp.zr_n) push(i, t, 0);
     // sweeps
     lp.fs_off = (int)work.size() / 3;
     for (int i : bylev[L])
@@ -802,18 +806,45 @@ void analyze_all(ietidp_s* h) {
       for (int j = 0; j <= i; ++j) {
         GemmWork g{};
         const int k0 = i * TB;
-        g.c_off = r.inv_off + (long long)(j * TB) * r.ldi + i * TB;
+        // written straight into the loop's row-major lower tile (i, j) of W
+        g.c_off = d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
         g.a_off = r.inv_off + (long long)(i * TB) * r.ldi + k0;  // A[r][k] = Linv[k][iTB + r] (k contiguous)
         g.b_off = r.inv_off + (long long)(j * TB) * r.ldi + k0;  // B[k][c] = Linv[k][jTB + c] (k contiguous)
-        g.lda = g.ldb = g.ldc = r.ldi;
+        g.lda = g.ldb = r.ldi;
+        g.ldc = TB;
         g.m = std::min(TB, d.nI - i * TB);
         g.n = std::min(TB, d.nI - j * TB);
         g.kdim = d.nI - k0;
-        g.mode = 0;
+        g.mode = 16;
+        g.diag = (i == j);
         gwork.push_back(g);
       }
   }
   P.w_n = (int)gwork.size() - P.w_off;
+  // G_k^T = L_PI L_II^-1 (n_P x n_I, column-major = G_k row-major), per 64-column tile
+  // of a: K = [a0, n_I) since L_II^-1[m][a] = 0 for m < a
+  P.g_off = (int)gwork.size();
+  for (int k = 0; k < ns; ++k) {
+    const SubDev& d = h->h_sub[k];
+    if (d.root < 0 || d.nP == 0 || d.nI == 0) continue;
+    const SnDev& r = sd[d.root];
+    for (int i = 0; i < d.nt; ++i) {
+      GemmWork g{};
+      const int a0 = i * TB;
+      g.c_off = d.g_off + (long long)a0 * d.nP;
+      g.a_off = d.lpi_off + a0;                          // A[q][k] = L_PI[q][a0 + k]
+      g.b_off = r.inv_off + (long long)a0 * r.ldi + a0;  // B[k][n] = Linv[a0 + k][a0 + n]
+      g.lda = d.nI;
+      g.ldb = r.ldi;
+      g.ldc = d.nP;
+      g.m = d.nP;
+      g.n = std::min(TB, d.nI - a0);
+      g.kdim = d.nI - a0;
+      g.mode = 0;
+      gwork.push_back(g);
+    }
+  }
+  P.g_n = (int)gwork.size() - P.g_off;
 
   // ---- scatter lists (per subdomain in parallel, merged per level) ----
   struct Scat {
@@ -869,12 +900,14 @@ void analyze_all(ietidp_s* h) {
   std::vector<long long> fdst, fxdst;
   std::vector<int> fsrc, fxsrc, kdiag;
   for (int L = 0; L <= P.max_level; ++L) {
+    P.levels[L].sc_off = (long long)fdst.size();
     for (int k = 0; k < ns; ++k) {
       fdst.insert(fdst.end(), sc[k].fd[L].begin(), sc[k].fd[L].end());
       fsrc.insert(fsrc.end(), sc[k].fs[L].begin(), sc[k].fs[L].end());
       std::vector<long long>().swap(sc[k].fd[L]);
       std::vector<int>().swap(sc[k].fs[L]);
     }
+    P.levels[L].sc_n = (long long)fdst.size() - P.levels[L].sc_off;
   }
   for (int k = 0; k < ns; ++k) {
     fxdst.insert(fxdst.end(), sc[k].fxd.begin(), sc[k].fxd.end());
@@ -961,7 +994,7 @@ void analyze_all(ietidp_s* h) {
       fprintf(stderr, "level %d: %d fronts, max npiv %d, max f %d, panels %d, GF %.2f\n", L, n, mx, mf,
               (mx + TB - 1) / TB, fl / 1e9);
     }
-    fprintf(stderr, "critical-path panels %d\n", crit);
+    fprintf(stderr, "critical-path panels %d, pool %.1f MB, inv %.1f MB\n", crit, P.pool_doubles * 8e-6, P.inv_doubles * 8e-6);
     auto gflops = [&](int off, int n) {
       long long f = 0;
       for (int q = off; q < off + n; ++q) f += 2LL * gwork[q].m * gwork[q].n * gwork[q].kdim;

@@ -18,6 +18,7 @@
 namespace ieti {
 
 void run_sweeps(ietidp_s* h, double* X, bool fwd, bool bwd);
+void launch_form_G(ietidp_s* h);
 void loop_fwd(ietidp_s* h, int ncols, const double* v, double* y, bool partials, const void* st);
 void loop_bwd(ietidp_s* h, int ncols, const double* y, const double* z, double zsign, double* x, const void* st);
 void bgather(ietidp_s* h, int ncols, const double* x, const double* weight, double* out, const double* dotv,
@@ -142,29 +143,42 @@ __global__ void k_scaling(int m, const LamDev* __restrict__ lam, const int* __re
   }
 }
 
-// Repack the r_I root front of every subdomain for the loop: L_II and L_II^-1
-// as row-major TB x TB lower tiles (row-block order), L_PI as nP x nI row-major.
-// One CTA per (subdomain, block row).
+// Repack the r_I root front of every subdomain for the loop: L_II^-1 (and, for the
+// triangular loop, L_II) as row-major TB x TB lower tiles (row-block order), L_PI as
+// nP x nI row-major. One CTA per (subdomain, lower tile); the tile is transposed
+// through shared memory. The CTAs of the tiles (i, 0) also write L_PI's columns of
+// block i.
 __global__ void __launch_bounds__(256)
     k_pack(const SubDev* __restrict__ sub, const SnDev* __restrict__ sn, const int* __restrict__ rows,
            const double* __restrict__ pool, const double* __restrict__ ipool, double* __restrict__ tiles,
-           double* __restrict__ itiles, double* __restrict__ lpi, int maxnt) {
-  const int k = blockIdx.x / maxnt, i = blockIdx.x % maxnt;
+           double* __restrict__ itiles, double* __restrict__ lpi, int maxnt, int want_tiles) {
+  __shared__ double S[TB][TB + 1];
+  const int ntl = maxnt * (maxnt + 1) / 2;
+  const int k = blockIdx.x / ntl, t = blockIdx.x % ntl;
+  int i = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while (i * (i + 1) / 2 > t) --i;
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  const int j = t - i * (i + 1) / 2;
   const SubDev d = sub[k];
   if (d.nI == 0 || i >= d.nt) return;
   const SnDev s = sn[d.root];
   const double* F = pool + s.front_off;
   const double* I = ipool + s.inv_off;
-  for (int j = 0; j <= i; ++j) {
-    const long long toff = d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
+  const long long toff = d.tile_off + (long long)t * TILE_ELEMS;
+  for (int pass = want_tiles ? 0 : 1; pass < 2; ++pass) {
+    const double* M = pass ? I : F;
+    const long long ld = pass ? s.ldi : s.ld;
     for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) {
-      const int c = e / TB, r = e % TB;  // read column-major (coalesced), write transposed
+      const int c = e >> 6, r = e & (TB - 1);  // coalesced column reads into smem
       const int R = i * TB + r, C = j * TB + c;
-      const bool in = R < d.nI && C < d.nI && R >= C;
-      tiles[toff + r * TB + c] = in ? F[(long long)C * s.ld + R] : 0.0;
-      itiles[toff + r * TB + c] = in ? I[(long long)C * s.ldi + R] : 0.0;
+      S[c][r] = (R < d.nI && C < d.nI && R >= C) ? M[(long long)C * ld + R] : 0.0;
     }
+    __syncthreads();
+    double* T = (pass ? itiles : tiles) + toff;
+    for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) T[e] = S[e & (TB - 1)][e >> 6];  // row writes
+    __syncthreads();
   }
+  if (j != 0) return;
   // L_PI: the root's update rows are P positions (>= nr)
   const int nu = s.f - s.npiv;
   const int* rw = rows + s.rows_off;
@@ -179,28 +193,6 @@ __global__ void __launch_bounds__(256)
       const int q = rw[rho] - d.nr;
       lpi[d.lpi_off + (long long)q * d.nI + a] = F[(long long)a * s.ld + s.npiv + rho];
     }
-  }
-}
-
-// G_k = L_II^-T L_PI^T (n_I x n_P, row-major): G[a][q] = sum_{m >= a} Linv[m][a] L_PI[q][m].
-// One CTA per (subdomain, 64-row chunk of G), warp per (a, q).
-__global__ void __launch_bounds__(256)
-    k_form_G(const SubDev* __restrict__ sub, const SnDev* __restrict__ sn, const double* __restrict__ ipool,
-             const double* __restrict__ lpi, double* __restrict__ G, int maxnt) {
-  const SubDev d = sub[blockIdx.x / maxnt];
-  const int chunk = blockIdx.x % maxnt;
-  if (d.nI == 0 || d.nP == 0 || chunk >= d.nt) return;
-  const SnDev s = sn[d.root];
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int a0 = chunk * TB, na = min(TB, d.nI - a0);
-  for (int e = warp; e < na * d.nP; e += 8) {
-    const int a = a0 + e / d.nP, q = e % d.nP;
-    const double* Ic = ipool + s.inv_off + (long long)a * s.ldi;  // column a of L_II^-1
-    const double* lp = lpi + d.lpi_off + (long long)q * d.nI;
-    double acc = 0.0;
-    for (int m = a + lane; m < d.nI; m += 32) acc += Ic[m] * lp[m];
-    acc = warp_sum(acc);
-    if (lane == 0) G[d.g_off + (long long)a * d.nP + q] = acc;
   }
 }
 
@@ -245,6 +237,9 @@ __global__ void __launch_bounds__(256)
 void run_coarse(ietidp_s* h) {
   cudaStream_t s = h->stream;
   const int nrhs = h->nrhs, ng = h->n_primal;
+  const int nlev = h->plan.max_level + 1;
+  // every L11^-1 is ready (factorisation side stream)
+  IETI_CUDA(cudaStreamWaitEvent(s, h->fev[nlev + 2], 0));
   if (h->n_lambda) {
     k_scaling<<<grid_for(h->n_lambda, 256), 256, 0, s>>>(h->n_lambda, h->lam.p, h->kdiag_src.p, h->kval.p, h->kdiag.p,
                                                         h->delta.p, h->opt.scaling == IETIDP_SCALE_STIFFNESS);
@@ -253,22 +248,23 @@ void run_coarse(ietidp_s* h) {
   int maxnt = 0;
   for (auto& d : h->h_sub) maxnt = std::max(maxnt, d.nt);
   if (maxnt) {
-    k_pack<<<h->n_sub * maxnt, 256, 0, s>>>(h->d_sub.p, h->d_sn.p, h->d_rows.p, h->pool.p, h->ipool.p, h->tiles.p,
-                                            h->itiles.p, h->lpi.p, maxnt);
+    k_pack<<<h->n_sub * (maxnt * (maxnt + 1) / 2), 256, 0, s>>>(h->d_sub.p, h->d_sn.p, h->d_rows.p, h->pool.p, h->ipool.p, h->tiles.p,
+                                            h->itiles.p, h->lpi.p, maxnt, h->opt.loop == IETIDP_LOOP_TRIANGULAR);
     IETI_LAUNCHED(h);
-    if (ng > 0) {
-      k_form_G<<<h->n_sub * maxnt, 256, 0, s>>>(h->d_sub.p, h->d_sn.p, h->ipool.p, h->lpi.p, h->G.p, maxnt);
-      IETI_LAUNCHED(h);
-    }
+    if (ng > 0) launch_form_G(h);
   }
   // loads -> X (position order), forward sweep: X = L^-1 j, P rows = ftilde^(k)
-  h->Xf.zero(s);
-  if (h->sc_fx_dst.n) {
-    k_scatter<<<grid_for((long long)h->sc_fx_dst.n, 256), 256, 0, s>>>((long long)h->sc_fx_dst.n, h->sc_fx_dst.p,
-                                                                      h->sc_fx_src.p, h->fval.p, h->Xf.p);
-    IETI_LAUNCHED(h);
+  if (!h->fwd_in_factor) {
+    h->Xf.zero(s);
+    if (h->sc_fx_dst.n) {
+      k_scatter<<<grid_for((long long)h->sc_fx_dst.n, 256), 256, 0, s>>>((long long)h->sc_fx_dst.n, h->sc_fx_dst.p,
+                                                                        h->sc_fx_src.p, h->fval.p, h->Xf.p);
+      IETI_LAUNCHED(h);
+    }
+    run_sweeps(h, h->Xf.p, true, false);
+  } else {
+    IETI_CUDA(cudaStreamWaitEvent(s, h->fev[nlev + 3], 0));
   }
-  run_sweeps(h, h->Xf.p, true, false);
   if (ng > 0) {
     const int smem = ng * (ng + 1) / 2 * sizeof(double);
     if (smem > 220 * 1024) throw Error(IETIDP_E_ARG, "coarse problem too large for the one-CTA coarse factorisation");
@@ -285,6 +281,7 @@ void run_coarse(ietidp_s* h) {
     loop_bwd(h, nrhs, h->yI.p, ng ? h->zc0.p : nullptr, -1.0, h->xI.p, nullptr);
     bgather(h, nrhs, h->xI.p, nullptr, h->d_vec.p, nullptr, nullptr, nullptr);
   }
+  IETI_CUDA(cudaStreamWaitEvent(s, h->fev[nlev], 0));  // W_k ready: join the side stream
   IETI_CHECK_LAUNCH();
 }
 

@@ -27,6 +27,19 @@ __global__ void k_scatter(long long n, const long long* __restrict__ dst, const 
     out[dst[i]] = vals[src[i]];
 }
 
+// Zero the lower trapezoid of columns [64 w.a, 64 w.a + 64) of front w.sn (rows c..f-1
+// of column c): the only part of a front any kernel reads.
+__global__ void __launch_bounds__(256) k_zero_fronts(const Work* __restrict__ work, const SnDev* __restrict__ sn,
+                                                     double* __restrict__ pool) {
+  const Work w = work[blockIdx.x];
+  const SnDev s = sn[w.sn];
+  const int c0 = w.a * TB, c1 = min(s.f, c0 + TB);
+  double* F = pool + s.front_off;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = c0 + warp; c < c1; c += 8)
+    for (int r = c + lane; r < s.f; r += 32) F[(long long)c * s.ld + r] = 0.0;
+}
+
 // POTRF of the diagonal block of panel w.a of front w.sn, and its inverse Dinv = L^-1.
 // 128 threads; thread (r, h) holds the columns c = 2i + h (i < 32) of row r in registers
 // (h is warp-uniform). Elimination step j (64 unrolled steps, one barrier each):
@@ -360,6 +373,19 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
     if (tid == 0) skcnt[w.cnt] = 0;  // ready for the next launch
     return;
   }
+  if (w.mode & 16) {
+    // row-major TB x TB tile (the loop's symmetric tile layout), zero padded
+    for (int r = warp; r < TB; r += 4) {
+      const int c = 2 * lane;
+      double v[2] = {0.0, 0.0};
+#pragma unroll
+      for (int q = 0; q < 2; ++q)
+        if (r < w.m && c + q < w.n)
+          v[q] = (w.diag && r < c + q) ? Ts[r * ETS + c + q] : Ts[(c + q) * ETS + r];
+      *reinterpret_cast<double2*>(Cb + w.c_off + r * TB + c) = make_double2(v[0], v[1]);
+    }
+    return;
+  }
   const bool ok0 = r0 < w.m, ok1 = r0 + 1 < w.m;
   if (w.mode & 4) {
     // fused multifrontal extend-add: parent[rel_c[c], rel_r[r]] += C - A B (lower part)
@@ -437,31 +463,52 @@ __global__ void k_inv_copy(const Work* __restrict__ work, const SnDev* __restric
 
 // Pack the symmetric n_I x n_I matrix held in the lower triangle of a column-major
 // block (the r_I root front, or its L11^-1-shaped buffer) into row-major lower
-// TB-tiles with full (mirrored) diagonal tiles. One CTA per (entry, block row).
+// TB-tiles with full (mirrored) diagonal tiles. One CTA per (entry, block row); each
+// tile is transposed through shared memory (coalesced column reads, row writes).
 __global__ void __launch_bounds__(256)
     k_pack_sym(const int* __restrict__ list, int maxnt, const SubDev* __restrict__ sub, const SnDev* __restrict__ sn,
                const double* __restrict__ base, int from_front, double* __restrict__ dst) {
-  const int e = blockIdx.x / maxnt, i = blockIdx.x % maxnt;
+  __shared__ double S[TB][TB + 1];
+  const int ntl = maxnt * (maxnt + 1) / 2;  // one CTA per lower tile (i, j)
+  const int e = blockIdx.x / ntl, t = blockIdx.x % ntl;
+  int i = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while (i * (i + 1) / 2 > t) --i;
+  while ((i + 1) * (i + 2) / 2 <= t) ++i;
+  const int j = t - i * (i + 1) / 2;
   const int k = list ? list[e] : e;
   const SubDev d = sub[k];
   if (d.nI == 0 || i >= d.nt) return;
   const SnDev s = sn[d.root];
   const double* M = base + (from_front ? s.front_off : s.inv_off);
   const long long ld = from_front ? s.ld : s.ldi;
-  for (int j = 0; j <= i; ++j) {
-    double* T = dst + d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
-    for (int q = threadIdx.x; q < TILE_ELEMS; q += blockDim.x) {
-      const int c = q / TB, r = q % TB;
-      const int R = i * TB + r, C = j * TB + c;
-      double v = 0.0;
-      if (R < d.nI && C < d.nI) v = (R >= C) ? M[(long long)C * ld + R] : M[(long long)R * ld + C];
-      T[r * TB + c] = v;
-    }
+  // S[c][r] = M(iTB + r, jTB + c), lower entries only (column c contiguous in r)
+  for (int q = threadIdx.x; q < TILE_ELEMS; q += blockDim.x) {
+    const int c = q >> 6, r = q & (TB - 1);
+    const int R = i * TB + r, C = j * TB + c;
+    S[c][r] = (R < d.nI && C < d.nI && R >= C) ? M[(long long)C * ld + R] : 0.0;
+  }
+  __syncthreads();
+  double* T = dst + d.tile_off + (long long)t * TILE_ELEMS;
+  for (int q = threadIdx.x; q < TILE_ELEMS; q += blockDim.x) {
+    const int r = q >> 6, c = q & (TB - 1);
+    T[q] = (i == j && r < c) ? S[r][c] : S[c][r];  // diagonal tile: mirror the lower part
   }
 }
 
 static void set_smem(const void* f, int bytes) {
   IETI_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
+}
+
+void fwd_sweep_level(ietidp_s* h, double* X, int L, cudaStream_t st);
+
+// G_k^T = L_PI L_II^-1 for every subdomain (one DMMA GEMM launch; after k_pack's L_PI)
+void launch_form_G(ietidp_s* h) {
+  const Plan& P = h->plan;
+  if (!P.g_n) return;
+  set_smem((const void*)k_gemm<true, true>, GEMM_SMEM);
+  k_gemm<true, true><<<P.g_n, 128, GEMM_SMEM, h->stream>>>(h->d_gwork.p + P.g_off, h->lpi.p, h->ipool.p, h->G.p,
+                                                           h->d_rel.p);
+  IETI_LAUNCHED(h);
 }
 
 void run_factor(ietidp_s* h) {
@@ -479,13 +526,22 @@ void run_factor(ietidp_s* h) {
   const Work* W = reinterpret_cast<const Work*>(h->d_work.p);
   const GemmWork* GW = h->d_gwork.p;
   double* pool = h->pool.p;
-  // assembly of every front at once: zero the pool, scatter all of K's entries
-  IETI_CUDA(cudaMemsetAsync(pool, 0, h->pool.n * sizeof(double), st));
-  const long long ne = (long long)h->sc_front_dst.n;
-  if (ne > 0) {
-    k_scatter<<<grid_for(ne, 256), 256, 0, st>>>(ne, h->sc_front_dst.p, h->sc_front_src.p, h->kval.p, pool);
-    IETI_LAUNCHED(h);
-  }
+  // assembly of the fronts, level by level: zero the lower trapezoids, scatter K's
+  // entries. Level 0 on the main stream; the levels above on the side stream while
+  // level 0 is factored (the main stream waits for them before the first SYRK).
+  auto assemble = [&](int L, cudaStream_t sx) {
+    const LevelPlan& lp = P.levels[L];
+    if (lp.zr_n) {
+      k_zero_fronts<<<lp.zr_n, 256, 0, sx>>>(W + lp.zr_off, h->d_sn.p, pool);
+      if (sx == st) IETI_LAUNCHED(h); else IETI_LAUNCHED_SIDE(h);
+    }
+    if (lp.sc_n) {
+      k_scatter<<<grid_for(lp.sc_n, 256), 256, 0, sx>>>(lp.sc_n, h->sc_front_dst.p + lp.sc_off,
+                                                          h->sc_front_src.p + lp.sc_off, h->kval.p, pool);
+      if (sx == st) IETI_LAUNCHED(h); else IETI_LAUNCHED_SIDE(h);
+    }
+  };
+  assemble(0, st);
   const int* rel = h->d_rel.p;
   int maxnt = 0;
   for (auto& d : h->h_sub) maxnt = std::max(maxnt, d.nt);
@@ -497,17 +553,29 @@ void run_factor(ietidp_s* h) {
   const int nlev = P.max_level + 1;
   if (!h->side) {
     IETI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
-    h->fev.resize(nlev + 2);
+    h->fev.resize(nlev + 5);
     for (auto& e : h->fev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t s2 = h->side;
-  IETI_CUDA(cudaEventRecord(h->fev[nlev + 1], st));  // side work starts after the scatter
+  IETI_CUDA(cudaEventRecord(h->fev[nlev + 1], st));  // side work starts after level 0's assembly
   IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[nlev + 1], 0));
+  for (int L = 1; L < nlev; ++L) assemble(L, s2);
+  IETI_CUDA(cudaEventRecord(h->fev[nlev + 4], s2));  // every front assembled
+  // the forward sweep of the loads rides on the side stream too (one column chunk)
+  h->fwd_in_factor = h->nrhs <= 16;
+  if (h->fwd_in_factor) {
+    h->Xf.zero(s2);
+    if (h->sc_fx_dst.n) {
+      k_scatter<<<grid_for((long long)h->sc_fx_dst.n, 256), 256, 0, s2>>>(
+          (long long)h->sc_fx_dst.n, h->sc_fx_dst.p, h->sc_fx_src.p, h->fval.p, h->Xf.p);
+      IETI_LAUNCHED_SIDE(h);
+    }
+  }
   for (int L = 0; L < nlev; ++L) {
     const LevelPlan& lp = P.levels[L];
     // explicit loop: S_II is the assembled r_I root front before its factorisation
     if (expl && h->rootlist_range[L].second > 0) {
-      k_pack_sym<<<h->rootlist_range[L].second * maxnt, 256, 0, st>>>(h->d_rootlist.p + h->rootlist_range[L].first,
+      k_pack_sym<<<h->rootlist_range[L].second * (maxnt * (maxnt + 1) / 2), 256, 0, st>>>(h->d_rootlist.p + h->rootlist_range[L].first,
                                                                        maxnt, h->d_sub.p, h->d_sn.p, pool, 1,
                                                                        h->stiles.p);
       IETI_LAUNCHED(h);
@@ -528,6 +596,7 @@ void run_factor(ietidp_s* h) {
       }
     }
     IETI_CUDA(cudaEventRecord(h->fev[L], st));
+    if (L == 0) IETI_CUDA(cudaStreamWaitEvent(st, h->fev[nlev + 4], 0));  // parents assembled
     for (auto& sy : lp.syrk) {
       k_gemm<false><<<sy.second, 128, GEMM_SMEM, st>>>(GW + sy.first, pool, pool, pool, rel);
       IETI_LAUNCHED(h);
@@ -547,16 +616,16 @@ void run_factor(ietidp_s* h) {
                                                       step1 ? h->tpool.p : h->ipool.p, rel);
       IETI_LAUNCHED_SIDE(h);
     }
+    if (L == nlev - 1) IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));  // every L11^-1 done
+    if (h->fwd_in_factor) fwd_sweep_level(h, h->Xf.p, L, s2);
   }
-  // explicit loop: W_k = L_II^-T L_II^-1 (lower tiles; tpool is free again)
+  IETI_CUDA(cudaEventRecord(h->fev[nlev + 3], s2));  // forward sweep done
+  // explicit loop: W_k = L_II^-T L_II^-1, straight into the loop's lower tiles
   if (expl && P.w_n) {
-    k_gemm<true, true><<<P.w_n, 128, GEMM_SMEM, s2>>>(GW + P.w_off, h->ipool.p, h->ipool.p, h->tpool.p, rel);
-    IETI_LAUNCHED_SIDE(h);
-    k_pack_sym<<<h->n_sub * maxnt, 256, 0, s2>>>(nullptr, maxnt, h->d_sub.p, h->d_sn.p, h->tpool.p, 0, h->wtiles.p);
+    k_gemm<true, true><<<P.w_n, 128, GEMM_SMEM, s2>>>(GW + P.w_off, h->ipool.p, h->ipool.p, h->wtiles.p, rel);
     IETI_LAUNCHED_SIDE(h);
   }
-  IETI_CUDA(cudaEventRecord(h->fev[nlev], s2));
-  IETI_CUDA(cudaStreamWaitEvent(st, h->fev[nlev], 0));
+  IETI_CUDA(cudaEventRecord(h->fev[nlev], s2));  // side stream done (joined in run_coarse)
   IETI_CHECK_LAUNCH();
 }
 

@@ -108,6 +108,7 @@ struct ietidp_s {
   // side stream of the factorisation (partitioned inverse, W_k) and its events
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> fev;  // [0..levels): level's panels done; [levels]: side done
+  bool fwd_in_factor = false;    // the forward sweep of the loads ran on the side stream
   long long launches = 0;
   LaunchTrace trace;
   ietidp_report rep{};

@@ -74,7 +74,8 @@ struct GemmWork {
   long long c_off, a_off, b_off;
   int lda, ldb, ldc, m, n, kdim;
   int mode;  // bit0: negate, bit1: accumulate into C, bit2: extend-add epilogue (below),
-             // bit3: split-K part (below)
+             // bit3: split-K part (below), bit4: C is a row-major TB x TB tile at c_off
+             // (zero padded; with diag, the upper part mirrors the lower)
   int diag;  // extend-add: the tile is on the diagonal of U (add only r >= c)
   // extend-add epilogue (multifrontal update of the parent, fused into the SYRK):
   //   parent[p_off + rel[rel_c + c] * p_ld + rel[rel_r + r]] += C[r][c] - (A B)[r][c]
@@ -141,6 +142,10 @@ struct LevelPlan {
   // partitioned inverse L11^-1 of this level's supernodes (runs on the side stream
   // as soon as the level's panels are factored, overlapping the SYRK and later levels)
   int inv_copy_off = 0, inv_copy_n = 0;          // Work items (sn, panel) copying Dinv into L11^-1
+  // front assembly of this level: zero the lower trapezoids (Work items (sn, column
+  // tile)), then scatter K's entries (range of the scatter list)
+  int zr_off = 0, zr_n = 0;
+  long long sc_off = 0, sc_n = 0;
   std::vector<std::pair<int, int>> inv_rounds;   // GemmWork ranges, 2 per doubling round
 };
 
@@ -150,6 +155,7 @@ struct Plan {
   std::vector<int> level_sn;  // supernode ids grouped by level
   std::vector<LevelPlan> levels;
   int w_off = 0, w_n = 0;                       // GemmWork: W = L_II^-T L_II^-1 lower tiles (explicit loop)
+  int g_off = 0, g_n = 0;                       // GemmWork: G_k^T = L_PI L_II^-1
   std::vector<std::vector<int>> roots_by_level; // subdomains whose r_I root front is at level L
   long long pool_doubles = 0, dinv_doubles = 0, inv_doubles = 0, vec_rows = 0;
   long long splitk_doubles = 0;  // split-K partials workspace (max over launches)

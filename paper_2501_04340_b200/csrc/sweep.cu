@@ -234,6 +234,37 @@ static void sweeps_t(ietidp_s* h, double* X, bool fwd, bool bwd, int cofs) {
   IETI_CHECK_LAUNCH();
 }
 
+// Forward sweep of one level for every column (nrhs <= 16), on stream st: used by the
+// factorisation's side stream, level by level as the partitioned inverse completes.
+template <int NCB>
+static void fwd_level_t(ietidp_s* h, double* X, int L, cudaStream_t st) {
+  const LevelPlan& lp = h->plan.levels[L];
+  const Work* W = reinterpret_cast<const Work*>(h->d_work.p);
+  const int ldx = h->nrhs;
+  if (!lp.sn_n) return;
+  k_fs_assemble<NCB><<<lp.sn_n, SWT, 0, st>>>(h->d_level_sn.p + lp.sn_off, h->d_sn.p, h->d_sub.p, h->d_rel.p,
+                                              h->d_children.p, X, h->vecw.p, ldx, 0);
+  IETI_LAUNCHED_SIDE(h);
+  if (lp.fs_n) {
+    k_fs_gemv<0, NCB><<<lp.fs_n, SWT, 0, st>>>(W + lp.fs_off, h->d_sn.p, h->d_sub.p, h->pool.p, h->ipool.p, X,
+                                               h->vecw.p, ldx, 0);
+    IETI_LAUNCHED_SIDE(h);
+  }
+  if (lp.fu_n) {
+    k_fs_gemv<1, NCB><<<lp.fu_n, SWT, 0, st>>>(W + lp.fu_off, h->d_sn.p, h->d_sub.p, h->pool.p, h->ipool.p, X,
+                                               h->vecw.p, ldx, 0);
+    IETI_LAUNCHED_SIDE(h);
+  }
+}
+void fwd_sweep_level(ietidp_s* h, double* X, int L, cudaStream_t st) {
+  const int n = h->nrhs;
+  if (n == 1) fwd_level_t<1>(h, X, L, st);
+  else if (n == 2) fwd_level_t<2>(h, X, L, st);
+  else if (n <= 4) fwd_level_t<4>(h, X, L, st);
+  else if (n <= 8) fwd_level_t<8>(h, X, L, st);
+  else fwd_level_t<16>(h, X, L, st);
+}
+
 // X (ne rows per subdomain x nrhs) <- L^-1 X (forward) and/or L^-T X (backward).
 void run_sweeps(ietidp_s* h, double* X, bool fwd, bool bwd) {
   const int nc = h->nrhs;
