@@ -501,6 +501,12 @@ void analyze_all(ietidp_s* h) {
   }
 
   auto push = [&](int a, int b, int c) { work.insert(work.end(), {a, b, c}); };
+  // L11^-1 of the levels holding r_I roots is formed block row by block row as their
+  // panels complete (it sits on the path to the loop); the other levels use recursive
+  // doubling once the level is factored
+  std::vector<char> prog_level(P.max_level + 1, 0);
+  for (auto& sp : P.subs)
+    if (sp.root >= 0) prog_level[P.sn[sp.root].level] = 1;
   auto tiles_of = [](int n) { return (n + TB - 1) / TB; };
   // ---- work lists: factorisation and sweeps, per level ----
   for (int L = 0; L <= P.max_level; ++L) {
@@ -591,6 +597,59 @@ void analyze_all(ietidp_s* h) {
           gwork.push_back(g);
         }
       }
+      // (e) progressive inverse of block row kp of L11^-1 (side stream)
+      pn.icopy_off = (int)work.size() / 3;
+      for (int i : bylev[L])
+        if (prog_level[L] && !P.sn[i].coarse && P.sn[i].npiv > kp * TB) {
+          push(i, kp, 0);
+          pn.icopy_n++;
+        }
+      pn.ia_off = (int)gwork.size();
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (!prog_level[L] || s.coarse || s.npiv <= kp * TB || kp == 0) continue;
+        const SnDev& d = sd[i];
+        const int p0 = kp * TB, b = std::min(TB, s.npiv - p0);
+        for (int k = 0; k < kp; ++k, ++pn.ia_n) {
+          // T[kp][k] = L[kp][k:kp] L11^-1[k:kp][k]  (into tpool at L11^-1[kp][k])
+          GemmWork g{};
+          g.c_off = d.inv_off + (long long)k * TB * d.ldi + p0;
+          g.a_off = d.front_off + (long long)k * TB * d.ld + p0;  // A[r][m] = L[p0 + r][kTB + m]
+          g.b_off = d.inv_off + (long long)k * TB * d.ldi + k * TB;  // B[m][n] = Linv[kTB + m][kTB + n]
+          g.lda = d.ld;
+          g.ldb = d.ldi;
+          g.ldc = d.ldi;
+          g.m = b;
+          g.n = TB;
+          g.kdim = p0 - k * TB;
+          g.mode = 0;
+          gwork.push_back(g);
+        }
+      }
+      pn.ib_off = (int)gwork.size();
+      for (int i : bylev[L]) {
+        const SnHost& s = P.sn[i];
+        if (!prog_level[L] || s.coarse || s.npiv <= kp * TB || kp == 0) continue;
+        const SnDev& d = sd[i];
+        const int p0 = kp * TB, b = std::min(TB, s.npiv - p0);
+        for (int k = 0; k < kp; ++k, ++pn.ib_n) {
+          // L11^-1[kp][k] = -Dinv_kp T[kp][k]
+          GemmWork g{};
+          g.c_off = d.inv_off + (long long)k * TB * d.ldi + p0;
+          g.a_off = d.dinv_off + (long long)kp * TILE_ELEMS;  // A = Dinv_kp (column-major TB x TB)
+          g.b_off = d.inv_off + (long long)k * TB * d.ldi + p0;  // B[m][n] = T[p0 + m][kTB + n] (tpool)
+          g.lda = TB;
+          g.ldb = d.ldi;
+          g.ldc = d.ldi;
+          g.m = b;
+          g.n = TB;
+          g.kdim = b;
+          g.mode = 1;  // negate
+          gwork.push_back(g);
+        }
+      }
+      pn.wacc_off = (int)gwork.size();  // filled below, once the loop tile offsets are known
+      pn.wacc_n = 0;
       lp.panels.push_back(pn);
     }
     // (d) update block: parent[rel] += F22 - L21 L21^T (lower tiles, K = npiv), fused
@@ -660,6 +719,7 @@ void analyze_all(ietidp_s* h) {
   // ---- partitioned inverse L11^-1 by recursive doubling over TB-blocks, per level ----
   for (int L = 0; L <= P.max_level; ++L) {
     LevelPlan& lp = P.levels[L];
+    if (prog_level[L]) continue;  // progressive, per panel (above)
     lp.inv_copy_off = (int)work.size() / 3;
     int maxnb = 0;
     for (int i : bylev[L])
@@ -792,35 +852,40 @@ void analyze_all(ietidp_s* h) {
   h->n_slots = (int)rio;
   h->sum_nP = po;
   h->n_loopwork = (int)loopwork.size();
-  // explicit loop operators: W = L_II^-T L_II^-1 (lower tiles, into tpool at the root's
-  // L11^-1 layout) and the roots by level (S_II is copied before the root is factored)
+  // the r_I roots by level (S_II is copied before the root is factored)
   P.roots_by_level.assign(P.max_level + 1, {});
-  P.w_off = (int)gwork.size();
-  for (int k = 0; k < ns; ++k) {
-    const SubDev& d = h->h_sub[k];
-    if (d.root < 0) continue;
-    P.roots_by_level[P.sn[d.root].level].push_back(k);
-    if (h->opt.loop != IETIDP_LOOP_EXPLICIT) continue;
-    const SnDev& r = sd[d.root];
-    for (int i = 0; i < d.nt; ++i)
-      for (int j = 0; j <= i; ++j) {
-        GemmWork g{};
-        const int k0 = i * TB;
-        // written straight into the loop's row-major lower tile (i, j) of W
-        g.c_off = d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
-        g.a_off = r.inv_off + (long long)(i * TB) * r.ldi + k0;  // A[r][k] = Linv[k][iTB + r] (k contiguous)
-        g.b_off = r.inv_off + (long long)(j * TB) * r.ldi + k0;  // B[k][c] = Linv[k][jTB + c] (k contiguous)
-        g.lda = g.ldb = r.ldi;
-        g.ldc = TB;
-        g.m = std::min(TB, d.nI - i * TB);
-        g.n = std::min(TB, d.nI - j * TB);
-        g.kdim = d.nI - k0;
-        g.mode = 16;
-        g.diag = (i == j);
-        gwork.push_back(g);
+  for (int k = 0; k < ns; ++k)
+    if (h->h_sub[k].root >= 0) P.roots_by_level[P.sn[h->h_sub[k].root].level].push_back(k);
+  // W_k = L_II^-T L_II^-1 accumulated block row by block row of L_II^-1 as the r_I
+  // root's panels complete: W[i][j] += L11^-1[kp][i]^T L11^-1[kp][j], j <= i <= kp,
+  // written into the loop's row-major lower tiles (zeroed before the factorisation)
+  for (int L = 0; L <= P.max_level; ++L)
+    for (int kp = 0; kp < (int)P.levels[L].panels.size(); ++kp) {
+      LevelPlan::Panel& pn = P.levels[L].panels[kp];
+      pn.wacc_off = (int)gwork.size();
+      if (h->opt.loop != IETIDP_LOOP_EXPLICIT) continue;
+      for (int k : P.roots_by_level[L]) {
+        const SubDev& d = h->h_sub[k];
+        if (kp >= d.nt) continue;
+        const SnDev& r = sd[d.root];
+        const int p0 = kp * TB, b = std::min(TB, d.nI - p0);
+        for (int i = 0; i <= kp; ++i)
+          for (int j = 0; j <= i; ++j, ++pn.wacc_n) {
+            GemmWork g{};
+            g.c_off = d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
+            g.a_off = r.inv_off + (long long)(i * TB) * r.ldi + p0;  // A[rr][m] = Linv[p0 + m][iTB + rr]
+            g.b_off = r.inv_off + (long long)(j * TB) * r.ldi + p0;  // B[m][c] = Linv[p0 + m][jTB + c]
+            g.lda = g.ldb = r.ldi;
+            g.ldc = TB;
+            g.m = std::min(TB, d.nI - i * TB);
+            g.n = std::min(TB, d.nI - j * TB);
+            g.kdim = b;
+            g.mode = 16 | 2;  // accumulate into the row-major tile
+            g.diag = (i == j);
+            gwork.push_back(g);
+          }
       }
-  }
-  P.w_n = (int)gwork.size() - P.w_off;
+    }
   // G_k^T = L_PI L_II^-1 (n_P x n_I, column-major = G_k row-major), per 64-column tile
   // of a: K = [a0, n_I) since L_II^-1[m][a] = 0 for m < a
   P.g_off = (int)gwork.size();

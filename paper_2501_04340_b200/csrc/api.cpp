@@ -225,14 +225,35 @@ ietidp_status ietidp_factor(ietidp_t h) {
     h->factored = false;
     h->solved = false;
     h->factor_failed = true;
+    // The factorisation's critical path runs on an internal highest-priority stream
+    // (ordered after the caller's stream and joined back into it), so that its
+    // latency-bound panel kernels are scheduled ahead of the side stream's work.
+    if (!h->hp) {
+      int lo = 0, hi = 0;
+      IETI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+      IETI_CUDA(cudaStreamCreateWithPriority(&h->hp, cudaStreamNonBlocking, hi));
+      IETI_CUDA(cudaEventCreateWithFlags(&h->hp_ev, cudaEventDisableTiming));
+    }
+    cudaStream_t user = h->stream;
+    IETI_CUDA(cudaEventRecord(h->hp_ev, user));
+    IETI_CUDA(cudaStreamWaitEvent(h->hp, h->hp_ev, 0));
+    h->stream = h->hp;
     EvPair e1, e2;
-    IETI_CUDA(cudaEventRecord(e1.a, h->stream));
-    h->trace.start(h->stream);
-    ieti::run_factor(h);
-    IETI_CUDA(cudaEventRecord(e1.b, h->stream));
-    IETI_CUDA(cudaEventRecord(e2.a, h->stream));
-    ieti::run_coarse(h);
-    IETI_CUDA(cudaEventRecord(e2.b, h->stream));
+    try {
+      IETI_CUDA(cudaEventRecord(e1.a, h->stream));
+      h->trace.start(h->stream);
+      ieti::run_factor(h);
+      IETI_CUDA(cudaEventRecord(e1.b, h->stream));
+      IETI_CUDA(cudaEventRecord(e2.a, h->stream));
+      ieti::run_coarse(h);
+      IETI_CUDA(cudaEventRecord(e2.b, h->stream));
+    } catch (...) {
+      h->stream = user;
+      throw;
+    }
+    h->stream = user;
+    IETI_CUDA(cudaEventRecord(h->hp_ev, h->hp));
+    IETI_CUDA(cudaStreamWaitEvent(user, h->hp_ev, 0));
     int flags[2];
     IETI_CUDA(cudaMemcpyAsync(flags, h->err_flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     IETI_CUDA(cudaStreamSynchronize(h->stream));
@@ -394,6 +415,9 @@ void ietidp_destroy(ietidp_t h) {
   if (h->stream) cudaStreamSynchronize(h->stream);
   ieti::destroy_graph(h);
   for (auto e : h->fev) cudaEventDestroy(e);
+  for (auto e : h->pev) cudaEventDestroy(e);
+  if (h->hp_ev) cudaEventDestroy(h->hp_ev);
+  if (h->hp) cudaStreamDestroy(h->hp);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;

@@ -382,7 +382,13 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
       for (int q = 0; q < 2; ++q)
         if (r < w.m && c + q < w.n)
           v[q] = (w.diag && r < c + q) ? Ts[r * ETS + c + q] : Ts[(c + q) * ETS + r];
-      *reinterpret_cast<double2*>(Cb + w.c_off + r * TB + c) = make_double2(v[0], v[1]);
+      double2* T = reinterpret_cast<double2*>(Cb + w.c_off + r * TB + c);
+      if (w.mode & 2) {
+        const double2 o = *T;
+        v[0] += o.x;
+        v[1] += o.y;
+      }
+      *T = make_double2(v[0], v[1]);
     }
     return;
   }
@@ -555,11 +561,19 @@ void run_factor(ietidp_s* h) {
     IETI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
     h->fev.resize(nlev + 5);
     for (auto& e : h->fev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    size_t np = 0;
+    for (auto& lv : P.levels) np += lv.panels.size();
+    h->pev.resize(np);
+    for (auto& e : h->pev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   cudaStream_t s2 = h->side;
+  size_t npan = 0;
+  const LevelPlan::Panel* wacc_last = nullptr;
+  IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));
   IETI_CUDA(cudaEventRecord(h->fev[nlev + 1], st));  // side work starts after level 0's assembly
   IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[nlev + 1], 0));
   for (int L = 1; L < nlev; ++L) assemble(L, s2);
+  if (expl) h->wtiles.zero(s2);  // W_k is accumulated block row by block row
   IETI_CUDA(cudaEventRecord(h->fev[nlev + 4], s2));  // every front assembled
   // the forward sweep of the loads rides on the side stream too (one column chunk)
   h->fwd_in_factor = h->nrhs <= 16;
@@ -590,9 +604,33 @@ void run_factor(ietidp_s* h) {
         k_potrf<<<pn.potrf_n, POTRF_T, 0, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
         IETI_LAUNCHED(h);
       }
+      cudaEvent_t pe = h->pev[npan++];
+      IETI_CUDA(cudaEventRecord(pe, st));
       if (pn.trsm_n) {
         k_gemm<false><<<pn.trsm_n, 128, GEMM_SMEM, st>>>(GW + pn.trsm_off, pool, h->dinv.p, pool, rel);
         IETI_LAUNCHED(h);
+      }
+      // side stream: block row kp of L11^-1 (and of W_k) as soon as Dinv_kp exists
+      IETI_CUDA(cudaStreamWaitEvent(s2, pe, 0));
+      if (pn.icopy_n) {
+        k_inv_copy<<<pn.icopy_n, 256, 0, s2>>>(W + pn.icopy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
+        IETI_LAUNCHED_SIDE(h);
+      }
+      if (pn.ia_n) {
+        k_gemm<true><<<pn.ia_n, 128, GEMM_SMEM, s2>>>(GW + pn.ia_off, pool, h->ipool.p, h->tpool.p, rel);
+        IETI_LAUNCHED_SIDE(h);
+      }
+      if (pn.ib_n) {
+        k_gemm<true><<<pn.ib_n, 128, GEMM_SMEM, s2>>>(GW + pn.ib_off, h->dinv.p, h->tpool.p, h->ipool.p, rel);
+        IETI_LAUNCHED_SIDE(h);
+      }
+      if (pn.icopy_n) IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));  // last record: every L11^-1 done
+      if (&pn == &lp.panels.back()) {
+        wacc_last = pn.wacc_n ? &pn : nullptr;  // after the level's forward sweep (not on the path)
+      } else if (pn.wacc_n) {
+        k_gemm<true, true><<<pn.wacc_n, 128, GEMM_SMEM, s2>>>(GW + pn.wacc_off, h->ipool.p, h->ipool.p,
+                                                              h->wtiles.p, rel);
+        IETI_LAUNCHED_SIDE(h);
       }
     }
     IETI_CUDA(cudaEventRecord(h->fev[L], st));
@@ -601,8 +639,8 @@ void run_factor(ietidp_s* h) {
       k_gemm<false><<<sy.second, 128, GEMM_SMEM, st>>>(GW + sy.first, pool, pool, pool, rel);
       IETI_LAUNCHED(h);
     }
-    // side stream: partitioned inverse L11^-1 of this level's supernodes
-    IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[L], 0));
+    // side stream: recursive-doubling L11^-1 of the level (if not formed per panel)
+    IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[L], 0));  // the level's factors
     if (lp.inv_copy_n) {
       k_inv_copy<<<lp.inv_copy_n, 256, 0, s2>>>(W + lp.inv_copy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
       IETI_LAUNCHED_SIDE(h);
@@ -616,15 +654,16 @@ void run_factor(ietidp_s* h) {
                                                       step1 ? h->tpool.p : h->ipool.p, rel);
       IETI_LAUNCHED_SIDE(h);
     }
-    if (L == nlev - 1) IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));  // every L11^-1 done
+    if (lp.inv_copy_n) IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));
     if (h->fwd_in_factor) fwd_sweep_level(h, h->Xf.p, L, s2);
+    if (wacc_last) {
+      k_gemm<true, true><<<wacc_last->wacc_n, 128, GEMM_SMEM, s2>>>(GW + wacc_last->wacc_off, h->ipool.p,
+                                                                    h->ipool.p, h->wtiles.p, rel);
+      IETI_LAUNCHED_SIDE(h);
+      wacc_last = nullptr;
+    }
   }
   IETI_CUDA(cudaEventRecord(h->fev[nlev + 3], s2));  // forward sweep done
-  // explicit loop: W_k = L_II^-T L_II^-1, straight into the loop's lower tiles
-  if (expl && P.w_n) {
-    k_gemm<true, true><<<P.w_n, 128, GEMM_SMEM, s2>>>(GW + P.w_off, h->ipool.p, h->ipool.p, h->wtiles.p, rel);
-    IETI_LAUNCHED_SIDE(h);
-  }
   IETI_CUDA(cudaEventRecord(h->fev[nlev], s2));  // side stream done (joined in run_coarse)
   IETI_CHECK_LAUNCH();
 }

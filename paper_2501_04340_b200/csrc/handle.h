@@ -105,9 +105,12 @@ struct ietidp_s {
   ieti::Plan plan;
   cudaStream_t stream = nullptr;
   bool own_stream = false;
+  cudaStream_t hp = nullptr;     // highest-priority stream of the factorisation's critical path
+  cudaEvent_t hp_ev = nullptr;
   // side stream of the factorisation (partitioned inverse, W_k) and its events
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> fev;  // [0..levels): level's panels done; [levels]: side done
+  std::vector<cudaEvent_t> pev;  // per panel: POTRF done (progressive inverse)
   bool fwd_in_factor = false;    // the forward sweep of the loads ran on the side stream
   long long launches = 0;
   LaunchTrace trace;

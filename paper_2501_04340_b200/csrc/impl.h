@@ -131,6 +131,10 @@ struct LevelPlan {
   // of the rows below with Dinv; then one GemmWork SYRK of the update block.
   struct Panel {
     int potrf_off, potrf_n, trsm_off, trsm_n, upd_off, upd_n;
+    // progressive L11^-1 (side stream, after this panel's POTRF): block row kp of
+    // L11^-1 = [-Dinv (L[kp][0:kp] L11^-1[0:kp][0:kp]), Dinv]  (Work copy + 2 GemmWork),
+    // and (explicit loop, r_I roots) W[0:kp+1][0:kp+1] += L11^-1[kp]^T L11^-1[kp]
+    int icopy_off, icopy_n, ia_off, ia_n, ib_off, ib_n, wacc_off, wacc_n;
   };
   std::vector<Panel> panels;
   std::vector<std::pair<int, int>> syrk;     // SYRK + extend-add launches (GemmWork offset, count), one per child slot
@@ -139,14 +143,14 @@ struct LevelPlan {
   int fu_off = 0, fu_n = 0;                  // forward sweep: update items (sn, update-row tile)
   int bt_off = 0, bt_n = 0;                  // backward sweep: t items (sn, pivot col tile), nupd > 0
   int bx_off = 0, bx_n = 0;                  // backward sweep: x items (sn, pivot col tile)
-  // partitioned inverse L11^-1 of this level's supernodes (runs on the side stream
-  // as soon as the level's panels are factored, overlapping the SYRK and later levels)
+  // partitioned inverse L11^-1 by recursive doubling (levels without r_I roots; side
+  // stream, once the level's panels are factored)
   int inv_copy_off = 0, inv_copy_n = 0;          // Work items (sn, panel) copying Dinv into L11^-1
+  std::vector<std::pair<int, int>> inv_rounds;   // GemmWork ranges, 2 per doubling round
   // front assembly of this level: zero the lower trapezoids (Work items (sn, column
   // tile)), then scatter K's entries (range of the scatter list)
   int zr_off = 0, zr_n = 0;
   long long sc_off = 0, sc_n = 0;
-  std::vector<std::pair<int, int>> inv_rounds;   // GemmWork ranges, 2 per doubling round
 };
 
 struct Plan {
@@ -154,7 +158,6 @@ struct Plan {
   std::vector<SnHost> sn;     // all supernodes, global ids
   std::vector<int> level_sn;  // supernode ids grouped by level
   std::vector<LevelPlan> levels;
-  int w_off = 0, w_n = 0;                       // GemmWork: W = L_II^-T L_II^-1 lower tiles (explicit loop)
   int g_off = 0, g_n = 0;                       // GemmWork: G_k^T = L_PI L_II^-1
   std::vector<std::vector<int>> roots_by_level; // subdomains whose r_I root front is at level L
   long long pool_doubles = 0, dinv_doubles = 0, inv_doubles = 0, vec_rows = 0;
