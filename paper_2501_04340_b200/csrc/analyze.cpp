@@ -1040,6 +1040,19 @@ void analyze_all(ietidp_s* h) {
     }
     pcon_ptr[g + 1] = (int)pcon_sub.size();
   }
+  // the same, flattened to the loop work items' coarse partial rows: g_gi = sum over
+  // gsrc[gsrc_ptr[gi] ..) of gpart[row][.]  (row = item * nPmax + local primal)
+  std::vector<int> gsrc_ptr(ng + 1, 0), gsrc;
+  {
+    const int npm = std::max(P.nPmax, 1);
+    for (int g = 0; g < ng; ++g) {
+      for (auto& x : pc[g]) {
+        const SubDev& d = h->h_sub[x.first];
+        for (int it = d.cta0; it < d.cta0 + sub_ncta[x.first]; ++it) gsrc.push_back(it * npm + x.second);
+      }
+      gsrc_ptr[g + 1] = (int)gsrc.size();
+    }
+  }
   auto t1 = std::chrono::steady_clock::now();
   fill_report(h);
   if (getenv("IETIDP_DEBUG")) {
@@ -1112,6 +1125,8 @@ void analyze_all(ietidp_s* h) {
   h->scoef_ptr.upload(scoef_ptr, s);
   h->scoef_src.upload(scoef_src, s);
   h->pcon_ptr.upload(pcon_ptr, s);
+  h->gsrc_ptr.upload(gsrc_ptr, s);
+  h->gsrc.upload(gsrc, s);
   h->pcon_sub.upload(pcon_sub, s);
   h->pcon_q.upload(pcon_q, s);
   h->d_loopwork.upload(loopwork, s);
@@ -1136,6 +1151,15 @@ void analyze_all(ietidp_s* h) {
       }
     }
     h->slot_goff.upload(goff, s);
+    std::vector<SlotRed> sred(h->n_slots);
+    for (int k = 0; k < ns; ++k) {
+      const SubDev& d = h->h_sub[k];
+      for (int a = 0; a < d.nI; ++a) {
+        const int j = a / TB, r = a % TB;
+        sred[d.rI_off + a] = {(d.spart_off + j) * TB + r, j, d.nt};
+      }
+    }
+    h->slot_red.upload(sred, s);
     std::vector<int2> blk;
     for (int k = 0; k < ns; ++k)
       for (int j = 0; j < h->h_sub[k].nt; ++j) blk.push_back(make_int2(k, j));

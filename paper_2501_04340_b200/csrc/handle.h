@@ -144,6 +144,7 @@ struct ietidp_s {
   ieti::DevBuf<long long> scoef_src;      // S_PP entry <- P-front pool offsets
   ieti::DevBuf<int> scoef_ptr;
   ieti::DevBuf<int> pcon_ptr, pcon_sub, pcon_q;  // global primal <- (subdomain, local primal)
+  ieti::DevBuf<int> gsrc_ptr, gsrc;              // global primal <- coarse partial rows of the loop items
   ieti::DevBuf<int> err_flag;             // [0] min failing subdomain (INT_MAX: none), [1] coarse ok
   // ---- loop ----
   ieti::DevBuf<double> tiles, itiles, lpi;  // packed L_II, L_II^-1 tiles; L_PI
@@ -155,6 +156,7 @@ struct ietidp_s {
   std::vector<std::pair<int, int>> rootlist_range;  // per level: (offset, count) into d_rootlist
   ieti::DevBuf<long long> slot_goff;        // per r_I slot: its row of G_k
   ieti::DevBuf<int> slot_np, slot_poff;     // per r_I slot: n_P of its subdomain, primal-row offset
+  ieti::DevBuf<ieti::SlotRed> slot_red;     // per r_I slot: its symmetric-pass partials
   ieti::DevBuf<ieti::LoopWork> d_loopwork;
   std::vector<ieti::LoopWork> h_loopwork;
   int n_loopwork = 0;

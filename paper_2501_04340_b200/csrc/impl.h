@@ -88,6 +88,13 @@ struct GemmWork {
   long long ws_off;
 };
 
+// Per r_I slot: where the symmetric pass left its partial sums (folded into the gather):
+// y[slot] = vout[slot] + sum_{i = j+1}^{nt-1} spart[(base + i (i-1)/2 TB) ncols + c].
+struct SlotRed {
+  long long base;  // (spart_off + j) TB + r
+  int j, nt;
+};
+
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).
 struct LoopWork {
   int sub, nblk, blk0, blk1;

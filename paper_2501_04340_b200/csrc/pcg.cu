@@ -853,7 +853,17 @@ struct PcgArgs {
   double tol;
   int m, ncols, ng, nPmax, max_iter, fixed, n_items, ncp, n_blk;
   const int *cta_ptr, *cta_items;  // this CTA's work items (tile-balanced, longest first)
+  unsigned long long* prof;        // optional (IETIDP_PCG_PROF): %globaltimer at every barrier
+  const SlotRed* slot_red;         // explicit loop: partial sums folded into the gathers
+  const int *gsrc_ptr, *gsrc;      // coarse partial rows per global primal
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ int g_prof_n;  // barrier counter of the profiled launch (CTA 0)
 
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
@@ -873,11 +883,24 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
 }
 
-// sum over the CTAs' partials of column c (fixed order)
-__device__ __forceinline__ double colsum(const double* part, int c, int ncols) {
-  double s = 0.0;
-  for (int b = 0; b < (int)gridDim.x; ++b) s += part[b * ncols + c];
-  return s;
+// Column sums of the CTAs' partials, computed by the whole CTA (every thread loads a
+// share, then a fixed-shape tree in shared memory: deterministic); out[c], c < ncols,
+// is valid for every thread on return.
+__device__ void colsum_all(const double* part, int ncols, double* out) {
+  __shared__ double red[VT];
+  const int tid = threadIdx.x, P2 = pow2ge(ncols);
+  const int c = tid % P2, g = tid / P2, G = VT / P2;
+  double v = 0.0;
+  if (c < ncols)
+    for (int b = g; b < (int)gridDim.x; b += G) v += __ldcg(part + b * ncols + c);
+  red[tid] = v;
+  __syncthreads();
+  for (int st = VT / 2; st >= P2; st >>= 1) {
+    if (tid < st) red[tid] += red[tid + st];
+    __syncthreads();
+  }
+  if (tid < ncols) out[tid] = red[tid];
+  __syncthreads();
 }
 
 template <int MODE, int NCP, int STAGES>
@@ -931,9 +954,44 @@ __device__ __forceinline__ void coarse_phase(const PcgArgs& P, double* smem) {
   }
 }
 
+// z = S_PP^-1 g, computed by every CTA into shared memory (ng x nc; redundant, no barrier)
+__device__ __forceinline__ void coarse_local(const PcgArgs& P, double* zs) {
+  const int nc = P.ncols, tid = threadIdx.x;
+  double* g = zs + P.ng * nc;
+  __syncthreads();
+  // g[gi][c]: a warp per (gi, c), lanes over the flattened partial rows (fixed order)
+  const int warp = tid >> 5, lane = tid & 31;
+  for (int e = warp; e < P.ng * nc; e += VT / 32) {
+    const int gi = e / nc, c = e - gi * nc;
+    double sacc = 0.0;
+    for (int q = P.gsrc_ptr[gi] + lane; q < P.gsrc_ptr[gi + 1]; q += 32)
+      sacc += __ldcg(P.gpart + (long long)P.gsrc[q] * nc + c);
+    sacc = warp_sum(sacc);
+    if (lane == 0) g[e] = sacc;
+  }
+  __syncthreads();
+  for (int e = tid; e < P.ng * nc; e += VT) {
+    const int i = e / nc, c = e - i * nc;
+    double sacc = 0.0;
+    for (int j = 0; j < P.ng; ++j) sacc += P.Sinv[(long long)i * P.ng + j] * g[j * nc + c];
+    zs[e] = sacc;
+  }
+  __syncthreads();
+}
+
+// y[slot][c] of a symmetric pass: the N part plus the transposed partials (fixed order)
+__device__ __forceinline__ double sym_value(const double* y, const double* spart, const SlotRed* sred, long long a,
+                                            int nc, int c) {
+  const SlotRed sr = sred[a];
+  double v = 0.0;
+  for (int i = sr.j + 1; i < sr.nt; ++i) v += spart[(sr.base + (long long)(i * (i - 1) / 2) * TB) * nc + c];
+  return y[a * nc + c] + v;
+}
+
 // out = sum_k B (w) (x + G z), with the per-CTA partial of out . dotv
 __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x, const double* w, double* out,
-                                              const double* dotv, double* part, bool coarse) {
+                                              const double* dotv, double* part, bool coarse,
+                                              const double* spart = nullptr, const double* zs = nullptr) {
   const int nc = P.ncols, P2 = pow2ge(nc);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
   double dot = 0.0;
@@ -944,8 +1002,19 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int a = L.slot[q];
-        double xv = x[(long long)a * nc + c];
-        if (coarse) xv += coarse_term(P.ct, a, nc, c);
+        double xv = spart ? sym_value(x, spart, P.slot_red, a, nc, c) : x[(long long)a * nc + c];
+        if (coarse) {
+          if (zs) {  // G_k[slot row] . z (z in shared memory)
+            const int np = P.ct.np[a];
+            const double* Gr = P.ct.G + P.ct.goff[a];
+            const int* gid = P.ct.prim_gid + P.ct.poff[a];
+            double sc = 0.0;
+            for (int q2 = 0; q2 < np; ++q2) sc += Gr[q2] * zs[gid[q2] * nc + c];
+            xv += sc;
+          } else {
+            xv += coarse_term(P.ct, a, nc, c);
+          }
+        }
         val += (double)L.sign[q] * (w ? w[a] : 1.0) * xv;
       }
       out[(long long)j * nc + c] = val;
@@ -964,24 +1033,33 @@ __device__ __forceinline__ void to_slots(const PcgArgs& P, long long j, int c, d
   }
 }
 
+// grid barrier of the PCG kernel; with P.prof, CTA 0 records the time of arrival
+__device__ __forceinline__ void pcg_barrier(const PcgArgs& P) {
+  if (P.prof && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int i = g_prof_n++;
+    if (i < 4096) P.prof[i] = gtimer();
+  }
+  grid_barrier(P.bar);
+}
+
 template <int NCP, int STAGES, bool EXPL>
 __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, double* pq) {
   if (EXPL) {
+    // W pass; then every CTA solves the coarse problem itself and folds the pass's
+    // partial sums into the gather (no reduction phase, one barrier)
     sym_phase<NCP, STAGES>(P.wsym, P.cta_ptr, P.cta_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    reduce_phase(P.wsym, P.blk, P.n_blk);
-    if (P.ng > 0) coarse_phase(P, smem);
-    grid_barrier(P.bar);
-    bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0);
+    pcg_barrier(P);
+    if (P.ng > 0) coarse_local(P, smem);
+    bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0, P.wsym.spart, smem);
   } else {
     tmv_phase<FWD, NCP, STAGES>(P.fwd, P.cta_ptr, P.cta_items, P.ncp, smem);
-    grid_barrier(P.bar);
+    pcg_barrier(P);
     if (P.ng > 0) {
       coarse_phase(P, smem);
-      grid_barrier(P.bar);
+      pcg_barrier(P);
     }
     tmv_phase<BWD, NCP, STAGES>(P.bwd, P.cta_ptr, P.cta_items, P.ncp, smem);
-    grid_barrier(P.bar);
+    pcg_barrier(P);
     bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, false);
   }
 }
@@ -990,22 +1068,21 @@ template <int NCP, int STAGES, bool EXPL>
 __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, double* rz) {
   if (EXPL) {
     sym_phase<NCP, STAGES>(P.ssym, P.cta_ptr, P.cta_items, P.ncp, smem);
-    grid_barrier(P.bar);
-    reduce_phase(P.ssym, P.blk, P.n_blk);
-    grid_barrier(P.bar);
+    pcg_barrier(P);
+    bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, P.ssym.spart);
   } else {
     tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.cta_ptr, P.cta_items, P.ncp, smem);
-    grid_barrier(P.bar);
+    pcg_barrier(P);
     tmv_phase<PRE2, NCP, STAGES>(P.pre2, P.cta_ptr, P.cta_items, P.ncp, smem);
-    grid_barrier(P.bar);
+    pcg_barrier(P);
+    bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false);
   }
-  bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false);
 }
 
 template <int NCP, int STAGES, bool EXPL>
 __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
   extern __shared__ __align__(16) double smem[];
-  __shared__ double s_rz[IETIDP_MAX_RHS], s_r0[IETIDP_MAX_RHS], s_coef[IETIDP_MAX_RHS];
+  __shared__ double s_rz[IETIDP_MAX_RHS], s_r0[IETIDP_MAX_RHS], s_coef[IETIDP_MAX_RHS], s_sum[IETIDP_MAX_RHS];
   __shared__ int s_act[IETIDP_MAX_RHS], s_new[IETIDP_MAX_RHS], s_iters[IETIDP_MAX_RHS];
   __shared__ int s_any;
   const int tid = threadIdx.x, nb = gridDim.x, nc = P.ncols, m = P.m;
@@ -1030,9 +1107,10 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
     });
     block_col_reduce(acc, nc, P2, rr);
   }
-  grid_barrier(P.bar);
+  pcg_barrier(P);
+  colsum_all(rr, nc, s_sum);
   if (tid < nc) {
-    s_r0[tid] = sqrt(colsum(rr, tid, nc));
+    s_r0[tid] = sqrt(s_sum[tid]);
     s_act[tid] = (m > 0 && s_r0[tid] > 0.0) ? 1 : 0;
     s_iters[tid] = 0;
     s_rz[tid] = 0.0;
@@ -1045,20 +1123,22 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
   if (run) {
     // z = M r, rz = r.z, p = z
     apply_M_phases<NCP, STAGES, EXPL>(P, smem, rz);
-    grid_barrier(P.bar);
-    if (tid < nc) s_rz[tid] = colsum(rz, tid, nc);
+    pcg_barrier(P);
+    colsum_all(rz, nc, s_sum);
+    if (tid < nc) s_rz[tid] = s_sum[tid];
     rows([&](long long e, int j) {
       const double zv = P.z[e];
       P.p[e] = zv;
       to_slots(P, j, cc, zv, nullptr, P.pslot);
     });
-    grid_barrier(P.bar);
+    pcg_barrier(P);
   }
   while (run) {
     apply_F_phases<NCP, STAGES, EXPL>(P, smem, pq);  // q = F p
-    grid_barrier(P.bar);
+    pcg_barrier(P);
     // alpha, lambda and r
-    if (tid < nc) s_coef[tid] = s_act[tid] ? s_rz[tid] / colsum(pq, tid, nc) : 0.0;
+    colsum_all(pq, nc, s_sum);
+    if (tid < nc) s_coef[tid] = s_act[tid] ? s_rz[tid] / s_sum[tid] : 0.0;
     __syncthreads();
     {
       double acc = 0.0;
@@ -1076,14 +1156,14 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
       });
       block_col_reduce(acc, nc, P2, rr);
     }
-    grid_barrier(P.bar);
+    pcg_barrier(P);
     // stop test (identical in every CTA)
     if (tid == 0) s_any = 0;
-    __syncthreads();
+    colsum_all(rr, nc, s_sum);
     if (tid < nc) {
       int a = s_act[tid];
       if (s_act[tid]) s_iters[tid]++;
-      if (a && !P.fixed && sqrt(colsum(rr, tid, nc)) <= P.tol * s_r0[tid]) a = 0;
+      if (a && !P.fixed && sqrt(s_sum[tid]) <= P.tol * s_r0[tid]) a = 0;
       s_new[tid] = a;
       if (a) atomicOr(&s_any, 1);
     }
@@ -1094,10 +1174,11 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
       break;
     }
     apply_M_phases<NCP, STAGES, EXPL>(P, smem, rz);  // z = M r
-    grid_barrier(P.bar);
+    pcg_barrier(P);
     // beta, p
+    colsum_all(rz, nc, s_sum);
     if (tid < nc) {
-      const double rzn = colsum(rz, tid, nc);
+      const double rzn = s_sum[tid];
       s_coef[tid] = rzn / s_rz[tid];
       if (s_new[tid]) s_rz[tid] = rzn;
     }
@@ -1115,7 +1196,7 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
       });
     }
     if (tid < nc) s_act[tid] = s_new[tid];
-    grid_barrier(P.bar);
+    pcg_barrier(P);
   }
   if (blockIdx.x == 0 && tid == 0) {
     P.st->it = it;
@@ -1460,9 +1541,34 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
   PcgArgs args = a;
   args.cta_ptr = h->cta_ptr.p;
   args.cta_items = h->cta_items.p;
+  const char* prof_env = getenv("IETIDP_PCG_PROF");
+  static DevBuf<unsigned long long> prof;
+  if (prof_env) {
+    if (!prof.p) prof.alloc(4096);
+    const int zero = 0;
+    IETI_CUDA(cudaMemcpyToSymbolAsync(g_prof_n, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, h->stream));
+    args.prof = prof.p;
+  }
   void* params[] = {&args};
   IETI_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, 256, params, cfg.smem, h->stream));
   IETI_LAUNCHED(h);
+  if (prof_env) {
+    // per-barrier intervals of CTA 0, averaged by position in the iteration (diagnostics)
+    std::vector<unsigned long long> t(4096);
+    int n = 0;
+    IETI_CUDA(cudaStreamSynchronize(h->stream));
+    IETI_CUDA(cudaMemcpyFromSymbol(&n, g_prof_n, sizeof(int)));
+    IETI_CUDA(cudaMemcpy(t.data(), prof.p, sizeof(unsigned long long) * std::min(n, 4096), cudaMemcpyDeviceToHost));
+    n = std::min(n, 4096);
+    const int per = EXPL ? 6 : 9, skip = EXPL ? 4 : 5;
+    std::vector<double> acc(per, 0.0);
+    int cnt = 0;
+    for (int i = skip; i + per < n; i += per, ++cnt)
+      for (int q = 0; q < per; ++q) acc[q] += (double)(t[i + q + 1] - t[i + q]) * 1e-3;
+    fprintf(stderr, "pcg profile: %d barriers, grid %d; us per phase (avg over %d iterations):", n, grid, cnt);
+    for (int q = 0; q < per; ++q) fprintf(stderr, " %.2f", cnt ? acc[q] / cnt : 0.0);
+    fprintf(stderr, "\n");
+  }
   return true;
 }
 
@@ -1470,7 +1576,13 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
 static bool run_solve_persistent(ietidp_s* h) {
   const int nc = h->nrhs, m = h->n_lambda;
   if (m == 0 || h->n_loopwork == 0) return false;
-  const TmvCfg cfg = tmv_cfg(h, nc);
+  TmvCfg cfg = tmv_cfg(h, nc);
+  // the explicit loop's per-CTA coarse solve keeps g and z (2 ng nc doubles) in shared memory
+  const int zbytes = 2 * h->n_primal * nc * (int)sizeof(double);
+  if (h->opt.loop == IETIDP_LOOP_EXPLICIT && zbytes > cfg.smem) {
+    if (zbytes > 200 * 1024) return false;
+    cfg.smem = zbytes;
+  }
   if (h->gbar.n == 0) h->gbar.alloc(2);
   h->gbar.zero(h->stream);
   PcgArgs a{};
@@ -1507,6 +1619,9 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.ssym.slot_in = 1;
   a.ssym.vout = h->zI.p;
   a.ct = coarse_term_args(h);
+  a.slot_red = h->slot_red.p;
+  a.gsrc_ptr = h->gsrc_ptr.p;
+  a.gsrc = h->gsrc.p;
   a.blk = h->d_blk.p;
   a.n_blk = h->n_blk;
   a.lam = h->lam.p;
