@@ -460,6 +460,10 @@ void analyze_all(ietidp_s* h) {
       pool += (long long)d.ld * d.f;
       d.vec_off = vec;
       vec += s.f;
+      d.bp_off = P.bpart_doubles;  // step-1 chunks, then step-2 chunks of the backward sweep
+      if (!s.coarse)
+        P.bpart_doubles += (long long)((s.f - s.npiv + BS_RB - 1) / BS_RB + (s.npiv + BS_RB - 1) / BS_RB) *
+                           s.npiv * 16;
       d.ldi = (s.npiv + 3) & ~3;
       if (!s.coarse) {
         d.dinv_off = dinv;
@@ -709,12 +713,22 @@ void analyze_all(ietidp_s* h) {
         for (int t = 0; t < tiles_of(P.sn[i].f - P.sn[i].npiv); ++t, ++lp.fu_n) push(i, t, 0);
     lp.bt_off = (int)work.size() / 3;
     for (int i : bylev[L])
-      if (!P.sn[i].coarse && P.sn[i].f > P.sn[i].npiv)
-        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bt_n) push(i, t, 0);
-    lp.bx_off = (int)work.size() / 3;
+      if (!P.sn[i].coarse && P.sn[i].f > P.sn[i].npiv) {
+        const int nch = (P.sn[i].f - P.sn[i].npiv + BS_RB - 1) / BS_RB;
+        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t)
+          for (int rc = 0; rc < nch; ++rc, ++lp.bt_n) push(i, t, rc);
+      }
+    lp.bx_off = (int)work.size() / 3;  // (sn, pivot col tile, row chunk >= the tile's)
+    for (int i : bylev[L])
+      if (!P.sn[i].coarse) {
+        const int nch = (P.sn[i].npiv + BS_RB - 1) / BS_RB;
+        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t)
+          for (int rc = t * TB / BS_RB; rc < nch; ++rc, ++lp.bx_n) push(i, t, rc);
+      }
+    lp.bxr_off = (int)work.size() / 3;
     for (int i : bylev[L])
       if (!P.sn[i].coarse)
-        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bx_n) push(i, t, 0);
+        for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bxr_n) push(i, t, 0);
   }
   // ---- partitioned inverse L11^-1 by recursive doubling over TB-blocks, per level ----
   for (int L = 0; L <= P.max_level; ++L) {
@@ -1183,6 +1197,7 @@ void analyze_all(ietidp_s* h) {
   h->ipool.alloc(P.inv_doubles);
   h->tpool.alloc(P.inv_doubles);
   h->skws.alloc(std::max<long long>(1, P.splitk_doubles));
+  h->bpart.alloc(std::max<long long>(1, P.bpart_doubles));
   h->skcnt.alloc(std::max(1, P.splitk_tiles));
   IETI_CUDA(cudaMemset(h->skcnt.p, 0, h->skcnt.n * sizeof(int)));
   h->vecw.alloc((size_t)P.vec_rows * 16);  // sweeps use up to 16 interleaved columns

@@ -138,6 +138,7 @@ struct ietidp_s {
   // ---- numeric ----
   ieti::DevBuf<double> pool, dinv, ipool, tpool, vecw;  // fronts, Dinv blocks, L11^-1, temp, sweep workspace
   ieti::DevBuf<double> skws;                             // split-K partial products
+  ieti::DevBuf<double> bpart;                            // backward-sweep partial products
   ieti::DevBuf<int> skcnt;                               // split-K arrival counters (zero between uses)
   ieti::DevBuf<double> Xf, Xr;            // forward-swept loads (kept) / recovery sweep (ne rows x nrhs)
   ieti::DevBuf<double> S, Sinv, ftil, zc0;  // coarse: S_PP, S_PP^-1, ftilde, S^-1 ftilde

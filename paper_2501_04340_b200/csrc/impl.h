@@ -38,7 +38,9 @@ struct SnDev {
   int rows_off;         // rows[rows_off .. +f-npiv): positions of the update rows
   int rel_off;          // rel[rel_off .. +f-npiv): row index of each update row in the parent front
   int child_off, nchild;
+  long long bp_off;     // backward sweep: partials of L21^T x per BS_RB-row chunk (chunks x npiv x 16)
 };
+constexpr int BS_RB = 256;  // rows of L21 per backward-sweep partial item
 
 // Per-subdomain descriptor.
 struct SubDev {
@@ -148,8 +150,9 @@ struct LevelPlan {
   int sn_off = 0, sn_n = 0;                  // supernodes of this level (level_sn list)
   int fs_off = 0, fs_n = 0;                  // forward sweep: solve items (sn, row tile)
   int fu_off = 0, fu_n = 0;                  // forward sweep: update items (sn, update-row tile)
-  int bt_off = 0, bt_n = 0;                  // backward sweep: t items (sn, pivot col tile), nupd > 0
-  int bx_off = 0, bx_n = 0;                  // backward sweep: x items (sn, pivot col tile)
+  int bt_off = 0, bt_n = 0;                  // backward sweep: partial items (sn, pivot col tile, row chunk)
+  int bx_off = 0, bx_n = 0;                  // backward sweep: x partial items (sn, pivot col tile, row chunk)
+  int bxr_off = 0, bxr_n = 0;                // backward sweep: x = sum of the partials (sn, pivot col tile)
   // partitioned inverse L11^-1 by recursive doubling (levels without r_I roots; side
   // stream, once the level's panels are factored)
   int inv_copy_off = 0, inv_copy_n = 0;          // Work items (sn, panel) copying Dinv into L11^-1
@@ -169,6 +172,7 @@ struct Plan {
   std::vector<std::vector<int>> roots_by_level; // subdomains whose r_I root front is at level L
   long long pool_doubles = 0, dinv_doubles = 0, inv_doubles = 0, vec_rows = 0;
   long long splitk_doubles = 0;  // split-K partials workspace (max over launches)
+  long long bpart_doubles = 0;   // backward-sweep partials
   int splitk_tiles = 0;          // split-K counters (max tiles per launch)
   int max_level = 0, max_front = 0, max_nI = 0, nPmax = 0;
   long long nnz_L = 0, flops = 0, inv_flops = 0;

@@ -116,80 +116,164 @@ __global__ void __launch_bounds__(SWT)
   }
 }
 
-// B1 (MODE 0): t[cols] = y[cols] - L21[:, cols]^T x_rows      -> Wv (pivot rows)
-// B2 (MODE 1): x[cols] = L11^-T[cols, :] t = sum_{r>=c} Linv[r][c] t[r] -> X
-// One warp per pivot column (lanes over the contiguous column), 8 columns per warp.
-template <int MODE, int NCB>
+// Backward sweep, first step, split over BS_RB-row chunks of L21 (many CTAs, short
+// dependent chains): partial[rc][col] = L21[chunk rc, col]^T x_rows[chunk rc] for the 64
+// pivot columns of tile w.a. The chunk's x rows are gathered once into shared memory;
+// warp w takes columns w, w+8, ..., two at a time, lanes over the contiguous rows.
+template <int NCB>
 __global__ void __launch_bounds__(SWT)
-    k_bs_gemv(const Work* __restrict__ work, const SnDev* __restrict__ sn, const SubDev* __restrict__ sub,
-              const int* __restrict__ rows, const double* __restrict__ pool, const double* __restrict__ ipool,
-              double* __restrict__ X, double* __restrict__ Wv, int ldx, int cofs) {
+    k_bs_partial(const Work* __restrict__ work, const SnDev* __restrict__ sn, const SubDev* __restrict__ sub,
+                 const int* __restrict__ rows, const double* __restrict__ pool, const double* __restrict__ X,
+                 double* __restrict__ bpart, int ldx, int cofs) {
+  constexpr int XS = NCB | 1;  // odd row stride: conflict-free column reads
+  __shared__ double xs[BS_RB][XS];
   const Work w = work[blockIdx.x];
   const SnDev s = sn[w.sn];
   const SubDev d = sub[s.sub];
   const int ncl = min(NCB, ldx - cofs);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nu = s.f - s.npiv;
+  const int q0 = w.b * BS_RB, nq = min(BS_RB, nu - q0);
+  const int* rw = rows + s.rows_off + q0;
+  const double* Xs = X + d.x_off * ldx + cofs;
+  for (int e = threadIdx.x; e < BS_RB * NCB; e += SWT) {
+    const int q = e / NCB, c = e - q * NCB;
+    xs[q][c] = (q < nq && c < ncl) ? Xs[(long long)rw[q] * ldx + c] : 0.0;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int cc = warp; cc < TB; cc += 2 * (SWT / 32)) {
+    double acc[2][NCB];
+    bool okc[2];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      okc[h2] = w.a * TB + cc + h2 * (SWT / 32) < s.npiv;
+#pragma unroll
+      for (int c = 0; c < NCB; ++c) acc[h2][c] = 0.0;
+    }
+    if (!okc[0]) break;
+    double l[2][BS_RB / 32];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int col = w.a * TB + cc + h2 * (SWT / 32);
+      const double* Lc = pool + s.front_off + (long long)col * s.ld + s.npiv + q0;
+#pragma unroll
+      for (int u = 0; u < BS_RB / 32; ++u) {
+        const int q = lane + 32 * u;
+        l[h2][u] = (okc[h2] && q < nq) ? Lc[q] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+      for (int u = 0; u < BS_RB / 32; ++u)
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) acc[h2][c] += l[h2][u] * xs[lane + 32 * u][c];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+      for (int c = 0; c < NCB; ++c) acc[h2][c] = warp_sum(acc[h2][c]);
+      const int col = w.a * TB + cc + h2 * (SWT / 32);
+      if (lane == 0 && okc[h2]) {
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) bpart[s.bp_off + ((long long)w.b * s.npiv + col) * NCB + c] = acc[h2][c];
+      }
+    }
+  }
+}
+
+// Backward sweep, second step, split over BS_RB-row chunks of L11^-1:
+// partial[rc][col] = sum_{r in chunk rc, r >= col} Linv[r][col] t[r], t from Wv (or,
+// for a supernode without update rows, the X pivot rows themselves).
+template <int NCB>
+__global__ void __launch_bounds__(SWT)
+    k_bx_partial(const Work* __restrict__ work, const SnDev* __restrict__ sn, const SubDev* __restrict__ sub,
+                 const double* __restrict__ ipool, const double* __restrict__ X, const double* __restrict__ Wv,
+                 double* __restrict__ bpart, int ldx, int cofs) {
+  constexpr int XS = NCB | 1;
+  __shared__ double ts[BS_RB][XS];
+  const Work w = work[blockIdx.x];
+  const SnDev s = sn[w.sn];
+  const SubDev d = sub[s.sub];
+  const int ncl = min(NCB, ldx - cofs);
+  const int r0 = w.b * BS_RB, nr = min(BS_RB, s.npiv - r0);
+  const bool from_t = s.f > s.npiv;
+  const double* Xs = X + d.x_off * ldx + cofs;
+  (void)Wv;
+  // t = y - L21^T x_rows: the pivot rows of X minus the step-1 partials (fixed order)
+  const int nchu = (s.f - s.npiv + BS_RB - 1) / BS_RB;
+  for (int e = threadIdx.x; e < BS_RB * NCB; e += SWT) {
+    const int q = e / NCB, c = e - q * NCB;
+    double v = 0.0;
+    if (q < nr && c < ncl) {
+      double p = 0.0;
+      if (from_t)
+        for (int rc = 0; rc < nchu; ++rc) p += bpart[s.bp_off + ((long long)rc * s.npiv + r0 + q) * NCB + c];
+      v = Xs[(long long)(s.c0 + r0 + q) * ldx + c] - p;
+    }
+    ts[q][c] = v;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int cc = warp; cc < TB; cc += 2 * (SWT / 32)) {
+    double acc[2][NCB];
+    bool okc[2];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      okc[h2] = w.a * TB + cc + h2 * (SWT / 32) < s.npiv;
+#pragma unroll
+      for (int c = 0; c < NCB; ++c) acc[h2][c] = 0.0;
+    }
+    if (!okc[0]) break;
+    double l[2][BS_RB / 32];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const int col = w.a * TB + cc + h2 * (SWT / 32);
+      const double* Ic = ipool + s.inv_off + (long long)col * s.ldi + r0;
+#pragma unroll
+      for (int u = 0; u < BS_RB / 32; ++u) {
+        const int q = lane + 32 * u;
+        l[h2][u] = (okc[h2] && q < nr && r0 + q >= col) ? Ic[q] : 0.0;
+      }
+    }
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+      for (int u = 0; u < BS_RB / 32; ++u)
+#pragma unroll
+        for (int c = 0; c < NCB; ++c) acc[h2][c] += l[h2][u] * ts[lane + 32 * u][c];
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+#pragma unroll
+      for (int c = 0; c < NCB; ++c) acc[h2][c] = warp_sum(acc[h2][c]);
+      const int col = w.a * TB + cc + h2 * (SWT / 32);
+      if (lane == 0 && okc[h2]) {
+#pragma unroll
+        for (int c = 0; c < NCB; ++c)
+          bpart[s.bp_off + ((long long)(nchu + w.b) * s.npiv + col) * NCB + c] = acc[h2][c];
+      }
+    }
+  }
+}
+
+// x[col] = sum over the row chunks rc >= col's tile of the partials (fixed order) -> X
+template <int NCB>
+__global__ void __launch_bounds__(SWT)
+    k_bx_red(const Work* __restrict__ work, const SnDev* __restrict__ sn, const SubDev* __restrict__ sub,
+             const double* __restrict__ bpart, double* __restrict__ X, int ldx, int cofs) {
+  const Work w = work[blockIdx.x];
+  const SnDev s = sn[w.sn];
+  const SubDev d = sub[s.sub];
+  const int ncl = min(NCB, ldx - cofs);
+  const int nch = (s.npiv + BS_RB - 1) / BS_RB, nchu = (s.f - s.npiv + BS_RB - 1) / BS_RB;
   double* Xs = X + d.x_off * ldx + cofs;
-  double* t = Wv + s.vec_off * NCB;
-  for (int cc = warp; cc < TB; cc += SWT / 32) {
+  for (int e = threadIdx.x; e < TB * NCB; e += SWT) {
+    const int cc = e / NCB, c = e - cc * NCB;
     const int col = w.a * TB + cc;
-    if (col >= s.npiv) break;
-    double acc[NCB];
-#pragma unroll
-    for (int c = 0; c < NCB; ++c) acc[c] = 0.0;
-    if (MODE == 0) {
-      const double* Lc = pool + s.front_off + (long long)col * s.ld + s.npiv;
-      const int* rw = rows + s.rows_off;
-      for (int q0 = 0; q0 < nu; q0 += 128) {  // 4 independent rows per lane
-        double l[4];
-        const double* xr[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int q = q0 + lane + 32 * u;
-          l[u] = q < nu ? Lc[q] : 0.0;
-          xr[u] = q < nu ? Xs + (long long)rw[q] * ldx : Xs;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-#pragma unroll
-          for (int c = 0; c < NCB; ++c)
-            if (c < ncl) acc[c] += l[u] * xr[u][c];
-      }
-    } else {
-      const double* Ic = ipool + s.inv_off + (long long)col * s.ldi;
-      const bool from_t = nu > 0;
-      for (int q0 = col; q0 < s.npiv; q0 += 128) {
-        double l[4];
-        int qq[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          qq[u] = q0 + lane + 32 * u;
-          l[u] = qq[u] < s.npiv ? Ic[qq[u]] : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          if (qq[u] >= s.npiv) continue;
-#pragma unroll
-          for (int c = 0; c < NCB; ++c) {
-            const double tv = from_t ? t[qq[u] * NCB + c] : (c < ncl ? Xs[(long long)(s.c0 + qq[u]) * ldx + c] : 0.0);
-            acc[c] += l[u] * tv;
-          }
-        }
-      }
-    }
-#pragma unroll
-    for (int c = 0; c < NCB; ++c) acc[c] = warp_sum(acc[c]);
-    if (lane == 0) {
-#pragma unroll
-      for (int c = 0; c < NCB; ++c) {
-        if (MODE == 0) {
-          t[col * NCB + c] = (c < ncl ? Xs[(long long)(s.c0 + col) * ldx + c] : 0.0) - acc[c];
-        } else if (c < ncl) {
-          Xs[(long long)(s.c0 + col) * ldx + c] = acc[c];
-        }
-      }
-    }
+    if (col >= s.npiv || c >= ncl) continue;
+    double v = 0.0;
+    for (int rc = w.a * TB / BS_RB; rc < nch; ++rc)
+      v += bpart[s.bp_off + ((long long)(nchu + rc) * s.npiv + col) * NCB + c];
+    Xs[(long long)(s.c0 + col) * ldx + c] = v;
   }
 }
 
@@ -221,13 +305,15 @@ static void sweeps_t(ietidp_s* h, double* X, bool fwd, bool bwd, int cofs) {
     for (int L = P.max_level; L >= 0; --L) {
       const LevelPlan& lp = P.levels[L];
       if (lp.bt_n) {
-        k_bs_gemv<0, NCB><<<lp.bt_n, SWT, 0, st>>>(W + lp.bt_off, h->d_sn.p, h->d_sub.p, h->d_rows.p, h->pool.p,
-                                                   h->ipool.p, X, h->vecw.p, ldx, cofs);
+        k_bs_partial<NCB><<<lp.bt_n, SWT, 0, st>>>(W + lp.bt_off, h->d_sn.p, h->d_sub.p, h->d_rows.p, h->pool.p, X,
+                                                   h->bpart.p, ldx, cofs);
         IETI_LAUNCHED(h);
       }
       if (lp.bx_n) {
-        k_bs_gemv<1, NCB><<<lp.bx_n, SWT, 0, st>>>(W + lp.bx_off, h->d_sn.p, h->d_sub.p, h->d_rows.p, h->pool.p,
-                                                   h->ipool.p, X, h->vecw.p, ldx, cofs);
+        k_bx_partial<NCB><<<lp.bx_n, SWT, 0, st>>>(W + lp.bx_off, h->d_sn.p, h->d_sub.p, h->ipool.p, X, h->vecw.p,
+                                                   h->bpart.p, ldx, cofs);
+        IETI_LAUNCHED(h);
+        k_bx_red<NCB><<<lp.bxr_n, SWT, 0, st>>>(W + lp.bxr_off, h->d_sn.p, h->d_sub.p, h->bpart.p, X, ldx, cofs);
         IETI_LAUNCHED(h);
       }
     }
