@@ -1232,6 +1232,7 @@ void analyze_all(ietidp_s* h) {
   h->zI.alloc((size_t)h->n_slots * nc);
   h->gpart.alloc((size_t)std::max(cta, 1) * std::max(P.nPmax, 1) * nc);
   h->zc.alloc((size_t)std::max(ng, 1) * nc);
+  h->gc.alloc((size_t)std::max(ng, 1) * nc);
   h->partial.alloc(4 * 1024 * (size_t)nc);
   h->state.alloc(16 * IETIDP_MAX_RHS + 64);
   h->tmp_in.alloc(m);

@@ -171,7 +171,7 @@ struct ietidp_s {
   ieti::DevBuf<double> d_vec, lam_vec, r_vec, p_vec, q_vec, z_vec;
   ieti::DevBuf<double> yI, xI, sI, zI;    // per-slot vectors (sum n_I x ncols)
   ieti::DevBuf<double> pslot, rslot;      // persistent PCG: B^T p and B_D^T r in slot order
-  ieti::DevBuf<double> gpart, zc;         // coarse partials per loop CTA; coarse solution
+  ieti::DevBuf<double> gpart, zc, gc;     // coarse partials per loop CTA; coarse solution; coarse rhs
   ieti::DevBuf<double> partial;           // per-block dot partials
   ieti::DevBuf<double> state;             // PCG scalars (see pcg.cu)
   ieti::DevBuf<double> tmp_in, tmp_out;   // col-major <-> interleaved staging

@@ -856,6 +856,7 @@ struct PcgArgs {
   unsigned long long* prof;        // optional (IETIDP_PCG_PROF): %globaltimer at every barrier
   const SlotRed* slot_red;         // explicit loop: partial sums folded into the gathers
   const int *gsrc_ptr, *gsrc;      // coarse partial rows per global primal
+  double* gc;                      // coarse right-hand side g (larger coarse problems)
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -932,19 +933,17 @@ __device__ __forceinline__ void reduce_phase(const TmvArgs& A, const int2* blk, 
 __device__ __forceinline__ void coarse_phase(const PcgArgs& P, double* smem) {
   const int nc = P.ncols, tid = threadIdx.x, nb = gridDim.x;
   double* g = smem;  // ng x nc
+  const int warp = tid >> 5, lane = tid & 31;
   __syncthreads();
-  for (int e = tid; e < P.ng * nc; e += VT) {
+  for (int e = warp; e < P.ng * nc; e += VT / 32) {
     const int gi = e / nc, c = e - gi * nc;
     double sacc = 0.0;
-    for (int q = P.pcon_ptr[gi]; q < P.pcon_ptr[gi + 1]; ++q) {
-      const int k = P.pcon_sub[q], lq = P.pcon_q[q];
-      for (int cta = P.sub_cta0[k]; cta < P.sub_cta0[k] + P.sub_ncta[k]; ++cta)
-        sacc += P.gpart[((long long)cta * P.nPmax + lq) * nc + c];
-    }
-    g[e] = sacc;
+    for (int q = P.gsrc_ptr[gi] + lane; q < P.gsrc_ptr[gi + 1]; q += 32)
+      sacc += __ldcg(P.gpart + (long long)P.gsrc[q] * nc + c);
+    sacc = warp_sum(sacc);
+    if (lane == 0) g[e] = sacc;
   }
   __syncthreads();
-  const int warp = tid >> 5, lane = tid & 31;
   for (int e = blockIdx.x * 8 + warp; e < P.ng * nc; e += nb * 8) {
     const int i = e / nc, c = e - i * nc;
     double sacc = 0.0;
@@ -955,6 +954,8 @@ __device__ __forceinline__ void coarse_phase(const PcgArgs& P, double* smem) {
 }
 
 // z = S_PP^-1 g, computed by every CTA into shared memory (ng x nc; redundant, no barrier)
+// -- for coarse problems up to COARSE_LOCAL_MAX primal DOFs (S_PP^-1 read by every CTA)
+constexpr int COARSE_LOCAL_MAX = 64;
 __device__ __forceinline__ void coarse_local(const PcgArgs& P, double* zs) {
   const int nc = P.ncols, tid = threadIdx.x;
   double* g = zs + P.ng * nc;
@@ -977,6 +978,30 @@ __device__ __forceinline__ void coarse_local(const PcgArgs& P, double* zs) {
     zs[e] = sacc;
   }
   __syncthreads();
+}
+
+// Larger coarse problems: g (warp per entry) and then z = S_PP^-1 g (warp per row),
+// both spread over the CTAs, through global memory.
+__device__ __forceinline__ void coarse_spread(const PcgArgs& P) {
+  const int nc = P.ncols, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = blockIdx.x * (VT / 32) + warp; e < P.ng * nc; e += gridDim.x * (VT / 32)) {
+    const int gi = e / nc, c = e - gi * nc;
+    double sacc = 0.0;
+    for (int q = P.gsrc_ptr[gi] + lane; q < P.gsrc_ptr[gi + 1]; q += 32)
+      sacc += __ldcg(P.gpart + (long long)P.gsrc[q] * nc + c);
+    sacc = warp_sum(sacc);
+    if (lane == 0) P.gc[e] = sacc;
+  }
+}
+__device__ __forceinline__ void coarse_spread_z(const PcgArgs& P) {
+  const int nc = P.ncols, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int e = blockIdx.x * (VT / 32) + warp; e < P.ng * nc; e += gridDim.x * (VT / 32)) {
+    const int i = e / nc, c = e - i * nc;
+    double sacc = 0.0;
+    for (int j = lane; j < P.ng; j += 32) sacc += P.Sinv[(long long)i * P.ng + j] * __ldcg(P.gc + j * nc + c);
+    sacc = warp_sum(sacc);
+    if (lane == 0) P.zc[e] = sacc;
+  }
 }
 
 // y[slot][c] of a symmetric pass: the N part plus the transposed partials (fixed order)
@@ -1049,8 +1074,23 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     // partial sums into the gather (no reduction phase, one barrier)
     sym_phase<NCP, STAGES>(P.wsym, P.cta_ptr, P.cta_items, P.ncp, smem);
     pcg_barrier(P);
-    if (P.ng > 0) coarse_local(P, smem);
-    bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0, P.wsym.spart, smem);
+    // one column: the partial sums are folded into the gather; several: a reduction
+    // phase (a slot shared by several multipliers would be summed repeatedly)
+    const bool fold = P.ncols == 1;
+    if (!fold) reduce_phase(P.wsym, P.blk, P.n_blk);
+    if (P.ng > 0 && P.ng <= COARSE_LOCAL_MAX) {
+      if (!fold) pcg_barrier(P);
+      coarse_local(P, smem);  // small coarse problem: every CTA solves it (no barrier)
+      bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, true, fold ? P.wsym.spart : nullptr, smem);
+    } else {
+      if (P.ng > 0) {  // g, then the rows of z, spread over the CTAs
+        coarse_spread(P);
+        pcg_barrier(P);
+        coarse_spread_z(P);
+      }
+      if (P.ng > 0 || !fold) pcg_barrier(P);
+      bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0, fold ? P.wsym.spart : nullptr);
+    }
   } else {
     tmv_phase<FWD, NCP, STAGES>(P.fwd, P.cta_ptr, P.cta_items, P.ncp, smem);
     pcg_barrier(P);
@@ -1069,7 +1109,13 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
   if (EXPL) {
     sym_phase<NCP, STAGES>(P.ssym, P.cta_ptr, P.cta_items, P.ncp, smem);
     pcg_barrier(P);
-    bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, P.ssym.spart);
+    if (P.ncols == 1) {
+      bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, P.ssym.spart);
+    } else {
+      reduce_phase(P.ssym, P.blk, P.n_blk);
+      pcg_barrier(P);
+      bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false);
+    }
   } else {
     tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.cta_ptr, P.cta_items, P.ncp, smem);
     pcg_barrier(P);
@@ -1560,7 +1606,9 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
     IETI_CUDA(cudaMemcpyFromSymbol(&n, g_prof_n, sizeof(int)));
     IETI_CUDA(cudaMemcpy(t.data(), prof.p, sizeof(unsigned long long) * std::min(n, 4096), cudaMemcpyDeviceToHost));
     n = std::min(n, 4096);
-    const int per = EXPL ? 6 : 9, skip = EXPL ? 4 : 5;
+    const int ng_ = h->n_primal, nc = a.fwd.ncols ? a.fwd.ncols : h->nrhs;
+    const int per = EXPL ? 6 + (nc > 1 ? 2 : 0) + (ng_ > COARSE_LOCAL_MAX ? 1 + (nc == 1 ? 1 : 0) : 0) : 9,
+              skip = EXPL ? 4 + (nc > 1 ? 1 : 0) : 5;
     std::vector<double> acc(per, 0.0);
     int cnt = 0;
     for (int i = skip; i + per < n; i += per, ++cnt)
@@ -1622,6 +1670,7 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.slot_red = h->slot_red.p;
   a.gsrc_ptr = h->gsrc_ptr.p;
   a.gsrc = h->gsrc.p;
+  a.gc = h->gc.p;
   a.blk = h->d_blk.p;
   a.n_blk = h->n_blk;
   a.lam = h->lam.p;
