@@ -42,6 +42,20 @@ def parse():
     return ap.parse_args()
 
 
+def traffic_from_profiles(config):
+    """DRAM traffic per PCG iteration of the persistent kernel, from the committed ncu
+    --set full capture (profiles/<run>_raw.txt: dram__bytes_read.sum + write.sum of the
+    whole k_pcg launch, divided by its iteration count); only for the captured config."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            t = json.load(f)
+    except OSError:
+        return {}
+    e = t.get(config)
+    return e or {}
+
+
 def peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -300,10 +314,14 @@ def run_ours(args, rank, world, local):
     phases = {"factor": rep["ms_factor"], "coarse_rhs": rep["ms_coarse"], "pcg": rep["ms_pcg"],
               "recover": rep["ms_recover"]}
     dominant = max(phases, key=phases.get)
-    roof_pcg = {"kernel": "pcg loop (k_local solve+precond, k_bgather x2, k_coarse, cg updates) per iteration",
+    tr = traffic_from_profiles(args.config)
+    roof_pcg = {"kernel": "persistent PCG kernel k_pcg (W_k and S_II symmetric tile passes, gathers, coarse "
+                          "solve, CG updates) per iteration",
                 "bound": "hbm", "achieved": pcg_gbs, "peak": hbm, "unit": "GB/s", "frac": pcg_gbs / hbm,
-                "traffic": None, "algorithmic_bytes_per_iter": int(pcg_bytes)}
-    roof_fac = {"kernel": "batched multifrontal Cholesky (k_potrf, k_panel_gemm DMMA, k_extend_add, k_scatter)",
+                "traffic": tr.get("pcg_bytes_per_iter"), "traffic_source": tr.get("pcg_source"),
+                "algorithmic_bytes_per_iter": int(pcg_bytes)}
+    roof_fac = {"kernel": "multifrontal Cholesky phase (k_gemm DMMA panel updates / TRSM / SYRK+extend-add, "
+                          "k_potrf, assembly; side stream: L11^-1, W_k, forward sweep)",
                 "bound": "tensor", "achieved": fac_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
                 "frac": fac_tflops / fp64_peak if fp64_peak else None, "traffic": None,
                 "useful_flops": rep["factor_flops"], "peak_source": "cuBLAS DGEMM 8192^3 measured in this run"}
@@ -323,7 +341,8 @@ def run_ours(args, rank, world, local):
                    "replicas": world},
         "phases_ms": phases, "iters": rep["iters"], "rel_residual": max(rep["rel_residual"]),
         "f_applies_per_s": f_apply_per_s, "f_apply_us": fa_ms * 1e3, "f_apply_gbs": fa_gbs,
-        "f_apply_note": "operator loop alone; L_II working set %.0f MB (L2 126 MB)" % (rep["f_apply_bytes"] / 2 / 1e6),
+        "f_apply_note": "ietidp_apply_F alone (explicit loop: W_k tiles %.0f MB per apply; L2 126 MB)"
+                        % (rep["f_apply_bytes"] / 1e6),
         "roofline": roofline, "rooflines": {"factor": roof_fac, "pcg": roof_pcg},
         "fp64_dgemm_tflops": fp64_peak, "clocks": clk.summary(), "gpu_launches": int(launches),
         "e2e": e2e, "cpu_baseline": cpu,
