@@ -15,6 +15,7 @@
 // S_loc = K_PP - K_Pr K_rr^-1 K_rP. Afterwards every pivot block is inverted
 // (partitioned inverse, recursive doubling with the same GEMM kernel).
 #include <climits>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -100,49 +101,11 @@ __device__ __forceinline__ void potrf_steps(double (&a)[32], int r, double (*cb)
     __syncthreads();
   }
 }
-__global__ void __launch_bounds__(POTRF_T) k_potrf(const Work* __restrict__ work, const SnDev* __restrict__ sn,
-                                                   double* __restrict__ pool, double* __restrict__ dinv,
-                                                   int* __restrict__ err) {
-  __shared__ double cb[2][TB];
-  __shared__ double pr[2];
-  __shared__ double dg[TB];  // 1 / L[j][j]
-  __shared__ double Ls[TB][TB + 1];
-  __shared__ double Ts[32][33];
-  const Work w = work[blockIdx.x];
-  const SnDev s = sn[w.sn];
-  const int p0 = w.a * TB;
-  const int b = min(TB, s.npiv - p0);
-  double* F = pool + s.front_off + (long long)p0 * s.ld + p0;
-  const int t = threadIdx.x, r = t & 63, h = t >> 6;
-  double a[32];
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const int c = 2 * i + h;
-    double v;
-    if (r < b && c < b) v = (c <= r) ? F[(long long)c * s.ld + r] : 0.0;
-    else v = (r == c) ? 1.0 : 0.0;  // identity padding of a partial block
-    a[i] = v;
-  }
-  bool ok = true;
-  if (h == 0) {
-    cb[0][r] = a[0];
-    if (r == 0) {
-      pr[0] = rsqrt_h(a[0]);
-      dg[0] = pr[0];
-      ok = a[0] > 0.0;
-    }
-  }
-  __syncthreads();
-  if (h == 0) potrf_steps<0>(a, r, cb, pr, dg, ok);
-  else potrf_steps<1>(a, r, cb, pr, dg, ok);
-  if (!ok) atomicMin(err, s.sub);
-#pragma unroll
-  for (int i = 0; i < 32; ++i) {
-    const int c = 2 * i + h;
-    if (r < b && c < b && c <= r) F[(long long)c * s.ld + r] = a[i];
-    Ls[r][c] = (c <= r) ? a[i] : 0.0;
-  }
-  __syncthreads();
+// X = L^-1 from L in Ls (lower, zero upper) into Dinv (column-major TB x TB): 32-blocks
+// X11 = L11^-1, X22 = L22^-1 by forward substitution (lane = column), X21 = -X22 (L21 X11).
+__device__ __forceinline__ void potrf_inverse(double (*Ls)[TB + 1], double (*Ts)[33], const double* dg, int b,
+                                              double* __restrict__ D) {
+  const int t = threadIdx.x;
   if (t < 64) {
     const int o = (t >> 5) * 32, c = t & 31;
     double x[32];
@@ -191,13 +154,151 @@ __global__ void __launch_bounds__(POTRF_T) k_potrf(const Work* __restrict__ work
 #pragma unroll
   for (int q = 0; q < 8; ++q) Ls[32 + rr][c0 + q] = -tv[q];
   __syncthreads();
-  double* D = dinv + s.dinv_off + (long long)w.a * TILE_ELEMS;  // column-major TB x TB
   for (int e = t; e < TILE_ELEMS; e += POTRF_T) {
     const int c = e >> 6, m = e & 63;
     double v = 0.0;
     if (m >= c && m < b && c < b) v = (c >= 32) ? Ls[m - 32][c] : Ls[m][c];
     D[e] = v;
   }
+}
+
+__global__ void __launch_bounds__(POTRF_T) k_potrf(const Work* __restrict__ work, const SnDev* __restrict__ sn,
+                                                   double* __restrict__ pool, double* __restrict__ dinv,
+                                                   int* __restrict__ err) {
+  __shared__ double cb[2][TB];
+  __shared__ double pr[2];
+  __shared__ double dg[TB];  // 1 / L[j][j]
+  __shared__ double Ls[TB][TB + 1];
+  __shared__ double Ts[32][33];
+  const Work w = work[blockIdx.x];
+  const SnDev s = sn[w.sn];
+  const int p0 = w.a * TB;
+  const int b = min(TB, s.npiv - p0);
+  double* F = pool + s.front_off + (long long)p0 * s.ld + p0;
+  const int t = threadIdx.x, r = t & 63, h = t >> 6;
+  double a[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = 2 * i + h;
+    double v;
+    if (r < b && c < b) v = (c <= r) ? F[(long long)c * s.ld + r] : 0.0;
+    else v = (r == c) ? 1.0 : 0.0;  // identity padding of a partial block
+    a[i] = v;
+  }
+  bool ok = true;
+  if (h == 0) {
+    cb[0][r] = a[0];
+    if (r == 0) {
+      pr[0] = rsqrt_h(a[0]);
+      dg[0] = pr[0];
+      ok = a[0] > 0.0;
+    }
+  }
+  __syncthreads();
+  if (h == 0) potrf_steps<0>(a, r, cb, pr, dg, ok);
+  else potrf_steps<1>(a, r, cb, pr, dg, ok);
+  if (!ok) atomicMin(err, s.sub);
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = 2 * i + h;
+    if (r < b && c < b && c <= r) F[(long long)c * s.ld + r] = a[i];
+    Ls[r][c] = (c <= r) ? a[i] : 0.0;
+  }
+  __syncthreads();
+  potrf_inverse(Ls, Ts, dg, b, dinv + s.dinv_off + (long long)w.a * TILE_ELEMS);
+}
+
+// Compact variant (default): the 64 elimination steps as a rolled loop over
+// 8-column panels (8 unrolled steps each) with the register window shifted by 4 per panel,
+// ~5x less code than k_potrf -- for an instruction cache that is cold at every launch.
+template <int H>
+__device__ __forceinline__ void potrf_steps_rolled(double (&a)[32], int r, double (*cb)[2 * TB], double* pr,
+                                                   double* dg, double (*Ls)[TB + 1], bool& ok) {
+#pragma unroll 1
+  for (int jb = 0; jb < TB; jb += 8) {
+#pragma unroll
+    for (int jj = 0; jj < 8; ++jj) {
+      const int j = jb + jj;
+      const double rj = pr[jj & 1];
+      const double* col = cb[jj & 1];
+      double* nxt = cb[(jj + 1) & 1];
+      const double cr = col[r];
+      const double sc = cr * rj * rj;
+      if ((jj & 1) == H) a[jj >> 1] = cr * rj;  // L[r][j] (valid for r >= j; 0 above: col is 0 there)
+      if (((jj + 1) & 1) == H && j + 1 < TB) {
+        const int i1 = (jj + 1) >> 1;
+        a[i1] = fma(-sc, col[j + 1], a[i1]);
+        const double v = a[i1];
+        nxt[r] = (r > j) ? v : 0.0;
+        const double rn = rsqrt_h(v);
+        if (r == j + 1) {
+          pr[(jj + 1) & 1] = rn;
+          dg[j + 1] = rn;
+          ok = ok && (v > 0.0);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 32; ++i) {
+        const int c = 2 * i + H;  // relative to jb
+        if (c >= jj + 2) a[i] = fma(-sc, col[jb + c], a[i]);
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int c = jb + 2 * i + H;
+      Ls[r][c] = (c <= r) ? a[i] : 0.0;
+    }
+#pragma unroll
+    for (int i = 0; i < 28; ++i) a[i] = a[i + 4];
+#pragma unroll
+    for (int i = 28; i < 32; ++i) a[i] = 0.0;
+  }
+}
+__global__ void __launch_bounds__(POTRF_T) k_potrf_c(const Work* __restrict__ work, const SnDev* __restrict__ sn,
+                                                     double* __restrict__ pool, double* __restrict__ dinv,
+                                                     int* __restrict__ err) {
+  __shared__ double cb[2][2 * TB];
+  __shared__ double pr[2];
+  __shared__ double dg[TB];
+  __shared__ double Ls[TB][TB + 1];
+  __shared__ double Ts[32][33];
+  const Work w = work[blockIdx.x];
+  const SnDev s = sn[w.sn];
+  const int p0 = w.a * TB;
+  const int b = min(TB, s.npiv - p0);
+  double* F = pool + s.front_off + (long long)p0 * s.ld + p0;
+  const int t = threadIdx.x, r = t & 63, h = t >> 6;
+  double a[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    const int c = 2 * i + h;
+    double v;
+    if (r < b && c < b) v = (c <= r) ? F[(long long)c * s.ld + r] : 0.0;
+    else v = (r == c) ? 1.0 : 0.0;
+    a[i] = v;
+  }
+  cb[0][TB + r] = 0.0;
+  cb[1][TB + r] = 0.0;
+  bool ok = true;
+  if (h == 0) {
+    cb[0][r] = a[0];
+    if (r == 0) {
+      pr[0] = rsqrt_h(a[0]);
+      dg[0] = pr[0];
+      ok = a[0] > 0.0;
+    }
+  }
+  __syncthreads();
+  if (h == 0) potrf_steps_rolled<0>(a, r, cb, pr, dg, Ls, ok);
+  else potrf_steps_rolled<1>(a, r, cb, pr, dg, Ls, ok);
+  if (!ok) atomicMin(err, s.sub);
+  __syncthreads();
+  for (int e = t; e < TILE_ELEMS; e += POTRF_T) {
+    const int c = e >> 6, m = e & 63;
+    if (m >= c && m < b && c < b) F[(long long)c * s.ld + m] = Ls[m][c];
+  }
+  potrf_inverse(Ls, Ts, dg, b, dinv + s.dinv_off + (long long)w.a * TILE_ELEMS);
 }
 
 // ---------------------------------------------------------------------------
@@ -568,6 +669,9 @@ void run_factor(ietidp_s* h) {
   }
   cudaStream_t s2 = h->side;
   size_t npan = 0;
+  // compact POTRF by default (measured faster in the pipeline: the instruction cache is
+  // cold at every launch); IETIDP_POTRF=unrolled selects the fully unrolled kernel
+  static const bool potrf_compact = !(getenv("IETIDP_POTRF") && !strcmp(getenv("IETIDP_POTRF"), "unrolled"));
   const LevelPlan::Panel* wacc_last = nullptr;
   IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));
   IETI_CUDA(cudaEventRecord(h->fev[nlev + 1], st));  // side work starts after level 0's assembly
@@ -601,7 +705,10 @@ void run_factor(ietidp_s* h) {
         IETI_LAUNCHED(h);
       }
       if (pn.potrf_n) {
-        k_potrf<<<pn.potrf_n, POTRF_T, 0, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
+        if (potrf_compact)
+          k_potrf_c<<<pn.potrf_n, POTRF_T, 0, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
+        else
+          k_potrf<<<pn.potrf_n, POTRF_T, 0, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
         IETI_LAUNCHED(h);
       }
       cudaEvent_t pe = h->pev[npan++];
