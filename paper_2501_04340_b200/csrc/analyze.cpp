@@ -811,7 +811,13 @@ void analyze_all(ietidp_s* h) {
   h->fval_off.resize(ns);
   h->u_off.resize(ns);
   std::vector<LoopWork> loopwork;
-  std::vector<int> sub_cta0(ns), sub_ncta(ns);
+  std::vector<SymWork> symwork;
+  std::vector<int> sub_cta0(ns), sub_ncta(ns), sub_blk0(ns), sub_nt(ns);
+  int maxnt_all = 0;
+  for (int k = 0; k < ns; ++k) maxnt_all = std::max(maxnt_all, tiles_of(P.subs[k].nI));
+  const int maxseg = std::max(1, (maxnt_all + SYM_SEG - 1) / SYM_SEG);
+  long long npo = 0;
+  int blk = 0;
   for (int k = 0; k < ns; ++k) {
     SubPlan& sp = P.subs[k];
     SubDev& d = h->h_sub[k];
@@ -860,12 +866,26 @@ void analyze_all(ietidp_s* h) {
       ++cta;
     }
     sub_ncta[k] = cta - d.cta0;
+    // symmetric-pass items (explicit loop): segments of SYM_SEG tiles of each block row
+    d.blk0 = blk;
+    sub_blk0[k] = blk;
+    sub_nt[k] = d.nt;
+    blk += d.nt;
+    d.npart_off = npo;
+    npo += (long long)d.nt * maxseg;
+    for (int o = 0; o < d.nt; ++o)
+      for (int seg = 0; seg * SYM_SEG <= o; ++seg) {
+        const int j0 = seg * SYM_SEG, j1 = std::min(o, j0 + SYM_SEG - 1);
+        symwork.push_back({k, o, j0, j1, seg, j1 - j0 + 2});
+      }
   }
+  h->sym_maxseg = maxseg;
   if (P.max_nI > 32 * TB) throw Error(IETIDP_E_ARG, "interface block larger than 2048 DOFs is not supported");
   if (P.nPmax > 16) throw Error(IETIDP_E_ARG, "more than 16 primal DOFs in one subdomain is not supported");
   h->n_slots = (int)rio;
   h->sum_nP = po;
   h->n_loopwork = (int)loopwork.size();
+  h->n_symwork = (int)symwork.size();
   // the r_I roots by level (S_II is copied before the root is factored)
   P.roots_by_level.assign(P.max_level + 1, {});
   for (int k = 0; k < ns; ++k)
@@ -1062,7 +1082,10 @@ void analyze_all(ietidp_s* h) {
     for (int g = 0; g < ng; ++g) {
       for (auto& x : pc[g]) {
         const SubDev& d = h->h_sub[x.first];
-        for (int it = d.cta0; it < d.cta0 + sub_ncta[x.first]; ++it) gsrc.push_back(it * npm + x.second);
+        if (h->opt.loop == IETIDP_LOOP_EXPLICIT)  // symmetric pass: one row per (subdomain, block)
+          for (int it = d.blk0; it < d.blk0 + d.nt; ++it) gsrc.push_back(it * npm + x.second);
+        else  // triangular loop: one row per block-pair item
+          for (int it = d.cta0; it < d.cta0 + sub_ncta[x.first]; ++it) gsrc.push_back(it * npm + x.second);
       }
       gsrc_ptr[g + 1] = (int)gsrc.size();
     }
@@ -1144,6 +1167,8 @@ void analyze_all(ietidp_s* h) {
   h->pcon_sub.upload(pcon_sub, s);
   h->pcon_q.upload(pcon_q, s);
   h->d_loopwork.upload(loopwork, s);
+  h->d_symwork.upload(symwork, s);
+  h->h_symwork = symwork;
   h->h_loopwork = loopwork;
   h->lpt_grid = 0;
   {
@@ -1170,7 +1195,8 @@ void analyze_all(ietidp_s* h) {
       const SubDev& d = h->h_sub[k];
       for (int a = 0; a < d.nI; ++a) {
         const int j = a / TB, r = a % TB;
-        sred[d.rI_off + a] = {(d.spart_off + j) * TB + r, j, d.nt};
+        sred[d.rI_off + a] = {(d.spart_off + j) * TB + r, (d.npart_off + (long long)j * h->sym_maxseg) * TB + r, j,
+                              d.nt, j / SYM_SEG + 1, 0};
       }
     }
     h->slot_red.upload(sred, s);
@@ -1184,6 +1210,8 @@ void analyze_all(ietidp_s* h) {
   }
   h->sub_cta0.upload(sub_cta0, s);
   h->sub_ncta.upload(sub_ncta, s);
+  h->sub_blk0.upload(sub_blk0, s);
+  h->sub_nt.upload(sub_nt, s);
   std::vector<double> kvals(kv), fvals(fv);
   for (int k = 0; k < ns; ++k) {
     std::copy(h->in[k].val.begin(), h->in[k].val.end(), kvals.begin() + h->kval_off[k]);
@@ -1217,6 +1245,7 @@ void analyze_all(ietidp_s* h) {
     h->stiles.alloc(to);
   }
   h->spart.alloc((size_t)std::max(spo, 1LL) * TB * nc);
+  h->npart.alloc((size_t)std::max(npo, 1LL) * TB * nc);
   h->delta.alloc(h->n_slots);
   h->kdiag.alloc(h->n_slots);
   const size_t m = (size_t)h->n_lambda * nc;
@@ -1230,7 +1259,7 @@ void analyze_all(ietidp_s* h) {
   h->xI.alloc((size_t)h->n_slots * nc);
   h->sI.alloc((size_t)h->n_slots * nc);
   h->zI.alloc((size_t)h->n_slots * nc);
-  h->gpart.alloc((size_t)std::max(cta, 1) * std::max(P.nPmax, 1) * nc);
+  h->gpart.alloc((size_t)std::max({cta, blk, 1}) * std::max(P.nPmax, 1) * nc);
   h->zc.alloc((size_t)std::max(ng, 1) * nc);
   h->gc.alloc((size_t)std::max(ng, 1) * nc);
   h->partial.alloc(4 * 1024 * (size_t)nc);

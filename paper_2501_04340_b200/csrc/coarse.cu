@@ -23,7 +23,7 @@ void loop_fwd(ietidp_s* h, int ncols, const double* v, double* y, bool partials,
 void loop_bwd(ietidp_s* h, int ncols, const double* y, const double* z, double zsign, double* x, const void* st);
 void bgather(ietidp_s* h, int ncols, const double* x, const double* weight, double* out, const double* dotv,
              double* partial, const void* st);
-void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const void* st);
+void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const void* st, bool sym_rows = false);
 __global__ void k_scatter(long long n, const long long* __restrict__ dst, const int* __restrict__ src,
                           const double* __restrict__ vals, double* __restrict__ out);
 

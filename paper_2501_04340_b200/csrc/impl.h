@@ -55,6 +55,8 @@ struct SubDev {
   long long g_off;             // G_k = L_II^-T L_PI^T: nI x nP row-major (explicit loop)
   long long spart_off;         // symmetric-pass partial blocks: nt(nt-1)/2 blocks of TB x ncols
   int prim_off, perm_off, nt, cta0;  // primal rows, perm, #tile blocks, first loop CTA
+  int blk0;             // first (subdomain, block) index: coarse partial rows of the symmetric pass
+  long long npart_off;  // symmetric pass: N-partials (nt x maxseg blocks of TB rows)
 };
 
 // One multiplier's two B entries (every row is {+1, -1} in two subdomains).
@@ -90,11 +92,21 @@ struct GemmWork {
   long long ws_off;
 };
 
-// Per r_I slot: where the symmetric pass left its partial sums (folded into the gather):
-// y[slot] = vout[slot] + sum_{i = j+1}^{nt-1} spart[(base + i (i-1)/2 TB) ncols + c].
+// Per r_I slot: where the symmetric pass left its partial sums (folded into the gather
+// or reduced), in this fixed order:
+//   y[slot] = sum_{s < nseg} npart[(nbase + s TB) ncols + c]
+//           + sum_{i = j+1}^{nt-1} spart[(base + i (i-1)/2 TB) ncols + c].
 struct SlotRed {
-  long long base;  // (spart_off + j) TB + r
-  int j, nt;
+  long long base;   // (spart_off + j) TB + r
+  long long nbase;  // (npart_off + j maxseg) TB + r
+  int j, nt, nseg, pad_;
+};
+
+// A work item of the symmetric tile passes (explicit loop): tiles (o, j0..j1) of the
+// lower block row o of one subdomain; segment seg of the row.
+constexpr int SYM_SEG = 4;  // tiles per segment
+struct SymWork {
+  int sub, o, j0, j1, seg, cost;
 };
 
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).

@@ -71,6 +71,9 @@ struct TmvArgs {
   double* gpart;           // FWD/SYM: coarse partials [cta][nPmax][ncols] (nullable)
   const double* gmat;      // SYM: G_k (n_I x n_P row-major) for the coarse partials
   double* spart;           // SYM: partial blocks of the transposed tile products
+  double* npart;           // SYM: partial row products per row segment
+  const SymWork* swork;    // SYM: work items (row segments)
+  int maxseg;              // SYM: segments per block row (npart layout)
   int slot_in;             // FWD/PRE1/SYM: vin is already in slot order (B^T, weights applied)
   int nPmax, ncols, c_off;
   const PcgState* st;
@@ -351,53 +354,53 @@ __device__ __forceinline__ void tmv_item(const TmvArgs& A, int item, double* sme
 // accumulates the coarse partial G_k^T x of its own rows.
 template <int NCP, int STAGES>
 __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* smem) {
+  // One row segment (o, j0..j1) of the symmetric lower tile matrix:
+  //   N: npart[o][seg] = sum_j S_oj x_j        (the row product, partial over the segment)
+  //   T: spart(o, j)   = S_oj^T x_o, j < o     (the transposed products, per tile)
+  // plus, for the first segment of a row, the coarse partial G_k[rows o]^T x_o.
   constexpr int VS = (NCP == 1) ? 1 : NCP + 4;
   constexpr int NB = (NCP == 1) ? 1 : NCP / 8;
-  __shared__ double red[8][TB];
+  __shared__ double red[2][8][TB];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int ncl = min(NCP, A.ncols - A.c_off);
   __syncthreads();
-  const LoopWork lw = A.work[item];
-  const SubDev d = A.sub[lw.sub];
-  const int ob[2] = {lw.blk0, lw.blk1};
-  const int nob = lw.nblk;
-  const int bmax = max(ob[0], ob[nob - 1]);
-  const int hi = (bmax + 1) * TB;
+  const SymWork sw = A.swork[item];
+  const SubDev d = A.sub[sw.sub];
+  const int o = sw.o, j0 = sw.j0, j1 = sw.j1, nsteps = j1 - j0 + 1;
+  const bool xo_sep = j1 < o;
   double* ring = smem;
-  double* vec = smem + STAGES * TILE_ELEMS;  // rows [0, hi)
-  double* outb = vec + hi * VS;
-  if (A.slot_in) gather_async<VS>(vec, 0, hi, d, A, ncl);  // committed with the first tile
-  else gather_rows<VS, true, false>(vec, 0, hi, d, A, ncl, nullptr, NCP);
-  const int n0 = ob[0] + 1;
-  const int nsteps = n0 + (nob == 2 ? ob[1] + 1 : 0);
-  auto tile_ptr = [&](int s) {
-    const int which = s < n0 ? 0 : 1;
-    const int o = ob[which], j = which ? s - n0 : s;
-    return A.tiles + d.tile_off + (long long)(o * (o + 1) / 2 + j) * TILE_ELEMS;
+  double* vec = smem + STAGES * TILE_ELEMS;  // blocks j0..j1, then block o if separate
+  double* xo = xo_sep ? vec + nsteps * TB * VS : vec + (o - j0) * TB * VS;
+  if (A.slot_in) {
+    gather_async<VS>(vec, j0 * TB, (j1 + 1) * TB, d, A, ncl);  // committed with the first tile
+    if (xo_sep) gather_async<VS>(xo, o * TB, (o + 1) * TB, d, A, ncl);
+  } else {
+    gather_rows<VS, true, false>(vec, j0 * TB, (j1 + 1) * TB, d, A, ncl, nullptr, NCP);
+    if (xo_sep) gather_rows<VS, true, false>(xo, o * TB, (o + 1) * TB, d, A, ncl, nullptr, NCP);
+  }
+  auto tile_ptr = [&](int st) {
+    return A.tiles + d.tile_off + (long long)(o * (o + 1) / 2 + j0 + st) * TILE_ELEMS;
   };
 #pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nsteps) load_tile_async(ring + s * TILE_ELEMS, tile_ptr(s), tid);
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nsteps) load_tile_async(ring + st * TILE_ELEMS, tile_ptr(st), tid);
     cp_async_commit();
   }
   cp_async_wait<STAGES - 2>();  // group 0: the gathered input and tile 0
   __syncthreads();              // vec complete
-  // coarse partial: G_k^T x over the own block rows (G rows staged in smem)
+  // coarse partial of block row o (first segment only): G_k[rows o]^T x_o
   double gacc = 0.0;
-  if (A.gpart && d.nP > 0) {
-    double* gs = outb + TB * VS;  // TB x nP
-    for (int w2 = 0; w2 < nob; ++w2) {
-      const int o = ob[w2];
-      const int na = min(TB, d.nI - o * TB);
-      const double* Gb = A.gmat + d.g_off + (long long)o * TB * d.nP;
-      for (int e = tid; e < na * d.nP; e += 256) gs[e] = Gb[e];
-      __syncthreads();
-      if (tid < d.nP * NCP) {
-        const int q = tid / NCP, c = tid % NCP;
-        for (int r = 0; r < na; ++r) gacc += gs[r * d.nP + q] * vec[(o * TB + r) * VS + c];
-      }
-      __syncthreads();
+  if (A.gpart && d.nP > 0 && sw.seg == 0) {
+    double* gs = xo + TB * VS;  // TB x nP
+    const int na = min(TB, d.nI - o * TB);
+    const double* Gb = A.gmat + d.g_off + (long long)o * TB * d.nP;
+    for (int e = tid; e < na * d.nP; e += 256) gs[e] = Gb[e];
+    __syncthreads();
+    if (tid < d.nP * NCP) {
+      const int q = tid / NCP, c = tid % NCP;
+      for (int r = 0; r < na; ++r) gacc += gs[r * d.nP + q] * xo[r * VS + c];
     }
+    __syncthreads();
   }
   double accN[8], acc[NB][2];
 #pragma unroll
@@ -405,20 +408,28 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
 #pragma unroll
   for (int i = 0; i < NB; ++i) acc[i][0] = acc[i][1] = 0.0;
   const int g = lane >> 2, t4 = lane & 3;
-  for (int s = 0; s < nsteps; ++s) {
+  double* pend = nullptr;  // NCP == 1: T partial of the previous tile still in red[]
+  for (int st = 0; st < nsteps; ++st) {
     cp_async_wait<STAGES - 2>();
     __syncthreads();
+    if constexpr (NCP == 1) {
+      if (pend && tid < TB) {
+        double v = 0.0;
+#pragma unroll
+        for (int w2 = 0; w2 < 8; ++w2) v += red[(st - 1) & 1][w2][tid];
+        pend[(long long)tid * A.ncols] = v;
+      }
+      pend = nullptr;
+    }
     {
-      const int sn = s + STAGES - 1;
+      const int sn = st + STAGES - 1;
       if (sn < nsteps) load_tile_async(ring + (sn % STAGES) * TILE_ELEMS, tile_ptr(sn), tid);
       cp_async_commit();
     }
-    const double* Tt = ring + (s % STAGES) * TILE_ELEMS;
-    const int which = s < n0 ? 0 : 1;
-    const int o = ob[which], j = which ? s - n0 : s;
-    const bool last = (j == o);
-    const double* xj = vec + j * TB * VS;
-    const double* xo = vec + o * TB * VS;
+    const double* Tt = ring + (st % STAGES) * TILE_ELEMS;
+    const int j = j0 + st;
+    const bool diag = (j == o);
+    const double* xj = vec + st * TB * VS;
     double* pblk = A.spart + ((d.spart_off + (long long)o * (o - 1) / 2 + j) * TB) * A.ncols + A.c_off;
     if constexpr (NCP == 1) {
       {  // N: y_o += S_oj x_j
@@ -429,7 +440,7 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
           accN[rr] += Tt[swz(r, lane)] * x0 + Tt[swz(r, lane + 32)] * x1;
         }
       }
-      if (!last) {  // T: partial (o, j) = S_oj^T x_o
+      if (!diag) {  // T: partial (o, j) = S_oj^T x_o, reduced over the warps at the next step
         double p0 = 0.0, p1 = 0.0;
 #pragma unroll
         for (int rr = 0; rr < 8; ++rr) {
@@ -438,29 +449,9 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
           p0 += Tt[swz(r, lane)] * xr;
           p1 += Tt[swz(r, lane + 32)] * xr;
         }
-        red[warp][lane] = p0;
-        red[warp][lane + 32] = p1;
-        __syncthreads();
-        if (tid < TB) {
-          double v = 0.0;
-#pragma unroll
-          for (int w2 = 0; w2 < 8; ++w2) v += red[w2][tid];
-          pblk[(long long)tid * A.ncols] = v;
-        }
-      } else {
-        double full[8];
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) full[rr] = warp_sum(accN[rr]);
-        if (lane < 8) {
-          double v = full[0];
-#pragma unroll
-          for (int rr = 1; rr < 8; ++rr)
-            if (lane == rr) v = full[rr];
-          const int a = o * TB + warp * 8 + lane;
-          if (a < d.nI) A.vout[(d.rI_off + a) * A.ncols + A.c_off] = v;
-        }
-#pragma unroll
-        for (int rr = 0; rr < 8; ++rr) accN[rr] = 0.0;
+        red[st & 1][warp][lane] = p0;
+        red[st & 1][warp][lane + 32] = p1;
+        pend = pblk;
       }
     } else {
 #pragma unroll 4
@@ -469,7 +460,7 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) dmma8x8x4(acc[nb][0], acc[nb][1], a, xj[(k0 + t4) * VS + nb * 8 + g]);
       }
-      if (!last) {
+      if (!diag) {
         double pt[NB][2];
 #pragma unroll
         for (int nb = 0; nb < NB; ++nb) pt[nb][0] = pt[nb][1] = 0.0;
@@ -486,38 +477,244 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
             const int c = nb * 8 + 2 * t4 + q;
             if (c < ncl) pblk[(long long)(warp * 8 + g) * A.ncols + c] = pt[nb][q];
           }
-      } else {
-#pragma unroll
-        for (int nb = 0; nb < NB; ++nb)
-#pragma unroll
-          for (int q = 0; q < 2; ++q) {
-            const int c = nb * 8 + 2 * t4 + q;
-            const int a = o * TB + warp * 8 + g;
-            if (c < ncl && a < d.nI) A.vout[(d.rI_off + a) * A.ncols + A.c_off + c] = acc[nb][q];
-            acc[nb][q] = 0.0;
-          }
       }
     }
   }
-  cp_async_wait<0>();
-  if (A.gpart && tid < d.nP * NCP) {
-    const int q = tid / NCP, c = tid % NCP;
-    if (c < ncl) A.gpart[((long long)item * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
+  double* nb_out = A.npart + ((d.npart_off + (long long)o * A.maxseg + sw.seg) * TB) * A.ncols + A.c_off;
+  if constexpr (NCP == 1) {
+    __syncthreads();
+    if (pend && tid < TB) {
+      double v = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < 8; ++w2) v += red[(nsteps - 1) & 1][w2][tid];
+      pend[(long long)tid * A.ncols] = v;
+    }
+    double full[8];
+#pragma unroll
+    for (int rr = 0; rr < 8; ++rr) full[rr] = warp_sum(accN[rr]);
+    if (lane < 8) {
+      double v = full[0];
+#pragma unroll
+      for (int rr = 1; rr < 8; ++rr)
+        if (lane == rr) v = full[rr];
+      nb_out[(long long)(warp * 8 + lane) * A.ncols] = v;
+    }
+  } else {
+#pragma unroll
+    for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        const int c = nb * 8 + 2 * t4 + q;
+        if (c < ncl) nb_out[(long long)(warp * 8 + g) * A.ncols + c] = acc[nb][q];
+      }
   }
-  (void)outb;
+  cp_async_wait<0>();
+  if (A.gpart && sw.seg == 0 && tid < d.nP * NCP) {
+    const int q = tid / NCP, c = tid % NCP;
+    if (c < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
+  }
 }
 
-// y_j += sum_{i > j} partial (i, j), for one (subdomain, block) work item.
+// The symmetric pass over a CTA's list of row-segment items as ONE tile stream: the
+// cp.async ring runs across item boundaries (the next item's input rows are gathered
+// into the other of NVB vector buffers together with its first tile), so there is no
+// pipeline refill per item. Same arithmetic and outputs as sym_item (slot_in only).
+template <int NCP, int STAGES>
+__device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, int nitems, double* smem) {
+  constexpr int VS = (NCP == 1) ? 1 : NCP + 4;
+  constexpr int NB = (NCP == 1) ? 1 : NCP / 8;
+  // vector buffers: at most STAGES items are in flight (the consumed one and up to
+  // STAGES - 1 issued ahead, each with at least one tile), so STAGES buffers suffice
+  constexpr int NVB = STAGES;
+  constexpr int VROWS = (SYM_SEG + 1) * TB;
+  __shared__ double red[2][8][TB];
+  __shared__ SymWork s_sw[NVB];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int ncl = min(NCP, A.ncols - A.c_off);
+  if (nitems == 0) return;
+  double* ring = smem;
+  double* vbase = smem + STAGES * TILE_ELEMS;
+  double* gs = vbase + NVB * VROWS * VS;  // TB x nP coarse rows
+  __syncthreads();
+  // issue cursor: (item ii, step is) of the next tile to prefetch
+  int ii = 0, is = 0;
+  auto nsteps_of = [&](const SymWork& w) { return w.j1 - w.j0 + 1; };
+  SymWork wi = A.swork[items[0]];
+  auto issue = [&](int gslot) {  // prefetch the next tile (and, at an item's first tile, its input rows)
+    if (ii < nitems) {
+      const SubDev d = A.sub[wi.sub];
+      if (is == 0) {
+        double* vec = vbase + (ii % NVB) * VROWS * VS;
+        const int nst = nsteps_of(wi);
+        gather_async<VS>(vec, wi.j0 * TB, (wi.j1 + 1) * TB, d, A, ncl);
+        if (wi.j1 < wi.o) gather_async<VS>(vec + nst * TB * VS, wi.o * TB, (wi.o + 1) * TB, d, A, ncl);
+        if (tid == 0) s_sw[ii % NVB] = wi;
+      }
+      load_tile_async(ring + gslot * TILE_ELEMS,
+                      A.tiles + d.tile_off + (long long)(wi.o * (wi.o + 1) / 2 + wi.j0 + is) * TILE_ELEMS, tid);
+      if (++is == nsteps_of(wi)) {
+        is = 0;
+        if (++ii < nitems) wi = A.swork[items[ii]];
+      }
+    }
+    cp_async_commit();
+  };
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) issue(st);
+  double accN[8], acc[NB][2];
+  double gacc = 0.0;
+  const int g = lane >> 2, t4 = lane & 3;
+  double* pend = nullptr;
+  int pend_buf = 0;
+  int gt = 0;  // global tile counter of the CTA
+  for (int k = 0; k < nitems; ++k) {
+    cp_async_wait<STAGES - 2>();
+    __syncthreads();  // item k's input rows and first tile are in; s_sw[k] visible
+    const SymWork sw = s_sw[k % NVB];
+    const SubDev d = A.sub[sw.sub];
+    const int o = sw.o, j0 = sw.j0, nst = nsteps_of(sw);
+    double* vec = vbase + (k % NVB) * VROWS * VS;
+    double* xo = (sw.j1 < o) ? vec + nst * TB * VS : vec + (o - j0) * TB * VS;
+    gacc = 0.0;
+    if (A.gpart && d.nP > 0 && sw.seg == 0) {  // coarse partial of block row o
+      const int na = min(TB, d.nI - o * TB);
+      const double* Gb = A.gmat + d.g_off + (long long)o * TB * d.nP;
+      for (int e = tid; e < na * d.nP; e += 256) gs[e] = Gb[e];
+      __syncthreads();
+      if (tid < d.nP * NCP) {
+        const int q = tid / NCP, c = tid % NCP;
+        for (int r = 0; r < na; ++r) gacc += gs[r * d.nP + q] * xo[r * VS + c];
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) accN[i] = 0.0;
+#pragma unroll
+    for (int i = 0; i < NB; ++i) acc[i][0] = acc[i][1] = 0.0;
+    for (int st = 0; st < nst; ++st, ++gt) {
+      if (st > 0) {
+        cp_async_wait<STAGES - 2>();
+        __syncthreads();
+      }
+      if constexpr (NCP == 1) {
+        if (pend && tid < TB) {
+          double v = 0.0;
+#pragma unroll
+          for (int w2 = 0; w2 < 8; ++w2) v += red[pend_buf][w2][tid];
+          pend[(long long)tid * A.ncols] = v;
+        }
+        pend = nullptr;
+      }
+      issue((gt + STAGES - 1) % STAGES);
+      const double* Tt = ring + (gt % STAGES) * TILE_ELEMS;
+      const int j = j0 + st;
+      const bool diag = (j == o);
+      const double* xj = vec + st * TB * VS;
+      double* pblk = A.spart + ((d.spart_off + (long long)o * (o - 1) / 2 + j) * TB) * A.ncols + A.c_off;
+      if constexpr (NCP == 1) {
+        {
+          const double x0 = xj[lane], x1 = xj[lane + 32];
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const int r = warp * 8 + rr;
+            accN[rr] += Tt[swz(r, lane)] * x0 + Tt[swz(r, lane + 32)] * x1;
+          }
+        }
+        if (!diag) {
+          double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+          for (int rr = 0; rr < 8; ++rr) {
+            const int r = warp * 8 + rr;
+            const double xr = xo[r];
+            p0 += Tt[swz(r, lane)] * xr;
+            p1 += Tt[swz(r, lane + 32)] * xr;
+          }
+          red[gt & 1][warp][lane] = p0;
+          red[gt & 1][warp][lane + 32] = p1;
+          pend = pblk;
+          pend_buf = gt & 1;
+        }
+      } else {
+#pragma unroll 4
+        for (int k0 = 0; k0 < TB; k0 += 4) {
+          const double a = Tt[swz(warp * 8 + g, k0 + t4)];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) dmma8x8x4(acc[nb][0], acc[nb][1], a, xj[(k0 + t4) * VS + nb * 8 + g]);
+        }
+        if (!diag) {
+          double pt[NB][2];
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb) pt[nb][0] = pt[nb][1] = 0.0;
+#pragma unroll 4
+          for (int k0 = 0; k0 < TB; k0 += 4) {
+            const double a = Tt[swz(k0 + t4, warp * 8 + g)];
+#pragma unroll
+            for (int nb = 0; nb < NB; ++nb) dmma8x8x4(pt[nb][0], pt[nb][1], a, xo[(k0 + t4) * VS + nb * 8 + g]);
+          }
+#pragma unroll
+          for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int c = nb * 8 + 2 * t4 + q;
+              if (c < ncl) pblk[(long long)(warp * 8 + g) * A.ncols + c] = pt[nb][q];
+            }
+        }
+      }
+    }
+    // item done: its row-segment partial and coarse partial
+    double* nb_out = A.npart + ((d.npart_off + (long long)o * A.maxseg + sw.seg) * TB) * A.ncols + A.c_off;
+    if constexpr (NCP == 1) {
+      double full[8];
+#pragma unroll
+      for (int rr = 0; rr < 8; ++rr) full[rr] = warp_sum(accN[rr]);
+      if (lane < 8) {
+        double v = full[0];
+#pragma unroll
+        for (int rr = 1; rr < 8; ++rr)
+          if (lane == rr) v = full[rr];
+        nb_out[(long long)(warp * 8 + lane) * A.ncols] = v;
+      }
+    } else {
+#pragma unroll
+      for (int nb = 0; nb < NB; ++nb)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = nb * 8 + 2 * t4 + q;
+          if (c < ncl) nb_out[(long long)(warp * 8 + g) * A.ncols + c] = acc[nb][q];
+        }
+    }
+    if (A.gpart && sw.seg == 0 && tid < d.nP * NCP) {
+      const int q = tid / NCP, c = tid % NCP;
+      if (c < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
+    }
+  }
+  if constexpr (NCP == 1) {
+    __syncthreads();
+    if (pend && tid < TB) {
+      double v = 0.0;
+#pragma unroll
+      for (int w2 = 0; w2 < 8; ++w2) v += red[pend_buf][w2][tid];
+      pend[(long long)tid * A.ncols] = v;
+    }
+  }
+  cp_async_wait<0>();
+  __syncthreads();
+}
+
+// y_j = sum over the row segments of the N-partials + sum_{i > j} partial (i, j),
+// for one (subdomain, block) work item (fixed order).
 __device__ __forceinline__ void sym_reduce_item(const TmvArgs& A, int k, int j) {
   const SubDev d = A.sub[k];
   const int nc = A.ncols;
+  const int nseg = j / SYM_SEG + 1;
   for (int e = threadIdx.x; e < TB * nc; e += 256) {
     const int r = e / nc, c = e - r * nc;
     const int a = j * TB + r;
     if (a >= d.nI) continue;
     double v = 0.0;
-    for (int i = j + 1; i < d.nt; ++i) v += A.spart[((d.spart_off + (long long)i * (i - 1) / 2 + j) * TB + r) * nc + c];
-    A.vout[(d.rI_off + a) * nc + c] += v;
+    for (int sg = 0; sg < nseg; ++sg) v += A.npart[((d.npart_off + (long long)j * A.maxseg + sg) * TB + r) * nc + c];
+    double t = 0.0;
+    for (int i = j + 1; i < d.nt; ++i) t += A.spart[((d.spart_off + (long long)i * (i - 1) / 2 + j) * TB + r) * nc + c];
+    A.vout[(d.rI_off + a) * nc + c] = v + t;
   }
 }
 
@@ -857,6 +1054,7 @@ struct PcgArgs {
   const SlotRed* slot_red;         // explicit loop: partial sums folded into the gathers
   const int *gsrc_ptr, *gsrc;      // coarse partial rows per global primal
   double* gc;                      // coarse right-hand side g (larger coarse problems)
+  int fold;                        // one column: fold the symmetric partials into the gathers
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -917,7 +1115,8 @@ template <int NCP, int STAGES>
 __device__ __forceinline__ void sym_phase(TmvArgs A, const int* cta_ptr, const int* cta_items, int ncp, double* smem) {
   for (int c0 = 0; c0 < A.ncols; c0 += ncp) {
     A.c_off = c0;
-    for (int e = cta_ptr[blockIdx.x]; e < cta_ptr[blockIdx.x + 1]; ++e) sym_item<NCP, STAGES>(A, cta_items[e], smem);
+    const int beg = cta_ptr[blockIdx.x], end = cta_ptr[blockIdx.x + 1];
+    sym_stream<NCP, STAGES>(A, cta_items + beg, end - beg, smem);
   }
 }
 
@@ -1004,19 +1203,22 @@ __device__ __forceinline__ void coarse_spread_z(const PcgArgs& P) {
   }
 }
 
-// y[slot][c] of a symmetric pass: the N part plus the transposed partials (fixed order)
-__device__ __forceinline__ double sym_value(const double* y, const double* spart, const SlotRed* sred, long long a,
+// y[slot][c] of a symmetric pass: the row-segment partials plus the transposed partials
+// (the same fixed order as sym_reduce_item)
+__device__ __forceinline__ double sym_value(const double* npart, const double* spart, const SlotRed* sred, long long a,
                                             int nc, int c) {
   const SlotRed sr = sred[a];
   double v = 0.0;
-  for (int i = sr.j + 1; i < sr.nt; ++i) v += spart[(sr.base + (long long)(i * (i - 1) / 2) * TB) * nc + c];
-  return y[a * nc + c] + v;
+  for (int sg = 0; sg < sr.nseg; ++sg) v += npart[(sr.nbase + (long long)sg * TB) * nc + c];
+  double t = 0.0;
+  for (int i = sr.j + 1; i < sr.nt; ++i) t += spart[(sr.base + (long long)(i * (i - 1) / 2) * TB) * nc + c];
+  return v + t;
 }
 
 // out = sum_k B (w) (x + G z), with the per-CTA partial of out . dotv
 __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x, const double* w, double* out,
                                               const double* dotv, double* part, bool coarse,
-                                              const double* spart = nullptr, const double* zs = nullptr) {
+                                              const TmvArgs* fold = nullptr, const double* zs = nullptr) {
   const int nc = P.ncols, P2 = pow2ge(nc);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
   double dot = 0.0;
@@ -1027,7 +1229,7 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int a = L.slot[q];
-        double xv = spart ? sym_value(x, spart, P.slot_red, a, nc, c) : x[(long long)a * nc + c];
+        double xv = fold ? sym_value(fold->npart, fold->spart, P.slot_red, a, nc, c) : x[(long long)a * nc + c];
         if (coarse) {
           if (zs) {  // G_k[slot row] . z (z in shared memory)
             const int np = P.ct.np[a];
@@ -1076,12 +1278,12 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     pcg_barrier(P);
     // one column: the partial sums are folded into the gather; several: a reduction
     // phase (a slot shared by several multipliers would be summed repeatedly)
-    const bool fold = P.ncols == 1;
+    const bool fold = P.ncols == 1 && P.fold;
     if (!fold) reduce_phase(P.wsym, P.blk, P.n_blk);
     if (P.ng > 0 && P.ng <= COARSE_LOCAL_MAX) {
       if (!fold) pcg_barrier(P);
       coarse_local(P, smem);  // small coarse problem: every CTA solves it (no barrier)
-      bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, true, fold ? P.wsym.spart : nullptr, smem);
+      bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, true, fold ? &P.wsym : nullptr, smem);
     } else {
       if (P.ng > 0) {  // g, then the rows of z, spread over the CTAs
         coarse_spread(P);
@@ -1089,7 +1291,7 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
         coarse_spread_z(P);
       }
       if (P.ng > 0 || !fold) pcg_barrier(P);
-      bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0, fold ? P.wsym.spart : nullptr);
+      bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0, fold ? &P.wsym : nullptr);
     }
   } else {
     tmv_phase<FWD, NCP, STAGES>(P.fwd, P.cta_ptr, P.cta_items, P.ncp, smem);
@@ -1109,8 +1311,8 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
   if (EXPL) {
     sym_phase<NCP, STAGES>(P.ssym, P.cta_ptr, P.cta_items, P.ncp, smem);
     pcg_barrier(P);
-    if (P.ncols == 1) {
-      bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, P.ssym.spart);
+    if (P.ncols == 1 && P.fold) {
+      bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, &P.ssym);
     } else {
       reduce_phase(P.ssym, P.blk, P.n_blk);
       pcg_barrier(P);
@@ -1264,9 +1466,21 @@ struct TmvCfg {
   int ncp, stages, smem;
 };
 
-static TmvCfg tmv_cfg(const ietidp_s* h, int ncols) {
+// sym: the explicit loop's symmetric passes (row-segment items); else the block-pair
+// items of the triangular operators
+static TmvCfg tmv_cfg(const ietidp_s* h, int ncols, bool sym = false) {
   const int nt = (h->plan.max_nI + TB - 1) / TB;
   if (ncols == 1) {
+    if (sym) {
+      // row-segment items streamed through one ring (sym_stream): STAGES tiles and
+      // STAGES input buffers of SYM_SEG + 1 blocks; two stages keep two CTAs per SM
+      int st = 2;
+      if (getenv("IETIDP_STAGES1")) {
+        const int e = atoi(getenv("IETIDP_STAGES1"));
+        st = (e == 3 || e == 5) ? e : 2;
+      }
+      return {1, st, (st * TILE_ELEMS + st * (SYM_SEG + 1) * TB + TB * 16) * 8};
+    }
     // many work items: 3 stages (two CTAs per SM hide each other's barriers);
     // few (C2: 128 items): 5 stages, one deep-pipelined CTA per SM
     int st = h->n_loopwork >= 2 * 148 ? 3 : 5;
@@ -1277,7 +1491,8 @@ static TmvCfg tmv_cfg(const ietidp_s* h, int ncols) {
     if (ncp == 16 && ncols <= 8) continue;
     const int vs = ncp + 4;
     for (int stages = 3; stages >= 2; --stages) {
-      int bytes = (stages * TILE_ELEMS + nt * TB * vs + TB * vs + TB * 16) * 8;
+      int bytes = sym ? (stages * TILE_ELEMS + stages * (SYM_SEG + 1) * TB * vs + TB * 16) * 8
+                      : (stages * TILE_ELEMS + nt * TB * vs + TB * vs + TB * 16) * 8;
       if (bytes <= 210 * 1024) return {ncp, stages, bytes};
     }
   }
@@ -1294,6 +1509,9 @@ static TmvArgs sym_args(ietidp_s* h, const double* tiles, int ncols) {
   a.prim_gid = h->d_prim_gid.p;
   a.gmat = h->G.p;
   a.spart = h->spart.p;
+  a.npart = h->npart.p;
+  a.swork = h->d_symwork.p;
+  a.maxseg = h->sym_maxseg;
   a.nPmax = std::max(h->plan.nPmax, 1);
   a.ncols = ncols;
   return a;
@@ -1381,14 +1599,18 @@ void bgather(ietidp_s* h, int ncols, const double* x, const double* weight, doub
 }
 
 // z = S^-1 (add + sum of the coarse partials)
-void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const void* stv) {
+void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const void* stv, bool sym_rows = false) {
   const PcgState* st = static_cast<const PcgState*>(stv);
   if (h->n_primal == 0) return;
+  // coarse partial rows per subdomain: (subdomain, block) rows of the symmetric pass, or
+  // the block-pair items of the triangular operators
+  const int* r0 = sym_rows ? h->sub_blk0.p : h->sub_cta0.p;
+  const int* rn = sym_rows ? h->sub_nt.p : h->sub_ncta.p;
   const int smem = h->n_primal * ncols * 8;
   if (smem > 48 * 1024)
     IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   k_coarse<<<1, 1024, smem, h->stream>>>(h->n_primal, ncols, std::max(h->plan.nPmax, 1), h->pcon_ptr.p,
-                                         h->pcon_sub.p, h->pcon_q.p, h->sub_cta0.p, h->sub_ncta.p, h->gpart.p, add,
+                                         h->pcon_sub.p, h->pcon_q.p, r0, rn, h->gpart.p, add,
                                          h->Sinv.p, z, st);
   IETI_LAUNCHED(h);
 }
@@ -1397,17 +1619,18 @@ template <int NCP, int STAGES>
 static void launch_sym_t(ietidp_s* h, const TmvCfg& cfg, TmvArgs a) {
   auto kern = k_sym<NCP, STAGES>;
   IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
-  kern<<<h->n_loopwork, 256, cfg.smem, h->stream>>>(a);
+  kern<<<h->n_symwork, 256, cfg.smem, h->stream>>>(a);
   IETI_LAUNCHED(h);
 }
 
 // y = S x for the symmetric tile matrix `tiles` (explicit loop), into the slot vector a.vout
 static void sym_apply(ietidp_s* h, TmvArgs a) {
-  if (h->n_loopwork == 0) return;
-  const TmvCfg cfg = tmv_cfg(h, a.ncols);
+  if (h->n_symwork == 0) return;
+  const TmvCfg cfg = tmv_cfg(h, a.ncols, true);
   for (int c0 = 0; c0 < a.ncols; c0 += cfg.ncp) {
     a.c_off = c0;
-    if (cfg.ncp == 1 && cfg.stages == 5) launch_sym_t<1, 5>(h, cfg, a);
+    if (cfg.ncp == 1 && cfg.stages == 2) launch_sym_t<1, 2>(h, cfg, a);
+    else if (cfg.ncp == 1 && cfg.stages == 5) launch_sym_t<1, 5>(h, cfg, a);
     else if (cfg.ncp == 1) launch_sym_t<1, 3>(h, cfg, a);
     else if (cfg.ncp == 16 && cfg.stages == 3) launch_sym_t<16, 3>(h, cfg, a);
     else if (cfg.ncp == 16) launch_sym_t<16, 2>(h, cfg, a);
@@ -1431,7 +1654,7 @@ static void apply_F_inter(ietidp_s* h, int ncols, const double* x, double* y, co
     a.vout = h->xI.p;
     a.gpart = h->n_primal ? h->gpart.p : nullptr;
     sym_apply(h, a);
-    coarse_apply(h, ncols, nullptr, h->zc.p, st);
+    coarse_apply(h, ncols, nullptr, h->zc.p, st, true);
     CoarseTerm ct = coarse_term_args(h);
     k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, h->xI.p, nullptr, y, dotv, partial, st, ct);
     IETI_LAUNCHED(h);
@@ -1561,8 +1784,10 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
   if (per_sm < 1) return false;
   const int grid = std::min(nsm * per_sm, 1024);
   if (h->lpt_grid != grid) {  // items over the persistent CTAs: longest processing time first
-    std::vector<std::pair<int, int>> cost(h->n_loopwork);
-    for (int i = 0; i < h->n_loopwork; ++i) cost[i] = {h->h_loopwork[i].cost, i};
+    const bool expl = h->opt.loop == IETIDP_LOOP_EXPLICIT;  // items: row segments, or block pairs
+    const int nitems = expl ? h->n_symwork : h->n_loopwork;
+    std::vector<std::pair<int, int>> cost(nitems);
+    for (int i = 0; i < nitems; ++i) cost[i] = {expl ? h->h_symwork[i].cost : h->h_loopwork[i].cost, i};
     std::sort(cost.begin(), cost.end(), [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second < y.second); });
     std::vector<std::vector<int>> lists(grid);
     std::vector<std::pair<long long, int>> heap;
@@ -1607,8 +1832,9 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
     IETI_CUDA(cudaMemcpy(t.data(), prof.p, sizeof(unsigned long long) * std::min(n, 4096), cudaMemcpyDeviceToHost));
     n = std::min(n, 4096);
     const int ng_ = h->n_primal, nc = a.fwd.ncols ? a.fwd.ncols : h->nrhs;
-    const int per = EXPL ? 6 + (nc > 1 ? 2 : 0) + (ng_ > COARSE_LOCAL_MAX ? 1 + (nc == 1 ? 1 : 0) : 0) : 9,
-              skip = EXPL ? 4 + (nc > 1 ? 1 : 0) : 5;
+    const bool nofold = nc > 1 || !args.fold;
+    const int per = EXPL ? 6 + (nofold ? 2 : 0) + (ng_ > COARSE_LOCAL_MAX ? 1 + (nofold ? 0 : 1) : 0) : 9,
+              skip = EXPL ? 4 + (nofold ? 1 : 0) : 5;
     std::vector<double> acc(per, 0.0);
     int cnt = 0;
     for (int i = skip; i + per < n; i += per, ++cnt)
@@ -1624,7 +1850,7 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
 static bool run_solve_persistent(ietidp_s* h) {
   const int nc = h->nrhs, m = h->n_lambda;
   if (m == 0 || h->n_loopwork == 0) return false;
-  TmvCfg cfg = tmv_cfg(h, nc);
+  TmvCfg cfg = tmv_cfg(h, nc, h->opt.loop == IETIDP_LOOP_EXPLICIT);
   // the explicit loop's per-CTA coarse solve keeps g and z (2 ng nc doubles) in shared memory
   const int zbytes = 2 * h->n_primal * nc * (int)sizeof(double);
   if (h->opt.loop == IETIDP_LOOP_EXPLICIT && zbytes > cfg.smem) {
@@ -1671,6 +1897,7 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.gsrc_ptr = h->gsrc_ptr.p;
   a.gsrc = h->gsrc.p;
   a.gc = h->gc.p;
+  a.fold = !(getenv("IETIDP_FOLD") && atoi(getenv("IETIDP_FOLD")) == 0);
   a.blk = h->d_blk.p;
   a.n_blk = h->n_blk;
   a.lam = h->lam.p;
@@ -1701,10 +1928,11 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.nPmax = std::max(h->plan.nPmax, 1);
   a.max_iter = h->opt.max_iter;
   a.fixed = h->opt.fixed_iters;
-  a.n_items = h->n_loopwork;
+  a.n_items = h->opt.loop == IETIDP_LOOP_EXPLICIT ? h->n_symwork : h->n_loopwork;
   a.ncp = cfg.ncp;
   if (h->n_primal * nc * 8 > cfg.smem) return false;
   if (h->opt.loop == IETIDP_LOOP_EXPLICIT) {
+    if (cfg.ncp == 1 && cfg.stages == 2) return launch_pcg_t<1, 2, true>(h, cfg, a);
     if (cfg.ncp == 1 && cfg.stages == 5) return launch_pcg_t<1, 5, true>(h, cfg, a);
     if (cfg.ncp == 1) return launch_pcg_t<1, 3, true>(h, cfg, a);
     if (cfg.ncp == 16 && cfg.stages == 3) return launch_pcg_t<16, 3, true>(h, cfg, a);
