@@ -1190,13 +1190,24 @@ void analyze_all(ietidp_s* h) {
       }
     }
     h->slot_goff.upload(goff, s);
+    // symmetric-pass partial blocks per (subdomain, block)
+    std::vector<long long> pboff;
+    long long pbo = 0;
+    for (int k = 0; k < ns; ++k) {
+      const SubDev& d = h->h_sub[k];
+      for (int j = 0; j < d.nt; ++j) {
+        pboff.push_back(pbo);
+        pbo += (j / SYM_SEG + 1) + (d.nt - 1 - j);
+      }
+    }
+    h->d_pboff.upload(pboff, s);
+    h->n_pblocks = pbo;
     std::vector<SlotRed> sred(h->n_slots);
     for (int k = 0; k < ns; ++k) {
       const SubDev& d = h->h_sub[k];
       for (int a = 0; a < d.nI; ++a) {
         const int j = a / TB, r = a % TB;
-        sred[d.rI_off + a] = {(d.spart_off + j) * TB + r, (d.npart_off + (long long)j * h->sym_maxseg) * TB + r, j,
-                              d.nt, j / SYM_SEG + 1, 0};
+        sred[d.rI_off + a] = {pboff[d.blk0 + j] * TB + r, (j / SYM_SEG + 1) + (d.nt - 1 - j), 0};
       }
     }
     h->slot_red.upload(sred, s);
@@ -1244,8 +1255,9 @@ void analyze_all(ietidp_s* h) {
     h->wtiles.alloc(to);
     h->stiles.alloc(to);
   }
-  h->spart.alloc((size_t)std::max(spo, 1LL) * TB * nc);
-  h->npart.alloc((size_t)std::max(npo, 1LL) * TB * nc);
+  h->spart.alloc((size_t)std::max(h->n_pblocks, 1LL) * TB * nc);
+  (void)spo;
+  (void)npo;
   h->delta.alloc(h->n_slots);
   h->kdiag.alloc(h->n_slots);
   const size_t m = (size_t)h->n_lambda * nc;

@@ -164,7 +164,8 @@ struct ietidp_s {
   ieti::DevBuf<ieti::SymWork> d_symwork;     // explicit loop: symmetric-pass items
   std::vector<ieti::SymWork> h_symwork;
   int n_symwork = 0, sym_maxseg = 1;
-  ieti::DevBuf<double> npart;                // symmetric pass: N-partials per row segment
+  ieti::DevBuf<long long> d_pboff;           // symmetric pass: first partial block of each (subdomain, block)
+  long long n_pblocks = 0;
   ieti::DevBuf<int> sub_blk0, sub_nt;        // (subdomain, block) rows of each subdomain
   ieti::DevBuf<int> cta_ptr, cta_items;     // persistent PCG: work items per CTA
   int lpt_grid = 0;

@@ -53,10 +53,10 @@ struct SubDev {
   long long tile_off;          // packed L_II tiles (row-block order, TB x TB row-major)
   long long itile_off;         // packed L_II^-1 tiles (same layout; also W = S_II^-1 and S_II tiles)
   long long g_off;             // G_k = L_II^-T L_PI^T: nI x nP row-major (explicit loop)
-  long long spart_off;         // symmetric-pass partial blocks: nt(nt-1)/2 blocks of TB x ncols
+  long long spart_off;         // (unused by the symmetric pass: see SlotRed / pboff)
   int prim_off, perm_off, nt, cta0;  // primal rows, perm, #tile blocks, first loop CTA
   int blk0;             // first (subdomain, block) index: coarse partial rows of the symmetric pass
-  long long npart_off;  // symmetric pass: N-partials (nt x maxseg blocks of TB rows)
+  long long npart_off;  // (reserved)
 };
 
 // One multiplier's two B entries (every row is {+1, -1} in two subdomains).
@@ -92,14 +92,14 @@ struct GemmWork {
   long long ws_off;
 };
 
-// Per r_I slot: where the symmetric pass left its partial sums (folded into the gather
-// or reduced), in this fixed order:
-//   y[slot] = sum_{s < nseg} npart[(nbase + s TB) ncols + c]
-//           + sum_{i = j+1}^{nt-1} spart[(base + i (i-1)/2 TB) ncols + c].
+// The symmetric pass leaves, for every (subdomain, block j), cnt_j = nseg_j + (nt-1-j)
+// partial blocks (TB rows x ncols) stored contiguously from pboff[blk0 + j]: first the
+// row-segment products of block row j (nseg_j = j / SYM_SEG + 1), then the transposed
+// products of the tiles (i, j), i = j+1 .. nt-1. Per r_I slot (row r of block j):
+//   y[slot][c] = sum_{p < cnt} spart[(base + p TB) ncols + c],  base = pboff_j TB + r.
 struct SlotRed {
-  long long base;   // (spart_off + j) TB + r
-  long long nbase;  // (npart_off + j maxseg) TB + r
-  int j, nt, nseg, pad_;
+  long long base;
+  int cnt, pad_;
 };
 
 // A work item of the symmetric tile passes (explicit loop): tiles (o, j0..j1) of the

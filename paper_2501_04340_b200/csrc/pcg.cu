@@ -71,7 +71,7 @@ struct TmvArgs {
   double* gpart;           // FWD/SYM: coarse partials [cta][nPmax][ncols] (nullable)
   const double* gmat;      // SYM: G_k (n_I x n_P row-major) for the coarse partials
   double* spart;           // SYM: partial blocks of the transposed tile products
-  double* npart;           // SYM: partial row products per row segment
+  const long long* pboff;  // SYM: first partial block of each (subdomain, block) (SlotRed)
   const SymWork* swork;    // SYM: work items (row segments)
   int maxseg;              // SYM: segments per block row (npart layout)
   int slot_in;             // FWD/PRE1/SYM: vin is already in slot order (B^T, weights applied)
@@ -430,7 +430,7 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
     const int j = j0 + st;
     const bool diag = (j == o);
     const double* xj = vec + st * TB * VS;
-    double* pblk = A.spart + ((d.spart_off + (long long)o * (o - 1) / 2 + j) * TB) * A.ncols + A.c_off;
+    double* pblk = A.spart + ((A.pboff[d.blk0 + j] + j / SYM_SEG + o - j) * TB) * A.ncols + A.c_off;
     if constexpr (NCP == 1) {
       {  // N: y_o += S_oj x_j
         const double x0 = xj[lane], x1 = xj[lane + 32];
@@ -480,7 +480,7 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
       }
     }
   }
-  double* nb_out = A.npart + ((d.npart_off + (long long)o * A.maxseg + sw.seg) * TB) * A.ncols + A.c_off;
+  double* nb_out = A.spart + ((A.pboff[d.blk0 + o] + sw.seg) * TB) * A.ncols + A.c_off;
   if constexpr (NCP == 1) {
     __syncthreads();
     if (pend && tid < TB) {
@@ -604,12 +604,13 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
         }
         pend = nullptr;
       }
+      const int j = j0 + st;
+      const long long pbj = __ldg(A.pboff + d.blk0 + j);  // before the issue: latency hidden
       issue((gt + STAGES - 1) % STAGES);
       const double* Tt = ring + (gt % STAGES) * TILE_ELEMS;
-      const int j = j0 + st;
       const bool diag = (j == o);
       const double* xj = vec + st * TB * VS;
-      double* pblk = A.spart + ((d.spart_off + (long long)o * (o - 1) / 2 + j) * TB) * A.ncols + A.c_off;
+      double* pblk = A.spart + ((pbj + j / SYM_SEG + o - j) * TB) * A.ncols + A.c_off;
       if constexpr (NCP == 1) {
         {
           const double x0 = xj[lane], x1 = xj[lane + 32];
@@ -661,7 +662,7 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
       }
     }
     // item done: its row-segment partial and coarse partial
-    double* nb_out = A.npart + ((d.npart_off + (long long)o * A.maxseg + sw.seg) * TB) * A.ncols + A.c_off;
+    double* nb_out = A.spart + ((A.pboff[d.blk0 + o] + sw.seg) * TB) * A.ncols + A.c_off;
     if constexpr (NCP == 1) {
       double full[8];
 #pragma unroll
@@ -705,16 +706,15 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
 __device__ __forceinline__ void sym_reduce_item(const TmvArgs& A, int k, int j) {
   const SubDev d = A.sub[k];
   const int nc = A.ncols;
-  const int nseg = j / SYM_SEG + 1;
+  const int cnt = (j / SYM_SEG + 1) + (d.nt - 1 - j);
+  const double* P0 = A.spart + A.pboff[d.blk0 + j] * TB * nc;
   for (int e = threadIdx.x; e < TB * nc; e += 256) {
     const int r = e / nc, c = e - r * nc;
     const int a = j * TB + r;
     if (a >= d.nI) continue;
     double v = 0.0;
-    for (int sg = 0; sg < nseg; ++sg) v += A.npart[((d.npart_off + (long long)j * A.maxseg + sg) * TB + r) * nc + c];
-    double t = 0.0;
-    for (int i = j + 1; i < d.nt; ++i) t += A.spart[((d.spart_off + (long long)i * (i - 1) / 2 + j) * TB + r) * nc + c];
-    A.vout[(d.rI_off + a) * nc + c] = v + t;
+    for (int p = 0; p < cnt; ++p) v += P0[((long long)p * TB + r) * nc + c];
+    A.vout[(d.rI_off + a) * nc + c] = v;
   }
 }
 
@@ -1055,6 +1055,7 @@ struct PcgArgs {
   const int *gsrc_ptr, *gsrc;      // coarse partial rows per global primal
   double* gc;                      // coarse right-hand side g (larger coarse problems)
   int fold;                        // one column: fold the symmetric partials into the gathers
+  long long n_slots;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1120,10 +1121,28 @@ __device__ __forceinline__ void sym_phase(TmvArgs A, const int* cta_ptr, const i
   }
 }
 
-__device__ __forceinline__ void reduce_phase(const TmvArgs& A, const int2* blk, int n_blk) {
-  for (int it = blockIdx.x; it < n_blk; it += gridDim.x) {
-    const int2 kb = blk[it];
-    sym_reduce_item(A, kb.x, kb.y);
+__device__ __forceinline__ double sym_value(const double* spart, const SlotRed* sred, long long a, int nc, int c);
+
+// y = the reduced symmetric pass, element-parallel over (slot, column) (same order as
+// sym_value / sym_reduce_item)
+__device__ __forceinline__ void reduce_phase(const TmvArgs& A, const SlotRed* sred, long long n_slots) {
+  const long long n = n_slots * A.ncols;
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  // four independent elements per thread in flight (memory-level parallelism)
+  for (long long e0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += 4 * stride) {
+    double v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const long long e = e0 + u * stride;
+      v[u] = 0.0;
+      if (e < n) {
+        const long long a = e / A.ncols;
+        v[u] = sym_value(A.spart, sred, a, A.ncols, (int)(e - a * A.ncols));
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u)
+      if (e0 + u * stride < n) A.vout[e0 + u * stride] = v[u];
   }
 }
 
@@ -1205,14 +1224,19 @@ __device__ __forceinline__ void coarse_spread_z(const PcgArgs& P) {
 
 // y[slot][c] of a symmetric pass: the row-segment partials plus the transposed partials
 // (the same fixed order as sym_reduce_item)
-__device__ __forceinline__ double sym_value(const double* npart, const double* spart, const SlotRed* sred, long long a,
-                                            int nc, int c) {
+__device__ __forceinline__ double sym_value(const double* spart, const SlotRed* sred, long long a, int nc, int c) {
   const SlotRed sr = sred[a];
-  double v = 0.0;
-  for (int sg = 0; sg < sr.nseg; ++sg) v += npart[(sr.nbase + (long long)sg * TB) * nc + c];
-  double t = 0.0;
-  for (int i = sr.j + 1; i < sr.nt; ++i) t += spart[(sr.base + (long long)(i * (i - 1) / 2) * TB) * nc + c];
-  return v + t;
+  const double* P0 = spart + sr.base * nc + c;
+  const long long st = (long long)TB * nc;
+  double v0 = 0.0;
+  int p = 0;
+  // the partials in order; four loads in flight (the additions stay in order)
+  for (; p + 4 <= sr.cnt; p += 4) {
+    const double a0 = P0[p * st], a1 = P0[(p + 1) * st], a2 = P0[(p + 2) * st], a3 = P0[(p + 3) * st];
+    v0 = (((v0 + a0) + a1) + a2) + a3;
+  }
+  for (; p < sr.cnt; ++p) v0 += P0[p * st];
+  return v0;
 }
 
 // out = sum_k B (w) (x + G z), with the per-CTA partial of out . dotv
@@ -1229,7 +1253,7 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
 #pragma unroll
       for (int q = 0; q < 2; ++q) {
         const int a = L.slot[q];
-        double xv = fold ? sym_value(fold->npart, fold->spart, P.slot_red, a, nc, c) : x[(long long)a * nc + c];
+        double xv = fold ? sym_value(fold->spart, P.slot_red, a, nc, c) : x[(long long)a * nc + c];
         if (coarse) {
           if (zs) {  // G_k[slot row] . z (z in shared memory)
             const int np = P.ct.np[a];
@@ -1279,7 +1303,7 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     // one column: the partial sums are folded into the gather; several: a reduction
     // phase (a slot shared by several multipliers would be summed repeatedly)
     const bool fold = P.ncols == 1 && P.fold;
-    if (!fold) reduce_phase(P.wsym, P.blk, P.n_blk);
+    if (!fold) reduce_phase(P.wsym, P.slot_red, P.n_slots);
     if (P.ng > 0 && P.ng <= COARSE_LOCAL_MAX) {
       if (!fold) pcg_barrier(P);
       coarse_local(P, smem);  // small coarse problem: every CTA solves it (no barrier)
@@ -1314,7 +1338,7 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
     if (P.ncols == 1 && P.fold) {
       bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, &P.ssym);
     } else {
-      reduce_phase(P.ssym, P.blk, P.n_blk);
+      reduce_phase(P.ssym, P.slot_red, P.n_slots);
       pcg_barrier(P);
       bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false);
     }
@@ -1509,7 +1533,7 @@ static TmvArgs sym_args(ietidp_s* h, const double* tiles, int ncols) {
   a.prim_gid = h->d_prim_gid.p;
   a.gmat = h->G.p;
   a.spart = h->spart.p;
-  a.npart = h->npart.p;
+  a.pboff = h->d_pboff.p;
   a.swork = h->d_symwork.p;
   a.maxseg = h->sym_maxseg;
   a.nPmax = std::max(h->plan.nPmax, 1);
@@ -1897,6 +1921,7 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.gsrc_ptr = h->gsrc_ptr.p;
   a.gsrc = h->gsrc.p;
   a.gc = h->gc.p;
+  a.n_slots = h->n_slots;
   a.fold = !(getenv("IETIDP_FOLD") && atoi(getenv("IETIDP_FOLD")) == 0);
   a.blk = h->d_blk.p;
   a.n_blk = h->n_blk;
