@@ -890,9 +890,12 @@ void analyze_all(ietidp_s* h) {
   P.roots_by_level.assign(P.max_level + 1, {});
   for (int k = 0; k < ns; ++k)
     if (h->h_sub[k].root >= 0) P.roots_by_level[P.sn[h->h_sub[k].root].level].push_back(k);
-  // W_k = L_II^-T L_II^-1 accumulated block row by block row of L_II^-1 as the r_I
-  // root's panels complete: W[i][j] += L11^-1[kp][i]^T L11^-1[kp][j], j <= i <= kp,
-  // written into the loop's row-major lower tiles (zeroed before the factorisation)
+  // W_k = L_II^-T L_II^-1 accumulated from groups of W_GROUP block rows of L_II^-1 as
+  // the r_I root's panels complete: after the group [k0, kp], W[i][j] += sum over
+  // the group's rows k >= i of L11^-1[k][i]^T L11^-1[k][j], j <= i <= kp, written into
+  // the loop's row-major lower tiles (zeroed before the factorisation). Groups keep
+  // the read-modify-write traffic of the tiles W_GROUP times below per-row updates.
+  constexpr int W_GROUP = 4;
   for (int L = 0; L <= P.max_level; ++L)
     for (int kp = 0; kp < (int)P.levels[L].panels.size(); ++kp) {
       LevelPlan::Panel& pn = P.levels[L].panels[kp];
@@ -901,19 +904,21 @@ void analyze_all(ietidp_s* h) {
       for (int k : P.roots_by_level[L]) {
         const SubDev& d = h->h_sub[k];
         if (kp >= d.nt) continue;
+        if ((kp + 1) % W_GROUP != 0 && kp != d.nt - 1) continue;  // not the end of a group
+        const int k0 = kp / W_GROUP * W_GROUP;
         const SnDev& r = sd[d.root];
-        const int p0 = kp * TB, b = std::min(TB, d.nI - p0);
         for (int i = 0; i <= kp; ++i)
           for (int j = 0; j <= i; ++j, ++pn.wacc_n) {
+            const int ks = std::max(i, k0);  // L11^-1[k][i] = 0 for k < i
             GemmWork g{};
             g.c_off = d.tile_off + (long long)(i * (i + 1) / 2 + j) * TILE_ELEMS;
-            g.a_off = r.inv_off + (long long)(i * TB) * r.ldi + p0;  // A[rr][m] = Linv[p0 + m][iTB + rr]
-            g.b_off = r.inv_off + (long long)(j * TB) * r.ldi + p0;  // B[m][c] = Linv[p0 + m][jTB + c]
+            g.a_off = r.inv_off + (long long)(i * TB) * r.ldi + ks * TB;  // A[rr][m] = Linv[ksTB + m][iTB + rr]
+            g.b_off = r.inv_off + (long long)(j * TB) * r.ldi + ks * TB;  // B[m][c] = Linv[ksTB + m][jTB + c]
             g.lda = g.ldb = r.ldi;
             g.ldc = TB;
             g.m = std::min(TB, d.nI - i * TB);
             g.n = std::min(TB, d.nI - j * TB);
-            g.kdim = b;
+            g.kdim = std::min(d.nI, (kp + 1) * TB) - ks * TB;
             g.mode = 16 | 2;  // accumulate into the row-major tile
             g.diag = (i == j);
             gwork.push_back(g);

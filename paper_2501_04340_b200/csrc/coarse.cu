@@ -33,6 +33,33 @@ __global__ void k_scatter(long long n, const long long* __restrict__ dst, const 
 // triangle lives packed in shared memory (n(n+1)/2 doubles).
 __device__ __forceinline__ int pk(int i, int j) { return i * (i + 1) / 2 + j; }
 
+// S_PP = sum_k C_k^T S_loc^(k) C_k from the P fronts, and ftilde = sum_k C_k^T ftilde^(k):
+// element-parallel over all CTAs (the gathers), ahead of the one-CTA factorisation
+__global__ void __launch_bounds__(256)
+    k_coarse_assemble(int n, int nrhs, const int* __restrict__ scoef_ptr, const long long* __restrict__ scoef_src,
+                      const double* __restrict__ pool, const int* __restrict__ pcon_ptr,
+                      const int* __restrict__ pcon_sub, const int* __restrict__ pcon_q,
+                      const SubDev* __restrict__ sub, const double* __restrict__ Xf, double* __restrict__ S,
+                      double* __restrict__ ftil) {
+  const long long tot = (long long)n * n + (long long)n * nrhs;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (long long)gridDim.x * blockDim.x) {
+    if (e < (long long)n * n) {
+      double s = 0.0;
+      for (int q = scoef_ptr[e]; q < scoef_ptr[e + 1]; ++q) s += pool[scoef_src[q]];
+      S[e] = s;
+    } else {
+      const long long f = e - (long long)n * n;
+      const int g = (int)(f / nrhs), c = (int)(f - (long long)g * nrhs);
+      double s = 0.0;
+      for (int q = pcon_ptr[g]; q < pcon_ptr[g + 1]; ++q) {
+        const SubDev& d = sub[pcon_sub[q]];
+        s += Xf[(d.x_off + d.nr + pcon_q[q]) * nrhs + c];
+      }
+      ftil[f] = s;
+    }
+  }
+}
+
 __global__ void __launch_bounds__(1024)
     k_coarse_factor(int n, int nrhs, const int* __restrict__ scoef_ptr, const long long* __restrict__ scoef_src,
                     const double* __restrict__ pool, const int* __restrict__ pcon_ptr,
@@ -40,24 +67,18 @@ __global__ void __launch_bounds__(1024)
                     const double* __restrict__ Xf, double* __restrict__ S, double* __restrict__ Sinv,
                     double* __restrict__ ftil, double* __restrict__ zc0, int* __restrict__ err) {
   extern __shared__ double Lp[];  // n(n+1)/2
-  __shared__ double tmp[1024];
+  __shared__ double tmp[1024], tsc[1024];
   __shared__ int bad;
   const int tid = threadIdx.x;
   if (tid == 0) bad = 0;
-  for (int e = tid; e < n * n; e += blockDim.x) {
-    double s = 0.0;
-    for (int q = scoef_ptr[e]; q < scoef_ptr[e + 1]; ++q) s += pool[scoef_src[q]];
-    S[e] = s;
-  }
-  for (int e = tid; e < n * nrhs; e += blockDim.x) {
-    const int g = e / nrhs, c = e - g * nrhs;
-    double s = 0.0;
-    for (int q = pcon_ptr[g]; q < pcon_ptr[g + 1]; ++q) {
-      const SubDev& d = sub[pcon_sub[q]];
-      s += Xf[(d.x_off + d.nr + pcon_q[q]) * nrhs + c];
-    }
-    ftil[e] = s;
-  }
+  (void)scoef_ptr;
+  (void)scoef_src;
+  (void)pool;
+  (void)pcon_ptr;
+  (void)pcon_sub;
+  (void)pcon_q;
+  (void)sub;
+  (void)Xf;
   __syncthreads();
   for (int e = tid; e < n * (n + 1) / 2; e += blockDim.x) {
     int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
@@ -67,53 +88,55 @@ __global__ void __launch_bounds__(1024)
     Lp[e] = 0.5 * (S[i * n + j] + S[j * n + i]);
   }
   __syncthreads();
-  // Cholesky (right-looking)
-  for (int j = 0; j < n; ++j) {
-    if (tid == 0) {
-      double dd = Lp[pk(j, j)];
-      if (!(dd > 0.0)) {
-        bad = 1;
-        dd = 1.0;
-      }
-      Lp[pk(j, j)] = sqrt(dd);
+  // S_PP^-1 by the symmetric sweep operator (Gauss-Jordan without pivoting on the SPD
+  // matrix, packed lower storage): sweeping pivot k maps
+  //   a_kk -> -1/a_kk,  a_ik -> a_ik / a_kk,  a_ij -> a_ij - a_ik a_jk / a_kk  (i, j != k);
+  // after all n pivots the matrix holds -S^-1. The pivots are the Schur-complement
+  // diagonals: one that is not positive means S_PP is not SPD. Two barriers per pivot.
+  constexpr int EPT = 32;  // packed entries per thread (n <= 255)
+  int pij[EPT];  // (i << 16) | j of this thread's packed entries, -1 past the end
+  const int ne = n * (n + 1) / 2;
+#pragma unroll
+  for (int m = 0; m < EPT; ++m) {
+    const int e = tid + m * 1024;
+    pij[m] = -1;
+    if (e < ne) {
+      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (pk(i, 0) > e) --i;
+      while (pk(i + 1, 0) <= e) ++i;
+      pij[m] = (i << 16) | (e - pk(i, 0));
+    }
+  }
+  for (int k = 0; k < n; ++k) {
+    double akk = Lp[pk(k, k)];
+    if (!(akk > 0.0)) {
+      if (tid == 0) bad = 1;
+      akk = 1.0;
+    }
+    const double inv = 1.0 / akk;
+    // column k of the current matrix (0 at k itself) and its scaled copy
+    for (int i = tid; i < n; i += blockDim.x) {
+      const double t = (i == k) ? 0.0 : Lp[i > k ? pk(i, k) : pk(k, i)];
+      tmp[i] = t;
+      tsc[i] = t * inv;
     }
     __syncthreads();
-    const double inv = 1.0 / Lp[pk(j, j)];
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) Lp[pk(i, j)] *= inv;
-    __syncthreads();
-    for (int i = j + 1 + (tid >> 3); i < n; i += (blockDim.x >> 3)) {
-      const double lij = Lp[pk(i, j)];
-      for (int c = j + 1 + (tid & 7); c <= i; c += 8) Lp[pk(i, c)] -= lij * Lp[pk(c, j)];
+    // a_ij -= (a_ik / a_kk) a_jk for every entry (row / column k unchanged: t_k = 0)
+#pragma unroll
+    for (int m = 0; m < EPT; ++m) {
+      if (pij[m] < 0) continue;
+      const int e = tid + m * 1024;
+      Lp[e] = fma(-tsc[pij[m] >> 16], tmp[pij[m] & 0xffff], Lp[e]);
     }
+    __syncthreads();
+    // then row / column k: a_ik / a_kk, and -1 / a_kk on the diagonal
+    for (int i = tid; i < n; i += blockDim.x) Lp[i > k ? pk(i, k) : pk(k, i)] = (i == k) ? -inv : tsc[i];
     __syncthreads();
   }
   if (tid == 0 && bad) atomicMin(err + 1, 0);
-  // in-place inverse of the lower factor (LAPACK trti2, lower, backward)
-  for (int j = n - 1; j >= 0; --j) {
-    if (tid == 0) Lp[pk(j, j)] = 1.0 / Lp[pk(j, j)];
-    __syncthreads();
-    const double ajj = -Lp[pk(j, j)];
-    for (int i = j + 1 + tid; i < n; i += blockDim.x) tmp[i] = Lp[pk(i, j)];
-    __syncthreads();
-    // X[i][j] = ajj * sum_{m=j+1}^{i} Xinv[i][m] tmp[m]
-    for (int base = j + 1; base < n; base += (blockDim.x >> 3)) {  // warp-uniform trip count
-      const int i = base + (tid >> 3);
-      double s = 0.0;
-      if (i < n)
-        for (int m = j + 1 + (tid & 7); m <= i; m += 8) s += Lp[pk(i, m)] * tmp[m];
-      s += __shfl_xor_sync(0xffffffffu, s, 1);
-      s += __shfl_xor_sync(0xffffffffu, s, 2);
-      s += __shfl_xor_sync(0xffffffffu, s, 4);
-      if (i < n && (tid & 7) == 0) Lp[pk(i, j)] = ajj * s;
-    }
-    __syncthreads();
-  }
-  // S^-1 = X^T X, X = L^-1 lower: Sinv[i][j] = sum_{m >= max(i,j)} X[m][i] X[m][j]
   for (int e = tid; e < n * n; e += blockDim.x) {
     const int i = e / n, j = e - i * n;
-    double s = 0.0;
-    for (int m = max(i, j); m < n; ++m) s += Lp[pk(m, i)] * Lp[pk(m, j)];
-    Sinv[e] = s;
+    Sinv[e] = -Lp[i >= j ? pk(i, j) : pk(j, i)];
   }
   __syncthreads();
   for (int e = tid; e < n * nrhs; e += blockDim.x) {
@@ -269,6 +292,10 @@ void run_coarse(ietidp_s* h) {
     const int smem = ng * (ng + 1) / 2 * sizeof(double);
     if (smem > 220 * 1024) throw Error(IETIDP_E_ARG, "coarse problem too large for the one-CTA coarse factorisation");
     IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_coarse_assemble<<<grid_for((long long)ng * (ng + nrhs), 256), 256, 0, s>>>(
+        ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p, h->pcon_sub.p, h->pcon_q.p, h->d_sub.p,
+        h->Xf.p, h->S.p, h->ftil.p);
+    IETI_LAUNCHED(h);
     k_coarse_factor<<<1, 1024, smem, s>>>(ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p,
                                           h->pcon_sub.p, h->pcon_q.p, h->d_sub.p, h->Xf.p, h->S.p, h->Sinv.p,
                                           h->ftil.p, h->zc0.p, h->err_flag.p);
