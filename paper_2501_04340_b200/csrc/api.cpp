@@ -233,21 +233,51 @@ ietidp_status ietidp_factor(ietidp_t h) {
       IETI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
       IETI_CUDA(cudaStreamCreateWithPriority(&h->hp, cudaStreamNonBlocking, hi));
       IETI_CUDA(cudaEventCreateWithFlags(&h->hp_ev, cudaEventDisableTiming));
+      for (auto& e : h->fg_ev) IETI_CUDA(cudaEventCreate(&e));
     }
     cudaStream_t user = h->stream;
     IETI_CUDA(cudaEventRecord(h->hp_ev, user));
     IETI_CUDA(cudaStreamWaitEvent(h->hp, h->hp_ev, 0));
     h->stream = h->hp;
     EvPair e1, e2;
+    // The ~200 launches of the factorisation and coarse set-up (two streams, events)
+    // are captured once into a CUDA graph and replayed: the plan and buffers are fixed
+    // after analyze, so every factor call launches the same work. Not with the launch
+    // tracer; IETIDP_GRAPH=0 launches directly.
+    const bool use_graph = !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
     try {
-      IETI_CUDA(cudaEventRecord(e1.a, h->stream));
-      h->trace.start(h->stream);
-      ieti::run_factor(h);
-      IETI_CUDA(cudaEventRecord(e1.b, h->stream));
-      IETI_CUDA(cudaEventRecord(e2.a, h->stream));
-      ieti::run_coarse(h);
-      IETI_CUDA(cudaEventRecord(e2.b, h->stream));
+      if (use_graph && !h->fgraph) {
+        const long long l0 = h->launches;
+        cudaGraph_t g = nullptr;
+        IETI_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+        IETI_CUDA(cudaEventRecordWithFlags(h->fg_ev[0], h->stream, cudaEventRecordExternal));
+        ieti::run_factor(h);
+        IETI_CUDA(cudaEventRecordWithFlags(h->fg_ev[1], h->stream, cudaEventRecordExternal));
+        ieti::run_coarse(h);
+        IETI_CUDA(cudaEventRecordWithFlags(h->fg_ev[2], h->stream, cudaEventRecordExternal));
+        IETI_CUDA(cudaStreamEndCapture(h->stream, &g));
+        IETI_CUDA(cudaGraphInstantiate(&h->fgraph, g, 0));
+        cudaGraphDestroy(g);
+        h->fgraph_launches = h->launches - l0;
+        h->launches = l0;
+      }
+      if (use_graph) {
+        IETI_CUDA(cudaGraphLaunch(h->fgraph, h->stream));
+        h->launches += h->fgraph_launches;
+      } else {
+        IETI_CUDA(cudaEventRecord(h->fg_ev[0], h->stream));
+        h->trace.start(h->stream);
+        ieti::run_factor(h);
+        IETI_CUDA(cudaEventRecord(h->fg_ev[1], h->stream));
+        ieti::run_coarse(h);
+        IETI_CUDA(cudaEventRecord(h->fg_ev[2], h->stream));
+      }
     } catch (...) {
+      if (h->fgraph == nullptr) {
+        cudaGraph_t g = nullptr;
+        cudaStreamEndCapture(h->stream, &g);  // abandon a failed capture
+        if (g) cudaGraphDestroy(g);
+      }
       h->stream = user;
       throw;
     }
@@ -258,8 +288,15 @@ ietidp_status ietidp_factor(ietidp_t h) {
     IETI_CUDA(cudaMemcpyAsync(flags, h->err_flag.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, h->stream));
     IETI_CUDA(cudaStreamSynchronize(h->stream));
     h->trace.dump("factor");
-    h->rep.ms_factor = e1.ms();
-    h->rep.ms_coarse = e2.ms();
+    {
+      float t1 = 0.f, t2 = 0.f;
+      cudaEventElapsedTime(&t1, h->fg_ev[0], h->fg_ev[1]);
+      cudaEventElapsedTime(&t2, h->fg_ev[1], h->fg_ev[2]);
+      h->rep.ms_factor = t1;
+      h->rep.ms_coarse = t2;
+    }
+    (void)e1;
+    (void)e2;
     if (flags[0] != INT_MAX) {
       h->failed_sub = flags[0];
       h->rep.failed_subdomain = flags[0];
@@ -417,6 +454,9 @@ void ietidp_destroy(ietidp_t h) {
   for (auto e : h->fev) cudaEventDestroy(e);
   for (auto e : h->pev) cudaEventDestroy(e);
   if (h->hp_ev) cudaEventDestroy(h->hp_ev);
+  for (auto e : h->fg_ev)
+    if (e) cudaEventDestroy(e);
+  if (h->fgraph) cudaGraphExecDestroy(h->fgraph);
   if (h->hp) cudaStreamDestroy(h->hp);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

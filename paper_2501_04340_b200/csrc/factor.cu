@@ -28,6 +28,13 @@ __global__ void k_scatter(long long n, const long long* __restrict__ dst, const 
     out[dst[i]] = vals[src[i]];
 }
 
+__global__ void k_init_flags(int* err) {
+  if (threadIdx.x == 0) {
+    err[0] = INT_MAX;
+    err[1] = 1;
+  }
+}
+
 // Zero the lower trapezoid of columns [64 w.a, 64 w.a + 64) of front w.sn (rows c..f-1
 // of column c): the only part of a front any kernel reads.
 __global__ void __launch_bounds__(256) k_zero_fronts(const Work* __restrict__ work, const SnDev* __restrict__ sn,
@@ -628,8 +635,8 @@ void run_factor(ietidp_s* h) {
     set_smem((const void*)k_gemm<true, true>, GEMM_SMEM);
     attr = true;
   }
-  static const int init_flags[2] = {INT_MAX, 1};  // failing subdomain (min), coarse OK
-  IETI_CUDA(cudaMemcpyAsync(h->err_flag.p, init_flags, 2 * sizeof(int), cudaMemcpyHostToDevice, st));
+  k_init_flags<<<1, 32, 0, st>>>(h->err_flag.p);  // failing subdomain (min), coarse OK
+  IETI_LAUNCHED(h);
   const Work* W = reinterpret_cast<const Work*>(h->d_work.p);
   const GemmWork* GW = h->d_gwork.p;
   double* pool = h->pool.p;

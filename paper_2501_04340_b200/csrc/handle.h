@@ -107,6 +107,9 @@ struct ietidp_s {
   bool own_stream = false;
   cudaStream_t hp = nullptr;     // highest-priority stream of the factorisation's critical path
   cudaEvent_t hp_ev = nullptr;
+  cudaGraphExec_t fgraph = nullptr;  // captured factorisation + coarse set-up
+  long long fgraph_launches = 0;
+  cudaEvent_t fg_ev[3] = {nullptr, nullptr, nullptr};
   // side stream of the factorisation (partitioned inverse, W_k) and its events
   cudaStream_t side = nullptr;
   std::vector<cudaEvent_t> fev;  // [0..levels): level's panels done; [levels]: side done
