@@ -324,7 +324,31 @@ ietidp_status ietidp_solve(ietidp_t h, double* lambda, ietidp_report* report) {
     ieti::run_solve(h);
     IETI_CUDA(cudaEventRecord(e1.b, h->stream));
     IETI_CUDA(cudaEventRecord(e2.a, h->stream));
-    ieti::run_recover(h);
+    // the recovery's ~40 launches (backward sweep level by level) as a captured graph
+    const bool use_graph = !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
+    if (use_graph) {
+      if (!h->rgraph) {
+        const long long l0 = h->launches;
+        cudaGraph_t g = nullptr;
+        IETI_CUDA(cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeRelaxed));
+        try {
+          ieti::run_recover(h);
+        } catch (...) {
+          cudaStreamEndCapture(h->stream, &g);
+          if (g) cudaGraphDestroy(g);
+          throw;
+        }
+        IETI_CUDA(cudaStreamEndCapture(h->stream, &g));
+        IETI_CUDA(cudaGraphInstantiate(&h->rgraph, g, 0));
+        cudaGraphDestroy(g);
+        h->rgraph_launches = h->launches - l0;
+        h->launches = l0;
+      }
+      IETI_CUDA(cudaGraphLaunch(h->rgraph, h->stream));
+      h->launches += h->rgraph_launches;
+    } else {
+      ieti::run_recover(h);
+    }
     IETI_CUDA(cudaEventRecord(e2.b, h->stream));
     ieti::finish_solve(h, &h->rep);
     h->trace.dump("solve");
@@ -457,6 +481,7 @@ void ietidp_destroy(ietidp_t h) {
   for (auto e : h->fg_ev)
     if (e) cudaEventDestroy(e);
   if (h->fgraph) cudaGraphExecDestroy(h->fgraph);
+  if (h->rgraph) cudaGraphExecDestroy(h->rgraph);
   if (h->hp) cudaStreamDestroy(h->hp);
   if (h->side) cudaStreamDestroy(h->side);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);

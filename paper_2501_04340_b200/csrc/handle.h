@@ -109,6 +109,8 @@ struct ietidp_s {
   cudaEvent_t hp_ev = nullptr;
   cudaGraphExec_t fgraph = nullptr;  // captured factorisation + coarse set-up
   long long fgraph_launches = 0;
+  cudaGraphExec_t rgraph = nullptr;  // captured recovery
+  long long rgraph_launches = 0;
   cudaEvent_t fg_ev[3] = {nullptr, nullptr, nullptr};
   // side stream of the factorisation (partitioned inverse, W_k) and its events
   cudaStream_t side = nullptr;
