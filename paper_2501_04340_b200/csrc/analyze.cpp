@@ -687,6 +687,9 @@ void analyze_all(ietidp_s* h) {
               g.n = std::min(TB, s.f - c0);
               g.kdim = s.npiv;
               g.mode = 4 | 1;  // extend-add of C - A B
+              // no children: the update block F22 received nothing (K entries go to the
+              // front owning their first position), so C is zero and not read
+              if (s.children.empty()) g.mode |= 32;
               g.diag = (r0 == c0);
               g.p_off = pd.front_off;
               g.p_ld = pd.ld;
@@ -700,8 +703,13 @@ void analyze_all(ietidp_s* h) {
     }
     // assembly: zero the lower trapezoid of every front of this level (coarse node too)
     lp.zr_off = (int)work.size() / 3;
-    for (int i : bylev[L])
-      for (int t = 0; t < tiles_of(P.sn[i].f); ++t, ++lp.zr_n) push(i, t, 0);
+    for (int i : bylev[L]) {
+      // a childless front's update block is never read (its SYRK treats it as zero):
+      // zero only its pivot columns
+      const bool leaf = P.sn[i].children.empty() && !P.sn[i].coarse;
+      const int ncol = leaf ? P.sn[i].npiv : P.sn[i].f;
+      for (int t = 0; t < tiles_of(ncol); ++t, ++lp.zr_n) push(i, t, leaf ? 1 : 0);
+    }
     // sweeps
     lp.fs_off = (int)work.size() / 3;
     for (int i : bylev[L])

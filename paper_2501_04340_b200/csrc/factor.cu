@@ -41,7 +41,7 @@ __global__ void __launch_bounds__(256) k_zero_fronts(const Work* __restrict__ wo
                                                      double* __restrict__ pool) {
   const Work w = work[blockIdx.x];
   const SnDev s = sn[w.sn];
-  const int c0 = w.a * TB, c1 = min(s.f, c0 + TB);
+  const int c0 = w.a * TB, c1 = min(w.b ? s.npiv : s.f, c0 + TB);  // w.b: pivot columns only
   double* F = pool + s.front_off;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c = c0 + warp; c < c1; c += 8)
@@ -508,6 +508,7 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
     const int pr0 = ok0 ? __ldg(rr + r0) : 0, pr1 = ok1 ? __ldg(rr + r0 + 1) : 0;
     const double* Cc = Cb + w.c_off + r0;
     double* Pb = Cb + w.p_off;
+    const bool noC = (w.mode & 32) != 0;  // the child's update block is zero (no children)
     constexpr int U = 4;  // columns in flight per warp
     for (int c0 = warp; c0 < w.n; c0 += 4 * U) {
       double cv[U][2], pv[U][2];
@@ -524,8 +525,8 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
 #pragma unroll
       for (int u = 0; u < U; ++u) {
         const int c = c0 + 4 * u;
-        cv[u][0] = v0[u] ? Cc[(long long)c * w.ldc] : 0.0;
-        cv[u][1] = v1[u] ? Cc[(long long)c * w.ldc + 1] : 0.0;
+        cv[u][0] = (v0[u] && !noC) ? Cc[(long long)c * w.ldc] : 0.0;
+        cv[u][1] = (v1[u] && !noC) ? Cc[(long long)c * w.ldc + 1] : 0.0;
         pv[u][0] = v0[u] ? Pb[po[u] + pr0] : 0.0;
         pv[u][1] = v1[u] ? Pb[po[u] + pr1] : 0.0;
       }

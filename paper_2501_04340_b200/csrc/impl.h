@@ -79,7 +79,8 @@ struct GemmWork {
   int lda, ldb, ldc, m, n, kdim;
   int mode;  // bit0: negate, bit1: accumulate into C, bit2: extend-add epilogue (below),
              // bit3: split-K part (below), bit4: C is a row-major TB x TB tile at c_off
-             // (zero padded; with diag, the upper part mirrors the lower)
+             // (zero padded; with diag, the upper part mirrors the lower), bit5: extend-add
+             // with C = 0 (a childless front's update block: not read)
   int diag;  // extend-add: the tile is on the diagonal of U (add only r >= c)
   // extend-add epilogue (multifrontal update of the parent, fused into the SYRK):
   //   parent[p_off + rel[rel_c + c] * p_ld + rel[rel_r + r]] += C[r][c] - (A B)[r][c]
