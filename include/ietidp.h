@@ -80,7 +80,9 @@ typedef enum {
 
 typedef enum {
   IETIDP_ORDER_NESTED_DISSECTION = 0, /* default: nested dissection of r_V, r_I last     */
-  IETIDP_ORDER_DENSE = 1              /* r_V as one dense supernode (test/oracle aid)    */
+  IETIDP_ORDER_DENSE = 1,             /* r_V as one dense supernode (test/oracle aid)    */
+  IETIDP_ORDER_MIN_DEGREE = 2         /* approximate minimum degree of r_V, fundamental
+                                         supernodes, r_I last                           */
 } ietidp_ordering;
 
 typedef struct {

@@ -15,6 +15,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <set>
 #include <thread>
 
 #include "handle.h"
@@ -33,6 +34,193 @@ struct LocalResult {
 // ---------------------------------------------------------------------------
 // Nested dissection on the graph of K_VV (level-structure vertex separators)
 // ---------------------------------------------------------------------------
+// Minimum-degree ordering of r_V on the quotient graph (variables and elements, the
+// approximate external degree bound of Amestoy-Davis-Duff AMD; no supervariables, no
+// aggressive absorption), deterministic ties by (degree, index). Returns order[k] =
+// variable eliminated k-th.
+static std::vector<int> min_degree_order(const std::vector<int>& xadj, const std::vector<int>& adj, int n) {
+  std::vector<std::vector<int>> av(n), ae(n), ev(n);
+  std::vector<int> deg(n), state(n, 0);  // 0 live variable, 1 element, 2 absorbed element / eliminated
+  std::vector<int> wstamp(n, -1), w(n, 0), mark(n, -1);
+  std::set<std::pair<int, int>> pq;
+  for (int i = 0; i < n; ++i) {
+    av[i].assign(adj.begin() + xadj[i], adj.begin() + xadj[i + 1]);
+    deg[i] = (int)av[i].size();
+    pq.insert({deg[i], i});
+  }
+  std::vector<int> order;
+  order.reserve(n);
+  std::vector<int> Lp;
+  for (int k = 0; k < n; ++k) {
+    const int p = pq.begin()->second;
+    pq.erase(pq.begin());
+    order.push_back(p);
+    // new element Lp = (A_p u union of the elements of p) \ {p}
+    Lp.clear();
+    mark[p] = k;
+    for (int v : av[p])
+      if (state[v] == 0 && mark[v] != k) {
+        mark[v] = k;
+        Lp.push_back(v);
+      }
+    for (int e : ae[p]) {
+      if (state[e] != 1) continue;
+      for (int v : ev[e])
+        if (state[v] == 0 && mark[v] != k) {
+          mark[v] = k;
+          Lp.push_back(v);
+        }
+      state[e] = 2;  // absorbed into p
+      std::vector<int>().swap(ev[e]);
+    }
+    state[p] = 1;
+    ev[p] = Lp;
+    std::vector<int>().swap(av[p]);
+    std::vector<int>().swap(ae[p]);
+    // w(e) = |L_e \ Lp| for the live elements adjacent to Lp
+    for (int i : Lp)
+      for (int e : ae[i]) {
+        if (state[e] != 1 || e == p) continue;
+        if (wstamp[e] != k) {
+          wstamp[e] = k;
+          w[e] = (int)ev[e].size();
+        }
+        --w[e];
+      }
+    const int nlive = n - k - 1;
+    for (int i : Lp) {
+      // prune: dead elements out, p in; variables of Lp (now reached through p) out
+      std::vector<int>& E = ae[i];
+      size_t q = 0;
+      int ext = 0;
+      for (int e : E)
+        if (state[e] == 1 && e != p) {
+          E[q++] = e;
+          ext += (wstamp[e] == k) ? w[e] : (int)ev[e].size();
+        }
+      E.resize(q);
+      E.push_back(p);
+      std::vector<int>& A = av[i];
+      q = 0;
+      for (int v : A)
+        if (state[v] == 0 && mark[v] != k) A[q++] = v;
+      A.resize(q);
+      int d = (int)A.size() + (int)Lp.size() - 1 + ext;
+      d = std::min(d, nlive);
+      d = std::min(d, deg[i] + (int)Lp.size() - 1);
+      d = std::max(d, 0);
+      if (d != deg[i]) {
+        pq.erase({deg[i], i});
+        deg[i] = d;
+        pq.insert({deg[i], i});
+      }
+    }
+  }
+  return order;
+}
+
+// Fundamental supernodes of the r_V block under the elimination order `order`:
+// column structures by the multifrontal merge (struct(j) = adj(j) u children's structs,
+// entries > j), etree parent = min row; j joins j+1 when parent(j) = j+1, j is j+1's only
+// child and |struct(j)| = |struct(j+1)| + 1. Supernodes in elimination order.
+static std::vector<std::vector<int>> md_supernodes(const std::vector<int>& xadj, const std::vector<int>& adj, int n,
+                                                   std::vector<int> order, bool postordered = false) {
+  std::vector<int> pos(n);
+  for (int k = 0; k < n; ++k) pos[order[k]] = k;
+  std::vector<std::vector<int>> st(n);
+  std::vector<int> parent(n, -1), nchild(n, 0), cnt(n, 0), mark(n, -1);
+  std::vector<std::vector<int>> kids(n);
+  for (int j = 0; j < n; ++j) {
+    std::vector<int>& S = st[j];
+    const int v = order[j];
+    for (int e = xadj[v]; e < xadj[v + 1]; ++e) {
+      const int r = pos[adj[e]];
+      if (r > j && mark[r] != j) {
+        mark[r] = j;
+        S.push_back(r);
+      }
+    }
+    for (int c : kids[j]) {
+      for (int r : st[c])
+        if (r > j && mark[r] != j) {
+          mark[r] = j;
+          S.push_back(r);
+        }
+      std::vector<int>().swap(st[c]);
+    }
+    std::sort(S.begin(), S.end());
+    cnt[j] = (int)S.size();
+    if (!S.empty()) {
+      parent[j] = S[0];
+      kids[S[0]].push_back(j);
+      ++nchild[S[0]];
+    }
+  }
+  if (!postordered) {
+    // reorder to a postorder of the elimination tree (same fill; makes every subtree,
+    // and each node with its last child, contiguous), then redo the symbolic pass
+    std::vector<int> post;
+    post.reserve(n);
+    std::vector<std::pair<int, size_t>> stk;
+    for (int r = 0; r < n; ++r) {
+      if (parent[r] != -1) continue;
+      stk.push_back({r, 0});
+      while (!stk.empty()) {
+        auto& t = stk.back();
+        if (t.second < kids[t.first].size()) {
+          const int c = kids[t.first][t.second++];
+          stk.push_back({c, 0});
+        } else {
+          post.push_back(t.first);
+          stk.pop_back();
+        }
+      }
+    }
+    std::vector<int> order2(n);
+    for (int k = 0; k < n; ++k) order2[k] = order[post[k]];
+    return md_supernodes(xadj, adj, n, std::move(order2), true);
+  }
+  // fundamental supernodes: [first, last] column ranges
+  struct FS {
+    int first, last;
+    long long f;      // front size (cnt[first] + 1)
+    long long nz;     // stored entries of the front's pivot columns (incl. padding)
+    int parent_col;   // etree parent of the last column (-1: root)
+  };
+  std::vector<FS> fs;
+  int first = 0;
+  for (int j = 1; j <= n; ++j) {
+    if (j < n && parent[j - 1] == j && nchild[j] == 1 && cnt[j - 1] == cnt[j] + 1) continue;
+    FS x{first, j - 1, cnt[first] + 1LL, 0, parent[j - 1]};
+    const long long np = j - first;
+    x.nz = np * x.f - np * (np - 1) / 2;
+    fs.push_back(x);
+    first = j;
+  }
+  // relaxed amalgamation: a supernode merges into the next one when that is its parent
+  // (contiguous in the order) and the merged front is small or adds few explicit zeros
+  std::vector<FS> st2;
+  for (const FS& x : fs) {
+    st2.push_back(x);
+    while (st2.size() >= 2) {
+      FS& c = st2[st2.size() - 2];
+      FS& q = st2.back();
+      if (c.parent_col < q.first || c.parent_col > q.last) break;  // not the parent
+      const long long npc = c.last - c.first + 1, npq = q.last - q.first + 1, np = npc + npq;
+      const long long fm = npc + q.f;  // child's update rows lie in the parent's front
+      const long long nzm = np * fm - np * (np - 1) / 2;
+      const long long zeros = nzm - c.nz - q.nz;
+      if (!(np <= 16 || (np <= 128 && zeros * 10 <= nzm))) break;
+      FS m{c.first, q.last, fm, nzm, q.parent_col};
+      st2.pop_back();
+      st2.back() = m;
+    }
+  }
+  std::vector<std::vector<int>> sn;
+  for (const FS& x : st2) sn.emplace_back(order.begin() + x.first, order.begin() + x.last + 1);
+  return sn;
+}
+
 struct NestedDissection {
   const std::vector<int>& xadj;
   const std::vector<int>& adj;
@@ -234,6 +422,8 @@ LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf) {
     std::iota(all.begin(), all.end(), 0);
     if (ordering == IETIDP_ORDER_DENSE) {
       sn_vars.push_back(all);
+    } else if (ordering == IETIDP_ORDER_MIN_DEGREE) {
+      sn_vars = md_supernodes(xadj, adj, sp.nV, min_degree_order(xadj, adj, sp.nV));
     } else {
       NestedDissection nd(xadj, adj, sp.nV, std::max(leaf, 8));
       for (int a = 0; a < sp.nV; ++a) nd.reg[a] = -1;

@@ -16,7 +16,7 @@ STATUS = {0: "IETIDP_OK", 1: "IETIDP_E_ARG", 2: "IETIDP_E_STATE", 3: "IETIDP_E_B
           4: "IETIDP_E_NOT_SPD", 5: "IETIDP_E_NO_CONVERGENCE", 6: "IETIDP_E_CUDA", 7: "IETIDP_E_NOMEM"}
 OK, E_ARG, E_STATE, E_B_STRUCTURE, E_NOT_SPD, E_NO_CONVERGENCE, E_CUDA, E_NOMEM = range(8)
 SCALING = {"multiplicity": 0, "stiffness": 1}
-ORDERING = {"nd": 0, "dense": 1}
+ORDERING = {"nd": 0, "dense": 1, "md": 2}
 LOOP = {"explicit": 0, "triangular": 1}
 
 # every entry point include/ietidp.h declares

@@ -214,3 +214,15 @@ def test_graph_replay_equals_direct_launches(lib, monkeypatch):
     lam2, _ = t.solve()
     assert np.array_equal(lam1, lam2)
     assert np.array_equal(u1, t.get_u(3))
+
+
+@pytest.mark.parametrize("name", ["C2r", "C5r"])
+def test_min_degree_ordering_solution(lib, name):
+    """The minimum-degree ordering option (postordered elimination tree, fundamental +
+    relaxed supernodes) gives, iteration-matched, the oracle's solution."""
+    b, ref = case(name)
+    nit = int(np.max(ref["iters"]))
+    ref_f = dp.solve(b, fixed_iters=nit)
+    s, lam, u, rep = gpu_solve(lib, b, fixed_iters=nit, ordering="md")
+    assert rel(lam, ref_f["lam"]) <= 1e-8
+    assert rel(np.concatenate(u), np.concatenate(ref_f["u"])) <= 1e-8
