@@ -317,7 +317,7 @@ __global__ void __launch_bounds__(POTRF_T) k_potrf_c(const Work* __restrict__ wo
 //   BKC = true:  B[k][n] = Bb[b_off + n*ldb + k]  (k contiguous: column-major B)
 //   ATR = true:  A[r][k] = Ab[a_off + r*lda + k]  (A given transposed, k contiguous)
 // ---------------------------------------------------------------------------
-constexpr int KC = 32, GST = 2, KS = 68;  // 2 stages: 70 KB smem, 3 CTAs/SM; KS = 4 mod 16: conflict-free fragment loads
+constexpr int KC = 16, GST = 3, KS = 68;  // 2 stages: 70 KB smem, 3 CTAs/SM; KS = 4 mod 16: conflict-free fragment loads
 constexpr int GEMM_SMEM = GST * 2 * KC * KS * (int)sizeof(double);
 
 __device__ __forceinline__ void cp_async_z16(void* smem, const void* gmem, int src_bytes) {
@@ -350,7 +350,7 @@ __device__ __forceinline__ void load_rc(double* dst, const double* src, long lon
 }
 
 template <bool BKC, bool ATR = false>
-__global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work, const double* __restrict__ Ab,
+__global__ void __launch_bounds__(128, 4) k_gemm(const GemmWork* __restrict__ work, const double* __restrict__ Ab,
                                               const double* __restrict__ Bb, double* __restrict__ Cb,
                                               const int* __restrict__ d_rel, double* __restrict__ skws = nullptr,
                                               int* __restrict__ skcnt = nullptr) {
@@ -371,7 +371,7 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
     } else {  // A[r][k] = Ab[a_off + r*lda + k] (k contiguous)
       double* d = As(st);
       for (int q = tid; q < KC * 64; q += 128) {
-        const int r = q >> 5, k = q & 31;
+        const int r = q / KC, k = q % KC;
         const int nv = (k < kb && r < w.m) ? 1 : 0;
         const double* gp = Ab + (nv ? w.a_off + (long long)r * w.lda + k0 + k : 0);
         cp_async_z8(d + k * KS + r, gp, nv * 8);
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
     } else {
       double* d = Bs(st);
       for (int q = tid; q < KC * 64; q += 128) {
-        const int n = q >> 5, k = q & 31;  // k fastest: coalesced global reads
+        const int n = q / KC, k = q % KC;  // k fastest: coalesced global reads
         const int nv = (k < kb && n < w.n) ? 1 : 0;
         const double* gp = Bb + (nv ? w.b_off + (long long)n * w.ldb + k0 + k : 0);
         cp_async_z8(d + k * KS + n, gp, nv * 8);
@@ -450,18 +450,18 @@ __global__ void __launch_bounds__(128) k_gemm(const GemmWork* __restrict__ work,
     __syncthreads();
     if (!last) return;
     __threadfence();
-    // each thread reduces 4 x 2 consecutive entries with all SPLITK_MAX loads in flight
+    // each thread reduces 2 x 2 consecutive entries with all SPLITK_MAX loads in flight
     const double* P0 = skws + w.ws_off;
-    for (int e0 = 2 * tid; e0 < TILE_ELEMS; e0 += 4 * 256) {
-      double2 v[4][SPLITK_MAX];
+    for (int e0 = 2 * tid; e0 < TILE_ELEMS; e0 += 2 * 256) {
+      double2 v[2][SPLITK_MAX];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
+      for (int u = 0; u < 2; ++u)
 #pragma unroll
         for (int q = 0; q < SPLITK_MAX; ++q)
           if (q < w.nks)
             v[u][q] = __ldcg(reinterpret_cast<const double2*>(P0 + (long long)q * TILE_ELEMS + e0 + u * 256));
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 2; ++u) {
         double s0 = v[u][0].x, s1 = v[u][0].y;
 #pragma unroll
         for (int q = 1; q < SPLITK_MAX; ++q)
