@@ -484,6 +484,11 @@ void ietidp_destroy(ietidp_t h) {
   if (h->rgraph) cudaGraphExecDestroy(h->rgraph);
   if (h->hp) cudaStreamDestroy(h->hp);
   if (h->side) cudaStreamDestroy(h->side);
+  for (auto x : h->gst)
+    if (x) cudaStreamDestroy(x);
+  for (auto x : h->gside)
+    if (x) cudaStreamDestroy(x);
+  for (auto e : h->gev) cudaEventDestroy(e);
   if (h->own_stream && h->stream) cudaStreamDestroy(h->stream);
   delete h;
 }

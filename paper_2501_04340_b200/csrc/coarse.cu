@@ -261,8 +261,7 @@ void run_coarse(ietidp_s* h) {
   cudaStream_t s = h->stream;
   const int nrhs = h->nrhs, ng = h->n_primal;
   const int nlev = h->plan.max_level + 1;
-  // every L11^-1 is ready (factorisation side stream)
-  IETI_CUDA(cudaStreamWaitEvent(s, h->fev[nlev + 2], 0));
+  (void)nlev;  // the factorisation's streams have joined the caller's stream
   if (h->n_lambda) {
     k_scaling<<<grid_for(h->n_lambda, 256), 256, 0, s>>>(h->n_lambda, h->lam.p, h->kdiag_src.p, h->kval.p, h->kdiag.p,
                                                         h->delta.p, h->opt.scaling == IETIDP_SCALE_STIFFNESS);
@@ -285,8 +284,6 @@ void run_coarse(ietidp_s* h) {
       IETI_LAUNCHED(h);
     }
     run_sweeps(h, h->Xf.p, true, false);
-  } else {
-    IETI_CUDA(cudaStreamWaitEvent(s, h->fev[nlev + 3], 0));
   }
   if (ng > 0) {
     const int smem = ng * (ng + 1) / 2 * sizeof(double);
@@ -308,7 +305,6 @@ void run_coarse(ietidp_s* h) {
     loop_bwd(h, nrhs, h->yI.p, ng ? h->zc0.p : nullptr, -1.0, h->xI.p, nullptr);
     bgather(h, nrhs, h->xI.p, nullptr, h->d_vec.p, nullptr, nullptr, nullptr);
   }
-  IETI_CUDA(cudaStreamWaitEvent(s, h->fev[nlev], 0));  // W_k ready: join the side stream
   IETI_CHECK_LAUNCH();
 }
 

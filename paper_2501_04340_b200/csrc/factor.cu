@@ -614,7 +614,7 @@ static void set_smem(const void* f, int bytes) {
   IETI_CUDA(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes));
 }
 
-void fwd_sweep_level(ietidp_s* h, double* X, int L, cudaStream_t st);
+void fwd_sweep_lp(ietidp_s* h, double* X, const LevelPlan& lp, cudaStream_t st);
 
 // G_k^T = L_PI L_II^-1 for every subdomain (one DMMA GEMM launch; after k_pack's L_PI)
 void launch_form_G(ietidp_s* h) {
@@ -661,125 +661,151 @@ void run_factor(ietidp_s* h) {
   int maxnt = 0;
   for (auto& d : h->h_sub) maxnt = std::max(maxnt, d.nt);
   const bool expl = h->opt.loop == IETIDP_LOOP_EXPLICIT;
-  // Two streams: the panels and SYRKs of level after level on the main stream; the
-  // partitioned inverse of a level's supernodes (and finally W_k) on the side stream,
-  // started as soon as that level's panels are factored, so that it overlaps the
-  // latency-bound SYRK / panel launches of the levels above.
-  const int nlev = P.max_level + 1;
+  // Streams. The subdomains are split into P.ngroups independent groups; group g runs
+  // its panels and SYRKs level after level on its own high-priority stream gst[g]
+  // (group 0 on the caller's stream), so that one group's latency-bound panels
+  // overlap the other's GEMMs. Each group has a low-priority side stream gside[g] for
+  // its partitioned inverse (started as soon as a level's / a panel's factors exist),
+  // W_k and the forward sweep of the loads. One more side stream assembles the fronts
+  // of levels >= 1 while level 0 is factored. Everything joins the caller's stream at
+  // the end.
+  const int nlev = P.max_level + 1, G = P.ngroups;
   if (!h->side) {
     IETI_CUDA(cudaStreamCreateWithFlags(&h->side, cudaStreamNonBlocking));
-    h->fev.resize(nlev + 5);
+    int lo = 0, hi = 0;
+    IETI_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    h->gst.assign(G, nullptr);
+    h->gside.assign(G, nullptr);
+    for (int g = 0; g < G; ++g) {
+      if (g > 0) IETI_CUDA(cudaStreamCreateWithPriority(&h->gst[g], cudaStreamNonBlocking, hi));
+      IETI_CUDA(cudaStreamCreateWithFlags(&h->gside[g], cudaStreamNonBlocking));
+    }
+    h->fev.resize(4);
     for (auto& e : h->fev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    h->gev.resize((size_t)G * (nlev + 2));
+    for (auto& e : h->gev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t np = 0;
-    for (auto& lv : P.levels) np += lv.panels.size();
+    for (auto& gl : P.glevels)
+      for (auto& lv : gl) np += lv.panels.size();
     h->pev.resize(np);
     for (auto& e : h->pev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  cudaStream_t s2 = h->side;
-  size_t npan = 0;
+  auto gevent = [&](int g, int i) { return h->gev[(size_t)g * (nlev + 2) + i]; };
+  cudaStream_t sa = h->side;  // assembly of the levels >= 1
   // compact POTRF by default (measured faster in the pipeline: the instruction cache is
   // cold at every launch); IETIDP_POTRF=unrolled selects the fully unrolled kernel
   static const bool potrf_compact = !(getenv("IETIDP_POTRF") && !strcmp(getenv("IETIDP_POTRF"), "unrolled"));
-  const LevelPlan::Panel* wacc_last = nullptr;
-  IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));
-  IETI_CUDA(cudaEventRecord(h->fev[nlev + 1], st));  // side work starts after level 0's assembly
-  IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[nlev + 1], 0));
-  for (int L = 1; L < nlev; ++L) assemble(L, s2);
-  if (expl) h->wtiles.zero(s2);  // W_k is accumulated block row by block row
-  IETI_CUDA(cudaEventRecord(h->fev[nlev + 4], s2));  // every front assembled
-  // the forward sweep of the loads rides on the side stream too (one column chunk)
+  IETI_CUDA(cudaEventRecord(h->fev[0], st));  // level 0 assembled, flags initialised
+  IETI_CUDA(cudaStreamWaitEvent(sa, h->fev[0], 0));
+  for (int L = 1; L < nlev; ++L) assemble(L, sa);
+  IETI_CUDA(cudaEventRecord(h->fev[1], sa));  // every front assembled
+  // the forward sweep of the loads rides on the groups' side streams (one column chunk)
   h->fwd_in_factor = h->nrhs <= 16;
+  if (expl) h->wtiles.zero(st);  // W_k is accumulated block row by block row
   if (h->fwd_in_factor) {
-    h->Xf.zero(s2);
+    h->Xf.zero(st);
     if (h->sc_fx_dst.n) {
-      k_scatter<<<grid_for((long long)h->sc_fx_dst.n, 256), 256, 0, s2>>>(
+      k_scatter<<<grid_for((long long)h->sc_fx_dst.n, 256), 256, 0, st>>>(
           (long long)h->sc_fx_dst.n, h->sc_fx_dst.p, h->sc_fx_src.p, h->fval.p, h->Xf.p);
-      IETI_LAUNCHED_SIDE(h);
-    }
-  }
-  for (int L = 0; L < nlev; ++L) {
-    const LevelPlan& lp = P.levels[L];
-    // explicit loop: S_II is the assembled r_I root front before its factorisation
-    if (expl && h->rootlist_range[L].second > 0) {
-      k_pack_sym<<<h->rootlist_range[L].second * (maxnt * (maxnt + 1) / 2), 256, 0, st>>>(h->d_rootlist.p + h->rootlist_range[L].first,
-                                                                       maxnt, h->d_sub.p, h->d_sn.p, pool, 1,
-                                                                       h->stiles.p);
       IETI_LAUNCHED(h);
     }
-    for (auto& pn : lp.panels) {
-      if (pn.upd_n) {
-        k_gemm<false><<<pn.upd_n, 128, GEMM_SMEM, st>>>(GW + pn.upd_off, pool, pool, pool, rel, h->skws.p,
-                                                         h->skcnt.p);
-        IETI_LAUNCHED(h);
-      }
-      if (pn.potrf_n) {
-        if (potrf_compact)
-          k_potrf_c<<<pn.potrf_n, POTRF_T, 0, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
-        else
-          k_potrf<<<pn.potrf_n, POTRF_T, 0, st>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
-        IETI_LAUNCHED(h);
-      }
-      cudaEvent_t pe = h->pev[npan++];
-      IETI_CUDA(cudaEventRecord(pe, st));
-      if (pn.trsm_n) {
-        k_gemm<false><<<pn.trsm_n, 128, GEMM_SMEM, st>>>(GW + pn.trsm_off, pool, h->dinv.p, pool, rel);
-        IETI_LAUNCHED(h);
-      }
-      // side stream: block row kp of L11^-1 (and of W_k) as soon as Dinv_kp exists
-      IETI_CUDA(cudaStreamWaitEvent(s2, pe, 0));
-      if (pn.icopy_n) {
-        k_inv_copy<<<pn.icopy_n, 256, 0, s2>>>(W + pn.icopy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
+  }
+  IETI_CUDA(cudaEventRecord(h->fev[2], st));
+  size_t npan = 0;
+  for (int g = 0; g < G; ++g) {
+    cudaStream_t sg = g == 0 ? st : h->gst[g];
+    cudaStream_t s2 = h->gside[g];
+    if (g > 0) IETI_CUDA(cudaStreamWaitEvent(sg, h->fev[2], 0));
+    IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[2], 0));
+    const LevelPlan::Panel* wacc_last = nullptr;
+    for (int L = 0; L < nlev; ++L) {
+      const LevelPlan& lp = P.glevels[g][L];
+      // explicit loop: S_II is the assembled r_I root front before its factorisation
+      const auto& rr = h->rootlist_range[g][L];
+      if (expl && rr.second > 0) {
+        k_pack_sym<<<rr.second * (maxnt * (maxnt + 1) / 2), 256, 0, sg>>>(h->d_rootlist.p + rr.first, maxnt,
+                                                                          h->d_sub.p, h->d_sn.p, pool, 1,
+                                                                          h->stiles.p);
         IETI_LAUNCHED_SIDE(h);
       }
-      if (pn.ia_n) {
-        k_gemm<true><<<pn.ia_n, 128, GEMM_SMEM, s2>>>(GW + pn.ia_off, pool, h->ipool.p, h->tpool.p, rel);
+      for (auto& pn : lp.panels) {
+        if (pn.upd_n) {
+          k_gemm<false><<<pn.upd_n, 128, GEMM_SMEM, sg>>>(GW + pn.upd_off, pool, pool, pool, rel, h->skws.p,
+                                                           h->skcnt.p);
+          IETI_LAUNCHED_SIDE(h);
+        }
+        if (pn.potrf_n) {
+          if (potrf_compact)
+            k_potrf_c<<<pn.potrf_n, POTRF_T, 0, sg>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
+          else
+            k_potrf<<<pn.potrf_n, POTRF_T, 0, sg>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
+          IETI_LAUNCHED_SIDE(h);
+        }
+        cudaEvent_t pe = h->pev[npan++];
+        IETI_CUDA(cudaEventRecord(pe, sg));
+        if (pn.trsm_n) {
+          k_gemm<false><<<pn.trsm_n, 128, GEMM_SMEM, sg>>>(GW + pn.trsm_off, pool, h->dinv.p, pool, rel);
+          IETI_LAUNCHED_SIDE(h);
+        }
+        // side stream: block row kp of L11^-1 (and of W_k) as soon as Dinv_kp exists
+        if (pn.icopy_n || pn.ia_n || pn.ib_n || pn.wacc_n) IETI_CUDA(cudaStreamWaitEvent(s2, pe, 0));
+        if (pn.icopy_n) {
+          k_inv_copy<<<pn.icopy_n, 256, 0, s2>>>(W + pn.icopy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
+          IETI_LAUNCHED_SIDE(h);
+        }
+        if (pn.ia_n) {
+          k_gemm<true><<<pn.ia_n, 128, GEMM_SMEM, s2>>>(GW + pn.ia_off, pool, h->ipool.p, h->tpool.p, rel);
+          IETI_LAUNCHED_SIDE(h);
+        }
+        if (pn.ib_n) {
+          k_gemm<true><<<pn.ib_n, 128, GEMM_SMEM, s2>>>(GW + pn.ib_off, h->dinv.p, h->tpool.p, h->ipool.p, rel);
+          IETI_LAUNCHED_SIDE(h);
+        }
+        if (&pn == &lp.panels.back()) {
+          wacc_last = pn.wacc_n ? &pn : nullptr;  // after the level's forward sweep (not on the path)
+        } else if (pn.wacc_n) {
+          k_gemm<true, true><<<pn.wacc_n, 128, GEMM_SMEM, s2>>>(GW + pn.wacc_off, h->ipool.p, h->ipool.p,
+                                                                h->wtiles.p, rel);
+          IETI_LAUNCHED_SIDE(h);
+        }
+      }
+      IETI_CUDA(cudaEventRecord(gevent(g, L), sg));
+      if (L == 0) IETI_CUDA(cudaStreamWaitEvent(sg, h->fev[1], 0));  // parents assembled
+      for (auto& sy : lp.syrk) {
+        k_gemm<false><<<sy.second, 128, GEMM_SMEM, sg>>>(GW + sy.first, pool, pool, pool, rel);
         IETI_LAUNCHED_SIDE(h);
       }
-      if (pn.ib_n) {
-        k_gemm<true><<<pn.ib_n, 128, GEMM_SMEM, s2>>>(GW + pn.ib_off, h->dinv.p, h->tpool.p, h->ipool.p, rel);
+      // side stream: recursive-doubling L11^-1 of the level (if not formed per panel)
+      IETI_CUDA(cudaStreamWaitEvent(s2, gevent(g, L), 0));  // the level's factors
+      if (lp.inv_copy_n) {
+        k_inv_copy<<<lp.inv_copy_n, 256, 0, s2>>>(W + lp.inv_copy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
         IETI_LAUNCHED_SIDE(h);
       }
-      if (pn.icopy_n) IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));  // last record: every L11^-1 done
-      if (&pn == &lp.panels.back()) {
-        wacc_last = pn.wacc_n ? &pn : nullptr;  // after the level's forward sweep (not on the path)
-      } else if (pn.wacc_n) {
-        k_gemm<true, true><<<pn.wacc_n, 128, GEMM_SMEM, s2>>>(GW + pn.wacc_off, h->ipool.p, h->ipool.p,
-                                                              h->wtiles.p, rel);
+      for (size_t r = 0; r < lp.inv_rounds.size(); ++r) {
+        const auto& rg = lp.inv_rounds[r];
+        if (!rg.second) continue;
+        const bool step1 = (r % 2) == 0;
+        k_gemm<true><<<rg.second, 128, GEMM_SMEM, s2>>>(GW + rg.first, step1 ? pool : h->ipool.p,
+                                                        step1 ? h->ipool.p : h->tpool.p,
+                                                        step1 ? h->tpool.p : h->ipool.p, rel);
         IETI_LAUNCHED_SIDE(h);
       }
+      if (h->fwd_in_factor) fwd_sweep_lp(h, h->Xf.p, lp, s2);
+      if (wacc_last) {
+        k_gemm<true, true><<<wacc_last->wacc_n, 128, GEMM_SMEM, s2>>>(GW + wacc_last->wacc_off, h->ipool.p,
+                                                                      h->ipool.p, h->wtiles.p, rel);
+        IETI_LAUNCHED_SIDE(h);
+        wacc_last = nullptr;
+      }
     }
-    IETI_CUDA(cudaEventRecord(h->fev[L], st));
-    if (L == 0) IETI_CUDA(cudaStreamWaitEvent(st, h->fev[nlev + 4], 0));  // parents assembled
-    for (auto& sy : lp.syrk) {
-      k_gemm<false><<<sy.second, 128, GEMM_SMEM, st>>>(GW + sy.first, pool, pool, pool, rel);
-      IETI_LAUNCHED(h);
-    }
-    // side stream: recursive-doubling L11^-1 of the level (if not formed per panel)
-    IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[L], 0));  // the level's factors
-    if (lp.inv_copy_n) {
-      k_inv_copy<<<lp.inv_copy_n, 256, 0, s2>>>(W + lp.inv_copy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
-      IETI_LAUNCHED_SIDE(h);
-    }
-    for (size_t r = 0; r < lp.inv_rounds.size(); ++r) {
-      const auto& rg = lp.inv_rounds[r];
-      if (!rg.second) continue;
-      const bool step1 = (r % 2) == 0;
-      k_gemm<true><<<rg.second, 128, GEMM_SMEM, s2>>>(GW + rg.first, step1 ? pool : h->ipool.p,
-                                                      step1 ? h->ipool.p : h->tpool.p,
-                                                      step1 ? h->tpool.p : h->ipool.p, rel);
-      IETI_LAUNCHED_SIDE(h);
-    }
-    if (lp.inv_copy_n) IETI_CUDA(cudaEventRecord(h->fev[nlev + 2], s2));
-    if (h->fwd_in_factor) fwd_sweep_level(h, h->Xf.p, L, s2);
-    if (wacc_last) {
-      k_gemm<true, true><<<wacc_last->wacc_n, 128, GEMM_SMEM, s2>>>(GW + wacc_last->wacc_off, h->ipool.p,
-                                                                    h->ipool.p, h->wtiles.p, rel);
-      IETI_LAUNCHED_SIDE(h);
-      wacc_last = nullptr;
+    // join: the group's main and side streams into the caller's stream
+    IETI_CUDA(cudaEventRecord(gevent(g, nlev), s2));
+    IETI_CUDA(cudaStreamWaitEvent(st, gevent(g, nlev), 0));
+    if (g > 0) {
+      IETI_CUDA(cudaEventRecord(gevent(g, nlev + 1), sg));
+      IETI_CUDA(cudaStreamWaitEvent(st, gevent(g, nlev + 1), 0));
     }
   }
-  IETI_CUDA(cudaEventRecord(h->fev[nlev + 3], s2));  // forward sweep done
-  IETI_CUDA(cudaEventRecord(h->fev[nlev], s2));  // side stream done (joined in run_coarse)
   IETI_CHECK_LAUNCH();
 }
 

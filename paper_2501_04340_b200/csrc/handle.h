@@ -114,6 +114,8 @@ struct ietidp_s {
   cudaEvent_t fg_ev[3] = {nullptr, nullptr, nullptr};
   // side stream of the factorisation (partitioned inverse, W_k) and its events
   cudaStream_t side = nullptr;
+  std::vector<cudaStream_t> gst, gside;  // per subdomain group: main and side streams
+  std::vector<cudaEvent_t> gev;          // per group: events (see run_factor)
   std::vector<cudaEvent_t> fev;  // [0..levels): level's panels done; [levels]: side done
   std::vector<cudaEvent_t> pev;  // per panel: POTRF done (progressive inverse)
   bool fwd_in_factor = false;    // the forward sweep of the loads ran on the side stream
@@ -159,7 +161,7 @@ struct ietidp_s {
   ieti::DevBuf<int2> d_blk;                 // (subdomain, block) items of the partial reduction
   int n_blk = 0;
   ieti::DevBuf<int> d_rootlist;             // subdomains by level of their r_I root (for the S_II copy)
-  std::vector<std::pair<int, int>> rootlist_range;  // per level: (offset, count) into d_rootlist
+  std::vector<std::vector<std::pair<int, int>>> rootlist_range;  // [group][level]: (offset, count) into d_rootlist
   ieti::DevBuf<long long> slot_goff;        // per r_I slot: its row of G_k
   ieti::DevBuf<int> slot_np, slot_poff;     // per r_I slot: n_P of its subdomain, primal-row offset
   ieti::DevBuf<ieti::SlotRed> slot_red;     // per r_I slot: its symmetric-pass partials

@@ -180,7 +180,9 @@ struct Plan {
   std::vector<SubPlan> subs;
   std::vector<SnHost> sn;     // all supernodes, global ids
   std::vector<int> level_sn;  // supernode ids grouped by level
-  std::vector<LevelPlan> levels;
+  std::vector<LevelPlan> levels;                 // all supernodes by level: assembly and sweeps
+  int ngroups = 1;                               // subdomain groups of the factorisation
+  std::vector<std::vector<LevelPlan>> glevels;   // [group][level]: panels, SYRK, inverse, sweep lists
   int g_off = 0, g_n = 0;                       // GemmWork: G_k^T = L_PI L_II^-1
   std::vector<std::vector<int>> roots_by_level; // subdomains whose r_I root front is at level L
   long long pool_doubles = 0, dinv_doubles = 0, inv_doubles = 0, vec_rows = 0;

@@ -323,8 +323,7 @@ static void sweeps_t(ietidp_s* h, double* X, bool fwd, bool bwd, int cofs) {
 // Forward sweep of one level for every column (nrhs <= 16), on stream st: used by the
 // factorisation's side stream, level by level as the partitioned inverse completes.
 template <int NCB>
-static void fwd_level_t(ietidp_s* h, double* X, int L, cudaStream_t st) {
-  const LevelPlan& lp = h->plan.levels[L];
+static void fwd_level_t(ietidp_s* h, double* X, const LevelPlan& lp, cudaStream_t st) {
   const Work* W = reinterpret_cast<const Work*>(h->d_work.p);
   const int ldx = h->nrhs;
   if (!lp.sn_n) return;
@@ -342,13 +341,13 @@ static void fwd_level_t(ietidp_s* h, double* X, int L, cudaStream_t st) {
     IETI_LAUNCHED_SIDE(h);
   }
 }
-void fwd_sweep_level(ietidp_s* h, double* X, int L, cudaStream_t st) {
+void fwd_sweep_lp(ietidp_s* h, double* X, const LevelPlan& lp, cudaStream_t st) {
   const int n = h->nrhs;
-  if (n == 1) fwd_level_t<1>(h, X, L, st);
-  else if (n == 2) fwd_level_t<2>(h, X, L, st);
-  else if (n <= 4) fwd_level_t<4>(h, X, L, st);
-  else if (n <= 8) fwd_level_t<8>(h, X, L, st);
-  else fwd_level_t<16>(h, X, L, st);
+  if (n == 1) fwd_level_t<1>(h, X, lp, st);
+  else if (n == 2) fwd_level_t<2>(h, X, lp, st);
+  else if (n <= 4) fwd_level_t<4>(h, X, lp, st);
+  else if (n <= 8) fwd_level_t<8>(h, X, lp, st);
+  else fwd_level_t<16>(h, X, lp, st);
 }
 
 // X (ne rows per subdomain x nrhs) <- L^-1 X (forward) and/or L^-T X (backward).
