@@ -151,8 +151,12 @@ ietidp_status ietidp_set_subdomain(ietidp_t h, int k, int n_k,
 ietidp_status ietidp_analyze(ietidp_t h);
 
 /* Replace the numeric values (same pattern) of subdomain k after analysis:
- * K_val[nnz] and f[n_k*nrhs] (host, copied to the device in the call; either may
- * be NULL to keep the current values). The next ietidp_factor uses them. */
+ * K_val[nnz] and f[n_k*nrhs] (host; either may be NULL to keep the current values).
+ * The copy is asynchronous, on an internal stream ordered after the handle's stream;
+ * the caller's buffers must stay unchanged until the next ietidp_factor returns (use
+ * page-locked memory for an asynchronous copy). The next ietidp_factor uses the values:
+ * each subdomain group of the factorisation starts as soon as its subdomains' copies
+ * have arrived, so the transfer overlaps the factorisation of earlier groups. */
 ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const double* f);
 
 /* Device numeric phase: batched supernodal Cholesky of every K_rr^(k)

@@ -204,12 +204,23 @@ ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const do
     require(h->analyzed, IETIDP_E_STATE, "set_values before analysis");
     require(k >= 0 && k < h->n_sub, IETIDP_E_ARG, "subdomain index out of range");
     const ieti::SubIn& in = h->in[k];
+    // copies on a dedicated stream, one event per subdomain: the next factorisation
+    // starts a subdomain group as soon as that group's values have arrived
+    if (!h->cstream) {
+      IETI_CUDA(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+      h->kev.resize(h->n_sub);
+      for (auto& e : h->kev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      IETI_CUDA(cudaEventCreateWithFlags(&h->hp_ev_set, cudaEventDisableTiming));
+    }
+    IETI_CUDA(cudaEventRecord(h->hp_ev_set, h->stream));  // after the caller's prior work
+    IETI_CUDA(cudaStreamWaitEvent(h->cstream, h->hp_ev_set, 0));
     if (K_val)
       IETI_CUDA(cudaMemcpyAsync(h->kval.p + h->kval_off[k], K_val, in.val.size() * sizeof(double),
-                                cudaMemcpyHostToDevice, h->stream));
+                                cudaMemcpyHostToDevice, h->cstream));
     if (f)
       IETI_CUDA(cudaMemcpyAsync(h->fval.p + h->fval_off[k], f, (size_t)in.n * h->nrhs * sizeof(double),
-                                cudaMemcpyHostToDevice, h->stream));
+                                cudaMemcpyHostToDevice, h->cstream));
+    IETI_CUDA(cudaEventRecord(h->kev[k], h->cstream));
     h->factored = false;
     h->solved = false;
   });
@@ -484,6 +495,9 @@ void ietidp_destroy(ietidp_t h) {
   if (h->rgraph) cudaGraphExecDestroy(h->rgraph);
   if (h->hp) cudaStreamDestroy(h->hp);
   if (h->side) cudaStreamDestroy(h->side);
+  if (h->cstream) cudaStreamDestroy(h->cstream);
+  for (auto e : h->kev) cudaEventDestroy(e);
+  if (h->hp_ev_set) cudaEventDestroy(h->hp_ev_set);
   for (auto x : h->gst)
     if (x) cudaStreamDestroy(x);
   for (auto x : h->gside)

@@ -644,8 +644,7 @@ void run_factor(ietidp_s* h) {
   // assembly of the fronts, level by level: zero the lower trapezoids, scatter K's
   // entries. Level 0 on the main stream; the levels above on the side stream while
   // level 0 is factored (the main stream waits for them before the first SYRK).
-  auto assemble = [&](int L, cudaStream_t sx) {
-    const LevelPlan& lp = P.levels[L];
+  auto assemble = [&](const LevelPlan& lp, cudaStream_t sx) {
     if (lp.zr_n) {
       k_zero_fronts<<<lp.zr_n, 256, 0, sx>>>(W + lp.zr_off, h->d_sn.p, pool);
       if (sx == st) IETI_LAUNCHED(h); else IETI_LAUNCHED_SIDE(h);
@@ -656,7 +655,6 @@ void run_factor(ietidp_s* h) {
       if (sx == st) IETI_LAUNCHED(h); else IETI_LAUNCHED_SIDE(h);
     }
   };
-  assemble(0, st);
   const int* rel = h->d_rel.p;
   int maxnt = 0;
   for (auto& d : h->h_sub) maxnt = std::max(maxnt, d.nt);
@@ -682,7 +680,7 @@ void run_factor(ietidp_s* h) {
     }
     h->fev.resize(4);
     for (auto& e : h->fev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    h->gev.resize((size_t)G * (nlev + 2));
+    h->gev.resize((size_t)G * (nlev + 4));
     for (auto& e : h->gev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     size_t np = 0;
     for (auto& gl : P.glevels)
@@ -690,33 +688,36 @@ void run_factor(ietidp_s* h) {
     h->pev.resize(np);
     for (auto& e : h->pev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
-  auto gevent = [&](int g, int i) { return h->gev[(size_t)g * (nlev + 2) + i]; };
-  cudaStream_t sa = h->side;  // assembly of the levels >= 1
+  auto gevent = [&](int g, int i) { return h->gev[(size_t)g * (nlev + 4) + i]; };
   // compact POTRF by default (measured faster in the pipeline: the instruction cache is
   // cold at every launch); IETIDP_POTRF=unrolled selects the fully unrolled kernel
   static const bool potrf_compact = !(getenv("IETIDP_POTRF") && !strcmp(getenv("IETIDP_POTRF"), "unrolled"));
-  IETI_CUDA(cudaEventRecord(h->fev[0], st));  // level 0 assembled, flags initialised
-  IETI_CUDA(cudaStreamWaitEvent(sa, h->fev[0], 0));
-  for (int L = 1; L < nlev; ++L) assemble(L, sa);
-  IETI_CUDA(cudaEventRecord(h->fev[1], sa));  // every front assembled
   // the forward sweep of the loads rides on the groups' side streams (one column chunk)
   h->fwd_in_factor = h->nrhs <= 16;
   if (expl) h->wtiles.zero(st);  // W_k is accumulated block row by block row
-  if (h->fwd_in_factor) {
-    h->Xf.zero(st);
-    if (h->sc_fx_dst.n) {
-      k_scatter<<<grid_for((long long)h->sc_fx_dst.n, 256), 256, 0, st>>>(
-          (long long)h->sc_fx_dst.n, h->sc_fx_dst.p, h->sc_fx_src.p, h->fval.p, h->Xf.p);
-      IETI_LAUNCHED(h);
-    }
-  }
+  if (h->fwd_in_factor) h->Xf.zero(st);
   IETI_CUDA(cudaEventRecord(h->fev[2], st));
   size_t npan = 0;
   for (int g = 0; g < G; ++g) {
     cudaStream_t sg = g == 0 ? st : h->gst[g];
     cudaStream_t s2 = h->gside[g];
     if (g > 0) IETI_CUDA(cudaStreamWaitEvent(sg, h->fev[2], 0));
-    IETI_CUDA(cudaStreamWaitEvent(s2, h->fev[2], 0));
+    // the group's values (ietidp_set_values copies, recorded per subdomain)
+    if (!h->kev.empty())
+      for (int k = 0; k < h->n_sub; ++k)
+        if (P.sub_group[k] == g) IETI_CUDA(cudaStreamWaitEvent(sg, h->kev[k], cudaEventWaitExternal));
+    // assembly: level 0 here, the levels above on the side stream while level 0 is factored
+    assemble(P.glevels[g][0], sg);
+    if (h->fwd_in_factor && P.gfx[g].second) {
+      k_scatter<<<grid_for(P.gfx[g].second, 256), 256, 0, sg>>>(P.gfx[g].second, h->sc_fx_dst.p + P.gfx[g].first,
+                                                                  h->sc_fx_src.p + P.gfx[g].first, h->fval.p,
+                                                                  h->Xf.p);
+      IETI_LAUNCHED_SIDE(h);
+    }
+    IETI_CUDA(cudaEventRecord(gevent(g, nlev), sg));
+    IETI_CUDA(cudaStreamWaitEvent(s2, gevent(g, nlev), 0));
+    for (int L = 1; L < nlev; ++L) assemble(P.glevels[g][L], s2);
+    IETI_CUDA(cudaEventRecord(gevent(g, nlev + 1), s2));  // the group's fronts assembled
     const LevelPlan::Panel* wacc_last = nullptr;
     for (int L = 0; L < nlev; ++L) {
       const LevelPlan& lp = P.glevels[g][L];
@@ -770,7 +771,7 @@ void run_factor(ietidp_s* h) {
         }
       }
       IETI_CUDA(cudaEventRecord(gevent(g, L), sg));
-      if (L == 0) IETI_CUDA(cudaStreamWaitEvent(sg, h->fev[1], 0));  // parents assembled
+      if (L == 0) IETI_CUDA(cudaStreamWaitEvent(sg, gevent(g, nlev + 1), 0));  // parents assembled
       for (auto& sy : lp.syrk) {
         k_gemm<false><<<sy.second, 128, GEMM_SMEM, sg>>>(GW + sy.first, pool, pool, pool, rel);
         IETI_LAUNCHED_SIDE(h);
@@ -799,11 +800,11 @@ void run_factor(ietidp_s* h) {
       }
     }
     // join: the group's main and side streams into the caller's stream
-    IETI_CUDA(cudaEventRecord(gevent(g, nlev), s2));
-    IETI_CUDA(cudaStreamWaitEvent(st, gevent(g, nlev), 0));
+    IETI_CUDA(cudaEventRecord(gevent(g, nlev + 2), s2));
+    IETI_CUDA(cudaStreamWaitEvent(st, gevent(g, nlev + 2), 0));
     if (g > 0) {
-      IETI_CUDA(cudaEventRecord(gevent(g, nlev + 1), sg));
-      IETI_CUDA(cudaStreamWaitEvent(st, gevent(g, nlev + 1), 0));
+      IETI_CUDA(cudaEventRecord(gevent(g, nlev + 3), sg));
+      IETI_CUDA(cudaStreamWaitEvent(st, gevent(g, nlev + 3), 0));
     }
   }
   IETI_CHECK_LAUNCH();

@@ -116,6 +116,9 @@ struct ietidp_s {
   cudaStream_t side = nullptr;
   std::vector<cudaStream_t> gst, gside;  // per subdomain group: main and side streams
   std::vector<cudaEvent_t> gev;          // per group: events (see run_factor)
+  cudaStream_t cstream = nullptr;        // host-to-device copies of ietidp_set_values
+  std::vector<cudaEvent_t> kev;          // per subdomain: its last set_values copy done
+  cudaEvent_t hp_ev_set = nullptr;
   std::vector<cudaEvent_t> fev;  // [0..levels): level's panels done; [levels]: side done
   std::vector<cudaEvent_t> pev;  // per panel: POTRF done (progressive inverse)
   bool fwd_in_factor = false;    // the forward sweep of the loads ran on the side stream

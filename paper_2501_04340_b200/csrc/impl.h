@@ -182,6 +182,8 @@ struct Plan {
   std::vector<int> level_sn;  // supernode ids grouped by level
   std::vector<LevelPlan> levels;                 // all supernodes by level: assembly and sweeps
   int ngroups = 1;                               // subdomain groups of the factorisation
+  std::vector<int> sub_group;                    // group of each subdomain (contiguous blocks)
+  std::vector<std::pair<long long, long long>> gfx;  // per group: range of the load scatter list
   std::vector<std::vector<LevelPlan>> glevels;   // [group][level]: panels, SYRK, inverse, sweep lists
   int g_off = 0, g_n = 0;                       // GemmWork: G_k^T = L_PI L_II^-1
   std::vector<std::vector<int>> roots_by_level; // subdomains whose r_I root front is at level L
