@@ -54,6 +54,23 @@ __device__ __forceinline__ void load_tile_async(double* dst, const double* src, 
     cp_async16(dst + r * TB + ((c ^ (r & 7)) << 1), src + r * TB + 2 * c);
   }
 }
+// the same with an L2 eviction-priority hint (createpolicy: 1 = evict_last, 2 = evict_first)
+__device__ __forceinline__ void load_tile_async_hint(double* dst, const double* src, int tid, int hint) {
+  if (hint == 0) {
+    load_tile_async(dst, src, tid);
+    return;
+  }
+  unsigned long long pol;
+  if (hint == 1) asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+#pragma unroll 4
+  for (int q = tid; q < TB * TB / 2; q += 256) {
+    const int r = q >> 5, c = q & 31;
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + r * TB + ((c ^ (r & 7)) << 1));
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
+                 "l"(src + r * TB + 2 * c), "l"(pol));
+  }
+}
 
 struct TmvArgs {
   const LoopWork* work;
@@ -74,6 +91,7 @@ struct TmvArgs {
   const long long* pboff;  // SYM: first partial block of each (subdomain, block) (SlotRed)
   const SymWork* swork;    // SYM: work items (row segments)
   int maxseg;              // SYM: segments per block row (npart layout)
+  int l2hint;              // SYM: L2 eviction priority of the tile stream (0 none, 1 last, 2 first)
   int slot_in;             // FWD/PRE1/SYM: vin is already in slot order (B^T, weights applied)
   int nPmax, ncols, c_off;
   const PcgState* st;
@@ -550,8 +568,9 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
         if (wi.j1 < wi.o) gather_async<VS>(vec + nst * TB * VS, wi.o * TB, (wi.o + 1) * TB, d, A, ncl);
         if (tid == 0) s_sw[ii % NVB] = wi;
       }
-      load_tile_async(ring + gslot * TILE_ELEMS,
-                      A.tiles + d.tile_off + (long long)(wi.o * (wi.o + 1) / 2 + wi.j0 + is) * TILE_ELEMS, tid);
+      load_tile_async_hint(ring + gslot * TILE_ELEMS,
+                           A.tiles + d.tile_off + (long long)(wi.o * (wi.o + 1) / 2 + wi.j0 + is) * TILE_ELEMS, tid,
+                           A.l2hint);
       if (++is == nsteps_of(wi)) {
         is = 0;
         if (++ii < nitems) wi = A.swork[items[ii]];
@@ -1913,6 +1932,16 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.wsym.vout = h->xI.p;
   a.wsym.gpart = h->n_primal ? h->gpart.p : nullptr;
   a.ssym = sym_args(h, h->stiles.p, nc);
+  {
+    // one RHS with S_II's tiles smaller than ~2/3 of the L2: keep them resident across
+    // iterations (evict_last) and stream W_k's past them (evict_first)
+    const double sbytes = (double)h->stiles.n * sizeof(double);
+    int l2 = 0;
+    IETI_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->opt.device));
+    const bool keep = nc == 1 && sbytes < 0.66 * l2 && !(getenv("IETIDP_L2HINT") && atoi(getenv("IETIDP_L2HINT")) == 0);
+    a.ssym.l2hint = keep ? 1 : 0;
+    a.wsym.l2hint = keep ? 2 : 0;
+  }
   a.ssym.vin = a.rslot;
   a.ssym.slot_in = 1;
   a.ssym.vout = h->zI.p;
