@@ -1192,7 +1192,7 @@ __device__ __forceinline__ void coarse_phase(const PcgArgs& P, double* smem) {
 
 // z = S_PP^-1 g, computed by every CTA into shared memory (ng x nc; redundant, no barrier)
 // -- for coarse problems up to COARSE_LOCAL_MAX primal DOFs (S_PP^-1 read by every CTA)
-constexpr int COARSE_LOCAL_MAX = 64;
+constexpr int COARSE_LOCAL_MAX = 32;
 __device__ __forceinline__ void coarse_local(const PcgArgs& P, double* zs) {
   const int nc = P.ncols, tid = threadIdx.x;
   double* g = zs + P.ng * nc;
