@@ -1323,7 +1323,39 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     // phase (a slot shared by several multipliers would be summed repeatedly)
     const bool fold = P.ncols == 1 && P.fold;
     if (!fold) reduce_phase(P.wsym, P.slot_red, P.n_slots);
-    if (P.ng > 0 && P.ng <= COARSE_LOCAL_MAX) {
+    if (P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT) {
+      // one row per thread: the row's folded operator value is loaded first, so that
+      // its latency chain overlaps the per-CTA coarse solve; then the coarse term
+      const int j = blockIdx.x * VT + threadIdx.x;
+      double pre[2] = {0.0, 0.0}, sg[2] = {0.0, 0.0};
+      LamDev L{};
+      if (j < P.m) {
+        L = P.lam[j];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          pre[q] = sym_value(P.wsym.spart, P.slot_red, L.slot[q], 1, 0);
+          sg[q] = (double)L.sign[q];
+        }
+      }
+      coarse_local(P, smem);  // small coarse problem: every CTA solves it (no barrier)
+      double dot = 0.0;
+      if (j < P.m) {
+        double val = 0.0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int a = L.slot[q];
+          const int np = P.ct.np[a];
+          const double* Gr = P.ct.G + P.ct.goff[a];
+          const int* gid = P.ct.prim_gid + P.ct.poff[a];
+          double sc = 0.0;
+          for (int q2 = 0; q2 < np; ++q2) sc += Gr[q2] * smem[gid[q2]];
+          val += sg[q] * (pre[q] + sc);
+        }
+        P.q[j] = val;
+        dot = val * P.p[j];
+      }
+      block_col_reduce(dot, 1, 1, pq);
+    } else if (P.ng > 0 && P.ng <= COARSE_LOCAL_MAX) {
       if (!fold) pcg_barrier(P);
       coarse_local(P, smem);  // small coarse problem: every CTA solves it (no barrier)
       bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, true, fold ? &P.wsym : nullptr, smem);
