@@ -1243,8 +1243,11 @@ __device__ __forceinline__ void coarse_spread_z(const PcgArgs& P) {
 
 // y[slot][c] of a symmetric pass: the row-segment partials plus the transposed partials
 // (the same fixed order as sym_reduce_item)
+__device__ __forceinline__ double sym_value_sr(const double* spart, const SlotRed& sr, int nc, int c);
 __device__ __forceinline__ double sym_value(const double* spart, const SlotRed* sred, long long a, int nc, int c) {
-  const SlotRed sr = sred[a];
+  return sym_value_sr(spart, sred[a], nc, c);
+}
+__device__ __forceinline__ double sym_value_sr(const double* spart, const SlotRed& sr, int nc, int c) {
   const double* P0 = spart + sr.base * nc + c;
   const long long st = (long long)TB * nc;
   double v0 = 0.0;
@@ -1317,23 +1320,29 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
   if (EXPL) {
     // W pass; then every CTA solves the coarse problem itself and folds the pass's
     // partial sums into the gather (no reduction phase, one barrier)
-    sym_phase<NCP, STAGES>(P.wsym, P.cta_ptr, P.cta_items, P.ncp, smem);
-    pcg_barrier(P);
     // one column: the partial sums are folded into the gather; several: a reduction
     // phase (a slot shared by several multipliers would be summed repeatedly)
     const bool fold = P.ncols == 1 && P.fold;
+    const bool row1 = P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;
+    const int j = blockIdx.x * VT + threadIdx.x;
+    LamDev L{};
+    SlotRed sr[2] = {};
+    sym_phase<NCP, STAGES>(P.wsym, P.cta_ptr, P.cta_items, P.ncp, smem);
+    if (row1 && j < P.m) {  // static row data, loaded ahead of the barrier
+      L = P.lam[j];
+      sr[0] = P.slot_red[L.slot[0]];
+      sr[1] = P.slot_red[L.slot[1]];
+    }
+    pcg_barrier(P);
     if (!fold) reduce_phase(P.wsym, P.slot_red, P.n_slots);
-    if (P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT) {
+    if (row1) {
       // one row per thread: the row's folded operator value is loaded first, so that
       // its latency chain overlaps the per-CTA coarse solve; then the coarse term
-      const int j = blockIdx.x * VT + threadIdx.x;
       double pre[2] = {0.0, 0.0}, sg[2] = {0.0, 0.0};
-      LamDev L{};
       if (j < P.m) {
-        L = P.lam[j];
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
-          pre[q] = sym_value(P.wsym.spart, P.slot_red, L.slot[q], 1, 0);
+          pre[q] = sym_value_sr(P.wsym.spart, sr[q], 1, 0);
           sg[q] = (double)L.sign[q];
         }
       }
@@ -1384,9 +1393,31 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
 template <int NCP, int STAGES, bool EXPL>
 __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, double* rz) {
   if (EXPL) {
+    const bool row1 = P.ncols == 1 && P.fold && P.m <= (int)gridDim.x * VT;
+    const int j = blockIdx.x * VT + threadIdx.x;
+    LamDev L{};
+    SlotRed sr[2] = {};
+    double w2[2] = {0.0, 0.0};
     sym_phase<NCP, STAGES>(P.ssym, P.cta_ptr, P.cta_items, P.ncp, smem);
+    if (row1 && j < P.m) {  // static row data, loaded ahead of the barrier
+      L = P.lam[j];
+      sr[0] = P.slot_red[L.slot[0]];
+      sr[1] = P.slot_red[L.slot[1]];
+      w2[0] = P.delta[L.slot[0]];
+      w2[1] = P.delta[L.slot[1]];
+    }
     pcg_barrier(P);
-    if (P.ncols == 1 && P.fold) {
+    if (row1) {  // z = B_D (S r) row by row, r.z partials (same order as bgather_phase)
+      double dot = 0.0;
+      if (j < P.m) {
+        double val = 0.0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) val += (double)L.sign[q] * w2[q] * sym_value_sr(P.ssym.spart, sr[q], 1, 0);
+        P.z[j] = val;
+        dot = val * P.r[j];
+      }
+      block_col_reduce(dot, 1, 1, rz);
+    } else if (P.ncols == 1 && P.fold) {
       bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, &P.ssym);
     } else {
       reduce_phase(P.ssym, P.slot_red, P.n_slots);
