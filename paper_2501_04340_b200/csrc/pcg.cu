@@ -1324,16 +1324,40 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     // phase (a slot shared by several multipliers would be summed repeatedly)
     const bool fold = P.ncols == 1 && P.fold;
     const bool row1 = P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;
+    const bool row1s = P.ng > COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;  // spread coarse
     const int j = blockIdx.x * VT + threadIdx.x;
     LamDev L{};
     SlotRed sr[2] = {};
     sym_phase<NCP, STAGES>(P.wsym, P.cta_ptr, P.cta_items, P.ncp, smem);
-    if (row1 && j < P.m) {  // static row data, loaded ahead of the barrier
+    if ((row1 || row1s) && j < P.m) {  // static row data, loaded ahead of the barrier
       L = P.lam[j];
       sr[0] = P.slot_red[L.slot[0]];
       sr[1] = P.slot_red[L.slot[1]];
     }
     pcg_barrier(P);
+    if (row1s) {
+      // one row per thread: folded operator values first (in flight across the coarse
+      // phases and their barriers), then the coarse term G_k z from the spread solve
+      double pre[2] = {0.0, 0.0};
+      if (j < P.m) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) pre[q] = sym_value_sr(P.wsym.spart, sr[q], 1, 0);
+      }
+      coarse_spread(P);
+      pcg_barrier(P);
+      coarse_spread_z(P);
+      pcg_barrier(P);
+      double dot = 0.0;
+      if (j < P.m) {
+        double val = 0.0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) val += (double)L.sign[q] * (pre[q] + coarse_term(P.ct, L.slot[q], 1, 0));
+        P.q[j] = val;
+        dot = val * P.p[j];
+      }
+      block_col_reduce(dot, 1, 1, pq);
+      return;
+    }
     if (!fold) reduce_phase(P.wsym, P.slot_red, P.n_slots);
     if (row1) {
       // one row per thread: the row's folded operator value is loaded first, so that
