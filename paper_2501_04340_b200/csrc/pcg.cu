@@ -1511,14 +1511,45 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
     });
     pcg_barrier(P);
   }
+  // one column, one multiplier row per thread: the vector phases preload their row
+  // data (slots, scaling, r, p) ahead of the grid barrier and issue the load of the
+  // freshly computed vector before the column sum (same arithmetic as the general path)
+  const bool fast1 = nc == 1 && m <= (int)gridDim.x * VT;
+  const int jr = blockIdx.x * VT + tid;
+  const bool myrow = fast1 && jr < m;
   while (run) {
     apply_F_phases<NCP, STAGES, EXPL>(P, smem, pq);  // q = F p
+    LamDev Lr{};
+    double r_pre = 0.0, p_pre = 0.0, d0 = 0.0, d1 = 0.0;
+    if (myrow) {
+      Lr = P.lam[jr];
+      r_pre = P.r[jr];
+      p_pre = P.p[jr];
+      d0 = P.delta[Lr.slot[0]];
+      d1 = P.delta[Lr.slot[1]];
+    }
     pcg_barrier(P);
     // alpha, lambda and r
+    const double qv = myrow ? P.q[jr] : 0.0;
     colsum_all(pq, nc, s_sum);
     if (tid < nc) s_coef[tid] = s_act[tid] ? s_rz[tid] / s_sum[tid] : 0.0;
     __syncthreads();
-    {
+    if (fast1) {
+      double acc = 0.0;
+      if (myrow) {
+        double rv = r_pre;
+        if (s_act[0]) {
+          const double a = s_coef[0];
+          P.lamv[jr] += a * p_pre;
+          rv -= a * qv;
+          P.r[jr] = rv;
+        }
+        P.rslot[Lr.slot[0]] = (double)Lr.sign[0] * d0 * rv;
+        P.rslot[Lr.slot[1]] = (double)Lr.sign[1] * d1 * rv;
+        acc = rv * rv;
+      }
+      block_col_reduce(acc, 1, 1, rr);
+    } else {
       double acc = 0.0;
       const bool act = cc < nc && s_act[cc];
       const double a = cc < nc ? s_coef[cc] : 0.0;
@@ -1552,8 +1583,11 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
       break;
     }
     apply_M_phases<NCP, STAGES, EXPL>(P, smem, rz);  // z = M r
+    double p_old = 0.0;
+    if (myrow) p_old = P.p[jr];
     pcg_barrier(P);
     // beta, p
+    const double zv = myrow ? P.z[jr] : 0.0;
     colsum_all(rz, nc, s_sum);
     if (tid < nc) {
       const double rzn = s_sum[tid];
@@ -1561,7 +1595,17 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
       if (s_new[tid]) s_rz[tid] = rzn;
     }
     __syncthreads();
-    {
+    if (fast1) {
+      if (myrow) {
+        double pv = p_old;
+        if (s_new[0]) {
+          pv = zv + s_coef[0] * pv;
+          P.p[jr] = pv;
+        }
+        P.pslot[Lr.slot[0]] = (double)Lr.sign[0] * 1.0 * pv;
+        P.pslot[Lr.slot[1]] = (double)Lr.sign[1] * 1.0 * pv;
+      }
+    } else {
       const bool act = cc < nc && s_new[cc];
       const double bta = cc < nc ? s_coef[cc] : 0.0;
       rows([&](long long e, int j) {
