@@ -1084,20 +1084,26 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 __device__ int g_prof_n;  // barrier counter of the profiled launch (CTA 0)
 
+// Grid barrier of the persistent kernel: arrival counter bar[0], generation bar[1].
+// Thread 0 of each CTA arrives with an acquire-release atomic (cumulative over the
+// CTA's writes ordered before it by __syncthreads), the last arrival resets the
+// counter and publishes the next generation with a release; the others poll the
+// generation with acquire loads.
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   __syncthreads();
   if (threadIdx.x == 0) {
-    volatile unsigned* gen = bar + 1;
-    const unsigned g = *gen;
-    __threadfence();
-    if (atomicAdd(bar, 1u) == gridDim.x - 1) {
-      bar[0] = 0;
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
+    unsigned g, old;
+    asm volatile("ld.relaxed.gpu.global.u32 %0, [%1];" : "=r"(g) : "l"(bar + 1) : "memory");
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(bar) : "memory");
+    if (old == gridDim.x - 1) {
+      asm volatile("st.relaxed.gpu.global.u32 [%0], 0;" ::"l"(bar) : "memory");
+      asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(bar + 1) : "memory");
     } else {
-      while (*gen == g) __nanosleep(20);
+      unsigned cur;
+      do {
+        asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(cur) : "l"(bar + 1) : "memory");
+      } while (cur == g);
     }
-    __threadfence();
   }
   __syncthreads();
 }
