@@ -1464,7 +1464,7 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
 }
 
 template <int NCP, int STAGES, bool EXPL>
-__global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
+__global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double s_rz[IETIDP_MAX_RHS], s_r0[IETIDP_MAX_RHS], s_coef[IETIDP_MAX_RHS], s_sum[IETIDP_MAX_RHS];
   __shared__ int s_act[IETIDP_MAX_RHS], s_new[IETIDP_MAX_RHS], s_iters[IETIDP_MAX_RHS];
@@ -1521,6 +1521,7 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
   // data (slots, scaling, r, p) ahead of the grid barrier and issue the load of the
   // freshly computed vector before the column sum (same arithmetic as the general path)
   const bool fast1 = nc == 1 && m <= (int)gridDim.x * VT;
+  constexpr int UR = NCP == 1 ? 1 : 4;  // rows in flight per thread in the vector phases
   const int jr = blockIdx.x * VT + tid;
   const bool myrow = fast1 && jr < m;
   while (run) {
@@ -1556,19 +1557,50 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
       }
       block_col_reduce(acc, 1, 1, rr);
     } else {
+      // four rows per thread in flight (all loads first); the same arithmetic and
+      // accumulation order as a one-row loop
       double acc = 0.0;
       const bool act = cc < nc && s_act[cc];
       const double a = cc < nc ? s_coef[cc] : 0.0;
-      rows([&](long long e, int j) {
-        double rv = P.r[e];
-        if (act) {
-          P.lamv[e] += a * P.p[e];
-          rv -= a * P.q[e];
-          P.r[e] = rv;
+      const int stride = nb * R;
+      if (cc < nc)
+        for (int j0 = blockIdx.x * R + rl; j0 < m; j0 += UR * stride) {
+          double rv[UR], pv[UR], qv4[UR], lv[UR], w0[UR], w1[UR];
+          LamDev L4[UR];
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int j = j0 + u * stride;
+            if (j < m) {
+              const long long e = (long long)j * nc + cc;
+              rv[u] = P.r[e];
+              pv[u] = P.p[e];
+              qv4[u] = P.q[e];
+              lv[u] = P.lamv[e];
+              L4[u] = P.lam[j];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < UR; ++u)
+            if (j0 + u * stride < m) {
+              w0[u] = P.delta[L4[u].slot[0]];
+              w1[u] = P.delta[L4[u].slot[1]];
+            }
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int j = j0 + u * stride;
+            if (j >= m) continue;
+            const long long e = (long long)j * nc + cc;
+            double r1 = rv[u];
+            if (act) {
+              P.lamv[e] = lv[u] + a * pv[u];
+              r1 -= a * qv4[u];
+              P.r[e] = r1;
+            }
+            P.rslot[(long long)L4[u].slot[0] * nc + cc] = (double)L4[u].sign[0] * w0[u] * r1;
+            P.rslot[(long long)L4[u].slot[1] * nc + cc] = (double)L4[u].sign[1] * w1[u] * r1;
+            acc += r1 * r1;
+          }
         }
-        to_slots(P, j, cc, rv, P.delta, P.rslot);
-        acc += rv * rv;
-      });
       block_col_reduce(acc, nc, P2, rr);
     }
     pcg_barrier(P);
@@ -1614,14 +1646,35 @@ __global__ void __launch_bounds__(256, 2) k_pcg(const PcgArgs P) {
     } else {
       const bool act = cc < nc && s_new[cc];
       const double bta = cc < nc ? s_coef[cc] : 0.0;
-      rows([&](long long e, int j) {
-        double pv = P.p[e];
-        if (act) {
-          pv = P.z[e] + bta * pv;
-          P.p[e] = pv;
+      const int stride = nb * R;
+      if (cc < nc)
+        for (int j0 = blockIdx.x * R + rl; j0 < m; j0 += UR * stride) {
+          double pv[UR], zv4[UR];
+          LamDev L4[UR];
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int j = j0 + u * stride;
+            if (j < m) {
+              const long long e = (long long)j * nc + cc;
+              pv[u] = P.p[e];
+              zv4[u] = P.z[e];
+              L4[u] = P.lam[j];
+            }
+          }
+#pragma unroll
+          for (int u = 0; u < UR; ++u) {
+            const int j = j0 + u * stride;
+            if (j >= m) continue;
+            const long long e = (long long)j * nc + cc;
+            double p1 = pv[u];
+            if (act) {
+              p1 = zv4[u] + bta * p1;
+              P.p[e] = p1;
+            }
+            P.pslot[(long long)L4[u].slot[0] * nc + cc] = (double)L4[u].sign[0] * 1.0 * p1;
+            P.pslot[(long long)L4[u].slot[1] * nc + cc] = (double)L4[u].sign[1] * 1.0 * p1;
+          }
         }
-        to_slots(P, j, cc, pv, nullptr, P.pslot);
-      });
     }
     if (tid < nc) s_act[tid] = s_new[tid];
     pcg_barrier(P);
