@@ -1268,12 +1268,56 @@ __device__ __forceinline__ double sym_value_sr(const double* spart, const SlotRe
 }
 
 // out = sum_k B (w) (x + G z), with the per-CTA partial of out . dotv
+template <int UR = 1>
 __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x, const double* w, double* out,
                                               const double* dotv, double* part, bool coarse,
                                               const TmvArgs* fold = nullptr, const double* zs = nullptr) {
   const int nc = P.ncols, P2 = pow2ge(nc);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
   double dot = 0.0;
+  if (UR > 1 && !fold && !zs) {
+    // UR rows per thread in flight (loads first); the row order of the dot partial is
+    // that of a one-row loop
+    const int stride = gridDim.x * R;
+    if (c < nc)
+      for (int j0 = blockIdx.x * R + rl; j0 < P.m; j0 += UR * stride) {
+        LamDev L4[UR];
+        double dv[UR], xv[UR][2], wv[UR][2];
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          const int j = j0 + u * stride;
+          if (j < P.m) {
+            L4[u] = P.lam[j];
+            dv[u] = dotv[(long long)j * nc + c];
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < UR; ++u)
+          if (j0 + u * stride < P.m)
+#pragma unroll
+            for (int q = 0; q < 2; ++q) {
+              const int a = L4[u].slot[q];
+              xv[u][q] = x[(long long)a * nc + c];
+              wv[u][q] = w ? w[a] : 1.0;
+            }
+#pragma unroll
+        for (int u = 0; u < UR; ++u) {
+          const int j = j0 + u * stride;
+          if (j >= P.m) continue;
+          double val = 0.0;
+#pragma unroll
+          for (int q = 0; q < 2; ++q) {
+            double x1 = xv[u][q];
+            if (coarse) x1 += coarse_term(P.ct, L4[u].slot[q], nc, c);
+            val += (double)L4[u].sign[q] * wv[u][q] * x1;
+          }
+          out[(long long)j * nc + c] = val;
+          dot += val * dv[u];
+        }
+      }
+    block_col_reduce(dot, nc, P2, part);
+    return;
+  }
   if (c < nc)
     for (int j = blockIdx.x * R + rl; j < P.m; j += gridDim.x * R) {
       const LamDev L = P.lam[j];
@@ -1405,7 +1449,7 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
         coarse_spread_z(P);
       }
       if (P.ng > 0 || !fold) pcg_barrier(P);
-      bgather_phase(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0, fold ? &P.wsym : nullptr);
+      bgather_phase<NCP == 1 ? 1 : 2>(P, P.xI, nullptr, P.q, P.p, pq, P.ng > 0, fold ? &P.wsym : nullptr);
     }
   } else {
     tmv_phase<FWD, NCP, STAGES>(P.fwd, P.cta_ptr, P.cta_items, P.ncp, smem);
@@ -1452,7 +1496,7 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
     } else {
       reduce_phase(P.ssym, P.slot_red, P.n_slots);
       pcg_barrier(P);
-      bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false);
+      bgather_phase<NCP == 1 ? 1 : 2>(P, P.zI, P.delta, P.z, P.r, rz, false);
     }
   } else {
     tmv_phase<PRE1, NCP, STAGES>(P.pre1, P.cta_ptr, P.cta_items, P.ncp, smem);
