@@ -1153,17 +1153,33 @@ __device__ __forceinline__ double sym_value(const double* spart, const SlotRed* 
 __device__ __forceinline__ void reduce_phase(const TmvArgs& A, const SlotRed* sred, long long n_slots) {
   const long long n = n_slots * A.ncols;
   const long long stride = (long long)gridDim.x * blockDim.x;
-  // four independent elements per thread in flight (memory-level parallelism)
+  const long long st = (long long)TB * A.ncols;
+  // four elements per thread, their partials loaded together (the sum of each element
+  // stays in index order, as in sym_value)
   for (long long e0 = (long long)blockIdx.x * blockDim.x + threadIdx.x; e0 < n; e0 += 4 * stride) {
-    double v[4];
+    const double* P0[4];
+    int cnt[4], maxc = 0;
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const long long e = e0 + u * stride;
-      v[u] = 0.0;
+      cnt[u] = 0;
+      P0[u] = A.spart;
       if (e < n) {
         const long long a = e / A.ncols;
-        v[u] = sym_value(A.spart, sred, a, A.ncols, (int)(e - a * A.ncols));
+        const SlotRed sr = sred[a];
+        P0[u] = A.spart + sr.base * A.ncols + (e - a * A.ncols);
+        cnt[u] = sr.cnt;
+        maxc = max(maxc, sr.cnt);
       }
+    }
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    for (int p = 0; p < maxc; ++p) {
+      double t[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t[u] = p < cnt[u] ? P0[u][p * st] : 0.0;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (p < cnt[u]) v[u] += t[u];
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u)

@@ -25,9 +25,13 @@ n = 10
 out = [0, 0]
 one(S[0], n, out, 0)
 print("one handle: %.3f ms per factor" % (out[0] / n * 1e3))
-ths = [threading.Thread(target=one, args=(S[i], n, out, i)) for i in range(2)]
-t0 = time.perf_counter()
-for t in ths: t.start()
-for t in ths: t.join()
-dt = time.perf_counter() - t0
-print("two handles concurrently: %.3f ms per pair of factors (%.2fx one)" % (dt / n * 1e3, dt / n / (out[0] / n)))
+for stagger in (0.0, 0.003):
+    ths = [threading.Thread(target=one, args=(S[i], n, out, i)) for i in range(2)]
+    t0 = time.perf_counter()
+    ths[0].start()
+    time.sleep(stagger)
+    ths[1].start()
+    for t in ths: t.join()
+    dt = time.perf_counter() - t0 - stagger
+    print("two handles concurrently (stagger %.1f ms): %.3f ms per pair of factors = %.2f x one"
+          % (stagger * 1e3, dt / n * 1e3, dt / n / (out[0] / n)))
