@@ -259,6 +259,10 @@ def run_ours(args, rank, world, local):
         torch.cuda.synchronize()
         barrier(world)
         launches = (S.kernel_launches() - launches0) // max(args.steps, 1)
+        # condition estimate of M_D^-1 F_DP from the last timed solve's PCG coefficients
+        # (untimed, like the paper's own estimate)
+        with torch.cuda.stream(stream):
+            c_lo, c_hi, c_k = S.estimate_condition()
         ms_step = max_over_ranks(statistics.mean(times), world, dev)
         rep = reps[-1]
 
@@ -357,6 +361,8 @@ def run_ours(args, rank, world, local):
                    "n_primal": b["n_primal"], "nrhs": nc, "l2": "flushed between timed steps (512 MB write)",
                    "replicas": world},
         "phases_ms": phases, "iters": rep["iters"], "rel_residual": max(rep["rel_residual"]),
+        "cond_estimate": {"omega_min": float(min(c_lo)), "omega_max": float(max(c_hi)),
+                          "cond_max": float(max(c_k)), "method": "Lanczos from the PCG alpha/beta (device)"},
         "f_applies_per_s": f_apply_per_s, "f_apply_us": fa_ms * 1e3, "f_apply_gbs": fa_gbs,
         "f_apply_note": "ietidp_apply_F alone (explicit loop: W_k tiles %.0f MB per apply; L2 126 MB)"
                         % (rep["f_apply_bytes"] / 1e6),

@@ -191,6 +191,24 @@ ietidp_status ietidp_apply_precond(ietidp_t h, int ncols, const double* d_x, dou
 /* The assembled coarse matrix S_PP (n_primal x n_primal, host, symmetric). */
 ietidp_status ietidp_get_coarse(ietidp_t h, double* S_PP);
 
+/* Condition estimate of the preconditioned interface operator M_D^-1 F_DP after a
+ * solve (Eq. (11): cond = omega_max / omega_min; SPEC
+ * estimate_condition): per column c, the extreme eigenvalues of the
+ * Lanczos tridiagonal built from that column's PCG coefficients alpha_j, beta_j
+ * (T_jj = 1/alpha_j + beta_{j-1}/alpha_{j-1}, T_{j,j+1} = sqrt(beta_j)/alpha_j),
+ * computed on the device by Sturm-count multisection. Outputs are host arrays of
+ * nrhs doubles (any may be NULL); a column with 0 iterations reports 0, 0, 0; one
+ * iteration gives cond = 1. The Ritz values lie inside the spectrum, so the
+ * estimate never exceeds the true condition number.
+ * Errors: E_STATE before a solve, E_CUDA. */
+ietidp_status ietidp_estimate_condition(ietidp_t h, double* omega_min, double* omega_max, double* cond);
+
+/* The PCG coefficients of the last solve (host, ld x nrhs column-major each,
+ * ld >= max iterations): alpha[c*ld + j] for j < iters[c], beta[c*ld + j] for
+ * j < iters[c] - 1 (p_{j+1} = z_{j+1} + beta_j p_j); other entries are 0.
+ * Errors: E_STATE before a solve, E_ARG (ld smaller than an iteration count). */
+ietidp_status ietidp_get_pcg_coefficients(ietidp_t h, int ld, double* alpha, double* beta);
+
 /* d_DP (host, n_lambda x nrhs column-major). */
 ietidp_status ietidp_get_rhs(ietidp_t h, double* d);
 

@@ -215,6 +215,8 @@ class DualPrimal:
         z = self.apply_M(r)
         p = z.copy()
         rz = np.sum(r * z, axis=0)
+        alphas = [[] for _ in range(nc)]  # per column: alpha_j, beta_j (Lanczos, cond_lanczos)
+        betas = [[] for _ in range(nc)]
         it = 0
         while np.any(active):
             if fixed_iters and it >= fixed_iters:
@@ -225,6 +227,8 @@ class DualPrimal:
             q = self.apply_F(p[:, a])
             pq = np.sum(p[:, a] * q, axis=0)
             alpha = rz[a] / pq
+            for c, v in zip(a, alpha):
+                alphas[c].append(v)
             lam[:, a] += alpha * p[:, a]
             r[:, a] -= alpha * q
             iters[a] += 1
@@ -239,11 +243,15 @@ class DualPrimal:
             zz = self.apply_M(r[:, a])
             rz_new = np.sum(r[:, a] * zz, axis=0)
             beta = rz_new / rz[a]
+            for c, v in zip(a, beta):
+                betas[c].append(v)
             p[:, a] = zz + beta * p[:, a]
             rz[a] = rz_new
         converged = ~active if not fixed_iters else np.ones(nc, bool)
         true_res = np.linalg.norm(d - self.apply_F(lam), axis=0) / np.where(r0 > 0, r0, 1.0)
-        return lam, dict(iters=iters, converged=converged, rel_residual=true_res)
+        return lam, dict(iters=iters, converged=converged, rel_residual=true_res,
+                         alpha=[np.array(x) for x in alphas],
+                         beta=[np.array(x[:max(len(y) - 1, 0)]) for x, y in zip(betas, alphas)])
 
     # ---- recovery, Eqs. (8)-(9) -------------------------------------------
     def recover(self, lam):
@@ -258,6 +266,43 @@ class DualPrimal:
             u[L.prim] = pk
             us.append(u)
         return us, p
+
+
+def lanczos_tridiagonal(alpha, beta):
+    """The Lanczos matrix T_k of the preconditioned operator M^-1 F from k PCG
+    iterations (the CG-Lanczos relation, e.g. Saad, Iterative Methods, §6.7.3;
+    SURVEY §8(c) Q25): T_jj = 1/alpha_j + beta_{j-1}/alpha_{j-1} (beta_{-1} = 0),
+    T_{j,j+1} = T_{j+1,j} = sqrt(beta_j)/alpha_j, j = 0..k-1."""
+    alpha = np.asarray(alpha, float)
+    beta = np.asarray(beta, float)
+    k = len(alpha)
+    T = np.zeros((k, k))
+    for j in range(k):
+        T[j, j] = 1.0 / alpha[j] + (beta[j - 1] / alpha[j - 1] if j > 0 else 0.0)
+        if j + 1 < k:
+            T[j, j + 1] = T[j + 1, j] = np.sqrt(beta[j]) / alpha[j]
+    return T
+
+
+def cond_lanczos(alpha, beta):
+    """(omega_min, omega_max, cond) of M_D^-1 F_DP estimated from the PCG coefficients:
+    the extreme eigenvalues of T_k (cond = omega_max / omega_min).
+    0 iterations: (0, 0, 0)."""
+    if len(alpha) == 0:
+        return 0.0, 0.0, 0.0
+    w = np.linalg.eigvalsh(lanczos_tridiagonal(alpha, beta))
+    return w[0], w[-1], w[-1] / w[0]
+
+
+def cond_dense(D):
+    """(omega_min, omega_max, cond) of M_D^-1 F_DP from its dense spectrum (small
+    cases only): F_DP and M_D^-1 applied to the identity, eigenvalues of the product
+    (similar to the symmetric M^1/2 F M^1/2, so real and positive)."""
+    E = np.eye(D.nl)
+    F = D.apply_F(E)
+    M = D.apply_M(E)
+    w = np.sort(np.linalg.eigvals(M @ F).real)
+    return w[0], w[-1], w[-1] / w[0]
 
 
 def solve(bundle, tol=None, max_iter=500, fixed_iters=0, scaling=None, check_spd=False):

@@ -1543,6 +1543,10 @@ void analyze_all(ietidp_s* h) {
   h->gc.alloc((size_t)std::max(ng, 1) * nc);
   h->partial.alloc(4 * 1024 * (size_t)nc);
   h->state.alloc(16 * IETIDP_MAX_RHS + 64);
+  h->coef_ld = std::max(1, std::max(h->opt.max_iter, h->opt.fixed_iters));
+  h->cgcoef.alloc(2 * (size_t)nc * h->coef_ld);
+  h->cgcoef.zero(h->stream);
+  h->cond_out.alloc(3 * (size_t)nc);
   h->tmp_in.alloc(m);
   h->tmp_out.alloc(m);
   h->U.alloc(uo);

@@ -455,6 +455,34 @@ ietidp_status ietidp_get_coarse(ietidp_t h, double* S) {
   });
 }
 
+ietidp_status ietidp_estimate_condition(ietidp_t h, double* omega_min, double* omega_max, double* cond) {
+  return guard(h, [&]() {
+    require(h->solved, IETIDP_E_STATE, "condition estimate before a solve");
+    set_device(h);
+    ieti::run_estimate_condition(h, omega_min, omega_max, cond);
+  });
+}
+
+ietidp_status ietidp_get_pcg_coefficients(ietidp_t h, int ld, double* alpha, double* beta) {
+  return guard(h, [&]() {
+    require(h->solved, IETIDP_E_STATE, "PCG coefficients before a solve");
+    const int nc = h->nrhs, cl = h->coef_ld;
+    int kmax = 0;
+    for (int c = 0; c < nc; ++c) kmax = std::max(kmax, h->rep.iters[c]);
+    require(ld >= kmax && ld >= 0, IETIDP_E_ARG, "ld smaller than the iteration count");
+    std::vector<double> co(2 * (size_t)nc * cl);
+    IETI_CUDA(cudaMemcpyAsync(co.data(), h->cgcoef.p, co.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+    IETI_CUDA(cudaStreamSynchronize(h->stream));
+    for (int c = 0; c < nc; ++c) {
+      const int k = std::min(h->rep.iters[c], cl);
+      for (int j = 0; j < ld; ++j) {
+        if (alpha) alpha[(size_t)c * ld + j] = j < k ? co[(size_t)c * cl + j] : 0.0;
+        if (beta) beta[(size_t)c * ld + j] = j < k - 1 ? co[(size_t)(nc + c) * cl + j] : 0.0;
+      }
+    }
+  });
+}
+
 ietidp_status ietidp_get_rhs(ietidp_t h, double* d) {
   return guard(h, [&]() {
     require(h->factored, IETIDP_E_STATE, "rhs before factor");

@@ -190,6 +190,9 @@ struct ietidp_s {
   ieti::DevBuf<double> gpart, zc, gc;     // coarse partials per loop CTA; coarse solution; coarse rhs
   ieti::DevBuf<double> partial;           // per-block dot partials
   ieti::DevBuf<double> state;             // PCG scalars (see pcg.cu)
+  ieti::DevBuf<double> cgcoef;            // PCG alpha_j / beta_j per column (Lanczos condition estimate)
+  int coef_ld = 0;                        // its leading dimension (max iterations)
+  ieti::DevBuf<double> cond_out;          // per column: omega_min, omega_max, cond
   ieti::DevBuf<double> tmp_in, tmp_out;   // col-major <-> interleaved staging
   ieti::DevBuf<double> U;                 // subdomain solutions u^(k), n_k x nrhs col-major
   int n_slots = 0, sum_nP = 0;
@@ -209,6 +212,7 @@ void run_solve(ietidp_s* h);                   // pcg.cu
 void run_apply_F(ietidp_s* h, int ncols, const double* x, double* y);
 void run_apply_M(ietidp_s* h, int ncols, const double* x, double* y);
 void run_recover(ietidp_s* h);                 // coarse.cu
+void run_estimate_condition(ietidp_s* h, double* omega_min, double* omega_max, double* cond);  // pcg.cu
 void transpose_in(ietidp_s* h, int rows, int ncols, const double* colmajor, double* inter);
 void transpose_out(ietidp_s* h, int rows, int ncols, const double* inter, double* colmajor);
 }  // namespace ieti

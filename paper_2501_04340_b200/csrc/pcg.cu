@@ -887,7 +887,7 @@ __device__ void active_after(const PcgState* st, const double* rr_part, int* act
 __global__ void __launch_bounds__(VT)
     k_cg_alpha(int m, PcgState* __restrict__ st, const double* __restrict__ pq_part, double* __restrict__ lam,
                double* __restrict__ r, const double* __restrict__ p, const double* __restrict__ q,
-               double* __restrict__ rr_part) {
+               double* __restrict__ rr_part, double* __restrict__ coef, int coef_ld) {
   if (st->done) return;
   const int ncols = st->ncols;
   __shared__ double pq[IETIDP_MAX_RHS], alpha[IETIDP_MAX_RHS];
@@ -896,6 +896,7 @@ __global__ void __launch_bounds__(VT)
   if (threadIdx.x < ncols) {
     const int c = threadIdx.x;
     alpha[c] = st->active[c] ? st->rz[c] / pq[c] : 0.0;
+    if (blockIdx.x == 0 && st->active[c] && st->iters[c] < coef_ld) coef[c * coef_ld + st->iters[c]] = alpha[c];
   }
   __syncthreads();
   const int P2 = pow2ge(ncols);
@@ -920,7 +921,8 @@ __global__ void __launch_bounds__(VT)
 
 __global__ void __launch_bounds__(VT)
     k_cg_beta(int m, const PcgState* __restrict__ st, const double* __restrict__ rr_part,
-              const double* __restrict__ rz_part, double* __restrict__ p, const double* __restrict__ z) {
+              const double* __restrict__ rz_part, double* __restrict__ p, const double* __restrict__ z,
+              double* __restrict__ coef, int coef_ld) {
   if (st->done) return;
   const int ncols = st->ncols;
   __shared__ int act[IETIDP_MAX_RHS];
@@ -928,7 +930,12 @@ __global__ void __launch_bounds__(VT)
   active_after(st, rr_part, act);
   reduce_cols(rz_part, NBLK, ncols, rz);
   __syncthreads();
-  if (threadIdx.x < ncols) beta[threadIdx.x] = rz[threadIdx.x] / st->rz[threadIdx.x];
+  if (threadIdx.x < ncols) {
+    const int c = threadIdx.x;
+    beta[c] = rz[c] / st->rz[c];
+    // iteration index j = st->iters[c] (k_ctl increments it after this kernel)
+    if (blockIdx.x == 0 && act[c] && st->iters[c] < coef_ld) coef[(ncols + c) * coef_ld + st->iters[c]] = beta[c];
+  }
   __syncthreads();
   const int P2 = pow2ge(ncols);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
@@ -1075,6 +1082,8 @@ struct PcgArgs {
   double* gc;                      // coarse right-hand side g (larger coarse problems)
   int fold;                        // one column: fold the symmetric partials into the gathers
   long long n_slots;
+  double* coef;  // PCG coefficients: alpha_j of column c at coef[c*coef_ld + j], beta_j at coef[(ncols+c)*coef_ld + j]
+  int coef_ld;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1599,7 +1608,10 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     // alpha, lambda and r
     const double qv = myrow ? P.q[jr] : 0.0;
     colsum_all(pq, nc, s_sum);
-    if (tid < nc) s_coef[tid] = s_act[tid] ? s_rz[tid] / s_sum[tid] : 0.0;
+    if (tid < nc) {
+      s_coef[tid] = s_act[tid] ? s_rz[tid] / s_sum[tid] : 0.0;
+      if (blockIdx.x == 0 && s_act[tid] && s_iters[tid] < P.coef_ld) P.coef[tid * P.coef_ld + s_iters[tid]] = s_coef[tid];
+    }
     __syncthreads();
     if (fast1) {
       double acc = 0.0;
@@ -1690,7 +1702,10 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     if (tid < nc) {
       const double rzn = s_sum[tid];
       s_coef[tid] = rzn / s_rz[tid];
-      if (s_new[tid]) s_rz[tid] = rzn;
+      if (s_new[tid]) {
+        s_rz[tid] = rzn;
+        if (blockIdx.x == 0 && s_iters[tid] - 1 < P.coef_ld) P.coef[(nc + tid) * P.coef_ld + s_iters[tid] - 1] = s_coef[tid];
+      }
     }
     __syncthreads();
     if (fast1) {
@@ -2009,10 +2024,11 @@ static void iteration_body(ietidp_s* h, PcgState* st, int use_graph) {
   double* rr_part = h->partial.p + NBLK * nc;
   double* rz_part = h->partial.p + 2 * NBLK * nc;
   apply_F_inter(h, nc, h->p_vec.p, h->q_vec.p, st, h->p_vec.p, pq_part);
-  k_cg_alpha<<<NBLK, VT, 0, h->stream>>>(m, st, pq_part, h->lam_vec.p, h->r_vec.p, h->p_vec.p, h->q_vec.p, rr_part);
+  k_cg_alpha<<<NBLK, VT, 0, h->stream>>>(m, st, pq_part, h->lam_vec.p, h->r_vec.p, h->p_vec.p, h->q_vec.p, rr_part,
+                                        h->cgcoef.p, h->coef_ld);
   IETI_LAUNCHED(h);
   apply_M_inter(h, nc, h->r_vec.p, h->z_vec.p, st, rr_part, 1, h->r_vec.p, rz_part);
-  k_cg_beta<<<NBLK, VT, 0, h->stream>>>(m, st, rr_part, rz_part, h->p_vec.p, h->z_vec.p);
+  k_cg_beta<<<NBLK, VT, 0, h->stream>>>(m, st, rr_part, rz_part, h->p_vec.p, h->z_vec.p, h->cgcoef.p, h->coef_ld);
   IETI_LAUNCHED(h);
   k_ctl<<<1, 64, 0, h->stream>>>(st, rr_part, rz_part, (unsigned long long)h->cond_handle, use_graph);
   IETI_LAUNCHED(h);
@@ -2232,6 +2248,8 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.nPmax = std::max(h->plan.nPmax, 1);
   a.max_iter = h->opt.max_iter;
   a.fixed = h->opt.fixed_iters;
+  a.coef = h->cgcoef.p;
+  a.coef_ld = h->coef_ld;
   a.n_items = h->opt.loop == IETIDP_LOOP_EXPLICIT ? h->n_symwork : h->n_loopwork;
   a.ncp = cfg.ncp;
   if (h->n_primal * nc * 8 > cfg.smem) return false;
@@ -2319,6 +2337,125 @@ void transpose_in(ietidp_s* h, int rows, int ncols, const double* colmajor, doub
 void transpose_out(ietidp_s* h, int rows, int ncols, const double* inter, double* colmajor) {
   k_transpose<<<grid_for((long long)rows * ncols, 256), 256, 0, h->stream>>>(rows, ncols, inter, colmajor, 0);
   IETI_LAUNCHED(h);
+}
+
+// ---------------------------------------------------------------------------
+// Condition estimate (SPEC estimate_condition; "cond(M_D^-1 S) with the
+// largest and smallest absolute eigenvalue omega_max, omega_min"; SURVEY §8(c) Q25:
+// Lanczos from the PCG alpha/beta). k PCG iterations of column c define the Lanczos
+// tridiagonal of the preconditioned operator (the CG-Lanczos relation):
+//   T_jj = 1/alpha_j + beta_{j-1}/alpha_{j-1}   (beta_{-1} = 0),
+//   T_{j,j+1}^2 = beta_j / alpha_j^2,           j = 0..k-1 (beta_0..beta_{k-2} used).
+// Its extreme eigenvalues (Ritz values) are found by multisection on the Sturm count
+// (number of negative pivots of T - xI = number of eigenvalues below x): one CTA per
+// column, threads 0..127 refine omega_min and 128..255 omega_max, 128 points per round.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ int sturm_below(const double* a, const double* b2, int k, double x, double pivmin) {
+  int cnt = 0;
+  double d = a[0] - x;
+  if (fabs(d) < pivmin) d = -pivmin;
+  cnt += d < 0.0;
+  for (int i = 1; i < k; ++i) {
+    d = (a[i] - x) - b2[i - 1] / d;
+    if (fabs(d) < pivmin) d = -pivmin;
+    cnt += d < 0.0;
+  }
+  return cnt;
+}
+
+__global__ void __launch_bounds__(256) k_lanczos_cond(const PcgState* __restrict__ st, const double* __restrict__ coef,
+                                                      int ld, double* __restrict__ out) {
+  extern __shared__ double sm[];
+  const int c = blockIdx.x, nc = gridDim.x, tid = threadIdx.x;
+  const int k = min(st->iters[c], ld);
+  double* a = sm;       // diagonal of T (k)
+  double* b2 = sm + ld; // squared off-diagonal (k - 1)
+  __shared__ double s_lo[2], s_hi[2], s_red[2][256];
+  __shared__ int s_cnt[256];
+  if (k == 0) {
+    if (tid == 0) out[3 * c] = out[3 * c + 1] = out[3 * c + 2] = 0.0;
+    return;
+  }
+  const double* al = coef + (size_t)c * ld;
+  const double* be = coef + (size_t)(nc + c) * ld;
+  for (int j = tid; j < k; j += blockDim.x) {
+    a[j] = 1.0 / al[j] + (j > 0 ? be[j - 1] / al[j - 1] : 0.0);
+    if (j < k - 1) b2[j] = be[j] / (al[j] * al[j]);
+  }
+  __syncthreads();
+  // Gershgorin interval and the largest squared off-diagonal (pivot floor, as LAPACK's pivmin)
+  double glo = INFINITY, ghi = -INFINITY, bmax = 0.0;
+  for (int j = tid; j < k; j += blockDim.x) {
+    const double r = (j > 0 ? sqrt(b2[j - 1]) : 0.0) + (j < k - 1 ? sqrt(b2[j]) : 0.0);
+    glo = fmin(glo, a[j] - r);
+    ghi = fmax(ghi, a[j] + r);
+    if (j < k - 1) bmax = fmax(bmax, b2[j]);
+  }
+  s_red[0][tid] = glo;
+  s_red[1][tid] = ghi;
+  s_cnt[tid] = 0;
+  __syncthreads();
+  if (tid == 0) {
+    for (int t = 1; t < blockDim.x; ++t) {
+      glo = fmin(glo, s_red[0][t]);
+      ghi = fmax(ghi, s_red[1][t]);
+    }
+    const double w = fmax(ghi - glo, fabs(ghi)) * 1e-14 + 1e-300;
+    s_lo[0] = s_lo[1] = glo - w;
+    s_hi[0] = s_hi[1] = ghi + w;
+  }
+  __syncthreads();
+  s_red[0][tid] = bmax;
+  __syncthreads();
+  if (tid == 0)
+    for (int t = 1; t < blockDim.x; ++t) s_red[0][0] = fmax(s_red[0][0], s_red[0][t]);
+  __syncthreads();
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, s_red[0][0]);
+  const int half = tid >> 7, lane = tid & 127;
+  // half 0: eigenvalue index 0 (omega_min), half 1: index k-1 (omega_max); the
+  // eigenvalue with index e lies where the count crosses from <= e to >= e+1
+  const int e = half ? k - 1 : 0;
+  for (int round = 0; round < 12; ++round) {
+    const double lo = s_lo[half], hi = s_hi[half];
+    const double x = lo + (hi - lo) * (double)(lane + 1) / 129.0;
+    s_cnt[tid] = sturm_below(a, b2, k, x, pivmin) >= e + 1;
+    __syncthreads();
+    if (lane == 0) {
+      int i = 0;
+      while (i < 128 && !s_cnt[tid + i]) ++i;
+      const double nlo = i == 0 ? lo : lo + (hi - lo) * (double)i / 129.0;
+      const double nhi = i == 128 ? hi : lo + (hi - lo) * (double)(i + 1) / 129.0;
+      s_lo[half] = nlo;
+      s_hi[half] = nhi;
+    }
+    __syncthreads();
+    if (s_hi[0] - s_lo[0] <= 2e-16 * fabs(s_hi[0]) && s_hi[1] - s_lo[1] <= 2e-16 * fabs(s_hi[1])) break;
+  }
+  if (tid == 0) {
+    const double wmin = 0.5 * (s_lo[0] + s_hi[0]), wmax = 0.5 * (s_lo[1] + s_hi[1]);
+    out[3 * c] = wmin;
+    out[3 * c + 1] = wmax;
+    out[3 * c + 2] = wmax / wmin;
+  }
+}
+
+void run_estimate_condition(ietidp_s* h, double* omega_min, double* omega_max, double* cond) {
+  const int nc = h->nrhs, ld = h->coef_ld;
+  const size_t smem = 2 * (size_t)ld * sizeof(double);
+  if (smem > 48 * 1024)
+    IETI_CUDA(cudaFuncSetAttribute(k_lanczos_cond, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_lanczos_cond<<<nc, 256, smem, h->stream>>>(reinterpret_cast<const PcgState*>(h->state.p), h->cgcoef.p, ld,
+                                               h->cond_out.p);
+  IETI_LAUNCHED(h);
+  IETI_CHECK_LAUNCH();
+  std::vector<double> o(3 * (size_t)nc);
+  IETI_CUDA(cudaMemcpyAsync(o.data(), h->cond_out.p, o.size() * sizeof(double), cudaMemcpyDeviceToHost, h->stream));
+  IETI_CUDA(cudaStreamSynchronize(h->stream));
+  for (int c = 0; c < nc; ++c) {
+    if (omega_min) omega_min[c] = o[3 * c];
+    if (omega_max) omega_max[c] = o[3 * c + 1];
+    if (cond) cond[c] = o[3 * c + 2];
+  }
 }
 
 }  // namespace ieti

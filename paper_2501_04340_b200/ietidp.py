@@ -23,7 +23,7 @@ LOOP = {"explicit": 0, "triangular": 1}
 SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "ietidp_analyze",
            "ietidp_set_values", "ietidp_factor", "ietidp_solve", "ietidp_get_u", "ietidp_get_u_device",
            "ietidp_get_lambda_device", "ietidp_apply_F", "ietidp_apply_precond", "ietidp_get_coarse",
-           "ietidp_get_rhs", "ietidp_get_report", "ietidp_kernel_launches", "ietidp_last_error",
+           "ietidp_estimate_condition", "ietidp_get_pcg_coefficients", "ietidp_get_rhs", "ietidp_get_report", "ietidp_kernel_launches", "ietidp_last_error",
            "ietidp_status_string", "ietidp_destroy"]
 
 
@@ -80,6 +80,8 @@ def load():
         "ietidp_apply_F": (I, [P, I, P, P]),
         "ietidp_apply_precond": (I, [P, I, P, P]),
         "ietidp_get_coarse": (I, [P, P]),
+        "ietidp_estimate_condition": (I, [P, P, P, P]),
+        "ietidp_get_pcg_coefficients": (I, [P, I, P, P]),
         "ietidp_get_rhs": (I, [P, P]),
         "ietidp_get_report": (I, [P, C.POINTER(Report)]),
         "ietidp_kernel_launches": (LL, [P]),
@@ -172,6 +174,21 @@ class Solver:
         S = np.zeros((self.n_primal, self.n_primal))
         self._check(self.lib.ietidp_get_coarse(self.h, _ptr(S)))
         return S
+
+    def estimate_condition(self):
+        """(omega_min, omega_max, cond) per column of the last solve, from
+        the Lanczos tridiagonal of the PCG coefficients, computed on the device."""
+        n = self.nrhs
+        lo, hi, k = (np.zeros(n) for _ in range(3))
+        self._check(self.lib.ietidp_estimate_condition(self.h, _ptr(lo), _ptr(hi), _ptr(k)))
+        return lo, hi, k
+
+    def pcg_coefficients(self, ld):
+        """alpha, beta of the last solve: arrays (nrhs, ld), zero beyond each column's count."""
+        a = np.zeros((self.nrhs, ld))
+        b = np.zeros((self.nrhs, ld))
+        self._check(self.lib.ietidp_get_pcg_coefficients(self.h, ld, _ptr(a), _ptr(b)))
+        return a, b
 
     def get_rhs(self):
         d = np.zeros((self.nrhs, self.n_lambda))

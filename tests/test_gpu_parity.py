@@ -226,3 +226,78 @@ def test_min_degree_ordering_solution(lib, name):
     s, lam, u, rep = gpu_solve(lib, b, fixed_iters=nit, ordering="md")
     assert rel(lam, ref_f["lam"]) <= 1e-8
     assert rel(np.concatenate(u), np.concatenate(ref_f["u"])) <= 1e-8
+
+
+# ---- condition estimate (SPEC estimate_condition) ----
+
+def _check_condition(s, rep, ref_info, nrhs, coef_tol, cond_tol):
+    ld = max(max(rep["iters"]), 1)
+    a, bt = s.pcg_coefficients(ld)
+    lo, hi, k = s.estimate_condition()
+    for c in range(nrhs):
+        n = rep["iters"][c]
+        ra, rb = ref_info["alpha"][c], ref_info["beta"][c]
+        # the recorded coefficients: counts per column, values against the oracle's
+        m = min(n, len(ra))
+        assert np.all(a[c, n:] == 0) and np.all(bt[c, max(n - 1, 0):] == 0)
+        assert rel(a[c, :m], ra[:m]) <= coef_tol and rel(bt[c, :max(m - 1, 0)], rb[:max(m - 1, 0)]) <= coef_tol
+        # the device eigen-solver against a dense eigensolve of the same (GPU) coefficients
+        olo, ohi, ok = dp.cond_lanczos(a[c, :n], bt[c, :max(n - 1, 0)])
+        assert lo[c] == pytest.approx(olo, rel=1e-12) and hi[c] == pytest.approx(ohi, rel=1e-12)
+        # and against the oracle's estimate from its own run
+        rlo, rhi, rk = dp.cond_lanczos(ra, rb)
+        assert hi[c] == pytest.approx(rhi, rel=cond_tol) and k[c] == pytest.approx(rk, rel=cond_tol)
+        assert lo[c] >= 1.0 - 1e-8  # lambda_min(M_D^-1 F_DP) >= 1 (Dirichlet preconditioner)
+
+
+@pytest.mark.parametrize("name", CASES)
+def test_condition_estimate_iteration_matched(lib, name):
+    """fixed_iters = oracle N_iter: the GPU's alpha_j/beta_j equal the oracle's to 1e-8
+    (rounding only), the device Sturm multisection equals a dense eigensolve of the
+    same T_k to 1e-12, and omega_max / cond equal the oracle's estimate to 1e-8."""
+    b, ref = case(name)
+    nit = int(np.max(ref["iters"]))
+    ref_f = dp.solve(b, fixed_iters=nit)
+    s, lam, u, rep = gpu_solve(lib, b, fixed_iters=nit)
+    _check_condition(s, rep, ref_f, b["nrhs"], 1e-8, 1e-8)
+
+
+@pytest.mark.parametrize("pcg", ["persistent", "graph"])
+@pytest.mark.parametrize("name", ["C2r", "C5r"])
+def test_condition_estimate_natural_stopping(lib, name, pcg, monkeypatch):
+    """Natural stopping (each C5r column frozen at its own convergence), both PCG
+    drivers (the persistent kernel and the graph of per-phase kernels): the recorded
+    coefficients per column match the oracle's over the common iterations, and the
+    estimate matches to 1e-6 (the last Ritz value may move by one iteration's worth)."""
+    if pcg == "graph":
+        monkeypatch.setenv("IETIDP_PCG", "graph")
+    b, ref = case(name)
+    s, lam, u, rep = gpu_solve(lib, b)
+    if all(abs(x - y) == 0 for x, y in zip(rep["iters"], ref["iters"])):
+        _check_condition(s, rep, ref, b["nrhs"], 1e-8, 1e-6)
+    else:  # +-1 iteration: compare the estimate only
+        lo, hi, k = s.estimate_condition()
+        for c in range(b["nrhs"]):
+            rlo, rhi, rk = dp.cond_lanczos(ref["alpha"][c], ref["beta"][c])
+            assert hi[c] == pytest.approx(rhi, rel=1e-6)
+
+
+def test_condition_estimate_edge_cases(lib):
+    """C1: one iteration, cond = 1 (M_D^-1 F_DP = I for two subdomains); zero RHS:
+    0 iterations reports (0, 0, 0); before a solve: E_STATE."""
+    b, ref = case("C1")
+    s = lib.from_bundle(b)
+    s.factor()
+    with pytest.raises(lib.IetiError):
+        s.estimate_condition()
+    s.solve()
+    lo, hi, k = s.estimate_condition()
+    assert k[0] == pytest.approx(1.0, abs=1e-12)
+    b0 = make_bundle("C2r")
+    for sd in b0["subs"]:
+        sd["f"] = np.zeros_like(sd["f"])
+    z = lib.from_bundle(b0)
+    z.factor()
+    z.solve()
+    lo, hi, k = z.estimate_condition()
+    assert lo[0] == hi[0] == k[0] == 0.0

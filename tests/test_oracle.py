@@ -192,3 +192,61 @@ def test_cylinder_flux_error_order():
         errs.append(np.sqrt(tot + bnorm2))
     eoc = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
     assert np.all(np.abs(eoc - 2) <= 0.35), (errs, eoc)
+
+
+# ---- condition estimate (Eq. (11); SPEC estimate_condition) ----
+
+def _stub(A, Minv, d):
+    """An object with the three members DualPrimal.pcg uses, for a plain SPD system."""
+    from types import SimpleNamespace
+    return SimpleNamespace(apply_F=lambda X: A @ X, apply_M=lambda R: Minv @ R, d=d)
+
+
+def test_lanczos_recovers_known_spectrum():
+    """n PCG steps on an n x n system: T_n is similar to M^-1 A in exact arithmetic, so
+    its extreme eigenvalues are the closed-form ones built into the test matrix
+    (A = M^-1/2 Q diag(ev) Q^T M^-1/2 gives M A similar to diag(ev))."""
+    rng = np.random.default_rng(3)
+    n = 10
+    ev = np.geomspace(0.5, 40.0, n)
+    Q, _ = np.linalg.qr(rng.standard_normal((n, n)))
+    m = rng.uniform(0.5, 2.0, n)
+    Mh = np.diag(1 / np.sqrt(m))
+    A = Mh @ Q @ np.diag(ev) @ Q.T @ Mh
+    for A_, Minv in ((Q @ np.diag(ev) @ Q.T, np.eye(n)), (A, np.diag(m))):
+        lam, info = dp.DualPrimal.pcg(_stub(A_, Minv, rng.standard_normal((n, 1))), fixed_iters=n)
+        wmin, wmax, k = dp.cond_lanczos(info["alpha"][0], info["beta"][0])
+        assert len(info["alpha"][0]) == n and len(info["beta"][0]) == n - 1
+        assert abs(wmin - ev[0]) <= 1e-8 * ev[0] and abs(wmax - ev[-1]) <= 1e-8 * ev[-1]
+        assert abs(k - ev[-1] / ev[0]) <= 1e-7 * k
+    # fewer steps: Ritz values inside the spectrum (interlacing), the estimate below cond
+    lam, info = dp.DualPrimal.pcg(_stub(Q @ np.diag(ev) @ Q.T, np.eye(n), rng.standard_normal((n, 1))),
+                                  fixed_iters=4)
+    wmin, wmax, k = dp.cond_lanczos(info["alpha"][0], info["beta"][0])
+    assert ev[0] - 1e-12 <= wmin <= wmax <= ev[-1] + 1e-12 and k <= ev[-1] / ev[0]
+
+
+def test_condition_two_subdomains_is_one(bundles):
+    """C1 (two subdomains, no primal DOFs): the Dirichlet preconditioner inverts F_DP
+    exactly, M_D^-1 F_DP = I (one PCG iteration, cond = 1), by the dense spectrum too."""
+    D = dp.DualPrimal(bundles["C1"])
+    lam, info = D.pcg(tol=1e-12)
+    assert info["iters"][0] == 1
+    assert dp.cond_lanczos(info["alpha"][0], info["beta"][0])[2] == pytest.approx(1.0, abs=1e-12)
+    wmin, wmax, k = dp.cond_dense(D)
+    assert wmin == pytest.approx(1.0, abs=1e-10) and wmax == pytest.approx(1.0, abs=1e-10)
+
+
+def test_condition_lanczos_vs_dense_spectrum(bundles):
+    """C2r: the Lanczos omega_max from a converged PCG equals the dense spectrum's; the
+    dense omega_min is 1 (FETI-DP with the Dirichlet preconditioner: lambda_min(M^-1 F) >= 1,
+    attained), the Lanczos omega_min lies in [1, omega_max] and its cond below the dense one."""
+    D = dp.DualPrimal(bundles["C2r"])
+    lam, info = D.pcg(tol=1e-12)
+    lo, hi, k = dp.cond_lanczos(info["alpha"][0], info["beta"][0])
+    dlo, dhi, dk = dp.cond_dense(D)
+    assert dlo == pytest.approx(1.0, abs=1e-9)
+    assert hi == pytest.approx(dhi, rel=1e-9)
+    assert 1.0 - 1e-10 <= lo <= hi and k <= dk * (1 + 1e-10)
+    # P:262 bound shape: a small, h-independent-ish constant for this configuration
+    assert 1.0 < k < 10.0
