@@ -1027,6 +1027,15 @@ __global__ void k_init_rz(PcgState* st, const double* __restrict__ rz_part) {
   if (threadIdx.x < st->ncols) st->rz[threadIdx.x] = rz[threadIdx.x];
 }
 
+// true relative dual residual per column: sqrt(sum of the k_resid partials) / ||r_0||
+__global__ void k_resid_ratio(const double* __restrict__ part, const PcgState* __restrict__ st,
+                              double* __restrict__ out) {
+  __shared__ double s[IETIDP_MAX_RHS];
+  const int nc = st->ncols;
+  reduce_cols(part, NBLK, nc, s);
+  if (threadIdx.x < nc) out[threadIdx.x] = st->r0[threadIdx.x] > 0 ? sqrt(s[threadIdx.x]) / st->r0[threadIdx.x] : 0.0;
+}
+
 __global__ void __launch_bounds__(VT) k_resid(int m, int ncols, const double* __restrict__ d,
                                               const double* __restrict__ Fl, double* __restrict__ part) {
   const int P2 = pow2ge(ncols);
@@ -2317,14 +2326,12 @@ void finish_solve(ietidp_s* h, ietidp_report* rep) {
     apply_F_inter(h, nc, h->lam_vec.p, h->tmp_out.p, nullptr, nullptr, nullptr);
     k_resid<<<NBLK, VT, 0, h->stream>>>(m, nc, h->d_vec.p, h->tmp_out.p, part);
     IETI_LAUNCHED(h);
-    std::vector<double> hp((size_t)NBLK * nc);
-    IETI_CUDA(cudaMemcpyAsync(hp.data(), part, hp.size() * 8, cudaMemcpyDeviceToHost, h->stream));
+    double* ratio = h->cond_out.p;  // scratch (nc doubles), rewritten by the condition estimate
+    k_resid_ratio<<<1, 64, 0, h->stream>>>(part, reinterpret_cast<const PcgState*>(h->state.p), ratio);
+    IETI_LAUNCHED(h);
+    IETI_CUDA(cudaMemcpyAsync(rep->rel_residual, ratio, (size_t)nc * sizeof(double), cudaMemcpyDeviceToHost,
+                              h->stream));
     IETI_CUDA(cudaStreamSynchronize(h->stream));
-    for (int c = 0; c < nc; ++c) {
-      double s = 0.0;
-      for (int b = 0; b < NBLK; ++b) s += hp[(size_t)b * nc + c];
-      rep->rel_residual[c] = hs.r0[c] > 0 ? std::sqrt(s) / hs.r0[c] : 0.0;
-    }
   } else {
     for (int c = 0; c < nc; ++c) rep->rel_residual[c] = 0.0;
   }
