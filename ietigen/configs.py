@@ -56,6 +56,8 @@ def get(name: str) -> Config:
     'C4m<p>e<e>' -> the cylinder with the manufactured A* = sin(2 pi (r - 1/2)) e_z."""
     if name in CONFIGS:
         return CONFIGS[name]
+    if name.startswith("E27_"):
+        return paper_cube(name)
     if name.startswith("C4m"):
         p, e = name[3:].split("e")
         return replace(C4, name=name, p=int(p), e=int(e), material="one", rhs="c4_manufactured",
@@ -66,6 +68,15 @@ def get(name: str) -> Config:
         base, e = name.split("e", 1)[0], int(name.split("e", 1)[1])
         return replace(CONFIGS[base], name=name, e=e)
     raise KeyError(name)
+
+
+def paper_cube(name: str) -> Config:
+    """The paper's experiment family: 27 cube patches (3 x 3 x 3),
+    nu = 1, homogeneous manufactured A* (our reading, R14), degree p, e elements
+    per patch direction (normalised h = 1/(3e)), a box tiling of the patch
+    grid: 'E27_<tx><ty><tz>_p<p>_e<e>', e.g. 'E27_311_p2_e4' (N_sub = 3)."""
+    _, t, p, e = name.split("_")
+    return Config(name, (3, 3, 3), int(p[1:]), int(e[1:]), tuple(int(x) for x in t), tol=1e-6)
 
 
 def patch_nu(cfg: Config) -> np.ndarray:

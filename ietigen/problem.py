@@ -116,15 +116,18 @@ class Subdomain:
 
 
 def tiling_subdomains(cfg):
+    """Boxes of patches: T[a] parts along axis a, cut at floor(i N[a] / T[a]) (equal
+    blocks when T[a] divides N[a]; otherwise sizes differ by one, e.g. 3 patches in 2
+    parts -> 1 + 2, for the paper's N_sub in {2..12} on 27 patches)."""
     N, T = cfg.npatch, cfg.tiling
-    bs = [N[a] // T[a] for a in range(3)]
-    assert all(N[a] % T[a] == 0 for a in range(3))
+    assert all(1 <= T[a] <= N[a] for a in range(3))
+    cuts = [[(i * N[a]) // T[a] for i in range(T[a] + 1)] for a in range(3)]
     subs = []
     for tz in range(T[2]):
         for ty in range(T[1]):
             for tx in range(T[0]):
-                lo = (tx * bs[0], ty * bs[1], tz * bs[2])
-                hi = (lo[0] + bs[0], lo[1] + bs[1], lo[2] + bs[2])
+                lo = (cuts[0][tx], cuts[1][ty], cuts[2][tz])
+                hi = (cuts[0][tx + 1], cuts[1][ty + 1], cuts[2][tz + 1])
                 subs.append(Subdomain(len(subs), lo, hi))
     return subs
 

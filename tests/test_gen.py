@@ -258,3 +258,26 @@ def test_cylinder_curl_grad_and_loads():
         K, j = P.assemble(sd)
         ev = np.linalg.eigvalsh(K.toarray())
         assert ev.min() >= -1e-10 * ev.max()
+
+
+# ---- the paper's 27-patch experiment family (R14) ----
+
+@pytest.mark.parametrize("tiling", ["311", "221", "321", "222", "322"])
+def test_paper_cube_ngp_independent_of_h_and_p(tiling):
+    """n_gp depends on the subdomain configuration only, not on h or p (PAPER.md:180,
+    :268 "n_gp is independent of h and p")."""
+    from ietigen.problem import build
+    ngp = {build(cf.get(f"E27_{tiling}_p{p}_e{e}")).counts()["n_gp"] for p in (1, 2, 3) for e in (2, 4)}
+    assert len(ngp) == 1, ngp
+
+
+@pytest.mark.parametrize("name", ["E27_221_p2_e2", "E27_322_p1_e2"])
+def test_uneven_tiling_dd_equals_monolithic(name):
+    """Uneven box tilings (3 patches cut 1 + 2): every K_rr SPD, the DD solution equals
+    the monolithic gauged solve."""
+    from oracle import dp, brute
+    b = make_bundle(name)
+    res = dp.solve(b, tol=1e-12, check_spd=True)
+    um, _, _, _ = brute.monolithic_solve(b)
+    U, Um = np.concatenate(res["u"]), np.concatenate(um)
+    assert np.linalg.norm(U - Um) <= 1e-10 * np.linalg.norm(Um)
