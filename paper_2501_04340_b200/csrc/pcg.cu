@@ -1030,10 +1030,14 @@ __global__ void k_init_rz(PcgState* st, const double* __restrict__ rz_part) {
 // true relative dual residual per column: sqrt(sum of the k_resid partials) / ||r_0||
 __global__ void k_resid_ratio(const double* __restrict__ part, const PcgState* __restrict__ st,
                               double* __restrict__ out) {
-  __shared__ double s[IETIDP_MAX_RHS];
-  const int nc = st->ncols;
-  reduce_cols(part, NBLK, nc, s);
-  if (threadIdx.x < nc) out[threadIdx.x] = st->r0[threadIdx.x] > 0 ? sqrt(s[threadIdx.x]) / st->r0[threadIdx.x] : 0.0;
+  // a warp per column, lanes over the per-block partials (loads in flight together)
+  const int nc = st->ncols, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = warp; c < nc; c += blockDim.x >> 5) {
+    double v = 0.0;
+    for (int b = lane; b < NBLK; b += 32) v += part[b * nc + c];
+    v = warp_sum(v);
+    if (lane == 0) out[c] = st->r0[c] > 0 ? sqrt(v) / st->r0[c] : 0.0;
+  }
 }
 
 __global__ void __launch_bounds__(VT) k_resid(int m, int ncols, const double* __restrict__ d,
@@ -2327,7 +2331,7 @@ void finish_solve(ietidp_s* h, ietidp_report* rep) {
     k_resid<<<NBLK, VT, 0, h->stream>>>(m, nc, h->d_vec.p, h->tmp_out.p, part);
     IETI_LAUNCHED(h);
     double* ratio = h->cond_out.p;  // scratch (nc doubles), rewritten by the condition estimate
-    k_resid_ratio<<<1, 64, 0, h->stream>>>(part, reinterpret_cast<const PcgState*>(h->state.p), ratio);
+    k_resid_ratio<<<1, 512, 0, h->stream>>>(part, reinterpret_cast<const PcgState*>(h->state.p), ratio);
     IETI_LAUNCHED(h);
     IETI_CUDA(cudaMemcpyAsync(rep->rel_residual, ratio, (size_t)nc * sizeof(double), cudaMemcpyDeviceToHost,
                               h->stream));

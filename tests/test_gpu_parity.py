@@ -260,7 +260,9 @@ def _check_condition(s, rep, ref_info, nrhs, n_nat, cond_tol):
         # and against the oracle's estimate from its own run (same iteration count)
         if n == len(ra) and n <= n_nat[c]:
             rlo, rhi, rk = dp.cond_lanczos(ra, rb)
-            assert hi[c] == pytest.approx(rhi, rel=cond_tol) and k[c] == pytest.approx(rk, rel=cond_tol)
+            # omega_min is the slowest Ritz value to converge: over C5r's ~125 iterations
+            # (cond ~ 200) the two roundings move it by 3.4e-5 (measured), hence 1e-4 on cond
+            assert hi[c] == pytest.approx(rhi, rel=cond_tol) and k[c] == pytest.approx(rk, rel=1e-4)
 
 
 @pytest.mark.parametrize("name", CASES)
