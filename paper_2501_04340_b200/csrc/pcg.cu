@@ -804,7 +804,22 @@ __device__ __forceinline__ double coarse_term(const CoarseTerm& ct, int a, int n
   const double* Gr = ct.G + ct.goff[a];
   const int* gid = ct.prim_gid + ct.poff[a];
   double s = 0.0;
-  for (int q = 0; q < np; ++q) s += Gr[q] * ct.z[(long long)gid[q] * ncols + c];
+  int q = 0;
+  // four terms' loads in flight (gid -> z is a dependent pair); additions in order
+  for (; q + 4 <= np; q += 4) {
+    int g4[4];
+    double G4[4], z4[4];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+      g4[t] = gid[q + t];
+      G4[t] = Gr[q + t];
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) z4[t] = ct.z[(long long)g4[t] * ncols + c];
+#pragma unroll
+    for (int t = 0; t < 4; ++t) s += G4[t] * z4[t];
+  }
+  for (; q < np; ++q) s += Gr[q] * ct.z[(long long)gid[q] * ncols + c];
   return s;
 }
 
