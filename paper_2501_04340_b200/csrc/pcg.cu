@@ -1109,6 +1109,7 @@ struct PcgArgs {
   const int *gsrc_ptr, *gsrc;      // coarse partial rows per global primal
   double* gc;                      // coarse right-hand side g (larger coarse problems)
   int fold;                        // one column: fold the symmetric partials into the gathers
+  int fold_multi;                  // ... and with several columns too
   long long n_slots;
   double* coef;  // PCG coefficients: alpha_j of column c at coef[c*coef_ld + j], beta_j at coef[(ncols+c)*coef_ld + j]
   int coef_ld;
@@ -1425,9 +1426,9 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     // partial sums into the gather (no reduction phase, one barrier)
     // one column: the partial sums are folded into the gather; several: a reduction
     // phase (a slot shared by several multipliers would be summed repeatedly)
-    const bool fold = P.ncols == 1 && P.fold;
-    const bool row1 = P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;
-    const bool row1s = P.ng > COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;  // spread coarse
+    const bool fold = P.fold && (P.ncols == 1 || P.fold_multi);
+    const bool row1 = P.ncols == 1 && P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;
+    const bool row1s = P.ncols == 1 && P.ng > COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;  // spread coarse
     const int j = blockIdx.x * VT + threadIdx.x;
     LamDev L{};
     SlotRed sr[2] = {};
@@ -1544,7 +1545,7 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
         dot = val * P.r[j];
       }
       block_col_reduce(dot, 1, 1, rz);
-    } else if (P.ncols == 1 && P.fold) {
+    } else if (P.fold && (P.ncols == 1 || P.fold_multi)) {
       bgather_phase(P, P.zI, P.delta, P.z, P.r, rz, false, &P.ssym);
     } else {
       reduce_phase(P.ssym, P.slot_red, P.n_slots);
@@ -2169,7 +2170,7 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
     IETI_CUDA(cudaMemcpy(t.data(), prof.p, sizeof(unsigned long long) * std::min(n, 4096), cudaMemcpyDeviceToHost));
     n = std::min(n, 4096);
     const int ng_ = h->n_primal, nc = a.fwd.ncols ? a.fwd.ncols : h->nrhs;
-    const bool nofold = nc > 1 || !args.fold;
+    const bool nofold = (nc > 1 && !args.fold_multi) || !args.fold;
     const int per = EXPL ? 6 + (nofold ? 2 : 0) + (ng_ > COARSE_LOCAL_MAX ? 1 + (nofold ? 0 : 1) : 0) : 9,
               skip = EXPL ? 4 + (nofold ? 1 : 0) : 5;
     std::vector<double> acc(per, 0.0);
@@ -2246,6 +2247,7 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.gc = h->gc.p;
   a.n_slots = h->n_slots;
   a.fold = !(getenv("IETIDP_FOLD") && atoi(getenv("IETIDP_FOLD")) == 0);
+  a.fold_multi = getenv("IETIDP_FOLD_MULTI") && atoi(getenv("IETIDP_FOLD_MULTI")) == 1;
   a.blk = h->d_blk.p;
   a.n_blk = h->n_blk;
   a.lam = h->lam.p;
