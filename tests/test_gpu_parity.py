@@ -332,3 +332,19 @@ def test_paper_cube_family(lib, name):
     s, lam, u, rep = gpu_solve(lib, b, fixed_iters=nit)
     assert rel(np.concatenate(u), np.concatenate(ref_f["u"])) <= 1e-8
     _check_condition(s, rep, ref_f, 1, [nit], 1e-6)
+
+
+def test_fold_multi_bitwise(lib, monkeypatch):
+    """IETIDP_FOLD_MULTI=1 (several RHS: symmetric-pass partials summed inside the
+    gathers, no reduction phase) sums the same partials in the same order: lambda and u
+    bit-identical to the default path (where the time goes in C5)."""
+    b, _ = case("C5r")
+    s = lib.from_bundle(b)
+    s.factor()
+    lam0, _ = s.solve()
+    u0 = s.get_u(5)
+    monkeypatch.setenv("IETIDP_FOLD_MULTI", "1")
+    t = lib.from_bundle(b)
+    t.factor()
+    lam1, _ = t.solve()
+    assert np.array_equal(lam0, lam1) and np.array_equal(u0, t.get_u(5))
