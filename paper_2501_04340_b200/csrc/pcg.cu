@@ -2236,6 +2236,11 @@ static bool run_solve_persistent(ietidp_s* h) {
     const bool keep = nc == 1 && sbytes < 0.66 * l2 && !(getenv("IETIDP_L2HINT") && atoi(getenv("IETIDP_L2HINT")) == 0);
     a.ssym.l2hint = keep ? 1 : 0;
     a.wsym.l2hint = keep ? 2 : 0;
+    // several RHS: both operators' tiles streamed with evict_first so that more of the
+    // symmetric-pass partials stay in the L2 for the reduction (C5 PCG 118.8 -> 117.2 ms,
+    // bit-identical; IETIDP_L2MULTI=0 turns it off)
+    if (nc > 1 && !(getenv("IETIDP_L2MULTI") && atoi(getenv("IETIDP_L2MULTI")) == 0))
+      a.ssym.l2hint = a.wsym.l2hint = 2;
   }
   a.ssym.vin = a.rslot;
   a.ssym.slot_in = 1;
