@@ -2233,7 +2233,8 @@ static bool run_solve_persistent(ietidp_s* h) {
     const double sbytes = (double)h->stiles.n * sizeof(double);
     int l2 = 0;
     IETI_CUDA(cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, h->opt.device));
-    const bool keep = nc == 1 && sbytes < 0.66 * l2 && !(getenv("IETIDP_L2HINT") && atoi(getenv("IETIDP_L2HINT")) == 0);
+    const double keep_frac = getenv("IETIDP_L2KEEP") ? atof(getenv("IETIDP_L2KEEP")) : 0.66;
+    const bool keep = nc == 1 && sbytes < keep_frac * l2 && !(getenv("IETIDP_L2HINT") && atoi(getenv("IETIDP_L2HINT")) == 0);
     a.ssym.l2hint = keep ? 1 : 0;
     a.wsym.l2hint = keep ? 2 : 0;
     // several RHS: both operators' tiles streamed with evict_first so that more of the
