@@ -195,6 +195,19 @@ ietidp_status ietidp_analyze(ietidp_t h) {
     require(!h->analyzed, IETIDP_E_STATE, "already analyzed");
     if (h->opt.device >= 0) set_device(h);
     ieti::analyze_all(h);
+    if (h->opt.device >= 0) {
+      // The copy stream and the per-subdomain copy events exist before the first
+      // factorisation is captured into a graph, so the graph always carries the
+      // external waits on them (a later ietidp_set_values is then ordered before
+      // the replayed factorisation). Each event is recorded once here (complete).
+      IETI_CUDA(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
+      h->kev.resize(h->n_sub);
+      for (auto& e : h->kev) {
+        IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        IETI_CUDA(cudaEventRecord(e, h->cstream));
+      }
+      IETI_CUDA(cudaEventCreateWithFlags(&h->hp_ev_set, cudaEventDisableTiming));
+    }
     h->analyzed = true;
   });
 }
@@ -206,12 +219,7 @@ ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const do
     const ieti::SubIn& in = h->in[k];
     // copies on a dedicated stream, one event per subdomain: the next factorisation
     // starts a subdomain group as soon as that group's values have arrived
-    if (!h->cstream) {
-      IETI_CUDA(cudaStreamCreateWithFlags(&h->cstream, cudaStreamNonBlocking));
-      h->kev.resize(h->n_sub);
-      for (auto& e : h->kev) IETI_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      IETI_CUDA(cudaEventCreateWithFlags(&h->hp_ev_set, cudaEventDisableTiming));
-    }
+    require(h->cstream != nullptr, IETIDP_E_STATE, "set_values on a host-only handle");
     IETI_CUDA(cudaEventRecord(h->hp_ev_set, h->stream));  // after the caller's prior work
     IETI_CUDA(cudaStreamWaitEvent(h->cstream, h->hp_ev_set, 0));
     if (K_val)

@@ -703,9 +703,15 @@ void run_factor(ietidp_s* h) {
     cudaStream_t s2 = h->gside[g];
     if (g > 0) IETI_CUDA(cudaStreamWaitEvent(sg, h->fev[2], 0));
     // the group's values (ietidp_set_values copies, recorded per subdomain)
-    if (!h->kev.empty())
+    // (inside a graph capture as external wait nodes, so every replay waits for the
+    // copies recorded before it)
+    if (!h->kev.empty()) {
+      cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+      IETI_CUDA(cudaStreamIsCapturing(sg, &cs));
+      const unsigned wflag = cs == cudaStreamCaptureStatusActive ? cudaEventWaitExternal : 0;
       for (int k = 0; k < h->n_sub; ++k)
-        if (P.sub_group[k] == g) IETI_CUDA(cudaStreamWaitEvent(sg, h->kev[k], cudaEventWaitExternal));
+        if (P.sub_group[k] == g) IETI_CUDA(cudaStreamWaitEvent(sg, h->kev[k], wflag));
+    }
     // assembly: level 0 here, the levels above on the side stream while level 0 is factored
     assemble(P.glevels[g][0], sg);
     if (h->fwd_in_factor && P.gfx[g].second) {

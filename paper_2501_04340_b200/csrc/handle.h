@@ -123,6 +123,7 @@ struct ietidp_s {
   std::vector<cudaEvent_t> pev;  // per panel: POTRF done (progressive inverse)
   bool fwd_in_factor = false;    // the forward sweep of the loads ran on the side stream
   long long launches = 0;
+  ieti::DevBuf<unsigned long long> pcg_prof;  // IETIDP_PCG_PROF barrier timestamps
   LaunchTrace trace;
   ietidp_report rep{};
 

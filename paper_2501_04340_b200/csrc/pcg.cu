@@ -2151,7 +2151,7 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
   args.cta_ptr = h->cta_ptr.p;
   args.cta_items = h->cta_items.p;
   const char* prof_env = getenv("IETIDP_PCG_PROF");
-  static DevBuf<unsigned long long> prof;
+  DevBuf<unsigned long long>& prof = h->pcg_prof;  // per handle, on the handle's device
   if (prof_env) {
     if (!prof.p) prof.alloc(4096);
     const int zero = 0;

@@ -348,3 +348,37 @@ def test_fold_multi_bitwise(lib, monkeypatch):
     t.factor()
     lam1, _ = t.solve()
     assert np.array_equal(lam0, lam1) and np.array_equal(u0, t.get_u(5))
+
+
+@pytest.mark.parametrize("pinned", [False, True])
+def test_set_values_then_refactor(lib, pinned):
+    """analyze -> factor -> set_values(new K, f) -> factor -> solve (the e2e loop of
+    bench.py): the captured factorisation graph must wait for the new values' copies.
+    Subdomain k's K is scaled by s_k = 1 + (k mod 3) and its loads by 2 (a different
+    problem, not a uniform rescaling); compared, iteration-matched, against the
+    oracle on the new values."""
+    import copy
+    import torch
+    b, _ = case("C2r")
+    b2 = copy.deepcopy(b)
+    for k, sd in enumerate(b2["subs"]):
+        sd["K_data"] = sd["K_data"] * (1.0 + (k % 3))
+        sd["f"] = sd["f"] * 2.0
+    ref = dp.solve(b2)
+    nit = int(ref["iters"][0])
+    ref_f = dp.solve(b2, fixed_iters=nit)
+    s = lib.from_bundle(b, fixed_iters=nit)
+    s.factor()  # captures the factorisation graph on the original values
+    s.solve()
+    for k, sd in enumerate(b2["subs"]):
+        if pinned:
+            kv = torch.from_numpy(sd["K_data"]).pin_memory()
+            fv = torch.from_numpy(np.ascontiguousarray(sd["f"])).pin_memory()
+            s.set_values(k, kv.numpy(), fv.numpy())
+        else:
+            s.set_values(k, sd["K_data"], sd["f"])
+    s.factor()
+    lam, rep = s.solve()
+    u = [s.get_u(k) for k in range(b2["n_sub"])]
+    assert rel(lam, ref_f["lam"]) <= 1e-8
+    assert rel(np.concatenate(u), np.concatenate(ref_f["u"])) <= 1e-8
