@@ -250,3 +250,55 @@ def test_condition_lanczos_vs_dense_spectrum(bundles):
     assert 1.0 - 1e-10 <= lo <= hi and k <= dk * (1 + 1e-10)
     # P:262 bound shape: a small, h-independent-ish constant for this configuration
     assert 1.0 < k < 10.0
+
+
+def _cond(D, tol=1e-10):
+    _, info = D.pcg(tol=tol)
+    return int(info["iters"][0]), dp.cond_lanczos(info["alpha"][0], info["beta"][0])[2]
+
+
+def test_stiffness_scaling_orientation():
+    """Pin of the orientation of the stiffness scaling delta (PAPER.md:143-146, D_s;
+    DESIGN.md R5): on C3r the 10^3 coefficient jump is aligned with subdomain
+    boundaries, where the scaled Dirichlet preconditioner is robust in the jump
+    (FETI-DP theory): cond(M_D^-1 F_DP) with mu_r = 1000 stays within 1.5x of mu_r = 1.
+    The swapped weight delta' = 1 - delta (own stiffness over the sum) loses that
+    robustness (measured cond ~6e3, 133 iterations): it must fail the bound."""
+    import scipy.sparse as sp
+    jump = make_bundle(replace(cf.get("C3r"), name="C3r"))
+    flat = make_bundle(replace(cf.get("C3r"), name="C3r_flat", material="one"))
+    n1, k1 = _cond(dp.DualPrimal(flat))
+    D = dp.DualPrimal(jump)
+    n2, k2 = _cond(D)
+    assert k2 <= 1.5 * k1, (k1, k2)
+    for L in D.loc:  # swapped orientation: delta' = mine / (mine + other)
+        L.BD = sp.csr_matrix((L.B_sign * (1.0 - L.delta), (L.B_lambda, L.B_Ipos)), shape=(D.nl, len(L.rI)))
+    n3, k3 = _cond(D)
+    assert k3 > 10 * k1 and n3 > 2 * n2, (k1, k3, n2, n3)
+
+
+def test_multi_rhs_columns_independent():
+    """Pin of the several-RHS PCG (independent PCGs sharing the operator,
+    each column frozen at its own convergence) on C5e1 (C5's tiling, materials, n_gp =
+    177 and 16 seeded right-hand sides at e = 1): every column of the 16-column DD solve
+    equals the direct solve of Eq. (5) and the monolithic gauged solve (PAPER.md:49-56,
+    :101-116) at tol 1e-12; and three columns stopping at different iterations give the
+    same iteration count (+-1: the LU solves of one and of 16 columns round
+    differently) and multipliers when solved alone."""
+    from oracle_variants import slice_columns
+    b = make_bundle("C5e1")
+    res = dp.solve(b, tol=1e-12)
+    U = np.concatenate(res["u"])
+    us, lam_s, _ = brute.saddle_solve(b)
+    um = np.concatenate(brute.monolithic_solve(b)[0])
+    S = np.concatenate(us)
+    for c in range(b["nrhs"]):
+        assert rel(U[:, c], S[:, c]) <= 1e-9 and rel(U[:, c], um[:, c]) <= 1e-9, c
+        assert rel(res["lam"][:, c], lam_s[:, c]) <= 1e-8, c
+    it = np.asarray(res["iters"])
+    assert len(set(it.tolist())) >= 2  # the columns do stop at different iterations
+    picks = [int(np.argmin(it)), int(np.argmax(it)), 7]
+    for c in picks:
+        r1 = dp.solve(slice_columns(b, [c]), tol=1e-12)
+        assert abs(int(r1["iters"][0]) - int(it[c])) <= 1, (c, r1["iters"], it[c])
+        assert rel(r1["lam"][:, 0], res["lam"][:, c]) <= 1e-9
