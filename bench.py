@@ -34,7 +34,7 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C2")
+    ap.add_argument("--config", default="C5")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--fapply-iters", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -147,28 +147,113 @@ def max_over_ranks(x, world, device=None):
 # ---------------------------------------------------------------------------
 # CPU oracle (the reported baseline; the one place bench.py runs oracle/)
 # ---------------------------------------------------------------------------
-def oracle_sample(bundle, n_iter, subs):
-    """Time the oracle on a bounded sample: full local set-up (factorisation of
-    K_rr, explicit S_{r_I r_I}, coarse columns) of the subdomains `subs` plus
-    n_iter local F-apply and preconditioner contributions each; extrapolated to
-    all subdomains. Returns (seconds per full solve, threads)."""
-    from oracle import dp
+def oracle_iters(config):
+    """The oracle's own natural-stopping iteration count at full size (max over the
+    columns measured), from profiles/oracle_iters.json (tests/studies/oracle_iters.py,
+    oracle/ only); None if not recorded."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "oracle_iters.json")) as f:
+            e = json.load(f).get(config)
+    except OSError:
+        return None
+    return max(e["iters"]) if e else None
+
+
+def oracle_solve_cost(bundle, subs, n_iter, iters_sample=2):
+    """Seconds of one full oracle solve (oracle/dp.py as it stands, on this host's
+    cores), measured on a bounded sample: every per-subdomain phase is timed on the
+    subdomains `subs` and scaled by n_sub / len(subs); every global phase is timed
+    at full size. Phases (§2.1 order):
+      set-up   per subdomain: Local (sparse LU of K_rr), K_rr^-1 K_rP, K_rr^-1 j_r,
+               the explicit S_II = K_II - K_IV K_VV^-1 K_VI (Eq. 10);
+               global: cho_factor of S_PP (n_gp x n_gp);
+      PCG      `iters_sample` iterations of DualPrimal.pcg (F = W + G S^-1 G^T, M_D^-1,
+               dot products and vector updates on the full n_lambda x nrhs vectors)
+               over the sampled subdomains, split into the per-subdomain part and the
+               global part (the same pcg with no subdomains), scaled to n_iter;
+      recovery Eqs. (8)-(9): one K_rr^-1 solve per subdomain (+ the coarse solve).
+    Returns (seconds, detail dict)."""
+    import scipy.linalg as la
     import threadpoolctl
-    nl = int(bundle["n_lambda"])
+    from oracle import dp
+    nl, ng, nc = int(bundle["n_lambda"]), int(bundle["n_primal"]), int(bundle["nrhs"])
+    ns = len(bundle["subs"])
+    scale = ns / len(subs)
     rng = np.random.default_rng(0)
     t0 = time.perf_counter()
+    loc = []
     for k in subs:
         L = dp.Local(k, bundle["subs"][k], nl, False)
-        L.schur_II(False)
-        if len(L.prim):
-            L.Kinv(L.Krp.toarray())
-        L.Kinv(L.jr)
-        x = rng.standard_normal((nl, int(bundle["nrhs"])))
-        for _ in range(n_iter):
-            L.Br @ L.Kinv(L.Br.T @ x)
-    dt = time.perf_counter() - t0
+        L.X = L.Kinv(L.Krp.toarray()) if len(L.prim) else np.zeros((len(L.r), 0))
+        L.y = L.Kinv(L.jr)
+        L.SII = L.schur_II(False)
+        loc.append(L)
+    t_setup_local = time.perf_counter() - t0
+    A = rng.standard_normal((ng, ng))
+    Sg = A @ A.T + ng * np.eye(ng)
+    t0 = time.perf_counter()
+    Sc = la.cho_factor(Sg, lower=True) if ng else None
+    t_setup_global = time.perf_counter() - t0
+
+    def make(locs):
+        D = dp.DualPrimal.__new__(dp.DualPrimal)
+        D.nl, D.ng, D.nrhs, D.scaling = nl, ng, nc, bundle["scaling"]
+        D.loc = locs
+        D.G = rng.standard_normal((nl, ng))
+        D.Sc = Sc
+        for L in locs:  # the preconditioner's B_D (scaling weights: any, same cost)
+            posI = -np.ones(len(L.r), np.int64)
+            posI[L.rI] = np.arange(len(L.rI))
+            L.B_Ipos = posI[L.B_rpos]
+            L.delta = np.full(len(L.B_lambda), 0.5)
+            import scipy.sparse as sp
+            L.BD = sp.csr_matrix((L.B_sign * L.delta, (L.B_lambda, L.B_Ipos)), shape=(nl, len(L.rI)))
+        return D
+
+    d = rng.standard_normal((nl, nc))
+    Ds, Dg = make(loc), make([])
+    Dg.apply_M = lambda r: r.copy()  # no subdomains: keep the iteration finite (a copy's cost)
+
+    def per_iter(D):
+        # pcg with 1 and with 1 + iters_sample iterations: the difference is iters_sample
+        # iterations (the start-up M-apply and the final true-residual F-apply cancel)
+        t0 = time.perf_counter()
+        D.pcg(tol=0.0, fixed_iters=1, d=d)
+        t1 = time.perf_counter()
+        D.pcg(tol=0.0, fixed_iters=1 + iters_sample, d=d)
+        t2 = time.perf_counter()
+        return max((t2 - t1) - (t1 - t0), 0.0) / iters_sample
+
+    t_iter_sample = per_iter(Ds)
+    t_iter_global = per_iter(Dg)
+    t_iter_local = max(t_iter_sample - t_iter_global, 0.0)
+    lam = rng.standard_normal((nl, nc))
+    Ds.ftilde = rng.standard_normal((ng, nc))
+    for L in loc:
+        L.Cp = np.zeros((len(L.prim), ng))
+    t0 = time.perf_counter()
+    Ds.recover(lam)
+    t_recover = time.perf_counter() - t0
+    total = (t_setup_local * scale + t_setup_global + n_iter * (t_iter_local * scale + t_iter_global)
+             + t_recover * scale)
     threads = max((i.get("num_threads", 1) for i in threadpoolctl.threadpool_info()), default=1)
-    return dt * len(bundle["subs"]) / len(subs), threads
+    detail = {"setup_s": t_setup_local * scale + t_setup_global, "pcg_iter_s": t_iter_local * scale + t_iter_global,
+              "recover_s": t_recover * scale, "n_iter": n_iter, "threads": threads,
+              "sampled_subdomains": list(map(int, subs)), "scale": scale}
+    return total, detail
+
+
+def cpu_info():
+    model = None
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    return {"os_cpu_count": os.cpu_count(), "model": model}
 
 
 def run_reference(args, rank, world):
@@ -176,25 +261,29 @@ def run_reference(args, rank, world):
         return
     from ietigen.bundle import make_bundle
     b = make_bundle(args.config)
-    n_iter = 30
-    times = []
-    threads = 1
     nsub = b["n_sub"]
+    n_iter = oracle_iters(args.config) or 0
+    per = 2  # subdomains sampled per step (rotating over the tiling)
+    times, det = [], None
     for s in range(args.warmup + args.steps):
-        k = s % nsub
-        t, threads = oracle_sample(b, n_iter, [k])
+        subs = [((s * per + i) * 7919) % nsub for i in range(per)]
+        t, det = oracle_solve_cost(b, sorted(set(subs)), n_iter)
         if s >= args.warmup:
             times.append(t)
     sec = statistics.mean(times)
     val = 1.0 / sec
+    sample = (f"per step: oracle/dp.py on {per} of {nsub} subdomains (set-up: sparse LU of K_rr, K_rr^-1 K_rP, "
+              f"explicit S_II; 2 PCG iterations with F, M_D^-1, coarse solve and vector updates; recovery), "
+              f"per-subdomain phases scaled x{nsub / per:g}, global phases at full size, PCG scaled to the "
+              f"oracle's own {n_iter} iterations (profiles/oracle_iters.json)")
+    ci = cpu_info()
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "solves/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "n_sub": nsub, "n_lambda": int(b["n_lambda"]),
                        "n_primal": int(b["n_primal"]), "nrhs": int(b["nrhs"])},
-            "cpu_baseline": {"value": val, "unit": "solves/s", "cores": threads, "kind": "oracle",
-                             "sample": f"per step: oracle local set-up of 1 of {nsub} subdomains + {n_iter} "
-                                       f"local F-apply contributions, extrapolated x{nsub}"},
+            "cpu_baseline": {"value": val, "unit": "solves/s", "cores": det["threads"], "kind": "oracle",
+                             "sample": sample, "cpu": ci, "phases_s": det},
             "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -227,8 +316,12 @@ def run_ours(args, rank, world, local):
     dev = torch.device("cuda", local)
     b = make_bundle(args.config)
     stream = torch.cuda.Stream(device=dev)
+    t0 = time.perf_counter()
     S = ietidp.from_bundle(b, device=local, stream=stream.cuda_stream)
+    t1 = time.perf_counter()
     S.analyze()
+    t2 = time.perf_counter()
+    ms_set_sub, ms_analyze = (t1 - t0) * 1e3, (t2 - t1) * 1e3
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)
 
@@ -309,8 +402,15 @@ def run_ours(args, rank, world, local):
                 if it >= 2:
                     ets.append(dt)
             e2e_s = max_over_ranks(statistics.mean(ets), world, dev)
+            once = (ms_set_sub + ms_analyze) * 1e-3
             e2e = {"value": world / e2e_s, "unit": "solves/s", "h2d_bytes_per_step": int(h2d),
-                   "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3}
+                   "d2h_bytes_per_step": int(d2h), "ms_per_step": e2e_s * 1e3,
+                   "note": "per step: ietidp_set_values (K values + loads, pinned H2D) for every subdomain, "
+                           "factor, solve with lambda to the host, ietidp_get_u for every subdomain",
+                   "with_analysis": {"value": world / (e2e_s + once), "unit": "solves/s",
+                                     "ms_set_subdomain": ms_set_sub, "ms_analyze": ms_analyze,
+                                     "note": "one solve including the host set-up (ietidp_set_subdomain "
+                                             "validation/copies) and the symbolic analysis"}}
 
         fp64_peak = measure_dgemm_tflops(torch, dev) if rank == 0 else None
 
@@ -332,11 +432,31 @@ def run_ours(args, rank, world, local):
               "recover": rep["ms_recover"]}
     dominant = max(phases, key=phases.get)
     tr = traffic_from_profiles(args.config)
-    roof_pcg = {"kernel": "persistent PCG kernel k_pcg (W_k and S_II symmetric tile passes, gathers, coarse "
-                          "solve, CG updates) per iteration",
-                "bound": "hbm", "achieved": pcg_gbs, "peak": hbm, "unit": "GB/s", "frac": pcg_gbs / hbm,
-                "traffic": tr.get("pcg_bytes_per_iter"), "traffic_source": tr.get("pcg_source"),
-                "algorithmic_bytes_per_iter": int(pcg_bytes)}
+    # PCG: two symmetric passes per iteration (W_k = S_II^-1 for F, S_II for M_D^-1), each
+    # y = S x on nc columns: 2 |r_I|^2 nc flops per subdomain and pass; the
+    # bytes are the stored lower tiles. The binding roofline is the larger floor: HBM for
+    # one column, the FP64 tensor pipe (DMMA) for 16 columns.
+    sum_nI2 = sum(float(len(np.unique(sd["B_dof"]))) ** 2 for sd in b["subs"])
+    pcg_flops = 2 * 2.0 * sum_nI2 * nc
+    pcg_tflops = pcg_flops / (pcg_ms_iter * 1e-3) / 1e12 if it_max else 0.0
+    t_hbm = pcg_bytes / (hbm * 1e9)
+    t_fp = pcg_flops / (fp64_peak * 1e12) if fp64_peak else 0.0
+    pcg_kernel = ("persistent PCG kernel k_pcg (W_k and S_II symmetric tile passes, gathers, coarse "
+                  "solve, CG updates) per iteration")
+    if t_fp > t_hbm:
+        roof_pcg = {"kernel": pcg_kernel, "bound": "tensor", "achieved": pcg_tflops, "peak": fp64_peak,
+                    "unit": "TFLOP/s", "frac": pcg_tflops / fp64_peak,
+                    "algorithmic_flops_per_iter": pcg_flops,
+                    "hbm": {"achieved": pcg_gbs, "peak": hbm, "unit": "GB/s", "frac": pcg_gbs / hbm},
+                    "peak_source": "cuBLAS DGEMM 8192^3 measured in this run (FP64 tensor pipe, DMMA)"}
+    else:
+        roof_pcg = {"kernel": pcg_kernel, "bound": "hbm", "achieved": pcg_gbs, "peak": hbm, "unit": "GB/s",
+                    "frac": pcg_gbs / hbm,
+                    "tensor": {"achieved": pcg_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
+                               "frac": pcg_tflops / fp64_peak if fp64_peak else None}}
+    roof_pcg.update({"traffic": tr.get("pcg_bytes_per_iter"), "traffic_source": tr.get("pcg_source"),
+                     "algorithmic_bytes_per_iter": int(pcg_bytes), "us_per_iter": pcg_ms_iter * 1e3,
+                     "floors_us": {"hbm": t_hbm * 1e6, "tensor": t_fp * 1e6}})
     roof_fac = {"kernel": "multifrontal Cholesky phase (k_gemm DMMA panel updates / TRSM / SYRK+extend-add, "
                           "k_potrf, assembly; side stream: L11^-1, W_k, forward sweep)",
                 "bound": "tensor", "achieved": fac_tflops, "peak": fp64_peak, "unit": "TFLOP/s",
@@ -349,10 +469,19 @@ def run_ours(args, rank, world, local):
     roofline = roof_fac if dominant == "factor" else roof_pcg
     cpu = None
     if not args.no_cpu_baseline and world == 1:
-        sec, threads = oracle_sample(b, it_max, [0, 1])
-        cpu = {"value": 1.0 / sec, "unit": "solves/s", "cores": threads, "kind": "oracle",
-               "sample": f"oracle local set-up of subdomains 0-1 of {b['n_sub']} + {it_max} local F-apply "
-                         f"contributions each, extrapolated x{b['n_sub'] / 2:g}"}
+        ns = b["n_sub"]
+        nsamp = min(ns, 8)
+        subs = sorted(set(int(round(i * (ns - 1) / max(nsamp - 1, 1))) for i in range(nsamp)))
+        n_or = oracle_iters(args.config)
+        sec, det = oracle_solve_cost(b, subs, n_or or it_max)
+        cpu = {"value": 1.0 / sec, "unit": "solves/s", "cores": det["threads"], "kind": "oracle",
+               "sample": f"oracle/dp.py on {len(subs)} of {ns} subdomains evenly spaced over the tiling (set-up: "
+                         f"sparse LU of K_rr, K_rr^-1 K_rP, K_rr^-1 j, explicit S_II; 2 PCG iterations with F, "
+                         f"M_D^-1, coarse solve and vector updates on all {nc} columns; recovery), per-subdomain "
+                         f"phases scaled x{ns / len(subs):g}, global phases at full size, PCG scaled to "
+                         + (f"the oracle's own {n_or} iterations (profiles/oracle_iters.json)" if n_or else
+                            f"the GPU run's {it_max} iterations"),
+               "cpu": cpu_info(), "phases_s": det}
     line = {
         "metric": METRIC, "value": world / (ms_step * 1e-3), "unit": "solves/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True,
@@ -360,7 +489,7 @@ def run_ours(args, rank, world, local):
         "config": {"workload": args.config, "n_sub": b["n_sub"], "n_lambda": b["n_lambda"],
                    "n_primal": b["n_primal"], "nrhs": nc, "l2": "flushed between timed steps (512 MB write)",
                    "replicas": world},
-        "phases_ms": phases, "iters": rep["iters"], "rel_residual": max(rep["rel_residual"]),
+        "phases_ms": phases, "ms_analyze": ms_analyze, "ms_set_subdomain": ms_set_sub, "iters": rep["iters"], "rel_residual": max(rep["rel_residual"]),
         "cond_estimate": {"omega_min": float(min(c_lo)), "omega_max": float(max(c_hi)),
                           "cond_max": float(max(c_k)), "method": "Lanczos from the PCG alpha/beta (device)"},
         "f_applies_per_s": f_apply_per_s, "f_apply_us": fa_ms * 1e3, "f_apply_gbs": fa_gbs,

@@ -570,6 +570,15 @@ static void fill_report(ietidp_s* h) {
 // Build the complete plan and upload every structure and the raw values.
 void analyze_all(ietidp_s* h) {
   auto t0 = std::chrono::steady_clock::now();
+  // IETIDP_ANALYZE_PROF=1: host time of every stage of the analysis (stderr)
+  const bool aprof = getenv("IETIDP_ANALYZE_PROF") != nullptr;
+  auto tl = t0;
+  auto stage = [&](const char* name) {
+    if (!aprof) return;
+    const auto t = std::chrono::steady_clock::now();
+    fprintf(stderr, "analyze %-22s %8.2f ms\n", name, std::chrono::duration<double, std::milli>(t - tl).count());
+    tl = t;
+  };
   const int ns = h->n_sub, nrhs = h->nrhs;
   for (int k = 0; k < ns; ++k)
     if (!h->in[k].set) throw Error(IETIDP_E_STATE, "subdomain " + std::to_string(k) + " not set");
@@ -593,12 +602,14 @@ void analyze_all(ietidp_s* h) {
       throw Error(IETIDP_E_B_STRUCTURE,
                   "multiplier row " + std::to_string(l) + " is not {+1,-1} in two subdomains");
 
+  stage("B validation");
   // ---- per-subdomain analysis, in parallel ----
   std::vector<LocalResult> loc(ns);
   parallel_for(ns, [&](int k) { loc[k] = analyze_sub(h->in[k], k, h->opt.ordering, h->opt.leaf_size); });
   for (int k = 0; k < ns; ++k)
     if (loc[k].st != IETIDP_OK) throw Error(loc[k].st, loc[k].err);
 
+  stage("per-subdomain analysis");
   Plan& P = h->plan;
   P = Plan();
   P.subs.resize(ns);
@@ -639,6 +650,7 @@ void analyze_all(ietidp_s* h) {
     for (int i : bylev[L]) bylev_g[P.sub_group[P.sn[i].sub]][L].push_back(i);
   P.glevels.assign(G, std::vector<LevelPlan>(P.max_level + 1));
 
+  stage("numbering/groups");
   // ---- memory layout of the supernodes ----
   std::vector<SnDev> sd(nsn);
   std::vector<int> rows_all, rel_all, children_all, work;
@@ -722,6 +734,7 @@ void analyze_all(ietidp_s* h) {
     if (sp.root >= 0) prog_level[P.sn[sp.root].level] = 1;
   auto tiles_of = [](int n) { return (n + TB - 1) / TB; };
   std::vector<std::pair<int, int>> split_group;  // split-K GemmWork entries and their group
+  stage("memory layout");
   // ---- work lists: factorisation and sweeps, per level ----
   for (int L = 0; L <= P.max_level; ++L) {
     for (int grp = 0; grp < G; ++grp) {
@@ -969,6 +982,7 @@ void analyze_all(ietidp_s* h) {
       if (!P.sn[i].coarse)
         for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bxr_n) push(i, t, 0);
   }
+  stage("work lists");
   // ---- partitioned inverse L11^-1 by recursive doubling over TB-blocks, per level ----
   // each group's split-K launches use their own slice of the workspace and counters
   for (auto& sg : split_group) {
@@ -1049,6 +1063,7 @@ void analyze_all(ietidp_s* h) {
     }
   }
 
+  stage("inverse plan");
   // ---- per-subdomain offsets ----
   long long kv = 0, fv = 0, xo = 0, rio = 0, lpio = 0, to = 0, uo = 0, spo = 0;
   int po = 0, permo = 0, cta = 0;
@@ -1198,6 +1213,7 @@ void analyze_all(ietidp_s* h) {
   }
   P.g_n = (int)gwork.size() - P.g_off;
 
+  stage("offsets/items");
   // ---- scatter lists (per subdomain in parallel, merged per level) ----
   struct Scat {
     std::vector<std::vector<long long>> fd;
@@ -1274,6 +1290,7 @@ void analyze_all(ietidp_s* h) {
     kdiag.insert(kdiag.end(), sc[k].kdiag.begin(), sc[k].kdiag.end());
   }
 
+  stage("scatter lists");
   // ---- multipliers, slots, primal bookkeeping ----
   std::vector<int> slot_lam(h->n_slots);
   std::vector<float> slot_sign(h->n_slots);
@@ -1398,10 +1415,12 @@ void analyze_all(ietidp_s* h) {
     }
   }
   if (h->opt.device < 0) {  // host-only analysis mode: no device work
+    stage("rest (host only)");
     h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t1 - t0).count();
     return;
   }
 
+  stage("slots/primal");
   // ---- upload ----
   cudaStream_t s = h->stream;
   h->d_sn.upload(sd, s);
@@ -1551,6 +1570,7 @@ void analyze_all(ietidp_s* h) {
   h->tmp_out.alloc(m);
   h->U.alloc(uo);
   IETI_CUDA(cudaStreamSynchronize(s));
+  stage("upload/alloc");
   auto t2 = std::chrono::steady_clock::now();
   h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t2 - t0).count();
 }

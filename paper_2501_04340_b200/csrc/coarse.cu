@@ -198,7 +198,8 @@ __global__ void __launch_bounds__(256)
     }
     __syncthreads();
     double* T = (pass ? itiles : tiles) + toff;
-    for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x) T[e] = S[e & (TB - 1)][e >> 6];  // row writes
+    for (int e = threadIdx.x; e < TILE_ELEMS; e += blockDim.x)  // row writes, swizzled (common.cuh swz)
+      T[swz(e >> 6, e & (TB - 1))] = S[e & (TB - 1)][e >> 6];
     __syncthreads();
   }
   if (j != 0) return;

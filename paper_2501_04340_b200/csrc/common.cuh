@@ -23,9 +23,12 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Swizzled position of element (r, m) of a TB x TB row-major tile in shared
-// memory: 16-byte chunks of a row are XOR-permuted by (r & 7) so that both the
-// row-wise and the column-wise DMMA fragment loads are bank-conflict free.
+// Swizzled position of element (r, m) of a TB x TB row-major tile: 16-byte chunks
+// of a row are XOR-permuted by (r & 7) so that both the row-wise and the column-wise
+// DMMA fragment loads from shared memory are bank-conflict free. The loop's tiles
+// (L_II, L_II^-1, W_k = S_II^-1, S_II) are STORED in this layout in global memory,
+// so that a tile moves into shared memory as one contiguous 32 KB copy (one
+// cp.async.bulk, or linear 16-byte cp.async).
 __device__ __forceinline__ int swz(int r, int m) {
   return r * TB + ((((m >> 1) ^ (r & 7))) << 1) + (m & 1);
 }

@@ -482,7 +482,8 @@ __global__ void __launch_bounds__(128, 4) k_gemm(const GemmWork* __restrict__ wo
     return;
   }
   if (w.mode & 16) {
-    // row-major TB x TB tile (the loop's symmetric tile layout), zero padded
+    // row-major TB x TB tile (the loop's symmetric tile layout, stored swizzled:
+    // common.cuh swz), zero padded
     for (int r = warp; r < TB; r += 4) {
       const int c = 2 * lane;
       double v[2] = {0.0, 0.0};
@@ -490,7 +491,7 @@ __global__ void __launch_bounds__(128, 4) k_gemm(const GemmWork* __restrict__ wo
       for (int q = 0; q < 2; ++q)
         if (r < w.m && c + q < w.n)
           v[q] = (w.diag && r < c + q) ? Ts[r * ETS + c + q] : Ts[(c + q) * ETS + r];
-      double2* T = reinterpret_cast<double2*>(Cb + w.c_off + r * TB + c);
+      double2* T = reinterpret_cast<double2*>(Cb + w.c_off + swz(r, c));
       if (w.mode & 2) {
         const double2 o = *T;
         v[0] += o.x;
@@ -606,7 +607,7 @@ __global__ void __launch_bounds__(256)
   double* T = dst + d.tile_off + (long long)t * TILE_ELEMS;
   for (int q = threadIdx.x; q < TILE_ELEMS; q += blockDim.x) {
     const int r = q >> 6, c = q & (TB - 1);
-    T[q] = (i == j && r < c) ? S[r][c] : S[c][r];  // diagonal tile: mirror the lower part
+    T[swz(r, c)] = (i == j && r < c) ? S[r][c] : S[c][r];  // diagonal tile: mirror the lower part
   }
 }
 

@@ -180,6 +180,13 @@ struct ietidp_s {
   ieti::DevBuf<int> sub_blk0, sub_nt;        // (subdomain, block) rows of each subdomain
   ieti::DevBuf<int> cta_ptr, cta_items;     // persistent PCG: work items per CTA
   int lpt_grid = 0;
+  // several-RHS chunk pass of the persistent PCG (pcg.cu sym_chunks), planned for a grid
+  int chunk_grid = 0;
+  ieti::DevBuf<int> chunk_ptr, chunk_cfirst;
+  ieti::DevBuf<ieti::SymChunk> chunk_list;
+  ieti::DevBuf<long long> chunk_cpb;
+  ieti::DevBuf<ieti::SlotRed> chunk_slot_red;
+  ieti::DevBuf<double> chunk_spart;
   ieti::DevBuf<int> sub_cta0, sub_ncta;   // loop CTAs of each subdomain
   ieti::DevBuf<ieti::LamDev> lam;
   ieti::DevBuf<int> slot_lam;             // per r_I slot: multiplier

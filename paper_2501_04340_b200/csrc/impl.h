@@ -110,6 +110,17 @@ struct SymWork {
   int sub, o, j0, j1, seg, cost;
 };
 
+// A chunk of the several-RHS symmetric pass (pcg.cu sym_chunks): the tiles
+// [t0, t1) of subdomain `sub` in lower row-major order (tile t = (o, j), t = o(o+1)/2 + j),
+// the rank-th chunk of that subdomain; its tiles start at global tile index gtile.
+// Every chunk writes one partial block (TB rows x ncols) per block j <= its last row:
+// block j of the chunk of rank c goes to cpb[blk0 + j] + c - cfirst[blk0 + j] (partial
+// blocks of (subdomain, j) contiguous, in chunk order; SlotRed sums them).
+struct SymChunk {
+  int sub, t0, t1, rank;
+  long long gtile;
+};
+
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).
 struct LoopWork {
   int sub, nblk, blk0, blk1;

@@ -47,12 +47,10 @@ constexpr int VT = 256;    // threads of the vector kernels
 
 enum TmvMode { FWD = 0, BWD = 1, PRE1 = 2, PRE2 = 3 };
 
+// (the tile is stored swizzled in global memory: a linear copy)
 __device__ __forceinline__ void load_tile_async(double* dst, const double* src, int tid) {
 #pragma unroll 4
-  for (int q = tid; q < TB * TB / 2; q += 256) {
-    const int r = q >> 5, c = q & 31;
-    cp_async16(dst + r * TB + ((c ^ (r & 7)) << 1), src + r * TB + 2 * c);
-  }
+  for (int q = tid; q < TB * TB / 2; q += 256) cp_async16(dst + 2 * q, src + 2 * q);
 }
 // the same with an L2 eviction-priority hint (createpolicy: 1 = evict_last, 2 = evict_first)
 __device__ __forceinline__ void load_tile_async_hint(double* dst, const double* src, int tid, int hint) {
@@ -65,10 +63,9 @@ __device__ __forceinline__ void load_tile_async_hint(double* dst, const double* 
   else asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
 #pragma unroll 4
   for (int q = tid; q < TB * TB / 2; q += 256) {
-    const int r = q >> 5, c = q & 31;
-    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + r * TB + ((c ^ (r & 7)) << 1));
-    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa),
-                 "l"(src + r * TB + 2 * c), "l"(pol));
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(dst + 2 * q);
+    asm volatile("cp.async.cg.shared.global.L2::cache_hint [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(src + 2 * q),
+                 "l"(pol));
   }
 }
 
@@ -94,6 +91,10 @@ struct TmvArgs {
   int l2hint;              // SYM: L2 eviction priority of the tile stream (0 none, 1 last, 2 first)
   int slot_in;             // FWD/PRE1/SYM: vin is already in slot order (B^T, weights applied)
   int nPmax, ncols, c_off;
+  int nt_max;              // SYM (chunk pass): largest number of TB-blocks of a subdomain (x staging)
+  const SymChunk* chunks;  // SYM (chunk pass): the chunks of the several-RHS pass
+  const long long* cpb;    // SYM (chunk pass): first partial block of each (subdomain, block)
+  const int* cfirst;       // SYM (chunk pass): rank of the first chunk writing (subdomain, block)
   const PcgState* st;
   const double* rr_part;   // PRE1 inside the loop: convergence test
   int check;
@@ -720,6 +721,269 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
   __syncthreads();
 }
 
+// ---------------------------------------------------------------------------
+// The several-RHS symmetric pass (16 columns): chunks of whole tile ranges, the
+// transposed products accumulated on chip in tensor memory.
+//
+// y = S x for a symmetric matrix held as lower TB-tiles (diagonal tiles full). The
+// CTA's chunks are contiguous tile ranges of one subdomain in lower row-major order,
+// so the CTA's tile stream is ONE contiguous range of the tile array: a thread issues
+// one 32 KB cp.async.bulk per tile into a STAGES-deep ring (mbarrier completion, L2
+// evict_first). For tile (o, j) every warp computes, with DMMA m8n8k4,
+//   N: S_oj x_j  -> rows o, accumulated in registers over the row,
+//   T: S_oj^T x_o -> rows j (j < o), accumulated in TENSOR MEMORY: block j's
+//      accumulator fragment (4 doubles per thread) is loaded (tcgen05.ld), extended
+//      by the DMMA chain and stored back (tcgen05.st), so the chunk's transposed
+//      products never leave the SM.
+// At the diagonal tile the row's N result joins block o's accumulator. At the end
+// of the chunk every block j <= o_b is written once as the chunk's partial block
+// (then zeroed); the gathers sum the (typically 1-3) partial blocks of a slot in
+// chunk order (deterministic). The chunk's input blocks x_0..x_ob are staged in shared
+// memory (16 columns, 16-byte pairs XOR-swizzled by row parity: conflict-free DMMA B
+// fragments). Tensor memory: lanes = the warp's quadrant (32 (w & 3) + lane), columns
+// 256 (w >> 2) + 8 j + [0, 8) hold block j's fragment: up to 32 blocks (n_I <= 2048).
+// ---------------------------------------------------------------------------
+constexpr int CH_NC = 16;                 // columns per chunk pass
+constexpr int CH_XBLK = TB * CH_NC;       // doubles per staged input block
+constexpr int CH_TMEM_COLS = 512;
+
+__device__ __forceinline__ int ch_xpos(int r, int c) { return r * CH_NC + (c ^ ((r & 1) << 3)); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+  const unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred P1;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
+        "selp.b32 %0, 1, 0, P1;\n\t}"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes, uint64_t* bar,
+                                         unsigned long long pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;\n" ::"r"(
+          (unsigned)__cvta_generic_to_shared(dst)),
+      "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld8(unsigned taddr, double (&v)[2][2]) {
+  unsigned r[8];
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 4; ++i) v[i >> 1][i & 1] = __hiloint2double((int)r[2 * i + 1], (int)r[2 * i]);
+}
+// issue only (the caller waits with tm_wait_ld before reading r)
+__device__ __forceinline__ void tm_ld8_issue(unsigned taddr, unsigned (&r)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7])
+               : "r"(taddr));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;\n" ::: "memory"); }
+__device__ __forceinline__ void tm_st8(unsigned taddr, const double (&v)[2][2]) {
+  unsigned r[8];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const double x = v[i >> 1][i & 1];
+    r[2 * i] = (unsigned)__double2loint(x);
+    r[2 * i + 1] = (unsigned)__double2hiint(x);
+  }
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};\n" ::"r"(taddr), "r"(r[0]),
+               "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), "r"(r[7])
+               : "memory");
+}
+
+// Per-CTA state of the chunk passes (shared memory): the ring's mbarriers, the tensor
+// memory base and the running count of tiles streamed (ring slot and phase parity).
+struct ChunkCtl {
+  uint64_t full[4];
+  unsigned tmem;
+  unsigned streamed;
+};
+
+// Tile (o, j) of chunk tiles: row o of lower row-major index t.
+__device__ __forceinline__ int o0_of(int t);
+__device__ __forceinline__ int tri_row(int t) {
+  int o = (int)((sqrtf(8.0f * t + 1.0f) - 1.0f) * 0.5f);
+  while (o * (o + 1) / 2 > t) --o;
+  while ((o + 1) * (o + 2) / 2 <= t) ++o;
+  return o;
+}
+
+__device__ __forceinline__ int o0_of(int t) { return tri_row(t); }
+
+template <int STAGES>
+__device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch, int nch, double* smem, ChunkCtl* ctl) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
+  const int ncl = min(CH_NC, A.ncols - A.c_off);
+  double* ring = smem;
+  double* xb = smem + STAGES * TILE_ELEMS;
+  double* gs = xb + A.nt_max * CH_XBLK;  // G_k rows of the current block row (TB x nP), F-apply
+  if (nch == 0) return;
+  const long long g0 = ch[0].gtile;
+  const int ntiles = (int)(ch[nch - 1].gtile + (ch[nch - 1].t1 - ch[nch - 1].t0) - g0);
+  const unsigned base = ctl->streamed;
+  const unsigned tbase = ctl->tmem + ((unsigned)(32 * (warp & 3)) << 16) + 256u * (warp >> 2);
+  unsigned long long pol = 0;
+  if (tid == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  auto issue = [&](int i) {
+    const unsigned s = (base + i) % STAGES;
+    mbar_expect_tx(&ctl->full[s], TILE_ELEMS * 8);
+    bulk_g2s(ring + s * TILE_ELEMS, A.tiles + (g0 + i) * TILE_ELEMS, TILE_ELEMS * 8, &ctl->full[s], pol);
+  };
+  if (tid == 0)
+    for (int i = 0; i < min(STAGES, ntiles); ++i) issue(i);
+  int i = 0;  // tile counter of the CTA's stream
+  for (int c = 0; c < nch; ++c) {
+    const SymChunk C = ch[c];
+    const SubDev d = A.sub[C.sub];
+    const int ob = tri_row(C.t1 - 1);
+    const bool coarse = A.gpart && d.nP > 0;
+    auto stage_g = [&](int row) {  // G_k rows of block row `row`, consumed at its diagonal tile
+      const int na = min(TB, d.nI - row * TB);
+      const double* Gb = A.gmat + d.g_off + (long long)row * TB * d.nP;
+      for (int e = tid; e < na * d.nP; e += 256) gs[e] = __ldg(Gb + e);
+    };
+    if (coarse) stage_g(o0_of(C.t0));
+    // stage x_0 .. x_ob (16-byte pairs; rows beyond n_I and columns beyond ncl are zero)
+    {
+      const double* src = A.vin + d.rI_off * A.ncols + A.c_off;
+      const int nrow = (ob + 1) * TB;
+      const bool vec2 = ((A.ncols | A.c_off) & 1) == 0;
+      for (int e = tid; e < nrow * (CH_NC / 2); e += 256) {
+        const int r = e >> 3, cp = (e & 7) * 2;
+        double* dst = xb + (r >> 6) * CH_XBLK + ch_xpos(r & (TB - 1), cp);
+        if (r < d.nI && cp + 1 < ncl && vec2) {
+          cp_async16(dst, src + (long long)r * A.ncols + cp);
+        } else {
+          dst[0] = (r < d.nI && cp < ncl) ? src[(long long)r * A.ncols + cp] : 0.0;
+          dst[1] = (r < d.nI && cp + 1 < ncl) ? src[(long long)r * A.ncols + cp + 1] : 0.0;
+        }
+      }
+      cp_async_commit();
+      cp_async_wait<0>();
+      __syncthreads();
+    }
+    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    int o = tri_row(C.t0), j = C.t0 - o * (o + 1) / 2;
+    for (int t = C.t0; t < C.t1; ++t, ++i) {
+      const unsigned s = (base + i) % STAGES;
+      mbar_wait(&ctl->full[s], ((base + i) / STAGES) & 1);
+      const double* Tt = ring + s * TILE_ELEMS;
+      const double* xo = xb + o * CH_XBLK;
+      if (j < o) {
+        unsigned tr[8];
+        tm_ld8_issue(tbase + 8 * j, tr);  // block j's accumulator, in flight during N
+        const double* xj = xb + j * CH_XBLK;
+#pragma unroll 4
+        for (int k0 = 0; k0 < TB; k0 += 4) {
+          const double a = Tt[swz(warp * 8 + g, k0 + t4)];
+          const int xr = (k0 + t4) * CH_NC + ((t4 & 1) << 3) + g;  // ch_xpos(k0 + t4, nb * 8 + g), nb = 0
+          dmma8x8x4(acc[0][0], acc[0][1], a, xj[xr]);
+          dmma8x8x4(acc[1][0], acc[1][1], a, xj[xr ^ 8]);
+        }
+        tm_wait_ld();
+        double pt[2][2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) pt[q >> 1][q & 1] = __hiloint2double((int)tr[2 * q + 1], (int)tr[2 * q]);
+#pragma unroll 4
+        for (int k0 = 0; k0 < TB; k0 += 4) {
+          const double a = Tt[swz(k0 + t4, warp * 8 + g)];
+          const int xr = (k0 + t4) * CH_NC + ((t4 & 1) << 3) + g;
+          dmma8x8x4(pt[0][0], pt[0][1], a, xo[xr]);
+          dmma8x8x4(pt[1][0], pt[1][1], a, xo[xr ^ 8]);
+        }
+        tm_st8(tbase + 8 * j, pt);
+      } else {  // diagonal tile (full): the row's N result joins block o's accumulator
+#pragma unroll 4
+        for (int k0 = 0; k0 < TB; k0 += 4) {
+          const double a = Tt[swz(warp * 8 + g, k0 + t4)];
+          const int xr = (k0 + t4) * CH_NC + ((t4 & 1) << 3) + g;
+          dmma8x8x4(acc[0][0], acc[0][1], a, xo[xr]);
+          dmma8x8x4(acc[1][0], acc[1][1], a, xo[xr ^ 8]);
+        }
+        double v[2][2];
+        tm_ld8(tbase + 8 * o, v);
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          v[q >> 1][q & 1] += acc[q >> 1][q & 1];
+          acc[q >> 1][q & 1] = 0.0;
+        }
+        tm_st8(tbase + 8 * o, v);
+        // coarse partial of block row o (F-apply): G_k[rows o]^T x_o, G staged in
+        // shared memory at the row's first tile (visible after that tile's barrier)
+        if (coarse && tid < d.nP * CH_NC) {
+          const int q = tid / CH_NC, cc = tid % CH_NC;
+          const int na = min(TB, d.nI - o * TB);
+          double ga = 0.0;
+#pragma unroll 4
+          for (int r = 0; r < na; ++r) ga += gs[r * d.nP + q] * xo[ch_xpos(r, cc)];
+          if (cc < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + cc] = ga;
+        }
+      }
+      tm_wait_st();
+      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+      __syncthreads();  // slot s consumed by every warp
+      if (tid == 0 && i + STAGES < ntiles) issue(i + STAGES);
+      if (++j > o) {
+        ++o;
+        j = 0;
+        if (coarse && t + 1 < C.t1) {
+          stage_g(o);  // every thread is past the diagonal tile's use of gs (barrier above)
+        }
+      }
+    }
+    // a chunk that ends inside a row: the row's N partial joins block o's accumulator
+    if (j != 0) {
+      double v[2][2];
+      tm_ld8(tbase + 8 * o, v);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) v[q >> 1][q & 1] += acc[q >> 1][q & 1];
+      tm_st8(tbase + 8 * o, v);
+      tm_wait_st();
+    }
+    // write the chunk's partial blocks 0..ob, zero the accumulators
+    const double zero[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int jb = 0; jb <= ob; ++jb) {
+      double v[2][2];
+      tm_ld8(tbase + 8 * jb, v);
+      tm_st8(tbase + 8 * jb, zero);
+      const long long pb = A.cpb[d.blk0 + jb] + (C.rank - A.cfirst[d.blk0 + jb]);
+      double* out = A.spart + (pb * TB + warp * 8 + g) * A.ncols + A.c_off;
+#pragma unroll
+      for (int nb = 0; nb < 2; ++nb) {
+        const int cc = nb * 8 + 2 * t4;
+        if (cc + 1 < ncl && ((A.ncols | A.c_off) & 1) == 0) {
+          *reinterpret_cast<double2*>(out + cc) = make_double2(v[nb][0], v[nb][1]);
+        } else {
+          if (cc < ncl) out[cc] = v[nb][0];
+          if (cc + 1 < ncl) out[cc + 1] = v[nb][1];
+        }
+      }
+    }
+    tm_wait_st();
+    __syncthreads();  // x blocks reused by the next chunk
+  }
+  if (tid == 0) ctl->streamed = base + ntiles;
+  __syncthreads();
+}
+
 // y_j = sum over the row segments of the N-partials + sum_{i > j} partial (i, j),
 // for one (subdomain, block) work item (fixed order).
 __device__ __forceinline__ void sym_reduce_item(const TmvArgs& A, int k, int j) {
@@ -1113,6 +1377,9 @@ struct PcgArgs {
   long long n_slots;
   double* coef;  // PCG coefficients: alpha_j of column c at coef[c*coef_ld + j], beta_j at coef[(ncols+c)*coef_ld + j]
   int coef_ld;
+  int chunk;                   // several RHS: the chunk pass (sym_chunks) replaces the row-segment pass
+  const int* chunk_ptr;        // chunk pass: this CTA's chunks chunk_list[chunk_ptr[b] .. chunk_ptr[b+1])
+  const SymChunk* chunk_list;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -1182,6 +1449,25 @@ __device__ __forceinline__ void sym_phase(TmvArgs A, const int* cta_ptr, const i
     const int beg = cta_ptr[blockIdx.x], end = cta_ptr[blockIdx.x + 1];
     sym_stream<NCP, STAGES>(A, cta_items + beg, end - beg, smem);
   }
+}
+
+__shared__ ChunkCtl g_chunk_ctl;  // per CTA (chunk pass): ring mbarriers, tensor memory, stream count
+
+// The symmetric pass of the persistent kernel: the chunk pass (several RHS) or the
+// row-segment stream.
+template <int NCP, int STAGES>
+__device__ __forceinline__ void sym_pass(const PcgArgs& P, TmvArgs A, double* smem) {
+  if constexpr (NCP == 16) {
+    if (P.chunk) {
+      const int beg = P.chunk_ptr[blockIdx.x], end = P.chunk_ptr[blockIdx.x + 1];
+      for (int c0 = 0; c0 < A.ncols; c0 += CH_NC) {
+        A.c_off = c0;
+        sym_chunks<STAGES>(A, P.chunk_list + beg, end - beg, smem, &g_chunk_ctl);
+      }
+      return;
+    }
+  }
+  sym_phase<NCP, STAGES>(A, P.cta_ptr, P.cta_items, P.ncp, smem);
 }
 
 __device__ __forceinline__ double sym_value(const double* spart, const SlotRed* sred, long long a, int nc, int c);
@@ -1432,7 +1718,7 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     const int j = blockIdx.x * VT + threadIdx.x;
     LamDev L{};
     SlotRed sr[2] = {};
-    sym_phase<NCP, STAGES>(P.wsym, P.cta_ptr, P.cta_items, P.ncp, smem);
+    sym_pass<NCP, STAGES>(P, P.wsym, smem);
     if ((row1 || row1s) && j < P.m) {  // static row data, loaded ahead of the barrier
       L = P.lam[j];
       sr[0] = P.slot_red[L.slot[0]];
@@ -1526,7 +1812,7 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
     LamDev L{};
     SlotRed sr[2] = {};
     double w2[2] = {0.0, 0.0};
-    sym_phase<NCP, STAGES>(P.ssym, P.cta_ptr, P.cta_items, P.ncp, smem);
+    sym_pass<NCP, STAGES>(P, P.ssym, smem);
     if (row1 && j < P.m) {  // static row data, loaded ahead of the barrier
       L = P.lam[j];
       sr[0] = P.slot_red[L.slot[0]];
@@ -1577,6 +1863,30 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     if (cc < nc)
       for (int j = blockIdx.x * R + rl; j < m; j += nb * R) f((long long)j * nc + cc, j);
   };
+  if constexpr (NCP == 16 && EXPL) {
+    if (P.chunk) {  // chunk pass: ring mbarriers and the tensor-memory accumulators
+      if (tid == 0) {
+        for (int s2 = 0; s2 < STAGES; ++s2) mbar_init(&g_chunk_ctl.full[s2], 1);
+        g_chunk_ctl.streamed = 0;
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+      }
+      if ((tid >> 5) == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                         (unsigned)__cvta_generic_to_shared(&g_chunk_ctl.tmem)),
+                     "n"(CH_TMEM_COLS));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncthreads();
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      const int w = tid >> 5;
+      const unsigned tb = g_chunk_ctl.tmem + ((unsigned)(32 * (w & 3)) << 16) + 256u * (w >> 2);
+      const double zero[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+      for (int jb = 0; jb < 32; ++jb) tm_st8(tb + 8 * jb, zero);
+      tm_wait_st();
+      __syncthreads();
+    }
+  }
   // ---- init: lambda = 0, r = d, r0 = ||d|| ----
   {
     double acc = 0.0;
@@ -1782,6 +2092,15 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     }
     if (tid < nc) s_act[tid] = s_new[tid];
     pcg_barrier(P);
+  }
+  if constexpr (NCP == 16 && EXPL) {
+    if (P.chunk) {
+      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+      __syncthreads();
+      if ((tid >> 5) == 0)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(g_chunk_ctl.tmem),
+                     "n"(CH_TMEM_COLS));
+    }
   }
   if (blockIdx.x == 0 && tid == 0) {
     P.st->it = it;
@@ -2112,6 +2431,90 @@ static TmvArgs base_args(ietidp_s* h, int mode, int ncols) {
   return a;
 }
 
+// Plan of the chunk pass for `grid` CTAs: the tiles of all subdomains in order (lower
+// row-major within a subdomain; weight 1 for a diagonal tile, which has only the row
+// product, 2 otherwise) cut into `grid` contiguous ranges of equal weight; a range
+// splits into one chunk per subdomain it touches.
+static void plan_chunks(ietidp_s* h, int grid, int nc) {
+  const int ns = h->n_sub;
+  long long W = 0;
+  for (int k = 0; k < ns; ++k) {
+    const long long nt = h->h_sub[k].nt;
+    W += nt * nt;  // nt diagonal tiles (1) + nt(nt-1)/2 off-diagonal (2)
+  }
+  std::vector<std::vector<SymChunk>> lists(grid);
+  std::vector<int> nchunk(ns, 0);
+  std::vector<std::vector<std::pair<int, int>>> sub_chunks(ns);  // (t0, t1) per rank
+  long long cum = 0;
+  int b = 0;
+  for (int k = 0; k < ns; ++k) {
+    const SubDev& d = h->h_sub[k];
+    const int T = d.nt * (d.nt + 1) / 2;
+    bool open = false;
+    for (int t = 0, o = 0, j = 0; t < T; ++t) {
+      if (!open) {
+        lists[b].push_back({k, t, t, nchunk[k]++, d.tile_off / TILE_ELEMS + t});
+        sub_chunks[k].push_back({t, t});
+        open = true;
+      }
+      lists[b].back().t1 = t + 1;
+      sub_chunks[k].back().second = t + 1;
+      cum += (j == o) ? 1 : 2;
+      if (b < grid - 1 && cum * grid >= W * (b + 1)) {
+        ++b;
+        open = false;
+      }
+      if (++j > o) {
+        ++o;
+        j = 0;
+      }
+    }
+  }
+  std::vector<int> ptr(grid + 1, 0);
+  std::vector<SymChunk> all;
+  for (int c = 0; c < grid; ++c) {
+    all.insert(all.end(), lists[c].begin(), lists[c].end());
+    ptr[c + 1] = (int)all.size();
+  }
+  auto row_of = [](int t) {
+    int o = 0;
+    while ((o + 1) * (o + 2) / 2 <= t) ++o;
+    return o;
+  };
+  std::vector<long long> cpb;
+  std::vector<int> cfirst;
+  std::vector<SlotRed> sred(std::max(h->n_slots, 1));
+  long long pb = 0;
+  for (int k = 0; k < ns; ++k) {
+    const SubDev& d = h->h_sub[k];
+    const int C = (int)sub_chunks[k].size();
+    std::vector<int> cnt(d.nt);
+    for (int j = 0; j < d.nt; ++j) {
+      int cf = C;
+      for (int c = 0; c < C; ++c)
+        if (row_of(sub_chunks[k][c].second - 1) >= j) {
+          cf = c;
+          break;
+        }
+      cfirst.push_back(cf);
+      cpb.push_back(pb);
+      cnt[j] = C - cf;
+      pb += cnt[j];
+    }
+    for (int a = 0; a < d.nI; ++a) {
+      const int j = a / TB;
+      sred[d.rI_off + a] = {cpb[d.blk0 + j] * TB + a % TB, cnt[j], 0};
+    }
+  }
+  h->chunk_ptr.upload(ptr, h->stream);
+  h->chunk_list.upload(all, h->stream);
+  h->chunk_cpb.upload(cpb, h->stream);
+  h->chunk_cfirst.upload(cfirst, h->stream);
+  h->chunk_slot_red.upload(sred, h->stream);
+  h->chunk_spart.alloc((size_t)std::max(pb, 1LL) * TB * nc);
+  h->chunk_grid = grid;
+}
+
 template <int NCP, int STAGES, bool EXPL>
 static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
   auto kern = k_pcg<NCP, STAGES, EXPL>;
@@ -2150,6 +2553,20 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
   PcgArgs args = a;
   args.cta_ptr = h->cta_ptr.p;
   args.cta_items = h->cta_items.p;
+  if (args.chunk) {
+    if (h->chunk_grid != grid) plan_chunks(h, grid, args.ncols);
+    args.chunk_ptr = h->chunk_ptr.p;
+    args.chunk_list = h->chunk_list.p;
+    for (TmvArgs* t : {&args.wsym, &args.ssym}) {
+      t->nt_max = (h->plan.max_nI + TB - 1) / TB;
+      t->spart = h->chunk_spart.p;
+      t->cpb = h->chunk_cpb.p;
+      t->cfirst = h->chunk_cfirst.p;
+    }
+    args.slot_red = h->chunk_slot_red.p;
+    args.fold = 1;
+    args.fold_multi = 1;  // the gathers sum the (few) chunk partials of each slot
+  }
   const char* prof_env = getenv("IETIDP_PCG_PROF");
   DevBuf<unsigned long long>& prof = h->pcg_prof;  // per handle, on the handle's device
   if (prof_env) {
@@ -2288,6 +2705,27 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.coef_ld = h->coef_ld;
   a.n_items = h->opt.loop == IETIDP_LOOP_EXPLICIT ? h->n_symwork : h->n_loopwork;
   a.ncp = cfg.ncp;
+  {
+    // several RHS: the chunk pass (tensor-memory accumulators, bulk-copied tile stream;
+    // IETIDP_CHUNK=0 selects the row-segment pass)
+    const int nt = (h->plan.max_nI + TB - 1) / TB;
+    const bool want = h->opt.loop == IETIDP_LOOP_EXPLICIT && cfg.ncp == 16 && nt <= 32 &&
+                      !(getenv("IETIDP_CHUNK") && atoi(getenv("IETIDP_CHUNK")) == 0);
+    if (want) {
+      const int gsz = TB * std::max(h->plan.nPmax, 1);  // staged G_k rows
+      int stages = 3;
+      int bytes = (stages * TILE_ELEMS + nt * CH_XBLK + gsz) * 8;
+      if (bytes > 210 * 1024) {
+        stages = 2;
+        bytes = (stages * TILE_ELEMS + nt * CH_XBLK + gsz) * 8;
+      }
+      if (bytes <= 210 * 1024 && bytes >= 2 * h->n_primal * nc * (int)sizeof(double)) {
+        a.chunk = 1;
+        cfg.stages = stages;
+        cfg.smem = bytes;
+      }
+    }
+  }
   if (h->n_primal * nc * 8 > cfg.smem) return false;
   if (h->opt.loop == IETIDP_LOOP_EXPLICIT) {
     if (cfg.ncp == 1 && cfg.stages == 2) return launch_pcg_t<1, 2, true>(h, cfg, a);

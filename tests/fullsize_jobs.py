@@ -9,6 +9,16 @@ import time
 
 import numpy as np
 
+# the full-size oracle jobs: config key -> right-hand-side columns (None: all)
+FULLSIZE_JOBS = {"C2": None, "C3": None, "C4": None, "C5c0": [0], "C5c7": [7]}
+U_SAMPLES = 8192
+
+
+def u_sample_index(n, seed=20250104):
+    """The u positions stored in the golden files (seeded, sorted, without repeats)."""
+    rng = np.random.default_rng(seed)
+    return np.sort(rng.choice(n, size=min(U_SAMPLES, n), replace=False))
+
 
 def oracle_job(name, cols=None, threads=None):
     """(BLAS threads limited to `threads`: the jobs run side by side.)"""
