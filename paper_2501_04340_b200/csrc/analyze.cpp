@@ -17,6 +17,7 @@
 #include <numeric>
 #include <set>
 #include <thread>
+#include <unordered_map>
 
 #include "handle.h"
 
@@ -603,11 +604,69 @@ void analyze_all(ietidp_s* h) {
                   "multiplier row " + std::to_string(l) + " is not {+1,-1} in two subdomains");
 
   stage("B validation");
-  // ---- per-subdomain analysis, in parallel ----
-  std::vector<LocalResult> loc(ns);
-  parallel_for(ns, [&](int k) { loc[k] = analyze_sub(h->in[k], k, h->opt.ordering, h->opt.leaf_size); });
+  // ---- pattern classes: subdomains whose K pattern, tree, primal DOFs and r_I set
+  // (supp B) coincide have identical symbolic analyses (the box tilings repeat a few
+  // face/edge/corner patterns: C5 has 27 classes of 128) ----
+  std::vector<int> rep(ns);
+  {
+    std::vector<uint64_t> hs(ns);
+    std::vector<std::vector<int32_t>> bsorted(ns);
+    parallel_for(ns, [&](int k) {
+      const SubIn& in = h->in[k];
+      bsorted[k] = in.B_dof;
+      std::sort(bsorted[k].begin(), bsorted[k].end());
+      uint64_t x = 1469598103934665603ull;
+      auto mix = [&](const void* p, size_t n) {
+        const unsigned char* b = static_cast<const unsigned char*>(p);
+        for (size_t i = 0; i < n; ++i) x = (x ^ b[i]) * 1099511628211ull;
+      };
+      auto mixv = [&](const auto& v) {
+        const uint64_t n = v.size();
+        mix(&n, sizeof(n));
+        if (n) mix(v.data(), n * sizeof(v[0]));
+      };
+      mix(&in.n, sizeof(in.n));
+      mixv(in.rowptr);
+      mixv(in.col);
+      mixv(in.tree);
+      mixv(in.prim);
+      mixv(bsorted[k]);
+      hs[k] = x;
+    });
+    std::unordered_map<uint64_t, std::vector<int>> byhash;
+    for (int k = 0; k < ns; ++k) {
+      rep[k] = k;
+      auto& cand = byhash[hs[k]];
+      for (int r : cand) {
+        const SubIn &a = h->in[k], &b = h->in[r];
+        if (a.n == b.n && a.rowptr == b.rowptr && a.col == b.col && a.tree == b.tree && a.prim == b.prim &&
+            bsorted[k] == bsorted[r]) {
+          rep[k] = r;
+          break;
+        }
+      }
+      if (rep[k] == k) cand.push_back(k);
+    }
+  }
+  std::vector<int> reps;
   for (int k = 0; k < ns; ++k)
+    if (rep[k] == k) reps.push_back(k);
+  h->n_pattern_classes = (int)reps.size();
+  stage("pattern classes");
+
+  // ---- per-subdomain analysis (one per pattern class), in parallel ----
+  std::vector<LocalResult> loc(ns);
+  parallel_for((int)reps.size(), [&](int i) {
+    const int k = reps[i];
+    loc[k] = analyze_sub(h->in[k], k, h->opt.ordering, h->opt.leaf_size);
+  });
+  for (int k : reps)
     if (loc[k].st != IETIDP_OK) throw Error(loc[k].st, loc[k].err);
+  parallel_for(ns, [&](int k) {
+    if (rep[k] == k) return;
+    loc[k] = loc[rep[k]];
+    for (auto& x : loc[k].sn) x.sub = k;
+  });
 
   stage("per-subdomain analysis");
   Plan& P = h->plan;
@@ -1214,83 +1273,111 @@ void analyze_all(ietidp_s* h) {
   P.g_n = (int)gwork.size() - P.g_off;
 
   stage("offsets/items");
-  // ---- scatter lists (per subdomain in parallel, merged per level) ----
-  struct Scat {
-    std::vector<std::vector<long long>> fd;
-    std::vector<std::vector<int>> fs;
-    std::vector<long long> fxd;
-    std::vector<int> fxs;
-    std::vector<int> kdiag;
+  // ---- scatter lists: relative entries once per pattern class (in parallel), then
+  // every subdomain's absolute lists written in parallel into the merged arrays ----
+  struct Rel {
+    std::vector<std::vector<int>> off, sl, src;  // per level: in-front offset, local supernode, CSR index
+    std::vector<int> fxr, fxs;                   // loads: position, local DOF
+    std::vector<int> kdiag;                      // r_I diagonal entries: CSR index
     std::string err;
   };
-  std::vector<Scat> sc(ns);
-  parallel_for(ns, [&](int k) {
-    Scat& S = sc[k];
+  std::vector<Rel> rel(ns);
+  parallel_for((int)reps.size(), [&](int ri) {
+    const int k = reps[ri];
+    Rel& S = rel[k];
     const SubIn& in = h->in[k];
     const SubPlan& sp = P.subs[k];
     const SubDev& d = h->h_sub[k];
     const int ne = d.ne;
-    S.fd.resize(P.max_level + 1);
-    S.fs.resize(P.max_level + 1);
+    const int sb = sp.sn_begin[0];
+    S.off.resize(P.max_level + 1);
+    S.sl.resize(P.max_level + 1);
+    S.src.resize(P.max_level + 1);
     std::vector<int> own(ne);
-    for (int s = sp.sn_begin[0]; s < sp.sn_begin[1]; ++s)
-      for (int q = 0; q < P.sn[s].npiv; ++q) own[P.sn[s].c0 + q] = s;
+    for (int sn = sp.sn_begin[0]; sn < sp.sn_begin[1]; ++sn)
+      for (int q = 0; q < P.sn[sn].npiv; ++q) own[P.sn[sn].c0 + q] = sn;
     S.kdiag.assign(sp.nI, -1);
     // K lower triangle in position order, column by column (pi >= pj)
     for (int pj = 0; pj < ne; ++pj) {
-      int j = sp.perm[pj];
-      int s = own[pj];
-      const SnHost& hs = P.sn[s];
-      const SnDev& ds = sd[s];
-      int lcol = pj - hs.c0;
+      const int j = sp.perm[pj];
+      const int sn = own[pj];
+      const SnHost& hs = P.sn[sn];
+      const SnDev& ds = sd[sn];
+      const int lcol = pj - hs.c0;
       for (int64_t e = in.rowptr[j]; e < in.rowptr[j + 1]; ++e) {
-        int pi = sp.pos[in.col[e]];
+        const int pi = sp.pos[in.col[e]];
         if (pi < pj) continue;  // tree DOF (-1) or upper triangle
-        int lrow = find_in_front(hs, pi);
+        const int lrow = find_in_front(hs, pi);
         if (lrow < 0) {
           S.err = "internal: entry outside the symbolic structure";
           return;
         }
-        S.fd[hs.level].push_back(ds.front_off + (long long)lcol * ds.ld + lrow);
-        S.fs[hs.level].push_back((int)(d.kval_off + e));
-        if (pi == pj && pj >= sp.nV && pj < sp.nr) S.kdiag[pj - sp.nV] = (int)(d.kval_off + e);
+        S.off[hs.level].push_back(lcol * ds.ld + lrow);
+        S.sl[hs.level].push_back(sn - sb);
+        S.src[hs.level].push_back((int)e);
+        if (pi == pj && pj >= sp.nV && pj < sp.nr) S.kdiag[pj - sp.nV] = (int)e;
       }
-      for (int c = 0; c < nrhs; ++c) {
-        S.fxd.push_back((d.x_off + pj) * nrhs + c);
-        S.fxs.push_back((int)(d.f_off + j + (long long)c * in.n));
-      }
+      S.fxr.push_back(pj);
+      S.fxs.push_back(j);
     }
     for (int a = 0; a < sp.nI; ++a)
       if (S.kdiag[a] < 0) S.err = "subdomain " + std::to_string(k) + ": missing diagonal entry";
   });
-  for (int k = 0; k < ns; ++k)
-    if (!sc[k].err.empty()) throw Error(IETIDP_E_ARG, sc[k].err);
-  std::vector<long long> fdst, fxdst;
-  std::vector<int> fsrc, fxsrc, kdiag;
-  for (int L = 0; L <= P.max_level; ++L) {
-    P.levels[L].sc_off = (long long)fdst.size();
-    for (int k = 0; k < ns; ++k) {
-      LevelPlan& gl = P.glevels[P.sub_group[k]][L];
-      if (k == 0 || P.sub_group[k] != P.sub_group[k - 1]) gl.sc_off = (long long)fdst.size();
-      gl.sc_n = (long long)fdst.size() + (long long)sc[k].fd[L].size() - gl.sc_off;
-      fdst.insert(fdst.end(), sc[k].fd[L].begin(), sc[k].fd[L].end());
-      fsrc.insert(fsrc.end(), sc[k].fs[L].begin(), sc[k].fs[L].end());
-      std::vector<long long>().swap(sc[k].fd[L]);
-      std::vector<int>().swap(sc[k].fs[L]);
+  for (int k : reps)
+    if (!rel[k].err.empty()) throw Error(IETIDP_E_ARG, rel[k].err);
+  // segment offsets in the merged arrays: by level, then subdomain (groups contiguous)
+  const int NL = P.max_level + 1;
+  std::vector<long long> segoff((size_t)NL * ns + 1, 0);
+  {
+    long long o = 0;
+    for (int L = 0; L < NL; ++L) {
+      P.levels[L].sc_off = o;
+      for (int k = 0; k < ns; ++k) {
+        LevelPlan& gl = P.glevels[P.sub_group[k]][L];
+        if (k == 0 || P.sub_group[k] != P.sub_group[k - 1]) gl.sc_off = o;
+        segoff[(size_t)L * ns + k] = o;
+        o += (long long)rel[rep[k]].off[L].size();
+        gl.sc_n = o - gl.sc_off;
+      }
+      P.levels[L].sc_n = o - P.levels[L].sc_off;
     }
-    P.levels[L].sc_n = (long long)fdst.size() - P.levels[L].sc_off;
+    segoff[(size_t)NL * ns] = o;
+  }
+  std::vector<long long> fxoff(ns + 1, 0), kdoff(ns + 1, 0);
+  for (int k = 0; k < ns; ++k) {
+    fxoff[k + 1] = fxoff[k] + (long long)rel[rep[k]].fxr.size() * nrhs;
+    kdoff[k + 1] = kdoff[k] + (long long)rel[rep[k]].kdiag.size();
   }
   P.gfx.assign(P.ngroups, {0, 0});
   for (int k = 0; k < ns; ++k) {
     auto& gx = P.gfx[P.sub_group[k]];
-    if (k == 0 || P.sub_group[k] != P.sub_group[k - 1]) gx.first = (long long)fxdst.size();
-    gx.second = (long long)fxdst.size() + (long long)sc[k].fxd.size() - gx.first;
-    fxdst.insert(fxdst.end(), sc[k].fxd.begin(), sc[k].fxd.end());
-    fxsrc.insert(fxsrc.end(), sc[k].fxs.begin(), sc[k].fxs.end());
-    kdiag.insert(kdiag.end(), sc[k].kdiag.begin(), sc[k].kdiag.end());
+    if (k == 0 || P.sub_group[k] != P.sub_group[k - 1]) gx.first = fxoff[k];
+    gx.second = fxoff[k + 1] - gx.first;
   }
+  std::vector<long long> fdst(segoff[(size_t)NL * ns]), fxdst(fxoff[ns]);
+  std::vector<int> fsrc(fdst.size()), fxsrc(fxoff[ns]), kdiag(kdoff[ns]);
+  parallel_for(ns, [&](int k) {
+    const Rel& S = rel[rep[k]];
+    const SubPlan& sp = P.subs[k];
+    const SubDev& d = h->h_sub[k];
+    const int sb = sp.sn_begin[0];
+    for (int L = 0; L < NL; ++L) {
+      const long long o = segoff[(size_t)L * ns + k];
+      const size_t n = S.off[L].size();
+      for (size_t q = 0; q < n; ++q) {
+        fdst[o + q] = sd[sb + S.sl[L][q]].front_off + S.off[L][q];
+        fsrc[o + q] = (int)(d.kval_off + S.src[L][q]);
+      }
+    }
+    long long o = fxoff[k];
+    for (size_t q = 0; q < S.fxr.size(); ++q)
+      for (int c = 0; c < nrhs; ++c, ++o) {
+        fxdst[o] = (d.x_off + S.fxr[q]) * nrhs + c;
+        fxsrc[o] = (int)(d.f_off + S.fxs[q] + (long long)c * d.nk);
+      }
+    for (size_t a = 0; a < S.kdiag.size(); ++a) kdiag[kdoff[k] + a] = (int)(d.kval_off + S.kdiag[a]);
+  });
 
-  stage("scatter lists");
   // ---- multipliers, slots, primal bookkeeping ----
   std::vector<int> slot_lam(h->n_slots);
   std::vector<float> slot_sign(h->n_slots);
@@ -1442,6 +1529,7 @@ void analyze_all(ietidp_s* h) {
   h->slot_lam.upload(slot_lam, s);
   h->slot_sign.upload(slot_sign, s);
   h->lam.upload(lam, s);
+  h->h_lam = lam;
   h->scoef_ptr.upload(scoef_ptr, s);
   h->scoef_src.upload(scoef_src, s);
   h->pcon_ptr.upload(pcon_ptr, s);

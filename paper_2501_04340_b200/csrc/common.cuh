@@ -23,15 +23,16 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Swizzled position of element (r, m) of a TB x TB row-major tile: 16-byte chunks
-// of a row are XOR-permuted by (r & 7) so that both the row-wise and the column-wise
-// DMMA fragment loads from shared memory are bank-conflict free. The loop's tiles
+// Swizzled position of element (r, m) of a TB x TB row-major tile: the 4-double
+// groups of a row are XOR-permuted by (r & 3), so that the 16 lanes of each half-warp
+// of an 8-byte DMMA fragment load -- 4 rows x 4 consecutive columns, row-wise
+// (A = S) or column-wise (A = S^T) -- hit 16 distinct bank pairs (measured: the
+// previous (r & 7) permutation of 16-byte chunks left every LDS.64 2-way
+// conflicted, ncu profiles/r02_pcg_c5_chunk_raw.txt). The loop's tiles
 // (L_II, L_II^-1, W_k = S_II^-1, S_II) are STORED in this layout in global memory,
 // so that a tile moves into shared memory as one contiguous 32 KB copy (one
 // cp.async.bulk, or linear 16-byte cp.async).
-__device__ __forceinline__ int swz(int r, int m) {
-  return r * TB + ((((m >> 1) ^ (r & 7))) << 1) + (m & 1);
-}
+__device__ __forceinline__ int swz(int r, int m) { return r * TB + (m ^ ((r & 3) << 2)); }
 
 __device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
   unsigned s = (unsigned)__cvta_generic_to_shared(smem);

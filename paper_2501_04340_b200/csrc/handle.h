@@ -182,11 +182,15 @@ struct ietidp_s {
   int lpt_grid = 0;
   // several-RHS chunk pass of the persistent PCG (pcg.cu sym_chunks), planned for a grid
   int chunk_grid = 0;
+  int n_pattern_classes = 0;  // distinct subdomain patterns found by the analysis
   ieti::DevBuf<int> chunk_ptr, chunk_cfirst;
   ieti::DevBuf<ieti::SymChunk> chunk_list;
   ieti::DevBuf<long long> chunk_cpb;
   ieti::DevBuf<ieti::SlotRed> chunk_slot_red;
   ieti::DevBuf<double> chunk_spart;
+  ieti::DevBuf<ieti::GatherRec> chunk_grec;
+  ieti::DevBuf<double> chunk_wrec;
+  std::vector<ieti::LamDev> h_lam;  // host copy of the multiplier rows (slots, signs)
   ieti::DevBuf<int> sub_cta0, sub_ncta;   // loop CTAs of each subdomain
   ieti::DevBuf<ieti::LamDev> lam;
   ieti::DevBuf<int> slot_lam;             // per r_I slot: multiplier

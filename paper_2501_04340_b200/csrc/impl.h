@@ -121,6 +121,14 @@ struct SymChunk {
   long long gtile;
 };
 
+// One multiplier row of the chunk-mode gathers: its two slots' partial-sum lists
+// (SlotRed base/count of the chunk partial blocks) and B signs.
+struct GatherRec {
+  long long base[2];
+  int cnt[2];
+  float sign[2];
+};
+
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).
 struct LoopWork {
   int sub, nblk, blk0, blk1;

@@ -92,6 +92,7 @@ struct TmvArgs {
   int slot_in;             // FWD/PRE1/SYM: vin is already in slot order (B^T, weights applied)
   int nPmax, ncols, c_off;
   int nt_max;              // SYM (chunk pass): largest number of TB-blocks of a subdomain (x staging)
+  int n_sub;               // number of subdomains (chunk-mode coarse phase)
   const SymChunk* chunks;  // SYM (chunk pass): the chunks of the several-RHS pass
   const long long* cpb;    // SYM (chunk pass): first partial block of each (subdomain, block)
   const int* cfirst;       // SYM (chunk pass): rank of the first chunk writing (subdomain, block)
@@ -739,15 +740,15 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
 // of the chunk every block j <= o_b is written once as the chunk's partial block
 // (then zeroed); the gathers sum the (typically 1-3) partial blocks of a slot in
 // chunk order (deterministic). The chunk's input blocks x_0..x_ob are staged in shared
-// memory (16 columns, 16-byte pairs XOR-swizzled by row parity: conflict-free DMMA B
-// fragments). Tensor memory: lanes = the warp's quadrant (32 (w & 3) + lane), columns
+// memory (16 columns, 4-double groups XOR-swizzled by (r & 3): conflict-free DMMA B
+// fragments, ch_xpos). Tensor memory: lanes = the warp's quadrant (32 (w & 3) + lane), columns
 // 256 (w >> 2) + 8 j + [0, 8) hold block j's fragment: up to 32 blocks (n_I <= 2048).
 // ---------------------------------------------------------------------------
 constexpr int CH_NC = 16;                 // columns per chunk pass
 constexpr int CH_XBLK = TB * CH_NC;       // doubles per staged input block
 constexpr int CH_TMEM_COLS = 512;
 
-__device__ __forceinline__ int ch_xpos(int r, int c) { return r * CH_NC + (c ^ ((r & 1) << 3)); }
+__device__ __forceinline__ int ch_xpos(int r, int c) { return r * CH_NC + (c ^ ((r & 3) << 2)); }
 
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
@@ -894,7 +895,7 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
 #pragma unroll 4
         for (int k0 = 0; k0 < TB; k0 += 4) {
           const double a = Tt[swz(warp * 8 + g, k0 + t4)];
-          const int xr = (k0 + t4) * CH_NC + ((t4 & 1) << 3) + g;  // ch_xpos(k0 + t4, nb * 8 + g), nb = 0
+          const int xr = (k0 + t4) * CH_NC + (g ^ (t4 << 2));  // ch_xpos(k0 + t4, nb * 8 + g), nb = 0
           dmma8x8x4(acc[0][0], acc[0][1], a, xj[xr]);
           dmma8x8x4(acc[1][0], acc[1][1], a, xj[xr ^ 8]);
         }
@@ -905,7 +906,7 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
 #pragma unroll 4
         for (int k0 = 0; k0 < TB; k0 += 4) {
           const double a = Tt[swz(k0 + t4, warp * 8 + g)];
-          const int xr = (k0 + t4) * CH_NC + ((t4 & 1) << 3) + g;
+          const int xr = (k0 + t4) * CH_NC + (g ^ (t4 << 2));
           dmma8x8x4(pt[0][0], pt[0][1], a, xo[xr]);
           dmma8x8x4(pt[1][0], pt[1][1], a, xo[xr ^ 8]);
         }
@@ -914,7 +915,7 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
 #pragma unroll 4
         for (int k0 = 0; k0 < TB; k0 += 4) {
           const double a = Tt[swz(warp * 8 + g, k0 + t4)];
-          const int xr = (k0 + t4) * CH_NC + ((t4 & 1) << 3) + g;
+          const int xr = (k0 + t4) * CH_NC + (g ^ (t4 << 2));
           dmma8x8x4(acc[0][0], acc[0][1], a, xo[xr]);
           dmma8x8x4(acc[1][0], acc[1][1], a, xo[xr ^ 8]);
         }
@@ -1377,6 +1378,8 @@ struct PcgArgs {
   long long n_slots;
   double* coef;  // PCG coefficients: alpha_j of column c at coef[c*coef_ld + j], beta_j at coef[(ncols+c)*coef_ld + j]
   int coef_ld;
+  const GatherRec* grec;        // chunk pass: per multiplier row, its slots' partial lists and signs
+  const double* wrec;           // chunk pass: per multiplier row, the two slots' scaling weights delta
   int chunk;                   // several RHS: the chunk pass (sym_chunks) replaces the row-segment pass
   const int* chunk_ptr;        // chunk pass: this CTA's chunks chunk_list[chunk_ptr[b] .. chunk_ptr[b+1])
   const SymChunk* chunk_list;
@@ -1686,6 +1689,114 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
   block_col_reduce(dot, nc, P2, part);
 }
 
+// ---- chunk mode (several RHS): coarse correction and folded gathers ----
+
+// After the coarse right-hand side g (P.gc, ng x nc) is complete: every CTA takes its
+// subdomains, forms z_k = (S_PP^-1 g)[C_k rows] (S_PP^-1 rows and g staged in shared
+// memory) and adds G_k z_k into the first chunk partial of each of the subdomain's
+// slots, so that the gather of q = sum_k B (W_k p_k + G_k z_k) is a plain fold of the
+// partials (F_DP = W + G S_PP^-1 G^T, SURVEY F1 signs).
+__device__ __forceinline__ void coarse_gz_phase(const PcgArgs& P, const TmvArgs& A, double* smem) {
+  const int nc = P.ncols, ng = P.ng, tid = threadIdx.x;
+  double* gs = smem;                 // ng x nc
+  double* srow = gs + ng * nc;       // nP x ng rows of S_PP^-1
+  double* zk = srow + 16 * ng;       // nP x nc
+  for (int e = tid; e < ng * nc; e += VT) gs[e] = __ldcg(P.gc + e);
+  bool staged = false;
+  for (int k = blockIdx.x; k < A.n_sub; k += gridDim.x) {
+    const SubDev d = A.sub[k];
+    if (d.nP == 0 || d.nI == 0) continue;
+    __syncthreads();  // gs complete (first), srow / zk free (later)
+    staged = true;
+    const int* gid = A.prim_gid + d.prim_off;
+    for (int e = tid; e < d.nP * ng; e += VT) {
+      const int q = e / ng, j = e - q * ng;
+      srow[e] = __ldg(P.Sinv + (long long)gid[q] * ng + j);
+    }
+    __syncthreads();
+    for (int e = tid; e < d.nP * nc; e += VT) {
+      const int q = e / nc, c = e - q * nc;
+      double acc = 0.0;
+      for (int j = 0; j < ng; ++j) acc += srow[q * ng + j] * gs[j * nc + c];
+      zk[e] = acc;
+    }
+    __syncthreads();
+    // G_k z_k into partial 0 of every slot (nc threads per row)
+    const int P2 = pow2ge(nc), c = tid % P2, rl = tid / P2, R = VT / P2;
+    if (c < nc)
+      for (int a = rl; a < d.nI; a += R) {
+        const double* Gr = A.gmat + d.g_off + (long long)a * d.nP;
+        double acc = 0.0;
+        for (int q = 0; q < d.nP; ++q) acc += __ldg(Gr + q) * zk[q * nc + c];
+        const long long base = P.slot_red[d.rI_off + a].base;
+        A.spart[base * nc + c] += acc;
+      }
+  }
+  (void)staged;
+}
+
+// out[j][c] = sum_{2 slots} sign (w) sum_{p < cnt} partial_p[slot][c], plus the per-CTA
+// partial of out . dotv; UR multiplier rows per thread in flight (metadata, then all
+// partial loads, then the sums in index order: the same arithmetic as sym_value).
+template <int UR>
+__device__ __forceinline__ void gather_fold(const PcgArgs& P, const double* spart, bool weighted, double* out,
+                                            const double* dotv, double* part) {
+  const int nc = P.ncols, P2 = pow2ge(nc);
+  const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
+  const long long st = (long long)TB * nc;
+  constexpr int CM = 4;  // partials per slot loaded together (more: a loop)
+  double dot = 0.0;
+  const int stride = gridDim.x * R;
+  if (c < nc)
+    for (int j0 = blockIdx.x * R + rl; j0 < P.m; j0 += UR * stride) {
+      GatherRec g[UR];
+      double w[UR][2], dv[UR];
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const int j = j0 + u * stride;
+        if (j < P.m) {
+          g[u] = P.grec[j];
+          dv[u] = dotv[(long long)j * nc + c];
+          if (weighted) {
+            w[u][0] = P.wrec[2 * j];
+            w[u][1] = P.wrec[2 * j + 1];
+          } else {
+            w[u][0] = w[u][1] = 1.0;
+          }
+        } else {
+          g[u].cnt[0] = g[u].cnt[1] = 0;
+        }
+      }
+      double v[UR][2][CM];
+#pragma unroll
+      for (int u = 0; u < UR; ++u)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const double* p0 = spart + g[u].base[q] * nc + c;
+#pragma unroll
+          for (int p = 0; p < CM; ++p) v[u][q][p] = p < g[u].cnt[q] ? __ldcg(p0 + p * st) : 0.0;
+        }
+#pragma unroll
+      for (int u = 0; u < UR; ++u) {
+        const int j = j0 + u * stride;
+        if (j >= P.m) continue;
+        double val = 0.0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          double y = 0.0;
+#pragma unroll
+          for (int p = 0; p < CM; ++p)
+            if (p < g[u].cnt[q]) y += v[u][q][p];
+          for (int p = CM; p < g[u].cnt[q]; ++p) y += __ldcg(spart + g[u].base[q] * nc + c + p * st);
+          val += (double)g[u].sign[q] * w[u][q] * y;
+        }
+        out[(long long)j * nc + c] = val;
+        dot += val * dv[u];
+      }
+    }
+  block_col_reduce(dot, nc, P2, part);
+}
+
 // write B^T v (optionally weighted) of lambda-row j, column c into the slot vector
 __device__ __forceinline__ void to_slots(const PcgArgs& P, long long j, int c, double v, const double* w, double* out) {
   const LamDev L = P.lam[j];
@@ -1712,6 +1823,19 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
     // partial sums into the gather (no reduction phase, one barrier)
     // one column: the partial sums are folded into the gather; several: a reduction
     // phase (a slot shared by several multipliers would be summed repeatedly)
+    if (NCP == 16 && P.chunk) {
+      // chunk mode: W pass | g | z_k, G_k z_k into the partials | folded gather of q
+      sym_pass<NCP, STAGES>(P, P.wsym, smem);
+      pcg_barrier(P);
+      if (P.ng > 0) {
+        coarse_spread(P);
+        pcg_barrier(P);
+        coarse_gz_phase(P, P.wsym, smem);
+        pcg_barrier(P);
+      }
+      gather_fold<4>(P, P.wsym.spart, false, P.q, P.p, pq);
+      return;
+    }
     const bool fold = P.fold && (P.ncols == 1 || P.fold_multi);
     const bool row1 = P.ncols == 1 && P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;
     const bool row1s = P.ncols == 1 && P.ng > COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;  // spread coarse
@@ -1806,6 +1930,12 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
 
 template <int NCP, int STAGES, bool EXPL>
 __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, double* rz) {
+  if (EXPL && NCP == 16 && P.chunk) {  // chunk mode: S pass | folded, weighted gather of z
+    sym_pass<NCP, STAGES>(P, P.ssym, smem);
+    pcg_barrier(P);
+    gather_fold<4>(P, P.ssym.spart, true, P.z, P.r, rz);
+    return;
+  }
   if (EXPL) {
     const bool row1 = P.ncols == 1 && P.fold && P.m <= (int)gridDim.x * VT;
     const int j = blockIdx.x * VT + threadIdx.x;
@@ -2431,6 +2561,15 @@ static TmvArgs base_args(ietidp_s* h, int mode, int ncols) {
   return a;
 }
 
+__global__ void k_wrec(int m, const LamDev* __restrict__ lam, const double* __restrict__ delta,
+                       double* __restrict__ wrec) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < m) {
+    wrec[2 * j] = delta[lam[j].slot[0]];
+    wrec[2 * j + 1] = delta[lam[j].slot[1]];
+  }
+}
+
 // Plan of the chunk pass for `grid` CTAs: the tiles of all subdomains in order (lower
 // row-major within a subdomain; weight 1 for a diagonal tile, which has only the row
 // product, 2 otherwise) cut into `grid` contiguous ranges of equal weight; a range
@@ -2511,6 +2650,17 @@ static void plan_chunks(ietidp_s* h, int grid, int nc) {
   h->chunk_cpb.upload(cpb, h->stream);
   h->chunk_cfirst.upload(cfirst, h->stream);
   h->chunk_slot_red.upload(sred, h->stream);
+  std::vector<GatherRec> grec(std::max(h->n_lambda, 1));
+  for (int j = 0; j < h->n_lambda; ++j) {
+    const LamDev& L = h->h_lam[j];
+    for (int q = 0; q < 2; ++q) {
+      grec[j].base[q] = sred[L.slot[q]].base;
+      grec[j].cnt[q] = sred[L.slot[q]].cnt;
+      grec[j].sign[q] = L.sign[q];
+    }
+  }
+  h->chunk_grec.upload(grec, h->stream);
+  h->chunk_wrec.alloc(2 * (size_t)std::max(h->n_lambda, 1));
   h->chunk_spart.alloc((size_t)std::max(pb, 1LL) * TB * nc);
   h->chunk_grid = grid;
 }
@@ -2564,6 +2714,12 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
       t->cfirst = h->chunk_cfirst.p;
     }
     args.slot_red = h->chunk_slot_red.p;
+    args.grec = h->chunk_grec.p;
+    args.wrec = h->chunk_wrec.p;
+    args.wsym.n_sub = args.ssym.n_sub = h->n_sub;
+    if (h->n_lambda)  // the two slots' scaling weights per multiplier row (delta: set by the factorisation)
+      k_wrec<<<grid_for(h->n_lambda, 256), 256, 0, h->stream>>>(h->n_lambda, h->lam.p, h->delta.p, h->chunk_wrec.p);
+    IETI_LAUNCHED(h);
     args.fold = 1;
     args.fold_multi = 1;  // the gathers sum the (few) chunk partials of each slot
   }
