@@ -85,15 +85,27 @@ typedef enum {
                                          supernodes, r_I last                           */
 } ietidp_ordering;
 
+typedef enum {
+  IETIDP_STOP_RESIDUAL = 0,       /* ||r_k||_2 <= tol ||r_0||_2: the unpreconditioned dual
+                                     residual (BASELINE "dual residual <= 1e-10") */
+  IETIDP_STOP_PRECONDITIONED = 1  /* sqrt(r_k^T z_k) <= tol sqrt(r_0^T z_0), z = M_D^-1 r: the
+                                     preconditioned residual of the paper's experiments
+                                     (eta_tol); tested after the
+                                     preconditioner apply of each iteration (persistent PCG
+                                     kernel only)                                            */
+} ietidp_stop;
+
 typedef struct {
-  double tol;       /* PCG stop: ||r_k||_2 <= tol * ||r_0||_2 per column (unpreconditioned
-                       dual residual, r_0 = d_DP, lambda_0 = 0); default 1e-10           */
+  double tol;       /* PCG stop: per column, criterion ietidp_stop below; default ||r_k||_2 <= tol
+                       ||r_0||_2, unpreconditioned dual residual, r_0 = d_DP, lambda_0 = 0;
+                       default 1e-10                                                         */
   int max_iter;     /* default 500                                                        */
   int scaling;      /* ietidp_scaling; default IETIDP_SCALE_MULTIPLICITY                   */
   int fixed_iters;  /* > 0: run exactly this many iterations, no stop test (parity mode)  */
   int ordering;     /* ietidp_ordering; default nested dissection                         */
   int leaf_size;    /* nested-dissection leaf size (supernode of the leaves); default 96  */
   int loop;         /* ietidp_loop: operators of the PCG loop; default IETIDP_LOOP_EXPLICIT */
+  int stop;         /* ietidp_stop: PCG stopping criterion; default IETIDP_STOP_RESIDUAL      */
   int device;       /* CUDA device ordinal; default 0                                     */
   void* stream;     /* cudaStream_t all work is issued on; NULL = library-owned stream    */
 } ietidp_options;
@@ -109,7 +121,12 @@ typedef struct {
   int iters[IETIDP_MAX_RHS];     /* F-applies per column in the PCG loop                   */
   int converged[IETIDP_MAX_RHS];
   double rel_residual[IETIDP_MAX_RHS]; /* true ||d - F lambda|| / ||d|| after the loop     */
-  double ms_analyze, ms_factor, ms_coarse, ms_pcg, ms_recover; /* CUDA-event / host times  */
+  double ms_analyze, ms_factor, ms_coarse, ms_pcg, ms_recover; /* CUDA-event / host times:
+                                    ms_analyze = host symbolic analysis (validation, pattern
+                                    classes, ordering, plan), without the device part     */
+  double ms_upload;              /* device allocations, uploads and scatter-list expansion
+                                    of ietidp_analyze (host wall time)                     */
+  int n_pattern_classes;         /* distinct subdomain patterns (analysed once each)       */
 } ietidp_report;
 
 /* Defaults as documented in ietidp_options. */

@@ -202,7 +202,11 @@ class DualPrimal:
         return out
 
     # ---- PCG (SURVEY §8(c) variant) ---------------------------------------
-    def pcg(self, tol=1e-10, max_iter=500, fixed_iters=0, d=None):
+    def pcg(self, tol=1e-10, max_iter=500, fixed_iters=0, d=None, stop="residual"):
+        """stop="residual": ||r_k|| <= tol ||r_0|| tested after the r update (SURVEY §8(c)
+        variant, BASELINE's dual residual); stop="preconditioned": sqrt(r_k.z_k) <= tol
+        sqrt(r_0.z_0) tested after the preconditioner apply (the paper's eta_tol of its
+        experiments, PAPER.md:397; SPEC.md:434)."""
         d = self.d if d is None else d
         nl, nc = d.shape
         lam = np.zeros((nl, nc))
@@ -215,6 +219,7 @@ class DualPrimal:
         z = self.apply_M(r)
         p = z.copy()
         rz = np.sum(r * z, axis=0)
+        rz0 = rz.copy()
         alphas = [[] for _ in range(nc)]  # per column: alpha_j, beta_j (Lanczos, cond_lanczos)
         betas = [[] for _ in range(nc)]
         it = 0
@@ -234,7 +239,7 @@ class DualPrimal:
             iters[a] += 1
             it += 1
             rn = np.linalg.norm(r[:, a], axis=0)
-            if not fixed_iters:
+            if not fixed_iters and stop == "residual":
                 done = rn <= tol * r0[a]
                 active[a[done]] = False
                 a = np.flatnonzero(active)
@@ -242,6 +247,13 @@ class DualPrimal:
                     break
             zz = self.apply_M(r[:, a])
             rz_new = np.sum(r[:, a] * zz, axis=0)
+            if not fixed_iters and stop == "preconditioned":
+                done = np.sqrt(np.maximum(rz_new, 0.0)) <= tol * np.sqrt(rz0[a])
+                active[a[done]] = False
+                keep = ~done
+                a, zz, rz_new = a[keep], zz[:, keep], rz_new[keep]
+                if len(a) == 0:
+                    break
             beta = rz_new / rz[a]
             for c, v in zip(a, beta):
                 betas[c].append(v)
@@ -305,10 +317,10 @@ def cond_dense(D):
     return w[0], w[-1], w[-1] / w[0]
 
 
-def solve(bundle, tol=None, max_iter=500, fixed_iters=0, scaling=None, check_spd=False):
+def solve(bundle, tol=None, max_iter=500, fixed_iters=0, scaling=None, check_spd=False, stop="residual"):
     """Full oracle solve: returns dict(lam, u (list n_k x nrhs), iters, ...)."""
     dp = DualPrimal(bundle, scaling=scaling, check_spd=check_spd)
     tol = bundle["tol"] if tol is None else tol
-    lam, info = dp.pcg(tol=tol, max_iter=max_iter, fixed_iters=fixed_iters)
+    lam, info = dp.pcg(tol=tol, max_iter=max_iter, fixed_iters=fixed_iters, stop=stop)
     us, p = dp.recover(lam)
     return dict(lam=lam, u=us, p=p, dp=dp, **info)

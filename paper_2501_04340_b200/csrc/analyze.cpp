@@ -616,9 +616,16 @@ void analyze_all(ietidp_s* h) {
       bsorted[k] = in.B_dof;
       std::sort(bsorted[k].begin(), bsorted[k].end());
       uint64_t x = 1469598103934665603ull;
-      auto mix = [&](const void* p, size_t n) {
+      auto mix = [&](const void* p, size_t n) {  // 64-bit words (tail bytes), multiply-xorshift
         const unsigned char* b = static_cast<const unsigned char*>(p);
-        for (size_t i = 0; i < n; ++i) x = (x ^ b[i]) * 1099511628211ull;
+        size_t i = 0;
+        for (; i + 8 <= n; i += 8) {
+          uint64_t w;
+          memcpy(&w, b + i, 8);
+          x = (x ^ w) * 0x9E3779B97F4A7C15ull;
+          x ^= x >> 29;
+        }
+        for (; i < n; ++i) x = (x ^ b[i]) * 1099511628211ull;
       };
       auto mixv = [&](const auto& v) {
         const uint64_t n = v.size();
@@ -765,20 +772,38 @@ void analyze_all(ietidp_s* h) {
   P.dinv_doubles = dinv;
   P.inv_doubles = inv;
   P.vec_rows = vec;
+  // relative positions of every supernode's update rows in its parent's front, once
+  // per pattern class (the members' supernodes are the representative's, shifted)
+  std::vector<std::vector<int>> relv(nsn);
+  std::vector<int> relfail(ns, 0);
+  parallel_for((int)reps.size(), [&](int ri) {
+    const int k = reps[ri];
+    for (int i = P.subs[k].sn_begin[0]; i < P.subs[k].sn_begin[1]; ++i) {
+      const SnHost& sx = P.sn[i];
+      if (sx.parent < 0) continue;
+      const SnHost& par = P.sn[sx.parent];
+      relv[i].reserve(sx.rows.size());
+      for (int x : sx.rows) {
+        const int r = find_in_front(par, x);
+        if (r < 0) relfail[k] = 1;
+        relv[i].push_back(r);
+      }
+    }
+  });
+  for (int k : reps)
+    if (relfail[k]) throw Error(IETIDP_E_ARG, "internal: symbolic structure not nested");
+  parallel_for(ns, [&](int k) {
+    if (rep[k] == k) return;
+    const int d0 = P.subs[rep[k]].sn_begin[0] - P.subs[k].sn_begin[0];
+    for (int i = P.subs[k].sn_begin[0]; i < P.subs[k].sn_begin[1]; ++i) relv[i] = relv[i + d0];
+  });
   for (int i = 0; i < nsn; ++i) {
     SnHost& s = P.sn[i];
     SnDev& d = sd[i];
     d.rows_off = (int)rows_all.size();
     rows_all.insert(rows_all.end(), s.rows.begin(), s.rows.end());
     d.rel_off = (int)rel_all.size();
-    if (s.parent >= 0) {
-      const SnHost& par = P.sn[s.parent];
-      for (int x : s.rows) {
-        int r = find_in_front(par, x);
-        if (r < 0) throw Error(IETIDP_E_ARG, "internal: symbolic structure not nested");
-        rel_all.push_back(r);
-      }
-    }
+    rel_all.insert(rel_all.end(), relv[i].begin(), relv[i].end());
     d.child_off = (int)children_all.size();
     d.nchild = (int)s.children.size();
     children_all.insert(children_all.end(), s.children.begin(), s.children.end());
@@ -1354,29 +1379,44 @@ void analyze_all(ietidp_s* h) {
     if (k == 0 || P.sub_group[k] != P.sub_group[k - 1]) gx.first = fxoff[k];
     gx.second = fxoff[k + 1] - gx.first;
   }
-  std::vector<long long> fdst(segoff[(size_t)NL * ns]), fxdst(fxoff[ns]);
-  std::vector<int> fsrc(fdst.size()), fxsrc(fxoff[ns]), kdiag(kdoff[ns]);
-  parallel_for(ns, [&](int k) {
-    const Rel& S = rel[rep[k]];
-    const SubPlan& sp = P.subs[k];
-    const SubDev& d = h->h_sub[k];
-    const int sb = sp.sn_begin[0];
+  // relative entries of the pattern classes, concatenated; one expansion segment per
+  // (level, subdomain) and per subdomain's loads (expanded on the device at upload)
+  std::vector<int> rel_off, rel_sl, rel_src;
+  std::vector<long long> relbase((size_t)ns * (NL + 1), -1);  // per class rep: start of level L / loads
+  for (int k : reps) {
+    const Rel& S = rel[k];
     for (int L = 0; L < NL; ++L) {
-      const long long o = segoff[(size_t)L * ns + k];
-      const size_t n = S.off[L].size();
-      for (size_t q = 0; q < n; ++q) {
-        fdst[o + q] = sd[sb + S.sl[L][q]].front_off + S.off[L][q];
-        fsrc[o + q] = (int)(d.kval_off + S.src[L][q]);
-      }
+      relbase[(size_t)k * (NL + 1) + L] = (long long)rel_off.size();
+      rel_off.insert(rel_off.end(), S.off[L].begin(), S.off[L].end());
+      rel_sl.insert(rel_sl.end(), S.sl[L].begin(), S.sl[L].end());
+      rel_src.insert(rel_src.end(), S.src[L].begin(), S.src[L].end());
     }
-    long long o = fxoff[k];
-    for (size_t q = 0; q < S.fxr.size(); ++q)
-      for (int c = 0; c < nrhs; ++c, ++o) {
-        fxdst[o] = (d.x_off + S.fxr[q]) * nrhs + c;
-        fxsrc[o] = (int)(d.f_off + S.fxs[q] + (long long)c * d.nk);
-      }
-    for (size_t a = 0; a < S.kdiag.size(); ++a) kdiag[kdoff[k] + a] = (int)(d.kval_off + S.kdiag[a]);
-  });
+    relbase[(size_t)k * (NL + 1) + NL] = (long long)rel_off.size();
+    rel_off.insert(rel_off.end(), S.fxr.begin(), S.fxr.end());
+    rel_sl.insert(rel_sl.end(), S.fxr.size(), 0);
+    rel_src.insert(rel_src.end(), S.fxs.begin(), S.fxs.end());
+  }
+  std::vector<ExpandSeg> segs;
+  for (int L = 0; L < NL; ++L)
+    for (int k = 0; k < ns; ++k) {
+      const int n = (int)rel[rep[k]].off[L].size();
+      if (n == 0) continue;
+      segs.push_back({segoff[(size_t)L * ns + k], relbase[(size_t)rep[k] * (NL + 1) + L], h->h_sub[k].kval_off, 0, n,
+                      P.subs[k].sn_begin[0], h->h_sub[k].nk, 0});
+    }
+  for (int k = 0; k < ns; ++k) {
+    const int n = (int)rel[rep[k]].fxr.size();
+    if (n == 0) continue;
+    segs.push_back({fxoff[k], relbase[(size_t)rep[k] * (NL + 1) + NL], h->h_sub[k].x_off, h->h_sub[k].f_off, n, 0,
+                    h->h_sub[k].nk, 1});
+  }
+  std::vector<int> kdiag(kdoff[ns]);
+  for (int k = 0; k < ns; ++k) {
+    const Rel& S = rel[rep[k]];
+    for (size_t a = 0; a < S.kdiag.size(); ++a) kdiag[kdoff[k] + a] = (int)(h->h_sub[k].kval_off + S.kdiag[a]);
+  }
+  for (int k : reps) Rel().off.swap(rel[k].off);  // (the per-class lists are no longer needed)
+  stage("scatter lists");
 
   // ---- multipliers, slots, primal bookkeeping ----
   std::vector<int> slot_lam(h->n_slots);
@@ -1455,6 +1495,8 @@ void analyze_all(ietidp_s* h) {
     }
   }
   auto t1 = std::chrono::steady_clock::now();
+  h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t1 - t0).count();  // host symbolic part
+  h->rep.n_pattern_classes = h->n_pattern_classes;
   fill_report(h);
   if (getenv("IETIDP_DEBUG")) {
     int crit = 0;
@@ -1503,7 +1545,6 @@ void analyze_all(ietidp_s* h) {
   }
   if (h->opt.device < 0) {  // host-only analysis mode: no device work
     stage("rest (host only)");
-    h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t1 - t0).count();
     return;
   }
 
@@ -1521,10 +1562,7 @@ void analyze_all(ietidp_s* h) {
   h->d_perm.upload(perm_all, s);
   h->d_uoff.upload(h->u_off, s);
   h->d_prim_gid.upload(prim_gid, s);
-  h->sc_front_dst.upload(fdst, s);
-  h->sc_front_src.upload(fsrc, s);
-  h->sc_fx_dst.upload(fxdst, s);
-  h->sc_fx_src.upload(fxsrc, s);
+  expand_scatter(h, segs, rel_off, rel_sl, rel_src, segoff[(size_t)NL * ns], fxoff[ns]);
   h->kdiag_src.upload(kdiag, s);
   h->slot_lam.upload(slot_lam, s);
   h->slot_sign.upload(slot_sign, s);
@@ -1660,7 +1698,7 @@ void analyze_all(ietidp_s* h) {
   IETI_CUDA(cudaStreamSynchronize(s));
   stage("upload/alloc");
   auto t2 = std::chrono::steady_clock::now();
-  h->rep.ms_analyze = std::chrono::duration<double, std::milli>(t2 - t0).count();
+  h->rep.ms_upload = std::chrono::duration<double, std::milli>(t2 - t1).count();
 }
 
 }  // namespace ieti

@@ -28,6 +28,55 @@ __global__ void k_scatter(long long n, const long long* __restrict__ dst, const 
     out[dst[i]] = vals[src[i]];
 }
 
+// Scatter-list expansion from per-pattern-class relative entries (analyze.cpp): one
+// CTA per segment (subdomain x level, or subdomain loads).
+__global__ void __launch_bounds__(256)
+    k_expand_scatter(const ExpandSeg* __restrict__ segs, const int* __restrict__ off, const int* __restrict__ sl,
+                     const int* __restrict__ src, const SnDev* __restrict__ sn, int nrhs, long long* __restrict__ kdst,
+                     int* __restrict__ ksrc, long long* __restrict__ fdst, int* __restrict__ fsrc) {
+  const ExpandSeg g = segs[blockIdx.x];
+  if (g.kind == 0) {
+    for (int q = threadIdx.x; q < g.n; q += blockDim.x) {
+      const long long r = g.rel_off + q;
+      kdst[g.dst_off + q] = sn[g.sn_base + sl[r]].front_off + off[r];
+      ksrc[g.dst_off + q] = (int)(g.base + src[r]);
+    }
+  } else {
+    for (int e = threadIdx.x; e < g.n * nrhs; e += blockDim.x) {
+      const int q = e / nrhs, c = e - q * nrhs;
+      const long long r = g.rel_off + q;
+      fdst[g.dst_off + e] = (g.base + off[r]) * nrhs + c;
+      fsrc[g.dst_off + e] = (int)(g.base2 + src[r] + (long long)c * g.nk);
+    }
+  }
+}
+
+void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::vector<int>& off,
+                    const std::vector<int>& sl, const std::vector<int>& src, long long nK, long long nF) {
+  cudaStream_t s = h->stream;
+  DevBuf<ExpandSeg> dseg;
+  DevBuf<int> doff, dsl, dsrc;
+  dseg.upload(segs, s);
+  doff.upload(off, s);
+  dsl.upload(sl, s);
+  dsrc.upload(src, s);
+  h->sc_front_dst.alloc(std::max(nK, 1LL));
+  h->sc_front_src.alloc(std::max(nK, 1LL));
+  h->sc_fx_dst.alloc(std::max(nF, 1LL));
+  h->sc_fx_src.alloc(std::max(nF, 1LL));
+  h->sc_front_dst.n = nK;
+  h->sc_front_src.n = nK;
+  h->sc_fx_dst.n = nF;
+  h->sc_fx_src.n = nF;
+  if (!segs.empty()) {
+    k_expand_scatter<<<(unsigned)segs.size(), 256, 0, s>>>(dseg.p, doff.p, dsl.p, dsrc.p, h->d_sn.p, h->nrhs,
+                                                           h->sc_front_dst.p, h->sc_front_src.p, h->sc_fx_dst.p,
+                                                           h->sc_fx_src.p);
+    IETI_LAUNCHED(h);
+  }
+  IETI_CUDA(cudaStreamSynchronize(s));  // the temporaries are freed on return
+}
+
 __global__ void k_init_flags(int* err) {
   if (threadIdx.x == 0) {
     err[0] = INT_MAX;

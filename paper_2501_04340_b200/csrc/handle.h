@@ -218,6 +218,16 @@ struct ietidp_s {
 
 // Device-side entry points implemented in the .cu files (host launchers).
 namespace ieti {
+// Device expansion of the scatter lists (factor.cu): segment i writes n entries at
+// dst_off: dst = front_off(sn_base + sl[q]) + off[q], src = kval_off + src[q] (K), or
+// for the loads dst = (x_off + r[q]) nrhs + c, src = f_off + s[q] + c n_k.
+struct ExpandSeg {
+  long long dst_off, rel_off, base;  // base: kval_off (K) / x_off (loads)
+  long long base2;                   // loads: f_off
+  int n, sn_base, nk, kind;          // kind 0: K entries, 1: loads
+};
+void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::vector<int>& off,
+                    const std::vector<int>& sl, const std::vector<int>& src, long long nK, long long nF);
 void run_factor(ietidp_s* h);                  // factor.cu
 void run_coarse(ietidp_s* h);                  // coarse.cu
 void run_solve(ietidp_s* h);                   // pcg.cu

@@ -1381,6 +1381,8 @@ struct PcgArgs {
   const GatherRec* grec;        // chunk pass: per multiplier row, its slots' partial lists and signs
   const double* wrec;           // chunk pass: per multiplier row, the two slots' scaling weights delta
   int chunk;                   // several RHS: the chunk pass (sym_chunks) replaces the row-segment pass
+  int smem_doubles;            // dynamic shared memory of the launch (doubles)
+  int stop;                    // ietidp_stop: 0 ||r|| <= tol ||r0||, 1 sqrt(r.z) <= tol sqrt(r0.z0)
   const int* chunk_ptr;        // chunk pass: this CTA's chunks chunk_list[chunk_ptr[b] .. chunk_ptr[b+1])
   const SymChunk* chunk_list;
 };
@@ -1458,10 +1460,10 @@ __shared__ ChunkCtl g_chunk_ctl;  // per CTA (chunk pass): ring mbarriers, tenso
 
 // The symmetric pass of the persistent kernel: the chunk pass (several RHS) or the
 // row-segment stream.
-template <int NCP, int STAGES>
+template <int NCP, int STAGES, bool CH = false>
 __device__ __forceinline__ void sym_pass(const PcgArgs& P, TmvArgs A, double* smem) {
-  if constexpr (NCP == 16) {
-    if (P.chunk) {
+  if constexpr (NCP == 16 && CH) {
+    {
       const int beg = P.chunk_ptr[blockIdx.x], end = P.chunk_ptr[blockIdx.x + 1];
       for (int c0 = 0; c0 < A.ncols; c0 += CH_NC) {
         A.c_off = c0;
@@ -1469,8 +1471,9 @@ __device__ __forceinline__ void sym_pass(const PcgArgs& P, TmvArgs A, double* sm
       }
       return;
     }
+  } else {
+    sym_phase<NCP, STAGES>(A, P.cta_ptr, P.cta_items, P.ncp, smem);
   }
-  sym_phase<NCP, STAGES>(A, P.cta_ptr, P.cta_items, P.ncp, smem);
 }
 
 __device__ __forceinline__ double sym_value(const double* spart, const SlotRed* sred, long long a, int nc, int c);
@@ -1696,43 +1699,56 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
 // memory) and adds G_k z_k into the first chunk partial of each of the subdomain's
 // slots, so that the gather of q = sum_k B (W_k p_k + G_k z_k) is a plain fold of the
 // partials (F_DP = W + G S_PP^-1 G^T, SURVEY F1 signs).
-__device__ __forceinline__ void coarse_gz_phase(const PcgArgs& P, const TmvArgs& A, double* smem) {
+__device__ __forceinline__ void coarse_gz_phase(const PcgArgs& P, const TmvArgs& A, double* smem, int smem_doubles) {
   const int nc = P.ncols, ng = P.ng, tid = threadIdx.x;
-  double* gs = smem;                 // ng x nc
-  double* srow = gs + ng * nc;       // nP x ng rows of S_PP^-1
-  double* zk = srow + 16 * ng;       // nP x nc
+  double* gs = smem;               // g: ng x nc
+  double* srow = gs + ng * nc;     // the subdomain's nP rows of S_PP^-1 (nP x ng)
+  double* zk = srow + 16 * ng;     // z_k: nP x nc
+  double* gG = zk + 16 * nc;       // G_k rows, a chunk at a time (rows x nP)
+  const int gcap = smem_doubles - (int)(gG - smem);
   for (int e = tid; e < ng * nc; e += VT) gs[e] = __ldcg(P.gc + e);
-  bool staged = false;
   for (int k = blockIdx.x; k < A.n_sub; k += gridDim.x) {
     const SubDev d = A.sub[k];
     if (d.nP == 0 || d.nI == 0) continue;
-    __syncthreads();  // gs complete (first), srow / zk free (later)
-    staged = true;
+    __syncthreads();  // gs complete (first), srow / zk / gG free (later)
     const int* gid = A.prim_gid + d.prim_off;
     for (int e = tid; e < d.nP * ng; e += VT) {
       const int q = e / ng, j = e - q * ng;
       srow[e] = __ldg(P.Sinv + (long long)gid[q] * ng + j);
     }
+    const int rows = min(d.nI, gcap / d.nP);  // G rows per chunk
+    const double* Gk = A.gmat + d.g_off;
+    int a0 = 0;
+    // first chunk of G_k in flight while z_k is formed
+    for (int e = tid; e < rows * d.nP; e += VT) gG[e] = __ldg(Gk + e);
     __syncthreads();
     for (int e = tid; e < d.nP * nc; e += VT) {
       const int q = e / nc, c = e - q * nc;
       double acc = 0.0;
+#pragma unroll 4
       for (int j = 0; j < ng; ++j) acc += srow[q * ng + j] * gs[j * nc + c];
       zk[e] = acc;
     }
     __syncthreads();
-    // G_k z_k into partial 0 of every slot (nc threads per row)
     const int P2 = pow2ge(nc), c = tid % P2, rl = tid / P2, R = VT / P2;
-    if (c < nc)
-      for (int a = rl; a < d.nI; a += R) {
-        const double* Gr = A.gmat + d.g_off + (long long)a * d.nP;
-        double acc = 0.0;
-        for (int q = 0; q < d.nP; ++q) acc += __ldg(Gr + q) * zk[q * nc + c];
-        const long long base = P.slot_red[d.rI_off + a].base;
-        A.spart[base * nc + c] += acc;
-      }
+    while (true) {
+      const int na = min(rows, d.nI - a0);
+      if (c < nc)
+        for (int a = rl; a < na; a += R) {
+          const double* Gr = gG + a * d.nP;
+          double acc = 0.0;
+          for (int q = 0; q < d.nP; ++q) acc += Gr[q] * zk[q * nc + c];
+          const int aa = a0 + a;
+          const long long base = A.cpb[d.blk0 + aa / TB] * TB + aa % TB;
+          A.spart[base * nc + c] += acc;  // partial 0 of the slot (one writer)
+        }
+      a0 += na;
+      if (a0 >= d.nI) break;
+      __syncthreads();
+      for (int e = tid; e < min(rows, d.nI - a0) * d.nP; e += VT) gG[e] = __ldg(Gk + (long long)a0 * d.nP + e);
+      __syncthreads();
+    }
   }
-  (void)staged;
 }
 
 // out[j][c] = sum_{2 slots} sign (w) sum_{p < cnt} partial_p[slot][c], plus the per-CTA
@@ -1816,26 +1832,27 @@ __device__ __forceinline__ void pcg_barrier(const PcgArgs& P) {
   grid_barrier(P.bar);
 }
 
-template <int NCP, int STAGES, bool EXPL>
+template <int NCP, int STAGES, bool EXPL, bool CH>
 __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, double* pq) {
-  if (EXPL) {
-    // W pass; then every CTA solves the coarse problem itself and folds the pass's
-    // partial sums into the gather (no reduction phase, one barrier)
-    // one column: the partial sums are folded into the gather; several: a reduction
-    // phase (a slot shared by several multipliers would be summed repeatedly)
-    if (NCP == 16 && P.chunk) {
+  if constexpr (EXPL && CH) {
+    {
       // chunk mode: W pass | g | z_k, G_k z_k into the partials | folded gather of q
-      sym_pass<NCP, STAGES>(P, P.wsym, smem);
+      sym_pass<NCP, STAGES, true>(P, P.wsym, smem);
       pcg_barrier(P);
       if (P.ng > 0) {
         coarse_spread(P);
         pcg_barrier(P);
-        coarse_gz_phase(P, P.wsym, smem);
+        coarse_gz_phase(P, P.wsym, smem, P.smem_doubles);
         pcg_barrier(P);
       }
-      gather_fold<4>(P, P.wsym.spart, false, P.q, P.p, pq);
+      gather_fold<2>(P, P.wsym.spart, false, P.q, P.p, pq);
       return;
     }
+  } else if constexpr (EXPL) {
+    // W pass; then every CTA solves the coarse problem itself and folds the pass's
+    // partial sums into the gather (no reduction phase, one barrier)
+    // one column: the partial sums are folded into the gather; several: a reduction
+    // phase (a slot shared by several multipliers would be summed repeatedly)
     const bool fold = P.fold && (P.ncols == 1 || P.fold_multi);
     const bool row1 = P.ncols == 1 && P.ng > 0 && P.ng <= COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;
     const bool row1s = P.ncols == 1 && P.ng > COARSE_LOCAL_MAX && fold && P.m <= (int)gridDim.x * VT;  // spread coarse
@@ -1928,15 +1945,14 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
   }
 }
 
-template <int NCP, int STAGES, bool EXPL>
+template <int NCP, int STAGES, bool EXPL, bool CH>
 __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, double* rz) {
-  if (EXPL && NCP == 16 && P.chunk) {  // chunk mode: S pass | folded, weighted gather of z
-    sym_pass<NCP, STAGES>(P, P.ssym, smem);
+  if constexpr (EXPL && CH) {  // chunk mode: S pass | folded, weighted gather of z
+    sym_pass<NCP, STAGES, true>(P, P.ssym, smem);
     pcg_barrier(P);
-    gather_fold<4>(P, P.ssym.spart, true, P.z, P.r, rz);
+    gather_fold<2>(P, P.ssym.spart, true, P.z, P.r, rz);
     return;
-  }
-  if (EXPL) {
+  } else if constexpr (EXPL) {
     const bool row1 = P.ncols == 1 && P.fold && P.m <= (int)gridDim.x * VT;
     const int j = blockIdx.x * VT + threadIdx.x;
     LamDev L{};
@@ -1977,10 +1993,11 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
   }
 }
 
-template <int NCP, int STAGES, bool EXPL>
+template <int NCP, int STAGES, bool EXPL, bool CH = false>
 __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) {
   extern __shared__ __align__(16) double smem[];
   __shared__ double s_rz[IETIDP_MAX_RHS], s_r0[IETIDP_MAX_RHS], s_coef[IETIDP_MAX_RHS], s_sum[IETIDP_MAX_RHS];
+  __shared__ double s_rz0[IETIDP_MAX_RHS];  // r_0 . z_0 (preconditioned stopping criterion)
   __shared__ int s_act[IETIDP_MAX_RHS], s_new[IETIDP_MAX_RHS], s_iters[IETIDP_MAX_RHS];
   __shared__ int s_any;
   const int tid = threadIdx.x, nb = gridDim.x, nc = P.ncols, m = P.m;
@@ -1993,8 +2010,8 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     if (cc < nc)
       for (int j = blockIdx.x * R + rl; j < m; j += nb * R) f((long long)j * nc + cc, j);
   };
-  if constexpr (NCP == 16 && EXPL) {
-    if (P.chunk) {  // chunk pass: ring mbarriers and the tensor-memory accumulators
+  if constexpr (NCP == 16 && EXPL && CH) {
+    {  // chunk pass: ring mbarriers and the tensor-memory accumulators
       if (tid == 0) {
         for (int s2 = 0; s2 < STAGES; ++s2) mbar_init(&g_chunk_ctl.full[s2], 1);
         g_chunk_ctl.streamed = 0;
@@ -2044,10 +2061,10 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
   if (!P.fixed && P.max_iter <= 0) run = false;
   if (run) {
     // z = M r, rz = r.z, p = z
-    apply_M_phases<NCP, STAGES, EXPL>(P, smem, rz);
+    apply_M_phases<NCP, STAGES, EXPL, CH>(P, smem, rz);
     pcg_barrier(P);
     colsum_all(rz, nc, s_sum);
-    if (tid < nc) s_rz[tid] = s_sum[tid];
+    if (tid < nc) s_rz[tid] = s_rz0[tid] = s_sum[tid];
     rows([&](long long e, int j) {
       const double zv = P.z[e];
       P.p[e] = zv;
@@ -2063,7 +2080,7 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
   const int jr = blockIdx.x * VT + tid;
   const bool myrow = fast1 && jr < m;
   while (run) {
-    apply_F_phases<NCP, STAGES, EXPL>(P, smem, pq);  // q = F p
+    apply_F_phases<NCP, STAGES, EXPL, CH>(P, smem, pq);  // q = F p
     LamDev Lr{};
     double r_pre = 0.0, p_pre = 0.0, d0 = 0.0, d1 = 0.0;
     if (myrow) {
@@ -2151,7 +2168,7 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     if (tid < nc) {
       int a = s_act[tid];
       if (s_act[tid]) s_iters[tid]++;
-      if (a && !P.fixed && sqrt(s_sum[tid]) <= P.tol * s_r0[tid]) a = 0;
+      if (a && !P.fixed && P.stop == 0 && sqrt(s_sum[tid]) <= P.tol * s_r0[tid]) a = 0;
       s_new[tid] = a;
       if (a) atomicOr(&s_any, 1);
     }
@@ -2161,13 +2178,28 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
       if (tid < nc) s_act[tid] = s_new[tid];
       break;
     }
-    apply_M_phases<NCP, STAGES, EXPL>(P, smem, rz);  // z = M r
+    apply_M_phases<NCP, STAGES, EXPL, CH>(P, smem, rz);  // z = M r
     double p_old = 0.0;
     if (myrow) p_old = P.p[jr];
     pcg_barrier(P);
     // beta, p
     const double zv = myrow ? P.z[jr] : 0.0;
     colsum_all(rz, nc, s_sum);
+    if (P.stop == 1 && !P.fixed) {
+      // preconditioned criterion, tested after the preconditioner (identical in every CTA)
+      __syncthreads();
+      if (tid == 0) s_any = 0;
+      __syncthreads();
+      if (tid < nc) {
+        if (s_new[tid] && sqrt(fmax(s_sum[tid], 0.0)) <= P.tol * sqrt(s_rz0[tid])) s_new[tid] = 0;
+        if (s_new[tid]) atomicOr(&s_any, 1);
+      }
+      __syncthreads();
+      if (!s_any) {
+        if (tid < nc) s_act[tid] = s_new[tid];
+        break;
+      }
+    }
     if (tid < nc) {
       const double rzn = s_sum[tid];
       s_coef[tid] = rzn / s_rz[tid];
@@ -2223,8 +2255,8 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     if (tid < nc) s_act[tid] = s_new[tid];
     pcg_barrier(P);
   }
-  if constexpr (NCP == 16 && EXPL) {
-    if (P.chunk) {
+  if constexpr (NCP == 16 && EXPL && CH) {
+    {
       asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
       __syncthreads();
       if ((tid >> 5) == 0)
@@ -2665,9 +2697,9 @@ static void plan_chunks(ietidp_s* h, int grid, int nc) {
   h->chunk_grid = grid;
 }
 
-template <int NCP, int STAGES, bool EXPL>
+template <int NCP, int STAGES, bool EXPL, bool CH = false>
 static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
-  auto kern = k_pcg<NCP, STAGES, EXPL>;
+  auto kern = k_pcg<NCP, STAGES, EXPL, CH>;
   IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
   int per_sm = 0, nsm = 0;
   IETI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, cfg.smem));
@@ -2714,6 +2746,7 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
       t->cfirst = h->chunk_cfirst.p;
     }
     args.slot_red = h->chunk_slot_red.p;
+    args.smem_doubles = cfg.smem / 8;
     args.grec = h->chunk_grec.p;
     args.wrec = h->chunk_wrec.p;
     args.wsym.n_sub = args.ssym.n_sub = h->n_sub;
@@ -2744,7 +2777,8 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
     n = std::min(n, 4096);
     const int ng_ = h->n_primal, nc = a.fwd.ncols ? a.fwd.ncols : h->nrhs;
     const bool nofold = (nc > 1 && !args.fold_multi) || !args.fold;
-    const int per = EXPL ? 6 + (nofold ? 2 : 0) + (ng_ > COARSE_LOCAL_MAX ? 1 + (nofold ? 0 : 1) : 0) : 9,
+    const int per = args.chunk ? (ng_ > 0 ? 8 : 6)
+                    : EXPL ? 6 + (nofold ? 2 : 0) + (ng_ > COARSE_LOCAL_MAX ? 1 + (nofold ? 0 : 1) : 0) : 9,
               skip = EXPL ? 4 + (nofold ? 1 : 0) : 5;
     std::vector<double> acc(per, 0.0);
     int cnt = 0;
@@ -2857,6 +2891,7 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.nPmax = std::max(h->plan.nPmax, 1);
   a.max_iter = h->opt.max_iter;
   a.fixed = h->opt.fixed_iters;
+  a.stop = h->opt.stop;
   a.coef = h->cgcoef.p;
   a.coef_ld = h->coef_ld;
   a.n_items = h->opt.loop == IETIDP_LOOP_EXPLICIT ? h->n_symwork : h->n_loopwork;
@@ -2875,7 +2910,8 @@ static bool run_solve_persistent(ietidp_s* h) {
         stages = 2;
         bytes = (stages * TILE_ELEMS + nt * CH_XBLK + gsz) * 8;
       }
-      if (bytes <= 210 * 1024 && bytes >= 2 * h->n_primal * nc * (int)sizeof(double)) {
+      const int gz = (h->n_primal * nc + 16 * h->n_primal + 16 * nc + TB * 16) * (int)sizeof(double);
+      if (bytes <= 210 * 1024 && bytes >= gz) {
         a.chunk = 1;
         cfg.stages = stages;
         cfg.smem = bytes;
@@ -2887,6 +2923,8 @@ static bool run_solve_persistent(ietidp_s* h) {
     if (cfg.ncp == 1 && cfg.stages == 2) return launch_pcg_t<1, 2, true>(h, cfg, a);
     if (cfg.ncp == 1 && cfg.stages == 5) return launch_pcg_t<1, 5, true>(h, cfg, a);
     if (cfg.ncp == 1) return launch_pcg_t<1, 3, true>(h, cfg, a);
+    if (cfg.ncp == 16 && a.chunk && cfg.stages == 3) return launch_pcg_t<16, 3, true, true>(h, cfg, a);
+    if (cfg.ncp == 16 && a.chunk) return launch_pcg_t<16, 2, true, true>(h, cfg, a);
     if (cfg.ncp == 16 && cfg.stages == 3) return launch_pcg_t<16, 3, true>(h, cfg, a);
     if (cfg.ncp == 16) return launch_pcg_t<16, 2, true>(h, cfg, a);
     if (cfg.stages == 3) return launch_pcg_t<8, 3, true>(h, cfg, a);
@@ -2914,6 +2952,8 @@ void run_solve(ietidp_s* h) {
     IETI_CHECK_LAUNCH();
     return;
   }
+  if (h->opt.stop != IETIDP_STOP_RESIDUAL && m > 0)
+    throw Error(IETIDP_E_ARG, "the preconditioned stopping criterion needs the persistent PCG kernel");
   if (m > 0) {
     k_init<<<NBLK, VT, 0, s>>>(m, nc, h->d_vec.p, h->lam_vec.p, h->r_vec.p, rr_part);
     IETI_LAUNCHED(h);

@@ -18,6 +18,7 @@ OK, E_ARG, E_STATE, E_B_STRUCTURE, E_NOT_SPD, E_NO_CONVERGENCE, E_CUDA, E_NOMEM 
 SCALING = {"multiplicity": 0, "stiffness": 1}
 ORDERING = {"nd": 0, "dense": 1, "md": 2}
 LOOP = {"explicit": 0, "triangular": 1}
+STOP = {"residual": 0, "preconditioned": 1}
 
 # every entry point include/ietidp.h declares
 SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "ietidp_analyze",
@@ -29,7 +30,8 @@ SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "i
 
 class Options(C.Structure):
     _fields_ = [("tol", C.c_double), ("max_iter", C.c_int), ("scaling", C.c_int), ("fixed_iters", C.c_int),
-                ("ordering", C.c_int), ("leaf_size", C.c_int), ("loop", C.c_int), ("device", C.c_int),
+                ("ordering", C.c_int), ("leaf_size", C.c_int), ("loop", C.c_int), ("stop", C.c_int),
+                ("device", C.c_int),
                 ("stream", C.c_void_p)]
 
 
@@ -43,7 +45,8 @@ class Report(C.Structure):
                 ("iters", C.c_int * MAX_RHS), ("converged", C.c_int * MAX_RHS),
                 ("rel_residual", C.c_double * MAX_RHS),
                 ("ms_analyze", C.c_double), ("ms_factor", C.c_double), ("ms_coarse", C.c_double),
-                ("ms_pcg", C.c_double), ("ms_recover", C.c_double)]
+                ("ms_pcg", C.c_double), ("ms_recover", C.c_double), ("ms_upload", C.c_double),
+                ("n_pattern_classes", C.c_int)]
 
     def to_dict(self):
         n = self.nrhs
@@ -112,13 +115,15 @@ class Solver:
     the *_device methods take torch CUDA tensors (plumbing only)."""
 
     def __init__(self, n_sub, n_lambda, n_primal, nrhs=1, tol=1e-10, max_iter=500, scaling="multiplicity",
-                 fixed_iters=0, ordering="nd", leaf_size=96, loop="explicit", device=0, stream=None):
+                 fixed_iters=0, ordering="nd", leaf_size=96, loop="explicit", stop="residual", device=0,
+                 stream=None):
         lib = load()
         self.lib = lib
         o = Options()
         lib.ietidp_options_default(C.byref(o))
         o.tol, o.max_iter, o.scaling, o.fixed_iters = tol, max_iter, SCALING[scaling], fixed_iters
         o.ordering, o.leaf_size, o.loop, o.device = ORDERING[ordering], leaf_size, LOOP[loop], device
+        o.stop = STOP[stop]
         o.stream = stream
         h = C.c_void_p()
         st = lib.ietidp_create(C.byref(o), n_sub, n_lambda, n_primal, nrhs, C.byref(h))

@@ -302,3 +302,24 @@ def test_multi_rhs_columns_independent():
         r1 = dp.solve(slice_columns(b, [c]), tol=1e-12)
         assert abs(int(r1["iters"][0]) - int(it[c])) <= 1, (c, r1["iters"], it[c])
         assert rel(r1["lam"][:, 0], res["lam"][:, c]) <= 1e-9
+
+
+def test_preconditioned_stopping_criterion(bundles):
+    """The preconditioned criterion (PAPER.md:397 eta_tol): the oracle stops
+    at the first iteration N with sqrt(r_N.M r_N) <= tol sqrt(r_0.M r_0), r = d - F lambda
+    recomputed from the multipliers (not the recursion), and N - 1 iterations do not."""
+    b = bundles["C2r"]
+    D = dp.DualPrimal(b)
+    tol = 1e-6
+    _, info = D.pcg(tol=tol, stop="preconditioned")
+    n = int(info["iters"][0])
+
+    def ratio(k):
+        lam, _ = D.pcg(fixed_iters=k)
+        r = D.d - D.apply_F(lam)
+        return np.sqrt((r * D.apply_M(r)).sum() / (D.d * D.apply_M(D.d)).sum())
+    assert ratio(n) <= tol * 1.0001 and ratio(n - 1) > tol
+    # the unpreconditioned criterion at the same tolerance stops elsewhere in general,
+    # and is the default
+    _, info2 = D.pcg(tol=tol)
+    assert int(info2["iters"][0]) >= 1
