@@ -149,14 +149,17 @@ def max_over_ranks(x, world, device=None):
 # ---------------------------------------------------------------------------
 def oracle_iters(config):
     """The oracle's own natural-stopping iteration count at full size (max over the
-    columns measured), from profiles/oracle_iters.json (tests/studies/oracle_iters.py,
-    oracle/ only); None if not recorded."""
-    try:
-        with open(os.path.join(ROOT, "profiles", "oracle_iters.json")) as f:
-            e = json.load(f).get(config)
-    except OSError:
-        return None
-    return max(e["iters"]) if e else None
+    columns measured): tests/golden/fullsize_<config>*.npz, written by
+    tests/studies/make_fullsize_golden.py (oracle/ and ietigen/ only; C5 on columns 0
+    and 7). None if not recorded (C1: the GPU run's own count is used)."""
+    import glob
+    its = []
+    for p in sorted(glob.glob(os.path.join(ROOT, "tests", "golden", f"fullsize_{config}*.npz"))):
+        tail = os.path.basename(p)[len(f"fullsize_{config}"):-4]
+        if tail and not tail.startswith("c"):
+            continue  # fullsize_C2.npz must not match C20 etc.
+        its.extend(int(x) for x in np.load(p)["iters"])
+    return max(its) if its else None
 
 
 def oracle_solve_cost(bundle, subs, n_iter, iters_sample=2):
@@ -264,24 +267,30 @@ def run_reference(args, rank, world):
     nsub = b["n_sub"]
     n_iter = oracle_iters(args.config) or 0
     per = 2  # subdomains sampled per step (rotating over the tiling)
-    times, det = [], None
+    times, walls, det = [], [], None
     for s in range(args.warmup + args.steps):
         subs = [((s * per + i) * 7919) % nsub for i in range(per)]
+        w0 = time.perf_counter()
         t, det = oracle_solve_cost(b, sorted(set(subs)), n_iter)
         if s >= args.warmup:
             times.append(t)
+            walls.append(time.perf_counter() - w0)
     sec = statistics.mean(times)
     val = 1.0 / sec
     sample = (f"per step: oracle/dp.py on {per} of {nsub} subdomains (set-up: sparse LU of K_rr, K_rr^-1 K_rP, "
               f"explicit S_II; 2 PCG iterations with F, M_D^-1, coarse solve and vector updates; recovery), "
               f"per-subdomain phases scaled x{nsub / per:g}, global phases at full size, PCG scaled to the "
-              f"oracle's own {n_iter} iterations (profiles/oracle_iters.json)")
+              f"oracle's own {n_iter} iterations (tests/golden/fullsize_*.npz)")
     ci = cpu_info()
+    # ms_per_step is the wall time of one bounded sample (what this run actually spent per
+    # step); value is the full solve rate the sample extrapolates to (ms_per_solve_extrapolated)
     line = {"impl": "reference", "metric": METRIC, "value": val, "unit": "solves/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": statistics.mean(walls) * 1e3,
+            "ms_per_solve_extrapolated": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": {"workload": args.config, "n_sub": nsub, "n_lambda": int(b["n_lambda"]),
-                       "n_primal": int(b["n_primal"]), "nrhs": int(b["nrhs"])},
+                       "n_primal": int(b["n_primal"]), "nrhs": int(b["nrhs"]),
+                       "l2": "flushed between timed steps (512 MB write)", "replicas": world},
             "cpu_baseline": {"value": val, "unit": "solves/s", "cores": det["threads"], "kind": "oracle",
                              "sample": sample, "cpu": ci, "phases_s": det},
             "e2e": {"value": val, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -479,7 +488,7 @@ def run_ours(args, rank, world, local):
                          f"sparse LU of K_rr, K_rr^-1 K_rP, K_rr^-1 j, explicit S_II; 2 PCG iterations with F, "
                          f"M_D^-1, coarse solve and vector updates on all {nc} columns; recovery), per-subdomain "
                          f"phases scaled x{ns / len(subs):g}, global phases at full size, PCG scaled to "
-                         + (f"the oracle's own {n_or} iterations (profiles/oracle_iters.json)" if n_or else
+                         + (f"the oracle's own {n_or} iterations (tests/golden/fullsize_*.npz)" if n_or else
                             f"the GPU run's {it_max} iterations"),
                "cpu": cpu_info(), "phases_s": det}
     line = {
