@@ -124,6 +124,7 @@ struct ietidp_s {
   bool fwd_in_factor = false;    // the forward sweep of the loads ran on the side stream
   long long launches = 0;
   ieti::DevBuf<unsigned long long> pcg_prof;  // IETIDP_PCG_PROF barrier timestamps
+  ieti::DevBuf<unsigned long long> dbg_tl;    // IETIDP_DBG_TL chunk-pass timeline (diagnostics)
   LaunchTrace trace;
   ietidp_report rep{};
 

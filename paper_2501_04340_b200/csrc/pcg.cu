@@ -99,6 +99,8 @@ struct TmvArgs {
   const PcgState* st;
   const double* rr_part;   // PRE1 inside the loop: convergence test
   int check;
+  unsigned long long* tl;  // diagnostics (IETIDP_DBG_TL): CTA 0's timeline of one pass
+  int dbg;                 // experiments only (IETIDP_DBG_PASS): bits: 1 every tile read is tile 0, 2 no DMMA, 4 no TMEM in T, 8 no x staging, 16 no write-out
 };
 
 // Asynchronous gather of rows [lo, hi) of a slot-ordered vector (row-major,
@@ -730,19 +732,26 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
 // CTA's chunks are contiguous tile ranges of one subdomain in lower row-major order,
 // so the CTA's tile stream is ONE contiguous range of the tile array: a thread issues
 // one 32 KB cp.async.bulk per tile into a STAGES-deep ring (mbarrier completion, L2
-// evict_first). For tile (o, j) every warp computes, with DMMA m8n8k4,
-//   N: S_oj x_j  -> rows o, accumulated in registers over the row,
-//   T: S_oj^T x_o -> rows j (j < o), accumulated in TENSOR MEMORY: block j's
-//      accumulator fragment (4 doubles per thread) is loaded (tcgen05.ld), extended
-//      by the DMMA chain and stored back (tcgen05.st), so the chunk's transposed
-//      products never leave the SM.
-// At the diagonal tile the row's N result joins block o's accumulator. At the end
-// of the chunk every block j <= o_b is written once as the chunk's partial block
-// (then zeroed); the gathers sum the (typically 1-3) partial blocks of a slot in
-// chunk order (deterministic). The chunk's input blocks x_0..x_ob are staged in shared
-// memory (16 columns, 4-double groups XOR-swizzled by (r & 3): conflict-free DMMA B
-// fragments, ch_xpos). Tensor memory: lanes = the warp's quadrant (32 (w & 3) + lane), columns
-// 256 (w >> 2) + 8 j + [0, 8) hold block j's fragment: up to 32 blocks (n_I <= 2048).
+// evict_first). For tile (o, j), with DMMA m8n8k4 on 16 x 16 warp fragments (four
+// independent accumulation chains per warp: the DMMA latency is covered):
+//   N (warps 0-3): S_oj x_j  -> rows o, warp q = rows 16q .. 16q+15, accumulated in
+//      registers over the row;
+//   T (warps 4-7): S_oj^T x_o -> rows j (j < o), warp 4+q = rows 16q .. 16q+15,
+//      accumulated in TENSOR MEMORY: block j's fragment (8 doubles per thread) is
+//      loaded (tcgen05.ld), extended by the DMMA chain and stored back (tcgen05.st),
+//      so the chunk's transposed products never leave the SM.
+// At the diagonal tile the N warps finish the row's chain (it becomes block o's
+// accumulator) while the T warps form the coarse partial G_k[rows o]^T x_o of the F-apply.
+// The warps are not synchronised per tile: each releases a ring slot when it is done with
+// it (the last of the eight issues the slot's next copy), and T warp q waits for N warp q
+// only at a diagonal (a release/acquire counter), before it touches the block just stored.
+// At the end of the chunk every block j <= o_b is written once as the chunk's partial
+// block (then zeroed); the gathers sum the (typically 1-3) partial blocks of a slot in
+// chunk order (deterministic).
+// The chunk's input blocks x_0..x_ob are staged in shared memory (16 columns, 4-double
+// groups XOR-swizzled by (r & 3): conflict-free DMMA B fragments, ch_xpos). Tensor
+// memory: lanes = the warp's quadrant (32 (w & 3) + lane), columns 16 j + 8 h + [0, 8)
+// hold half h (RHS columns 8h .. 8h+7) of block j: up to 32 blocks (n_I <= 2048).
 // ---------------------------------------------------------------------------
 constexpr int CH_NC = 16;                 // columns per chunk pass
 constexpr int CH_XBLK = TB * CH_NC;       // doubles per staged input block
@@ -750,6 +759,11 @@ constexpr int CH_TMEM_COLS = 512;
 
 __device__ __forceinline__ int ch_xpos(int r, int c) { return r * CH_NC + (c ^ ((r & 3) << 2)); }
 
+__device__ __forceinline__ void cp_async_z16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"((unsigned)__cvta_generic_to_shared(smem)), "l"(gmem),
+               "r"(src_bytes)
+               : "memory");
+}
 __device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count));
 }
@@ -814,8 +828,12 @@ __device__ __forceinline__ void tm_st8(unsigned taddr, const double (&v)[2][2]) 
 // memory base and the running count of tiles streamed (ring slot and phase parity).
 struct ChunkCtl {
   uint64_t full[4];
+  unsigned rel[4];   // per ring slot: warps done with it, counted over all its uses
+  unsigned diag[4];  // per quadrant: diagonal tiles whose row accumulator N warp q has stored
+  long long pb[32];  // the chunk's partial block of each block row (write-out)
   unsigned tmem;
   unsigned streamed;
+  unsigned ncall, ntl;  // diagnostics: pass calls, timeline entries
 };
 
 // Tile (o, j) of chunk tiles: row o of lower row-major index t.
@@ -829,6 +847,17 @@ __device__ __forceinline__ int tri_row(int t) {
 
 __device__ __forceinline__ int o0_of(int t) { return tri_row(t); }
 
+__device__ __forceinline__ void tl_mark(const TmvArgs& A, ChunkCtl* ctl, bool rec, int ev, int a, int b) {
+  if (rec) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    const unsigned k = ctl->ntl++;
+    if (k < 2048) {
+      A.tl[2 * k] = t;
+      A.tl[2 * k + 1] = ((unsigned long long)ev << 32) | ((unsigned)a << 16) | (unsigned)b;
+    }
+  }
+}
 template <int STAGES>
 __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch, int nch, double* smem, ChunkCtl* ctl) {
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t4 = lane & 3;
@@ -837,16 +866,32 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
   double* xb = smem + STAGES * TILE_ELEMS;
   double* gs = xb + A.nt_max * CH_XBLK;  // G_k rows of the current block row (TB x nP), F-apply
   if (nch == 0) return;
+  // diagnostics: CTA 0, thread 0 (N warp 0) records its timeline of pass call 100 and 101
+  const bool rec = A.tl && blockIdx.x == 0 && tid == 0 && (ctl->ncall == 100 || ctl->ncall == 101);
+  tl_mark(A, ctl, rec, 0, ctl->ncall, nch);
   const long long g0 = ch[0].gtile;
   const int ntiles = (int)(ch[nch - 1].gtile + (ch[nch - 1].t1 - ch[nch - 1].t0) - g0);
   const unsigned base = ctl->streamed;
-  const unsigned tbase = ctl->tmem + ((unsigned)(32 * (warp & 3)) << 16) + 256u * (warp >> 2);
-  unsigned long long pol = 0;
-  if (tid == 0) asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  // tensor memory: lanes = the warp's quadrant q = w & 3 (rows 16q .. 16q+15 of a block),
+  // block j at columns 16 j .. 16 j + 15 (columns 0-7 of the RHS, then 8-15; 4 doubles each)
+  const int q4 = warp & 3, r0 = 16 * q4 + g;
+  const bool tw = warp >= 4;
+  const unsigned tq = ctl->tmem + ((unsigned)(32 * q4) << 16);
+  // fragment offsets (doubles) with the swizzles resolved once: for k-step k0 (a multiple
+  // of 4), A = S rows r0 (+8): swz(r0, k0 + t4) = r0 TB + (k0 & ~15) + acol[(k0 >> 2) & 3];
+  // A = S^T: swz(k0 + t4, r0 (+8)) = at0 (at1) + k0 TB; B = x: ch_xpos(k0 + t4, g (+8)) =
+  // xb0 (xb1) + k0 CH_NC
+  int acol[4];
+#pragma unroll
+  for (int kl = 0; kl < 4; ++kl) acol[kl] = 4 * (kl ^ (g & 3)) + t4;
+  const int at0 = t4 * TB + (r0 ^ (t4 << 2)), at1 = t4 * TB + ((r0 + 8) ^ (t4 << 2));
+  const int xb0 = t4 * CH_NC + (g ^ (t4 << 2)), xb1 = t4 * CH_NC + ((g ^ (t4 << 2)) ^ 8);
+  unsigned long long pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
   auto issue = [&](int i) {
     const unsigned s = (base + i) % STAGES;
     mbar_expect_tx(&ctl->full[s], TILE_ELEMS * 8);
-    bulk_g2s(ring + s * TILE_ELEMS, A.tiles + (g0 + i) * TILE_ELEMS, TILE_ELEMS * 8, &ctl->full[s], pol);
+    bulk_g2s(ring + s * TILE_ELEMS, A.tiles + ((A.dbg & 1) ? (g0 + (i & 1)) * TILE_ELEMS : (g0 + i) * TILE_ELEMS), TILE_ELEMS * 8, &ctl->full[s], pol);
   };
   if (tid == 0)
     for (int i = 0; i < min(STAGES, ntiles); ++i) issue(i);
@@ -856,18 +901,19 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
     const SubDev d = A.sub[C.sub];
     const int ob = tri_row(C.t1 - 1);
     const bool coarse = A.gpart && d.nP > 0;
-    auto stage_g = [&](int row) {  // G_k rows of block row `row`, consumed at its diagonal tile
+    auto stage_g = [&](int row, int t0, int nt) {  // G_k rows of block row `row` (threads t0 of nt)
       const int na = min(TB, d.nI - row * TB);
       const double* Gb = A.gmat + d.g_off + (long long)row * TB * d.nP;
-      for (int e = tid; e < na * d.nP; e += 256) gs[e] = __ldg(Gb + e);
+      for (int e = t0; e < na * d.nP; e += nt) gs[e] = __ldg(Gb + e);
     };
-    if (coarse) stage_g(o0_of(C.t0));
+    if (coarse) stage_g(o0_of(C.t0), tid, 256);
+    if (tid <= ob) ctl->pb[tid] = A.cpb[d.blk0 + tid] + (C.rank - A.cfirst[d.blk0 + tid]);  // partial blocks
     // stage x_0 .. x_ob (16-byte pairs; rows beyond n_I and columns beyond ncl are zero)
     {
       const double* src = A.vin + d.rI_off * A.ncols + A.c_off;
       const int nrow = (ob + 1) * TB;
       const bool vec2 = ((A.ncols | A.c_off) & 1) == 0;
-      for (int e = tid; e < nrow * (CH_NC / 2); e += 256) {
+      for (int e = tid; e < ((A.dbg & 8) ? 0 : nrow * (CH_NC / 2)); e += 256) {
         const int r = e >> 3, cp = (e & 7) * 2;
         double* dst = xb + (r >> 6) * CH_XBLK + ch_xpos(r & (TB - 1), cp);
         if (r < d.nI && cp + 1 < ncl && vec2) {
@@ -881,107 +927,198 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
       cp_async_wait<0>();
       __syncthreads();
     }
-    double acc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    tl_mark(A, ctl, rec, 1, c, ob);
+    // N warps (0-3): rows 16q .. 16q+15 of the row's product (all 16 columns, registers,
+    // acc[nb][mb], x_j, then x_o at the diagonal tile); T warps (4-7): rows 16q .. 16q+15 of
+    // block j's transposed product (tensor memory), and at the diagonal tile the coarse
+    // partial. Four independent DMMA chains per warp. The warps are not synchronised per
+    // tile: each releases a ring slot when done with it (the last of the eight issues the
+    // slot's next copy), and T warp q waits for N warp q at each diagonal (release/acquire
+    // counter diag[q]) before it touches the block the N warp has just stored.
+    double acc[2][2][2] = {};
+    unsigned ndiag = ctl->diag[q4];  // diagonals of this quadrant so far (the warps are in step here)
+    unsigned tr[2][8];
+    int preb = -1;  // T warps: block whose accumulator load (tr) is in flight
     int o = tri_row(C.t0), j = C.t0 - o * (o + 1) / 2;
     for (int t = C.t0; t < C.t1; ++t, ++i) {
       const unsigned s = (base + i) % STAGES;
       mbar_wait(&ctl->full[s], ((base + i) / STAGES) & 1);
+      tl_mark(A, ctl, rec, 2, o, j);
       const double* Tt = ring + s * TILE_ELEMS;
       const double* xo = xb + o * CH_XBLK;
-      if (j < o) {
-        unsigned tr[8];
-        tm_ld8_issue(tbase + 8 * j, tr);  // block j's accumulator, in flight during N
+      if (!tw) {  // N: S_oj x_j (x_o on the diagonal)
         const double* xj = xb + j * CH_XBLK;
-#pragma unroll 4
-        for (int k0 = 0; k0 < TB; k0 += 4) {
-          const double a = Tt[swz(warp * 8 + g, k0 + t4)];
-          const int xr = (k0 + t4) * CH_NC + (g ^ (t4 << 2));  // ch_xpos(k0 + t4, nb * 8 + g), nb = 0
-          dmma8x8x4(acc[0][0], acc[0][1], a, xj[xr]);
-          dmma8x8x4(acc[1][0], acc[1][1], a, xj[xr ^ 8]);
+#pragma unroll 8
+        for (int k0 = 0; k0 < ((A.dbg & 2) ? 0 : TB); k0 += 4) {
+          const double* An = Tt + r0 * TB + (k0 & ~15) + acol[(k0 >> 2) & 3];  // swz(r0, k0 + t4)
+          const double a0 = An[0], a1 = An[8 * TB];
+          const double b0 = xj[xb0 + k0 * CH_NC], b1 = xj[xb1 + k0 * CH_NC];
+          dmma8x8x4(acc[0][0][0], acc[0][0][1], a0, b0);
+          dmma8x8x4(acc[0][1][0], acc[0][1][1], a1, b0);
+          dmma8x8x4(acc[1][0][0], acc[1][0][1], a0, b1);
+          dmma8x8x4(acc[1][1][0], acc[1][1][1], a1, b1);
         }
-        tm_wait_ld();
-        double pt[2][2];
+        if (j == o) {
+          // the row's chain is block o's accumulator (zero until now: block o only receives
+          // later rows' transposed products)
+          tm_st8(tq + 16 * o, acc[0]);
+          tm_st8(tq + 16 * o + 8, acc[1]);
+          tm_wait_st();
+          asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+          __syncwarp();
+          if (lane == 0)  // diagonals done by this N warp (release: the block's stores before it)
+            asm volatile("st.release.cta.shared::cta.u32 [%0], %1;\n" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(&ctl->diag[q4])),
+                         "r"(ndiag + 1)
+                         : "memory");
+          ++ndiag;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) pt[q >> 1][q & 1] = __hiloint2double((int)tr[2 * q + 1], (int)tr[2 * q]);
-#pragma unroll 4
-        for (int k0 = 0; k0 < TB; k0 += 4) {
-          const double a = Tt[swz(k0 + t4, warp * 8 + g)];
-          const int xr = (k0 + t4) * CH_NC + (g ^ (t4 << 2));
-          dmma8x8x4(pt[0][0], pt[0][1], a, xo[xr]);
-          dmma8x8x4(pt[1][0], pt[1][1], a, xo[xr ^ 8]);
+          for (int e = 0; e < 8; ++e) acc[e >> 2][(e >> 1) & 1][e & 1] = 0.0;
         }
-        tm_st8(tbase + 8 * j, pt);
-      } else {  // diagonal tile (full): the row's N result joins block o's accumulator
-#pragma unroll 4
-        for (int k0 = 0; k0 < TB; k0 += 4) {
-          const double a = Tt[swz(warp * 8 + g, k0 + t4)];
-          const int xr = (k0 + t4) * CH_NC + (g ^ (t4 << 2));
-          dmma8x8x4(acc[0][0], acc[0][1], a, xo[xr]);
-          dmma8x8x4(acc[1][0], acc[1][1], a, xo[xr ^ 8]);
+      } else if (j < o) {  // T: S_oj^T x_o onto block j's accumulator
+        if (preb != j && !(A.dbg & 4)) {
+          tm_ld8_issue(tq + 16 * j, tr[0]);
+          tm_ld8_issue(tq + 16 * j + 8, tr[1]);
         }
-        double v[2][2];
-        tm_ld8(tbase + 8 * o, v);
+        if (!(A.dbg & 4)) tm_wait_ld();
+        double pt[2][2][2];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          v[q >> 1][q & 1] += acc[q >> 1][q & 1];
-          acc[q >> 1][q & 1] = 0.0;
+        for (int h2 = 0; h2 < 2; ++h2)
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            pt[h2][e >> 1][e & 1] = __hiloint2double((int)tr[h2][2 * e + 1], (int)tr[h2][2 * e]);
+#pragma unroll 8
+        for (int k0 = 0; k0 < ((A.dbg & 2) ? 0 : TB); k0 += 4) {
+          const double a0 = Tt[at0 + k0 * TB], a1 = Tt[at1 + k0 * TB];  // swz(k0 + t4, r0 (+ 8))
+          const double b0 = xo[xb0 + k0 * CH_NC], b1 = xo[xb1 + k0 * CH_NC];
+          dmma8x8x4(pt[0][0][0], pt[0][0][1], a0, b0);
+          dmma8x8x4(pt[0][1][0], pt[0][1][1], a1, b0);
+          dmma8x8x4(pt[1][0][0], pt[1][0][1], a0, b1);
+          dmma8x8x4(pt[1][1][0], pt[1][1][1], a1, b1);
         }
-        tm_st8(tbase + 8 * o, v);
-        // coarse partial of block row o (F-apply): G_k[rows o]^T x_o, G staged in
-        // shared memory at the row's first tile (visible after that tile's barrier)
-        if (coarse && tid < d.nP * CH_NC) {
-          const int q = tid / CH_NC, cc = tid % CH_NC;
-          const int na = min(TB, d.nI - o * TB);
-          double ga = 0.0;
+        if ((A.dbg & 4)) {
+#pragma unroll
+          for (int e = 0; e < 8; ++e) tr[e >> 2][(e & 3) * 2] += __double2loint(pt[e >> 2][(e >> 1) & 1][e & 1]);
+        } else {
+        tm_st8(tq + 16 * j, pt[0]);
+        tm_st8(tq + 16 * j + 8, pt[1]);
+        }
+        preb = -1;
+        if (j + 1 < o && t + 1 < C.t1 && !(A.dbg & 4)) {  // the next tile's block, in flight across the release
+          tm_ld8_issue(tq + 16 * (j + 1), tr[0]);
+          tm_ld8_issue(tq + 16 * (j + 1) + 8, tr[1]);
+          preb = j + 1;
+        }
+        tm_wait_st();
+      } else {  // T warps at the diagonal tile
+        if (coarse) {
+          // coarse partial of block row o (F-apply): G_k[rows o]^T x_o, G staged in shared
+          // memory (two outputs per thread in flight; each sum in row order)
+          const int tt = tid - 128, n = d.nP * CH_NC, na = min(TB, d.nI - o * TB);
+          const int e0 = tt, e1 = tt + 128;
+          const int q0 = e0 / CH_NC, c0 = e0 % CH_NC, q1 = e1 / CH_NC, c1 = e1 % CH_NC;
+          double ga0 = 0.0, ga1 = 0.0;
+          if (e1 < n) {
 #pragma unroll 4
-          for (int r = 0; r < na; ++r) ga += gs[r * d.nP + q] * xo[ch_xpos(r, cc)];
-          if (cc < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + cc] = ga;
+            for (int r = 0; r < na; ++r) {
+              ga0 += gs[r * d.nP + q0] * xo[ch_xpos(r, c0)];
+              ga1 += gs[r * d.nP + q1] * xo[ch_xpos(r, c1)];
+            }
+          } else if (e0 < n) {
+#pragma unroll 4
+            for (int r = 0; r < na; ++r) ga0 += gs[r * d.nP + q0] * xo[ch_xpos(r, c0)];
+          }
+          double* gp = A.gpart + (long long)(d.blk0 + o) * A.nPmax * A.ncols + A.c_off;
+          if (e0 < n && c0 < ncl) gp[q0 * A.ncols + c0] = ga0;
+          if (e1 < n && c1 < ncl) gp[q1 * A.ncols + c1] = ga1;
+          asm volatile("bar.sync 5, 128;\n" ::: "memory");  // every T warp is done with gs
+          if (t + 1 < C.t1) stage_g(o + 1, tt, 128);
+          asm volatile("bar.sync 5, 128;\n" ::: "memory");  // G rows of row o + 1 staged
+        }
+        {  // N warp q has stored block o (its diagonal count reaches this one's)
+          const unsigned want = ++ndiag;
+          unsigned have;
+          do {
+            asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n"
+                         : "=r"(have)
+                         : "r"((unsigned)__cvta_generic_to_shared(&ctl->diag[q4]))
+                         : "memory");
+          } while ((int)(have - want) < 0);
+        }
+        __syncwarp();
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        if (t + 1 < C.t1) {  // the next tile is (o + 1, 0)
+          tm_ld8_issue(tq, tr[0]);
+          tm_ld8_issue(tq + 8, tr[1]);
+          preb = 0;
         }
       }
-      tm_wait_st();
-      asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-      __syncthreads();  // slot s consumed by every warp
-      if (tid == 0 && i + STAGES < ntiles) issue(i + STAGES);
+      // release ring slot s: the last of the eight warps to be done with it issues the
+      // slot's next copy (arrivals counted per use: use u of slot s ends at 8u + 8)
+      __syncwarp();
+      if (lane == 0) {
+        unsigned old;
+        asm volatile("atom.acq_rel.cta.shared::cta.add.u32 %0, [%1], 1;\n"
+                     : "=r"(old)
+                     : "r"((unsigned)__cvta_generic_to_shared(&ctl->rel[s]))
+                     : "memory");
+        if (old == 8u * ((base + i) / STAGES) + 7u && i + STAGES < ntiles) {
+          asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+          issue(i + STAGES);
+        }
+      }
       if (++j > o) {
         ++o;
         j = 0;
-        if (coarse && t + 1 < C.t1) {
-          stage_g(o);  // every thread is past the diagonal tile's use of gs (barrier above)
-        }
       }
     }
     // a chunk that ends inside a row: the row's N partial joins block o's accumulator
-    if (j != 0) {
-      double v[2][2];
-      tm_ld8(tbase + 8 * o, v);
+    if (j != 0 && !tw) {
 #pragma unroll
-      for (int q = 0; q < 4; ++q) v[q >> 1][q & 1] += acc[q >> 1][q & 1];
-      tm_st8(tbase + 8 * o, v);
+      for (int h2 = 0; h2 < 2; ++h2) {
+        double v[2][2];
+        tm_ld8(tq + 16 * o + 8 * h2, v);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) v[e >> 1][e & 1] += acc[h2][e >> 1][e & 1];
+        tm_st8(tq + 16 * o + 8 * h2, v);
+      }
       tm_wait_st();
     }
-    // write the chunk's partial blocks 0..ob, zero the accumulators
+    tl_mark(A, ctl, rec, 3, o, j);
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    tl_mark(A, ctl, rec, 4, o, j);
+    // write the chunk's partial blocks 0..ob (warp: quadrant q, columns 8 (w >> 2) ..),
+    // zero the accumulators
+    // (partial block indices staged at chunk start)
     const double zero[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-    for (int jb = 0; jb <= ob; ++jb) {
+    const int h2 = warp >> 2;
+    for (int jb = 0; jb <= ((A.dbg & 16) ? -1 : ob); ++jb) {
       double v[2][2];
-      tm_ld8(tbase + 8 * jb, v);
-      tm_st8(tbase + 8 * jb, zero);
-      const long long pb = A.cpb[d.blk0 + jb] + (C.rank - A.cfirst[d.blk0 + jb]);
-      double* out = A.spart + (pb * TB + warp * 8 + g) * A.ncols + A.c_off;
+      tm_ld8(tq + 16 * jb + 8 * h2, v);
+      tm_st8(tq + 16 * jb + 8 * h2, zero);
+      const long long pb = ctl->pb[jb];
 #pragma unroll
-      for (int nb = 0; nb < 2; ++nb) {
-        const int cc = nb * 8 + 2 * t4;
+      for (int mb = 0; mb < 2; ++mb) {
+        double* out = A.spart + (pb * TB + r0 + 8 * mb) * A.ncols + A.c_off;
+        const int cc = h2 * 8 + 2 * t4;
         if (cc + 1 < ncl && ((A.ncols | A.c_off) & 1) == 0) {
-          *reinterpret_cast<double2*>(out + cc) = make_double2(v[nb][0], v[nb][1]);
+          *reinterpret_cast<double2*>(out + cc) = make_double2(v[mb][0], v[mb][1]);
         } else {
-          if (cc < ncl) out[cc] = v[nb][0];
-          if (cc + 1 < ncl) out[cc + 1] = v[nb][1];
+          if (cc < ncl) out[cc] = v[mb][0];
+          if (cc + 1 < ncl) out[cc + 1] = v[mb][1];
         }
       }
     }
     tm_wait_st();
     __syncthreads();  // x blocks reused by the next chunk
   }
-  if (tid == 0) ctl->streamed = base + ntiles;
+  tl_mark(A, ctl, rec, 5, 0, 0);
+  if (tid == 0) {
+    ctl->streamed = base + ntiles;
+    ctl->ncall++;
+  }
   __syncthreads();
 }
 
@@ -2013,8 +2150,13 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
   if constexpr (NCP == 16 && EXPL && CH) {
     {  // chunk pass: ring mbarriers and the tensor-memory accumulators
       if (tid == 0) {
-        for (int s2 = 0; s2 < STAGES; ++s2) mbar_init(&g_chunk_ctl.full[s2], 1);
+        for (int s2 = 0; s2 < STAGES; ++s2) {
+          mbar_init(&g_chunk_ctl.full[s2], 1);
+          g_chunk_ctl.rel[s2] = 0;
+        }
+        for (int q = 0; q < 4; ++q) g_chunk_ctl.diag[q] = 0;
         g_chunk_ctl.streamed = 0;
+        g_chunk_ctl.ncall = g_chunk_ctl.ntl = 0;
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
       }
       if ((tid >> 5) == 0) {
@@ -2027,9 +2169,9 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
       __syncthreads();
       asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
       const int w = tid >> 5;
-      const unsigned tb = g_chunk_ctl.tmem + ((unsigned)(32 * (w & 3)) << 16) + 256u * (w >> 2);
+      const unsigned tb = g_chunk_ctl.tmem + ((unsigned)(32 * (w & 3)) << 16) + 8u * (w >> 2);
       const double zero[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-      for (int jb = 0; jb < 32; ++jb) tm_st8(tb + 8 * jb, zero);
+      for (int jb = 0; jb < 32; ++jb) tm_st8(tb + 16 * jb, zero);
       tm_wait_st();
       __syncthreads();
     }
@@ -2764,9 +2906,21 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
     IETI_CUDA(cudaMemcpyToSymbolAsync(g_prof_n, &zero, sizeof(int), 0, cudaMemcpyHostToDevice, h->stream));
     args.prof = prof.p;
   }
+  if (args.wsym.tl) IETI_CUDA(cudaMemsetAsync(args.wsym.tl, 0, 4096 * sizeof(unsigned long long), h->stream));
   void* params[] = {&args};
   IETI_CUDA(cudaLaunchCooperativeKernel((const void*)kern, grid, 256, params, cfg.smem, h->stream));
   IETI_LAUNCHED(h);
+  if (args.wsym.tl) {
+    std::vector<unsigned long long> t(4096);
+    IETI_CUDA(cudaStreamSynchronize(h->stream));
+    IETI_CUDA(cudaMemcpy(t.data(), args.wsym.tl, sizeof(unsigned long long) * 4096, cudaMemcpyDeviceToHost));
+    static const char* ev[] = {"pass", "xstaged", "tile", "loopend", "synced", "end"};
+    for (int k = 0; k < 2048 && t[2 * k]; ++k) {
+      const unsigned long long c = t[2 * k + 1];
+      fprintf(stderr, "tl %8.3f us %-8s %4u %4u\n", (t[2 * k] - t[0]) * 1e-3, ev[(c >> 32) & 7],
+              (unsigned)((c >> 16) & 0xffff), (unsigned)(c & 0xffff));
+    }
+  }
   if (prof_env) {
     // per-barrier intervals of CTA 0, averaged by position in the iteration (diagnostics)
     std::vector<unsigned long long> t(4096);
@@ -2860,6 +3014,11 @@ static bool run_solve_persistent(ietidp_s* h) {
   a.gc = h->gc.p;
   a.n_slots = h->n_slots;
   a.fold = !(getenv("IETIDP_FOLD") && atoi(getenv("IETIDP_FOLD")) == 0);
+  a.wsym.dbg = a.ssym.dbg = getenv("IETIDP_DBG_PASS") ? atoi(getenv("IETIDP_DBG_PASS")) : 0;
+  if (getenv("IETIDP_DBG_TL")) {  // diagnostics: CTA 0's timeline of two passes (stderr after the solve)
+    if (!h->dbg_tl.p) h->dbg_tl.alloc(4096);
+    a.wsym.tl = a.ssym.tl = h->dbg_tl.p;
+  }
   a.fold_multi = getenv("IETIDP_FOLD_MULTI") && atoi(getenv("IETIDP_FOLD_MULTI")) == 1;
   a.blk = h->d_blk.p;
   a.n_blk = h->n_blk;

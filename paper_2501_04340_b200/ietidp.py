@@ -10,6 +10,8 @@ import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libietidp.so")
+# IETIDP_LIB: path of another build of the same library (A/B comparisons in tools/)
+LIB_PATH = os.environ.get("IETIDP_LIB", LIB_PATH)
 
 MAX_RHS = 64
 STATUS = {0: "IETIDP_OK", 1: "IETIDP_E_ARG", 2: "IETIDP_E_STATE", 3: "IETIDP_E_B_STRUCTURE",
