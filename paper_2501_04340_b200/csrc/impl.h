@@ -127,6 +127,7 @@ struct GatherRec {
   long long base[2];
   int cnt[2];
   float sign[2];
+  int slot[2];  // the two r_I slots (the coarse term G_k z_k of the chunk-mode gather)
 };
 
 // A CTA of the loop kernels: one subdomain, one or two TB-blocks (i and nt-1-i).

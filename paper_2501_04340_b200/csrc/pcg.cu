@@ -1517,6 +1517,7 @@ struct PcgArgs {
   int coef_ld;
   const GatherRec* grec;        // chunk pass: per multiplier row, its slots' partial lists and signs
   const double* wrec;           // chunk pass: per multiplier row, the two slots' scaling weights delta
+  double* gzv;                  // chunk pass: G_k z_k per slot (n_slots x ncols), added by the gather of q
   int chunk;                   // several RHS: the chunk pass (sym_chunks) replaces the row-segment pass
   int smem_doubles;            // dynamic shared memory of the launch (doubles)
   int stop;                    // ietidp_stop: 0 ||r|| <= tol ||r0||, 1 sqrt(r.z) <= tol sqrt(r0.z0)
@@ -1709,14 +1710,49 @@ __device__ __forceinline__ void coarse_local(const PcgArgs& P, double* zs) {
 // Larger coarse problems: g (warp per entry) and then z = S_PP^-1 g (warp per row),
 // both spread over the CTAs, through global memory.
 __device__ __forceinline__ void coarse_spread(const PcgArgs& P) {
+  // a warp per entry (gi, c), lanes over the flattened partial rows (each lane's rows in
+  // order, then the butterfly); the warp's entries, their row indices and the first four
+  // rows of each lane are loaded together
   const int nc = P.ncols, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  for (int e = blockIdx.x * (VT / 32) + warp; e < P.ng * nc; e += gridDim.x * (VT / 32)) {
-    const int gi = e / nc, c = e - gi * nc;
-    double sacc = 0.0;
-    for (int q = P.gsrc_ptr[gi] + lane; q < P.gsrc_ptr[gi + 1]; q += 32)
-      sacc += __ldcg(P.gpart + (long long)P.gsrc[q] * nc + c);
-    sacc = warp_sum(sacc);
-    if (lane == 0) P.gc[e] = sacc;
+  const int n = P.ng * nc, W = gridDim.x * (VT / 32);
+  constexpr int K = 3, M = 4;
+  for (int eb = blockIdx.x * (VT / 32) + warp; eb < n; eb += K * W) {
+    int lo[K], hi[K], cc[K], idx[K][M];
+    double v[K][M];
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const int e = eb + u * W;
+      lo[u] = hi[u] = 0;
+      cc[u] = 0;
+      if (e < n) {
+        const int gi = e / nc;
+        cc[u] = e - gi * nc;
+        lo[u] = P.gsrc_ptr[gi];
+        hi[u] = P.gsrc_ptr[gi + 1];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int m = 0; m < M; ++m) {
+        const int q = lo[u] + lane + 32 * m;
+        idx[u][m] = q < hi[u] ? P.gsrc[q] : -1;
+      }
+#pragma unroll
+    for (int u = 0; u < K; ++u)
+#pragma unroll
+      for (int m = 0; m < M; ++m) v[u][m] = idx[u][m] >= 0 ? __ldcg(P.gpart + (long long)idx[u][m] * nc + cc[u]) : 0.0;
+#pragma unroll
+    for (int u = 0; u < K; ++u) {
+      const int e = eb + u * W;
+      double sacc = 0.0;
+#pragma unroll
+      for (int m = 0; m < M; ++m)
+        if (idx[u][m] >= 0) sacc += v[u][m];
+      for (int q = lo[u] + lane + 32 * M; q < hi[u]; q += 32) sacc += __ldcg(P.gpart + (long long)P.gsrc[q] * nc + cc[u]);
+      sacc = warp_sum(sacc);
+      if (lane == 0 && e < n) P.gc[e] = sacc;
+    }
   }
 }
 __device__ __forceinline__ void coarse_spread_z(const PcgArgs& P) {
@@ -1833,9 +1869,9 @@ __device__ __forceinline__ void bgather_phase(const PcgArgs& P, const double* x,
 
 // After the coarse right-hand side g (P.gc, ng x nc) is complete: every CTA takes its
 // subdomains, forms z_k = (S_PP^-1 g)[C_k rows] (S_PP^-1 rows and g staged in shared
-// memory) and adds G_k z_k into the first chunk partial of each of the subdomain's
-// slots, so that the gather of q = sum_k B (W_k p_k + G_k z_k) is a plain fold of the
-// partials (F_DP = W + G S_PP^-1 G^T, SURVEY F1 signs).
+// memory) and writes G_k z_k per slot (P.gzv); the gather of q = sum_k B (W_k p_k +
+// G_k z_k) adds it to the slot's first chunk partial (F_DP = W +
+// G S_PP^-1 G^T, SURVEY F1 signs).
 __device__ __forceinline__ void coarse_gz_phase(const PcgArgs& P, const TmvArgs& A, double* smem, int smem_doubles) {
   const int nc = P.ncols, ng = P.ng, tid = threadIdx.x;
   double* gs = smem;               // g: ng x nc
@@ -1875,9 +1911,7 @@ __device__ __forceinline__ void coarse_gz_phase(const PcgArgs& P, const TmvArgs&
           const double* Gr = gG + a * d.nP;
           double acc = 0.0;
           for (int q = 0; q < d.nP; ++q) acc += Gr[q] * zk[q * nc + c];
-          const int aa = a0 + a;
-          const long long base = A.cpb[d.blk0 + aa / TB] * TB + aa % TB;
-          A.spart[base * nc + c] += acc;  // partial 0 of the slot (one writer)
+          P.gzv[(d.rI_off + a0 + a) * nc + c] = acc;  // (G_k z_k) of the slot; the gather adds it to partial 0
         }
       a0 += na;
       if (a0 >= d.nI) break;
@@ -1893,7 +1927,7 @@ __device__ __forceinline__ void coarse_gz_phase(const PcgArgs& P, const TmvArgs&
 // partial loads, then the sums in index order: the same arithmetic as sym_value).
 template <int UR>
 __device__ __forceinline__ void gather_fold(const PcgArgs& P, const double* spart, bool weighted, double* out,
-                                            const double* dotv, double* part) {
+                                            const double* dotv, double* part, const double* gzv = nullptr) {
   const int nc = P.ncols, P2 = pow2ge(nc);
   const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
   const long long st = (long long)TB * nc;
@@ -1929,6 +1963,13 @@ __device__ __forceinline__ void gather_fold(const PcgArgs& P, const double* spar
 #pragma unroll
           for (int p = 0; p < CM; ++p) v[u][q][p] = p < g[u].cnt[q] ? __ldcg(p0 + p * st) : 0.0;
         }
+      if (gzv) {  // the coarse term joins the first partial of each slot
+#pragma unroll
+        for (int u = 0; u < UR; ++u)
+#pragma unroll
+          for (int q = 0; q < 2; ++q)
+            if (g[u].cnt[q] > 0) v[u][q][0] += __ldcg(gzv + (long long)g[u].slot[q] * nc + c);
+      }
 #pragma unroll
       for (int u = 0; u < UR; ++u) {
         const int j = j0 + u * stride;
@@ -1982,7 +2023,7 @@ __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, d
         coarse_gz_phase(P, P.wsym, smem, P.smem_doubles);
         pcg_barrier(P);
       }
-      gather_fold<2>(P, P.wsym.spart, false, P.q, P.p, pq);
+      gather_fold<2>(P, P.wsym.spart, false, P.q, P.p, pq, P.ng > 0 ? P.gzv : nullptr);
       return;
     }
   } else if constexpr (EXPL) {
@@ -2831,6 +2872,7 @@ static void plan_chunks(ietidp_s* h, int grid, int nc) {
       grec[j].base[q] = sred[L.slot[q]].base;
       grec[j].cnt[q] = sred[L.slot[q]].cnt;
       grec[j].sign[q] = L.sign[q];
+      grec[j].slot[q] = L.slot[q];
     }
   }
   h->chunk_grec.upload(grec, h->stream);
@@ -2891,6 +2933,8 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
     args.smem_doubles = cfg.smem / 8;
     args.grec = h->chunk_grec.p;
     args.wrec = h->chunk_wrec.p;
+    if (h->chunk_gzv.n < (size_t)h->n_slots * args.ncols) h->chunk_gzv.alloc(std::max<size_t>(1, (size_t)h->n_slots * args.ncols));
+    args.gzv = h->chunk_gzv.p;
     args.wsym.n_sub = args.ssym.n_sub = h->n_sub;
     if (h->n_lambda)  // the two slots' scaling weights per multiplier row (delta: set by the factorisation)
       k_wrec<<<grid_for(h->n_lambda, 256), 256, 0, h->stream>>>(h->n_lambda, h->lam.p, h->delta.p, h->chunk_wrec.p);
