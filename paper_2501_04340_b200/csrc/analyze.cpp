@@ -609,51 +609,20 @@ void analyze_all(ietidp_s* h) {
   // face/edge/corner patterns: C5 has 27 classes of 128) ----
   std::vector<int> rep(ns);
   {
-    std::vector<uint64_t> hs(ns);
-    std::vector<std::vector<int32_t>> bsorted(ns);
+    // fingerprints from ietidp_set_subdomain; members of a fingerprint group are compared
+    // with the group's first subdomain in full (in parallel); a mismatch (a fingerprint
+    // collision) makes the subdomain its own class
+    std::unordered_map<uint64_t, int> first;
+    std::vector<int> cand(ns);
+    for (int k = 0; k < ns; ++k) cand[k] = first.emplace(h->in[k].fp, k).first->second;
     parallel_for(ns, [&](int k) {
-      const SubIn& in = h->in[k];
-      bsorted[k] = in.B_dof;
-      std::sort(bsorted[k].begin(), bsorted[k].end());
-      uint64_t x = 1469598103934665603ull;
-      auto mix = [&](const void* p, size_t n) {  // 64-bit words (tail bytes), multiply-xorshift
-        const unsigned char* b = static_cast<const unsigned char*>(p);
-        size_t i = 0;
-        for (; i + 8 <= n; i += 8) {
-          uint64_t w;
-          memcpy(&w, b + i, 8);
-          x = (x ^ w) * 0x9E3779B97F4A7C15ull;
-          x ^= x >> 29;
-        }
-        for (; i < n; ++i) x = (x ^ b[i]) * 1099511628211ull;
-      };
-      auto mixv = [&](const auto& v) {
-        const uint64_t n = v.size();
-        mix(&n, sizeof(n));
-        if (n) mix(v.data(), n * sizeof(v[0]));
-      };
-      mix(&in.n, sizeof(in.n));
-      mixv(in.rowptr);
-      mixv(in.col);
-      mixv(in.tree);
-      mixv(in.prim);
-      mixv(bsorted[k]);
-      hs[k] = x;
+      const int r = cand[k];
+      const SubIn &a = h->in[k], &b = h->in[r];
+      rep[k] = (r == k || (a.n == b.n && a.rowptr == b.rowptr && a.col == b.col && a.tree == b.tree &&
+                           a.prim == b.prim && a.B_dof_sorted == b.B_dof_sorted))
+                   ? r
+                   : k;
     });
-    std::unordered_map<uint64_t, std::vector<int>> byhash;
-    for (int k = 0; k < ns; ++k) {
-      rep[k] = k;
-      auto& cand = byhash[hs[k]];
-      for (int r : cand) {
-        const SubIn &a = h->in[k], &b = h->in[r];
-        if (a.n == b.n && a.rowptr == b.rowptr && a.col == b.col && a.tree == b.tree && a.prim == b.prim &&
-            bsorted[k] == bsorted[r]) {
-          rep[k] = r;
-          break;
-        }
-      }
-      if (rep[k] == k) cand.push_back(k);
-    }
   }
   std::vector<int> reps;
   for (int k = 0; k < ns; ++k)
@@ -772,6 +741,7 @@ void analyze_all(ietidp_s* h) {
   P.dinv_doubles = dinv;
   P.inv_doubles = inv;
   P.vec_rows = vec;
+  stage(" layout: fronts");
   // relative positions of every supernode's update rows in its parent's front, once
   // per pattern class (the members' supernodes are the representative's, shifted)
   std::vector<std::vector<int>> relv(nsn);
@@ -783,8 +753,15 @@ void analyze_all(ietidp_s* h) {
       if (sx.parent < 0) continue;
       const SnHost& par = P.sn[sx.parent];
       relv[i].reserve(sx.rows.size());
+      size_t q = 0;  // both row lists are sorted: one merge
       for (int x : sx.rows) {
-        const int r = find_in_front(par, x);
+        int r;
+        if (x >= par.c0 && x < par.c0 + par.npiv) {
+          r = x - par.c0;
+        } else {
+          while (q < par.rows.size() && par.rows[q] < x) ++q;
+          r = (q < par.rows.size() && par.rows[q] == x) ? par.npiv + (int)q : -1;
+        }
         if (r < 0) relfail[k] = 1;
         relv[i].push_back(r);
       }
@@ -797,17 +774,31 @@ void analyze_all(ietidp_s* h) {
     const int d0 = P.subs[rep[k]].sn_begin[0] - P.subs[k].sn_begin[0];
     for (int i = P.subs[k].sn_begin[0]; i < P.subs[k].sn_begin[1]; ++i) relv[i] = relv[i + d0];
   });
-  for (int i = 0; i < nsn; ++i) {
-    SnHost& s = P.sn[i];
-    SnDev& d = sd[i];
-    d.rows_off = (int)rows_all.size();
-    rows_all.insert(rows_all.end(), s.rows.begin(), s.rows.end());
-    d.rel_off = (int)rel_all.size();
-    rel_all.insert(rel_all.end(), relv[i].begin(), relv[i].end());
-    d.child_off = (int)children_all.size();
-    d.nchild = (int)s.children.size();
-    children_all.insert(children_all.end(), s.children.begin(), s.children.end());
+  stage(" layout: relative rows");
+  {  // offsets first, then the copies in parallel (per subdomain)
+    long long nr = 0, nc = 0;
+    for (int i = 0; i < nsn; ++i) {
+      SnDev& d = sd[i];
+      d.rows_off = d.rel_off = (int)nr;
+      nr += (long long)P.sn[i].rows.size();
+      d.child_off = (int)nc;
+      d.nchild = (int)P.sn[i].children.size();
+      nc += d.nchild;
+    }
+    rows_all.resize(nr);
+    rel_all.resize(nr);
+    children_all.resize(nc);
+    parallel_for(ns, [&](int k) {
+      for (int i = P.subs[k].sn_begin[0]; i < P.subs[k].sn_begin[1]; ++i) {
+        const SnHost& s = P.sn[i];
+        const SnDev& d = sd[i];
+        std::copy(s.rows.begin(), s.rows.end(), rows_all.begin() + d.rows_off);
+        std::copy(relv[i].begin(), relv[i].end(), rel_all.begin() + d.rel_off);
+        std::copy(s.children.begin(), s.children.end(), children_all.begin() + d.child_off);
+      }
+    });
   }
+  stage(" layout: concatenation");
 
   auto push = [&](int a, int b, int c) { work.insert(work.end(), {a, b, c}); };
   // L11^-1 of the levels holding r_I roots is formed block row by block row as their
@@ -820,6 +811,16 @@ void analyze_all(ietidp_s* h) {
   std::vector<std::pair<int, int>> split_group;  // split-K GemmWork entries and their group
   stage("memory layout");
   // ---- work lists: factorisation and sweeps, per level ----
+  {  // capacity bounds (one allocation each; untouched capacity costs no page faults)
+    long long gb = 0, wb = 0;
+    for (const SnHost& x : P.sn) {
+      const long long np = tiles_of(x.npiv), ft = tiles_of(x.f), ut = tiles_of(x.f - x.npiv);
+      gb += np * ft * (SPLITK_MAX + 1) + 2 * np * np + ut * (ut + 1) / 2;
+      wb += 6 * (np + ft + ut) + 2 * np * (x.f / BS_RB + 2);
+    }
+    gwork.reserve((size_t)gb);
+    work.reserve((size_t)(3 * wb));
+  }
   for (int L = 0; L <= P.max_level; ++L) {
     for (int grp = 0; grp < G; ++grp) {
       LevelPlan& lp = P.glevels[grp][L];
@@ -1067,6 +1068,7 @@ void analyze_all(ietidp_s* h) {
         for (int t = 0; t < tiles_of(P.sn[i].npiv); ++t, ++lp.bxr_n) push(i, t, 0);
   }
   stage("work lists");
+  if (aprof) fprintf(stderr, "analyze: %d supernodes, %zu GemmWork, %zu Work, %zu rows\n", nsn, gwork.size(), work.size() / 3, rows_all.size());
   // ---- partitioned inverse L11^-1 by recursive doubling over TB-blocks, per level ----
   // each group's split-K launches use their own slice of the workspace and counters
   for (auto& sg : split_group) {
@@ -1304,6 +1306,8 @@ void analyze_all(ietidp_s* h) {
     std::vector<std::vector<int>> off, sl, src;  // per level: in-front offset, local supernode, CSR index
     std::vector<int> fxr, fxs;                   // loads: position, local DOF
     std::vector<int> kdiag;                      // r_I diagonal entries: CSR index
+    std::vector<int> foff, fsl, fsrc;            // the levels, then the loads, one after another
+    std::vector<long long> lev;                  // start of level L (L = NL: the loads) in f*
     std::string err;
   };
   std::vector<Rel> rel(ns);
@@ -1322,17 +1326,26 @@ void analyze_all(ietidp_s* h) {
     for (int sn = sp.sn_begin[0]; sn < sp.sn_begin[1]; ++sn)
       for (int q = 0; q < P.sn[sn].npiv; ++q) own[P.sn[sn].c0 + q] = sn;
     S.kdiag.assign(sp.nI, -1);
-    // K lower triangle in position order, column by column (pi >= pj)
+    // K lower triangle in position order, column by column (pi >= pj); the owning
+    // front's row positions in a position map while its columns are visited
+    std::vector<int> pmap(ne, -1);
+    int cur = -1;
     for (int pj = 0; pj < ne; ++pj) {
       const int j = sp.perm[pj];
       const int sn = own[pj];
       const SnHost& hs = P.sn[sn];
       const SnDev& ds = sd[sn];
+      if (sn != cur) {
+        if (cur >= 0)
+          for (int x : P.sn[cur].rows) pmap[x] = -1;
+        for (size_t q = 0; q < hs.rows.size(); ++q) pmap[hs.rows[q]] = hs.npiv + (int)q;
+        cur = sn;
+      }
       const int lcol = pj - hs.c0;
       for (int64_t e = in.rowptr[j]; e < in.rowptr[j + 1]; ++e) {
         const int pi = sp.pos[in.col[e]];
         if (pi < pj) continue;  // tree DOF (-1) or upper triangle
-        const int lrow = find_in_front(hs, pi);
+        const int lrow = pi < hs.c0 + hs.npiv ? pi - hs.c0 : pmap[pi];
         if (lrow < 0) {
           S.err = "internal: entry outside the symbolic structure";
           return;
@@ -1347,9 +1360,28 @@ void analyze_all(ietidp_s* h) {
     }
     for (int a = 0; a < sp.nI; ++a)
       if (S.kdiag[a] < 0) S.err = "subdomain " + std::to_string(k) + ": missing diagonal entry";
+    // one contiguous array per class (uploaded as it is)
+    const int nl = P.max_level + 1;
+    S.lev.assign(nl + 2, 0);
+    for (int L = 0; L < nl; ++L) S.lev[L + 1] = S.lev[L] + (long long)S.off[L].size();
+    S.lev[nl + 1] = S.lev[nl] + (long long)S.fxr.size();
+    S.foff.reserve(S.lev[nl + 1]);
+    S.fsl.reserve(S.lev[nl + 1]);
+    S.fsrc.reserve(S.lev[nl + 1]);
+    for (int L = 0; L < nl; ++L) {
+      S.foff.insert(S.foff.end(), S.off[L].begin(), S.off[L].end());
+      S.fsl.insert(S.fsl.end(), S.sl[L].begin(), S.sl[L].end());
+      S.fsrc.insert(S.fsrc.end(), S.src[L].begin(), S.src[L].end());
+      std::vector<int>().swap(S.sl[L]);
+      std::vector<int>().swap(S.src[L]);
+    }
+    S.foff.insert(S.foff.end(), S.fxr.begin(), S.fxr.end());
+    S.fsl.insert(S.fsl.end(), S.fxr.size(), 0);
+    S.fsrc.insert(S.fsrc.end(), S.fxs.begin(), S.fxs.end());
   });
   for (int k : reps)
     if (!rel[k].err.empty()) throw Error(IETIDP_E_ARG, rel[k].err);
+  stage(" scatter: relative entries");
   // segment offsets in the merged arrays: by level, then subdomain (groups contiguous)
   const int NL = P.max_level + 1;
   std::vector<long long> segoff((size_t)NL * ns + 1, 0);
@@ -1379,23 +1411,19 @@ void analyze_all(ietidp_s* h) {
     if (k == 0 || P.sub_group[k] != P.sub_group[k - 1]) gx.first = fxoff[k];
     gx.second = fxoff[k + 1] - gx.first;
   }
+  stage(" scatter: offsets");
   // relative entries of the pattern classes, concatenated; one expansion segment per
   // (level, subdomain) and per subdomain's loads (expanded on the device at upload)
-  std::vector<int> rel_off, rel_sl, rel_src;
   std::vector<long long> relbase((size_t)ns * (NL + 1), -1);  // per class rep: start of level L / loads
+  std::vector<long long> class_base(ns, -1);
+  long long nrel = 0;
   for (int k : reps) {
     const Rel& S = rel[k];
-    for (int L = 0; L < NL; ++L) {
-      relbase[(size_t)k * (NL + 1) + L] = (long long)rel_off.size();
-      rel_off.insert(rel_off.end(), S.off[L].begin(), S.off[L].end());
-      rel_sl.insert(rel_sl.end(), S.sl[L].begin(), S.sl[L].end());
-      rel_src.insert(rel_src.end(), S.src[L].begin(), S.src[L].end());
-    }
-    relbase[(size_t)k * (NL + 1) + NL] = (long long)rel_off.size();
-    rel_off.insert(rel_off.end(), S.fxr.begin(), S.fxr.end());
-    rel_sl.insert(rel_sl.end(), S.fxr.size(), 0);
-    rel_src.insert(rel_src.end(), S.fxs.begin(), S.fxs.end());
+    class_base[k] = nrel;
+    for (int L = 0; L <= NL; ++L) relbase[(size_t)k * (NL + 1) + L] = nrel + S.lev[L];
+    nrel += S.lev[NL + 1];
   }
+  stage(" scatter: concatenation");
   std::vector<ExpandSeg> segs;
   for (int L = 0; L < NL; ++L)
     for (int k = 0; k < ns; ++k) {
@@ -1415,7 +1443,7 @@ void analyze_all(ietidp_s* h) {
     const Rel& S = rel[rep[k]];
     for (size_t a = 0; a < S.kdiag.size(); ++a) kdiag[kdoff[k] + a] = (int)(h->h_sub[k].kval_off + S.kdiag[a]);
   }
-  for (int k : reps) Rel().off.swap(rel[k].off);  // (the per-class lists are no longer needed)
+  for (int k : reps) std::vector<std::vector<int>>().swap(rel[k].off);  // (only the flattened lists are kept)
   stage("scatter lists");
 
   // ---- multipliers, slots, primal bookkeeping ----
@@ -1562,7 +1590,11 @@ void analyze_all(ietidp_s* h) {
   h->d_perm.upload(perm_all, s);
   h->d_uoff.upload(h->u_off, s);
   h->d_prim_gid.upload(prim_gid, s);
-  expand_scatter(h, segs, rel_off, rel_sl, rel_src, segoff[(size_t)NL * ns], fxoff[ns]);
+  {
+    std::vector<ClassRel> cls;
+    for (int k : reps) cls.push_back({class_base[k], &rel[k].foff, &rel[k].fsl, &rel[k].fsrc});
+    expand_scatter(h, segs, cls, nrel, segoff[(size_t)NL * ns], fxoff[ns]);
+  }
   h->kdiag_src.upload(kdiag, s);
   h->slot_lam.upload(slot_lam, s);
   h->slot_sign.upload(slot_sign, s);

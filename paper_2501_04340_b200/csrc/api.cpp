@@ -1,3 +1,4 @@
+#include <algorithm>
 // C-ABI entry points of libietidp.so (include/ietidp.h). Argument checking,
 // call-order state machine, error translation; the work is in analyze.cpp and
 // the CUDA translation units.
@@ -161,15 +162,22 @@ ietidp_status ietidp_set_subdomain(ietidp_t h, int k, int n_k, const int64_t* K_
         require(e == in.rowptr[i] || in.col[e] > in.col[e - 1], IETIDP_E_ARG, "CSR columns not sorted/unique");
       }
     }
-    // pattern symmetry
-    for (int i = 0; i < n_k; ++i)
-      for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) {
-        const int j = in.col[e];
-        const int32_t* b = in.col.data() + in.rowptr[j];
-        const int32_t* en = in.col.data() + in.rowptr[j + 1];
-        const int32_t* it = std::lower_bound(b, en, i);
-        require(it != en && *it == i, IETIDP_E_ARG, "CSR pattern not symmetric");
-      }
+    // pattern symmetry in one sweep: rows i in increasing order; each upper entry (i, j)
+    // must be the next unvisited lower entry of row j (cursor nx[j]); afterwards every
+    // row's lower entries must all have been visited
+    {
+      std::vector<int64_t> nx(in.rowptr.begin(), in.rowptr.end() - 1);
+      for (int i = 0; i < n_k; ++i)
+        for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) {
+          const int j = in.col[e];
+          if (j <= i) continue;
+          const int64_t q = nx[j];
+          require(q < in.rowptr[j + 1] && in.col[q] == i, IETIDP_E_ARG, "CSR pattern not symmetric");
+          nx[j] = q + 1;
+        }
+      for (int j = 0; j < n_k; ++j)
+        require(nx[j] == in.rowptr[j + 1] || in.col[nx[j]] >= j, IETIDP_E_ARG, "CSR pattern not symmetric");
+    }
     in.B_lambda.assign(B_lambda, B_lambda + nB);
     in.B_dof.assign(B_dof, B_dof + nB);
     in.B_sign.assign(B_sign, B_sign + nB);
@@ -186,6 +194,34 @@ ietidp_status ietidp_set_subdomain(ietidp_t h, int k, int n_k, const int64_t* K_
       require(in.prim[q] >= 0 && in.prim[q] < n_k, IETIDP_E_ARG, "primal DOF out of range");
       require(in.prim_gid[q] >= 0 && in.prim_gid[q] < h->n_primal, IETIDP_E_ARG, "primal id out of range");
     }
+    // pattern fingerprint (the analysis groups subdomains with identical patterns and
+    // compares the members of a group in full)
+    in.B_dof_sorted = in.B_dof;
+    std::sort(in.B_dof_sorted.begin(), in.B_dof_sorted.end());
+    uint64_t x = 1469598103934665603ull;
+    auto mix = [&](const void* p, size_t nb) {  // 64-bit words (tail bytes), multiply-xorshift
+      const unsigned char* b = static_cast<const unsigned char*>(p);
+      size_t i = 0;
+      for (; i + 8 <= nb; i += 8) {
+        uint64_t w;
+        memcpy(&w, b + i, 8);
+        x = (x ^ w) * 0x9E3779B97F4A7C15ull;
+        x ^= x >> 29;
+      }
+      for (; i < nb; ++i) x = (x ^ b[i]) * 1099511628211ull;
+    };
+    auto mixv = [&](const auto& v) {
+      const uint64_t nv = v.size();
+      mix(&nv, sizeof(nv));
+      if (nv) mix(v.data(), nv * sizeof(v[0]));
+    };
+    mix(&in.n, sizeof(in.n));
+    mixv(in.rowptr);
+    mixv(in.col);
+    mixv(in.tree);
+    mixv(in.prim);
+    mixv(in.B_dof_sorted);
+    in.fp = x;
     in.set = true;
   });
 }

@@ -51,15 +51,22 @@ __global__ void __launch_bounds__(256)
   }
 }
 
-void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::vector<int>& off,
-                    const std::vector<int>& sl, const std::vector<int>& src, long long nK, long long nF) {
+void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::vector<ClassRel>& cls, long long nrel,
+                    long long nK, long long nF) {
   cudaStream_t s = h->stream;
   DevBuf<ExpandSeg> dseg;
   DevBuf<int> doff, dsl, dsrc;
   dseg.upload(segs, s);
-  doff.upload(off, s);
-  dsl.upload(sl, s);
-  dsrc.upload(src, s);
+  doff.alloc(std::max(nrel, 1LL));
+  dsl.alloc(std::max(nrel, 1LL));
+  dsrc.alloc(std::max(nrel, 1LL));
+  for (const ClassRel& c : cls) {  // each pattern class's entries at their offset
+    const size_t n = c.off->size() * sizeof(int);
+    if (!n) continue;
+    IETI_CUDA(cudaMemcpyAsync(doff.p + c.base, c.off->data(), n, cudaMemcpyHostToDevice, s));
+    IETI_CUDA(cudaMemcpyAsync(dsl.p + c.base, c.sl->data(), n, cudaMemcpyHostToDevice, s));
+    IETI_CUDA(cudaMemcpyAsync(dsrc.p + c.base, c.src->data(), n, cudaMemcpyHostToDevice, s));
+  }
   h->sc_front_dst.alloc(std::max(nK, 1LL));
   h->sc_front_src.alloc(std::max(nK, 1LL));
   h->sc_fx_dst.alloc(std::max(nF, 1LL));

@@ -228,8 +228,13 @@ struct ExpandSeg {
   long long base2;                   // loads: f_off
   int n, sn_base, nk, kind;          // kind 0: K entries, 1: loads
 };
-void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::vector<int>& off,
-                    const std::vector<int>& sl, const std::vector<int>& src, long long nK, long long nF);
+// per-class relative scatter entries (analyze.cpp), uploaded at their offset
+struct ClassRel {
+  long long base;
+  const std::vector<int>*off, *sl, *src;
+};
+void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::vector<ClassRel>& cls, long long nrel,
+                    long long nK, long long nF);
 void run_factor(ietidp_s* h);                  // factor.cu
 void run_coarse(ietidp_s* h);                  // coarse.cu
 void run_solve(ietidp_s* h);                   // pcg.cu

@@ -150,6 +150,8 @@ struct SubIn {
   std::vector<int32_t> B_lambda, B_dof;
   std::vector<int8_t> B_sign;
   std::vector<int32_t> tree, prim, prim_gid;
+  std::vector<int32_t> B_dof_sorted;  // supp B, sorted (pattern classes)
+  uint64_t fp = 0;                    // fingerprint of the pattern (n, CSR pattern, tree, primal, supp B)
 };
 
 struct SnHost {

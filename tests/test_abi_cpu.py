@@ -117,6 +117,35 @@ def test_nonsymmetric_pattern_rejected(lib):
     assert e.value.status == lib.E_ARG
 
 
+def test_nonsymmetric_pattern_same_counts_rejected(lib):
+    """A pattern whose row and column counts match but which is not symmetric: in a
+    symmetric pattern, entry (i, j) is moved to (i, j') with (j, i) left in place -- every
+    row keeps its length, the column sets do not mirror."""
+    import scipy.sparse as sp
+    b = make_bundle("C1")
+    sd = b["subs"][0]
+    n = len(sd["K_indptr"]) - 1
+    A = sp.csr_matrix((sd["K_data"], sd["K_indices"], sd["K_indptr"]), shape=(n, n)).tolil()
+    rows, cols = A.nonzero()
+    # an upper entry (i, j) and a column j' > i absent from row i
+    for i, j in zip(rows, cols):
+        if j > i:
+            free = [c for c in range(i + 1, n) if A[i, c] == 0]
+            if free:
+                jp = free[0]
+                break
+    A[i, jp] = A[i, j]
+    A[i, j] = 0
+    B = A.tocsr()
+    B.eliminate_zeros()
+    B.sort_indices()
+    assert B.nnz == sp.csr_matrix((sd["K_data"], sd["K_indices"], sd["K_indptr"])).nnz
+    sd["K_indptr"], sd["K_indices"], sd["K_data"] = B.indptr.astype(np.int64), B.indices.astype(np.int32), B.data
+    with pytest.raises(lib.IetiError) as e:
+        host_solver(lib, b)
+    assert e.value.status == lib.E_ARG
+
+
 def test_state_machine(lib):
     b = make_bundle("C1")
     s = host_solver(lib, b)
