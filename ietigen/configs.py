@@ -49,6 +49,10 @@ C5 = Config("C5", (8, 8, 8), 2, 6, (8, 4, 4), material="c5_random",
             rhs="c5_random", nrhs=16, scaling="stiffness")
 
 CONFIGS = {c.name: c for c in (C1, C2, C3, C4, C5)}
+# scaling case (not a BASELINE config): C5r's discretisation and data with every patch
+# its own subdomain (8 x 8 x 8 = 512 subdomains, n_gp = 833): the coarse problem is
+# larger than the one-CTA coarse factorisation (n_gp grows with N_sub)
+EXTRA = {"C5s": replace(C5, name="C5s", e=2, tiling=(8, 8, 8))}
 
 
 def get(name: str) -> Config:
@@ -56,6 +60,8 @@ def get(name: str) -> Config:
     'C4m<p>e<e>' -> the cylinder with the manufactured A* = sin(2 pi (r - 1/2)) e_z."""
     if name in CONFIGS:
         return CONFIGS[name]
+    if name in EXTRA:
+        return EXTRA[name]
     if name.startswith("E27_"):
         return paper_cube(name)
     if name.startswith("C4m"):

@@ -1228,7 +1228,9 @@ void analyze_all(ietidp_s* h) {
   }
   h->sym_maxseg = maxseg;
   if (P.max_nI > 32 * TB) throw Error(IETIDP_E_ARG, "interface block larger than 2048 DOFs is not supported");
-  if (P.nPmax > 16) throw Error(IETIDP_E_ARG, "more than 16 primal DOFs in one subdomain is not supported");
+  // the loop kernels' coarse partials: two (primal, column) outputs per thread of 256,
+  // the G_k rows of one block (TB x nP) staged in shared memory
+  if (P.nPmax > 32) throw Error(IETIDP_E_ARG, "more than 32 primal DOFs in one subdomain is not supported");
   h->n_slots = (int)rio;
   h->sum_nP = po;
   h->n_loopwork = (int)loopwork.size();

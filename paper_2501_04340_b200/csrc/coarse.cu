@@ -147,6 +147,170 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Larger coarse problems (n_gp > COARSE_CTA_MAX: n_gp grows with the
+// number of subdomains): S_PP^-1 by the BLOCKED sweep operator on the full n x n
+// matrix in global memory (row-major A = S_PP, TB-blocks). Sweeping block K:
+//   A_KK -> -A_KK^-1,  A_KJ -> A_KK^-1 A_KJ,  A_IK -> A_IK A_KK^-1,
+//   A_IJ -> A_IJ - A_IK A_KK^-1 A_KJ   (I, J != K);
+// after all blocks A = -S_PP^-1 (the block form of the scalar sweep of k_coarse_factor).
+// Per block: the pivot block's inverse (one CTA, scalar sweep in shared memory; a
+// pivot that is not positive means S_PP is not SPD), T_K* = A_KK^-1 A_K* (a tile per
+// block), the update of every other tile (DMMA), then row / column K.
+// ---------------------------------------------------------------------------
+constexpr int COARSE_CTA_MAX = 230;  // the one-CTA packed factorisation above up to this size
+
+__global__ void __launch_bounds__(256) k_bsw_pivot(int n, int K, const double* __restrict__ A, double* __restrict__ D,
+                                                  int* __restrict__ err) {
+  __shared__ double M[TB][TB + 1];
+  __shared__ double col[TB], scol[TB];
+  const int tid = threadIdx.x, k0 = K * TB, b = min(TB, n - k0);
+  for (int e = tid; e < TILE_ELEMS; e += 256) {
+    const int r = e >> 6, c = e & (TB - 1);
+    M[r][c] = (r < b && c < b) ? A[(long long)(k0 + r) * n + k0 + c] : (r == c ? 1.0 : 0.0);
+  }
+  __syncthreads();
+  bool bad = false;
+  for (int k = 0; k < TB; ++k) {
+    double akk = M[k][k];
+    if (!(akk > 0.0)) {
+      bad = true;
+      akk = 1.0;
+    }
+    const double inv = 1.0 / akk;
+    if (tid < TB) {
+      const double t = (tid == k) ? 0.0 : M[tid][k];
+      col[tid] = t;
+      scol[tid] = t * inv;
+    }
+    __syncthreads();
+    for (int e = tid; e < TILE_ELEMS; e += 256) {
+      const int r = e >> 6, c = e & (TB - 1);
+      M[r][c] = fma(-scol[r], col[c], M[r][c]);
+    }
+    __syncthreads();
+    if (tid < TB) {
+      M[tid][k] = (tid == k) ? -inv : scol[tid];
+      M[k][tid] = (tid == k) ? -inv : scol[tid];
+    }
+    __syncthreads();
+  }
+  if (bad && tid == 0) atomicMin(err + 1, 0);
+  for (int e = tid; e < TILE_ELEMS; e += 256) D[e] = -M[e >> 6][e & (TB - 1)];  // A_KK^-1 (row-major)
+}
+
+// C(64 x 64 tile) = op of A-tile (row-major, lda) times B-tile (row-major, ldb), DMMA,
+// 4 warps x 32 x 32; tiles staged in shared memory (zero padded). mode 0: C = A B,
+// 1: C -= A B.
+constexpr int BSW_SMEM = 2 * TB * (TB + 1) * (int)sizeof(double);  // two staged tiles (dynamic)
+__device__ __forceinline__ void bsw_tile_mma(const double* A, long long lda, int am, int ak, const double* B,
+                                             long long ldb, int bn, double* C, long long ldc, int cm, int cn,
+                                             int mode, double (*As)[TB + 1], double (*Bs)[TB + 1]) {
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31, g = lane >> 2, t = lane & 3;
+  for (int e = tid; e < TILE_ELEMS; e += 128) {
+    const int r = e >> 6, c = e & (TB - 1);
+    As[r][c] = (r < am && c < ak) ? A[r * lda + c] : 0.0;
+    Bs[r][c] = (r < ak && c < bn) ? B[r * ldb + c] : 0.0;
+  }
+  __syncthreads();
+  const int wm = (warp & 1) * 32, wn = (warp >> 1) * 32;
+  double acc[4][4][2] = {};
+#pragma unroll 4
+  for (int k0 = 0; k0 < TB; k0 += 4) {
+    double a[4], bb[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) a[i] = As[wm + 8 * i + g][k0 + t];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) bb[j] = Bs[k0 + t][wn + 8 * j + g];
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) dmma8x8x4(acc[i][j][0], acc[i][j][1], a[i], bb[j]);
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int r = wm + 8 * i + g, c = wn + 8 * j + 2 * t + e;
+        if (r < cm && c < cn) {
+          double* p = C + r * ldc + c;
+          *p = mode ? *p - acc[i][j][e] : acc[i][j][e];
+        }
+      }
+  __syncthreads();
+}
+
+// T_KJ = A_KK^-1 A_KJ for every block J (J = K included: unused)
+__global__ void __launch_bounds__(128) k_bsw_row(int n, int K, const double* __restrict__ A,
+                                                const double* __restrict__ D, double* __restrict__ T) {
+  extern __shared__ double bsm[];
+  auto As = reinterpret_cast<double(*)[TB + 1]>(bsm);
+  auto Bs = reinterpret_cast<double(*)[TB + 1]>(bsm + TB * (TB + 1));
+  const int J = blockIdx.x, k0 = K * TB, j0 = J * TB;
+  const int bk = min(TB, n - k0), bj = min(TB, n - j0);
+  bsw_tile_mma(D, TB, bk, bk, A + (long long)k0 * n + j0, n, bj, T + j0, n, bk, bj, 0, As, Bs);
+}
+
+// A_IJ -= A_IK T_KJ for I, J != K
+__global__ void __launch_bounds__(128) k_bsw_update(int n, int nb, int K, double* __restrict__ A,
+                                                   const double* __restrict__ T) {
+  extern __shared__ double bsm[];
+  auto As = reinterpret_cast<double(*)[TB + 1]>(bsm);
+  auto Bs = reinterpret_cast<double(*)[TB + 1]>(bsm + TB * (TB + 1));
+  const int I = blockIdx.x / nb, J = blockIdx.x % nb;
+  if (I == K || J == K) return;
+  const int i0 = I * TB, j0 = J * TB, k0 = K * TB;
+  const int bi = min(TB, n - i0), bj = min(TB, n - j0), bk = min(TB, n - k0);
+  bsw_tile_mma(A + (long long)i0 * n + k0, n, bi, bk, T + j0, n, bj, A + (long long)i0 * n + j0, n, bi, bj, 1, As,
+               Bs);
+}
+
+// row / column K: A_KJ = T_KJ, A_JK = T_KJ^T (J != K), A_KK = -A_KK^-1
+__global__ void __launch_bounds__(256) k_bsw_fix(int n, int K, double* __restrict__ A, const double* __restrict__ D,
+                                                const double* __restrict__ T) {
+  const int k0 = K * TB, bk = min(TB, n - k0);
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)bk * n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e - (long long)r * n);
+    if (c >= k0 && c < k0 + bk) {
+      A[(long long)(k0 + r) * n + c] = -D[r * TB + (c - k0)];
+    } else {
+      const double v = T[(long long)r * n + c];
+      A[(long long)(k0 + r) * n + c] = v;
+      A[(long long)c * n + k0 + r] = v;
+    }
+  }
+}
+
+// S = 1/2 (S + S^T) into A; afterwards Sinv = -A, zc0 = Sinv ftilde
+__global__ void k_bsw_init(int n, const double* __restrict__ S, double* __restrict__ A) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * n;
+       e += (long long)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e - (long long)i * n);
+    A[e] = 0.5 * (S[(long long)i * n + j] + S[(long long)j * n + i]);
+  }
+}
+__global__ void k_bsw_finish(int n, int nrhs, const double* __restrict__ A, double* __restrict__ Sinv,
+                             const double* __restrict__ ftil, double* __restrict__ zc0) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < (long long)n * n;
+       e += (long long)gridDim.x * blockDim.x)
+    Sinv[e] = -A[e];
+}
+__global__ void k_bsw_z(int n, int nrhs, const double* __restrict__ Sinv, const double* __restrict__ ftil,
+                        double* __restrict__ zc0) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = warp; e < n * nrhs; e += nw) {
+    const int i = e / nrhs, c = e - i * nrhs;
+    double s = 0.0;
+    for (int j = lane; j < n; j += 32) s += Sinv[(long long)i * n + j] * ftil[j * nrhs + c];
+    s = warp_sum(s);
+    if (lane == 0) zc0[e] = s;
+  }
+}
+
 // Dirichlet scaling weights (R5).
 __global__ void k_scaling(int m, const LamDev* __restrict__ lam, const int* __restrict__ kdiag_src,
                           const double* __restrict__ kval, double* __restrict__ kdiag, double* __restrict__ delta,
@@ -287,17 +451,41 @@ void run_coarse(ietidp_s* h) {
     run_sweeps(h, h->Xf.p, true, false);
   }
   if (ng > 0) {
-    const int smem = ng * (ng + 1) / 2 * sizeof(double);
-    if (smem > 220 * 1024) throw Error(IETIDP_E_ARG, "coarse problem too large for the one-CTA coarse factorisation");
-    IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     k_coarse_assemble<<<grid_for((long long)ng * (ng + nrhs), 256), 256, 0, s>>>(
         ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p, h->pcon_sub.p, h->pcon_q.p, h->d_sub.p,
         h->Xf.p, h->S.p, h->ftil.p);
     IETI_LAUNCHED(h);
-    k_coarse_factor<<<1, 1024, smem, s>>>(ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p,
-                                          h->pcon_sub.p, h->pcon_q.p, h->d_sub.p, h->Xf.p, h->S.p, h->Sinv.p,
-                                          h->ftil.p, h->zc0.p, h->err_flag.p);
-    IETI_LAUNCHED(h);
+    if (ng <= COARSE_CTA_MAX) {
+      const int smem = ng * (ng + 1) / 2 * sizeof(double);
+      IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      k_coarse_factor<<<1, 1024, smem, s>>>(ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p,
+                                            h->pcon_sub.p, h->pcon_q.p, h->d_sub.p, h->Xf.p, h->S.p, h->Sinv.p,
+                                            h->ftil.p, h->zc0.p, h->err_flag.p);
+      IETI_LAUNCHED(h);
+    } else {  // blocked sweep operator over all SMs
+      const int nb = (ng + TB - 1) / TB;
+      if (h->bsw_A.n < (size_t)ng * ng) {
+        h->bsw_A.alloc((size_t)ng * ng);
+        h->bsw_T.alloc((size_t)TB * ng);
+        h->bsw_D.alloc(TILE_ELEMS);
+      }
+      IETI_CUDA(cudaFuncSetAttribute((const void*)k_bsw_row, cudaFuncAttributeMaxDynamicSharedMemorySize, BSW_SMEM));
+      IETI_CUDA(cudaFuncSetAttribute((const void*)k_bsw_update, cudaFuncAttributeMaxDynamicSharedMemorySize, BSW_SMEM));
+      k_bsw_init<<<grid_for((long long)ng * ng, 256), 256, 0, s>>>(ng, h->S.p, h->bsw_A.p);
+      IETI_LAUNCHED(h);
+      for (int K = 0; K < nb; ++K) {
+        k_bsw_pivot<<<1, 256, 0, s>>>(ng, K, h->bsw_A.p, h->bsw_D.p, h->err_flag.p);
+        k_bsw_row<<<nb, 128, BSW_SMEM, s>>>(ng, K, h->bsw_A.p, h->bsw_D.p, h->bsw_T.p);
+        k_bsw_update<<<nb * nb, 128, BSW_SMEM, s>>>(ng, nb, K, h->bsw_A.p, h->bsw_T.p);
+        k_bsw_fix<<<grid_for((long long)TB * ng, 256), 256, 0, s>>>(ng, K, h->bsw_A.p, h->bsw_D.p, h->bsw_T.p);
+        for (int q = 0; q < 4; ++q) IETI_LAUNCHED(h);
+      }
+      k_bsw_finish<<<grid_for((long long)ng * ng, 256), 256, 0, s>>>(ng, nrhs, h->bsw_A.p, h->Sinv.p, h->ftil.p,
+                                                                      h->zc0.p);
+      k_bsw_z<<<grid_for((long long)ng * nrhs * 32, 256), 256, 0, s>>>(ng, nrhs, h->Sinv.p, h->ftil.p, h->zc0.p);
+      IETI_LAUNCHED(h);
+      IETI_LAUNCHED(h);
+    }
   }
   // d = sum_k B_I L_II^-T (y_I - L_PI^T C_k S^-1 ftilde)
   if (h->n_lambda) {

@@ -192,6 +192,7 @@ struct ietidp_s {
   ieti::DevBuf<ieti::GatherRec> chunk_grec;
   ieti::DevBuf<double> chunk_wrec;
   ieti::DevBuf<double> chunk_gzv;  // G_k z_k per slot (chunk-mode gather of q)
+  ieti::DevBuf<double> bsw_A, bsw_T, bsw_D;  // blocked sweep operator of large coarse problems (coarse.cu)
   std::vector<ieti::LamDev> h_lam;  // host copy of the multiplier rows (slots, signs)
   ieti::DevBuf<int> sub_cta0, sub_ncta;   // loop CTAs of each subdomain
   ieti::DevBuf<ieti::LamDev> lam;

@@ -251,7 +251,7 @@ __device__ __forceinline__ void tmv_item(const TmvArgs& A, int item, double* sme
     if (s < nsteps) load_tile_async(ring + s * TILE_ELEMS, tile_ptr(s), tid);
     cp_async_commit();
   }
-  double gacc = 0.0;  // FWD coarse partial of (q, c) = (tid / NCP, tid % NCP)
+  double gacc[2] = {0.0, 0.0};  // FWD coarse partials of (q, c) = ((tid + 256 u) / NCP, (tid + 256 u) % NCP)
   double accN[8], accT[2], acc[NB][2];
 #pragma unroll
   for (int i = 0; i < 8; ++i) accN[i] = 0.0;
@@ -353,19 +353,27 @@ __device__ __forceinline__ void tmv_item(const TmvArgs& A, int item, double* sme
           gs[e] = r < na ? A.lpi[d.lpi_off + (long long)q * d.nI + o * TB + r] : 0.0;
         }
         __syncthreads();
-        if (tid < d.nP * NCP) {
-          const int q = tid / NCP, c = tid % NCP;
-          for (int r = 0; r < na; ++r) gacc += gs[q * TB + r] * outb[r * VS + c];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int e = tid + 256 * u;
+          if (e < d.nP * NCP) {
+            const int q = e / NCP, c = e % NCP;
+            for (int r = 0; r < na; ++r) gacc[u] += gs[q * TB + r] * outb[r * VS + c];
+          }
         }
       }
       __syncthreads();
     }
   }
   cp_async_wait<0>();
-  if (MODE == FWD && A.gpart && tid < d.nP * NCP) {
-    const int q = tid / NCP, c = tid % NCP;
-    if (c < ncl) A.gpart[((long long)item * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
-  }
+  if (MODE == FWD && A.gpart)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = tid + 256 * u;
+      if (e >= d.nP * NCP) break;
+      const int q = e / NCP, c = e % NCP;
+      if (c < ncl) A.gpart[((long long)item * A.nPmax + q) * A.ncols + A.c_off + c] = gacc[u];
+    }
 }
 
 // One work item of a symmetric matrix held as lower TB-tiles (diagonal tiles full):
@@ -411,16 +419,20 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
   cp_async_wait<STAGES - 2>();  // group 0: the gathered input and tile 0
   __syncthreads();              // vec complete
   // coarse partial of block row o (first segment only): G_k[rows o]^T x_o
-  double gacc = 0.0;
+  double gacc[2] = {0.0, 0.0};
   if (A.gpart && d.nP > 0 && sw.seg == 0) {
     double* gs = xo + TB * VS;  // TB x nP
     const int na = min(TB, d.nI - o * TB);
     const double* Gb = A.gmat + d.g_off + (long long)o * TB * d.nP;
     for (int e = tid; e < na * d.nP; e += 256) gs[e] = Gb[e];
     __syncthreads();
-    if (tid < d.nP * NCP) {
-      const int q = tid / NCP, c = tid % NCP;
-      for (int r = 0; r < na; ++r) gacc += gs[r * d.nP + q] * xo[r * VS + c];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int e = tid + 256 * u;
+      if (e < d.nP * NCP) {
+        const int q = e / NCP, c = e % NCP;
+        for (int r = 0; r < na; ++r) gacc[u] += gs[r * d.nP + q] * xo[r * VS + c];
+      }
     }
     __syncthreads();
   }
@@ -531,10 +543,13 @@ __device__ __forceinline__ void sym_item(const TmvArgs& A, int item, double* sme
       }
   }
   cp_async_wait<0>();
-  if (A.gpart && sw.seg == 0 && tid < d.nP * NCP) {
-    const int q = tid / NCP, c = tid % NCP;
-    if (c < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
-  }
+  if (A.gpart && sw.seg == 0)
+    for (int u = 0; u < 2; ++u) {
+      const int e = tid + 256 * u;
+      if (e >= d.nP * NCP) break;
+      const int q = e / NCP, c = e % NCP;
+      if (c < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + c] = gacc[u];
+    }
 }
 
 // The symmetric pass over a CTA's list of row-segment items as ONE tile stream: the
@@ -585,7 +600,7 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
 #pragma unroll
   for (int st = 0; st < STAGES - 1; ++st) issue(st);
   double accN[8], acc[NB][2];
-  double gacc = 0.0;
+  double gacc[2] = {0.0, 0.0};
   const int g = lane >> 2, t4 = lane & 3;
   double* pend = nullptr;
   int pend_buf = 0;
@@ -598,15 +613,19 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
     const int o = sw.o, j0 = sw.j0, nst = nsteps_of(sw);
     double* vec = vbase + (k % NVB) * VROWS * VS;
     double* xo = (sw.j1 < o) ? vec + nst * TB * VS : vec + (o - j0) * TB * VS;
-    gacc = 0.0;
+    gacc[0] = gacc[1] = 0.0;
     if (A.gpart && d.nP > 0 && sw.seg == 0) {  // coarse partial of block row o
       const int na = min(TB, d.nI - o * TB);
       const double* Gb = A.gmat + d.g_off + (long long)o * TB * d.nP;
       for (int e = tid; e < na * d.nP; e += 256) gs[e] = Gb[e];
       __syncthreads();
-      if (tid < d.nP * NCP) {
-        const int q = tid / NCP, c = tid % NCP;
-        for (int r = 0; r < na; ++r) gacc += gs[r * d.nP + q] * xo[r * VS + c];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int e = tid + 256 * u;
+        if (e < d.nP * NCP) {
+          const int q = e / NCP, c = e % NCP;
+          for (int r = 0; r < na; ++r) gacc[u] += gs[r * d.nP + q] * xo[r * VS + c];
+        }
       }
     }
 #pragma unroll
@@ -706,10 +725,13 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
           if (c < ncl) nb_out[(long long)(warp * 8 + g) * A.ncols + c] = acc[nb][q];
         }
     }
-    if (A.gpart && sw.seg == 0 && tid < d.nP * NCP) {
-      const int q = tid / NCP, c = tid % NCP;
-      if (c < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + c] = gacc;
-    }
+    if (A.gpart && sw.seg == 0)
+      for (int u = 0; u < 2; ++u) {
+        const int e = tid + 256 * u;
+        if (e >= d.nP * NCP) break;
+        const int q = e / NCP, c = e % NCP;
+        if (c < ncl) A.gpart[((long long)(d.blk0 + o) * A.nPmax + q) * A.ncols + A.c_off + c] = gacc[u];
+      }
   }
   if constexpr (NCP == 1) {
     __syncthreads();
@@ -1015,22 +1037,24 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
           // coarse partial of block row o (F-apply): G_k[rows o]^T x_o, G staged in shared
           // memory (two outputs per thread in flight; each sum in row order)
           const int tt = tid - 128, n = d.nP * CH_NC, na = min(TB, d.nI - o * TB);
-          const int e0 = tt, e1 = tt + 128;
-          const int q0 = e0 / CH_NC, c0 = e0 % CH_NC, q1 = e1 / CH_NC, c1 = e1 % CH_NC;
-          double ga0 = 0.0, ga1 = 0.0;
-          if (e1 < n) {
-#pragma unroll 4
-            for (int r = 0; r < na; ++r) {
-              ga0 += gs[r * d.nP + q0] * xo[ch_xpos(r, c0)];
-              ga1 += gs[r * d.nP + q1] * xo[ch_xpos(r, c1)];
-            }
-          } else if (e0 < n) {
-#pragma unroll 4
-            for (int r = 0; r < na; ++r) ga0 += gs[r * d.nP + q0] * xo[ch_xpos(r, c0)];
-          }
           double* gp = A.gpart + (long long)(d.blk0 + o) * A.nPmax * A.ncols + A.c_off;
-          if (e0 < n && c0 < ncl) gp[q0 * A.ncols + c0] = ga0;
-          if (e1 < n && c1 < ncl) gp[q1 * A.ncols + c1] = ga1;
+          for (int e0 = tt; e0 < n; e0 += 256) {
+            const int e1 = e0 + 128;
+            const int q0 = e0 / CH_NC, c0 = e0 % CH_NC, q1 = e1 / CH_NC, c1 = e1 % CH_NC;
+            double ga0 = 0.0, ga1 = 0.0;
+            if (e1 < n) {
+#pragma unroll 4
+              for (int r = 0; r < na; ++r) {
+                ga0 += gs[r * d.nP + q0] * xo[ch_xpos(r, c0)];
+                ga1 += gs[r * d.nP + q1] * xo[ch_xpos(r, c1)];
+              }
+            } else {
+#pragma unroll 4
+              for (int r = 0; r < na; ++r) ga0 += gs[r * d.nP + q0] * xo[ch_xpos(r, c0)];
+            }
+            if (c0 < ncl) gp[q0 * A.ncols + c0] = ga0;
+            if (e1 < n && c1 < ncl) gp[q1 * A.ncols + c1] = ga1;
+          }
           asm volatile("bar.sync 5, 128;\n" ::: "memory");  // every T warp is done with gs
           if (t + 1 < C.t1) stage_g(o + 1, tt, 128);
           asm volatile("bar.sync 5, 128;\n" ::: "memory");  // G rows of row o + 1 staged
@@ -1876,8 +1900,8 @@ __device__ __forceinline__ void coarse_gz_phase(const PcgArgs& P, const TmvArgs&
   const int nc = P.ncols, ng = P.ng, tid = threadIdx.x;
   double* gs = smem;               // g: ng x nc
   double* srow = gs + ng * nc;     // the subdomain's nP rows of S_PP^-1 (nP x ng)
-  double* zk = srow + 16 * ng;     // z_k: nP x nc
-  double* gG = zk + 16 * nc;       // G_k rows, a chunk at a time (rows x nP)
+  double* zk = srow + P.nPmax * ng;  // z_k: nP x nc
+  double* gG = zk + P.nPmax * nc;    // G_k rows, a chunk at a time (rows x nP)
   const int gcap = smem_doubles - (int)(gG - smem);
   for (int e = tid; e < ng * nc; e += VT) gs[e] = __ldcg(P.gc + e);
   for (int k = blockIdx.x; k < A.n_sub; k += gridDim.x) {
@@ -2471,6 +2495,7 @@ struct TmvCfg {
 // items of the triangular operators
 static TmvCfg tmv_cfg(const ietidp_s* h, int ncols, bool sym = false) {
   const int nt = (h->plan.max_nI + TB - 1) / TB;
+  const int npg = std::max(h->plan.nPmax, 16);  // staged coarse rows: TB x nP (at least 16)
   if (ncols == 1) {
     if (sym) {
       // row-segment items streamed through one ring (sym_stream): STAGES tiles and
@@ -2480,20 +2505,20 @@ static TmvCfg tmv_cfg(const ietidp_s* h, int ncols, bool sym = false) {
         const int e = atoi(getenv("IETIDP_STAGES1"));
         st = (e == 3 || e == 5) ? e : 2;
       }
-      return {1, st, (st * TILE_ELEMS + st * (SYM_SEG + 1) * TB + TB * 16) * 8};
+      return {1, st, (st * TILE_ELEMS + st * (SYM_SEG + 1) * TB + TB * npg) * 8};
     }
     // many work items: 3 stages (two CTAs per SM hide each other's barriers);
     // few (C2: 128 items): 5 stages, one deep-pipelined CTA per SM
     int st = h->n_loopwork >= 2 * 148 ? 3 : 5;
     if (getenv("IETIDP_STAGES1")) st = atoi(getenv("IETIDP_STAGES1")) == 5 ? 5 : 3;
-    return {1, st, (st * TILE_ELEMS + nt * TB + TB + TB * 16) * 8};
+    return {1, st, (st * TILE_ELEMS + nt * TB + TB + TB * npg) * 8};
   }
   for (int ncp : {16, 8}) {
     if (ncp == 16 && ncols <= 8) continue;
     const int vs = ncp + 4;
     for (int stages = 3; stages >= 2; --stages) {
-      int bytes = sym ? (stages * TILE_ELEMS + stages * (SYM_SEG + 1) * TB * vs + TB * 16) * 8
-                      : (stages * TILE_ELEMS + nt * TB * vs + TB * vs + TB * 16) * 8;
+      int bytes = sym ? (stages * TILE_ELEMS + stages * (SYM_SEG + 1) * TB * vs + TB * npg) * 8
+                      : (stages * TILE_ELEMS + nt * TB * vs + TB * vs + TB * npg) * 8;
       if (bytes <= 210 * 1024) return {ncp, stages, bytes};
     }
   }
@@ -3113,7 +3138,8 @@ static bool run_solve_persistent(ietidp_s* h) {
         stages = 2;
         bytes = (stages * TILE_ELEMS + nt * CH_XBLK + gsz) * 8;
       }
-      const int gz = (h->n_primal * nc + 16 * h->n_primal + 16 * nc + TB * 16) * (int)sizeof(double);
+      const int npm = std::max(h->plan.nPmax, 1);
+      const int gz = (h->n_primal * nc + npm * h->n_primal + npm * nc + TB * npm) * (int)sizeof(double);
       if (bytes <= 210 * 1024 && bytes >= gz) {
         a.chunk = 1;
         cfg.stages = stages;

@@ -103,6 +103,31 @@ def test_solution_iteration_matched(lib, name):
     check_solution(b, lam, u, ref_f["lam"], ref_f["u"])
 
 
+def test_large_coarse_problem(lib):
+    """C5s: C5r with every patch its own subdomain (512 subdomains, n_gp = 833 > the
+    one-CTA coarse factorisation's 230): S_PP^-1 by the blocked sweep operator over all
+    SMs (coarse.cu). Operators within 1e-10 (F_DP contains G S_PP^-1 G^T), the solution
+    at natural stopping per column against the oracle."""
+    b, ref = case("C5s")
+    assert b["n_primal"] > 230
+    D = ref["dp"]
+    s = lib.from_bundle(b)
+    s.factor()
+    assert rel(s.get_coarse(), D.S) <= 1e-10
+    rng = np.random.default_rng(11)
+    X = rng.standard_normal((b["n_lambda"], b["nrhs"]))
+    assert rel(s.apply_F(X), D.apply_F(X)) <= 1e-10
+    assert rel(s.apply_precond(X), D.apply_M(X)) <= 1e-10
+    lam, rep = s.solve()
+    u = [s.get_u(k) for k in range(b["n_sub"])]
+    it_ref, it_gpu = np.asarray(ref["iters"]), np.asarray(rep["iters"])
+    it_alt = None if np.all(np.abs(it_gpu - it_ref) <= 1) else explicit_inverse_iters(b)
+    print("C5s iters gpu", list(it_gpu), "oracle", list(it_ref), "explicit", it_alt)
+    check_iters(it_gpu, it_ref, it_alt)
+    assert max(rep["rel_residual"]) <= 1e-10
+    check_solution(b, lam, u, ref["lam"], ref["u"])
+
+
 @pytest.mark.parametrize("name", ["C2r", "C3r"])
 def test_triangular_loop_solution(lib, name):
     b, ref = case(name)
