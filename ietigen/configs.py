@@ -26,6 +26,7 @@ class Config:
     tol: float = 1e-10
     seed: int = 0
     load_nq_extra: int = 3  # Gauss points per element for loads: p + load_nq_extra
+    parts: tuple = None     # explicit partition: a subdomain id per patch (x fastest), else the tiling
 
     @property
     def n_sub(self):
@@ -57,7 +58,8 @@ EXTRA = {"C5s": replace(C5, name="C5s", e=2, tiling=(8, 8, 8))}
 
 def get(name: str) -> Config:
     """'C2' -> full config; 'C2r' -> reduced e=2 variant; 'C1e4' -> C1 with e=4;
-    'C4m<p>e<e>' -> the cylinder with the manufactured A* = sin(2 pi (r - 1/2)) e_z."""
+    'C4m<p>e<e>' -> the cylinder with the manufactured A* = sin(2 pi (r - 1/2)) e_z;
+    'E27_<tiling or partition>_p<p>_e<e>' -> the paper's 27-patch family."""
     if name in CONFIGS:
         return CONFIGS[name]
     if name in EXTRA:
@@ -76,12 +78,31 @@ def get(name: str) -> Config:
     raise KeyError(name)
 
 
+# E1's three subdomains of 9 patches each (Fig. 1: a METIS-like partition
+# of the 27 patches, our reading, R14): part 0 = the patch layer x = 0, part 1
+# = (x >= 1, y = 0) + (x = 1, y = 1), part 2 = the rest -- L-shaped cross-sections
+# extruded in z. All three meet along the line x = 1/3, y = 2/3: cross edges, n_gp > 0.
+def _l3_parts():
+    out = []
+    for k in range(3):
+        for j in range(3):
+            for i in range(3):
+                out.append(0 if i == 0 else (1 if (j == 0 or (i == 1 and j == 1)) else 2))
+    return tuple(out)
+
+
+PAPER_PARTS = {"L3": _l3_parts()}
+
+
 def paper_cube(name: str) -> Config:
     """The paper's experiment family: 27 cube patches (3 x 3 x 3),
     nu = 1, homogeneous manufactured A* (our reading, R14), degree p, e elements
     per patch direction (normalised h = 1/(3e)), a box tiling of the patch
     grid: 'E27_<tx><ty><tz>_p<p>_e<e>', e.g. 'E27_311_p2_e4' (N_sub = 3)."""
     _, t, p, e = name.split("_")
+    if t in PAPER_PARTS:  # explicit partition ('E27_L3_p<p>_e<e>')
+        parts = PAPER_PARTS[t]
+        return Config(name, (3, 3, 3), int(p[1:]), int(e[1:]), (max(parts) + 1, 1, 1), tol=1e-6, parts=parts)
     return Config(name, (3, 3, 3), int(p[1:]), int(e[1:]), tuple(int(x) for x in t), tol=1e-6)
 
 

@@ -111,15 +111,30 @@ class Grid:
 
 
 class Subdomain:
-    def __init__(self, idx, lo, hi):
+    """A box of patches [lo, hi), or (explicit partitions) a union of unit patch boxes."""
+
+    def __init__(self, idx, lo, hi, boxes=None):
         self.idx, self.lo, self.hi = idx, tuple(lo), tuple(hi)
+        self.boxes = boxes if boxes is not None else [(self.lo, self.hi)]
 
 
 def tiling_subdomains(cfg):
     """Boxes of patches: T[a] parts along axis a, cut at floor(i N[a] / T[a]) (equal
     blocks when T[a] divides N[a]; otherwise sizes differ by one, e.g. 3 patches in 2
-    parts -> 1 + 2, for the paper's N_sub in {2..12} on 27 patches)."""
+    parts -> 1 + 2, for the paper's N_sub in {2..12} on 27 patches).
+    With cfg.parts (a part id per patch, x fastest) every subdomain is the union of its
+    patches (subdomains are unions of patches, e.g. METIS partitions)."""
     N, T = cfg.npatch, cfg.tiling
+    if cfg.parts is not None:
+        parts = np.asarray(cfg.parts).reshape(N[2], N[1], N[0])
+        subs = []
+        for q in range(int(parts.max()) + 1):
+            kk, jj, ii = np.nonzero(parts == q)
+            boxes = [((int(i), int(j), int(k)), (int(i) + 1, int(j) + 1, int(k) + 1)) for i, j, k in zip(ii, jj, kk)]
+            lo = (int(ii.min()), int(jj.min()), int(kk.min()))
+            hi = (int(ii.max()) + 1, int(jj.max()) + 1, int(kk.max()) + 1)
+            subs.append(Subdomain(q, lo, hi, boxes))
+        return subs
     assert all(1 <= T[a] <= N[a] for a in range(3))
     cuts = [[(i * N[a]) // T[a] for i in range(T[a] + 1)] for a in range(3)]
     subs = []
@@ -251,10 +266,14 @@ class Problem:
         smin = np.full(ne, 1 << 30, np.int64)
         smax = np.full(ne, -1, np.int64)
         for sd in self.subs:
-            gids, ml = g.block_edges(sd.lo, sd.hi)
+            if len(sd.boxes) == 1:
+                gids, ml = g.block_edges(sd.lo, sd.hi)
+                sd.ml = ml
+            else:  # union of patch boxes: the distinct global edges, in increasing order
+                gids = np.unique(np.concatenate([g.block_edges(lo, hi)[0] for lo, hi in sd.boxes]))
+                sd.ml = None
             assert len(np.unique(gids)) == len(gids)
             self.sub_edges.append(gids)
-            sd.ml = ml
             np.add.at(count, gids, 1)
             np.minimum.at(smin, gids, sd.idx)
             np.maximum.at(smax, gids, sd.idx)
@@ -268,10 +287,29 @@ class Problem:
         T = self.cfg.tiling
         per = self.cfg.periodic
         pos = {}
-        for sd in self.subs:
+        self.iface_pairs = []
+        if self.cfg.parts is not None:
+            # explicit partitions: an interface per pair of parts with face-adjacent patches
+            # (one facet each), its closure = the edges the two share
+            N = self.cfg.npatch
+            parts = np.asarray(self.cfg.parts).reshape(N[2], N[1], N[0])
+            for pz in range(N[2]):
+                for py in range(N[1]):
+                    for px in range(N[0]):
+                        for a in range(3):
+                            q = [px, py, pz]
+                            q[a] += 1
+                            if q[a] >= N[a]:
+                                continue
+                            k, l = int(parts[pz, py, px]), int(parts[q[2], q[1], q[0]])
+                            if k != l and (min(k, l), max(k, l)) not in self.iface_pairs:
+                                self.iface_pairs.append((min(k, l), max(k, l)))
+            for k, l in self.iface_pairs:
+                shared = np.intersect1d(sets[k], sets[l], assume_unique=True)
+                nfacet[shared] += 1
+        for sd in self.subs if self.cfg.parts is None else []:
             t = (sd.idx % T[0], (sd.idx // T[0]) % T[1], sd.idx // (T[0] * T[1]))
             pos[t] = sd.idx
-        self.iface_pairs = []
         for t, k in pos.items():
             for a in range(3):
                 t2 = list(t)
@@ -392,6 +430,30 @@ class Problem:
         if self.cfg.geometry != "cube":
             from .cylinder import assemble_cylinder
             return assemble_cylinder(self, sd, with_face)
+        if len(sd.boxes) > 1:
+            # union of patch boxes: every box's K and loads in its own numbering, summed
+            # into the subdomain's (global edge ids in increasing order): the integrals
+            # over the union (torn assembly)
+            assert not with_face
+            gid_all = self.sub_edges[sd.idx]
+            n_all = len(gid_all)
+            K = None
+            j = np.zeros((n_all, self.cfg.nrhs))
+            for lo, hi in sd.boxes:
+                bx = Subdomain(sd.idx, lo, hi)
+                gb, mlb = self.grid.block_edges(lo, hi)
+                spaces = cube_spaces(self.cfg, bx)
+                C = local_curl(mlb)
+                Kb = (C.T @ cube_mass2(self.cfg, bx, spaces, self.nu) @ C).tocoo()
+                loc = np.searchsorted(gid_all, gb)
+                Kb = sp.csr_matrix((Kb.data, (loc[Kb.row], loc[Kb.col])), shape=(n_all, n_all))
+                K = Kb if K is None else K + Kb
+                np.add.at(j, loc, C.T @ cube_face_loads(self.cfg, bx, spaces))
+            m = sd.local_mask
+            K = K[m][:, m].tocsr()
+            K = ((K + K.T) * 0.5).tocsr()
+            K.sort_indices()
+            return K, np.ascontiguousarray(j[m])
         spaces = cube_spaces(self.cfg, sd)
         C = local_curl(sd.ml)
         M2 = cube_mass2(self.cfg, sd, spaces, self.nu)

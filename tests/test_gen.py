@@ -262,7 +262,7 @@ def test_cylinder_curl_grad_and_loads():
 
 # ---- the paper's 27-patch experiment family (R14) ----
 
-@pytest.mark.parametrize("tiling", ["311", "221", "321", "222", "322"])
+@pytest.mark.parametrize("tiling", ["311", "221", "321", "222", "322", "L3"])
 def test_paper_cube_ngp_independent_of_h_and_p(tiling):
     """n_gp depends on the subdomain configuration only, not on h or p (PAPER.md:180,
     :268 "n_gp is independent of h and p")."""
@@ -271,7 +271,40 @@ def test_paper_cube_ngp_independent_of_h_and_p(tiling):
     assert len(ngp) == 1, ngp
 
 
-@pytest.mark.parametrize("name", ["E27_221_p2_e2", "E27_322_p1_e2"])
+def test_paper_e1_partition_has_cross_points():
+    """E1's partition (three L-shaped 9-patch subdomains, ietigen.configs.PAPER_PARTS):
+    all three subdomains meet along one patch line, so the coarse problem is not empty
+    (n_gp > 0), unlike a 3 x 1 x 1 slab tiling (n_gp = 0); every subdomain has 9 patches
+    and is face-connected to the other two."""
+    from ietigen.problem import build
+    P = build(cf.get("E27_L3_p1_e2"))
+    assert P.counts()["n_gp"] > 0
+    assert sorted(len(sd.boxes) for sd in P.subs) == [9, 9, 9]
+    assert sorted(P.iface_pairs) == [(0, 1), (0, 2), (1, 2)]
+    assert build(cf.get("E27_311_p1_e2")).counts()["n_gp"] == 0
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_union_of_patches_assembly_gives_the_same_field(p):
+    """The union-of-patches assembly (L-shaped subdomains) against the single-box one: the
+    gauged solutions of E27_L3 and of the slab tiling E27_311 differ by a discrete
+    gradient (different trees), so their curls C a -- the flux B_h of PAPER.md:255 --
+    agree (to the solver's rounding); a wrong torn assembly on the unions would not."""
+    from oracle import brute
+    from ietigen.problem import build, local_curl
+    fields = []
+    for t in ("L3", "311"):
+        b, P = make_bundle(f"E27_{t}_p{p}_e2", with_problem=True)
+        _, a, _, _ = brute.monolithic_solve(b)
+        g = P.grid
+        x = np.zeros((g.ne, a.shape[1]))
+        x[P.gauged_edges] = a
+        gids, ml = g.block_edges((0, 0, 0), tuple(P.cfg.npatch))
+        fields.append(local_curl(ml) @ x[gids])
+    assert np.linalg.norm(fields[0] - fields[1]) <= 1e-9 * np.linalg.norm(fields[1])
+
+
+@pytest.mark.parametrize("name", ["E27_221_p2_e2", "E27_322_p1_e2", "E27_L3_p1_e2", "E27_L3_p2_e2"])
 def test_uneven_tiling_dd_equals_monolithic(name):
     """Uneven box tilings (3 patches cut 1 + 2): every K_rr SPD, the DD solution equals
     the monolithic gauged solve."""

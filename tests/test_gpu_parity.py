@@ -313,6 +313,26 @@ def test_condition_estimate_edge_cases(lib):
     assert lo[0] == hi[0] == k[0] == 0.0
 
 
+def test_paper_e1_partition(lib):
+    """E1's configuration (27 patches, N_sub = 3, here the L-shaped 9-patch
+    partition with a cross line, n_gp > 0), with the paper's stopping rule (the
+    preconditioned residual, eta_tol = 1e-6): iteration count within +-1 of
+    the oracle run with the same rule, lambda/u iteration-matched within 1e-8, and the
+    condition estimate in the range of the paper's Fig. 4 (1.5 .. 5.5)."""
+    b = make_bundle("E27_L3_p2_e4")
+    assert b["n_primal"] > 0
+    ref = dp.solve(b, stop="preconditioned")
+    s, lam, u, rep = gpu_solve(lib, b, stop="preconditioned")
+    assert abs(rep["iters"][0] - int(ref["iters"][0])) <= 1
+    nit = int(ref["iters"][0])
+    ref_f = dp.solve(b, fixed_iters=nit)
+    s, lam, u, rep = gpu_solve(lib, b, fixed_iters=nit)
+    assert rel(np.concatenate(u), np.concatenate(ref_f["u"])) <= 1e-8
+    lo, hi, k = s.estimate_condition()
+    print("E27_L3_p2_e4 iters", rep["iters"][0], "oracle", nit, "cond", k[0])
+    assert 1.5 <= k[0] <= 5.5
+
+
 @pytest.mark.parametrize("name", ["E27_322_p2_e2", "E27_221_p3_e2"])
 def test_paper_cube_family(lib, name):
     """The paper's 27-patch experiment family with uneven box tilings (PAPER.md:268,

@@ -2,10 +2,13 @@
 as trends: 27 cube patches, nu = 1, homogeneous manufactured A*
 (R14), PCG tolerance eta_tol = 1e-6.
 
-  E1: N_sub = 3 (slabs, tiling 3x1x1), p in {1,2,3}, e in {2,4,8} (h = 1/6, 1/12, 1/24)
+  E1: N_sub = 3 (three L-shaped 9-patch subdomains meeting along one patch line,
+      ietigen.configs.PAPER_PARTS["L3"]), p in {1,2,3}, e in {2,4,8} (h = 1/6, 1/12, 1/24)
   E2: h = 1/12 (e = 4), p in {1,2,3}, N_sub in {2,3,4,6,8,9,12} (box tilings)
 
-Per case: n_gp, m_r, N_iter, the Lanczos condition estimate of M_D^-1 F_DP
+Stopping rule: the preconditioned residual sqrt(r.z) <= eta_tol sqrt(r0.z0) (the
+paper's eta_tol; ietidp_options.stop). Per case: n_gp, m_r, N_iter, the
+Lanczos condition estimate of M_D^-1 F_DP
 (ietidp_estimate_condition), and the two bounds' arguments
 (1 + log(H/h))^2 (Eq. 11) and log10(p^2/h) (Eq. 12). GPU only (no oracle import);
 parity of this family is in tests/test_gpu_parity.py::test_paper_cube_family.
@@ -27,6 +30,9 @@ from ietigen.bundle import make_bundle  # noqa: E402
 from paper_2501_04340_b200 import ietidp  # noqa: E402
 
 E2_TILINGS = {2: "211", 3: "311", 4: "221", 6: "321", 8: "222", 9: "331", 12: "322"}
+# the paper's E1 fits (PAPER.md:354-356 cond = C (2 + log10(p^2/h))^2, :385-387 N_iter =
+# C (2 + log10(p^2/h))), per degree p: (C_cond, C_iter) -- context for the trend only
+PAPER_E1_FIT = {1: (0.33, 3.5), 2: (0.29, 3.2), 3: (0.27, 3.2)}
 
 
 def run(name):
@@ -34,7 +40,7 @@ def run(name):
     t0 = time.perf_counter()
     b = make_bundle(cfg)
     t_gen = time.perf_counter() - t0
-    s = ietidp.from_bundle(b)
+    s = ietidp.from_bundle(b, stop="preconditioned")
     s.factor()
     lam, rep = s.solve()
     s.factor()  # second run: timings without first-call set-up
@@ -44,9 +50,13 @@ def run(name):
     # subdomain size H in patches along its largest extent (patch side 1/3)
     T = cfg.tiling
     H = max(math.ceil(3 / T[a]) for a in range(3)) / 3.0
+    if cfg.parts is not None:  # the L-shaped parts span 2 patches across (x, y) and 3 in z
+        H = 1.0
     out = dict(name=name, p=cfg.p, e=cfg.e, h=h, n_sub=b["n_sub"], n_gp=b["n_primal"], m_r=b["n_lambda"],
                iters=rep["iters"][0], rel_residual=rep["rel_residual"][0], omega_min=lo[0], omega_max=hi[0],
                cond=k[0], bound11_arg=(1 + math.log(H / h)) ** 2, bound12_arg=math.log10(cfg.p ** 2 / h),
+               paper_fit_cond=None if cfg.parts is None else PAPER_E1_FIT[cfg.p][0] * (2.0 + math.log10(cfg.p ** 2 / h)) ** 2,
+               paper_fit_iters=None if cfg.parts is None else PAPER_E1_FIT[cfg.p][1] * (2.0 + math.log10(cfg.p ** 2 / h)),
                ms_factor=rep["ms_factor"], ms_pcg=rep["ms_pcg"], gen_s=t_gen)
     s.close()
     return out
@@ -55,13 +65,13 @@ def run(name):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--which", default="all")
-    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r01_experiments"))
+    ap.add_argument("--out", default=os.path.join(ROOT, "profiles", "r02_experiments"))
     a = ap.parse_args()
     rows = []
     if a.which in ("e1", "all"):
         for p in (1, 2, 3):
             for e in (2, 4, 8):
-                rows.append(dict(exp="E1", **run(f"E27_311_p{p}_e{e}")))
+                rows.append(dict(exp="E1", **run(f"E27_L3_p{p}_e{e}")))
                 print(json.dumps(rows[-1]), flush=True)
     if a.which in ("e2", "all"):
         for p in (1, 2, 3):
@@ -71,11 +81,13 @@ def main():
     with open(a.out + ".json", "w") as f:
         json.dump(rows, f, indent=1)
     with open(a.out + ".md", "w") as f:
-        f.write("| exp | case | p | h | N_sub | n_gp | m_r | N_iter | cond (Lanczos) | "
-                "(1+log H/h)^2 | log10(p^2/h) | factor ms | PCG ms |\n|" + "---|" * 13 + "\n")
+        f.write("| exp | case | p | h | N_sub | n_gp | m_r | N_iter | paper fit N_iter | cond (Lanczos) | "
+                "paper fit cond | (1+log H/h)^2 | log10(p^2/h) | factor ms | PCG ms |\n|" + "---|" * 15 + "\n")
         for r in rows:
+            pfi = "" if r["paper_fit_iters"] is None else f"{r['paper_fit_iters']:.1f}"
+            pfc = "" if r["paper_fit_cond"] is None else f"{r['paper_fit_cond']:.2f}"
             f.write(f"| {r['exp']} | {r['name']} | {r['p']} | 1/{round(1 / r['h'])} | {r['n_sub']} | {r['n_gp']} | "
-                    f"{r['m_r']} | {r['iters']} | {r['cond']:.3f} | {r['bound11_arg']:.2f} | "
+                    f"{r['m_r']} | {r['iters']} | {pfi} | {r['cond']:.3f} | {pfc} | {r['bound11_arg']:.2f} | "
                     f"{r['bound12_arg']:.2f} | {r['ms_factor']:.2f} | {r['ms_pcg']:.2f} |\n")
 
 
