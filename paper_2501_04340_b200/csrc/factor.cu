@@ -749,6 +749,9 @@ void run_factor(ietidp_s* h) {
   // compact POTRF by default (measured faster in the pipeline: the instruction cache is
   // cold at every launch); IETIDP_POTRF=unrolled selects the fully unrolled kernel
   static const bool potrf_compact = !(getenv("IETIDP_POTRF") && !strcmp(getenv("IETIDP_POTRF"), "unrolled"));
+  // experiments only (results meaningless): IETIDP_DBG_FACTOR bits skip launches: 1 POTRF,
+  // 2 panel updates, 4 TRSM, 8 SYRK / extend-add, 16 side-stream inverse and W_k
+  static const int dbgf = getenv("IETIDP_DBG_FACTOR") ? atoi(getenv("IETIDP_DBG_FACTOR")) : 0;
   // the forward sweep of the loads rides on the groups' side streams (one column chunk)
   h->fwd_in_factor = h->nrhs <= 16;
   if (expl) h->wtiles.zero(st);  // W_k is accumulated block row by block row
@@ -793,12 +796,12 @@ void run_factor(ietidp_s* h) {
         IETI_LAUNCHED_SIDE(h);
       }
       for (auto& pn : lp.panels) {
-        if (pn.upd_n) {
+        if (pn.upd_n && !(dbgf & 2)) {
           k_gemm<false><<<pn.upd_n, 128, GEMM_SMEM, sg>>>(GW + pn.upd_off, pool, pool, pool, rel, h->skws.p,
                                                            h->skcnt.p);
           IETI_LAUNCHED_SIDE(h);
         }
-        if (pn.potrf_n) {
+        if (pn.potrf_n && !(dbgf & 1)) {
           if (potrf_compact)
             k_potrf_c<<<pn.potrf_n, POTRF_T, 0, sg>>>(W + pn.potrf_off, h->d_sn.p, pool, h->dinv.p, h->err_flag.p);
           else
@@ -807,27 +810,27 @@ void run_factor(ietidp_s* h) {
         }
         cudaEvent_t pe = h->pev[npan++];
         IETI_CUDA(cudaEventRecord(pe, sg));
-        if (pn.trsm_n) {
+        if (pn.trsm_n && !(dbgf & 4)) {
           k_gemm<false><<<pn.trsm_n, 128, GEMM_SMEM, sg>>>(GW + pn.trsm_off, pool, h->dinv.p, pool, rel);
           IETI_LAUNCHED_SIDE(h);
         }
         // side stream: block row kp of L11^-1 (and of W_k) as soon as Dinv_kp exists
         if (pn.icopy_n || pn.ia_n || pn.ib_n || pn.wacc_n) IETI_CUDA(cudaStreamWaitEvent(s2, pe, 0));
-        if (pn.icopy_n) {
+        if (pn.icopy_n && !(dbgf & 16)) {
           k_inv_copy<<<pn.icopy_n, 256, 0, s2>>>(W + pn.icopy_off, h->d_sn.p, h->dinv.p, h->ipool.p);
           IETI_LAUNCHED_SIDE(h);
         }
-        if (pn.ia_n) {
+        if (pn.ia_n && !(dbgf & 16)) {
           k_gemm<true><<<pn.ia_n, 128, GEMM_SMEM, s2>>>(GW + pn.ia_off, pool, h->ipool.p, h->tpool.p, rel);
           IETI_LAUNCHED_SIDE(h);
         }
-        if (pn.ib_n) {
+        if (pn.ib_n && !(dbgf & 16)) {
           k_gemm<true><<<pn.ib_n, 128, GEMM_SMEM, s2>>>(GW + pn.ib_off, h->dinv.p, h->tpool.p, h->ipool.p, rel);
           IETI_LAUNCHED_SIDE(h);
         }
         if (&pn == &lp.panels.back()) {
           wacc_last = pn.wacc_n ? &pn : nullptr;  // after the level's forward sweep (not on the path)
-        } else if (pn.wacc_n) {
+        } else if (pn.wacc_n && !(dbgf & 16)) {
           k_gemm<true, true><<<pn.wacc_n, 128, GEMM_SMEM, s2>>>(GW + pn.wacc_off, h->ipool.p, h->ipool.p,
                                                                 h->wtiles.p, rel);
           IETI_LAUNCHED_SIDE(h);
@@ -836,6 +839,7 @@ void run_factor(ietidp_s* h) {
       IETI_CUDA(cudaEventRecord(gevent(g, L), sg));
       if (L == 0) IETI_CUDA(cudaStreamWaitEvent(sg, gevent(g, nlev + 1), 0));  // parents assembled
       for (auto& sy : lp.syrk) {
+        if (dbgf & 8) break;
         k_gemm<false><<<sy.second, 128, GEMM_SMEM, sg>>>(GW + sy.first, pool, pool, pool, rel);
         IETI_LAUNCHED_SIDE(h);
       }
@@ -847,7 +851,7 @@ void run_factor(ietidp_s* h) {
       }
       for (size_t r = 0; r < lp.inv_rounds.size(); ++r) {
         const auto& rg = lp.inv_rounds[r];
-        if (!rg.second) continue;
+        if (!rg.second || (dbgf & 16)) continue;
         const bool step1 = (r % 2) == 0;
         k_gemm<true><<<rg.second, 128, GEMM_SMEM, s2>>>(GW + rg.first, step1 ? pool : h->ipool.p,
                                                         step1 ? h->ipool.p : h->tpool.p,
@@ -855,7 +859,7 @@ void run_factor(ietidp_s* h) {
         IETI_LAUNCHED_SIDE(h);
       }
       if (h->fwd_in_factor) fwd_sweep_lp(h, h->Xf.p, lp, s2);
-      if (wacc_last) {
+      if (wacc_last && !(dbgf & 16)) {
         k_gemm<true, true><<<wacc_last->wacc_n, 128, GEMM_SMEM, s2>>>(GW + wacc_last->wacc_off, h->ipool.p,
                                                                       h->ipool.p, h->wtiles.p, rel);
         IETI_LAUNCHED_SIDE(h);
