@@ -14,6 +14,8 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <memory>
+#include <mutex>
 #include <numeric>
 #include <set>
 #include <thread>
@@ -365,7 +367,36 @@ struct NestedDissection {
   }
 };
 
-LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf) {
+// Orderings of r_V shared between subdomains whose K_VV graphs are identical (a box
+// tiling's subdomains differ only in their interface rows: C5's 27 pattern classes share
+// one r_V graph): computed once per distinct graph (fingerprint, then a full comparison).
+struct OrderCache {
+  struct Entry {
+    std::once_flag once;
+    std::vector<int> xadj, adj;
+    std::vector<std::vector<int>> sn_vars;
+  };
+  std::mutex mu;
+  std::unordered_map<uint64_t, std::shared_ptr<Entry>> map;
+};
+
+static uint64_t graph_fingerprint(const std::vector<int>& xadj, const std::vector<int>& adj) {
+  uint64_t x = 1469598103934665603ull;
+  auto mix = [&](const std::vector<int>& v) {
+    x = (x ^ (uint64_t)v.size()) * 0x9E3779B97F4A7C15ull;
+    for (size_t i = 0; i + 1 < v.size(); i += 2) {
+      const uint64_t w = (uint64_t)(uint32_t)v[i] | ((uint64_t)(uint32_t)v[i + 1] << 32);
+      x = (x ^ w) * 0x9E3779B97F4A7C15ull;
+      x ^= x >> 29;
+    }
+    if (v.size() & 1) x = (x ^ (uint64_t)(uint32_t)v.back()) * 1099511628211ull;
+  };
+  mix(xadj);
+  mix(adj);
+  return x;
+}
+
+LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf, OrderCache* cache = nullptr) {
   LocalResult R;
   SubPlan& sp = R.sp;
   const int n = in.n;
@@ -416,8 +447,10 @@ LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf) {
     xadj[a + 1] = (int)adj.size();
   }
 
+  const auto ta0 = std::chrono::steady_clock::now();
   // ---- ordering of r_V: supernode tree in postorder ----
   std::vector<std::vector<int>> sn_vars;
+  auto compute_order = [&](std::vector<std::vector<int>>& sn_vars) {
   if (sp.nV > 0) {
     std::vector<int> all(sp.nV);
     std::iota(all.begin(), all.end(), 0);
@@ -447,6 +480,26 @@ LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf) {
         }
       }
     }
+  }
+  };
+  if (cache && sp.nV > 0) {
+    const uint64_t fp = graph_fingerprint(xadj, adj) ^ ((uint64_t)ordering << 56) ^ ((uint64_t)leaf << 40);
+    std::shared_ptr<OrderCache::Entry> ent;
+    {
+      std::lock_guard<std::mutex> lk(cache->mu);
+      auto& slot = cache->map[fp];
+      if (!slot) slot = std::make_shared<OrderCache::Entry>();
+      ent = slot;
+    }
+    std::call_once(ent->once, [&]() {
+      ent->xadj = xadj;
+      ent->adj = adj;
+      compute_order(ent->sn_vars);
+    });
+    if (ent->xadj == xadj && ent->adj == adj) sn_vars = ent->sn_vars;
+    else compute_order(sn_vars);  // fingerprint collision: not shared
+  } else {
+    compute_order(sn_vars);
   }
   // ---- positions: r_V (ND), r_I, P ----
   sp.perm.resize(ne);
@@ -479,6 +532,7 @@ LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf) {
   if (sp.nI > 0) sp.root = add_sn(rI, 0);
   if (sp.nP > 0) sp.pnode = add_sn(std::vector<int>(in.prim.begin(), in.prim.end()), 1);
 
+  const auto ta1 = std::chrono::steady_clock::now();
   // ---- symbolic factorisation: row structure of every supernode ----
   std::vector<int> mark(ne, -1);
   for (size_t s = 0; s < R.sn.size(); ++s) {
@@ -511,6 +565,12 @@ LocalResult analyze_sub(const SubIn& in, int k, int ordering, int leaf) {
     int lv = 0;
     for (int c : h.children) lv = std::max(lv, R.sn[c].level + 1);
     h.level = lv;
+  }
+  if (getenv("IETIDP_ANALYZE_PROF")) {
+    const auto ta2 = std::chrono::steady_clock::now();
+    fprintf(stderr, "analyze_sub %d: n %d nV %d nI %d nnz %lld: ordering %.2f ms, symbolic %.2f ms\n", k, n, sp.nV,
+            sp.nI, (long long)in.rowptr[n], std::chrono::duration<double, std::milli>(ta1 - ta0).count(),
+            std::chrono::duration<double, std::milli>(ta2 - ta1).count());
   }
   return R;
 }
@@ -632,9 +692,10 @@ void analyze_all(ietidp_s* h) {
 
   // ---- per-subdomain analysis (one per pattern class), in parallel ----
   std::vector<LocalResult> loc(ns);
+  OrderCache ocache;
   parallel_for((int)reps.size(), [&](int i) {
     const int k = reps[i];
-    loc[k] = analyze_sub(h->in[k], k, h->opt.ordering, h->opt.leaf_size);
+    loc[k] = analyze_sub(h->in[k], k, h->opt.ordering, h->opt.leaf_size, &ocache);
   });
   for (int k : reps)
     if (loc[k].st != IETIDP_OK) throw Error(loc[k].st, loc[k].err);
