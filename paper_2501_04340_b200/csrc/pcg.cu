@@ -766,7 +766,9 @@ __device__ __forceinline__ void sym_stream(const TmvArgs& A, const int* items, i
 // accumulator) while the T warps form the coarse partial G_k[rows o]^T x_o of the F-apply.
 // The warps are not synchronised per tile: each releases a ring slot when it is done with
 // it (the last of the eight issues the slot's next copy), and T warp q waits for N warp q
-// only at a diagonal (a release/acquire counter), before it touches the block just stored.
+// (a release/acquire counter of its diagonals) only before its first tile (o', j) of a
+// block j whose row lies in the chunk, so it runs on into the next row while the N warps
+// finish a diagonal.
 // At the end of the chunk every block j <= o_b is written once as the chunk's partial
 // block (then zeroed); the gathers sum the (typically 1-3) partial blocks of a slot in
 // chunk order (deterministic).
@@ -959,9 +961,28 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
     // counter diag[q]) before it touches the block the N warp has just stored.
     double acc[2][2][2] = {};
     unsigned ndiag = ctl->diag[q4];  // diagonals of this quadrant so far (the warps are in step here)
+    const unsigned ndiag0 = ndiag;
     unsigned tr[2][8];
     int preb = -1;  // T warps: block whose accumulator load (tr) is in flight
     int o = tri_row(C.t0), j = C.t0 - o * (o + 1) / 2;
+    // T warps: block j >= o0 starts from N warp q's diagonal store (row j of this chunk);
+    // blocks below o0 start from zero. synced = the highest block already waited for.
+    const int o0 = o;
+    int synced = o0 - 1;
+    auto wait_block = [&](int jb) {  // N warp q has stored block jb (diagonal jb of the chunk)
+      if (jb <= synced) return;
+      const unsigned want = ndiag0 + (unsigned)(jb - o0 + 1);
+      unsigned have;
+      do {
+        asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n"
+                     : "=r"(have)
+                     : "r"((unsigned)__cvta_generic_to_shared(&ctl->diag[q4]))
+                     : "memory");
+      } while ((int)(have - want) < 0);
+      __syncwarp();
+      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+      synced = jb;
+    };
     for (int t = C.t0; t < C.t1; ++t, ++i) {
       const unsigned s = (base + i) % STAGES;
       mbar_wait(&ctl->full[s], ((base + i) / STAGES) & 1);
@@ -998,6 +1019,7 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
           for (int e = 0; e < 8; ++e) acc[e >> 2][(e >> 1) & 1][e & 1] = 0.0;
         }
       } else if (j < o) {  // T: S_oj^T x_o onto block j's accumulator
+        if (preb != j) wait_block(j);
         if (preb != j && !(A.dbg & 4)) {
           tm_ld8_issue(tq + 16 * j, tr[0]);
           tm_ld8_issue(tq + 16 * j + 8, tr[1]);
@@ -1026,7 +1048,7 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
         tm_st8(tq + 16 * j + 8, pt[1]);
         }
         preb = -1;
-        if (j + 1 < o && t + 1 < C.t1 && !(A.dbg & 4)) {  // the next tile's block, in flight across the release
+        if (j + 1 < o && j + 1 <= synced && t + 1 < C.t1 && !(A.dbg & 4)) {  // the next tile's block, in flight
           tm_ld8_issue(tq + 16 * (j + 1), tr[0]);
           tm_ld8_issue(tq + 16 * (j + 1) + 8, tr[1]);
           preb = j + 1;
@@ -1059,19 +1081,10 @@ __device__ __forceinline__ void sym_chunks(const TmvArgs& A, const SymChunk* ch,
           if (t + 1 < C.t1) stage_g(o + 1, tt, 128);
           asm volatile("bar.sync 5, 128;\n" ::: "memory");  // G rows of row o + 1 staged
         }
-        {  // N warp q has stored block o (its diagonal count reaches this one's)
-          const unsigned want = ++ndiag;
-          unsigned have;
-          do {
-            asm volatile("ld.acquire.cta.shared::cta.u32 %0, [%1];\n"
-                         : "=r"(have)
-                         : "r"((unsigned)__cvta_generic_to_shared(&ctl->diag[q4]))
-                         : "memory");
-          } while ((int)(have - want) < 0);
-        }
-        __syncwarp();
-        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        if (t + 1 < C.t1) {  // the next tile is (o + 1, 0)
+        // no wait here: block o is needed only at tile (o + 1, o), the last of the next
+        // row (wait_block), so the T warps run on into row o + 1 while the N warps finish
+        // the diagonal
+        if (t + 1 < C.t1 && 0 <= synced) {  // the next tile is (o + 1, 0)
           tm_ld8_issue(tq, tr[0]);
           tm_ld8_issue(tq + 8, tr[1]);
           preb = 0;
