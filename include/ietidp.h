@@ -176,6 +176,17 @@ ietidp_status ietidp_analyze(ietidp_t h);
  * have arrived, so the transfer overlaps the factorisation of earlier groups. */
 ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const double* f);
 
+/* The same with half the bytes: K_lower_val holds only the values of the stored entries
+ * (i, j) with j <= i of subdomain k's CSR pattern, in CSR order (row by row, columns
+ * ascending) -- K is symmetric (K = C^T M_2 C), so an upper entry's value is its
+ * mirror's. The library expands them on the device into its full CSR value array
+ * (k_expand_lower). Copy semantics as for ietidp_set_values: asynchronous on the copy
+ * stream, ordered before the next ietidp_factor; the caller's buffers must stay
+ * unchanged until that factorisation returns. The first call builds the per-pattern-class
+ * maps (host integer work, once per handle). Either pointer may be NULL (keep).
+ * Errors: E_STATE (before analysis, host-only handle), E_ARG (k out of range), E_CUDA. */
+ietidp_status ietidp_set_values_lower(ietidp_t h, int k, const double* K_lower_val, const double* f);
+
 /* Device numeric phase: batched supernodal Cholesky of every K_rr^(k)
  * (its trailing block is L_II, L_II L_II^T = S_{r_I r_I} of Eq. (10)),
  * coarse basis X_k = K_rr^-1 K_rP, S_PP and its factorisation, G, and d_DP.

@@ -688,6 +688,7 @@ void analyze_all(ietidp_s* h) {
   for (int k = 0; k < ns; ++k)
     if (rep[k] == k) reps.push_back(k);
   h->n_pattern_classes = (int)reps.size();
+  h->class_rep = rep;
   stage("pattern classes");
 
   // ---- per-subdomain analysis (one per pattern class), in parallel ----

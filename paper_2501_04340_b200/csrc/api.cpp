@@ -270,6 +270,76 @@ ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const do
   });
 }
 
+// the lower-triangle maps of every pattern class (host integer work, once)
+static void prepare_lower(ietidp_t h) {
+  const int ns = h->n_sub;
+  h->low_off.assign(ns + 1, 0);
+  h->low_n.assign(ns, 0);
+  h->low_map_off.assign(ns, -1);
+  std::vector<int> map;
+  for (int k = 0; k < ns; ++k) {
+    const ieti::SubIn& in = h->in[k];
+    long long nl = 0;
+    for (int i = 0; i < in.n; ++i)
+      for (int64_t e = in.rowptr[i]; e < in.rowptr[i + 1]; ++e) nl += in.col[e] <= i;
+    h->low_n[k] = nl;
+    h->low_off[k + 1] = h->low_off[k] + nl;
+    const int r = h->class_rep[k];
+    if (h->low_map_off[r] >= 0) continue;
+    h->low_map_off[r] = (long long)map.size();
+    const ieti::SubIn& rin = h->in[r];
+    const size_t base = map.size();
+    map.resize(base + rin.col.size());
+    // lower index of the entries of row i: lowstart[i] + (e - rowptr[i]) for col <= i;
+    // an upper entry (i, j) is the next unvisited lower entry of row j (cursor nx[j])
+    std::vector<long long> lowstart(rin.n + 1, 0);
+    for (int i = 0; i < rin.n; ++i) {
+      long long c = 0;
+      for (int64_t e = rin.rowptr[i]; e < rin.rowptr[i + 1]; ++e) c += rin.col[e] <= i;
+      lowstart[i + 1] = lowstart[i] + c;
+    }
+    std::vector<int64_t> nx(rin.rowptr.begin(), rin.rowptr.end() - 1);
+    for (int i = 0; i < rin.n; ++i)
+      for (int64_t e = rin.rowptr[i]; e < rin.rowptr[i + 1]; ++e) {
+        const int j = rin.col[e];
+        if (j <= i) {
+          map[base + e] = (int)(lowstart[i] + (e - rin.rowptr[i]));
+        } else {
+          const int64_t q = nx[j]++;  // (j, i): the pattern is symmetric (checked at set_subdomain)
+          map[base + e] = (int)(lowstart[j] + (q - rin.rowptr[j]));
+        }
+      }
+  }
+  set_device(h);
+  h->low_map.upload(map, h->stream);
+  h->klow.alloc(std::max<long long>(1, h->low_off[ns]));
+  IETI_CUDA(cudaStreamSynchronize(h->stream));
+  h->lower_ready = true;
+}
+
+ietidp_status ietidp_set_values_lower(ietidp_t h, int k, const double* K_lower_val, const double* f) {
+  return guard(h, [&]() {
+    require(h->analyzed, IETIDP_E_STATE, "set_values_lower before analysis");
+    require(k >= 0 && k < h->n_sub, IETIDP_E_ARG, "subdomain index out of range");
+    require(h->cstream != nullptr, IETIDP_E_STATE, "set_values_lower on a host-only handle");
+    if (!h->lower_ready) prepare_lower(h);
+    const ieti::SubIn& in = h->in[k];
+    IETI_CUDA(cudaEventRecord(h->hp_ev_set, h->stream));  // after the caller's prior work
+    IETI_CUDA(cudaStreamWaitEvent(h->cstream, h->hp_ev_set, 0));
+    if (K_lower_val) {
+      IETI_CUDA(cudaMemcpyAsync(h->klow.p + h->low_off[k], K_lower_val, h->low_n[k] * sizeof(double),
+                                cudaMemcpyHostToDevice, h->cstream));
+      ieti::launch_expand_lower(h, k, h->cstream);
+    }
+    if (f)
+      IETI_CUDA(cudaMemcpyAsync(h->fval.p + h->fval_off[k], f, (size_t)in.n * h->nrhs * sizeof(double),
+                                cudaMemcpyHostToDevice, h->cstream));
+    IETI_CUDA(cudaEventRecord(h->kev[k], h->cstream));
+    h->factored = false;
+    h->solved = false;
+  });
+}
+
 ietidp_status ietidp_factor(ietidp_t h) {
   if (h && !h->analyzed) {
     ietidp_status st = ietidp_analyze(h);

@@ -84,6 +84,21 @@ void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::
   IETI_CUDA(cudaStreamSynchronize(s));  // the temporaries are freed on return
 }
 
+// ietidp_set_values_lower: a subdomain's full CSR values from its lower-triangle list
+// (the mirror's value for an upper entry; the pattern is symmetric, the values are)
+__global__ void __launch_bounds__(256) k_expand_lower(long long nnz, const int* __restrict__ map,
+                                                     const double* __restrict__ low, double* __restrict__ full) {
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < nnz; e += (long long)gridDim.x * blockDim.x)
+    full[e] = low[map[e]];
+}
+void launch_expand_lower(ietidp_s* h, int k, cudaStream_t st) {
+  const long long nnz = (long long)h->in[k].val.size();
+  if (!nnz) return;
+  k_expand_lower<<<grid_for(nnz, 256), 256, 0, st>>>(nnz, h->low_map.p + h->low_map_off[h->class_rep[k]],
+                                                     h->klow.p + h->low_off[k], h->kval.p + h->kval_off[k]);
+  IETI_LAUNCHED_SIDE(h);
+}
+
 __global__ void k_init_flags(int* err) {
   if (threadIdx.x == 0) {
     err[0] = INT_MAX;

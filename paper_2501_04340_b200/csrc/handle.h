@@ -184,6 +184,15 @@ struct ietidp_s {
   // several-RHS chunk pass of the persistent PCG (pcg.cu sym_chunks), planned for a grid
   int chunk_grid = 0;
   int n_pattern_classes = 0;  // distinct subdomain patterns found by the analysis
+  std::vector<int> class_rep;  // per subdomain: the representative of its pattern class
+  // ietidp_set_values_lower: per pattern class, full CSR entry -> index of its value in the
+  // lower-triangle list (the entry itself if j <= i, else its mirror (j, i)); built and
+  // uploaded at the first call
+  bool lower_ready = false;
+  std::vector<long long> low_off, low_map_off;  // per subdomain: lower values offset; per class rep: map offset
+  std::vector<long long> low_n;                 // per subdomain: number of lower entries
+  ieti::DevBuf<int> low_map;
+  ieti::DevBuf<double> klow;
   ieti::DevBuf<int> chunk_ptr, chunk_cfirst;
   ieti::DevBuf<ieti::SymChunk> chunk_list;
   ieti::DevBuf<long long> chunk_cpb;
@@ -234,6 +243,7 @@ struct ClassRel {
   long long base;
   const std::vector<int>*off, *sl, *src;
 };
+void launch_expand_lower(ietidp_s* h, int k, cudaStream_t st);  // factor.cu (ietidp_set_values_lower)
 void expand_scatter(ietidp_s* h, const std::vector<ExpandSeg>& segs, const std::vector<ClassRel>& cls, long long nrel,
                     long long nK, long long nF);
 void run_factor(ietidp_s* h);                  // factor.cu

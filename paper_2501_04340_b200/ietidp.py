@@ -24,7 +24,7 @@ STOP = {"residual": 0, "preconditioned": 1}
 
 # every entry point include/ietidp.h declares
 SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "ietidp_analyze",
-           "ietidp_set_values", "ietidp_factor", "ietidp_solve", "ietidp_get_u", "ietidp_get_u_device",
+           "ietidp_set_values", "ietidp_set_values_lower", "ietidp_factor", "ietidp_solve", "ietidp_get_u", "ietidp_get_u_device",
            "ietidp_get_lambda_device", "ietidp_apply_F", "ietidp_apply_precond", "ietidp_get_coarse",
            "ietidp_estimate_condition", "ietidp_get_pcg_coefficients", "ietidp_get_rhs", "ietidp_get_report", "ietidp_kernel_launches", "ietidp_last_error",
            "ietidp_status_string", "ietidp_destroy"]
@@ -77,6 +77,7 @@ def load():
         "ietidp_set_subdomain": (I, [P, I, I, P, P, P, P, I, P, P, P, I, P, I, P, P]),
         "ietidp_analyze": (I, [P]),
         "ietidp_set_values": (I, [P, I, P, P]),
+        "ietidp_set_values_lower": (I, [P, I, P, P]),
         "ietidp_factor": (I, [P]),
         "ietidp_solve": (I, [P, P, C.POINTER(Report)]),
         "ietidp_get_u": (I, [P, I, P]),
@@ -161,6 +162,13 @@ class Solver:
         v = None if K_data is None else np.ascontiguousarray(K_data, np.float64)
         ff = None if f is None else np.ascontiguousarray(f, np.float64)
         self._check(self.lib.ietidp_set_values(self.h, k, _ptr(v), _ptr(ff)))
+
+    def set_values_lower(self, k, K_lower=None, f=None):
+        """Values of the lower-triangle entries (j <= i) of subdomain k's CSR pattern, in
+        CSR order (ietidp_set_values_lower: half the bytes of set_values)."""
+        v = None if K_lower is None else np.ascontiguousarray(K_lower, np.float64)
+        ff = None if f is None else np.ascontiguousarray(f, np.float64)
+        self._check(self.lib.ietidp_set_values_lower(self.h, k, _ptr(v), _ptr(ff)))
 
     def factor(self):
         self._check(self.lib.ietidp_factor(self.h))

@@ -364,6 +364,41 @@ def test_fold_multi_bitwise(lib, monkeypatch):
     assert np.array_equal(lam0, lam1) and np.array_equal(u0, t.get_u(5))
 
 
+def lower_values(sd):
+    """The lower-triangle (j <= i) values of a subdomain's CSR, in CSR order."""
+    ip, ix = sd["K_indptr"], sd["K_indices"]
+    rows = np.repeat(np.arange(len(ip) - 1), np.diff(ip))
+    return np.ascontiguousarray(sd["K_data"][ix <= rows])
+
+
+@pytest.mark.parametrize("name", ["C2r", "C5r"])
+def test_set_values_lower_bitwise(lib, name):
+    """ietidp_set_values_lower (half the bytes) gives bit for bit the factorisation and
+    solution of ietidp_set_values with the same (symmetric) values: the device expands
+    the lower list into the full CSR values exactly. New values (K_k scaled by
+    1 + (k mod 3), loads by 2) so the expansion, not the analysis upload, is used."""
+    import copy
+    b, _ = case(name)
+    b2 = copy.deepcopy(b)
+    for k, sd in enumerate(b2["subs"]):
+        sd["K_data"] = sd["K_data"] * (1.0 + (k % 3))
+        sd["f"] = sd["f"] * 2.0
+    out = []
+    for mode in ("full", "lower"):
+        s = lib.from_bundle(b)
+        s.factor()
+        for k, sd in enumerate(b2["subs"]):
+            if mode == "full":
+                s.set_values(k, sd["K_data"], sd["f"])
+            else:
+                s.set_values_lower(k, lower_values(sd), sd["f"])
+        s.factor()
+        lam, rep = s.solve()
+        out.append((lam, np.concatenate([s.get_u(k) for k in range(b["n_sub"])]), rep["iters"]))
+    assert np.array_equal(out[0][0], out[1][0]) and np.array_equal(out[0][1], out[1][1])
+    assert out[0][2] == out[1][2]
+
+
 @pytest.mark.parametrize("pinned", [False, True])
 def test_set_values_then_refactor(lib, pinned):
     """analyze -> factor -> set_values(new K, f) -> factor -> solve (the e2e loop of
