@@ -39,6 +39,7 @@ def parse():
     ap.add_argument("--fapply-iters", type=int, default=200)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-pre", action="store_true", help="skip the device pre-processing (f1) measurement")
     return ap.parse_args()
 
 
@@ -316,6 +317,40 @@ def measure_dgemm_tflops(torch, dev):
     return 2 * n ** 3 / (best * 1e-3) / 1e12
 
 
+def measure_pre(ietidp, prob, device, nsamp=8):
+    """Device pre-processing (include/ietidp_pre.h) on the same workload,
+    outside the timed solve: the tree-cotree gauge of the whole control graph and the
+    assembly K = C^T M_2 C, j = C^T t of a sample of subdomains (device times from the
+    library's CUDA events, second call of each)."""
+    from ietigen import predesc
+    g = predesc.gauge_desc(prob)
+    for _ in range(2):
+        tree, prim, g_ms = ietidp.pre_gauge(g["nv"], g["ne"], g["eu"], g["ev"], g["w"], device=device)
+    ns = len(prob.subs)
+    subs = [sd for sd in prob.subs if len(sd.boxes) == 1]
+    subs = [subs[i] for i in sorted(set(int(round(i * (len(subs) - 1) / max(nsamp - 1, 1))) for i in range(nsamp)))] if subs else []
+    ms = ms_fill = 0.0
+    nnz = 0
+    wall = 0.0
+    for sd in subs:
+        d = predesc.subdomain_desc(prob, sd)
+        for _ in range(2):
+            t0 = time.perf_counter()
+            out = ietidp.pre_assemble(d, device=device)
+            w = time.perf_counter() - t0
+        ms += out["ms"]
+        ms_fill += out["ms_fill"]
+        nnz += len(out["K_data"])
+        wall += w
+    return {"gauge_ms": g_ms, "graph": {"nv": int(g["nv"]), "ne": int(g["ne"])},
+            "tree_matches_generator": bool(np.array_equal(tree, prob.tree)),
+            "assembly": {"subdomains_sampled": len(subs), "of": ns, "nnz": int(nnz), "device_ms": ms,
+                         "fill_kernel_ms": ms_fill, "wall_ms_with_copies": wall * 1e3,
+                         "fill_gb_s": (nnz * 12 / (ms_fill * 1e-3) / 1e9) if ms_fill else None,
+                         "note": "k_rows<1> writes 12 B per CSR entry (value + column): HBM-write bound at "
+                                 "scale; one launch per subdomain here, so launch- and latency-bound"}}
+
+
 def run_ours(args, rank, world, local):
     import torch
     from ietigen.bundle import make_bundle
@@ -323,7 +358,7 @@ def run_ours(args, rank, world, local):
 
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    b = make_bundle(args.config)
+    b, prob = make_bundle(args.config, with_problem=True)
     stream = torch.cuda.Stream(device=dev)
     t0 = time.perf_counter()
     S = ietidp.from_bundle(b, device=local, stream=stream.cuda_stream)
@@ -428,6 +463,7 @@ def run_ours(args, rank, world, local):
                                              "validation/copies) and the symbolic analysis"}}
 
         fp64_peak = measure_dgemm_tflops(torch, dev) if rank == 0 else None
+        pre = measure_pre(ietidp, prob, local) if (rank == 0 and not args.no_pre) else None
 
     if rank != 0:
         return
@@ -516,7 +552,7 @@ def run_ours(args, rank, world, local):
                         % (rep["f_apply_bytes"] / 1e6),
         "roofline": roofline, "rooflines": {"factor": roof_fac, "pcg": roof_pcg},
         "fp64_dgemm_tflops": fp64_peak, "clocks": clk.summary(), "gpu_launches": int(launches),
-        "e2e": e2e, "cpu_baseline": cpu,
+        "e2e": e2e, "cpu_baseline": cpu, "pre": pre,
         "symbolic": {"n_supernodes": rep["n_supernodes"], "n_levels": rep["n_levels"], "max_front": rep["max_front"],
                      "nnz_L": rep["nnz_L"], "factor_flops": rep["factor_flops"]},
         "wall_s": t_wall,

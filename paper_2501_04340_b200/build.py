@@ -16,7 +16,7 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-std=c++17", "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 CUFLAGS = ARCH + ["-lineinfo", "--expt-relaxed-constexpr", "-Xptxas", "-v"]
-SOURCES = ["api.cpp", "analyze.cpp", "factor.cu", "sweep.cu", "coarse.cu", "pcg.cu"]
+SOURCES = ["api.cpp", "analyze.cpp", "factor.cu", "sweep.cu", "coarse.cu", "pcg.cu", "pre.cu"]
 HEADERS = ["impl.h", "handle.h", "common.cuh"]
 
 
@@ -30,7 +30,7 @@ def _newer(src, obj, deps):
 def _compile(src):
     path = os.path.join(CSRC, src)
     obj = os.path.join(OBJ, src + ".o")
-    deps = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", "ietidp.h")]
+    deps = [os.path.join(CSRC, h) for h in HEADERS] + [os.path.join(ROOT, "include", h) for h in ("ietidp.h", "ietidp_pre.h")]
     if not _newer(path, obj, deps):
         return obj, ""
     flags = COMMON + (CUFLAGS if src.endswith(".cu") else ["-x", "c++"])

@@ -28,6 +28,9 @@ SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "i
            "ietidp_get_lambda_device", "ietidp_apply_F", "ietidp_apply_precond", "ietidp_get_coarse",
            "ietidp_estimate_condition", "ietidp_get_pcg_coefficients", "ietidp_get_rhs", "ietidp_get_report", "ietidp_kernel_launches", "ietidp_last_error",
            "ietidp_status_string", "ietidp_destroy"]
+# every entry point include/ietidp_pre.h declares (device pre-processing)
+PRE_SYMBOLS = ["ietidp_pre_assemble", "ietidp_pre_sizes", "ietidp_pre_get", "ietidp_pre_get_gram",
+               "ietidp_pre_last_error", "ietidp_pre_destroy", "ietidp_pre_gauge"]
 
 
 class Options(C.Structure):
@@ -35,6 +38,16 @@ class Options(C.Structure):
                 ("ordering", C.c_int), ("leaf_size", C.c_int), ("loop", C.c_int), ("stop", C.c_int),
                 ("device", C.c_int),
                 ("stream", C.c_void_p)]
+
+
+class PreSubdomain(C.Structure):
+    """ietidp_pre_subdomain (include/ietidp_pre.h)."""
+    _fields_ = [("p", C.c_int), ("e", C.c_int), ("npatch", C.c_int * 3), ("knots", C.c_void_p * 3),
+                ("nq", C.c_int), ("qx", C.c_void_p * 3), ("qw", (C.c_void_p * 3) * 3), ("nu", C.c_void_p),
+                ("dof_of_edge", C.c_void_p), ("n_dof", C.c_int), ("nrhs", C.c_int), ("lq", C.c_int),
+                ("lx", C.c_void_p * 3), ("nfac", C.c_int * 3), ("fac_kind", C.c_void_p * 3),
+                ("fac_val", C.c_void_p * 3), ("nterms", C.c_int), ("term_col", C.c_void_p),
+                ("term_comp", C.c_void_p), ("term_fac", C.c_void_p), ("term_coef", C.c_void_p)]
 
 
 class Report(C.Structure):
@@ -94,6 +107,13 @@ def load():
         "ietidp_last_error": (C.c_char_p, [P]),
         "ietidp_status_string": (C.c_char_p, [I]),
         "ietidp_destroy": (None, [P]),
+        "ietidp_pre_assemble": (I, [I, C.POINTER(PreSubdomain), C.POINTER(P)]),
+        "ietidp_pre_sizes": (I, [P, C.POINTER(I), C.POINTER(C.c_int64), C.POINTER(D), C.POINTER(D)]),
+        "ietidp_pre_get": (I, [P, P, P, P, P]),
+        "ietidp_pre_get_gram": (I, [P, I, I, I, P, C.POINTER(I)]),
+        "ietidp_pre_last_error": (C.c_char_p, []),
+        "ietidp_pre_destroy": (None, [P]),
+        "ietidp_pre_gauge": (I, [I, C.c_int64, C.c_int64, P, P, P, P, P, C.POINTER(D)]),
     }
     for name, (res, args) in sig.items():
         fn = getattr(lib, name)
@@ -272,3 +292,81 @@ def from_bundle(b, **opts):
         s.set_subdomain(k, sd["K_indptr"], sd["K_indices"], sd["K_data"], sd["f"], sd["B_lambda"], sd["B_dof"],
                         sd["B_sign"], sd["tree"], sd["prim"], sd["prim_gid"])
     return s
+
+
+# ---- device pre-processing (include/ietidp_pre.h): marshalling only ----
+
+def _pre_check(lib, st):
+    if st != OK:
+        raise IetiError(st, lib.ietidp_pre_last_error().decode())
+
+
+def pre_assemble(desc, device=0, want_gram=False):
+    """ietidp_pre_assemble + ietidp_pre_get for one box subdomain described by plain arrays
+    (ietigen.predesc.subdomain_desc). Returns dict(K_indptr, K_indices, K_data, f (nrhs, n),
+    ms [, gram])."""
+    lib = load()
+    keep = []
+
+    def arr(a, dt):
+        a = np.ascontiguousarray(a, dt)
+        keep.append(a)
+        return a.ctypes.data if a.size else None
+
+    s = PreSubdomain()
+    s.p, s.e, s.nq, s.n_dof, s.nrhs, s.lq = desc["p"], desc["e"], desc["nq"], desc["n_dof"], desc["nrhs"], desc["lq"]
+    for a in range(3):
+        s.npatch[a] = desc["npatch"][a]
+        s.knots[a] = arr(desc["knots"][a], np.float64)
+        s.qx[a] = arr(desc["qx"][a], np.float64)
+        s.lx[a] = arr(desc["lx"][a], np.float64)
+        s.nfac[a] = len(desc["fac_kind"][a])
+        s.fac_kind[a] = arr(desc["fac_kind"][a], np.int32)
+        s.fac_val[a] = arr(desc["fac_val"][a], np.float64)
+        for c in range(3):
+            s.qw[c][a] = arr(desc["qw"][c][a], np.float64)
+    s.nu = arr(desc["nu"], np.float64)
+    s.dof_of_edge = arr(desc["dof_of_edge"], np.int32)
+    s.nterms = len(desc["term_coef"])
+    s.term_col = arr(desc["term_col"], np.int32)
+    s.term_comp = arr(desc["term_comp"], np.int32)
+    s.term_fac = arr(desc["term_fac"], np.int32)
+    s.term_coef = arr(desc["term_coef"], np.float64)
+    h = C.c_void_p()
+    _pre_check(lib, lib.ietidp_pre_assemble(device, C.byref(s), C.byref(h)))
+    try:
+        n, nnz, ms, msf = C.c_int(), C.c_int64(), C.c_double(), C.c_double()
+        _pre_check(lib, lib.ietidp_pre_sizes(h, C.byref(n), C.byref(nnz), C.byref(ms), C.byref(msf)))
+        ip = np.zeros(n.value + 1, np.int64)
+        ix = np.zeros(nnz.value, np.int32)
+        v = np.zeros(nnz.value, np.float64)
+        f = np.zeros((desc["nrhs"], n.value), np.float64)
+        _pre_check(lib, lib.ietidp_pre_get(h, _ptr(ip), _ptr(ix), _ptr(v), _ptr(f)))
+        out = dict(K_indptr=ip, K_indices=ix, K_data=v, f=f, ms=ms.value, ms_fill=msf.value)
+        if want_gram:
+            gram = {}
+            for c in range(3):
+                for a in range(3):
+                    for q in range(desc["npatch"][a]):
+                        nb = C.c_int()
+                        _pre_check(lib, lib.ietidp_pre_get_gram(h, c, a, q, None, C.byref(nb)))
+                        g = np.zeros((nb.value, nb.value))
+                        _pre_check(lib, lib.ietidp_pre_get_gram(h, c, a, q, _ptr(g), None))
+                        gram[(c, a, q)] = g.T.copy()
+            out["gram"] = gram
+        return out
+    finally:
+        lib.ietidp_pre_destroy(h)
+
+
+def pre_gauge(nv, ne, eu, ev, w, device=0):
+    """ietidp_pre_gauge: (in_tree bool[ne], primal bool[ne], ms)."""
+    lib = load()
+    eu = np.ascontiguousarray(eu, np.int32)
+    ev = np.ascontiguousarray(ev, np.int32)
+    w = np.ascontiguousarray(w, np.int8)
+    tree = np.zeros(ne, np.uint8)
+    prim = np.zeros(ne, np.uint8)
+    ms = C.c_double()
+    _pre_check(lib, lib.ietidp_pre_gauge(device, nv, ne, _ptr(eu), _ptr(ev), _ptr(w), _ptr(tree), _ptr(prim), C.byref(ms)))
+    return tree.astype(bool), prim.astype(bool), ms.value

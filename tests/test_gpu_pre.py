@@ -1,0 +1,161 @@
+"""Device pre-processing (include/ietidp_pre.h) against the generator's
+plain NumPy/SciPy assembly and gauge (ietigen/problem.py, pinned in tests/test_gen.py and
+tests/test_oracle.py by curl o grad = 0, the DOF counts, EOC of the manufactured solutions and
+DD = monolithic), which is the reference side here: it shares no code with csrc/pre.cu.
+
+PAPER.md:49-57 (K = C^T M_2 C per subdomain, torn), :83, :150-178 (tree-cotree gauge on the
+weighted control graph, primal DOFs).
+
+Tolerances: every K entry is a signed sum of at most 8 x 8 products of three Gram entries, each
+a Gauss sum of a few dozen terms; the two sides differ only in summation order, so entries
+agree to a few ulp of the largest entry: 1e-12 relative to max|K| with
+two orders of margin. Integer results (pattern after dropping exact zeros, tree, primal
+set) are compared bit for bit.
+"""
+import numpy as np
+import pytest
+import scipy.sparse as sp
+
+from ietigen import predesc
+from ietigen.problem import build
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def lib():
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2501_04340_b200 import ietidp
+    return ietidp
+
+
+def _csr(out, n):
+    return sp.csr_matrix((out["K_data"], out["K_indices"], out["K_indptr"]), shape=(n, n))
+
+
+def _subs(P, limit):
+    n = len(P.subs)
+    if n <= limit:
+        return list(range(n))
+    return sorted(set(np.linspace(0, n - 1, limit).astype(int).tolist()))
+
+
+@pytest.mark.parametrize("name", ["C1", "C2r", "C3r", "C4r", "C5r", "E27_221_p3_e2", "E27_311_p1_e3"])
+def test_assembly_matches_generator(lib, name):
+    P = build(name)
+    for k in _subs(P, 6):
+        sd = P.subs[k]
+        Kref, jref = P.assemble(sd)
+        out = lib.pre_assemble(predesc.subdomain_desc(P, sd))
+        K = _csr(out, sd.n)
+        # CSR invariants of the C ABI (ietidp_set_subdomain): sorted columns, symmetric pattern
+        for r in range(0, sd.n, max(1, sd.n // 50)):
+            c = out["K_indices"][out["K_indptr"][r]:out["K_indptr"][r + 1]]
+            assert np.all(np.diff(c) > 0)
+        assert (abs(K - K.T)).max() == 0.0, "exactly symmetric by construction"
+        scale = abs(Kref).max()
+        assert abs(K - Kref).max() <= 1e-12 * scale, (name, k, abs(K - Kref).max() / scale)
+        # structural pattern: a superset of the generator's; the extra entries are exact cancellations
+        Kz = K.copy()
+        Kz.data[abs(Kz.data) <= 1e-13 * scale] = 0.0
+        Kz.eliminate_zeros()
+        Rz = Kref.copy()
+        Rz.data[abs(Rz.data) <= 1e-13 * scale] = 0.0
+        Rz.eliminate_zeros()
+        assert (Kz != 0).astype(np.int8).nnz == (Rz != 0).astype(np.int8).nnz
+        assert ((Kz != 0) != (Rz != 0)).nnz == 0
+        js = abs(jref).max()
+        assert abs(out["f"].T - jref).max() <= 1e-12 * max(js, 1e-300), (name, k)
+
+
+def test_gram_blocks_closed_form(lib):
+    """First stage pinned independently of the generator: on one patch with p = 1, e = 2 over
+    [0, 1/2] the hat functions' Gram matrix is h/6 [[2,1,0],[1,4,1],[0,1,2]] (h = 1/4) and the
+    Curry-Schoenberg D_j = 1/h on element j give diag(1/h)."""
+    P = build("C1")
+    sd = P.subs[0]
+    out = lib.pre_assemble(predesc.subdomain_desc(P, sd), want_gram=True)
+    h = 0.25
+    GB = h / 6 * np.array([[2, 1, 0], [1, 4, 1], [0, 1, 2.0]])
+    GD = np.diag([1 / h, 1 / h])
+    # axis 0 of subdomain 0 spans one patch ([0, 1/2]); component 0 is B along x, D along y, z
+    assert np.allclose(out["gram"][(0, 0, 0)], GB, rtol=0, atol=1e-15)
+    assert np.allclose(out["gram"][(1, 0, 0)], GD, rtol=0, atol=1e-13)
+    # partition of unity: the B Gram entries of a patch sum to its length
+    for (c, a, q), g in out["gram"].items():
+        if c == a:
+            assert abs(g.sum() - 0.5) < 1e-14
+
+
+@pytest.mark.parametrize("name", ["C1", "C2r", "C3r", "C4r", "C5r", "E27_L3_p2_e2", "C5"])
+def test_gauge_tree_and_primal_bitwise(lib, name):
+    P = build(name)
+    g = predesc.gauge_desc(P)
+    tree, prim, ms = lib.pre_gauge(g["nv"], g["ne"], g["eu"], g["ev"], g["w"])
+    assert np.array_equal(tree, P.tree), (name, int((tree != P.tree).sum()))
+    assert np.array_equal(np.flatnonzero(prim), P.primal_edges)
+
+
+def test_gauge_matches_sequential_kruskal(lib):
+    """Against Kruskal's algorithm itself (union-find scan in (weight, id) order)
+    on a seeded random multigraph with several components and parallel edges."""
+    from ietigen.problem import kruskal_unionfind
+    from ietigen.rng import SplitMix64
+    g = SplitMix64(7)
+    nv, ne = 500, 1800
+    eu = np.array([int(g.uniform() * 460) for _ in range(ne)], np.int32)   # vertices 460.. stay isolated
+    ev = np.array([int(g.uniform() * 460) for _ in range(ne)], np.int32)
+    keep = eu != ev
+    eu, ev = eu[keep], ev[keep]
+    ne = len(eu)
+    w = np.array([1 + int(g.uniform() * 5) for _ in range(ne)], np.int8)
+    order = np.lexsort((np.arange(ne), w))
+    ref = kruskal_unionfind(nv, eu.astype(np.int64), ev.astype(np.int64), order)
+    tree, prim, _ = lib.pre_gauge(nv, ne, eu, ev, w)
+    assert np.array_equal(tree, ref)
+    assert np.array_equal(prim, (~ref) & (w == 2))
+
+
+def test_device_assembled_problem_solves(lib):
+    """The device-assembled K^(k), j^(k) and the device gauge fed to the solve phase give the
+    oracle's solution (u within 1e-8, N_iter within 1)."""
+    from ietigen.bundle import make_bundle
+    from oracle import dp
+    b, P = make_bundle("C3r", with_problem=True)
+    ref = dp.solve(b)
+    g = predesc.gauge_desc(P)
+    tree, prim, _ = lib.pre_gauge(g["nv"], g["ne"], g["eu"], g["ev"], g["w"])
+    s = lib.Solver(b["n_sub"], b["n_lambda"], b["n_primal"], b["nrhs"], scaling=b["scaling"], tol=b["tol"])
+    for k, sd in enumerate(P.subs):
+        out = lib.pre_assemble(predesc.subdomain_desc(P, sd))
+        bs = b["subs"][k]
+        tr = np.flatnonzero(tree[sd.gid]).astype(np.int32)
+        pm = np.flatnonzero(prim[sd.gid]).astype(np.int32)
+        assert np.array_equal(tr, bs["tree"]) and np.array_equal(pm, bs["prim"])
+        s.set_subdomain(k, out["K_indptr"], out["K_indices"], out["K_data"], out["f"], bs["B_lambda"], bs["B_dof"],
+                        bs["B_sign"], tr, pm, bs["prim_gid"])
+    s.factor()
+    lam, rep = s.solve()
+    u = np.concatenate([s.get_u(k) for k in range(b["n_sub"])])
+    uref = np.concatenate(ref["u"])
+    assert np.linalg.norm(u - uref) <= 1e-8 * np.linalg.norm(uref)
+    assert abs(rep["iters"][0] - int(ref["iters"][0])) <= 1
+
+
+def test_pre_argument_errors(lib):
+    P = build("C1")
+    d = predesc.subdomain_desc(P, P.subs[0])
+    bad = dict(d)
+    bad["p"] = 4
+    with pytest.raises(lib.IetiError) as e:
+        lib.pre_assemble(bad)
+    assert e.value.status == lib.E_ARG
+    bad = dict(d)
+    bad["fac_kind"] = [1 - k for k in d["fac_kind"]]
+    with pytest.raises(lib.IetiError) as e:
+        lib.pre_assemble(bad)
+    assert e.value.status == lib.E_ARG
+    with pytest.raises(lib.IetiError) as e:
+        lib.pre_gauge(3, 1, np.array([0], np.int32), np.array([5], np.int32), np.array([1], np.int8))
+    assert e.value.status == lib.E_ARG
