@@ -317,38 +317,35 @@ def measure_dgemm_tflops(torch, dev):
     return 2 * n ** 3 / (best * 1e-3) / 1e12
 
 
-def measure_pre(ietidp, prob, device, nsamp=8):
+def measure_pre(ietidp, prob, device):
     """Device pre-processing (include/ietidp_pre.h) on the same workload,
-    outside the timed solve: the tree-cotree gauge of the whole control graph and the
-    assembly K = C^T M_2 C, j = C^T t of a sample of subdomains (device times from the
-    library's CUDA events, second call of each)."""
+    outside the timed solve: the tree-cotree gauge of the whole control graph and the batched
+    assembly K = C^T M_2 C, j = C^T t of every box subdomain (device times from the library's
+    CUDA events, best of three calls; results stay on the device)."""
     from ietigen import predesc
     g = predesc.gauge_desc(prob)
     for _ in range(2):
         tree, prim, g_ms = ietidp.pre_gauge(g["nv"], g["ne"], g["eu"], g["ev"], g["w"], device=device)
-    ns = len(prob.subs)
-    subs = [sd for sd in prob.subs if len(sd.boxes) == 1]
-    subs = [subs[i] for i in sorted(set(int(round(i * (len(subs) - 1) / max(nsamp - 1, 1))) for i in range(nsamp)))] if subs else []
-    ms = ms_fill = 0.0
-    nnz = 0
-    wall = 0.0
-    for sd in subs:
-        d = predesc.subdomain_desc(prob, sd)
-        for _ in range(2):
+    descs = [predesc.subdomain_desc(prob, sd) for sd in prob.subs if len(sd.boxes) == 1]
+    asm = None
+    if descs:
+        best = None
+        for _ in range(3):
             t0 = time.perf_counter()
-            out = ietidp.pre_assemble(d, device=device)
-            w = time.perf_counter() - t0
-        ms += out["ms"]
-        ms_fill += out["ms_fill"]
-        nnz += len(out["K_data"])
-        wall += w
+            _, info = ietidp.pre_assemble_batch(descs, device=device, fetch=False)
+            info["wall_ms"] = (time.perf_counter() - t0) * 1e3
+            if best is None or info["ms"] < best["ms"]:
+                best = info
+        pk = peaks().get("hbm_gbs", 6650.0)
+        gbs = best["nnz"] * 12 / (best["ms_fill"] * 1e-3) / 1e9
+        asm = {"subdomains": len(descs), "of": len(prob.subs), "nnz": int(best["nnz"]), "device_ms": best["ms"],
+               "fill_kernel_ms": best["ms_fill"], "wall_ms_with_upload": best["wall_ms"],
+               "roofline": {"kernel": "k_rows<1> (CSR columns and values of C^T M_2 C, all subdomains in one launch)",
+                            "bound": "hbm", "achieved": gbs, "peak": pk, "unit": "GB/s", "frac": gbs / pk,
+                            "algorithmic_bytes": int(best["nnz"]) * 12,
+                            "note": "12 B written per CSR entry (value + column)"}}
     return {"gauge_ms": g_ms, "graph": {"nv": int(g["nv"]), "ne": int(g["ne"])},
-            "tree_matches_generator": bool(np.array_equal(tree, prob.tree)),
-            "assembly": {"subdomains_sampled": len(subs), "of": ns, "nnz": int(nnz), "device_ms": ms,
-                         "fill_kernel_ms": ms_fill, "wall_ms_with_copies": wall * 1e3,
-                         "fill_gb_s": (nnz * 12 / (ms_fill * 1e-3) / 1e9) if ms_fill else None,
-                         "note": "k_rows<1> writes 12 B per CSR entry (value + column): HBM-write bound at "
-                                 "scale; one launch per subdomain here, so launch- and latency-bound"}}
+            "tree_matches_generator": bool(np.array_equal(tree, prob.tree)), "assembly": asm}
 
 
 def run_ours(args, rank, world, local):

@@ -87,7 +87,15 @@ typedef struct {
  * match its term, dof_of_edge not ascending), E_CUDA, E_NOMEM. */
 int ietidp_pre_assemble(int device, const ietidp_pre_subdomain* s, ietidp_pre_t* out);
 
-/* n_dof and nnz of the assembled matrix; ms = device time of the assembly kernels
+/* The same for n subdomains of one workload in one pass: all inputs travel in one upload,
+ * and every stage is ONE launch over the whole batch (k_stage1d: a CTA per subdomain;
+ * k_rows: grid.y = subdomain), so the value kernel runs at a full-GPU grid. out[0..n)
+ * receive one handle per subdomain (each released with ietidp_pre_destroy; they share
+ * the batch's device memory, freed with the last of them). Errors as above; on failure no
+ * handle is returned. */
+int ietidp_pre_assemble_batch(int device, int n, const ietidp_pre_subdomain* subs, ietidp_pre_t* out);
+
+/* n_dof and nnz of the assembled matrix (for a batch, ms and ms_fill are the batch's); ms = device time of the assembly kernels
  * (CUDA events; uploads excluded); ms_fill = of the value kernel alone (the dominant one:
  * 12 bytes written per entry). Any pointer may be NULL. */
 int ietidp_pre_sizes(ietidp_pre_t a, int* n_dof, int64_t* nnz, double* ms, double* ms_fill);

@@ -29,7 +29,7 @@ SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "i
            "ietidp_estimate_condition", "ietidp_get_pcg_coefficients", "ietidp_get_rhs", "ietidp_get_report", "ietidp_kernel_launches", "ietidp_last_error",
            "ietidp_status_string", "ietidp_destroy"]
 # every entry point include/ietidp_pre.h declares (device pre-processing)
-PRE_SYMBOLS = ["ietidp_pre_assemble", "ietidp_pre_sizes", "ietidp_pre_get", "ietidp_pre_get_gram",
+PRE_SYMBOLS = ["ietidp_pre_assemble", "ietidp_pre_assemble_batch", "ietidp_pre_sizes", "ietidp_pre_get", "ietidp_pre_get_gram",
                "ietidp_pre_last_error", "ietidp_pre_destroy", "ietidp_pre_gauge"]
 
 
@@ -108,6 +108,7 @@ def load():
         "ietidp_status_string": (C.c_char_p, [I]),
         "ietidp_destroy": (None, [P]),
         "ietidp_pre_assemble": (I, [I, C.POINTER(PreSubdomain), C.POINTER(P)]),
+        "ietidp_pre_assemble_batch": (I, [I, I, C.POINTER(PreSubdomain), C.POINTER(P)]),
         "ietidp_pre_sizes": (I, [P, C.POINTER(I), C.POINTER(C.c_int64), C.POINTER(D), C.POINTER(D)]),
         "ietidp_pre_get": (I, [P, P, P, P, P]),
         "ietidp_pre_get_gram": (I, [P, I, I, I, P, C.POINTER(I)]),
@@ -301,19 +302,12 @@ def _pre_check(lib, st):
         raise IetiError(st, lib.ietidp_pre_last_error().decode())
 
 
-def pre_assemble(desc, device=0, want_gram=False):
-    """ietidp_pre_assemble + ietidp_pre_get for one box subdomain described by plain arrays
-    (ietigen.predesc.subdomain_desc). Returns dict(K_indptr, K_indices, K_data, f (nrhs, n),
-    ms [, gram])."""
-    lib = load()
-    keep = []
-
+def _pre_fill(s, desc, keep):
     def arr(a, dt):
         a = np.ascontiguousarray(a, dt)
         keep.append(a)
         return a.ctypes.data if a.size else None
 
-    s = PreSubdomain()
     s.p, s.e, s.nq, s.n_dof, s.nrhs, s.lq = desc["p"], desc["e"], desc["nq"], desc["n_dof"], desc["nrhs"], desc["lq"]
     for a in range(3):
         s.npatch[a] = desc["npatch"][a]
@@ -332,31 +326,70 @@ def pre_assemble(desc, device=0, want_gram=False):
     s.term_comp = arr(desc["term_comp"], np.int32)
     s.term_fac = arr(desc["term_fac"], np.int32)
     s.term_coef = arr(desc["term_coef"], np.float64)
+
+
+def _pre_fetch(lib, h, desc, want_gram):
+    n, nnz, ms, msf = C.c_int(), C.c_int64(), C.c_double(), C.c_double()
+    _pre_check(lib, lib.ietidp_pre_sizes(h, C.byref(n), C.byref(nnz), C.byref(ms), C.byref(msf)))
+    ip = np.zeros(n.value + 1, np.int64)
+    ix = np.zeros(nnz.value, np.int32)
+    v = np.zeros(nnz.value, np.float64)
+    f = np.zeros((desc["nrhs"], n.value), np.float64)
+    _pre_check(lib, lib.ietidp_pre_get(h, _ptr(ip), _ptr(ix), _ptr(v), _ptr(f)))
+    out = dict(K_indptr=ip, K_indices=ix, K_data=v, f=f, ms=ms.value, ms_fill=msf.value)
+    if want_gram:
+        gram = {}
+        for c in range(3):
+            for a in range(3):
+                for q in range(desc["npatch"][a]):
+                    nb = C.c_int()
+                    _pre_check(lib, lib.ietidp_pre_get_gram(h, c, a, q, None, C.byref(nb)))
+                    g = np.zeros((nb.value, nb.value))
+                    _pre_check(lib, lib.ietidp_pre_get_gram(h, c, a, q, _ptr(g), None))
+                    gram[(c, a, q)] = g.T.copy()
+        out["gram"] = gram
+    return out
+
+
+def pre_assemble(desc, device=0, want_gram=False):
+    """ietidp_pre_assemble + ietidp_pre_get for one box subdomain described by plain arrays
+    (ietigen.predesc.subdomain_desc). Returns dict(K_indptr, K_indices, K_data, f (nrhs, n),
+    ms, ms_fill [, gram])."""
+    lib = load()
+    keep = []
+    s = PreSubdomain()
+    _pre_fill(s, desc, keep)
     h = C.c_void_p()
     _pre_check(lib, lib.ietidp_pre_assemble(device, C.byref(s), C.byref(h)))
     try:
-        n, nnz, ms, msf = C.c_int(), C.c_int64(), C.c_double(), C.c_double()
-        _pre_check(lib, lib.ietidp_pre_sizes(h, C.byref(n), C.byref(nnz), C.byref(ms), C.byref(msf)))
-        ip = np.zeros(n.value + 1, np.int64)
-        ix = np.zeros(nnz.value, np.int32)
-        v = np.zeros(nnz.value, np.float64)
-        f = np.zeros((desc["nrhs"], n.value), np.float64)
-        _pre_check(lib, lib.ietidp_pre_get(h, _ptr(ip), _ptr(ix), _ptr(v), _ptr(f)))
-        out = dict(K_indptr=ip, K_indices=ix, K_data=v, f=f, ms=ms.value, ms_fill=msf.value)
-        if want_gram:
-            gram = {}
-            for c in range(3):
-                for a in range(3):
-                    for q in range(desc["npatch"][a]):
-                        nb = C.c_int()
-                        _pre_check(lib, lib.ietidp_pre_get_gram(h, c, a, q, None, C.byref(nb)))
-                        g = np.zeros((nb.value, nb.value))
-                        _pre_check(lib, lib.ietidp_pre_get_gram(h, c, a, q, _ptr(g), None))
-                        gram[(c, a, q)] = g.T.copy()
-            out["gram"] = gram
-        return out
+        return _pre_fetch(lib, h, desc, want_gram)
     finally:
         lib.ietidp_pre_destroy(h)
+
+
+def pre_assemble_batch(descs, device=0, fetch=True):
+    """ietidp_pre_assemble_batch: every subdomain of a workload in one pass. Returns
+    (list of result dicts (or None when fetch is False), dict(ms, ms_fill, nnz))."""
+    lib = load()
+    keep = []
+    n = len(descs)
+    subs = (PreSubdomain * n)()
+    for k, d in enumerate(descs):
+        _pre_fill(subs[k], d, keep)
+    hs = (C.c_void_p * n)()
+    _pre_check(lib, lib.ietidp_pre_assemble_batch(device, n, subs, hs))
+    try:
+        outs, nnz_tot = [], 0
+        ms, msf = C.c_double(), C.c_double()
+        for k in range(n):
+            nz = C.c_int64()
+            _pre_check(lib, lib.ietidp_pre_sizes(hs[k], None, C.byref(nz), C.byref(ms), C.byref(msf)))
+            nnz_tot += nz.value
+            outs.append(_pre_fetch(lib, hs[k], descs[k], False) if fetch else None)
+        return outs, dict(ms=ms.value, ms_fill=msf.value, nnz=nnz_tot)
+    finally:
+        for k in range(n):
+            lib.ietidp_pre_destroy(hs[k])
 
 
 def pre_gauge(nv, ne, eu, ev, w, device=0):

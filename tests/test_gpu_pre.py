@@ -69,6 +69,26 @@ def test_assembly_matches_generator(lib, name):
         assert abs(out["f"].T - jref).max() <= 1e-12 * max(js, 1e-300), (name, k)
 
 
+@pytest.mark.parametrize("name", ["C3r", "C4r", "C5r"])
+def test_batch_assembly_bitwise_equals_single(lib, name):
+    """ietidp_pre_assemble_batch (one launch per stage over all subdomains, the configuration
+    bench.py times) gives bit for bit the per-subdomain results, on every subdomain."""
+    P = build(name)
+    descs = [predesc.subdomain_desc(P, sd) for sd in P.subs]
+    outs, info = lib.pre_assemble_batch(descs)
+    assert info["nnz"] == sum(len(o["K_data"]) for o in outs)
+    for k in _subs(P, 12):
+        one = lib.pre_assemble(descs[k])
+        for key in ("K_indptr", "K_indices", "K_data", "f"):
+            assert np.array_equal(one[key], outs[k][key]), (name, k, key)
+    # and against the generator on a subdomain the single-call test does not sample
+    k = len(P.subs) // 2 + 1
+    Kref, jref = P.assemble(P.subs[k])
+    K = _csr(outs[k], P.subs[k].n)
+    assert abs(K - Kref).max() <= 1e-12 * abs(Kref).max()
+    assert abs(outs[k]["f"].T - jref).max() <= 1e-12 * abs(jref).max()
+
+
 def test_gram_blocks_closed_form(lib):
     """First stage pinned independently of the generator: on one patch with p = 1, e = 2 over
     [0, 1/2] the hat functions' Gram matrix is h/6 [[2,1,0],[1,4,1],[0,1,2]] (h = 1/4) and the
