@@ -694,8 +694,9 @@ void analyze_all(ietidp_s* h) {
       firstsub[l] = k;
     }
   }
+  // sharded mode (ietidp_shard.h): a row may have one side, or none, on this rank
   for (int l = 0; l < h->n_lambda; ++l)
-    if (cnt[l] != 2 || ssum[l] != 0)
+    if (h->shard ? (cnt[l] > 2 || (cnt[l] == 2 && ssum[l] != 0)) : (cnt[l] != 2 || ssum[l] != 0))
       throw Error(IETIDP_E_B_STRUCTURE,
                   "multiplier row " + std::to_string(l) + " is not {+1,-1} in two subdomains");
 
@@ -1574,7 +1575,7 @@ void analyze_all(ietidp_s* h) {
     std::copy(sp.perm.begin(), sp.perm.end(), perm_all.begin() + d.perm_off);
   }
   for (int g = 0; g < h->n_primal; ++g)
-    if (!gid_seen[g]) throw Error(IETIDP_E_ARG, "global primal " + std::to_string(g) + " has no local DOF");
+    if (!gid_seen[g] && !h->shard) throw Error(IETIDP_E_ARG, "global primal " + std::to_string(g) + " has no local DOF");
   // S_PP entry (g1, g2) <- lower entries of the P fronts; global primal g <- (k, q)
   const int ng = h->n_primal;
   std::vector<std::vector<long long>> sl((size_t)ng * ng);

@@ -8,6 +8,7 @@
 #include <new>
 
 #include "handle.h"
+#include "../../include/ietidp_shard.h"
 
 namespace ieti {
 void analyze_all(ietidp_s* h);
@@ -226,6 +227,47 @@ ietidp_status ietidp_set_subdomain(ietidp_t h, int k, int n_k, const int64_t* K_
   });
 }
 
+// ---- sharded mode (include/ietidp_shard.h) ----
+ietidp_status ietidp_shard_enable(ietidp_t h, int rank, int nranks, ietidp_allreduce_fn fn, void* ctx) {
+  return guard(h, [&]() {
+    require(!h->analyzed, IETIDP_E_STATE, "shard_enable after analysis");
+    require(fn != nullptr && nranks >= 1 && rank >= 0 && rank < nranks, IETIDP_E_ARG, "bad rank or null all-reduce");
+    require(h->opt.loop == IETIDP_LOOP_EXPLICIT, IETIDP_E_ARG, "the sharded solve runs the explicit loop");
+    require(h->opt.stop == IETIDP_STOP_RESIDUAL, IETIDP_E_ARG, "the sharded solve uses the residual stopping criterion");
+    h->shard = true;
+    h->sh_rank = rank;
+    h->sh_n = nranks;
+    h->sh_allreduce = fn;
+    h->sh_ctx = ctx;
+  });
+}
+
+ietidp_status ietidp_shard_partition(int n_sub, const double* weight, int nranks, int32_t* owner) {
+  if (n_sub < 1 || nranks < 1 || !weight || !owner) return IETIDP_E_ARG;
+  double total = 0.0;
+  for (int k = 0; k < n_sub; ++k) {
+    if (!(weight[k] > 0.0)) return IETIDP_E_ARG;
+    total += weight[k];
+  }
+  // contiguous ranges: rank r ends where the running weight passes (r + 1) / nranks of the
+  // total (the subdomain straddling a cut goes to the side holding more of it), leaving at
+  // least one subdomain for every later rank
+  double run = 0.0;
+  int r = 0;
+  for (int k = 0; k < n_sub; ++k) {
+    const double cut = total * (r + 1) / nranks;
+    const int left_after = n_sub - k;        // subdomains k .. n_sub-1 still to place
+    const int ranks_after = nranks - r - 1;  // ranks after r
+    const bool must_advance = left_after <= ranks_after;  // keep one per later rank
+    const bool want_advance = run + 0.5 * weight[k] > cut;
+    bool started = k > 0 && owner[k - 1] == r;
+    if (r < nranks - 1 && started && (must_advance || want_advance)) ++r;
+    owner[k] = r;
+    run += weight[k];
+  }
+  return IETIDP_OK;
+}
+
 ietidp_status ietidp_analyze(ietidp_t h) {
   return guard(h, [&]() {
     require(!h->analyzed, IETIDP_E_STATE, "already analyzed");
@@ -369,7 +411,8 @@ ietidp_status ietidp_factor(ietidp_t h) {
     // are captured once into a CUDA graph and replayed: the plan and buffers are fixed
     // after analyze, so every factor call launches the same work. Not with the launch
     // tracer; IETIDP_GRAPH=0 launches directly.
-    const bool use_graph = !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
+    const bool use_graph =
+        !h->shard && !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
     try {
       if (use_graph && !h->fgraph) {
         const long long l0 = h->launches;
@@ -450,7 +493,8 @@ ietidp_status ietidp_solve(ietidp_t h, double* lambda, ietidp_report* report) {
     IETI_CUDA(cudaEventRecord(e1.b, h->stream));
     IETI_CUDA(cudaEventRecord(e2.a, h->stream));
     // the recovery's ~40 launches (backward sweep level by level) as a captured graph
-    const bool use_graph = !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
+    const bool use_graph =
+        !h->shard && !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
     if (use_graph) {
       if (!h->rgraph) {
         const long long l0 = h->launches;

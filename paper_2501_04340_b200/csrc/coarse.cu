@@ -330,6 +330,39 @@ __global__ void k_scaling(int m, const LamDev* __restrict__ lam, const int* __re
   }
 }
 
+// Sharded mode (ietidp_shard.h): the K diagonal of each multiplier's local side(s) into
+// kd2[2j + (sign < 0)] (zero where the side lives on another rank); after the sum over the
+// ranks both sides are known everywhere and the weights follow as in k_scaling.
+__global__ void k_sh_kdiag(int m, const LamDev* __restrict__ lam, const int* __restrict__ kdiag_src,
+                           const double* __restrict__ kval, double* __restrict__ kd2) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x) {
+    double v[2] = {0.0, 0.0};
+    for (int q = 0; q < 2; ++q)
+      if (lam[j].sign[q] != 0.f) v[lam[j].sign[q] < 0.f ? 1 : 0] = kval[kdiag_src[lam[j].slot[q]]];
+    kd2[2 * j] = v[0];
+    kd2[2 * j + 1] = v[1];
+  }
+}
+__global__ void k_sh_delta(int m, const LamDev* __restrict__ lam, const double* __restrict__ kd2,
+                           double* __restrict__ kdiag, double* __restrict__ delta, int stiffness) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < m; j += gridDim.x * blockDim.x)
+    for (int q = 0; q < 2; ++q) {
+      if (lam[j].sign[q] == 0.f) continue;
+      const int a = lam[j].slot[q], side = lam[j].sign[q] < 0.f ? 1 : 0;
+      const double mine = kd2[2 * j + side], other = kd2[2 * j + 1 - side];
+      kdiag[a] = mine;
+      delta[a] = stiffness ? other / (mine + other) : 0.5;
+    }
+}
+
+// Sum of a device buffer over the ranks of a sharded solve (the caller's all-reduce).
+void sh_sum(ietidp_s* h, double* buf, long long n) {
+  if (!h->shard || n <= 0) return;
+  if (h->sh_allreduce(h->sh_ctx, buf, (int64_t)n, (void*)h->stream) != 0)
+    throw Error(IETIDP_E_CUDA, "the all-reduce callback of the sharded solve failed");
+  h->sh_reduced_doubles += n;
+}
+
 // Repack the r_I root front of every subdomain for the loop: L_II^-1 (and, for the
 // triangular loop, L_II) as row-major TB x TB lower tiles (row-block order), L_PI as
 // nP x nI row-major. One CTA per (subdomain, lower tile); the tile is transposed
@@ -427,7 +460,15 @@ void run_coarse(ietidp_s* h) {
   const int nrhs = h->nrhs, ng = h->n_primal;
   const int nlev = h->plan.max_level + 1;
   (void)nlev;  // the factorisation's streams have joined the caller's stream
-  if (h->n_lambda) {
+  if (h->n_lambda && h->shard) {  // the partner's K diagonal may live on another rank
+    if (h->sh_kd2.n == 0) h->sh_kd2.alloc(2 * (size_t)h->n_lambda);
+    k_sh_kdiag<<<grid_for(h->n_lambda, 256), 256, 0, s>>>(h->n_lambda, h->lam.p, h->kdiag_src.p, h->kval.p, h->sh_kd2.p);
+    IETI_LAUNCHED(h);
+    sh_sum(h, h->sh_kd2.p, 2LL * h->n_lambda);
+    k_sh_delta<<<grid_for(h->n_lambda, 256), 256, 0, s>>>(h->n_lambda, h->lam.p, h->sh_kd2.p, h->kdiag.p, h->delta.p,
+                                                          h->opt.scaling == IETIDP_SCALE_STIFFNESS);
+    IETI_LAUNCHED(h);
+  } else if (h->n_lambda) {
     k_scaling<<<grid_for(h->n_lambda, 256), 256, 0, s>>>(h->n_lambda, h->lam.p, h->kdiag_src.p, h->kval.p, h->kdiag.p,
                                                         h->delta.p, h->opt.scaling == IETIDP_SCALE_STIFFNESS);
     IETI_LAUNCHED(h);
@@ -455,7 +496,11 @@ void run_coarse(ietidp_s* h) {
         ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p, h->pcon_sub.p, h->pcon_q.p, h->d_sub.p,
         h->Xf.p, h->S.p, h->ftil.p);
     IETI_LAUNCHED(h);
-    if (ng <= COARSE_CTA_MAX) {
+    if (h->shard) {  // S_PP and ftilde are sums over all subdomains
+      sh_sum(h, h->S.p, (long long)ng * ng);
+      sh_sum(h, h->ftil.p, (long long)ng * nrhs);
+    }
+    if (ng <= COARSE_CTA_MAX && !h->shard) {
       const int smem = ng * (ng + 1) / 2 * sizeof(double);
       IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       k_coarse_factor<<<1, 1024, smem, s>>>(ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p,
@@ -492,7 +537,7 @@ void run_coarse(ietidp_s* h) {
     k_gather_I<<<h->n_sub, 256, 0, s>>>(h->d_sub.p, nrhs, h->Xf.p, h->yI.p);
     IETI_LAUNCHED(h);
     loop_bwd(h, nrhs, h->yI.p, ng ? h->zc0.p : nullptr, -1.0, h->xI.p, nullptr);
-    bgather(h, nrhs, h->xI.p, nullptr, h->d_vec.p, nullptr, nullptr, nullptr);
+    bgather(h, nrhs, h->xI.p, nullptr, h->d_vec.p, nullptr, nullptr, nullptr);  // (sharded: summed over the ranks inside)
   }
   IETI_CHECK_LAUNCH();
 }

@@ -225,6 +225,13 @@ struct ietidp_s {
   void* graph = nullptr;
   unsigned long long cond_handle = 0;
   bool pcg_persistent = false;          // last solve ran the persistent cooperative PCG kernel
+  // ---- sharded mode (ietidp_shard.h): this handle holds one rank's subdomains ----
+  bool shard = false;
+  int sh_rank = 0, sh_n = 1;
+  int (*sh_allreduce)(void*, double*, int64_t, void*) = nullptr;
+  void* sh_ctx = nullptr;
+  ieti::DevBuf<double> sh_kd2;          // K diagonal on the (+, -) sides of every multiplier
+  long long sh_reduced_doubles = 0;     // doubles summed over the ranks so far (report)
   ieti::DevBuf<unsigned> gbar;          // its grid barrier
 };
 
@@ -252,6 +259,7 @@ void run_solve(ietidp_s* h);                   // pcg.cu
 void run_apply_F(ietidp_s* h, int ncols, const double* x, double* y);
 void run_apply_M(ietidp_s* h, int ncols, const double* x, double* y);
 void run_recover(ietidp_s* h);                 // coarse.cu
+void sh_sum(ietidp_s* h, double* buf, long long n);  // sharded mode: all-reduce of a device buffer (coarse.cu)
 void run_estimate_condition(ietidp_s* h, double* omega_min, double* omega_max, double* cond);  // pcg.cu
 void transpose_in(ietidp_s* h, int rows, int ncols, const double* colmajor, double* inter);
 void transpose_out(ietidp_s* h, int rows, int ncols, const double* inter, double* colmajor);

@@ -2604,6 +2604,62 @@ static int tmv_launches(const ietidp_s* h, int ncols) {
   return (ncols + cfg.ncp - 1) / cfg.ncp;
 }
 
+// ---- sharded mode (ietidp_shard.h) ----
+// per-column partial dot products of two replicated multiplier-space vectors, in the layout
+// of k_bgather's fused partials (partial[block * ncols + c], NBLK blocks)
+__global__ void __launch_bounds__(VT) k_sh_dotpart(int m, int ncols, const double* __restrict__ a,
+                                                   const double* __restrict__ b, double* __restrict__ partial,
+                                                   const PcgState* __restrict__ st) {
+  if (st && st->done) return;
+  const int P2 = pow2ge(ncols);
+  const int c = threadIdx.x % P2, rl = threadIdx.x / P2, R = VT / P2;
+  double dot = 0.0;
+  if (c < ncols)
+    for (int j = blockIdx.x * R + rl; j < m; j += gridDim.x * R) dot += a[(long long)j * ncols + c] * b[(long long)j * ncols + c];
+  block_col_reduce(dot, ncols, P2, partial);
+}
+// g[gi][c] = add + sum of the coarse partial rows of the LOCAL subdomains (first half of k_coarse)
+__global__ void __launch_bounds__(256)
+    k_sh_gsum(int ng, int ncols, int nPmax, const int* __restrict__ pcon_ptr, const int* __restrict__ pcon_sub,
+              const int* __restrict__ pcon_q, const int* __restrict__ sub_cta0, const int* __restrict__ sub_ncta,
+              const double* __restrict__ gpart, double* __restrict__ g, const PcgState* __restrict__ st) {
+  if (st && st->done) return;
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ng * ncols; e += gridDim.x * blockDim.x) {
+    const int gi = e / ncols, c = e - gi * ncols;
+    double s = 0.0;
+    for (int q = pcon_ptr[gi]; q < pcon_ptr[gi + 1]; ++q) {
+      const int k = pcon_sub[q], lq = pcon_q[q];
+      for (int cta = sub_cta0[k]; cta < sub_cta0[k] + sub_ncta[k]; ++cta)
+        s += gpart[((long long)cta * nPmax + lq) * ncols + c];
+    }
+    g[e] = s;
+  }
+}
+// z = S^-1 (add + g), a warp per entry
+__global__ void __launch_bounds__(256) k_sh_coarse_solve(int ng, int ncols, const double* __restrict__ Sinv,
+                                                        const double* __restrict__ g, const double* __restrict__ add,
+                                                        double* __restrict__ z, const PcgState* __restrict__ st) {
+  if (st && st->done) return;
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int e = warp; e < ng * ncols; e += nw) {
+    const int i = e / ncols, c = e - i * ncols;
+    double s = 0.0;
+    for (int j = lane; j < ng; j += 32)
+      s += Sinv[(long long)i * ng + j] * (g[j * ncols + c] + (add ? add[j * ncols + c] : 0.0));
+    s = warp_sum(s);
+    if (lane == 0) z[e] = s;
+  }
+}
+// after a local gather into the multiplier space: sum over the ranks, then the dot partials
+static void sh_finish_gather(ietidp_s* h, int ncols, double* out, const double* dotv, double* partial, const PcgState* st) {
+  sh_sum(h, out, (long long)h->n_lambda * ncols);
+  if (dotv && partial) {
+    k_sh_dotpart<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, out, dotv, partial, st);
+    IETI_LAUNCHED(h);
+  }
+}
+
 // y_k = L_II^-1 B_I^T v (per slot) and the coarse partials L_PI y_k
 void loop_fwd(ietidp_s* h, int ncols, const double* v, double* y, bool partials, const void* stv) {
   const PcgState* st = static_cast<const PcgState*>(stv);
@@ -2632,6 +2688,13 @@ void bgather(ietidp_s* h, int ncols, const double* x, const double* weight, doub
              double* partial, const void* stv) {
   const PcgState* st = static_cast<const PcgState*>(stv);
   if (h->n_lambda == 0) return;
+  if (h->shard) {
+    k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, x, weight, out, nullptr, nullptr, st,
+                                          CoarseTerm{});
+    IETI_LAUNCHED(h);
+    sh_finish_gather(h, ncols, out, dotv, partial, st);
+    return;
+  }
   k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, x, weight, out, dotv, partial, st,
                                         CoarseTerm{});
   IETI_LAUNCHED(h);
@@ -2645,6 +2708,17 @@ void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const vo
   // the block-pair items of the triangular operators
   const int* r0 = sym_rows ? h->sub_blk0.p : h->sub_cta0.p;
   const int* rn = sym_rows ? h->sub_nt.p : h->sub_ncta.p;
+  if (h->shard) {  // g summed over the ranks, S_PP^-1 replicated
+    k_sh_gsum<<<grid_for((long long)h->n_primal * ncols, 256), 256, 0, h->stream>>>(
+        h->n_primal, ncols, std::max(h->plan.nPmax, 1), h->pcon_ptr.p, h->pcon_sub.p, h->pcon_q.p, r0, rn, h->gpart.p,
+        h->gc.p, st);
+    IETI_LAUNCHED(h);
+    sh_sum(h, h->gc.p, (long long)h->n_primal * ncols);
+    k_sh_coarse_solve<<<grid_for((long long)h->n_primal * ncols * 32, 256), 256, 0, h->stream>>>(
+        h->n_primal, ncols, h->Sinv.p, h->gc.p, add, z, st);
+    IETI_LAUNCHED(h);
+    return;
+  }
   const int smem = h->n_primal * ncols * 8;
   if (smem > 48 * 1024)
     IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
@@ -2695,6 +2769,12 @@ static void apply_F_inter(ietidp_s* h, int ncols, const double* x, double* y, co
     sym_apply(h, a);
     coarse_apply(h, ncols, nullptr, h->zc.p, st, true);
     CoarseTerm ct = coarse_term_args(h);
+    if (h->shard) {
+      k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, h->xI.p, nullptr, y, nullptr, nullptr, st, ct);
+      IETI_LAUNCHED(h);
+      sh_finish_gather(h, ncols, y, dotv, partial, st);
+      return;
+    }
     k_bgather<<<NBLK, VT, 0, h->stream>>>(h->n_lambda, ncols, h->lam.p, h->xI.p, nullptr, y, dotv, partial, st, ct);
     IETI_LAUNCHED(h);
     return;
@@ -3189,7 +3269,7 @@ void run_solve(ietidp_s* h) {
   IETI_CUDA(cudaMemsetAsync(h->partial.p, 0, h->partial.n * sizeof(double), s));
   const char* mode = getenv("IETIDP_PCG");
   h->pcg_persistent = false;
-  if (!(mode && std::string(mode) == "graph") && run_solve_persistent(h)) {
+  if (!h->shard && !(mode && std::string(mode) == "graph") && run_solve_persistent(h)) {
     h->pcg_persistent = true;
     IETI_CHECK_LAUNCH();
     return;
@@ -3208,6 +3288,19 @@ void run_solve(ietidp_s* h) {
     IETI_LAUNCHED(h);
     k_init_rz<<<1, 64, 0, s>>>(st, rz_part);
     IETI_LAUNCHED(h);
+    if (h->shard) {
+      // the all-reduce callback runs on the host side: the loop is driven from the host; every
+      // rank reads the same replicated state and takes the same decision
+      for (;;) {
+        int itdone[2];
+        IETI_CUDA(cudaMemcpyAsync(itdone, st, sizeof(itdone), cudaMemcpyDeviceToHost, s));
+        IETI_CUDA(cudaStreamSynchronize(s));
+        if (itdone[1]) break;
+        iteration_body(h, st, 0);
+      }
+      IETI_CHECK_LAUNCH();
+      return;
+    }
     build_graph(h, st);
     IETI_CUDA(cudaGraphLaunch((cudaGraphExec_t)h->graph_exec, s));
   }

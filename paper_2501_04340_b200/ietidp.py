@@ -40,6 +40,11 @@ class Options(C.Structure):
                 ("stream", C.c_void_p)]
 
 
+# every entry point include/ietidp_shard.h declares (sharded multi-GPU solve)
+SHARD_SYMBOLS = ["ietidp_shard_enable", "ietidp_shard_partition"]
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
+
+
 class PreSubdomain(C.Structure):
     """ietidp_pre_subdomain (include/ietidp_pre.h)."""
     _fields_ = [("p", C.c_int), ("e", C.c_int), ("npatch", C.c_int * 3), ("knots", C.c_void_p * 3),
@@ -107,6 +112,8 @@ def load():
         "ietidp_last_error": (C.c_char_p, [P]),
         "ietidp_status_string": (C.c_char_p, [I]),
         "ietidp_destroy": (None, [P]),
+        "ietidp_shard_enable": (I, [P, I, I, ALLREDUCE_FN, P]),
+        "ietidp_shard_partition": (I, [I, P, I, P]),
         "ietidp_pre_assemble": (I, [I, C.POINTER(PreSubdomain), C.POINTER(P)]),
         "ietidp_pre_assemble_batch": (I, [I, I, C.POINTER(PreSubdomain), C.POINTER(P)]),
         "ietidp_pre_sizes": (I, [P, C.POINTER(I), C.POINTER(C.c_int64), C.POINTER(D), C.POINTER(D)]),
@@ -175,6 +182,21 @@ class Solver:
                                            len(a["bl"]), _ptr(a["bl"]), _ptr(a["bd"]), _ptr(a["bs"]),
                                            len(a["tr"]), _ptr(a["tr"]), len(a["pr"]), _ptr(a["pr"]), _ptr(a["pg"]))
         self._check(st)
+
+    def shard_enable(self, rank, nranks, allreduce):
+        """Sharded mode (include/ietidp_shard.h): this handle holds rank's subdomains only;
+        allreduce(ptr, n, stream) sums the device buffer of n doubles at ptr over the ranks in
+        place (raise or return non-zero on failure)."""
+        def thunk(ctx, ptr, n, stream):
+            try:
+                rc = allreduce(ptr, n, stream)
+                return int(rc or 0)
+            except Exception:  # never unwind through the C frames
+                import traceback
+                traceback.print_exc()
+                return 1
+        self._allreduce = ALLREDUCE_FN(thunk)  # keep the trampoline alive with the handle
+        self._check(self.lib.ietidp_shard_enable(self.h, rank, nranks, self._allreduce, None))
 
     def analyze(self):
         self._check(self.lib.ietidp_analyze(self.h))
@@ -403,3 +425,51 @@ def pre_gauge(nv, ne, eu, ev, w, device=0):
     ms = C.c_double()
     _pre_check(lib, lib.ietidp_pre_gauge(device, nv, ne, _ptr(eu), _ptr(ev), _ptr(w), _ptr(tree), _ptr(prim), C.byref(ms)))
     return tree.astype(bool), prim.astype(bool), ms.value
+
+
+def shard_partition(weights, nranks):
+    """ietidp_shard_partition: owner rank per subdomain (contiguous, balanced by weight)."""
+    lib = load()
+    w = np.ascontiguousarray(weights, np.float64)
+    owner = np.zeros(len(w), np.int32)
+    st = lib.ietidp_shard_partition(len(w), _ptr(w), nranks, _ptr(owner))
+    if st != OK:
+        raise IetiError(st, "ietidp_shard_partition")
+    return owner
+
+
+def shard_from_bundle(b, owner, rank, nranks, allreduce, **opts):
+    """A sharded Solver holding the subdomains k of a generator bundle with owner[k] == rank
+    (local ids in ascending global order; multiplier and primal ids stay global)."""
+    opts.setdefault("scaling", b["scaling"])
+    opts.setdefault("tol", b["tol"])
+    mine = [k for k in range(b["n_sub"]) if owner[k] == rank]
+    s = Solver(len(mine), b["n_lambda"], b["n_primal"], b["nrhs"], **opts)
+    s.shard_enable(rank, nranks, allreduce)
+    for i, k in enumerate(mine):
+        sd = b["subs"][k]
+        s.set_subdomain(i, sd["K_indptr"], sd["K_indices"], sd["K_data"], sd["f"], sd["B_lambda"], sd["B_dof"],
+                        sd["B_sign"], sd["tree"], sd["prim"], sd["prim_gid"])
+    s.global_ids = mine
+    return s
+
+
+class CudaView:
+    """Zero-copy view of n doubles at a raw device pointer (for torch.as_tensor)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<f8", "data": (int(ptr), False), "version": 2}
+
+
+def nccl_allreduce(device):
+    """An all-reduce callback over torch.distributed (backend nccl): sums the buffer in place on
+    the library's stream, so it is ordered with the kernels around it without a host sync."""
+    import torch
+    import torch.distributed as dist
+
+    def fn(ptr, n, stream):
+        t = torch.as_tensor(CudaView(ptr, n), device=torch.device("cuda", device))
+        with torch.cuda.stream(torch.cuda.ExternalStream(int(stream), device=device)):
+            dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return 0
+    return fn

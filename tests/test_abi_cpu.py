@@ -28,6 +28,11 @@ def test_exports_every_declared_symbol(lib):
     so = lib.load()
     for name in declared:
         assert hasattr(so, name), name
+    hdr = open(os.path.join(ROOT, "include", "ietidp_shard.h")).read()
+    declared = set(re.findall(r"\b(ietidp_shard_[A-Za-z_]+)\s*\(", hdr))
+    assert declared == set(lib.SHARD_SYMBOLS)
+    for name in declared:
+        assert hasattr(so, name), name
     hdr = open(os.path.join(ROOT, "include", "ietidp_pre.h")).read()
     declared = set(re.findall(r"\b(ietidp_pre_[A-Za-z_]+)\s*\(", hdr))
     assert declared == set(lib.PRE_SYMBOLS)
