@@ -40,6 +40,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-pre", action="store_true", help="skip the device pre-processing (f1) measurement")
+    ap.add_argument("--shard-transport", default="nccl", choices=["nccl", "torch"],
+                    help="--shard: ncclAllReduce called from the library (default) or torch.distributed through "
+                         "the Python callback")
     ap.add_argument("--shard", action="store_true",
                     help="ONE workload split over the ranks by subdomain (include/ietidp_shard.h, NCCL all-reduce; "
                          "strong scaling) instead of one replica per rank")
@@ -371,8 +374,8 @@ def run_sharded(args, rank, world, local):
     b = make_bundle(args.config)
     owner = ietidp.shard_partition([float(len(sd["K_data"])) for sd in b["subs"]], world)
     stream = torch.cuda.Stream(device=dev)
-    S = ietidp.shard_from_bundle(b, owner, rank, world, ietidp.nccl_allreduce(local), device=local,
-                                 stream=stream.cuda_stream)
+    comm = ietidp.NcclComm(rank, world, local) if args.shard_transport == "nccl" else ietidp.nccl_allreduce(local)
+    S = ietidp.shard_from_bundle(b, owner, rank, world, comm, device=local, stream=stream.cuda_stream)
     S.analyze()
     flush = torch.empty(L2_FLUSH_BYTES // 4, dtype=torch.float32, device=dev)
     ev = lambda: torch.cuda.Event(enable_timing=True)
@@ -413,6 +416,8 @@ def run_sharded(args, rank, world, local):
         "shard": {"subdomains_per_rank": np.bincount(owner, minlength=world).tolist(),
                   "allreduce_doubles_per_iteration": int((2 * b["n_lambda"] + b["n_primal"]) * b["nrhs"]),
                   "us_per_iteration": rep["ms_pcg"] / max(it_max, 1) * 1e3,
+                  "transport": "ncclAllReduce from the library, on its stream" if args.shard_transport == "nccl"
+                  else "torch.distributed all_reduce through the Python callback",
                   "loop": "host-driven, launch by launch (the persistent kernel's grid barrier cannot span GPUs)"},
         "clocks": clk.summary(), "gpu_launches": int(S.kernel_launches() // max(args.steps + args.warmup, 1)),
         "roofline": None, "e2e": None, "cpu_baseline": None,

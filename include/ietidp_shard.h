@@ -49,6 +49,14 @@ typedef int (*ietidp_allreduce_fn)(void* ctx, double* d_buf, int64_t n, void* st
  * selected), E_STATE (after analysis). */
 ietidp_status ietidp_shard_enable(ietidp_t h, int rank, int nranks, ietidp_allreduce_fn fn, void* ctx);
 
+/* The same with NCCL as the transport, called from the library without leaving native code:
+ * nccl_comm is the rank's ncclComm_t and nccl_allreduce the address of ncclAllReduce in the
+ * NCCL library the caller has loaded (the library itself does not link NCCL). Every sum is
+ * one ncclAllReduce(buf, buf, n, ncclFloat64, ncclSum, comm, stream) on the library's stream:
+ * over NVLink 5 / NVSwitch, in-switch reduction (NVLS) where NCCL enables it.
+ * Errors as ietidp_shard_enable. */
+ietidp_status ietidp_shard_enable_nccl(ietidp_t h, int rank, int nranks, void* nccl_comm, void* nccl_allreduce);
+
 /* Contiguous partition of n_sub subdomains over nranks ranks balanced by weight[k] > 0
  * (e.g. factor flops + loop bytes): owner[k] in [0, nranks), non-decreasing in
  * k; every rank gets at least one subdomain when n_sub >= nranks. Host only (no device).

@@ -242,6 +242,29 @@ ietidp_status ietidp_shard_enable(ietidp_t h, int rank, int nranks, ietidp_allre
   });
 }
 
+namespace {
+// ncclAllReduce(sendbuff, recvbuff, count, datatype, op, comm, stream); ncclFloat64 = 8, ncclSum = 0
+typedef int (*nccl_allreduce_t)(const void*, void*, size_t, int, int, void*, cudaStream_t);
+int nccl_trampoline(void* ctx, double* buf, int64_t n, void* stream) {
+  ietidp_s* h = static_cast<ietidp_s*>(ctx);
+  return reinterpret_cast<nccl_allreduce_t>(h->sh_nccl_fn)(buf, buf, (size_t)n, 8, 0, h->sh_nccl_comm,
+                                                           static_cast<cudaStream_t>(stream));
+}
+}  // namespace
+
+ietidp_status ietidp_shard_enable_nccl(ietidp_t h, int rank, int nranks, void* nccl_comm, void* nccl_allreduce) {
+  if (h && (!nccl_comm || !nccl_allreduce)) {
+    h->err = "null NCCL communicator or ncclAllReduce address";
+    return IETIDP_E_ARG;
+  }
+  ietidp_status st = ietidp_shard_enable(h, rank, nranks, nccl_trampoline, h);
+  if (st == IETIDP_OK) {
+    h->sh_nccl_comm = nccl_comm;
+    h->sh_nccl_fn = nccl_allreduce;
+  }
+  return st;
+}
+
 ietidp_status ietidp_shard_partition(int n_sub, const double* weight, int nranks, int32_t* owner) {
   if (n_sub < 1 || nranks < 1 || !weight || !owner) return IETIDP_E_ARG;
   double total = 0.0;
@@ -411,8 +434,10 @@ ietidp_status ietidp_factor(ietidp_t h) {
     // are captured once into a CUDA graph and replayed: the plan and buffers are fixed
     // after analyze, so every factor call launches the same work. Not with the launch
     // tracer; IETIDP_GRAPH=0 launches directly.
-    const bool use_graph =
-        !h->shard && !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
+    const bool use_graph = !h->trace.on && !(getenv("IETIDP_GRAPH") && atoi(getenv("IETIDP_GRAPH")) == 0);
+    // sharded mode: the coarse set-up calls the all-reduce (host side), so only the
+    // factorisation is captured and the coarse set-up is launched directly after it
+    const bool coarse_in_graph = !h->shard;
     try {
       if (use_graph && !h->fgraph) {
         const long long l0 = h->launches;
@@ -421,8 +446,10 @@ ietidp_status ietidp_factor(ietidp_t h) {
         IETI_CUDA(cudaEventRecordWithFlags(h->fg_ev[0], h->stream, cudaEventRecordExternal));
         ieti::run_factor(h);
         IETI_CUDA(cudaEventRecordWithFlags(h->fg_ev[1], h->stream, cudaEventRecordExternal));
-        ieti::run_coarse(h);
-        IETI_CUDA(cudaEventRecordWithFlags(h->fg_ev[2], h->stream, cudaEventRecordExternal));
+        if (coarse_in_graph) {
+          ieti::run_coarse(h);
+          IETI_CUDA(cudaEventRecordWithFlags(h->fg_ev[2], h->stream, cudaEventRecordExternal));
+        }
         IETI_CUDA(cudaStreamEndCapture(h->stream, &g));
         IETI_CUDA(cudaGraphInstantiate(&h->fgraph, g, 0));
         cudaGraphDestroy(g);
@@ -432,6 +459,10 @@ ietidp_status ietidp_factor(ietidp_t h) {
       if (use_graph) {
         IETI_CUDA(cudaGraphLaunch(h->fgraph, h->stream));
         h->launches += h->fgraph_launches;
+        if (!coarse_in_graph) {
+          ieti::run_coarse(h);
+          IETI_CUDA(cudaEventRecord(h->fg_ev[2], h->stream));
+        }
       } else {
         IETI_CUDA(cudaEventRecord(h->fg_ev[0], h->stream));
         h->trace.start(h->stream);

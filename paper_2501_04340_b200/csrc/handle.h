@@ -181,6 +181,8 @@ struct ietidp_s {
   ieti::DevBuf<int> sub_blk0, sub_nt;        // (subdomain, block) rows of each subdomain
   ieti::DevBuf<int> cta_ptr, cta_items;     // persistent PCG: work items per CTA
   int lpt_grid = 0;
+  ieti::DevBuf<int> cta_ptr2, cta_items2;   // the same plan for the standalone streamed pass (k_sym_stream)
+  int lpt2_grid = 0;
   // several-RHS chunk pass of the persistent PCG (pcg.cu sym_chunks), planned for a grid
   int chunk_grid = 0;
   int n_pattern_classes = 0;  // distinct subdomain patterns found by the analysis
@@ -230,6 +232,8 @@ struct ietidp_s {
   int sh_rank = 0, sh_n = 1;
   int (*sh_allreduce)(void*, double*, int64_t, void*) = nullptr;
   void* sh_ctx = nullptr;
+  void* sh_nccl_comm = nullptr;         // native NCCL transport (ietidp_shard_enable_nccl)
+  void* sh_nccl_fn = nullptr;
   ieti::DevBuf<double> sh_kd2;          // K diagonal on the (+, -) sides of every multiplier
   long long sh_reduced_doubles = 0;     // doubles summed over the ranks so far (report)
   ieti::DevBuf<unsigned> gbar;          // its grid barrier

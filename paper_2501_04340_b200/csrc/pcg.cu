@@ -1182,6 +1182,13 @@ __global__ void __launch_bounds__(256, 1) k_sym(const TmvArgs A) {
   sym_item<NCP, STAGES>(A, blockIdx.x, smem);
 }
 
+// The symmetric pass as a launch of its own with the persistent kernel's structure: a
+// resident grid, every CTA streaming its longest-processing-time list of row-segment items
+// through one tile ring (no pipeline refill per item; two CTAs per SM with one RHS).
+template <int NCP, int STAGES>
+__global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1)
+    k_sym_stream(const TmvArgs A, const int* __restrict__ cta_ptr, const int* __restrict__ cta_items);
+
 __global__ void __launch_bounds__(256) k_sym_reduce(const TmvArgs A, const int2* __restrict__ blk) {
   const int2 kb = blk[blockIdx.x];
   sym_reduce_item(A, kb.x, kb.y);
@@ -1317,11 +1324,17 @@ __global__ void __launch_bounds__(1024)
   }
 }
 
+// out[c] = sum over the blocks' partials of column c: a warp per column, lane l adds the
+// blocks l, l + 32, ... (independent loads in flight), then the xor-shuffle tree -- a fixed
+// order, so every CTA (and every rank of a sharded solve) gets bitwise the same sums. Called
+// by all threads of the block.
 __device__ void reduce_cols(const double* part, int nblk, int ncols, double* out_smem) {
-  if (threadIdx.x < ncols) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = warp; c < ncols; c += nw) {
     double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[b * ncols + threadIdx.x];
-    out_smem[threadIdx.x] = s;
+    for (int b = lane; b < nblk; b += 32) s += part[b * ncols + c];
+    s = warp_sum(s);
+    if (lane == 0) out_smem[c] = s;
   }
 }
 
@@ -1629,6 +1642,13 @@ __device__ __forceinline__ void sym_phase(TmvArgs A, const int* cta_ptr, const i
     const int beg = cta_ptr[blockIdx.x], end = cta_ptr[blockIdx.x + 1];
     sym_stream<NCP, STAGES>(A, cta_items + beg, end - beg, smem);
   }
+}
+
+template <int NCP, int STAGES>
+__global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1)
+    k_sym_stream(const TmvArgs A, const int* __restrict__ cta_ptr, const int* __restrict__ cta_items) {
+  extern __shared__ __align__(16) double smem[];
+  sym_phase<NCP, STAGES>(A, cta_ptr, cta_items, NCP, smem);
 }
 
 __shared__ ChunkCtl g_chunk_ctl;  // per CTA (chunk pass): ring mbarriers, tensor memory, stream count
@@ -2728,8 +2748,76 @@ void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const vo
   IETI_LAUNCHED(h);
 }
 
+// Work items over `grid` resident CTAs: longest processing time first (ptr/items lists).
+static void lpt_lists(const ietidp_s* h, int grid, std::vector<int>& ptr, std::vector<int>& items) {
+  const bool expl = h->opt.loop == IETIDP_LOOP_EXPLICIT;  // items: row segments, or block pairs
+  const int nitems = expl ? h->n_symwork : h->n_loopwork;
+  std::vector<std::pair<int, int>> cost(nitems);
+  for (int i = 0; i < nitems; ++i) cost[i] = {expl ? h->h_symwork[i].cost : h->h_loopwork[i].cost, i};
+  std::sort(cost.begin(), cost.end(), [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second < y.second); });
+  std::vector<std::vector<int>> lists(grid);
+  std::vector<std::pair<long long, int>> heap;
+  for (int b = 0; b < grid; ++b) heap.push_back({0, b});
+  auto cmp = [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second > y.second); };
+  std::make_heap(heap.begin(), heap.end(), cmp);
+  for (auto& c : cost) {
+    std::pop_heap(heap.begin(), heap.end(), cmp);
+    heap.back().first += c.first;
+    lists[heap.back().second].push_back(c.second);
+    std::push_heap(heap.begin(), heap.end(), cmp);
+  }
+  ptr.assign(grid + 1, 0);
+  items.clear();
+  for (int b = 0; b < grid; ++b) {
+    items.insert(items.end(), lists[b].begin(), lists[b].end());
+    ptr[b + 1] = (int)items.size();
+  }
+}
+
+// IETIDP_SYM_STREAM=0: one CTA per item (round 1's launch) instead of the streamed pass
+static bool sym_stream_enabled() {
+  static const bool on = !(getenv("IETIDP_SYM_STREAM") && atoi(getenv("IETIDP_SYM_STREAM")) == 0);
+  return on;
+}
+
+// out[slot][c] = sign * weight * x[multiplier of the slot][c]: B^T x (or B_D^T x) in slot order,
+// the input form of the streamed pass
+__global__ void __launch_bounds__(256) k_to_slots(long long n_slots, int ncols, const int* __restrict__ slot_lam,
+                                                  const float* __restrict__ slot_sign, const double* __restrict__ weight,
+                                                  const double* __restrict__ x, double* __restrict__ out,
+                                                  const PcgState* __restrict__ st) {
+  if (st && st->done) return;
+  for (long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x; e < n_slots * ncols;
+       e += (long long)gridDim.x * blockDim.x) {
+    const long long a = e / ncols;
+    const int c = (int)(e - a * ncols);
+    out[e] = (double)slot_sign[a] * (weight ? weight[a] : 1.0) * x[(long long)slot_lam[a] * ncols + c];
+  }
+}
+
 template <int NCP, int STAGES>
 static void launch_sym_t(ietidp_s* h, const TmvCfg& cfg, TmvArgs a) {
+  if (a.slot_in && sym_stream_enabled() && h->opt.loop == IETIDP_LOOP_EXPLICIT) {
+    auto kern = k_sym_stream<NCP, STAGES>;
+    IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
+    int per_sm = 0, nsm = 0;
+    IETI_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 256, cfg.smem));
+    IETI_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->opt.device));
+    if (per_sm >= 1) {
+      const int grid = std::min(nsm * per_sm, 1024);
+      if (h->lpt2_grid != grid) {
+        std::vector<int> ptr, items;
+        lpt_lists(h, grid, ptr, items);
+        h->cta_ptr2.upload(ptr, h->stream);
+        h->cta_items2.upload(items, h->stream);
+        IETI_CUDA(cudaStreamSynchronize(h->stream));  // the host vectors go out of scope
+        h->lpt2_grid = grid;
+      }
+      kern<<<grid, 256, cfg.smem, h->stream>>>(a, h->cta_ptr2.p, h->cta_items2.p);
+      IETI_LAUNCHED(h);
+      return;
+    }
+  }
   auto kern = k_sym<NCP, STAGES>;
   IETI_CUDA(cudaFuncSetAttribute((const void*)kern, cudaFuncAttributeMaxDynamicSharedMemorySize, cfg.smem));
   kern<<<h->n_symwork, 256, cfg.smem, h->stream>>>(a);
@@ -2740,6 +2828,18 @@ static void launch_sym_t(ietidp_s* h, const TmvCfg& cfg, TmvArgs a) {
 static void sym_apply(ietidp_s* h, TmvArgs a) {
   if (h->n_symwork == 0) return;
   const TmvCfg cfg = tmv_cfg(h, a.ncols, true);
+  if (!a.slot_in && sym_stream_enabled() && h->n_slots > 0) {  // the streamed pass reads slot order
+    if (h->pslot.n < (size_t)h->n_slots * h->nrhs) {
+      h->pslot.alloc((size_t)h->n_slots * h->nrhs);
+      h->rslot.alloc((size_t)h->n_slots * h->nrhs);
+    }
+    k_to_slots<<<grid_for((long long)h->n_slots * a.ncols, 256), 256, 0, h->stream>>>(
+        h->n_slots, a.ncols, h->slot_lam.p, h->slot_sign.p, a.weight, a.vin, h->pslot.p, a.st);
+    IETI_LAUNCHED(h);
+    a.vin = h->pslot.p;
+    a.slot_in = 1;
+    a.weight = nullptr;
+  }
   for (int c0 = 0; c0 < a.ncols; c0 += cfg.ncp) {
     a.c_off = c0;
     if (cfg.ncp == 1 && cfg.stages == 2) launch_sym_t<1, 2>(h, cfg, a);
@@ -3009,27 +3109,8 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
   if (per_sm < 1) return false;
   const int grid = std::min(nsm * per_sm, 1024);
   if (h->lpt_grid != grid) {  // items over the persistent CTAs: longest processing time first
-    const bool expl = h->opt.loop == IETIDP_LOOP_EXPLICIT;  // items: row segments, or block pairs
-    const int nitems = expl ? h->n_symwork : h->n_loopwork;
-    std::vector<std::pair<int, int>> cost(nitems);
-    for (int i = 0; i < nitems; ++i) cost[i] = {expl ? h->h_symwork[i].cost : h->h_loopwork[i].cost, i};
-    std::sort(cost.begin(), cost.end(), [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second < y.second); });
-    std::vector<std::vector<int>> lists(grid);
-    std::vector<std::pair<long long, int>> heap;
-    for (int b = 0; b < grid; ++b) heap.push_back({0, b});
-    auto cmp = [](auto& x, auto& y) { return x.first > y.first || (x.first == y.first && x.second > y.second); };
-    std::make_heap(heap.begin(), heap.end(), cmp);
-    for (auto& c : cost) {
-      std::pop_heap(heap.begin(), heap.end(), cmp);
-      heap.back().first += c.first;
-      lists[heap.back().second].push_back(c.second);
-      std::push_heap(heap.begin(), heap.end(), cmp);
-    }
-    std::vector<int> ptr(grid + 1, 0), items;
-    for (int b = 0; b < grid; ++b) {
-      items.insert(items.end(), lists[b].begin(), lists[b].end());
-      ptr[b + 1] = (int)items.size();
-    }
+    std::vector<int> ptr, items;
+    lpt_lists(h, grid, ptr, items);
     h->cta_ptr.upload(ptr, h->stream);
     h->cta_items.upload(items, h->stream);
     h->lpt_grid = grid;
@@ -3289,15 +3370,40 @@ void run_solve(ietidp_s* h) {
     k_init_rz<<<1, 64, 0, s>>>(st, rz_part);
     IETI_LAUNCHED(h);
     if (h->shard) {
-      // the all-reduce callback runs on the host side: the loop is driven from the host; every
-      // rank reads the same replicated state and takes the same decision
-      for (;;) {
-        int itdone[2];
-        IETI_CUDA(cudaMemcpyAsync(itdone, st, sizeof(itdone), cudaMemcpyDeviceToHost, s));
+      // The all-reduce is the caller's, so the loop is driven from the host. Every rank reads
+      // the same replicated state and takes the same decision. The stop flag of iteration i is
+      // read after iteration i + 1 has been enqueued (one iteration of look-ahead keeps the GPU
+      // fed while the host waits); the extra iteration launched past convergence is a no-op:
+      // every kernel returns at once when st->done is set, and the sums over the ranks then
+      // touch only q and z, which nothing reads afterwards.
+      int* flag = nullptr;  // pinned {it, done}
+      IETI_CUDA(cudaMallocHost(&flag, 2 * sizeof(int)));
+      cudaEvent_t fev = nullptr;
+      try {
+        IETI_CUDA(cudaEventCreateWithFlags(&fev, cudaEventDisableTiming));
+        flag[0] = flag[1] = 0;
+        IETI_CUDA(cudaMemcpyAsync(flag, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         IETI_CUDA(cudaStreamSynchronize(s));
-        if (itdone[1]) break;
-        iteration_body(h, st, 0);
+        if (!flag[1]) {
+          iteration_body(h, st, 0);
+          IETI_CUDA(cudaMemcpyAsync(flag, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+          IETI_CUDA(cudaEventRecord(fev, s));
+          for (;;) {
+            iteration_body(h, st, 0);                // the next iteration, speculatively
+            IETI_CUDA(cudaEventSynchronize(fev));    // the flag after the previous one
+            if (flag[1]) break;
+            IETI_CUDA(cudaMemcpyAsync(flag, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+            IETI_CUDA(cudaEventRecord(fev, s));
+          }
+        }
+        IETI_CUDA(cudaStreamSynchronize(s));
+      } catch (...) {
+        if (fev) cudaEventDestroy(fev);
+        cudaFreeHost(flag);
+        throw;
       }
+      cudaEventDestroy(fev);
+      cudaFreeHost(flag);
       IETI_CHECK_LAUNCH();
       return;
     }

@@ -41,7 +41,7 @@ class Options(C.Structure):
 
 
 # every entry point include/ietidp_shard.h declares (sharded multi-GPU solve)
-SHARD_SYMBOLS = ["ietidp_shard_enable", "ietidp_shard_partition"]
+SHARD_SYMBOLS = ["ietidp_shard_enable", "ietidp_shard_enable_nccl", "ietidp_shard_partition"]
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p)
 
 
@@ -113,6 +113,7 @@ def load():
         "ietidp_status_string": (C.c_char_p, [I]),
         "ietidp_destroy": (None, [P]),
         "ietidp_shard_enable": (I, [P, I, I, ALLREDUCE_FN, P]),
+        "ietidp_shard_enable_nccl": (I, [P, I, I, P, P]),
         "ietidp_shard_partition": (I, [I, P, I, P]),
         "ietidp_pre_assemble": (I, [I, C.POINTER(PreSubdomain), C.POINTER(P)]),
         "ietidp_pre_assemble_batch": (I, [I, I, C.POINTER(PreSubdomain), C.POINTER(P)]),
@@ -197,6 +198,11 @@ class Solver:
                 return 1
         self._allreduce = ALLREDUCE_FN(thunk)  # keep the trampoline alive with the handle
         self._check(self.lib.ietidp_shard_enable(self.h, rank, nranks, self._allreduce, None))
+
+    def shard_enable_nccl(self, rank, nranks, comm):
+        """Sharded mode with the native NCCL transport: comm = NcclComm (below)."""
+        self._nccl = comm
+        self._check(self.lib.ietidp_shard_enable_nccl(self.h, rank, nranks, comm.comm, comm.allreduce_addr))
 
     def analyze(self):
         self._check(self.lib.ietidp_analyze(self.h))
@@ -438,6 +444,44 @@ def shard_partition(weights, nranks):
     return owner
 
 
+class NcclComm:
+    """An ncclComm_t of this process created through ctypes on the NCCL library torch has
+    loaded (marshalling only): rank 0 draws the unique id, torch.distributed broadcasts its
+    128 bytes, every rank calls ncclCommInitRank. The library then calls ncclAllReduce itself."""
+
+    class _Uid(C.Structure):
+        _fields_ = [("internal", C.c_byte * 128)]
+
+    def __init__(self, rank, world, device):
+        import glob
+        import torch
+        import torch.distributed as dist
+        cands = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "nccl", "lib", "libnccl.so*"))
+        self.lib = C.CDLL(cands[0] if cands else "libnccl.so.2")
+        uid = self._Uid()
+        if rank == 0:
+            rc = self.lib.ncclGetUniqueId(C.byref(uid))
+            if rc != 0:
+                raise RuntimeError(f"ncclGetUniqueId failed ({rc})")
+        if world > 1:
+            t = torch.tensor(list(bytes(uid)), dtype=torch.uint8, device=torch.device("cuda", device))
+            dist.broadcast(t, src=0)
+            C.memmove(C.byref(uid), bytes(t.cpu().tolist()), 128)
+        self.comm = C.c_void_p()
+        torch.cuda.set_device(device)
+        self.lib.ncclCommInitRank.argtypes = [C.POINTER(C.c_void_p), C.c_int, self._Uid, C.c_int]
+        rc = self.lib.ncclCommInitRank(C.byref(self.comm), world, uid, rank)
+        if rc != 0:
+            raise RuntimeError(f"ncclCommInitRank failed ({rc})")
+        self.allreduce_addr = C.cast(self.lib.ncclAllReduce, C.c_void_p)
+
+    def close(self):
+        if self.comm:
+            self.lib.ncclCommDestroy.argtypes = [C.c_void_p]
+            self.lib.ncclCommDestroy(self.comm)
+            self.comm = None
+
+
 def shard_from_bundle(b, owner, rank, nranks, allreduce, **opts):
     """A sharded Solver holding the subdomains k of a generator bundle with owner[k] == rank
     (local ids in ascending global order; multiplier and primal ids stay global)."""
@@ -445,7 +489,10 @@ def shard_from_bundle(b, owner, rank, nranks, allreduce, **opts):
     opts.setdefault("tol", b["tol"])
     mine = [k for k in range(b["n_sub"]) if owner[k] == rank]
     s = Solver(len(mine), b["n_lambda"], b["n_primal"], b["nrhs"], **opts)
-    s.shard_enable(rank, nranks, allreduce)
+    if isinstance(allreduce, NcclComm):
+        s.shard_enable_nccl(rank, nranks, allreduce)
+    else:
+        s.shard_enable(rank, nranks, allreduce)
     for i, k in enumerate(mine):
         sd = b["subs"][k]
         s.set_subdomain(i, sd["K_indptr"], sd["K_indices"], sd["K_data"], sd["f"], sd["B_lambda"], sd["B_dof"],

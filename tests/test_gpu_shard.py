@@ -41,21 +41,25 @@ class HostSumComm:
         self.views = [None] * nranks
         self.calls = 0
         self.doubles = 0
+        self.side = torch.cuda.Stream()  # the sums run here (non-blocking stream)
 
     def fn(self, rank):
         def allreduce(ptr, n, stream):
             torch = self.torch
-            torch.cuda.synchronize()
+            # stream-level waits only: another rank's thread may be capturing its factorisation
+            # graph, during which a device-wide synchronisation is not permitted
+            torch.cuda.ExternalStream(int(stream)).synchronize()
             self.views[rank] = torch.as_tensor(self.lib.CudaView(ptr, n), device="cuda")
             self.bar.wait()
             if rank == 0:
                 assert all(v.numel() == n for v in self.views)
-                total = self.views[0].clone()
-                for r in range(1, self.n):
-                    total += self.views[r]
-                for r in range(self.n):
-                    self.views[r].copy_(total)
-                torch.cuda.synchronize()
+                with torch.cuda.stream(self.side):
+                    total = self.views[0].clone()
+                    for r in range(1, self.n):
+                        total += self.views[r]
+                    for r in range(self.n):
+                        self.views[r].copy_(total)
+                self.side.synchronize()
                 self.calls += 1
                 self.doubles += n
             self.bar.wait()
