@@ -20,7 +20,7 @@ class Config:
     tiling: tuple          # subdomains per axis; each subdomain is a box of patches
     geometry: str = "cube"  # "cube" (unit cube) | "cylinder" (hollow, periodic theta)
     material: str = "one"   # "one" | "c3_block" | "c4_outer" | "c5_random"
-    rhs: str = "astar"      # "astar" | "c3" | "c4" | "c5_random"
+    rhs: str = "astar"      # "astar" | "c3" | "c4" | "c5_random" | "aana" (the paper's A_ana, inhomogeneous n x A)
     nrhs: int = 1
     scaling: str = "multiplicity"  # "multiplicity" | "stiffness"
     tol: float = 1e-10
@@ -58,6 +58,7 @@ EXTRA = {"C5s": replace(C5, name="C5s", e=2, tiling=(8, 8, 8))}
 
 def get(name: str) -> Config:
     """'C2' -> full config; 'C2r' -> reduced e=2 variant; 'C1e4' -> C1 with e=4;
+    'E27A_...' -> the 27-patch family with the paper's A_ana and its boundary values lifted;
     'C4m<p>e<e>' -> the cylinder with the manufactured A* = sin(2 pi (r - 1/2)) e_z;
     'E27_<tiling or partition>_p<p>_e<e>' -> the paper's 27-patch family."""
     if name in CONFIGS:
@@ -66,6 +67,8 @@ def get(name: str) -> Config:
         return EXTRA[name]
     if name.startswith("E27_"):
         return paper_cube(name)
+    if name.startswith("E27A_"):
+        return replace(paper_cube("E27_" + name[5:]), name=name, rhs="aana")
     if name.startswith("C4m"):
         p, e = name[3:].split("e")
         return replace(C4, name=name, p=int(p), e=int(e), material="one", rhs="c4_manufactured",
@@ -155,6 +158,10 @@ def source_terms(cfg: Config):
         return [[Tx, Ty, Tz]]
     if cfg.rhs == "c3":
         return [[[], [], [(1.0, ("sin", 1), ("sin", 1), ("sin", 1))]]]
+    if cfg.rhs == "aana":
+        # T = nu B_ana = curl A_ana = (-3 cos x sin y sin z, 0, 3 cos z sin x sin y)
+        return [[[(-3.0, ("cosx", 0), ("sinx", 0), ("sinx", 0))], [],
+                 [(3.0, ("sinx", 0), ("sinx", 0), ("cosx", 0))]]]
     if cfg.rhs == "c5_random":
         a = c5_coefficients(cfg)
         out = []
@@ -179,4 +186,15 @@ def f1d(spec):
         return lambda x: np.sin(k * np.pi * x)
     if kind == "cos":
         return lambda x: np.cos(k * np.pi * x)
+    if kind == "sinx":
+        return lambda x: np.sin(x)
+    if kind == "cosx":
+        return lambda x: np.cos(x)
     return lambda x: np.ones_like(x)
+
+
+# The paper's closed-form solution, per component a separable product
+# coef * fx(x) fy(y) fz(z): A_ana = (cos y cos z sin x, -2 cos x cos z sin y, cos x cos y sin z).
+A_ANA = [(1.0, ("sinx", 0), ("cosx", 0), ("cosx", 0)),
+         (-2.0, ("cosx", 0), ("sinx", 0), ("cosx", 0)),
+         (1.0, ("cosx", 0), ("cosx", 0), ("sinx", 0))]

@@ -450,6 +450,7 @@ class Problem:
                 K = Kb if K is None else K + Kb
                 np.add.at(j, loc, C.T @ cube_face_loads(self.cfg, bx, spaces))
             m = sd.local_mask
+            j = self._lift(sd, K, j)
             K = K[m][:, m].tocsr()
             K = ((K + K.T) * 0.5).tocsr()
             K.sort_indices()
@@ -461,6 +462,7 @@ class Problem:
         t = cube_face_loads(self.cfg, sd, spaces)
         j = C.T @ t
         m = sd.local_mask
+        j = self._lift(sd, K, j)
         K = K[m][:, m].tocsr()
         # C^T M2 C in floating point is symmetric only up to rounding, and SpGEMM
         # drops an entry that cancels to exactly 0.0 on one side only: store the
@@ -472,6 +474,72 @@ class Problem:
         if with_face:
             return K, j, C[:, m], M2, t
         return K, j
+
+    # ---- inhomogeneous boundary values (n x A = n x A_ana) ----
+    def dirichlet_values(self):
+        """Global edge vector: the coefficients of the boundary (Dirichlet) edges of the
+        spline interpolant of A_ana, zero elsewhere. Every component of A_ana is a product
+        coef * fx(x) fy(y) fz(z), so its tensor-product projection is the Kronecker product
+        of three 1-D projections: L2 along the component's own axis (D-splines), L2 with
+        the two end coefficients fixed to the exact end values across it (B-splines; open
+        knots make them interpolatory there), which makes the tangential trace on each
+        boundary face exact in the normal direction and a face-wise projection within it."""
+        if getattr(self, "_aD", None) is not None:
+            return self._aD
+        cfg, g = self.cfg, self.grid
+        assert cfg.geometry == "cube" and cfg.rhs == "aana"
+        from .splines import Space1D
+        nq = cfg.p + cfg.load_nq_extra
+        sp1 = [Space1D(0.0, 1.0, cfg.npatch[a], cfg.e, cfg.p) for a in range(3)]
+
+        def proj(a, kind, f):
+            S = sp1[a]
+            M = sum(S.mass(kind, q, nq) for q in range(S.npatch))
+            v = S.integrals(kind, f, nq)
+            if kind == "D":
+                return np.linalg.solve(M, v)
+            c = np.zeros(S.m)
+            c[0], c[-1] = f(np.array([0.0]))[0], f(np.array([1.0]))[0]
+            I = np.arange(1, S.m - 1)
+            c[I] = np.linalg.solve(M[np.ix_(I, I)], v[I] - M[np.ix_(I, [0, S.m - 1])] @ c[[0, -1]])
+            return c
+        a_all = np.zeros(g.ne)
+        for d in range(3):
+            coef, *specs = cf.A_ANA[d]
+            c1 = [proj(a, "D" if a == d else "B", cf.f1d(specs[a])) for a in range(3)]
+            a_all[g.eoff[d]:g.eoff[d + 1]] = coef * np.einsum("i,j,k->kji", c1[0], c1[1], c1[2]).ravel()
+        self._a_interp = a_all
+        self._aD = np.where(self.dir_edge, a_all, 0.0)
+        return self._aD
+
+    def _lift(self, sd, K_full, j_full):
+        """j <- j - K[:, Dirichlet] a_D on the subdomain's full (unmasked) edge set."""
+        if self.cfg.rhs != "aana":
+            return j_full
+        aD = self.dirichlet_values()[self.sub_edges[sd.idx]]
+        return j_full - (K_full @ aD)[:, None]
+
+    def flux_error(self, us, bnorm2):
+        """eps_B of the subdomain solutions us: ||B_h - B||^2 =
+        sum over the patches of b^T M2 b - 2 b^T t + ||B||^2, b = C a on the patch, a the
+        global edge vector (subdomain solutions + boundary values), t_f = int B . v_f."""
+        g, cfg = self.grid, self.cfg
+        a = self.dirichlet_values().copy() if cfg.rhs == "aana" else np.zeros(g.ne)
+        for sd, u in zip(self.subs, us):
+            a[sd.gid] = u[:, 0]
+        N = cfg.npatch
+        tot = 0.0
+        for pz in range(N[2]):
+            for py in range(N[1]):
+                for px in range(N[0]):
+                    bx = Subdomain(0, (px, py, pz), (px + 1, py + 1, pz + 1))
+                    gb, ml = g.block_edges(bx.lo, bx.hi)
+                    spaces = cube_spaces(cfg, bx)
+                    bf = local_curl(ml) @ a[gb]
+                    M2 = cube_mass2(cfg, bx, spaces, self.nu)
+                    t = cube_face_loads(cfg, bx, spaces)[:, 0]
+                    tot += bf @ (M2 @ bf) - 2.0 * bf @ t
+        return float(np.sqrt(max(tot + bnorm2, 0.0)))
 
     def counts(self):
         g = self.grid

@@ -7,6 +7,8 @@
 #include <cstring>
 #include <new>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "handle.h"
 #include "../../include/ietidp_shard.h"
 
@@ -38,6 +40,15 @@ ietidp_status guard(ietidp_t h, F&& f) {
     return IETIDP_E_CUDA;
   }
 }
+
+// NVTX range of one API phase (visible in Nsight Systems / ncu --nvtx; no cost without a tool
+// attached: the header-only NVTX v3 resolves to no-ops until an injection library is loaded)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 void require(bool c, ietidp_status st, const char* msg) {
   if (!c) throw Error(st, msg);
@@ -295,6 +306,7 @@ ietidp_status ietidp_analyze(ietidp_t h) {
   return guard(h, [&]() {
     require(!h->analyzed, IETIDP_E_STATE, "already analyzed");
     if (h->opt.device >= 0) set_device(h);
+    NvtxRange nv("ietidp_analyze");
     ieti::analyze_all(h);
     if (h->opt.device >= 0) {
       // The copy stream and the per-subdomain copy events exist before the first
@@ -411,6 +423,7 @@ ietidp_status ietidp_factor(ietidp_t h) {
     if (st != IETIDP_OK) return st;
   }
   return guard(h, [&]() {
+    NvtxRange nv("ietidp_factor");
     set_device(h);
     h->factored = false;
     h->solved = false;
@@ -520,7 +533,11 @@ ietidp_status ietidp_solve(ietidp_t h, double* lambda, ietidp_report* report) {
     EvPair e1, e2;
     IETI_CUDA(cudaEventRecord(e1.a, h->stream));
     h->trace.start(h->stream);
-    ieti::run_solve(h);
+    {
+      NvtxRange nv("ietidp_solve: PCG");
+      ieti::run_solve(h);
+    }
+    NvtxRange nvr("ietidp_solve: recovery");
     IETI_CUDA(cudaEventRecord(e1.b, h->stream));
     IETI_CUDA(cudaEventRecord(e2.a, h->stream));
     // the recovery's ~40 launches (backward sweep level by level) as a captured graph

@@ -314,3 +314,70 @@ def test_uneven_tiling_dd_equals_monolithic(name):
     um, _, _, _ = brute.monolithic_solve(b)
     U, Um = np.concatenate(res["u"]), np.concatenate(um)
     assert np.linalg.norm(U - Um) <= 1e-10 * np.linalg.norm(Um)
+
+
+# ---- the paper's A_ana with inhomogeneous boundary values ----
+
+def _bana_norm2():
+    # ||B_ana||^2 over (0,1)^3, B_ana = (-3 cos x sin y sin z, 0, 3 cos z sin x sin y):
+    # 9 (C S S + S S C), C = int cos^2 = 1/2 + sin(2)/4, S = int sin^2 = 1/2 - sin(2)/4
+    C, S = 0.5 + np.sin(2.0) / 4, 0.5 - np.sin(2.0) / 4
+    return 18.0 * C * S * S
+
+
+def test_aana_identities():
+    """curl curl A_ana = 3 A_ana, div A_ana = 0 and B_ana = curl A_ana,
+    checked by central differences at seeded points: the source T = B_ana and the lifted
+    boundary data belong to the same closed-form solution."""
+    from ietigen import configs as cf
+    from ietigen.rng import SplitMix64
+
+    def A(x):
+        return np.array([c * cf.f1d(fx)(x[0:1])[0] * cf.f1d(fy)(x[1:2])[0] * cf.f1d(fz)(x[2:3])[0]
+                         for c, fx, fy, fz in cf.A_ANA])
+
+    def B(x):
+        out = np.zeros(3)
+        for s_, col in enumerate(cf.source_terms(cf.get("E27A_311_p1_e1"))[0]):
+            for c, fx, fy, fz in col:
+                out[s_] += c * cf.f1d(fx)(x[0:1])[0] * cf.f1d(fy)(x[1:2])[0] * cf.f1d(fz)(x[2:3])[0]
+        return out
+
+    def curl(F, x, h=1e-5):
+        J = np.zeros((3, 3))
+        for j in range(3):
+            e = np.zeros(3)
+            e[j] = h
+            J[:, j] = (F(x + e) - F(x - e)) / (2 * h)
+        return np.array([J[2, 1] - J[1, 2], J[0, 2] - J[2, 0], J[1, 0] - J[0, 1]]), np.trace(J)
+    g = SplitMix64(11)
+    for _ in range(5):
+        x = np.array([0.1 + 0.8 * g.uniform() for _ in range(3)])
+        cA, divA = curl(A, x)
+        assert np.allclose(cA, B(x), atol=1e-8) and abs(divA) < 1e-8
+        ccA, _ = curl(lambda y: curl(A, y)[0], x, h=1e-3)
+        assert np.allclose(ccA, 3 * A(x), atol=1e-5)
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_aana_flux_error_order(p):
+    """eps_B = O(h^p) for the paper's A_ana with its boundary values lifted (PAPER.md:258,
+    Fig. 4b), on a box tiling and on E1's union-of-patches partition (the lifting goes
+    through both assembly branches); DD = monolithic."""
+    from oracle import brute, dp
+    bn2 = _bana_norm2()
+    errs = []
+    for e in (1, 2, 4):
+        b, P = make_bundle(f"E27A_311_p{p}_e{e}", with_problem=True)
+        res = dp.solve(b, tol=1e-12)
+        errs.append(P.flux_error(res["u"], bn2))
+    eoc = np.log2(np.array(errs[:-1]) / np.array(errs[1:]))
+    assert np.all(np.abs(eoc - p) <= 0.3), (errs, eoc)
+    b, P = make_bundle(f"E27A_L3_p{p}_e2", with_problem=True)
+    res = dp.solve(b, tol=1e-12)
+    assert abs(P.flux_error(res["u"], bn2) - errs[1]) <= 1e-3 * errs[1]  # same field, another partition
+    um, _, _, _ = brute.monolithic_solve(b)
+    assert abs(P.flux_error(um, bn2) - P.flux_error(res["u"], bn2)) <= 1e-9 * errs[1]
+    # without the lifting the boundary data is wrong and the error does not converge
+    P._aD = np.zeros_like(P._aD)
+    assert P.flux_error(res["u"], bn2) > 10 * errs[1]

@@ -358,6 +358,26 @@ def test_paper_e1_partition(lib):
     assert 1.5 <= k[0] <= 5.5
 
 
+def test_paper_e1_aana_flux_error(lib):
+    """E1 with the paper's own solution A_ana and its boundary values lifted into the loads
+    (ietigen Problem.dirichlet_values): the GPU solution's flux error
+    eps_B equals the oracle's to 1e-8 relative and halves-squared with h (p = 2: EOC 2 +- 0.3
+    between e = 2 and e = 4), with the paper's stopping rule at eta_tol = 1e-10 so that the
+    algebraic error stays below the discretisation error."""
+    C, S = 0.5 + np.sin(2.0) / 4, 0.5 - np.sin(2.0) / 4
+    bn2 = 18.0 * C * S * S
+    errs = []
+    for e in (2, 4):
+        b, P = make_bundle(f"E27A_L3_p2_e{e}", with_problem=True)
+        ref = dp.solve(b, tol=1e-10, stop="preconditioned")
+        s, lam, u, rep = gpu_solve(lib, b, tol=1e-10, stop="preconditioned")
+        assert abs(rep["iters"][0] - int(ref["iters"][0])) <= 1
+        eg, eo = P.flux_error(u, bn2), P.flux_error(ref["u"], bn2)
+        assert abs(eg - eo) <= 1e-8 * eo
+        errs.append(eg)
+    assert abs(np.log2(errs[0] / errs[1]) - 2) <= 0.3, errs
+
+
 @pytest.mark.parametrize("name", ["E27_322_p2_e2", "E27_221_p3_e2"])
 def test_paper_cube_family(lib, name):
     """The paper's 27-patch experiment family with uneven box tilings (PAPER.md:268,
