@@ -176,6 +176,14 @@ ietidp_status ietidp_analyze(ietidp_t h);
  * have arrived, so the transfer overlaps the factorisation of earlier groups. */
 ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const double* f);
 
+/* The same from DEVICE buffers on the handle's device (e.g. the matrix the device assembly
+ * of ietidp_pre.h has just produced, ietidp_pre_device_ptrs): d_K_val[nnz] in the CSR order
+ * of ietidp_set_subdomain, d_f[n_k*nrhs] column-major; device-to-device copies on the
+ * handle's stream, so work the caller has ordered before this call on that stream (or
+ * completed) is visible. Either pointer may be NULL.
+ * Errors: E_STATE (before analysis, host-only handle), E_ARG (k out of range), E_CUDA. */
+ietidp_status ietidp_set_values_device(ietidp_t h, int k, const double* d_K_val, const double* d_f);
+
 /* The same with half the bytes: K_lower_val holds only the values of the stored entries
  * (i, j) with j <= i of subdomain k's CSR pattern, in CSR order (row by row, columns
  * ascending) -- K is symmetric (K = C^T M_2 C), so an upper entry's value is its

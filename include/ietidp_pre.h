@@ -105,6 +105,19 @@ int ietidp_pre_sizes(ietidp_pre_t a, int* n_dof, int64_t* nnz, double* ms, doubl
  * ietidp_set_subdomain. Any pointer may be NULL. */
 int ietidp_pre_get(ietidp_pre_t a, int64_t* rowptr, int32_t* col, double* val, double* f);
 
+/* New reluctivities, same discretisation: nu_all holds every subdomain's nu array of the
+ * handle's batch, concatenated in batch order (host). Only the value kernel reruns; pattern,
+ * Gram tables and loads are unchanged (the loads do not depend on nu). ms = its device time.
+ * The values are rewritten in place (the device pointers stay valid). */
+int ietidp_pre_refill(ietidp_pre_t a, const double* nu_all, double* ms);
+
+/* Device pointers of the assembled values and loads (owned by the handle's batch; valid until
+ * its last handle is destroyed; the assembly has completed when ietidp_pre_assemble[_batch]
+ * returns): d_val[nnz] in the CSR order of ietidp_pre_get, d_f[n_dof*nrhs] column-major --
+ * the arguments of ietidp_set_values_device, which keeps the matrix on the device between
+ * assembly and factorisation. Any pointer may be NULL. */
+int ietidp_pre_device_ptrs(ietidp_pre_t a, const double** d_val, const double** d_f);
+
 /* The 1-D Gram block of component c, axis a, patch q (host, nb x nb column-major, nb =
  * e+p for the B kind (a == c), e+p-1 for the D kind): test access to the first stage. */
 int ietidp_pre_get_gram(ietidp_pre_t a, int c, int axis, int q, double* block, int* nb);

@@ -347,6 +347,30 @@ ietidp_status ietidp_set_values(ietidp_t h, int k, const double* K_val, const do
   });
 }
 
+ietidp_status ietidp_set_values_device(ietidp_t h, int k, const double* d_K_val, const double* d_f) {
+  return guard(h, [&]() {
+    require(h->analyzed, IETIDP_E_STATE, "set_values before analysis");
+    require(k >= 0 && k < h->n_sub, IETIDP_E_ARG, "subdomain index out of range");
+    const ieti::SubIn& in = h->in[k];
+    require(h->cstream != nullptr, IETIDP_E_STATE, "set_values on a host-only handle");
+    // device-to-device on the handle's stream (the producer's work on that stream, e.g. the
+    // assembly kernels' results made visible by the caller, is ordered before it); the copy
+    // stream's event of the subdomain is re-recorded behind it so that the captured
+    // factorisation graph's external wait still covers the latest values
+    if (d_K_val)
+      IETI_CUDA(cudaMemcpyAsync(h->kval.p + h->kval_off[k], d_K_val, in.val.size() * sizeof(double),
+                                cudaMemcpyDeviceToDevice, h->stream));
+    if (d_f)
+      IETI_CUDA(cudaMemcpyAsync(h->fval.p + h->fval_off[k], d_f, (size_t)in.n * h->nrhs * sizeof(double),
+                                cudaMemcpyDeviceToDevice, h->stream));
+    IETI_CUDA(cudaEventRecord(h->hp_ev_set, h->stream));
+    IETI_CUDA(cudaStreamWaitEvent(h->cstream, h->hp_ev_set, 0));
+    IETI_CUDA(cudaEventRecord(h->kev[k], h->cstream));
+    h->factored = false;
+    h->solved = false;
+  });
+}
+
 // the lower-triangle maps of every pattern class (host integer work, once)
 static void prepare_lower(ietidp_t h) {
   const int ns = h->n_sub;

@@ -648,6 +648,8 @@ struct PreBatch {
   Buf<int> cnt, col;
   Buf<double> val, f;
   double ms = 0.0, ms_fill = 0.0;
+  std::vector<size_t> nu_off, nu_cnt;  // arena offsets / counts of every subdomain's nu
+  int gx = 1, smem = 0;                // launch shape of k_rows
 };
 
 }  // namespace
@@ -878,6 +880,12 @@ int ietidp_pre_assemble_batch(int device, int n, const ietidp_pre_subdomain* sub
     B->d_boxes.upload(B->boxes.data(), n);
     PRE_CUDA(cudaFuncSetAttribute((const void*)k_rows<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
     const int gx = std::max(1, (max_dof + ROWS_WARPS - 1) / ROWS_WARPS);
+    B->gx = gx;
+    B->smem = smem;
+    for (int k = 0; k < n; ++k) {
+      B->nu_off.push_back(fix[k].nu);
+      B->nu_cnt.push_back((size_t)B->boxes[k].np[0] * B->boxes[k].np[1] * B->boxes[k].np[2]);
+    }
     PRE_CUDA(cudaEventRecord(ev[0]));
     k_stage1d<<<n, 256>>>(B->d_boxes.p);
     k_rows<0><<<dim3(gx, n), 32 * ROWS_WARPS>>>(B->d_boxes.p);
@@ -955,6 +963,46 @@ int ietidp_pre_get(ietidp_pre_t a, int64_t* rowptr, int32_t* col, double* val, d
   } catch (const std::pair<int, std::string>& ex) {
     return fail(ex.first, ex.second);
   }
+}
+
+int ietidp_pre_refill(ietidp_pre_t a, const double* nu_all, double* ms) {
+  if (!a || !nu_all) return fail(IETIDP_E_ARG, "null argument");
+  PreBatch& B = *a->batch;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  try {
+    PRE_CUDA(cudaSetDevice(B.device));
+    size_t at = 0;
+    for (int k = 0; k < B.n; ++k) {
+      PRE_CUDA(cudaMemcpyAsync(B.arena.p + B.nu_off[k], nu_all + at, B.nu_cnt[k] * sizeof(double), cudaMemcpyHostToDevice, 0));
+      at += B.nu_cnt[k];
+    }
+    PRE_CUDA(cudaEventCreate(&e0));
+    PRE_CUDA(cudaEventCreate(&e1));
+    PRE_CUDA(cudaEventRecord(e0));
+    k_rows<1><<<dim3(B.gx, B.n), 32 * ROWS_WARPS, B.smem>>>(B.d_boxes.p);
+    PRE_CUDA(cudaEventRecord(e1));
+    PRE_CUDA(cudaEventSynchronize(e1));
+    PRE_CUDA(cudaGetLastError());
+    float t = 0;
+    PRE_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    B.ms_fill = t;
+    if (ms) *ms = t;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return IETIDP_OK;
+  } catch (const std::pair<int, std::string>& ex) {
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    return fail(ex.first, ex.second);
+  }
+}
+
+int ietidp_pre_device_ptrs(ietidp_pre_t a, const double** d_val, const double** d_f) {
+  if (!a) return fail(IETIDP_E_ARG, "null handle");
+  const Box& b = a->batch->boxes[a->idx];
+  if (d_val) *d_val = b.val;
+  if (d_f) *d_f = b.f;
+  return IETIDP_OK;
 }
 
 int ietidp_pre_get_gram(ietidp_pre_t a, int c, int axis, int q, double* block, int* nb_out) {

@@ -24,12 +24,12 @@ STOP = {"residual": 0, "preconditioned": 1}
 
 # every entry point include/ietidp.h declares
 SYMBOLS = ["ietidp_options_default", "ietidp_create", "ietidp_set_subdomain", "ietidp_analyze",
-           "ietidp_set_values", "ietidp_set_values_lower", "ietidp_factor", "ietidp_solve", "ietidp_get_u", "ietidp_get_u_device",
+           "ietidp_set_values", "ietidp_set_values_device", "ietidp_set_values_lower", "ietidp_factor", "ietidp_solve", "ietidp_get_u", "ietidp_get_u_device",
            "ietidp_get_lambda_device", "ietidp_apply_F", "ietidp_apply_precond", "ietidp_get_coarse",
            "ietidp_estimate_condition", "ietidp_get_pcg_coefficients", "ietidp_get_rhs", "ietidp_get_report", "ietidp_kernel_launches", "ietidp_last_error",
            "ietidp_status_string", "ietidp_destroy"]
 # every entry point include/ietidp_pre.h declares (device pre-processing)
-PRE_SYMBOLS = ["ietidp_pre_assemble", "ietidp_pre_assemble_batch", "ietidp_pre_sizes", "ietidp_pre_get", "ietidp_pre_get_gram",
+PRE_SYMBOLS = ["ietidp_pre_assemble", "ietidp_pre_assemble_batch", "ietidp_pre_device_ptrs", "ietidp_pre_refill", "ietidp_pre_sizes", "ietidp_pre_get", "ietidp_pre_get_gram",
                "ietidp_pre_last_error", "ietidp_pre_destroy", "ietidp_pre_gauge"]
 
 
@@ -96,6 +96,7 @@ def load():
         "ietidp_analyze": (I, [P]),
         "ietidp_set_values": (I, [P, I, P, P]),
         "ietidp_set_values_lower": (I, [P, I, P, P]),
+        "ietidp_set_values_device": (I, [P, I, P, P]),
         "ietidp_factor": (I, [P]),
         "ietidp_solve": (I, [P, P, C.POINTER(Report)]),
         "ietidp_get_u": (I, [P, I, P]),
@@ -117,6 +118,8 @@ def load():
         "ietidp_shard_partition": (I, [I, P, I, P]),
         "ietidp_pre_assemble": (I, [I, C.POINTER(PreSubdomain), C.POINTER(P)]),
         "ietidp_pre_assemble_batch": (I, [I, I, C.POINTER(PreSubdomain), C.POINTER(P)]),
+        "ietidp_pre_device_ptrs": (I, [P, C.POINTER(P), C.POINTER(P)]),
+        "ietidp_pre_refill": (I, [P, P, C.POINTER(D)]),
         "ietidp_pre_sizes": (I, [P, C.POINTER(I), C.POINTER(C.c_int64), C.POINTER(D), C.POINTER(D)]),
         "ietidp_pre_get": (I, [P, P, P, P, P]),
         "ietidp_pre_get_gram": (I, [P, I, I, I, P, C.POINTER(I)]),
@@ -218,6 +221,11 @@ class Solver:
         v = None if K_lower is None else np.ascontiguousarray(K_lower, np.float64)
         ff = None if f is None else np.ascontiguousarray(f, np.float64)
         self._check(self.lib.ietidp_set_values_lower(self.h, k, _ptr(v), _ptr(ff)))
+
+    def set_values_device(self, k, d_val_ptr=None, d_f_ptr=None):
+        """ietidp_set_values_device: raw device pointers (ints), e.g. of a PreBatch."""
+        self._check(self.lib.ietidp_set_values_device(self.h, k, C.c_void_p(d_val_ptr) if d_val_ptr else None,
+                                                      C.c_void_p(d_f_ptr) if d_f_ptr else None))
 
     def factor(self):
         self._check(self.lib.ietidp_factor(self.h))
@@ -393,6 +401,55 @@ def pre_assemble(desc, device=0, want_gram=False):
         return _pre_fetch(lib, h, desc, want_gram)
     finally:
         lib.ietidp_pre_destroy(h)
+
+
+class PreBatch:
+    """Handles of one ietidp_pre_assemble_batch call kept alive (the matrices stay on the
+    device): sizes, device pointers for ietidp_set_values_device, host copies on request."""
+
+    def __init__(self, descs, device=0):
+        self.lib = load()
+        self.descs = descs
+        keep = []
+        n = len(descs)
+        subs = (PreSubdomain * n)()
+        for k, d in enumerate(descs):
+            _pre_fill(subs[k], d, keep)
+        self.hs = (C.c_void_p * n)()
+        _pre_check(self.lib, self.lib.ietidp_pre_assemble_batch(device, n, subs, self.hs))
+        ms, msf = C.c_double(), C.c_double()
+        _pre_check(self.lib, self.lib.ietidp_pre_sizes(self.hs[0], None, None, C.byref(ms), C.byref(msf)))
+        self.ms, self.ms_fill = ms.value, msf.value
+
+    def device_ptrs(self, k):
+        v, f = C.c_void_p(), C.c_void_p()
+        _pre_check(self.lib, self.lib.ietidp_pre_device_ptrs(self.hs[k], C.byref(v), C.byref(f)))
+        return v.value, f.value
+
+    def fetch(self, k):
+        return _pre_fetch(self.lib, self.hs[k], self.descs[k], False)
+
+    def refill(self, nus):
+        """ietidp_pre_refill: new reluctivities per subdomain (list of arrays, or one concatenated
+        array); reruns the value kernel in place. Returns its device time in ms."""
+        nu = np.ascontiguousarray(np.concatenate([np.ravel(x) for x in nus]) if isinstance(nus, (list, tuple)) else nus,
+                                  np.float64)
+        ms = C.c_double()
+        _pre_check(self.lib, self.lib.ietidp_pre_refill(self.hs[0], _ptr(nu), C.byref(ms)))
+        self.ms_fill = ms.value
+        return ms.value
+
+    def close(self):
+        for k in range(len(self.hs)):
+            if self.hs[k]:
+                self.lib.ietidp_pre_destroy(self.hs[k])
+                self.hs[k] = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 def pre_assemble_batch(descs, device=0, fetch=True):

@@ -163,6 +163,52 @@ def test_device_assembled_problem_solves(lib):
     assert abs(rep["iters"][0] - int(ref["iters"][0])) <= 1
 
 
+def test_device_assembly_feeds_factorisation_on_device(lib):
+    """Assembly -> ietidp_set_values_device -> factor -> solve without the matrix leaving the
+    device: the solution is bitwise the one obtained by passing the same device-assembled
+    values through the host (ietidp_set_values), and a second assembly with other reluctivities
+    re-feeds the same handle."""
+    from ietigen.bundle import make_bundle
+    b, P = make_bundle("C3r", with_problem=True)
+    descs = [predesc.subdomain_desc(P, sd) for sd in P.subs]
+    batch = lib.PreBatch(descs)
+    host = [batch.fetch(k) for k in range(len(descs))]
+    s = lib.Solver(b["n_sub"], b["n_lambda"], b["n_primal"], b["nrhs"], scaling=b["scaling"], tol=b["tol"])
+    for k, bs in enumerate(b["subs"]):
+        o = host[k]
+        s.set_subdomain(k, o["K_indptr"], o["K_indices"], o["K_data"], o["f"], bs["B_lambda"], bs["B_dof"], bs["B_sign"],
+                        bs["tree"], bs["prim"], bs["prim_gid"])
+    s.factor()
+    lam0, _ = s.solve()
+    u0 = np.concatenate([s.get_u(k) for k in range(b["n_sub"])])
+    # perturbed material: nu scaled per patch; values through the host ...
+    descs2 = [dict(d, nu=d["nu"] * (1.0 + 0.25 * ((i % 3) - 1))) for i, d in enumerate(descs)]
+    batch2 = lib.PreBatch(descs2)
+    for k in range(len(descs)):
+        o = batch2.fetch(k)
+        s.set_values(k, o["K_data"], o["f"])
+    s.factor()
+    lam_h, _ = s.solve()
+    u_h = np.concatenate([s.get_u(k) for k in range(b["n_sub"])])
+    assert np.linalg.norm(u_h - u0) > 1e-3 * np.linalg.norm(u0)  # the material did change the solution
+    # ... back to the original values, then the perturbed ones straight from the device
+    for k in range(len(descs)):
+        s.set_values_device(k, *batch.device_ptrs(k))
+    s.factor()
+    lam1, _ = s.solve()
+    assert np.array_equal(lam1, lam0)
+    for k in range(len(descs)):
+        s.set_values_device(k, *batch2.device_ptrs(k))
+    s.factor()
+    lam_d, _ = s.solve()
+    u_d = np.concatenate([s.get_u(k) for k in range(b["n_sub"])])
+    assert np.array_equal(lam_d, lam_h) and np.array_equal(u_d, u_h)
+    # ietidp_pre_refill: the first batch re-assembled in place with the second one's nu
+    batch.refill([d["nu"] for d in descs2])
+    for k in range(len(descs)):
+        assert np.array_equal(batch.fetch(k)["K_data"], batch2.fetch(k)["K_data"])
+
+
 def test_pre_argument_errors(lib):
     P = build("C1")
     d = predesc.subdomain_desc(P, P.subs[0])
