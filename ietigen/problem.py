@@ -7,6 +7,13 @@ five edge weights of Fig. 2, Kruskal's tree, the primal
 selection, the multiplier pairing B.
 Nothing here factorises, solves or iterates.
 
+For the device pre-processing (include/ietidp_pre.h) the assembly and the
+Kruskal tree of this module are the CPU reference the kernels are compared with
+(tests/test_gpu_pre.py): plain SciPy, written from the paper, sharing no code with csrc/pre.cu
+and pinned on their own (tests/test_gen.py, tests/test_oracle.py: curl o grad = 0, the DOF counts,
+EOC of the manufactured solutions, DD = monolithic). The inputs of those kernels come from
+ietigen/predesc.py, which holds no assembly arithmetic.
+
 Index conventions:
 * vertices (0-form DOFs) on the global grid m_x x m_y x m_z, x fastest;
 * edge (1-form DOF) of direction a at (i,j,k) joins vertex (i,j,k) to (i,j,k)+e_a;

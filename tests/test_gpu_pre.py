@@ -89,6 +89,60 @@ def test_batch_assembly_bitwise_equals_single(lib, name):
     assert abs(outs[k]["f"].T - jref).max() <= 1e-12 * abs(jref).max()
 
 
+@pytest.mark.parametrize("name", ["C2r", "C5r", "E27_221_p3_e2"])
+def test_assembly_closed_form_energy_and_kernel(lib, name):
+    """Pins of the device-assembled K and j that do not involve the generator's assembly
+    (PAPER.md:49-57). With no Dirichlet rows removed:
+    (1) the field A = (-y/2, x/2, 0) lies in the spline 1-form space (constant along an edge's
+        own axis: coefficient (t_{j+p+1}-t_{j+1})/p of the Curry-Schoenberg D_j; linear across:
+        the Greville abscissae), curl A = e_z, so a^T K a = int nu |curl A|^2 = sum over the
+        patches of nu_q * volume_q -- exactly, for any degree and any per-patch nu;
+    (2) K annihilates discrete gradients (curl o grad = 0): K G phi = 0 for a seeded phi;
+    (3) the load of a constant T = tau e_z pairs with the same field: a^T j = tau * volume."""
+    from ietigen.rng import SplitMix64
+    P = build(name)
+    sd = P.subs[len(P.subs) // 2]
+    d = dict(predesc.subdomain_desc(P, sd))
+    p, e, npb = d["p"], d["e"], d["npatch"]
+    m = [npb[a] * (e + p - 1) + 1 for a in range(3)]
+    E = [[m[a] - (1 if a == dd else 0) for a in range(3)] for dd in range(3)]
+    ne = sum(int(np.prod(E[dd])) for dd in range(3))
+    d["dof_of_edge"] = np.arange(ne, dtype=np.int32)  # keep the Dirichlet edges
+    d["n_dof"] = ne
+    # one load column: T = tau e_z (component 2: B along z, D along x and y), factors "one"
+    tau = 0.75
+    lw = []
+    for a in range(3):
+        x = d["lx"][a]
+        h_el = (d["knots"][a][-1] - d["knots"][a][0]) / (npb[a] * e)
+        g, w = np.polynomial.legendre.leggauss(d["lq"])
+        lw.append(np.tile(0.5 * h_el * w, npb[a] * e))
+        assert len(lw[-1]) == len(x)
+    d.update(nrhs=1, fac_kind=[np.array([1], np.int32), np.array([1], np.int32), np.array([0], np.int32)],
+             fac_val=[lw[0][None, :], lw[1][None, :], lw[2][None, :]], term_col=np.array([0], np.int32),
+             term_comp=np.array([2], np.int32), term_fac=np.array([[0, 0, 0]], np.int32), term_coef=np.array([tau]))
+    out = lib.pre_assemble(d)
+    K = _csr(out, ne)
+    t = d["knots"]
+    cD = [np.array([(t[a][j + p + 1] - t[a][j + 1]) / p for j in range(m[a] - 1)]) for a in range(3)]
+    gv = [np.array([t[a][i + 1:i + p + 1].sum() / p for i in range(m[a])]) for a in range(3)]
+    one = [np.ones(m[a]) for a in range(3)]
+    ax = np.einsum("i,j,k->kji", cD[0], -0.5 * gv[1], one[2]).ravel()   # A_x = -y/2 on the x-edges
+    ay = np.einsum("i,j,k->kji", 0.5 * gv[0], cD[1], one[2]).ravel()    # A_y = x/2 on the y-edges
+    a = np.concatenate([ax, ay, np.zeros(int(np.prod(E[2])))])
+    vol_patch = np.prod([(t[a][-1] - t[a][0]) / npb[a] for a in range(3)])
+    energy = float(np.sum(d["nu"]) * vol_patch)
+    assert abs(a @ (K @ a) - energy) <= 1e-12 * energy, (a @ (K @ a), energy)
+    assert abs(a @ out["f"][0] - tau * vol_patch * np.prod(npb)) <= 1e-12 * tau
+    # discrete gradient of a seeded vertex function: edge (d; n) = phi(n + e_d) - phi(n)
+    g = SplitMix64(5)
+    phi = np.array([g.uniform() for _ in range(int(np.prod(m)))]).reshape(m[2], m[1], m[0])
+    grad = np.concatenate([np.diff(phi, axis=2).ravel(), np.diff(phi, axis=1).ravel(), np.diff(phi, axis=0).ravel()])
+    assert np.abs(K @ grad).max() <= 1e-12 * abs(K).max() * np.abs(grad).max()
+    lam_min = np.linalg.eigvalsh(K.toarray())[0] if ne <= 1500 else 0.0
+    assert lam_min >= -1e-10 * abs(K).max()
+
+
 def test_gram_blocks_closed_form(lib):
     """First stage pinned independently of the generator: on one patch with p = 1, e = 2 over
     [0, 1/2] the hat functions' Gram matrix is h/6 [[2,1,0],[1,4,1],[0,1,2]] (h = 1/4) and the
