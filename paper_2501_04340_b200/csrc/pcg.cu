@@ -2638,15 +2638,17 @@ __global__ void __launch_bounds__(VT) k_sh_dotpart(int m, int ncols, const doubl
     for (int j = blockIdx.x * R + rl; j < m; j += gridDim.x * R) dot += a[(long long)j * ncols + c] * b[(long long)j * ncols + c];
   block_col_reduce(dot, ncols, P2, partial);
 }
-// g[gi][c] = add + sum of the coarse partial rows of the LOCAL subdomains (first half of k_coarse)
+// g[gi][c] = (add +) sum of the coarse partial rows of the local subdomains, one thread per
+// entry over the whole grid (k_coarse does this part in one CTA: 340 us for C5's 177 x 16)
 __global__ void __launch_bounds__(256)
     k_sh_gsum(int ng, int ncols, int nPmax, const int* __restrict__ pcon_ptr, const int* __restrict__ pcon_sub,
               const int* __restrict__ pcon_q, const int* __restrict__ sub_cta0, const int* __restrict__ sub_ncta,
-              const double* __restrict__ gpart, double* __restrict__ g, const PcgState* __restrict__ st) {
+              const double* __restrict__ gpart, const double* __restrict__ add, double* __restrict__ g,
+              const PcgState* __restrict__ st) {
   if (st && st->done) return;
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < ng * ncols; e += gridDim.x * blockDim.x) {
     const int gi = e / ncols, c = e - gi * ncols;
-    double s = 0.0;
+    double s = add ? add[e] : 0.0;
     for (int q = pcon_ptr[gi]; q < pcon_ptr[gi + 1]; ++q) {
       const int k = pcon_sub[q], lq = pcon_q[q];
       for (int cta = sub_cta0[k]; cta < sub_cta0[k] + sub_ncta[k]; ++cta)
@@ -2728,14 +2730,20 @@ void coarse_apply(ietidp_s* h, int ncols, const double* add, double* z, const vo
   // the block-pair items of the triangular operators
   const int* r0 = sym_rows ? h->sub_blk0.p : h->sub_cta0.p;
   const int* rn = sym_rows ? h->sub_nt.p : h->sub_ncta.p;
-  if (h->shard) {  // g summed over the ranks, S_PP^-1 replicated
+  // g over the whole grid, then z = S_PP^-1 g with a warp per entry (the same sums, in the same
+  // order, as the one-CTA k_coarse; IETIDP_COARSE_1CTA=1 forces that kernel). Sharded: g is
+  // summed over the ranks in between (S_PP^-1 is replicated), `add` after it.
+  // (with few entries -- one RHS -- the single launch is quicker: C2 43 vs 51 us per F-apply)
+  static const bool force_1cta = getenv("IETIDP_COARSE_1CTA") && atoi(getenv("IETIDP_COARSE_1CTA")) == 1;
+  const bool one_cta = force_1cta || (long long)h->n_primal * ncols < 1024;
+  if (h->shard || !one_cta) {
     k_sh_gsum<<<grid_for((long long)h->n_primal * ncols, 256), 256, 0, h->stream>>>(
         h->n_primal, ncols, std::max(h->plan.nPmax, 1), h->pcon_ptr.p, h->pcon_sub.p, h->pcon_q.p, r0, rn, h->gpart.p,
-        h->gc.p, st);
+        h->shard ? nullptr : add, h->gc.p, st);
     IETI_LAUNCHED(h);
     sh_sum(h, h->gc.p, (long long)h->n_primal * ncols);
     k_sh_coarse_solve<<<grid_for((long long)h->n_primal * ncols * 32, 256), 256, 0, h->stream>>>(
-        h->n_primal, ncols, h->Sinv.p, h->gc.p, add, z, st);
+        h->n_primal, ncols, h->Sinv.p, h->gc.p, h->shard ? add : nullptr, z, st);
     IETI_LAUNCHED(h);
     return;
   }
@@ -2926,7 +2934,9 @@ void run_apply_M(ietidp_s* h, int ncols, const double* x, double* y) {
 }
 
 static int body_launches(ietidp_s* h, int ncols) {
-  return 4 * tmv_launches(h, ncols) + (h->n_primal ? 1 : 0) + 2 + 3;
+  if (h->opt.loop == IETIDP_LOOP_EXPLICIT)  // per pass: slot order, pass, reduction, gather; coarse g and z; 3 CG kernels
+    return 2 * (tmv_launches(h, ncols) + 3) + (h->n_primal ? 2 : 0) + 3;
+  return 4 * tmv_launches(h, ncols) + (h->n_primal ? 2 : 0) + 2 + 3;
 }
 
 static void iteration_body(ietidp_s* h, PcgState* st, int use_graph) {
