@@ -2067,6 +2067,45 @@ __device__ __forceinline__ void pcg_barrier(const PcgArgs& P) {
   grid_barrier(P.bar);
 }
 
+// Set-up of the chunk pass in a CTA: ring mbarriers, the tensor-memory allocation, zeroed
+// accumulators (the persistent kernel does it once; the sharded loop's pass kernels per launch).
+template <int STAGES>
+__device__ __forceinline__ void chunk_prologue() {
+  const int tid = threadIdx.x;
+  // ring mbarriers and the tensor-memory accumulators
+  if (tid == 0) {
+    for (int s2 = 0; s2 < STAGES; ++s2) {
+      mbar_init(&g_chunk_ctl.full[s2], 1);
+      g_chunk_ctl.rel[s2] = 0;
+    }
+    for (int q = 0; q < 4; ++q) g_chunk_ctl.diag[q] = 0;
+    g_chunk_ctl.streamed = 0;
+    g_chunk_ctl.ncall = g_chunk_ctl.ntl = 0;
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  if ((tid >> 5) == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
+                     (unsigned)__cvta_generic_to_shared(&g_chunk_ctl.tmem)),
+                 "n"(CH_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+  const int w = tid >> 5;
+  const unsigned tb = g_chunk_ctl.tmem + ((unsigned)(32 * (w & 3)) << 16) + 8u * (w >> 2);
+  const double zero[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  for (int jb = 0; jb < 32; ++jb) tm_st8(tb + 16 * jb, zero);
+  tm_wait_st();
+  __syncthreads();
+}
+__device__ __forceinline__ void chunk_epilogue() {
+  asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+  __syncthreads();
+  if ((threadIdx.x >> 5) == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(g_chunk_ctl.tmem), "n"(CH_TMEM_COLS));
+}
+
 template <int NCP, int STAGES, bool EXPL, bool CH>
 __device__ __forceinline__ void apply_F_phases(const PcgArgs& P, double* smem, double* pq) {
   if constexpr (EXPL && CH) {
@@ -2228,6 +2267,33 @@ __device__ __forceinline__ void apply_M_phases(const PcgArgs& P, double* smem, d
   }
 }
 
+// ---- the chunk-mode phases as launches of their own (sharded solve, several RHS): the same
+// device functions as the persistent kernel's phases, a kernel boundary where that has a grid
+// barrier, so that the sums over the ranks can run between them ----
+template <int STAGES, int WHICH>  // WHICH 0: W = S_II^-1 (F-apply), 1: S_II (preconditioner)
+__global__ void __launch_bounds__(256, 1) k_ch_pass(const PcgArgs P) {
+  extern __shared__ __align__(16) double smem[];
+  if (P.st->done) return;
+  chunk_prologue<STAGES>();
+  sym_pass<16, STAGES, true>(P, WHICH ? P.ssym : P.wsym, smem);
+  chunk_epilogue();
+}
+__global__ void __launch_bounds__(256, 1) k_ch_g(const PcgArgs P) {
+  if (P.st->done) return;
+  coarse_spread(P);
+}
+__global__ void __launch_bounds__(256, 1) k_ch_zk(const PcgArgs P) {
+  extern __shared__ __align__(16) double smem[];
+  if (P.st->done) return;
+  coarse_gz_phase(P, P.wsym, smem, P.smem_doubles);
+}
+template <int WHICH>
+__global__ void __launch_bounds__(256, 1) k_ch_gather(const PcgArgs P, double* scratch) {
+  if (P.st->done) return;
+  if (WHICH) gather_fold<2>(P, P.ssym.spart, true, P.z, P.r, scratch);
+  else gather_fold<2>(P, P.wsym.spart, false, P.q, P.p, scratch, P.ng > 0 ? P.gzv : nullptr);
+}
+
 template <int NCP, int STAGES, bool EXPL, bool CH = false>
 __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) {
   extern __shared__ __align__(16) double smem[];
@@ -2245,35 +2311,7 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     if (cc < nc)
       for (int j = blockIdx.x * R + rl; j < m; j += nb * R) f((long long)j * nc + cc, j);
   };
-  if constexpr (NCP == 16 && EXPL && CH) {
-    {  // chunk pass: ring mbarriers and the tensor-memory accumulators
-      if (tid == 0) {
-        for (int s2 = 0; s2 < STAGES; ++s2) {
-          mbar_init(&g_chunk_ctl.full[s2], 1);
-          g_chunk_ctl.rel[s2] = 0;
-        }
-        for (int q = 0; q < 4; ++q) g_chunk_ctl.diag[q] = 0;
-        g_chunk_ctl.streamed = 0;
-        g_chunk_ctl.ncall = g_chunk_ctl.ntl = 0;
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-      }
-      if ((tid >> 5) == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(
-                         (unsigned)__cvta_generic_to_shared(&g_chunk_ctl.tmem)),
-                     "n"(CH_TMEM_COLS));
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n");
-      }
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncthreads();
-      asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-      const int w = tid >> 5;
-      const unsigned tb = g_chunk_ctl.tmem + ((unsigned)(32 * (w & 3)) << 16) + 8u * (w >> 2);
-      const double zero[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-      for (int jb = 0; jb < 32; ++jb) tm_st8(tb + 16 * jb, zero);
-      tm_wait_st();
-      __syncthreads();
-    }
-  }
+  if constexpr (NCP == 16 && EXPL && CH) chunk_prologue<STAGES>();
   // ---- init: lambda = 0, r = d, r0 = ||d|| ----
   {
     double acc = 0.0;
@@ -2495,15 +2533,7 @@ __global__ void __launch_bounds__(256, NCP == 1 ? 2 : 1) k_pcg(const PcgArgs P) 
     if (tid < nc) s_act[tid] = s_new[tid];
     pcg_barrier(P);
   }
-  if constexpr (NCP == 16 && EXPL && CH) {
-    {
-      asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-      __syncthreads();
-      if ((tid >> 5) == 0)
-        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(g_chunk_ctl.tmem),
-                     "n"(CH_TMEM_COLS));
-    }
-  }
+  if constexpr (NCP == 16 && EXPL && CH) chunk_epilogue();
   if (blockIdx.x == 0 && tid == 0) {
     P.st->it = it;
     P.st->done = 1;
@@ -3109,6 +3139,15 @@ static void plan_chunks(ietidp_s* h, int grid, int nc) {
   h->chunk_grid = grid;
 }
 
+// run_solve_persistent in "prepare only" mode (the sharded chunk loop): launch_pcg_t fills the
+// kernel arguments and plans, hands them out here and does not launch
+struct PrepareOnly {
+  PcgArgs* out = nullptr;
+  int grid = 0, smem = 0, stages = 0;
+  bool chunk = false;
+};
+static thread_local PrepareOnly g_prepare;  // per host thread: handles may be driven concurrently
+
 template <int NCP, int STAGES, bool EXPL, bool CH = false>
 static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
   auto kern = k_pcg<NCP, STAGES, EXPL, CH>;
@@ -3150,6 +3189,14 @@ static bool launch_pcg_t(ietidp_s* h, const TmvCfg& cfg, const PcgArgs& a) {
     IETI_LAUNCHED(h);
     args.fold = 1;
     args.fold_multi = 1;  // the gathers sum the (few) chunk partials of each slot
+  }
+  if (g_prepare.out) {  // sharded loop: the arguments and the launch shape, no launch
+    *g_prepare.out = args;
+    g_prepare.grid = grid;
+    g_prepare.smem = cfg.smem;
+    g_prepare.stages = STAGES;
+    g_prepare.chunk = CH && args.chunk;
+    return true;
   }
   const char* prof_env = getenv("IETIDP_PCG_PROF");
   DevBuf<unsigned long long>& prof = h->pcg_prof;  // per handle, on the handle's device
@@ -3367,6 +3414,75 @@ void run_solve(ietidp_s* h) {
   }
   if (h->opt.stop != IETIDP_STOP_RESIDUAL && m > 0)
     throw Error(IETIDP_E_ARG, "the preconditioned stopping criterion needs the persistent PCG kernel");
+  // sharded, 16 RHS: the chunk pass and its phases as separate launches (the persistent
+  // kernel's device functions), IETIDP_SHARD_CHUNK=0 keeps the row-segment stream
+  PcgArgs CA{};
+  bool ch = false;
+  if (h->shard && m > 0 && h->opt.loop == IETIDP_LOOP_EXPLICIT &&
+      !(getenv("IETIDP_SHARD_CHUNK") && atoi(getenv("IETIDP_SHARD_CHUNK")) == 0)) {
+    g_prepare.out = &CA;
+    g_prepare.chunk = false;
+    bool ok = false;
+    try {
+      ok = run_solve_persistent(h);
+    } catch (...) {
+      g_prepare.out = nullptr;
+      throw;
+    }
+    g_prepare.out = nullptr;
+    ch = ok && g_prepare.chunk;
+  }
+  const int cgrid = g_prepare.grid, csmem = g_prepare.smem, cstages = g_prepare.stages;
+  double* gscratch = h->partial.p + 3 * NBLK * nc;
+  auto to_slots = [&](const double* x, const double* w, double* out) {
+    k_to_slots<<<grid_for((long long)h->n_slots * nc, 256), 256, 0, s>>>(h->n_slots, nc, h->slot_lam.p, h->slot_sign.p, w, x,
+                                                                        out, st);
+    IETI_LAUNCHED(h);
+  };
+  auto ch_pass = [&](int which) {
+    auto set = [&](const void* k) { IETI_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem)); };
+    if (cstages == 3) {
+      if (which) { set((const void*)k_ch_pass<3, 1>); k_ch_pass<3, 1><<<cgrid, 256, csmem, s>>>(CA); }
+      else { set((const void*)k_ch_pass<3, 0>); k_ch_pass<3, 0><<<cgrid, 256, csmem, s>>>(CA); }
+    } else {
+      if (which) { set((const void*)k_ch_pass<2, 1>); k_ch_pass<2, 1><<<cgrid, 256, csmem, s>>>(CA); }
+      else { set((const void*)k_ch_pass<2, 0>); k_ch_pass<2, 0><<<cgrid, 256, csmem, s>>>(CA); }
+    }
+    IETI_LAUNCHED(h);
+  };
+  auto ch_apply_F = [&]() {  // q = F_DP p, p.q partials
+    to_slots(h->p_vec.p, nullptr, h->pslot.p);
+    ch_pass(0);
+    if (h->n_primal) {
+      k_ch_g<<<cgrid, 256, 0, s>>>(CA);
+      IETI_LAUNCHED(h);
+      sh_sum(h, h->gc.p, (long long)h->n_primal * nc);
+      IETI_CUDA(cudaFuncSetAttribute((const void*)k_ch_zk, cudaFuncAttributeMaxDynamicSharedMemorySize, csmem));
+      k_ch_zk<<<cgrid, 256, csmem, s>>>(CA);
+      IETI_LAUNCHED(h);
+    }
+    k_ch_gather<0><<<cgrid, 256, 0, s>>>(CA, gscratch);
+    IETI_LAUNCHED(h);
+    sh_finish_gather(h, nc, h->q_vec.p, h->p_vec.p, h->partial.p, st);
+  };
+  auto ch_apply_M = [&]() {  // z = M_D^-1 r, r.z partials
+    to_slots(h->r_vec.p, h->delta.p, h->rslot.p);
+    ch_pass(1);
+    k_ch_gather<1><<<cgrid, 256, 0, s>>>(CA, gscratch);
+    IETI_LAUNCHED(h);
+    sh_finish_gather(h, nc, h->z_vec.p, h->r_vec.p, rz_part, st);
+  };
+  auto ch_body = [&]() {
+    ch_apply_F();
+    k_cg_alpha<<<NBLK, VT, 0, s>>>(m, st, h->partial.p, h->lam_vec.p, h->r_vec.p, h->p_vec.p, h->q_vec.p, rr_part,
+                                  h->cgcoef.p, h->coef_ld);
+    IETI_LAUNCHED(h);
+    ch_apply_M();
+    k_cg_beta<<<NBLK, VT, 0, s>>>(m, st, rr_part, rz_part, h->p_vec.p, h->z_vec.p, h->cgcoef.p, h->coef_ld);
+    IETI_LAUNCHED(h);
+    k_ctl<<<1, 64, 0, s>>>(st, rr_part, rz_part, 0ull, 0);
+    IETI_LAUNCHED(h);
+  };
   if (m > 0) {
     k_init<<<NBLK, VT, 0, s>>>(m, nc, h->d_vec.p, h->lam_vec.p, h->r_vec.p, rr_part);
     IETI_LAUNCHED(h);
@@ -3374,7 +3490,8 @@ void run_solve(ietidp_s* h) {
   k_init_ctl<<<1, 64, 0, s>>>(st, rr_part, nc, m, h->opt.tol, h->opt.max_iter, h->opt.fixed_iters);
   IETI_LAUNCHED(h);
   if (m > 0) {
-    apply_M_inter(h, nc, h->r_vec.p, h->z_vec.p, st, rr_part, 0, h->r_vec.p, rz_part);
+    if (ch) ch_apply_M();
+    else apply_M_inter(h, nc, h->r_vec.p, h->z_vec.p, st, rr_part, 0, h->r_vec.p, rz_part);
     k_init_p<<<NBLK, VT, 0, s>>>(m, st, h->z_vec.p, h->p_vec.p);
     IETI_LAUNCHED(h);
     k_init_rz<<<1, 64, 0, s>>>(st, rz_part);
@@ -3394,12 +3511,16 @@ void run_solve(ietidp_s* h) {
         flag[0] = flag[1] = 0;
         IETI_CUDA(cudaMemcpyAsync(flag, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
         IETI_CUDA(cudaStreamSynchronize(s));
+        auto body = [&]() {
+          if (ch) ch_body();
+          else iteration_body(h, st, 0);
+        };
         if (!flag[1]) {
-          iteration_body(h, st, 0);
+          body();
           IETI_CUDA(cudaMemcpyAsync(flag, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
           IETI_CUDA(cudaEventRecord(fev, s));
           for (;;) {
-            iteration_body(h, st, 0);                // the next iteration, speculatively
+            body();                                  // the next iteration, speculatively
             IETI_CUDA(cudaEventSynchronize(fev));    // the flag after the previous one
             if (flag[1]) break;
             IETI_CUDA(cudaMemcpyAsync(flag, st, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -137,6 +137,21 @@ def test_sharded_equals_single_handle_iteration_matched(lib):
     assert np.linalg.norm(u2 - u1) <= 1e-10 * np.linalg.norm(u1)
 
 
+def test_sharded_chunk_loop_equals_stream_loop(lib, monkeypatch):
+    """16 RHS: the sharded loop runs the chunk pass and its phases as separate launches
+    (IETIDP_SHARD_CHUNK=0: the row-segment stream instead). Same operators, different
+    summation layouts: after a fixed number of iterations lambda agrees to the parity bar 1e-8
+    (cond(M^-1 F) ~ 800 on C5r amplifies the two layouts' rounding to ~2e-9 by iteration 25)."""
+    b = make_bundle("C5r")
+    out1, _, _ = run_sharded(lib, b, 2, fixed_iters=25)
+    monkeypatch.setenv("IETIDP_SHARD_CHUNK", "0")
+    out0, _, _ = run_sharded(lib, b, 2, fixed_iters=25)
+    monkeypatch.delenv("IETIDP_SHARD_CHUNK")
+    lam1, lam0 = out1[0][0], out0[0][0]
+    assert np.all(np.linalg.norm(lam1 - lam0, axis=0) <= 1e-8 * np.linalg.norm(lam0, axis=0))
+    assert not np.array_equal(lam1, lam0)  # (they are different code paths)
+
+
 def test_uneven_partition_and_empty_coarse_rank(lib):
     """A lopsided owner map (one subdomain alone on rank 1): its rank sees only some primal
     DOFs and one-sided multipliers on all its faces."""
