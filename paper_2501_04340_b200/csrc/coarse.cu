@@ -500,7 +500,11 @@ void run_coarse(ietidp_s* h) {
       sh_sum(h, h->S.p, (long long)ng * ng);
       sh_sum(h, h->ftil.p, (long long)ng * nrhs);
     }
-    if (ng <= COARSE_CTA_MAX && !h->shard) {
+    // one CTA up to 127 primal DOFs; above, the blocked sweep operator over all SMs is quicker
+    // (C5, n_gp = 177: coarse set-up 1.38 -> 1.10 ms; C3, 145: 0.74 -> 0.64 ms); sharded: always
+    // (S_PP comes from the sum over the ranks, not from the local P fronts)
+    static const int one_cta_max = getenv("IETIDP_COARSE_CTA_MAX") ? atoi(getenv("IETIDP_COARSE_CTA_MAX")) : 127;
+    if (ng <= std::min(COARSE_CTA_MAX, one_cta_max) && !h->shard) {
       const int smem = ng * (ng + 1) / 2 * sizeof(double);
       IETI_CUDA(cudaFuncSetAttribute((const void*)k_coarse_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
       k_coarse_factor<<<1, 1024, smem, s>>>(ng, nrhs, h->scoef_ptr.p, h->scoef_src.p, h->pool.p, h->pcon_ptr.p,
