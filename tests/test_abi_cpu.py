@@ -182,3 +182,62 @@ def test_missing_subdomain(lib):
     with pytest.raises(lib.IetiError) as e:
         s.analyze()
     assert e.value.status == lib.E_STATE
+
+
+# ---- argument validation of the pre-processing and sharding entry points (host side) ----
+
+def test_pre_and_shard_argument_errors_without_gpu(lib):
+    """include/ietidp_pre.h / ietidp_shard.h: every documented E_ARG / E_STATE is raised by the
+    host-side validation, before any device work (so it can be checked without a GPU)."""
+    from ietigen import predesc
+    from ietigen.problem import build
+    P = build("C1")
+    d = predesc.subdomain_desc(P, P.subs[0])
+    for key, val in [("p", 4), ("p", 0), ("e", 0), ("nq", 0)]:
+        bad = dict(d)
+        bad[key] = val
+        with pytest.raises(lib.IetiError) as e:
+            lib.pre_assemble(bad, device=0)
+        assert e.value.status == lib.E_ARG, key
+    bad = dict(d)
+    bad["fac_kind"] = [1 - k for k in d["fac_kind"]]  # a B factor where the component needs D
+    with pytest.raises(lib.IetiError) as e:
+        lib.pre_assemble(bad)
+    assert e.value.status == lib.E_ARG
+    bad = dict(d)
+    dof = d["dof_of_edge"].copy()
+    i = np.flatnonzero(dof >= 0)[:2]
+    dof[i] = dof[i[::-1]]  # DOFs not ascending with the edge id
+    bad["dof_of_edge"] = dof
+    with pytest.raises(lib.IetiError) as e:
+        lib.pre_assemble(bad)
+    assert e.value.status == lib.E_ARG
+    bad = dict(d)
+    bad["term_col"] = d["term_col"] + 7  # RHS column out of range
+    with pytest.raises(lib.IetiError) as e:
+        lib.pre_assemble(bad)
+    assert e.value.status == lib.E_ARG
+    # gauge: endpoints and weights
+    one = np.array([0], np.int32)
+    for eu, ev, w in [(one, np.array([5], np.int32), np.array([1], np.int8)),
+                      (one, np.array([1], np.int32), np.array([0], np.int8)),
+                      (one, np.array([1], np.int32), np.array([6], np.int8))]:
+        with pytest.raises(lib.IetiError) as e:
+            lib.pre_gauge(3, 1, eu, ev, w)
+        assert e.value.status == lib.E_ARG
+    # sharded mode: only before analysis, only the explicit loop with the residual criterion
+    b = make_bundle("C1")
+    s = host_solver(lib, b)
+    s.analyze()
+    with pytest.raises(lib.IetiError) as e:
+        s.shard_enable(0, 2, lambda ptr, n, stream: 0)
+    assert e.value.status == lib.E_STATE
+    for kw in (dict(loop="triangular"), dict(stop="preconditioned")):
+        s = host_solver(lib, b, **kw)
+        with pytest.raises(lib.IetiError) as e:
+            s.shard_enable(0, 2, lambda ptr, n, stream: 0)
+        assert e.value.status == lib.E_ARG
+    s = host_solver(lib, b)
+    with pytest.raises(lib.IetiError) as e:
+        s.shard_enable(2, 2, lambda ptr, n, stream: 0)  # rank out of range
+    assert e.value.status == lib.E_ARG
