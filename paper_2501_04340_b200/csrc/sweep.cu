@@ -79,6 +79,60 @@ __global__ void __launch_bounds__(SWT)
   }
   const double* vin = (MODE == 0) ? Wv + s.vec_off * NCB : nullptr;       // v_piv
   const double* yin = (MODE == 1) ? X + (d.x_off + s.c0) * ldx + cofs : nullptr;  // y
+  if constexpr (NCB == 16) {
+    // 16 columns: the tile product on the FP64 tensor pipe. Warp w owns rows 8w .. 8w+7 of the
+    // tile and both 8-column halves: per 4-deep k step one global load of the A fragment
+    // (A[8w + lane/4][k + lane%4], 8 consecutive rows of a column: 64-byte segments), two
+    // shared-memory loads of the staged vector rows and two DMMAs; eight steps' loads in flight.
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int g = lane >> 2, t4 = lane & 3;
+    const int Rw = row0 + 8 * warp + g;
+    const bool rok = Rw < nrows;
+    const double* Aw = (MODE == 0) ? ipool + s.inv_off + Rw : pool + s.front_off + s.npiv + Rw;
+    double dacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int k0 = 0; k0 < kend; k0 += TB) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < TB * NCB; e += SWT) {
+        const int k = e / NCB, c = e % NCB;
+        double v = 0.0;
+        if (k0 + k < kend) v = (MODE == 0) ? vin[(k0 + k) * NCB + c] : (c < ncl ? yin[(long long)(k0 + k) * ldx + c] : 0.0);
+        xs[k][c] = v;
+      }
+      __syncthreads();
+      const int kn = min(TB, kend - k0);
+      for (int kb = 0; kb < kn; kb += 32) {
+        double a[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = kb + 4 * u + t4;
+          a[u] = (rok && k < kn) ? Aw[(long long)(k0 + k) * lda] : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int k = kb + 4 * u + t4;
+          if (kb + 4 * u < kn) {
+            const int kk = min(k, TB - 1);
+            dmma8x8x4(dacc[0][0], dacc[0][1], a[u], xs[kk][g]);
+            dmma8x8x4(dacc[1][0], dacc[1][1], a[u], xs[kk][8 + g]);
+          }
+        }
+      }
+    }
+    if (rok) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int c = 8 * hh + 2 * t4 + q;
+          if (MODE == 0) {
+            if (c < ncl) X[(d.x_off + s.c0 + Rw) * ldx + cofs + c] = dacc[hh][q];
+          } else {
+            Wv[(s.vec_off + s.npiv + Rw) * NCB + c] -= dacc[hh][q];
+          }
+        }
+    }
+    return;
+  }
   double acc[NCB];
 #pragma unroll
   for (int c = 0; c < NCB; ++c) acc[c] = 0.0;
@@ -141,6 +195,39 @@ __global__ void __launch_bounds__(SWT)
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (NCB == 16) {
+    // 16 columns: partial[col][c] = sum_q L21[q][col] x[q][c] on the FP64 tensor pipe; warp w owns
+    // the pivot columns 8w .. 8w+7 of the tile (fragment rows), lanes%4 the 4 rows q of a step;
+    // eight steps' loads in flight, no shuffle reductions
+    const int g = lane >> 2, t4 = lane & 3;
+    const int col = w.a * TB + 8 * warp + g;
+    const bool cok = col < s.npiv;
+    const double* Lc = pool + s.front_off + (long long)col * s.ld + s.npiv + q0;
+    double dacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int kb = 0; kb < nq; kb += 32) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = kb + 4 * u + t4;
+        a[u] = (cok && q < nq) ? Lc[q] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (kb + 4 * u < nq) {
+          const int qq = min(kb + 4 * u + t4, BS_RB - 1);
+          dmma8x8x4(dacc[0][0], dacc[0][1], a[u], xs[qq][g]);
+          dmma8x8x4(dacc[1][0], dacc[1][1], a[u], xs[qq][8 + g]);
+        }
+    }
+    if (cok) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2)
+          bpart[s.bp_off + ((long long)w.b * s.npiv + col) * NCB + 8 * hh + 2 * t4 + q2] = dacc[hh][q2];
+    }
+    return;
+  }
   for (int cc = warp; cc < TB; cc += 2 * (SWT / 32)) {
     double acc[2][NCB];
     bool okc[2];
@@ -214,6 +301,36 @@ __global__ void __launch_bounds__(SWT)
   }
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if constexpr (NCB == 16) {  // as k_bs_partial: partial[col][c] = sum_{r >= col} Linv[r][col] t[r][c] by DMMA
+    const int g = lane >> 2, t4 = lane & 3;
+    const int col = w.a * TB + 8 * warp + g;
+    const bool cok = col < s.npiv;
+    const double* Ic = ipool + s.inv_off + (long long)col * s.ldi + r0;
+    double dacc[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+    for (int kb = 0; kb < nr; kb += 32) {
+      double a[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int q = kb + 4 * u + t4;
+        a[u] = (cok && q < nr && r0 + q >= col) ? Ic[q] : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (kb + 4 * u < nr) {
+          const int qq = min(kb + 4 * u + t4, BS_RB - 1);
+          dmma8x8x4(dacc[0][0], dacc[0][1], a[u], ts[qq][g]);
+          dmma8x8x4(dacc[1][0], dacc[1][1], a[u], ts[qq][8 + g]);
+        }
+    }
+    if (cok) {
+#pragma unroll
+      for (int hh = 0; hh < 2; ++hh)
+#pragma unroll
+        for (int q2 = 0; q2 < 2; ++q2)
+          bpart[s.bp_off + ((long long)(nchu + w.b) * s.npiv + col) * NCB + 8 * hh + 2 * t4 + q2] = dacc[hh][q2];
+    }
+    return;
+  }
   for (int cc = warp; cc < TB; cc += 2 * (SWT / 32)) {
     double acc[2][NCB];
     bool okc[2];
