@@ -2556,7 +2556,8 @@ struct TmvCfg {
 
 // sym: the explicit loop's symmetric passes (row-segment items); else the block-pair
 // items of the triangular operators
-static TmvCfg tmv_cfg(const ietidp_s* h, int ncols, bool sym = false) {
+// big: a launch of its own without static shared memory (k_tmv) may use the whole 227 KB
+static TmvCfg tmv_cfg(const ietidp_s* h, int ncols, bool sym = false, bool big = false) {
   const int nt = (h->plan.max_nI + TB - 1) / TB;
   const int npg = std::max(h->plan.nPmax, 16);  // staged coarse rows: TB x nP (at least 16)
   if (ncols == 1) {
@@ -2582,7 +2583,7 @@ static TmvCfg tmv_cfg(const ietidp_s* h, int ncols, bool sym = false) {
     for (int stages = 3; stages >= 2; --stages) {
       int bytes = sym ? (stages * TILE_ELEMS + stages * (SYM_SEG + 1) * TB * vs + TB * npg) * 8
                       : (stages * TILE_ELEMS + nt * TB * vs + TB * vs + TB * npg) * 8;
-      if (bytes <= 210 * 1024) return {ncp, stages, bytes};
+      if (bytes <= (big && !sym ? 226 : 210) * 1024) return {ncp, stages, bytes};
     }
   }
   throw Error(IETIDP_E_ARG, "interface block too large for the shared-memory loop kernels");
@@ -2629,7 +2630,7 @@ static void launch_tmv_t(ietidp_s* h, const TmvCfg& cfg, TmvArgs a) {
 template <int MODE>
 static void launch_tmv(ietidp_s* h, TmvArgs a) {
   if (h->n_loopwork == 0) return;
-  const TmvCfg cfg = tmv_cfg(h, a.ncols);
+  const TmvCfg cfg = tmv_cfg(h, a.ncols, false, true);  // C5: 16 columns in one pass (212 KB) instead of two of 8
   a.work = h->d_loopwork.p;
   a.sub = h->d_sub.p;
   a.tiles = (MODE == FWD || MODE == BWD) ? h->itiles.p : h->tiles.p;
@@ -2650,7 +2651,7 @@ static void launch_tmv(ietidp_s* h, TmvArgs a) {
 }
 
 static int tmv_launches(const ietidp_s* h, int ncols) {
-  const TmvCfg cfg = tmv_cfg(h, ncols);
+  const TmvCfg cfg = tmv_cfg(h, ncols, false, true);
   return (ncols + cfg.ncp - 1) / cfg.ncp;
 }
 
