@@ -167,3 +167,31 @@ def test_uneven_partition_and_empty_coarse_rank(lib):
     u = np.concatenate([us[k] for k in range(b["n_sub"])])
     uref = np.concatenate(ref["u"])
     assert np.linalg.norm(u - uref) <= 1e-8 * np.linalg.norm(uref)
+
+
+def test_bench_shard_one_rank_native_nccl():
+    """`bench.py --shard` on one rank: the library calls ncclAllReduce itself on a one-rank
+    communicator created through the binding (ietidp_shard_enable_nccl); one JSON line, the
+    oracle's iteration count for C2r, strong scaling declared."""
+    import json
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    env = dict(os.environ, MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK="0", WORLD_SIZE="1", LOCAL_RANK="0")
+    r = subprocess.run([sys.executable, "bench.py", "--shard", "--config", "C2r", "--steps", "2", "--warmup", "3"],
+                       cwd=root, env=env, capture_output=True, text=True, timeout=600)
+    if r.returncode != 0 and ("NCCL" in r.stderr or "nccl" in r.stderr or "Address already in use" in r.stderr):
+        pytest.skip("NCCL could not initialise in this environment: " + r.stderr[-300:])
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [l for l in r.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    ref = dp.solve(make_bundle("C2r"))
+    assert d["scaling"] == "strong" and d["n_gpus"] == 1 and d["value"] > 0
+    assert abs(d["iters"][0] - int(ref["iters"][0])) <= 1 and d["rel_residual"] <= 1e-10
+    assert d["shard"]["transport"].startswith("ncclAllReduce")
