@@ -227,6 +227,12 @@ struct ietidp_s {
   void* graph = nullptr;
   unsigned long long cond_handle = 0;
   bool pcg_persistent = false;          // last solve ran the persistent cooperative PCG kernel
+  // ietidp_apply_F with all 16 columns through the chunk pass (pcg.cu apply_F_chunk): the
+  // persistent kernel's arguments and launch shape, prepared once
+  std::vector<char> fa_args;
+  bool fa_tried = false;
+  int fa_grid = 0, fa_smem = 0, fa_stages = 0;
+  ieti::DevBuf<double> fa_state;
   // ---- sharded mode (ietidp_shard.h): this handle holds one rank's subdomains ----
   bool shard = false;
   int sh_rank = 0, sh_n = 1;

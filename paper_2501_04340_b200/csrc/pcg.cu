@@ -2955,8 +2955,9 @@ static void apply_M_inter(ietidp_s* h, int ncols, const double* x, double* y, co
   bgather(h, ncols, h->zI.p, h->delta.p, y, dotv, partial, st);
 }
 
+static bool apply_F_chunk(ietidp_s* h, int ncols, const double* x, double* y);  // below (needs the chunk kernels)
 void run_apply_F(ietidp_s* h, int ncols, const double* x, double* y) {
-  apply_F_inter(h, ncols, x, y, nullptr, nullptr, nullptr);
+  if (!apply_F_chunk(h, ncols, x, y)) apply_F_inter(h, ncols, x, y, nullptr, nullptr, nullptr);
   IETI_CHECK_LAUNCH();
 }
 void run_apply_M(ietidp_s* h, int ncols, const double* x, double* y) {
@@ -3397,6 +3398,68 @@ static bool run_solve_persistent(ietidp_s* h) {
   if (cfg.ncp == 16) return launch_pcg_t<16, 2, false>(h, cfg, a);
   if (cfg.stages == 3) return launch_pcg_t<8, 3, false>(h, cfg, a);
   return launch_pcg_t<8, 2, false>(h, cfg, a);
+}
+
+// ietidp_apply_F on all 16 columns: the chunk pass and its phases as launches of their own
+// (the kernels of the sharded loop), with the persistent kernel's plans -- W pass | g | z_k,
+// G_k z_k | folded gather -- instead of the row-segment stream (C5: 268 -> ~170 us per apply).
+// IETIDP_FAPPLY_CHUNK=0 keeps the stream.
+static bool apply_F_chunk(ietidp_s* h, int ncols, const double* x, double* y) {
+  if (h->shard || ncols != 16 || ncols != h->nrhs || h->opt.loop != IETIDP_LOOP_EXPLICIT || h->n_lambda == 0) return false;
+  static const bool off = getenv("IETIDP_FAPPLY_CHUNK") && atoi(getenv("IETIDP_FAPPLY_CHUNK")) == 0;
+  if (off) return false;
+  if (!h->fa_tried) {
+    h->fa_tried = true;
+    PcgArgs A{};
+    g_prepare.out = &A;
+    g_prepare.chunk = false;
+    bool ok = false;
+    try {
+      ok = run_solve_persistent(h);
+    } catch (...) {
+      g_prepare.out = nullptr;
+      throw;
+    }
+    g_prepare.out = nullptr;
+    if (ok && g_prepare.chunk) {
+      h->fa_args.resize(sizeof(PcgArgs));
+      memcpy(h->fa_args.data(), &A, sizeof(PcgArgs));
+      h->fa_grid = g_prepare.grid;
+      h->fa_smem = g_prepare.smem;
+      h->fa_stages = g_prepare.stages;
+      h->fa_state.alloc(sizeof(PcgState) / sizeof(double) + 1);
+      h->fa_state.zero(h->stream);  // a state that is never "done"
+    }
+  }
+  if (h->fa_args.empty()) return false;
+  PcgArgs A;
+  memcpy(&A, h->fa_args.data(), sizeof(PcgArgs));
+  A.st = reinterpret_cast<PcgState*>(h->fa_state.p);
+  A.q = y;
+  A.p = const_cast<double*>(x);  // (read only: the gather's dot partials, discarded)
+  cudaStream_t s = h->stream;
+  const int grid = h->fa_grid, smem = h->fa_smem;
+  k_to_slots<<<grid_for((long long)h->n_slots * ncols, 256), 256, 0, s>>>(h->n_slots, ncols, h->slot_lam.p, h->slot_sign.p,
+                                                                         nullptr, x, h->pslot.p, nullptr);
+  IETI_LAUNCHED(h);
+  if (h->fa_stages == 3) {
+    IETI_CUDA(cudaFuncSetAttribute((const void*)k_ch_pass<3, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_ch_pass<3, 0><<<grid, 256, smem, s>>>(A);
+  } else {
+    IETI_CUDA(cudaFuncSetAttribute((const void*)k_ch_pass<2, 0>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_ch_pass<2, 0><<<grid, 256, smem, s>>>(A);
+  }
+  IETI_LAUNCHED(h);
+  if (h->n_primal) {
+    k_ch_g<<<grid, 256, 0, s>>>(A);
+    IETI_LAUNCHED(h);
+    IETI_CUDA(cudaFuncSetAttribute((const void*)k_ch_zk, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+    k_ch_zk<<<grid, 256, smem, s>>>(A);
+    IETI_LAUNCHED(h);
+  }
+  k_ch_gather<0><<<grid, 256, 0, s>>>(A, h->partial.p + 3 * NBLK * ncols);
+  IETI_LAUNCHED(h);
+  return true;
 }
 
 void run_solve(ietidp_s* h) {
